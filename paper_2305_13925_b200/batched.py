@@ -1,0 +1,356 @@
+"""Batched device API over the C-ABI (torch tensors in HBM, no host copies).
+
+These are the ``*_batched`` siblings of the reference entry points: one call
+processes B independent realizations with the sm_100a kernels of
+libxlmimo_b200.so.  The single-realization mirrors in linsolve.py /
+precoder.py / metrics.py are thin wrappers over these.
+
+Layouts (reference layout, batch-major, C-order): H[B, M, K], A/X[B, K, K],
+W/F[B, M, K].  complex64 runs the fp32/tensor-core path, complex128 the fp64
+path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib as L
+from .errors import ConfigurationError
+
+METHODS = {"jacpcg": L.XL_JACPCG, "cg": L.XL_CG, "direct": L.XL_DIRECT}
+VARIANTS = {"textbook": L.XL_TEXTBOOK, "algorithm": L.XL_ALGORITHM}
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    if dt == torch.complex64:
+        return L.XL_C64
+    if dt == torch.complex128:
+        return L.XL_C128
+    raise ConfigurationError(f"channel dtype must be complex64 or complex128, got {dt}")
+
+
+def _check_tensor(t, name, ndim, dt=None):
+    if not isinstance(t, torch.Tensor):
+        raise ConfigurationError(f"{name} must be a torch tensor on the GPU")
+    if not t.is_cuda:
+        raise ConfigurationError(f"{name} must live on a CUDA device (no CPU fallback)")
+    if t.dim() != ndim:
+        raise ConfigurationError(f"{name} must be {ndim}-D, got shape {tuple(t.shape)}")
+    if dt is not None and t.dtype != dt:
+        raise ConfigurationError(f"{name} must be {dt}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ConfigurationError(f"{name} must be contiguous")
+
+
+class _Workspace:
+    """Per-device scratch buffer that only grows (no per-call cudaMalloc)."""
+
+    def __init__(self):
+        self.buf = {}
+
+    def get(self, device, nbytes: int) -> torch.Tensor:
+        key = torch.device(device).index
+        cur = self.buf.get(key)
+        if cur is None or cur.numel() < nbytes:
+            cur = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            self.buf[key] = cur
+        return cur
+
+
+_WS = _Workspace()
+
+
+def _xi_args(xi, B, device):
+    if isinstance(xi, torch.Tensor):
+        xt = xi.to(device=device, dtype=torch.float64).contiguous()
+        if xt.numel() != B:
+            raise ConfigurationError("per-realization xi must have B entries")
+        return 0.0, xt
+    xi = float(xi)
+    if not xi > 0:
+        raise ConfigurationError(f"regularization xi must be positive, got {xi}")
+    return xi, None
+
+
+@dataclass
+class PrecoderBatch:
+    """Outputs of :func:`rzf_batched` (all device tensors)."""
+
+    W: torch.Tensor            # [B, M, K] = beta * F
+    beta: torch.Tensor         # [B] float64
+    sum_se: torch.Tensor       # [B] float64
+    status: torch.Tensor       # [B] int32 (0 = ok)
+    gamma: torch.Tensor | None = None   # [B, K] float64
+    F: torch.Tensor | None = None       # [B, M, K]
+    X: torch.Tensor | None = None       # [B, K, K]
+
+
+def alloc_outputs(H: torch.Tensor, want_gamma=True, want_F=False, want_X=False):
+    B, M, K = H.shape
+    dev = H.device
+    f64 = dict(dtype=torch.float64, device=dev)
+    return PrecoderBatch(
+        W=torch.empty_like(H), beta=torch.empty(B, **f64), sum_se=torch.empty(B, **f64),
+        status=torch.empty(B, dtype=torch.int32, device=dev),
+        gamma=torch.empty(B, K, **f64) if want_gamma else None,
+        F=torch.empty_like(H) if want_F else None,
+        X=torch.empty(B, K, K, dtype=H.dtype, device=dev) if want_X else None)
+
+
+def rzf_workspace_bytes(H_shape, dtype, method="jacpcg") -> int:
+    B, M, K = H_shape
+    L.load_library()
+    return int(L._lib.xl_rzf_workspace_bytes(dtype_code(dtype), METHODS[method], B, M, K))
+
+
+def uses_tensor_cores(dtype, method, M, K) -> bool:
+    L.load_library()
+    return bool(L._lib.xl_rzf_uses_tensor_cores(dtype_code(dtype), METHODS[method], M, K))
+
+
+def rzf_batched(H: torch.Tensor, xi, power: float, method: str = "jacpcg", T: int = 4,
+                variant: str = "textbook", sigma2: float = 1.0, *, want_gamma=True,
+                want_F=False, want_X=False, out: PrecoderBatch | None = None,
+                check: bool = True, stream=None) -> PrecoderBatch:
+    """Batched RZF precoder + SINR/SE (the hot path, one fused launch when the
+    tcgen05 kernel covers the shape).
+
+    Mirrors ``rzf_iterative`` / ``rzf_direct`` (precoder.py:73-91) followed by
+    ``sinr_eq9`` (metrics.py:47-58) on one full-array block per realization.
+    ``check=True`` copies the status vector to the host (one sync) and raises
+    the reference exception of the first failing realization.
+    """
+    lib = L.lib()
+    if method not in METHODS:
+        raise ConfigurationError(f"unknown solver {method!r}; expected one of {sorted(METHODS)}")
+    if variant not in VARIANTS:
+        raise ConfigurationError(f"unknown PCG variant {variant!r}")
+    _check_tensor(H, "H", 3)
+    dc = dtype_code(H.dtype)
+    B, M, K = H.shape
+    xs, xt = _xi_args(xi, B, H.device)
+    if out is None:
+        out = alloc_outputs(H, want_gamma, want_F, want_X)
+    nbytes = int(lib.xl_rzf_workspace_bytes(dc, METHODS[method], B, M, K))
+    ws = _WS.get(H.device, nbytes)
+    rc = lib.xl_rzf(dc, METHODS[method], VARIANTS[variant], L.ptr(H), B, M, K, xs,
+                    L.ptr(xt), float(power), int(T), float(sigma2), L.ptr(out.W),
+                    L.ptr(out.F), L.ptr(out.beta), L.ptr(out.gamma), L.ptr(out.sum_se),
+                    L.ptr(out.X), L.ptr(out.status), L.ptr(ws), ws.numel(),
+                    L.stream_ptr(stream))
+    L.check(rc, "xl_rzf")
+    if check:
+        L.raise_status(out.status.cpu().numpy(), "rzf_batched")
+    return out
+
+
+def gram_batched(H: torch.Tensor, xi, stream=None) -> torch.Tensor:
+    """A_b = H_b^H H_b + xi_b I (precoder.py:53-61), Hermitian by construction."""
+    lib = L.lib()
+    _check_tensor(H, "H", 3)
+    B, M, K = H.shape
+    xs, xt = _xi_args(xi, B, H.device)
+    A = torch.empty(B, K, K, dtype=H.dtype, device=H.device)
+    L.check(lib.xl_gram(dtype_code(H.dtype), L.ptr(H), B, M, K, xs, L.ptr(xt), L.ptr(A),
+                        L.stream_ptr(stream)), "xl_gram")
+    return A
+
+
+@dataclass
+class SolveBatch:
+    X: torch.Tensor
+    iterations: torch.Tensor
+    status: torch.Tensor
+    trace: torch.Tensor | None = None
+    iterates: torch.Tensor | None = None
+
+
+def solve_batched(A: torch.Tensor, method: str = "jacpcg", T: int = 5, variant: str = "textbook",
+                  S: torch.Tensor | None = None, w0: torch.Tensor | None = None,
+                  precond: torch.Tensor | None = None, precond_identity: bool = False,
+                  eps: float | None = None, trace: bool = False, iterates: bool = False,
+                  check: bool = True, stream=None) -> SolveBatch:
+    """Batched A_b X_b = S_b (S = identity when None): linsolve.py:109-294."""
+    lib = L.lib()
+    if method not in METHODS:
+        raise ConfigurationError(f"unknown solver {method!r}")
+    if variant not in VARIANTS:
+        raise ConfigurationError(f"unknown PCG variant {variant!r}")
+    _check_tensor(A, "A", 3)
+    B, K, K2 = A.shape
+    if K != K2:
+        raise ConfigurationError("A must be square")
+    dc = dtype_code(A.dtype)
+    if S is not None:
+        _check_tensor(S, "S", 3, A.dtype)
+        R = S.shape[2]
+        if S.shape[:2] != (B, K):
+            raise ConfigurationError("S shape mismatch")
+    else:
+        R = K
+    if w0 is not None:
+        _check_tensor(w0, "w0", 3, A.dtype)
+        if tuple(w0.shape) != (B, K, R):
+            raise ConfigurationError(f"w0 shape {tuple(w0.shape)} does not match rhs shape {(B, K, R)}")
+    if precond is not None:
+        precond = precond.to(device=A.device, dtype=torch.float64).contiguous()
+    dev = A.device
+    X = torch.empty(B, K, R, dtype=A.dtype, device=dev)
+    its = torch.empty(B, dtype=torch.int32, device=dev)
+    st = torch.zeros(B, dtype=torch.int32, device=dev)
+    Tn = max(int(T), 1)
+    tr = torch.empty(B, Tn + 1, dtype=torch.float64, device=dev) if trace else None
+    itr = torch.empty(B, Tn, K, R, dtype=A.dtype, device=dev) if iterates else None
+    nbytes = int(lib.xl_solve_workspace_bytes(dc, B, K, R))
+    ws = _WS.get(dev, nbytes)
+    rc = lib.xl_solve(dc, METHODS[method], VARIANTS[variant], L.ptr(A), B, K, L.ptr(S), R,
+                      L.ptr(w0), L.ptr(precond), int(bool(precond_identity)), int(T),
+                      -1.0 if eps is None else float(eps), L.ptr(X), L.ptr(its), L.ptr(tr),
+                      L.ptr(itr), L.ptr(st), L.ptr(ws), ws.numel(), L.stream_ptr(stream))
+    L.check(rc, "xl_solve")
+    if check:
+        L.raise_status(st.cpu().numpy(), "solve_batched")
+    return SolveBatch(X, its, st, tr, itr)
+
+
+def apply_precoder_batched(H: torch.Tensor, X: torch.Tensor, power: float, sigma2: float = 1.0,
+                           want_F=False, check=True, stream=None) -> PrecoderBatch:
+    """F = H X, power scaling and SINR/SE for a given solution X."""
+    lib = L.lib()
+    _check_tensor(H, "H", 3)
+    _check_tensor(X, "X", 3, H.dtype)
+    B, M, K = H.shape
+    out = alloc_outputs(H, True, want_F, False)
+    dc = dtype_code(H.dtype)
+    nbytes = int(lib.xl_apply_precoder_workspace_bytes(dc, B, M, K))
+    ws = _WS.get(H.device, nbytes)
+    L.check(lib.xl_apply_precoder(dc, L.ptr(H), L.ptr(X), B, M, K, float(power), float(sigma2),
+                                  L.ptr(out.W), L.ptr(out.F), L.ptr(out.beta), L.ptr(out.gamma),
+                                  L.ptr(out.sum_se), L.ptr(out.status), L.ptr(ws), ws.numel(),
+                                  L.stream_ptr(stream)), "xl_apply_precoder")
+    if check:
+        L.raise_status(out.status.cpu().numpy(), "apply_precoder_batched")
+    return out
+
+
+@dataclass
+class SinrBatch:
+    gamma: torch.Tensor
+    se: torch.Tensor
+    sum_se: torch.Tensor
+    coupling: torch.Tensor   # B = H^H G
+
+
+def sinr_batched(H: torch.Tensor, G: torch.Tensor, sigma2: float, stream=None) -> SinrBatch:
+    """Per-user SINR/SE of precoder G (metrics.py:35-58), coupling B = H^H G."""
+    lib = L.lib()
+    _check_tensor(H, "H", 3)
+    _check_tensor(G, "G", 3, H.dtype)
+    B, M, K = H.shape
+    if tuple(G.shape) != (B, M, K):
+        raise ConfigurationError("G must match H's shape")
+    dc = dtype_code(H.dtype)
+    dev = H.device
+    f64 = dict(dtype=torch.float64, device=dev)
+    gamma, se, s = torch.empty(B, K, **f64), torch.empty(B, K, **f64), torch.empty(B, **f64)
+    coup = torch.empty(B, K, K, dtype=H.dtype, device=dev)
+    nbytes = int(lib.xl_sinr_workspace_bytes(dc, B, K))
+    assert nbytes <= coup.numel() * coup.element_size() + 256
+    L.check(lib.xl_sinr(dc, L.ptr(H), L.ptr(G), B, M, K, float(sigma2), L.ptr(gamma), L.ptr(se),
+                        L.ptr(s), L.ptr(coup), max(nbytes, coup.numel() * coup.element_size()),
+                        L.stream_ptr(stream)), "xl_sinr")
+    return SinrBatch(gamma, se, s, coup)
+
+
+def se_partials(sum_se: torch.Tensor, chunk: int, stream=None) -> torch.Tensor:
+    """{sum, sum of squares, n} per `chunk` consecutive realizations (device)."""
+    lib = L.lib()
+    _check_tensor(sum_se, "sum_se", 1, torch.float64)
+    B = sum_se.numel()
+    nc = (B + chunk - 1) // chunk
+    out = torch.empty(nc, 3, dtype=torch.float64, device=sum_se.device)
+    L.check(lib.xl_se_partials(L.ptr(sum_se), B, int(chunk), L.ptr(out), L.stream_ptr(stream)),
+            "xl_se_partials")
+    return out
+
+
+def combine_se_partials(partials) -> tuple[float, float]:
+    """Mean and SEM (ddof=1) from ordered chunk partials (metrics.py:61-68)."""
+    import math
+    s = q = n = 0.0
+    for a, b, c in partials:
+        s += float(a); q += float(b); n += float(c)
+    if n < 1:
+        raise ConfigurationError("sum_se needs at least one trial")
+    mean = s / n
+    if n < 2:
+        return mean, 0.0
+    var = max(q - n * mean * mean, 0.0) / (n - 1)
+    return mean, math.sqrt(var) / math.sqrt(n)
+
+
+class HostPipeline:
+    """Host-buffer front end of the hot path: H (pinned host) -> W (pinned host).
+
+    Chunks of ``chunk`` realizations flow through three CUDA streams with
+    double-buffered device staging: H2D of chunk i+1 and D2H of chunk i-1
+    overlap the fused precoder on chunk i, so end-to-end throughput is bound by
+    the PCIe copies, not by the kernels.  This is the call a user with numpy /
+    host data makes (the reference's API takes host arrays).
+    """
+
+    def __init__(self, M: int, K: int, dtype=torch.complex64, chunk: int = 2048, device=None):
+        self.device = torch.device(device or "cuda")
+        self.M, self.K, self.dtype, self.chunk = M, K, dtype, chunk
+        mk = lambda: torch.empty(chunk, M, K, dtype=dtype, device=self.device)  # noqa: E731
+        self.Hd = [mk(), mk()]
+        self.outs = [alloc_outputs(self.Hd[0], want_gamma=False) for _ in range(2)]
+        self.s_h2d = torch.cuda.Stream(self.device)
+        self.s_comp = torch.cuda.Stream(self.device)
+        self.s_d2h = torch.cuda.Stream(self.device)
+
+    def run(self, H_host: torch.Tensor, W_host: torch.Tensor, sum_se_host: torch.Tensor,
+            status_host: torch.Tensor, xi, power, method="jacpcg", T=4, variant="textbook",
+            sigma2=1.0):
+        B = H_host.shape[0]
+        n = (B + self.chunk - 1) // self.chunk
+        ev_h = [torch.cuda.Event() for _ in range(2)]
+        ev_c = [torch.cuda.Event() for _ in range(2)]
+        ev_hfree = [torch.cuda.Event() for _ in range(2)]
+        ev_wfree = [torch.cuda.Event() for _ in range(2)]
+        started_h = [False, False]
+        started_w = [False, False]
+        for i in range(n):
+            j = i % 2
+            lo, hi = i * self.chunk, min(B, (i + 1) * self.chunk)
+            nb = hi - lo
+            Hd, out = self.Hd[j], self.outs[j]
+            with torch.cuda.stream(self.s_h2d):
+                if started_h[j]:
+                    self.s_h2d.wait_event(ev_hfree[j])
+                Hd[:nb].copy_(H_host[lo:hi], non_blocking=True)
+                ev_h[j].record(self.s_h2d)
+            with torch.cuda.stream(self.s_comp):
+                self.s_comp.wait_event(ev_h[j])
+                if started_w[j]:
+                    self.s_comp.wait_event(ev_wfree[j])
+                view = out if nb == self.chunk else PrecoderBatch(
+                    W=out.W[:nb], beta=out.beta[:nb], sum_se=out.sum_se[:nb],
+                    status=out.status[:nb])
+                rzf_batched(Hd[:nb], xi, power, method=method, T=T, variant=variant,
+                            sigma2=sigma2, want_gamma=False, out=view, check=False,
+                            stream=self.s_comp)
+                ev_c[j].record(self.s_comp)
+                ev_hfree[j].record(self.s_comp)
+                started_h[j] = True
+            with torch.cuda.stream(self.s_d2h):
+                self.s_d2h.wait_event(ev_c[j])
+                W_host[lo:hi].copy_(out.W[:nb], non_blocking=True)
+                sum_se_host[lo:hi].copy_(out.sum_se[:nb], non_blocking=True)
+                status_host[lo:hi].copy_(out.status[:nb], non_blocking=True)
+                ev_wfree[j].record(self.s_d2h)
+                started_w[j] = True
+        self.s_d2h.synchronize()
+        self.s_comp.synchronize()

@@ -1,0 +1,46 @@
+// Host-side launchers of the SIMT (general-shape / complex128) kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace xl {
+
+enum { EPI_STORE = 0, EPI_GRAM = 1, EPI_FNORM = 2 };
+
+template <typename R>
+int launch_cgemm(bool conjA, int epi, const void* A, int64_t sA, int lda,
+                 const void* Bm, int64_t sB, int ldb, void* Cm, int64_t sC,
+                 int ldc, int64_t batch, int m, int n, int k,
+                 const double* diag_add, double diag_scalar, double* partial,
+                 cudaStream_t st);
+int gemm_tiles(int m, int n);
+
+template <typename R>
+int launch_beta_scale(void* W, void* F, int64_t B, int64_t per, const double* partial,
+                      int nparts, double power, double* beta, int32_t* status,
+                      cudaStream_t st);
+template <typename R>
+int launch_sinr(const void* Bc, int64_t B, int K, double sigma2, double* gamma,
+                double* se, double* sum_se, cudaStream_t st);
+int launch_se_partials(const double* s, int64_t B, int64_t chunk, double* out, cudaStream_t st);
+
+// PCG / CG / Jac-PCG (linsolve.py:183-294) and Cholesky (linsolve.py:109-119).
+struct SolveArgs {
+  int method, variant;
+  const void* A; int64_t B; int K;
+  const void* S; int R;          // S == nullptr -> identity (R == K)
+  const void* w0;                // nullable
+  const double* precond;         // nullable -> Re diag(A)
+  int precond_identity;
+  int T; double eps;             // eps < 0 -> None
+  void* X; int32_t* iterations; double* trace; void* iterates; int32_t* status;
+  void* ws; size_t ws_bytes;
+};
+template <typename R> size_t solve_ws_bytes(int64_t B, int K, int Rcols);
+template <typename R> int launch_solve(const SolveArgs& a, cudaStream_t st);
+
+int launch_channel(int dtype, uint64_t seed, int64_t first, int64_t B, int S, int Ms,
+                   int K, double p, const double* Rsqrt, double gain_scale, double dmin,
+                   double dmax, void* H, int32_t* status, cudaStream_t st);
+
+}  // namespace xl

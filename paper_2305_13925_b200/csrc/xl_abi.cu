@@ -1,0 +1,234 @@
+// extern "C" boundary of libxlmimo_b200.so (declared in include/xlmimo_b200.h).
+//
+// Host-side argument validation mirrors the reference's ConfigurationError
+// checks (precoder.py:55-56, 86-87; linsolve.py:209-210, 260-261;
+// metrics.py:49-50) and returns XL_ERR_CONFIG before anything is launched.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "xl_common.cuh"
+#include "simt_kernels.cuh"
+#include "fused_tc.cuh"
+
+namespace xl {
+
+static thread_local char g_err[512] = "";
+static unsigned long long g_launches = 0;
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* what) {
+  __atomic_add_fetch(&g_launches, 1ull, __ATOMIC_RELAXED);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return XL_ERR_CUDA;
+  }
+  return XL_SUCCESS;
+}
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+static size_t csize(int dtype) { return dtype == XL_C64 ? 8 : 16; }
+
+static int check_dtype(int dtype) {
+  if (dtype != XL_C64 && dtype != XL_C128) { set_error("unknown dtype %d", dtype); return XL_ERR_CONFIG; }
+  return XL_SUCCESS;
+}
+
+// F = H X (+ per-tile ||F||^2) -> beta, W = beta F -> B = H^H W -> SINR/SE.
+static int apply_precoder(int dtype, const void* H, const void* X, int64_t B, int M, int K,
+                          double power, double sigma2, void* W, void* F, double* beta,
+                          double* gamma, double* sum_se, int32_t* status, double* part,
+                          void* Bc, cudaStream_t st) {
+  int64_t sH = (int64_t)M * K, sK = (int64_t)K * K;
+  const int nparts = gemm_tiles(M, K);
+  int e;
+  if (dtype == XL_C64) {
+    if ((e = launch_cgemm<float>(false, EPI_FNORM, H, sH, K, X, sK, K, W, sH, K, B, M, K, K, nullptr, 0, part, st))) return e;
+    if ((e = launch_beta_scale<float>(W, F, B, sH, part, nparts, power, beta, status, st))) return e;
+    if ((e = launch_cgemm<float>(true, EPI_STORE, H, sH, K, W, sH, K, Bc, sK, K, B, K, K, M, nullptr, 0, nullptr, st))) return e;
+    return launch_sinr<float>(Bc, B, K, sigma2, gamma, nullptr, sum_se, st);
+  }
+  if ((e = launch_cgemm<double>(false, EPI_FNORM, H, sH, K, X, sK, K, W, sH, K, B, M, K, K, nullptr, 0, part, st))) return e;
+  if ((e = launch_beta_scale<double>(W, F, B, sH, part, nparts, power, beta, status, st))) return e;
+  if ((e = launch_cgemm<double>(true, EPI_STORE, H, sH, K, W, sH, K, Bc, sK, K, B, K, K, M, nullptr, 0, nullptr, st))) return e;
+  return launch_sinr<double>(Bc, B, K, sigma2, gamma, nullptr, sum_se, st);
+}
+
+}  // namespace xl
+
+using namespace xl;
+
+extern "C" {
+
+int xl_abi_version(void) { return 1; }
+uint64_t xl_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+const char* xl_last_error(void) { return g_err; }
+
+int xl_rzf_uses_tensor_cores(int dtype, int method, int32_t M, int32_t K) {
+  return fused_supported(dtype, method, M, K) ? 1 : 0;
+}
+
+int xl_gram(int dtype, const void* H, int64_t B, int32_t M, int32_t K, double xi,
+            const double* xi_per_batch, void* A, xl_stream_t stream) {
+  if (int e = check_dtype(dtype)) return e;
+  if (!xi_per_batch && !(xi > 0)) { set_error("regularization xi must be positive, got %g", xi); return XL_ERR_CONFIG; }
+  if (M < 1 || K < 1 || B < 0) { set_error("bad sizes"); return XL_ERR_CONFIG; }
+  if (B == 0) return XL_SUCCESS;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t sH = (int64_t)M * K, sA = (int64_t)K * K;
+  if (dtype == XL_C64)
+    return launch_cgemm<float>(true, EPI_GRAM, H, sH, K, H, sH, K, A, sA, K, B, K, K, M, xi_per_batch, xi, nullptr, st);
+  return launch_cgemm<double>(true, EPI_GRAM, H, sH, K, H, sH, K, A, sA, K, B, K, K, M, xi_per_batch, xi, nullptr, st);
+}
+
+size_t xl_solve_workspace_bytes(int dtype, int64_t B, int32_t K, int32_t R) {
+  return dtype == XL_C64 ? solve_ws_bytes<float>(B, K, R) : solve_ws_bytes<double>(B, K, R);
+}
+
+int xl_solve(int dtype, int method, int variant, const void* A, int64_t B, int32_t K,
+             const void* S, int32_t R, const void* w0, const double* precond,
+             int32_t precond_identity, int32_t T, double eps, void* X, int32_t* iterations,
+             double* trace, void* iterates, int32_t* status, void* workspace,
+             size_t ws_bytes, xl_stream_t stream) {
+  if (int e = check_dtype(dtype)) return e;
+  if (method != XL_JACPCG && method != XL_CG && method != XL_DIRECT) { set_error("unknown method %d", method); return XL_ERR_CONFIG; }
+  if (variant != XL_TEXTBOOK && variant != XL_ALGORITHM) { set_error("unknown PCG variant %d", variant); return XL_ERR_CONFIG; }
+  if (method != XL_DIRECT && T < 1) { set_error("iteration count T must be >= 1, got %d", T); return XL_ERR_CONFIG; }
+  if (K < 1 || R < 1 || B < 0) { set_error("bad sizes"); return XL_ERR_CONFIG; }
+  if (!S && R != K) { set_error("identity RHS needs R == K"); return XL_ERR_CONFIG; }
+  if (B == 0) return XL_SUCCESS;
+  SolveArgs a{method, variant, A, B, K, S, R, w0, precond, precond_identity, T, eps,
+              X, iterations, trace, iterates, status, workspace, ws_bytes};
+  cudaStream_t st = (cudaStream_t)stream;
+  return dtype == XL_C64 ? launch_solve<float>(a, st) : launch_solve<double>(a, st);
+}
+
+// ---------------------------------------------------------------------------
+// Fused precoder.  Workspace (SIMT path): A | X | solver ws (reused for the
+// coupling matrix) | ||F||^2 partials | iterations.
+// ---------------------------------------------------------------------------
+static size_t simt_rzf_ws(int dtype, int64_t B, int M, int K) {
+  size_t cs = csize(dtype), kk = (size_t)B * K * K * cs;
+  size_t sws = xl_solve_workspace_bytes(dtype, B, K, K);
+  if (sws < kk) sws = kk;
+  return align_up(kk) + align_up(kk) + align_up(sws) +
+         align_up((size_t)B * gemm_tiles(M, K) * sizeof(double)) + align_up((size_t)B * 4);
+}
+
+size_t xl_rzf_workspace_bytes(int dtype, int method, int64_t B, int32_t M, int32_t K) {
+  if (fused_supported(dtype, method, M, K)) return fused_ws_bytes(dtype, method, B, M, K);
+  return simt_rzf_ws(dtype, B, M, K);
+}
+
+int xl_rzf(int dtype, int method, int variant, const void* H, int64_t B, int32_t M,
+           int32_t K, double xi, const double* xi_per_batch, double power, int32_t T,
+           double sigma2, void* W, void* F, double* beta, double* gamma, double* sum_se,
+           void* X, int32_t* status, void* workspace, size_t ws_bytes, xl_stream_t stream) {
+  if (int e = check_dtype(dtype)) return e;
+  if (method != XL_JACPCG && method != XL_CG && method != XL_DIRECT) { set_error("unknown method %d", method); return XL_ERR_CONFIG; }
+  if (variant != XL_TEXTBOOK && variant != XL_ALGORITHM) { set_error("unknown PCG variant %d", variant); return XL_ERR_CONFIG; }
+  if (method != XL_DIRECT && T < 1) { set_error("iteration count T must be >= 1, got %d", T); return XL_ERR_CONFIG; }
+  if (!xi_per_batch && !(xi > 0)) { set_error("regularization xi must be positive, got %g", xi); return XL_ERR_CONFIG; }
+  if (!(sigma2 > 0)) { set_error("noise power must be positive, got %g", sigma2); return XL_ERR_CONFIG; }
+  if (M < 1 || K < 1 || B < 0) { set_error("bad sizes"); return XL_ERR_CONFIG; }
+  if (B == 0) return XL_SUCCESS;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (ws_bytes < xl_rzf_workspace_bytes(dtype, method, B, M, K)) { set_error("rzf: workspace too small"); return XL_ERR_WORKSPACE; }
+  if (cudaMemsetAsync(status, 0, (size_t)B * sizeof(int32_t), st) != cudaSuccess) return check_launch("memset");
+
+  if (fused_supported(dtype, method, M, K))
+    return launch_fused(dtype, method, variant, H, B, M, K, xi, xi_per_batch, power, T,
+                        sigma2, W, F, beta, gamma, sum_se, X, status, workspace, ws_bytes, st);
+
+  // ---- general SIMT path: Gram -> solve -> F = H X (+||F||^2) -> beta, W -> B = H^H W -> SINR
+  const size_t cs = csize(dtype), kk = (size_t)B * K * K * cs;
+  char* p = (char*)workspace;
+  void* A = p; p += align_up(kk);
+  void* Xw = p; p += align_up(kk);
+  size_t sws = xl_solve_workspace_bytes(dtype, B, K, K);
+  if (sws < kk) sws = kk;
+  void* sw = p; p += align_up(sws);
+  double* part = (double*)p; p += align_up((size_t)B * gemm_tiles(M, K) * sizeof(double));
+  int32_t* iters = (int32_t*)p;
+  void* Xo = X ? X : Xw;
+  int e;
+  if ((e = xl_gram(dtype, H, B, M, K, xi, xi_per_batch, A, stream))) return e;
+  if ((e = xl_solve(dtype, method, variant, A, B, K, nullptr, K, nullptr, nullptr, method == XL_CG,
+                    T, -1.0, Xo, iters, nullptr, nullptr, status, sw, sws, stream))) return e;
+  return apply_precoder(dtype, H, Xo, B, M, K, power, sigma2, W, F, beta, gamma, sum_se, status,
+                        part, sw, st);
+}
+
+size_t xl_apply_precoder_workspace_bytes(int dtype, int64_t B, int32_t M, int32_t K) {
+  return align_up((size_t)B * K * K * csize(dtype)) + align_up((size_t)B * gemm_tiles(M, K) * sizeof(double));
+}
+
+int xl_apply_precoder(int dtype, const void* H, const void* X, int64_t B, int32_t M, int32_t K,
+                      double power, double sigma2, void* W, void* F, double* beta, double* gamma,
+                      double* sum_se, int32_t* status, void* workspace, size_t ws_bytes,
+                      xl_stream_t stream) {
+  if (int e = check_dtype(dtype)) return e;
+  if (!(sigma2 > 0)) { set_error("noise power must be positive, got %g", sigma2); return XL_ERR_CONFIG; }
+  if (M < 1 || K < 1 || B < 0) { set_error("bad sizes"); return XL_ERR_CONFIG; }
+  if (B == 0) return XL_SUCCESS;
+  if (ws_bytes < xl_apply_precoder_workspace_bytes(dtype, B, M, K)) { set_error("apply_precoder: workspace too small"); return XL_ERR_WORKSPACE; }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(status, 0, (size_t)B * sizeof(int32_t), st) != cudaSuccess) return check_launch("memset");
+  char* p = (char*)workspace;
+  void* Bc = p; p += align_up((size_t)B * K * K * csize(dtype));
+  double* part = (double*)p;
+  return apply_precoder(dtype, H, X, B, M, K, power, sigma2, W, F, beta, gamma, sum_se, status,
+                        part, Bc, st);
+}
+
+size_t xl_sinr_workspace_bytes(int dtype, int64_t B, int32_t K) {
+  return align_up((size_t)B * K * K * csize(dtype));
+}
+
+int xl_sinr(int dtype, const void* H, const void* G, int64_t B, int32_t M, int32_t K,
+            double sigma2, double* gamma, double* se, double* sum_se, void* workspace,
+            size_t ws_bytes, xl_stream_t stream) {
+  if (int e = check_dtype(dtype)) return e;
+  if (!(sigma2 > 0)) { set_error("noise power must be positive, got %g", sigma2); return XL_ERR_CONFIG; }
+  if (M < 1 || K < 1 || B < 0) { set_error("bad sizes"); return XL_ERR_CONFIG; }
+  if (B == 0) return XL_SUCCESS;
+  if (ws_bytes < xl_sinr_workspace_bytes(dtype, B, K)) { set_error("sinr: workspace too small"); return XL_ERR_WORKSPACE; }
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t sH = (int64_t)M * K, sK = (int64_t)K * K;
+  int e;
+  if (dtype == XL_C64) {
+    if ((e = launch_cgemm<float>(true, EPI_STORE, H, sH, K, G, sH, K, workspace, sK, K, B, K, K, M, nullptr, 0, nullptr, st))) return e;
+    return launch_sinr<float>(workspace, B, K, sigma2, gamma, se, sum_se, st);
+  }
+  if ((e = launch_cgemm<double>(true, EPI_STORE, H, sH, K, G, sH, K, workspace, sK, K, B, K, K, M, nullptr, 0, nullptr, st))) return e;
+  return launch_sinr<double>(workspace, B, K, sigma2, gamma, se, sum_se, st);
+}
+
+int xl_channel_generate(int dtype, uint64_t seed, int64_t first, int64_t B, int32_t S,
+                        int32_t Ms, int32_t K, double p, const double* Rsqrt, double beta_bar,
+                        double dmin, double dmax, void* H, int32_t* status, xl_stream_t stream) {
+  if (int e = check_dtype(dtype)) return e;
+  if (S < 1 || Ms < 2 || K < 1 || B < 0) { set_error("bad sizes"); return XL_ERR_CONFIG; }
+  if (!(p > 0 && p <= 1)) { set_error("visibility probability must lie in (0, 1], got %g", p); return XL_ERR_CONFIG; }
+  if (!(dmin > 0 && dmax >= dmin)) { set_error("bad distance range"); return XL_ERR_CONFIG; }
+  if (B == 0) return XL_SUCCESS;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(status, 0, (size_t)B * sizeof(int32_t), st) != cudaSuccess) return check_launch("memset");
+  return launch_channel(dtype, seed, first, B, S, Ms, K, p, Rsqrt, beta_bar, dmin, dmax, H, status, st);
+}
+
+int xl_se_partials(const double* sum_se, int64_t B, int64_t chunk, double* partials,
+                   xl_stream_t stream) {
+  if (chunk < 1 || B < 0) { set_error("bad chunk"); return XL_ERR_CONFIG; }
+  if (B == 0) return XL_SUCCESS;
+  return launch_se_partials(sum_se, B, chunk, partials, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,319 @@
+"""GPU parity: the CUDA path vs the reference's golden vectors and the CPU oracle.
+
+Tolerances (north_star): W relative Frobenius <= 1e-10 (complex128) and
+<= 1e-4 (complex64); sum-SE relative <= 1e-4.  Integer / status outputs and
+the CG == Jac-PCG(C=I) identity are bit-exact.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import xlmimo_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+import paper_2305_13925_b200 as X  # noqa: E402
+from paper_2305_13925_b200 import batched as BT  # noqa: E402
+from paper_2305_13925_b200.errors import (ConfigurationError, DegenerateChannelError,  # noqa: E402
+                                          NotHpdError, SplittingError)
+
+DEV = "cuda"
+
+
+def relf(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def dev(a, dt=torch.complex128):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV, dt)
+
+
+# ---------------------------------------------------------------- Gram ------
+
+def test_gram_golden_and_pins(golden):
+    g = golden("precoders")
+    for tag in ("cfg1", "small", "rand"):
+        H = g[tag + "_H"]
+        A = BT.gram_batched(dev(H), float(g[tag + "_alpha"])).cpu().numpy()
+        ref = g[tag + "_gram"]
+        assert relf(A, ref) < 1e-14
+        np.testing.assert_array_equal(A, np.conj(np.transpose(A, (0, 2, 1))))  # exact Hermitian
+    # test_precoder.py:14-31
+    np.testing.assert_array_equal(X.gram_regularized(np.zeros((4, 3)), 0.5).P, 0.5 * np.eye(3))
+    np.testing.assert_array_equal(X.gram_regularized(np.eye(2), 1.0).P, 2.0 * np.eye(2))
+    with pytest.raises(ConfigurationError):
+        X.gram_regularized(np.eye(2), 0.0)
+
+
+# -------------------------------------------------------------- solvers -----
+
+def test_solver_golden(golden):
+    g = golden("solvers")
+    for i in range(int(g["n_solver_cases"])):
+        pre = f"s{i}_"
+        P, S, T = g[pre + "P"], g[pre + "S"], int(g[pre + "T"])
+        w0 = g[pre + "w0"] if pre + "w0" in g else None
+        sysm = X.HpdSystem(P=P, rhs=S)
+        runs = {
+            "textbook": lambda: X.jacpcg_solve(sysm, T, w0=w0, keep_iterates=True, variant="textbook"),
+            "algorithm": lambda: X.jacpcg_solve(sysm, T, w0=w0, keep_iterates=True, variant="algorithm"),
+            "cg": lambda: X.cg_solve(sysm, T, w0=w0, keep_iterates=True),
+            "eps": lambda: X.jacpcg_solve(sysm, 50, eps=1e-6, w0=w0, variant="textbook"),
+        }
+        for name, fn in runs.items():
+            if pre + name + "_err" in g:
+                with pytest.raises(NotHpdError):
+                    fn()
+                continue
+            o = fn()
+            ref_w = g[pre + name + "_w"]
+            assert relf(o.w, ref_w) < 1e-10, (i, name, relf(o.w, ref_w))
+            assert o.iterations == int(g[pre + name + "_it"]), (i, name)
+            assert o.converged == bool(g[pre + name + "_conv"]), (i, name)
+            tr, rtr = o.residual_trace, g[pre + name + "_trace"]
+            assert tr.shape == rtr.shape
+            # trace values: relative where they are not at round-off level
+            np.testing.assert_allclose(tr, rtr, rtol=1e-6, atol=1e-20)
+            if pre + name + "_iterates" in g:
+                ri = g[pre + name + "_iterates"]
+                assert len(o.iterates) == ri.shape[0]
+                for a, b in zip(o.iterates, ri):
+                    assert relf(a, b) < 1e-10
+        o = X.direct_solve(sysm)
+        assert relf(o.w, g[pre + "direct_w"]) < 1e-11
+        assert o.iterations == 0 and o.converged
+
+
+def test_cg_equals_jacpcg_identity_bit_exact():
+    """test_linsolve.py:154-164 and acceptance criterion 5(b), on the GPU."""
+    rng = np.random.default_rng(9)
+    for n in (4, 10, 32):
+        A = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+        Q, _ = np.linalg.qr(A)
+        P = (Q * rng.uniform(1, 100, n)) @ Q.conj().T
+        P = (P + P.conj().T) / 2
+        s = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        sysm = X.HpdSystem(P=P, rhs=s)
+        cg = X.cg_solve(sysm, T=6, keep_iterates=True)
+        for variant in ("algorithm", "textbook"):
+            pcg = X.jacpcg_solve(sysm, T=6, precond_diag=np.ones(n), keep_iterates=True,
+                                 variant=variant)
+            for a, b in zip(cg.iterates, pcg.iterates):
+                np.testing.assert_array_equal(a, b)
+
+
+def test_solver_known_answers():
+    # test_linsolve.py:39-46, 126-134, 166-169
+    o = X.direct_solve(X.HpdSystem(P=np.eye(3), rhs=np.array([1.0, 0.0, 0.0])))
+    np.testing.assert_allclose(o.w, [1.0, 0.0, 0.0])
+    o = X.direct_solve(X.HpdSystem(P=np.diag([2.0, 4.0]), rhs=np.array([2.0, 8.0])))
+    np.testing.assert_allclose(o.w, [1.0, 2.0])
+    o = X.cg_solve(X.HpdSystem(P=np.eye(4), rhs=np.array([1.0, 2.0, 3.0, 4.0])), T=1)
+    np.testing.assert_allclose(o.w, [1.0, 2.0, 3.0, 4.0], atol=1e-14)
+    o = X.cg_solve(X.HpdSystem(P=np.eye(3), rhs=np.zeros(3)), T=5)
+    np.testing.assert_array_equal(o.w, 0.0)
+    o = X.jacpcg_solve(X.HpdSystem(P=np.diag([1.0, 10.0, 100.0]), rhs=np.ones(3)), T=1)
+    assert o.residual_trace[-1] < 1e-28
+    # multi-RHS == column solves (test_linsolve.py:191-199)
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((8, 8)) + 1j * rng.standard_normal((8, 8))
+    P = A @ A.conj().T + 8 * np.eye(8)
+    S = rng.standard_normal((8, 3)) + 1j * rng.standard_normal((8, 3))
+    joint = X.jacpcg_solve(X.HpdSystem(P=P, rhs=S), T=5)
+    for j in range(3):
+        single = X.jacpcg_solve(X.HpdSystem(P=P, rhs=S[:, j]), T=5)
+        np.testing.assert_allclose(joint.w[:, j], single.w, rtol=1e-12, atol=1e-14)
+
+
+def test_solver_errors():
+    with pytest.raises(NotHpdError):
+        X.direct_solve(X.HpdSystem(P=np.diag([1.0, -1.0]), rhs=np.ones(2)))
+    with pytest.raises(NotHpdError):
+        X.cg_solve(X.HpdSystem(P=np.diag([1.0, -1.0]), rhs=np.array([0.0, 1.0])), 2)
+    with pytest.raises(SplittingError):
+        X.jacpcg_solve(X.HpdSystem(P=np.diag([0.0, 1.0]), rhs=np.ones(2)), T=1)
+    with pytest.raises(ConfigurationError):
+        X.jacpcg_solve(X.HpdSystem(P=np.eye(2), rhs=np.ones(2)), T=1, variant="fast")
+    with pytest.raises(ConfigurationError):
+        X.cg_solve(X.HpdSystem(P=np.eye(2), rhs=np.ones(2)), T=0)
+    # batched: a bad realization is flagged per realization, others untouched
+    A = torch.eye(3, dtype=torch.complex128, device=DEV).repeat(3, 1, 1)
+    A[1, 2, 2] = -1.0
+    res = BT.solve_batched(A, "cg", T=3, check=False)
+    assert res.status.cpu().tolist() == [0, 1, 0]
+    res = BT.solve_batched(A, "direct", check=False)
+    assert res.status.cpu().tolist() == [0, 4, 0]
+
+
+# ----------------------------------------------------------- precoders ------
+
+@pytest.mark.parametrize("tag", ["cfg1", "small", "rand"])
+def test_precoder_golden_c128(golden, tag):
+    g = golden("precoders")
+    Hb = g[tag + "_H"]
+    alpha, power, sigma2 = float(g[tag + "_alpha"]), float(g[tag + "_power"]), float(g[tag + "_sigma2"])
+    H = dev(Hb)
+    for key in [k for k in g.files if k.startswith(tag + "_") and k.endswith("_G")]:
+        meth_T = key[len(tag) + 1:-2]
+        meth, T = meth_T.rsplit("_T", 1)
+        method = meth.split("_")[0]
+        variant = meth.split("_")[1] if "_" in meth else "textbook"
+        out = BT.rzf_batched(H, alpha, power, method=method, T=int(T), variant=variant,
+                             sigma2=sigma2, want_F=True)
+        W = out.W.cpu().numpy()
+        for b in range(Hb.shape[0]):
+            assert relf(W[b], g[key][b]) <= 1e-10, (key, b, relf(W[b], g[key][b]))
+        np.testing.assert_allclose(out.beta.cpu().numpy(), g[key[:-2] + "_beta"], rtol=1e-10)
+        np.testing.assert_allclose(out.gamma.cpu().numpy(), g[key[:-2] + "_gamma"], rtol=1e-9)
+        np.testing.assert_allclose(out.sum_se.cpu().numpy(), g[key[:-2] + "_sumse"], rtol=1e-10)
+        # G = beta F (precoder.py:70)
+        np.testing.assert_allclose(W, out.F.cpu().numpy() * out.beta.cpu().numpy()[:, None, None],
+                                   rtol=1e-14, atol=0)
+
+
+def test_precoder_mirror_pins():
+    """test_precoder.py:38-103 through the reference-named mirror."""
+    power = 3.0
+    blk = X.rzf_direct(np.eye(2), 1.0, power)
+    np.testing.assert_allclose(blk.F, 0.5 * np.eye(2), atol=1e-14)
+    assert blk.beta == pytest.approx(np.sqrt(power / 0.5))
+    rng = np.random.default_rng(2)
+    H = rng.standard_normal((12, 6)) + 1j * rng.standard_normal((12, 6))
+    blk = X.rzf_direct(H, 0.3, 2.5)
+    assert float(np.vdot(blk.G, blk.G).real) == pytest.approx(2.5, rel=1e-10)
+    H = rng.standard_normal((10, 4)) + 1j * rng.standard_normal((10, 4))
+    blk = X.rzf_direct(H, 1e6, 1.0)   # matched-filter limit
+    assert np.linalg.norm(blk.G / np.linalg.norm(blk.G) - H / np.linalg.norm(H)) < 1e-3
+    with pytest.raises(DegenerateChannelError):
+        X.rzf_direct(np.zeros((4, 2)), 0.5, 1.0)
+    H = np.random.default_rng(4).standard_normal((12, 6)) + 1j * np.random.default_rng(5).standard_normal((12, 6))
+    exact = X.rzf_direct(H, 0.2, 1.0)
+    approx = X.rzf_iterative(H, 0.2, 1.0, solver="cg", T=6)
+    assert np.linalg.norm(approx.G - exact.G) / np.linalg.norm(exact.G) < 1e-6
+    for solver in ("cg", "jacpcg"):
+        blk = X.rzf_iterative(H, 0.2, 4.0, solver=solver, T=3, pcg_variant="textbook")
+        assert float(np.vdot(blk.G, blk.G).real) == pytest.approx(4.0, rel=1e-10)
+    errs = [np.linalg.norm(X.rzf_iterative(H, 0.2, 1.0, solver="cg", T=T).G - exact.G)
+            for T in range(1, 7)]
+    assert all(b <= a * (1 + 1e-9) for a, b in zip(errs, errs[1:]))
+    with pytest.raises(ConfigurationError):
+        X.rzf_iterative(H, 0.2, 1.0, solver="cg", T=0)
+    with pytest.raises(ConfigurationError):
+        X.rzf_iterative(H, 0.2, 1.0, solver="sor", T=2)
+    # eps early stop path matches the oracle
+    ref = O.rzf_iterative(H, 0.2, 1.0, "jacpcg", 50, eps=1e-8, pcg_variant="textbook")
+    blk = X.rzf_iterative(H, 0.2, 1.0, solver="jacpcg", T=50, eps=1e-8, pcg_variant="textbook")
+    assert relf(blk.G, ref[0]) < 1e-10
+
+
+def test_sinr_mirror_pins():
+    rng = np.random.default_rng(0)
+    H = rng.standard_normal((9, 4)) + 1j * rng.standard_normal((9, 4))
+    G, _, _ = O.rzf_direct(H, 0.5, 1.0)
+    rep = X.sinr_eq9(H, G, 1e-9)
+    g_ref, se_ref, s_ref = O.sinr_single_block(H, G, 1e-9)
+    np.testing.assert_allclose(rep.gamma, g_ref, rtol=1e-12)
+    assert rep.sum_se == pytest.approx(rep.se_per_user.sum())
+    np.testing.assert_allclose(X.coupling_matrix(H, G), H.conj().T @ G, atol=1e-12)
+    zero = X.sinr_eq9(H, np.zeros_like(G), 1e-8)
+    np.testing.assert_array_equal(zero.gamma, 0.0)
+    assert zero.sum_se == 0.0
+    with pytest.raises(ConfigurationError):
+        X.sinr_eq9(H, G, 0.0)
+    assert X.sum_se([5.0]) == (5.0, 0.0)
+    m, s = X.sum_se(torch.tensor([1.0, 2.0, 3.0], dtype=torch.float64, device=DEV))
+    assert m == pytest.approx(2.0) and s == pytest.approx(1.0 / np.sqrt(3.0))
+
+
+# ------------------------------------------------------- complex64 path -----
+
+@pytest.mark.parametrize("cfg,B", [("cfg2", 16), ("cfg3", 8), ("cfg4", 2)])
+@pytest.mark.parametrize("method", ["jacpcg", "cg", "direct"])
+def test_c64_vs_oracle(cfg, B, method):
+    wl = X.CONFIGS[cfg]
+    H = X.generate_channels(wl.model, seed=0, first=1000, B=B, dtype=torch.complex64)
+    out = BT.rzf_batched(H, wl.alpha(), wl.power(), method=method, T=wl.T, sigma2=1.0)
+    Hn = H.cpu().numpy().astype(np.complex128)   # input quantisation not charged to the kernel
+    W = out.W.cpu().numpy()
+    S = out.sum_se.cpu().numpy()
+    for b in range(B):
+        Gr, beta, gam, s = O.precoder_and_se(Hn[b], wl.alpha(), wl.power(), 1.0, method, wl.T,
+                                             "textbook")
+        assert relf(W[b], Gr) <= 1e-4, (cfg, method, b, relf(W[b], Gr))
+        assert abs(S[b] - s) / abs(s) <= 1e-4, (cfg, method, b, S[b], s)
+
+
+def test_c128_cfg1_full_batch():
+    """configs[0]: 100 realizations, complex128, Jac-PCG T=4 and direct at 1e-10."""
+    wl = X.CONFIGS["cfg1"]
+    H = X.generate_channels(wl.model, seed=0, first=0, B=wl.B, dtype=torch.complex128)
+    Hn = H.cpu().numpy()
+    for method in ("jacpcg", "direct"):
+        out = BT.rzf_batched(H, wl.alpha(), wl.power(), method=method, T=wl.T)
+        W = out.W.cpu().numpy()
+        S = out.sum_se.cpu().numpy()
+        for b in range(wl.B):
+            Gr, beta, gam, s = O.precoder_and_se(Hn[b], wl.alpha(), wl.power(), 1.0, method,
+                                                 wl.T, "textbook")
+            assert relf(W[b], Gr) <= 1e-10
+            assert abs(S[b] - s) <= 1e-10 * abs(s)
+
+
+def test_power_identity_and_properties_full_size():
+    """Size-independent properties at a BASELINE size (cfg3 shape, 512 realizations)."""
+    wl = X.CONFIGS["cfg3"]
+    H = X.generate_channels(wl.model, seed=1, first=0, B=512, dtype=torch.complex64)
+    out = BT.rzf_batched(H, wl.alpha(), wl.power(), T=wl.T, want_F=True)
+    tr = (out.W.abs() ** 2).sum(dim=(1, 2)).double()
+    assert torch.allclose(tr, torch.full_like(tr, wl.power()), rtol=1e-5)
+    assert (out.gamma >= 0).all() and torch.isfinite(out.gamma).all()
+    se = torch.log2(1 + out.gamma).sum(dim=1)
+    assert torch.allclose(se, out.sum_se, rtol=1e-12)
+    assert (out.status == 0).all()
+    # determinism: identical bits on a second run
+    out2 = BT.rzf_batched(H, wl.alpha(), wl.power(), T=wl.T)
+    assert torch.equal(out.W, out2.W) and torch.equal(out.sum_se, out2.sum_se)
+    # batch independence: a sub-batch reproduces the same bits
+    sub = BT.rzf_batched(H[100:117].contiguous(), wl.alpha(), wl.power(), T=wl.T)
+    assert torch.equal(sub.W, out.W[100:117])
+
+
+def test_degenerate_realization_flagged():
+    H = torch.randn(3, 64, 8, dtype=torch.complex64, device=DEV)
+    H[1] = 0
+    out = BT.rzf_batched(H, 0.5, 1.0, T=3, check=False)
+    assert out.status.cpu().tolist() == [0, 3, 0]
+    with pytest.raises(DegenerateChannelError):
+        BT.rzf_batched(H, 0.5, 1.0, T=3)
+
+
+# ------------------------------------------------------------- channel ------
+
+@pytest.mark.parametrize("dt,tol", [(torch.complex128, 1e-12), (torch.complex64, 2e-6)])
+def test_channel_generator_vs_oracle(dt, tol):
+    for (S, K, p, r) in ((4, 16, 0.5, 0.5), (16, 64, 0.4, 0.7), (3, 5, 0.3, 0.9)):
+        m = X.ChannelModel(S=S, K=K, p=p, r=r)
+        H = X.generate_channels(m, seed=123, first=77, B=6, dtype=dt).cpu().numpy()
+        ref = O.generate_channels(123, 77, 6, S, K, p, r)
+        # exact zeros on invisible subarrays
+        np.testing.assert_array_equal(H == 0, ref == 0)
+        assert relf(H, ref) < tol
+
+
+def test_channel_sharding_property():
+    m = X.ChannelModel(S=16, K=64, p=0.4, r=0.7)
+    full = X.generate_channels(m, seed=5, first=0, B=64)
+    a = X.generate_channels(m, seed=5, first=0, B=32)
+    b = X.generate_channels(m, seed=5, first=32, B=32)
+    assert torch.equal(torch.cat([a, b]), full)
+
+
+def test_se_partials_vs_oracle():
+    x = torch.rand(10000, dtype=torch.float64, device=DEV) * 50
+    parts = BT.se_partials(x, 2048).cpu().numpy()
+    assert parts.shape == (5, 3) and parts[:, 2].sum() == 10000
+    mean, sem = BT.combine_se_partials(parts)
+    rm, rs = O.sum_se(x.cpu().numpy())
+    assert mean == pytest.approx(rm, rel=1e-13) and sem == pytest.approx(rs, rel=1e-9)
