@@ -43,7 +43,9 @@ enum {
   XL_STATUS_SPLITTING = 2,   /* zero preconditioner diagonal: linsolve.py:205-208 */
   XL_STATUS_DEGENERATE = 3,  /* tr(F^H F) <= 0: precoder.py:66-68 */
   XL_STATUS_CHOLESKY = 4,    /* Cholesky breakdown -> NotHpdError: linsolve.py:113-116 */
-  XL_STATUS_NO_VISIBLE = 5   /* generator: no visible subarray (geometry.py:179-180) */
+  XL_STATUS_NO_VISIBLE = 5,  /* generator: no visible subarray (geometry.py:179-180) */
+  XL_STATUS_RANGE = 6        /* fused c64 kernel: |H| dynamic range exceeds the fp16-split
+                                scaling; re-run those realizations with xl_rzf_general */
 };
 
 enum {
@@ -116,6 +118,21 @@ int xl_apply_precoder(int dtype, const void* H, const void* X, int64_t B, int32_
                       int32_t K, double power, double sigma2, void* W, void* F,
                       double* beta, double* gamma, double* sum_se, int32_t* status,
                       void* workspace, size_t ws_bytes, xl_stream_t stream);
+
+/* Same contract as xl_rzf, always on the general (SIMT) kernels; the
+ * fallback for XL_STATUS_RANGE realizations and a cross-check of the fused
+ * tensor-core path. */
+size_t xl_rzf_general_workspace_bytes(int dtype, int method, int64_t B, int32_t M,
+                                      int32_t K);
+int xl_rzf_general(int dtype, int method, int variant, const void* H, int64_t B,
+                   int32_t M, int32_t K, double xi, const double* xi_per_batch,
+                   double power, int32_t T, double sigma2, void* W, void* F,
+                   double* beta, double* gamma, double* sum_se, void* X,
+                   int32_t* status, void* workspace, size_t ws_bytes,
+                   xl_stream_t stream);
+/* Test hook: when non-NULL, the fused kernel also writes the regularized Gram
+ * A[B][K][K] (complex64) of every realization it processes. */
+void xl_debug_set_gram_out(void* A);
 
 /* Per-user SINR/SE of an arbitrary precoder G on one full-array block:
  * sinr_eq9 (metrics.py:47-58) with coupling B = H^H G (metrics.py:35-44).

@@ -21,6 +21,7 @@ XL_C64, XL_C128 = 0, 1
 XL_JACPCG, XL_CG, XL_DIRECT = 0, 1, 2
 XL_TEXTBOOK, XL_ALGORITHM = 0, 1
 XL_SUCCESS, XL_ERR_CONFIG, XL_ERR_CUDA, XL_ERR_UNSUPPORTED, XL_ERR_WORKSPACE = 0, 1, 2, 3, 4
+XL_STATUS_RANGE = 6
 
 STATUS_EXCEPTIONS = {
     1: (NotHpdError, "nonpositive direction curvature encountered; P is not HPD"),
@@ -28,6 +29,7 @@ STATUS_EXCEPTIONS = {
     3: (DegenerateChannelError, "tr(F^H F) = 0; channel block carries no energy"),
     4: (NotHpdError, "Cholesky breakdown: matrix is not positive definite"),
     5: (GeometryInfeasibleError, "no visible subarray after the retry budget"),
+    6: (XlMimoError, "fp16-split range exceeded (re-run on the general path)"),
 }
 
 
@@ -61,6 +63,10 @@ _SIGNATURES = {
     "xl_rzf_workspace_bytes": (_sz, [_int, _int, _i64, _i32, _i32]),
     "xl_rzf": (_int, [_int, _int, _int, _p, _i64, _i32, _i32, _f64, _p, _f64, _i32,
                       _f64, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
+    "xl_rzf_general_workspace_bytes": (_sz, [_int, _int, _i64, _i32, _i32]),
+    "xl_rzf_general": (_int, [_int, _int, _int, _p, _i64, _i32, _i32, _f64, _p, _f64, _i32,
+                              _f64, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
+    "xl_debug_set_gram_out": (None, [_p]),
     "xl_apply_precoder_workspace_bytes": (_sz, [_int, _i64, _i32, _i32]),
     "xl_apply_precoder": (_int, [_int, _p, _p, _i64, _i32, _i32, _f64, _f64, _p, _p, _p,
                                  _p, _p, _p, _p, _sz, _p]),

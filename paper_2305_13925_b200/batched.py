@@ -113,14 +113,16 @@ def uses_tensor_cores(dtype, method, M, K) -> bool:
 def rzf_batched(H: torch.Tensor, xi, power: float, method: str = "jacpcg", T: int = 4,
                 variant: str = "textbook", sigma2: float = 1.0, *, want_gamma=True,
                 want_F=False, want_X=False, out: PrecoderBatch | None = None,
-                check: bool = True, stream=None) -> PrecoderBatch:
+                check: bool = True, stream=None, general: bool = False) -> PrecoderBatch:
     """Batched RZF precoder + SINR/SE (the hot path, one fused launch when the
     tcgen05 kernel covers the shape).
 
     Mirrors ``rzf_iterative`` / ``rzf_direct`` (precoder.py:73-91) followed by
     ``sinr_eq9`` (metrics.py:47-58) on one full-array block per realization.
-    ``check=True`` copies the status vector to the host (one sync) and raises
-    the reference exception of the first failing realization.
+    ``check=True`` copies the status vector to the host (one sync), re-runs
+    realizations the fused kernel flagged XL_STATUS_RANGE on the general GPU
+    kernels, and raises the reference exception of the first failing
+    realization.  ``general=True`` forces the general (SIMT) kernels.
     """
     lib = L.lib()
     if method not in METHODS:
@@ -133,17 +135,40 @@ def rzf_batched(H: torch.Tensor, xi, power: float, method: str = "jacpcg", T: in
     xs, xt = _xi_args(xi, B, H.device)
     if out is None:
         out = alloc_outputs(H, want_gamma, want_F, want_X)
-    nbytes = int(lib.xl_rzf_workspace_bytes(dc, METHODS[method], B, M, K))
+    if general:
+        nbytes = int(lib.xl_rzf_general_workspace_bytes(dc, METHODS[method], B, M, K))
+        fn = lib.xl_rzf_general
+    else:
+        nbytes = int(lib.xl_rzf_workspace_bytes(dc, METHODS[method], B, M, K))
+        fn = lib.xl_rzf
     ws = _WS.get(H.device, nbytes)
-    rc = lib.xl_rzf(dc, METHODS[method], VARIANTS[variant], L.ptr(H), B, M, K, xs,
-                    L.ptr(xt), float(power), int(T), float(sigma2), L.ptr(out.W),
-                    L.ptr(out.F), L.ptr(out.beta), L.ptr(out.gamma), L.ptr(out.sum_se),
-                    L.ptr(out.X), L.ptr(out.status), L.ptr(ws), ws.numel(),
-                    L.stream_ptr(stream))
+    rc = fn(dc, METHODS[method], VARIANTS[variant], L.ptr(H), B, M, K, xs,
+            L.ptr(xt), float(power), int(T), float(sigma2), L.ptr(out.W),
+            L.ptr(out.F), L.ptr(out.beta), L.ptr(out.gamma), L.ptr(out.sum_se),
+            L.ptr(out.X), L.ptr(out.status), L.ptr(ws), ws.numel(),
+            L.stream_ptr(stream))
     L.check(rc, "xl_rzf")
     if check:
-        L.raise_status(out.status.cpu().numpy(), "rzf_batched")
+        st = out.status.cpu().numpy()
+        redo = (st == L.XL_STATUS_RANGE).nonzero()[0]
+        if redo.size:
+            _rerun_general(H, redo, xi, power, method, T, variant, sigma2, out, stream)
+            st = out.status.cpu().numpy()
+        L.raise_status(st, "rzf_batched")
     return out
+
+
+def _rerun_general(H, idx, xi, power, method, T, variant, sigma2, out, stream):
+    """Re-run flagged realizations on the general GPU kernels and scatter back."""
+    it = torch.from_numpy(idx).to(H.device)
+    xsub = xi[it] if isinstance(xi, torch.Tensor) else xi
+    sub = rzf_batched(H.index_select(0, it).contiguous(), xsub, power, method, T, variant, sigma2,
+                      want_gamma=out.gamma is not None, want_F=out.F is not None,
+                      want_X=out.X is not None, check=False, stream=stream, general=True)
+    for name in ("W", "beta", "sum_se", "status", "gamma", "F", "X"):
+        dst = getattr(out, name)
+        if dst is not None:
+            dst.index_copy_(0, it, getattr(sub, name))
 
 
 def gram_batched(H: torch.Tensor, xi, stream=None) -> torch.Tensor:

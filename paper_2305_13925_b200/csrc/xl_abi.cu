@@ -127,10 +127,19 @@ size_t xl_rzf_workspace_bytes(int dtype, int method, int64_t B, int32_t M, int32
   return simt_rzf_ws(dtype, B, M, K);
 }
 
-int xl_rzf(int dtype, int method, int variant, const void* H, int64_t B, int32_t M,
-           int32_t K, double xi, const double* xi_per_batch, double power, int32_t T,
-           double sigma2, void* W, void* F, double* beta, double* gamma, double* sum_se,
-           void* X, int32_t* status, void* workspace, size_t ws_bytes, xl_stream_t stream) {
+size_t xl_rzf_general_workspace_bytes(int dtype, int method, int64_t B, int32_t M, int32_t K) {
+  (void)method;
+  return simt_rzf_ws(dtype, B, M, K);
+}
+
+static void* g_dbg_gram = nullptr;
+void xl_debug_set_gram_out(void* A) { g_dbg_gram = A; }
+
+static int rzf_impl(bool allow_fused, int dtype, int method, int variant, const void* H, int64_t B,
+                    int32_t M, int32_t K, double xi, const double* xi_per_batch, double power,
+                    int32_t T, double sigma2, void* W, void* F, double* beta, double* gamma,
+                    double* sum_se, void* X, int32_t* status, void* workspace, size_t ws_bytes,
+                    xl_stream_t stream) {
   if (int e = check_dtype(dtype)) return e;
   if (method != XL_JACPCG && method != XL_CG && method != XL_DIRECT) { set_error("unknown method %d", method); return XL_ERR_CONFIG; }
   if (variant != XL_TEXTBOOK && variant != XL_ALGORITHM) { set_error("unknown PCG variant %d", variant); return XL_ERR_CONFIG; }
@@ -140,12 +149,15 @@ int xl_rzf(int dtype, int method, int variant, const void* H, int64_t B, int32_t
   if (M < 1 || K < 1 || B < 0) { set_error("bad sizes"); return XL_ERR_CONFIG; }
   if (B == 0) return XL_SUCCESS;
   cudaStream_t st = (cudaStream_t)stream;
-  if (ws_bytes < xl_rzf_workspace_bytes(dtype, method, B, M, K)) { set_error("rzf: workspace too small"); return XL_ERR_WORKSPACE; }
+  const bool fused = allow_fused && fused_supported(dtype, method, M, K);
+  const size_t need = fused ? fused_ws_bytes(dtype, method, B, M, K) : simt_rzf_ws(dtype, B, M, K);
+  if (ws_bytes < need) { set_error("rzf: workspace too small"); return XL_ERR_WORKSPACE; }
   if (cudaMemsetAsync(status, 0, (size_t)B * sizeof(int32_t), st) != cudaSuccess) return check_launch("memset");
 
-  if (fused_supported(dtype, method, M, K))
+  if (fused)
     return launch_fused(dtype, method, variant, H, B, M, K, xi, xi_per_batch, power, T,
-                        sigma2, W, F, beta, gamma, sum_se, X, status, workspace, ws_bytes, st);
+                        sigma2, W, F, beta, gamma, sum_se, X, status, workspace, ws_bytes,
+                        g_dbg_gram, st);
 
   // ---- general SIMT path: Gram -> solve -> F = H X (+||F||^2) -> beta, W -> B = H^H W -> SINR
   const size_t cs = csize(dtype), kk = (size_t)B * K * K * cs;
@@ -164,6 +176,22 @@ int xl_rzf(int dtype, int method, int variant, const void* H, int64_t B, int32_t
                     T, -1.0, Xo, iters, nullptr, nullptr, status, sw, sws, stream))) return e;
   return apply_precoder(dtype, H, Xo, B, M, K, power, sigma2, W, F, beta, gamma, sum_se, status,
                         part, sw, st);
+}
+
+int xl_rzf(int dtype, int method, int variant, const void* H, int64_t B, int32_t M,
+           int32_t K, double xi, const double* xi_per_batch, double power, int32_t T,
+           double sigma2, void* W, void* F, double* beta, double* gamma, double* sum_se,
+           void* X, int32_t* status, void* workspace, size_t ws_bytes, xl_stream_t stream) {
+  return rzf_impl(true, dtype, method, variant, H, B, M, K, xi, xi_per_batch, power, T, sigma2,
+                  W, F, beta, gamma, sum_se, X, status, workspace, ws_bytes, stream);
+}
+
+int xl_rzf_general(int dtype, int method, int variant, const void* H, int64_t B, int32_t M,
+                   int32_t K, double xi, const double* xi_per_batch, double power, int32_t T,
+                   double sigma2, void* W, void* F, double* beta, double* gamma, double* sum_se,
+                   void* X, int32_t* status, void* workspace, size_t ws_bytes, xl_stream_t stream) {
+  return rzf_impl(false, dtype, method, variant, H, B, M, K, xi, xi_per_batch, power, T, sigma2,
+                  W, F, beta, gamma, sum_se, X, status, workspace, ws_bytes, stream);
 }
 
 size_t xl_apply_precoder_workspace_bytes(int dtype, int64_t B, int32_t M, int32_t K) {
