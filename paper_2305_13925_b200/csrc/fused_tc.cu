@@ -1,38 +1,41 @@
-// Fused complex64 RZF precoder on the 5th-gen tensor cores (tcgen05 + TMEM).
+// Fused complex64 RZF precoder on the 5th-gen tensor cores (tcgen05 + TMEM),
+// warp-specialised and persistent (one CTA per SM walks over realizations).
 //
-// One persistent CTA per SM walks over realizations b.  Per realization:
+// Per realization b the CTA computes, entirely on chip:
+//   Gram   G = Z^T Z with Z the interleaved real embedding of H (M x 2K),
+//          A = G + xi I                      (gram_regularized, precoder.py:53-61)
+//   Jac-PCG / CG / Algorithm-1 with T iterations on the K identity right-hand
+//          sides at once                      (linsolve.py:217-294)
+//   ||F||^2 = tr(X^H G X), beta, coupling B = beta G X, SINR, sum-SE
+//                                              (precoder.py:64-70, metrics.py:35-58)
+//   W^T = beta Xe^T Z^T (second pass over H)  (precoder.py:90)
 //
-//   1. Gram   G' = Z'^T Z'  (Z' = s_z * [Re H | Im H] interleaved, real 2K-wide
-//             embedding of H, streamed in 128-antenna chunks through a double
-//             buffered smem ring; tcgen05.mma kind::f16, fp32 accumulators in
-//             TMEM).  Reference: gram_regularized, precoder.py:53-61.
-//   2. A'' = 2^ea (G' + s_z^2 xi I), written to smem as the real 2K x 2K
-//             embedding [[Ar,-Ai],[Ai,Ar]] (exactly Hermitian by construction).
-//   3. Jac-PCG / CG, T iterations, K identity right-hand sides at once
-//             (linsolve.py:217-294): Q = A'' P on the tensor core (N = K
-//             columns), per-column inner products by warp transpose-reductions
-//             (fixed order, deterministic), state X, R, P in registers.
-//   4. beta:  ||F||^2 = tr(X^H G X) and the coupling B = H^H W = beta G X from
-//             one more tensor-core product Q = G'' X (precoder.py:64-70,
-//             metrics.py:35-58); SINR, log2(1+gamma), sum-SE.
-//   5. W = beta H X: second pass over H (L2-resident, evict-first) with the
-//             real embedding of X as the B operand; TMEM accumulators double
-//             buffered so the epilogue (scale + store) of chunk c overlaps the
-//             MMAs of chunk c+1.
+// Roles (14 warps):
+//   warp 13       producer: cp.async.bulk (TMA) of raw fp32 H chunks (64
+//                 antennas) into an NS-stage smem ring, for the Gram pass and
+//                 again (L2-resident) for the W pass;
+//   warps 0-3     converters: raw fp32 -> (hi, lo) fp16 split tiles in place;
+//   warp 12       streaming MMA issuer: Gram and W tcgen05.mma per stage;
+//   warps 4-11    math: A build (TMEM -> registers, warp shuffles), the PCG
+//                 vector recurrences (state in registers, one RHS column per
+//                 register slot), its K x K tensor-core products, beta/SINR,
+//                 and the W epilogue (TMEM -> coalesced global stores).
 //
-// Precision ("3xFP16"): every fp32 operand x is split x = hi + 2^-11 lo with
-// hi, lo fp16 (22 significant bits); a product is hi*hi' + 2^-11 (hi*lo' +
-// lo*hi'), two TMEM accumulators, fp32 accumulation.  All operands are first
-// scaled by exact powers of two into fp16 range, so the result equals an
-// fp32-class computation (relative error ~1e-7; north_star bound 1e-4).  The
-// Gram needs only hi*hi and hi*lo (lo*hi is its transpose).
+// Precision ("3xFP16"): x = hi + lo, hi = fp16(x), lo = fp16(x - hi); a
+// product is hi*hi' + hi*lo' + lo*hi' accumulated in fp32 in TMEM (relative
+// error ~2^-22).  Operands are pre-scaled by exact powers of two (Z: first
+// nonzero chunk -> max in [2^10, 2^11); A'': diag < 2^14; P, X: max < 2^14),
+// which leaves every recurrence bit-equivalent to the unscaled one up to
+// rounding.  A |H| dynamic range that overflows the scaling is reported as
+// XL_STATUS_RANGE (the host re-runs those realizations on xl_rzf_general).
 //
-// smem operands use the SWIZZLE_NONE canonical layouts (8x8 fp16 core
-// matrices of 128 B).  One Z tile layout serves the Gram (MN-major A and B)
-// and the W product (K-major A).
+// smem operand layouts are the SWIZZLE_NONE canonical 8x8 fp16 core matrices
+// (128 B).  One Z tile layout (core rows = antennas, 16 B rows of 8
+// components) serves the Gram (MN-major A and B) and W^T (K-major B).
 #include <cuda_fp16.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "xl_common.cuh"
 #include "fused_tc.cuh"
@@ -48,7 +51,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
-// kind::f16 instruction descriptor: F16 x F16 -> F32, dense.
+// kind::f16 instruction descriptor: F16 x F16 -> F32, dense, no negation.
 __host__ __device__ constexpr uint32_t idesc(int M, int N, int a_mn, int b_mn) {
   return (1u << 4) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -66,16 +69,37 @@ __device__ __forceinline__ void commit(uint64_t* bar) {
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t cnt) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(cnt));
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+// Wait for the phase with this parity to complete.  A bounded spin traps
+// instead of hanging the GPU if a pipeline accounting bug ever deadlocks.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0, spins = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(done)
+        : "r"(su32(bar)), "r"(parity)
+        : "memory");
+    if (++spins > (1u << 28)) asm volatile("trap;");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t hint) {
   asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE_%=;\n\t"
-      "bra WAIT_%=;\n"
-      "DONE_%=:\n\t}\n" ::"r"(su32(bar)),
-      "r"(parity)
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar)), "l"(hint)
       : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -100,7 +124,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t ta, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
-// N consecutive fp32 TMEM columns of this thread's lane (N multiple of 8).
 template <int N>
 __device__ __forceinline__ void tmem_ld(uint32_t ta, float* v) {
   if constexpr (N % 16 == 0) {
@@ -112,43 +135,24 @@ __device__ __forceinline__ void tmem_ld(uint32_t ta, float* v) {
   }
 }
 
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ float4 ldg_hint(const float4* p, uint64_t pol) {
-  float4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ void stg_hint(float4* p, float4 v, uint64_t pol) {
-  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
-               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
-               : "memory");
-}
+constexpr uint64_t HINT_EVICT_FIRST = 0x12F0000000000000ull;
+constexpr uint64_t HINT_EVICT_LAST = 0x14F0000000000000ull;
 
 // ------------------------------------------------------------- helpers ----
-// x = hi + 2^-11 lo (both fp16), x already scaled into fp16 range.
+// x = hi + lo, hi = fp16(x), lo = fp16(x - hi)  (x pre-scaled into range)
 __device__ __forceinline__ void split(float x, __half& hi, __half& lo) {
   hi = __float2half_rn(x);
-  lo = __float2half_rn((x - __half2float(hi)) * 2048.0f);
+  lo = __float2half_rn(x - __half2float(hi));
 }
+__device__ __forceinline__ uint32_t h2u(__half2 v) { return *reinterpret_cast<uint32_t*>(&v); }
 __device__ __forceinline__ uint32_t pack2(__half a, __half b) {
   return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
 }
-// power-of-two scale s with max*s in [2^(t-1), 2^t); 1 when max == 0.
+// power-of-two s with max*s in [2^(t-1), 2^t); 1 when max == 0 / not finite.
 __device__ __forceinline__ float pow2_scale(float mx, int t) {
   if (!(mx > 0.0f) || !isfinite(mx)) return 1.0f;
   int e;
-  frexpf(mx, &e);  // mx in [2^(e-1), 2^e)
+  frexpf(mx, &e);
   return ldexpf(1.0f, t - e);
 }
 __device__ __forceinline__ float warp_max(float v) {
@@ -156,23 +160,15 @@ __device__ __forceinline__ float warp_max(float v) {
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
-__device__ __forceinline__ float warp_sumf(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
 // Sum each of N per-lane values over the 32 lanes; lane l returns the total
-// of column (l % N).  Fixed butterfly order -> bit-reproducible.
+// of column l % N.  Fixed butterfly order -> bit-reproducible.
 template <int N>
 __device__ __forceinline__ float warp_transpose_reduce(float (&v)[N]) {
   const int lane = threadIdx.x & 31;
-  // fold lanes above N first (plain sums)
 #pragma unroll
   for (int o = 16; o >= N; o >>= 1)
 #pragma unroll
     for (int i = 0; i < N; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
-  // transpose-reduce across the remaining N lanes
 #pragma unroll
   for (int half = N / 2; half >= 1; half >>= 1) {
     const bool up = (lane & half) != 0;
@@ -187,30 +183,34 @@ __device__ __forceinline__ float warp_transpose_reduce(float (&v)[N]) {
 }
 
 // ----------------------------------------------------------- geometry ----
+constexpr int NCONV = 4, NMATH = 8;
+constexpr int W_MMA = NCONV + NMATH, W_PROD = W_MMA + 1;
+constexpr int NTHREADS = 512;  // 16 warps = 4 warpgroups (setmaxnreg granularity)
+constexpr int BAR_CONV = 1, BAR_MATH = 2;
+constexpr int NMT = 32 * NMATH;               // math threads
+
 template <int KU>
 struct Geo {
-  static constexpr int NC = 2 * KU;           // real components (interleaved re/im)
-  static constexpr int MA = 128;              // antennas per chunk (W MMA M)
-  static constexpr int CMA = NC * 16;         // antenna-group stride in a Z tile
-  static constexpr int ZPART = MA * NC * 2;   // one fp16 Z tile (hi or lo)
-  static constexpr int ZBUF = 2 * ZPART;      // hi + lo
-  static constexpr int SLACK = 2048;          // M-padding reads past a tile
-  static constexpr int OFF_Z = 0;             // 2 ring buffers
-  static constexpr int GLD = NC + 1;          // fp32 Gram staging row stride
-  static constexpr int OFF_GS = 0;            // aliases the ring (after Gram)
-  static constexpr int OFF_PB = ((NC * GLD * 4) + 1023) / 1024 * 1024;  // P / X columns (B op)
+  static constexpr int NC = 2 * KU;          // real components (interleaved re/im)
+  static constexpr int CH = 64;              // antennas per ring stage
+  static constexpr int NS = 3;               // ring depth
+  static constexpr int SB = CH * NC * 4;     // stage bytes (raw fp32 == hi + lo fp16 tiles)
+  static constexpr int ZT = SB / 2;          // one fp16 tile
+  static constexpr int CMA = NC * 16;        // antenna-group (core row group) stride
+  static constexpr int OFF_AE = NS * SB + 2048;   // + slack for M-padded Gram reads
+  static constexpr int AEPART = 128 * NC * 2;     // A operand padded to 128 rows
+  static constexpr int OFF_PB = OFF_AE + 2 * AEPART;
   static constexpr int PBPART = KU * NC * 2;
-  static constexpr int RING_END = 2 * ZBUF + SLACK;
-  static constexpr int PB_END = OFF_PB + 2 * PBPART;
-  static constexpr int OFF_AE = ((RING_END > PB_END ? RING_END : PB_END) + 1023) / 1024 * 1024;
-  static constexpr int AEPART = 128 * NC * 2;  // A operand padded to 128 rows
-  static constexpr int OFF_SMALL = OFF_AE + 2 * AEPART + SLACK;
-  static constexpr int SMALL = 4096 + 64 * NC;
-  static constexpr int SMEM = OFF_SMALL + SMALL;
-  static constexpr int JH = KU / 2;            // PCG columns per thread
+  static constexpr int OFF_SMALL = OFF_PB + 2 * PBPART;
+  static constexpr int SMEM = OFF_SMALL + 4096;
+  static constexpr int JH = KU / 2;          // PCG columns per math thread
+  static constexpr int HC = NC / 2;          // Gram columns per math thread
+  static constexpr int NB = NC / 8;          // converter float4 blocks per thread
   static constexpr uint32_t ID_GRAM = idesc(128, NC, 1, 1);
-  static constexpr uint32_t ID_W = idesc(128, NC, 0, 0);
+  static constexpr uint32_t ID_W = idesc(128, CH, 0, 0);
   static constexpr uint32_t ID_P = idesc(128, KU, 0, 0);
+  // TMEM columns
+  static constexpr uint32_t T_GRAM = 0, T_Q = 128, T_W0 = 256, T_W1 = 320;
 };
 
 struct Params {
@@ -229,543 +229,557 @@ struct Params {
   float2* X;
   int32_t* status;
   float2* dbgA;  // optional [B][K][K] regularized Gram (tests)
+  int dbg;       // bisection: 1 = Gram + A only, 2 = no W pass
 };
 
-constexpr int NTHREADS = 256;
-
-// Load one 128-antenna chunk of H (fp32, row m = 2K interleaved floats),
-// scale by sz and store the fp16 hi / lo tiles.  Warp instruction = 8
-// antennas x 16 components (64 B per antenna row: full sectors).
-template <int KU>
-__device__ __forceinline__ void load_chunk(const float* Hb, int m0, uint8_t* zh, uint8_t* zl,
-                                           float& sz, int& have_scale, int* s_flag, float* s_red,
-                                           uint64_t pol, int& range_bad) {
-  using G = Geo<KU>;
-  constexpr int NB = (G::MA / 8) * (G::NC / 16) / 8;  // blocks per warp
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float4 v[NB];
-#pragma unroll
-  for (int i = 0; i < NB; ++i) {
-    const int blk = warp * NB + i;
-    const int rg = blk / (G::NC / 16), cb = blk % (G::NC / 16);
-    const int m = rg * 8 + (lane & 7), c = cb * 16 + 4 * (lane >> 3);
-    v[i] = ldg_hint(reinterpret_cast<const float4*>(Hb + (int64_t)(m0 + m) * G::NC + c), pol);
-  }
-  if (!have_scale) {  // block-uniform: first chunk with data fixes s_z
-    float mx = 0.0f;
-#pragma unroll
-    for (int i = 0; i < NB; ++i)
-      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
-    mx = warp_max(mx);
-    __syncthreads();
-    if (lane == 0) s_red[warp] = mx;
-    __syncthreads();
-    float m8 = s_red[0];
-#pragma unroll
-    for (int w = 1; w < 8; ++w) m8 = fmaxf(m8, s_red[w]);
-    if (m8 > 0.0f) {
-      sz = pow2_scale(m8, 7);  // max |Z'| in [2^6, 2^7): 2^8 headroom
-      have_scale = 1;
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < NB; ++i) {
-    const int blk = warp * NB + i;
-    const int rg = blk / (G::NC / 16), cb = blk % (G::NC / 16);
-    const int m = rg * 8 + (lane & 7), c = cb * 16 + 4 * (lane >> 3);
-    float f[4] = {v[i].x * sz, v[i].y * sz, v[i].z * sz, v[i].w * sz};
-    __half h[4], l[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (!(fabsf(f[e]) < 32768.0f)) range_bad = 1;  // also catches NaN / Inf
-      split(f[e], h[e], l[e]);
-    }
-    const int off = (m >> 3) * G::CMA + (c >> 3) * 128 + (m & 7) * 16 + (c & 7) * 2;
-    *reinterpret_cast<uint2*>(zh + off) = make_uint2(pack2(h[0], h[1]), pack2(h[2], h[3]));
-    *reinterpret_cast<uint2*>(zl + off) = make_uint2(pack2(l[0], l[1]), pack2(l[2], l[3]));
-  }
-  (void)s_flag;
-}
-
-// B-operand element (n, k) of an N x NC K-major tile (core rows = n).
+// Element (row n, col k) of an n x NC K-major operand tile (core rows = n).
 template <int KU>
 __device__ __forceinline__ int boff(int n, int k) {
   return (n >> 3) * (Geo<KU>::NC * 16) + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2;
 }
 
-// Cross-CTA-quadrant reduction of per-column partials: each of the 4 warps
-// sharing a column half writes its warp-reduced totals, then every thread
-// sums the 4 quadrants in fixed order for its JH columns.
-template <int JH>
-__device__ __forceinline__ void column_allreduce(float (&v)[JH], float* red, int q, int h) {
-  const int lane = threadIdx.x & 31;
-  float t = warp_transpose_reduce<JH>(v);
-  if (lane < JH) red[(q * 2 + h) * JH + lane] = t;
-  __syncthreads();
-#pragma unroll
-  for (int jj = 0; jj < JH; ++jj)
-    v[jj] = ((red[(0 * 2 + h) * JH + jj] + red[(1 * 2 + h) * JH + jj]) + red[(2 * 2 + h) * JH + jj]) +
-            red[(3 * 2 + h) * JH + jj];
-  __syncthreads();
-}
+struct Small {
+  uint64_t raw_full[4], conv_full[4], stage_free[4];
+  uint64_t gram_full, q_full, xe_ready, scale_ready;
+  uint64_t wfull[2], wfree[2];
+  uint32_t tmem_slot;
+  int pad0;
+  float sz_slot[2];
+  float conv_red[4];
+  float mred[8];
+  double dred[8];
+  float cdg[64];        // Re diag of A' (no xi) per user
+  float red[8 * 32];    // column reductions (4 quadrants x 2 halves x JH)
+  float rsq[2 * 128];
+  float dgq[128];
+  double sse[64];
+  int flags[4];
+};
 
-__device__ __forceinline__ float block_max(float v, float* red) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ __forceinline__ float math_max(float v, Small* sm) {
+  const int mw = (threadIdx.x >> 5) - NCONV, lane = threadIdx.x & 31;
   v = warp_max(v);
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  float m = red[0];
+  if (lane == 0) sm->mred[mw] = v;
+  named_sync(BAR_MATH, NMT);
+  float m = sm->mred[0];
 #pragma unroll
-  for (int w = 1; w < 8; ++w) m = fmaxf(m, red[w]);
-  __syncthreads();
+  for (int w = 1; w < NMATH; ++w) m = fmaxf(m, sm->mred[w]);
+  named_sync(BAR_MATH, NMT);
   return m;
 }
-
-__device__ __forceinline__ double block_sum_d(double v, double* red) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ __forceinline__ double math_sum_d(double v, Small* sm) {
+  const int mw = (threadIdx.x >> 5) - NCONV, lane = threadIdx.x & 31;
   v = warp_sum(v);
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
+  if (lane == 0) sm->dred[mw] = v;
+  named_sync(BAR_MATH, NMT);
   double s = 0.0;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) s += red[w];
-  __syncthreads();
+  for (int w = 0; w < NMATH; ++w) s += sm->dred[w];
+  named_sync(BAR_MATH, NMT);
   return s;
 }
+template <int JH>
+__device__ __forceinline__ void column_allreduce(float (&v)[JH], Small* sm, int q, int h) {
+  const int lane = threadIdx.x & 31;
+  float t = warp_transpose_reduce<JH>(v);
+  if (lane < JH) sm->red[(q * 2 + h) * JH + lane] = t;
+  named_sync(BAR_MATH, NMT);
+#pragma unroll
+  for (int jj = 0; jj < JH; ++jj)
+    v[jj] = ((sm->red[(0 * 2 + h) * JH + jj] + sm->red[(1 * 2 + h) * JH + jj]) + sm->red[(2 * 2 + h) * JH + jj]) +
+            sm->red[(3 * 2 + h) * JH + jj];
+  named_sync(BAR_MATH, NMT);
+}
 
-// Write the real 2K x 2K embedding of a complex K x K matrix M'' (from the
-// symmetrised fp32 Gram staging Gs, optionally + alpha on the diagonal) as
-// the split fp16 A operand (K-major, rows = output components).
+// Write the JH columns of this thread's component row r of an NC x KU
+// matrix (scaled by s) as the split B operand (rows = columns j, K = r).
 template <int KU>
-__device__ void build_A(const float* Gs, uint8_t* ah, uint8_t* al, float alpha_s, float sa,
-                        float2* dbg, float dbg_scale) {
-  using G = Geo<KU>;
-  for (int e = threadIdx.x; e < KU * KU; e += NTHREADS) {
-    const int k = e / KU, j = e % KU;
-    auto g = [&](int x, int y) { return Gs[x * G::GLD + y] + Gs[y * G::GLD + x]; };
-    float ar = g(2 * k, 2 * j) + g(2 * k + 1, 2 * j + 1);
-    float ai = g(2 * k, 2 * j + 1) - g(2 * k + 1, 2 * j);
-    if (k == j) ar += alpha_s;
-    if (dbg) dbg[e] = make_float2(ar * dbg_scale, ai * dbg_scale);
-    ar *= sa;
-    ai *= sa;
-    __half h0, l0, h1, l1, h2, l2;
-    split(ar, h0, l0);
-    split(-ai, h1, l1);
-    split(ai, h2, l2);
-    // rows 2k: (ar, -ai) at k-index 2j, 2j+1; row 2k+1: (ai, ar)
-    const int o0 = boff<KU>(2 * k, 2 * j), o1 = boff<KU>(2 * k + 1, 2 * j);
-    *reinterpret_cast<uint32_t*>(ah + o0) = pack2(h0, h1);
-    *reinterpret_cast<uint32_t*>(al + o0) = pack2(l0, l1);
-    *reinterpret_cast<uint32_t*>(ah + o1) = pack2(h2, h0);
-    *reinterpret_cast<uint32_t*>(al + o1) = pack2(l2, l0);
+__device__ __forceinline__ void write_cols(const float* v, float s, int r, int h, uint8_t* bh, uint8_t* bl) {
+  constexpr int JH = Geo<KU>::JH;
+#pragma unroll
+  for (int jj = 0; jj < JH; ++jj) {
+    __half hh, ll;
+    split(v[jj] * s, hh, ll);
+    const int o = boff<KU>(h * JH + jj, r);
+    *reinterpret_cast<__half*>(bh + o) = hh;
+    *reinterpret_cast<__half*>(bl + o) = ll;
   }
 }
 
+// K x K tensor-core product Q = A'' * Bop (3xFP16), issued by one thread.
+template <int KU>
+__device__ __forceinline__ void issue_kxk(uint32_t tq, uint32_t ah, uint32_t al, uint32_t bh, uint32_t bl,
+                                          uint64_t* bar) {
+  using G = Geo<KU>;
+  tc_after();
+#pragma unroll
+  for (int s = 0; s < G::NC / 16; ++s) {
+    const uint64_t dah = sdesc(ah + 256 * s, 128, G::NC * 16), dal = sdesc(al + 256 * s, 128, G::NC * 16);
+    const uint64_t dbh = sdesc(bh + 256 * s, 128, G::NC * 16), dbl = sdesc(bl + 256 * s, 128, G::NC * 16);
+    mma(tq, dah, dbh, G::ID_P, s != 0);
+    mma(tq, dah, dbl, G::ID_P, 1);
+    mma(tq, dal, dbh, G::ID_P, 1);
+  }
+  commit(bar);
+}
+
+// ------------------------------------------------------------ kernel ----
 template <int KU>
 __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
   using G = Geo<KU>;
-  constexpr int NC = G::NC, JH = G::JH;
+  constexpr int NC = G::NC, JH = G::JH, HC = G::HC, NS = G::NS;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* zh[2] = {smem + G::OFF_Z, smem + G::OFF_Z + G::ZBUF};
-  uint8_t* zl[2] = {smem + G::OFF_Z + G::ZPART, smem + G::OFF_Z + G::ZBUF + G::ZPART};
-  float* Gs = reinterpret_cast<float*>(smem + G::OFF_GS);
-  uint8_t* pbh = smem + G::OFF_PB;
-  uint8_t* pbl = smem + G::OFF_PB + G::PBPART;
+  uint8_t* ring = smem;
   uint8_t* aeh = smem + G::OFF_AE;
-  uint8_t* ael = smem + G::OFF_AE + G::AEPART;
-  uint8_t* small = smem + G::OFF_SMALL;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(small);           // [0,1]: ring, [2]: q
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(small + 64);
-  int* flags = reinterpret_cast<int*>(small + 128);              // [0] not_hpd, [1] range
-  float* fred = reinterpret_cast<float*>(small + 256);           // 64 floats
-  double* dred = reinterpret_cast<double*>(small + 512);         // 16 doubles
-  float* cd = reinterpret_cast<float*>(small + 1024);            // KU <= 64 (diag of A')
-  float* red = reinterpret_cast<float*>(small + 1280);           // 8 * JH <= 256 floats
-  float* rsq = reinterpret_cast<float*>(small + 2304);           // 2 * NC
-  float* dgq = rsq + 2 * NC;                                     // NC
-  double* sse = reinterpret_cast<double*>(small + 2304 + 12 * NC);  // KU
+  uint8_t* ael = aeh + G::AEPART;
+  uint8_t* pbh = smem + G::OFF_PB;
+  uint8_t* pbl = pbh + G::PBPART;
+  Small* sm = reinterpret_cast<Small*>(smem + G::OFF_SMALL);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int q = warp & 3, h = warp >> 2;
-  const int r = 32 * q + lane;  // TMEM lane / component row
+  const int nch = p.M / G::CH;
 
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    mbar_init(&bars[2], 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm->raw_full[s], 1);
+      mbar_init(&sm->conv_full[s], 1);
+      mbar_init(&sm->stage_free[s], 1);
+    }
+    mbar_init(&sm->gram_full, 1);
+    mbar_init(&sm->q_full, 1);
+    mbar_init(&sm->xe_ready, 1);
+    mbar_init(&sm->scale_ready, 1);
+    for (int j = 0; j < 2; ++j) {
+      mbar_init(&sm->wfull[j], 1);
+      mbar_init(&sm->wfree[j], NMT);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm->tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_before();
   __syncthreads();
   tc_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);  // this warp's lane quadrant
-  uint32_t nring[2] = {0, 0}, nq = 0;                     // commits per barrier
-  const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
-  const int nch = p.M / G::MA;
+  const uint32_t tmem = sm->tmem_slot;
 
-  for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
-    const float* Hb = reinterpret_cast<const float*>(p.H + b * (int64_t)p.M * KU);
-    const double alpha = p.xi_b ? p.xi_b[b] : p.xi;
-    float sz = 1.0f;
-    int have_scale = 0, range_bad = 0;
-    if (tid == 0) { flags[0] = 0; flags[1] = 0; }
-
-    // ---------------------------------------------------------- Gram ------
-    for (int c = 0; c < nch; ++c) {
-      const int j = c & 1;
-      if (c >= 2) mbar_wait(&bars[j], (nring[j] - 1) & 1);  // MMAs of chunk c-2 done
-      load_chunk<KU>(Hb, c * G::MA, zh[j], zl[j], sz, have_scale, flags, fred, pol_keep, range_bad);
-      fence_async_smem();
-      __syncthreads();
-      if (tid == 0) {
-        tc_after();
-        const uint32_t bh = su32(zh[j]), bl = su32(zl[j]);
-#pragma unroll
-        for (int s = 0; s < G::MA / 16; ++s) {
-          const uint64_t dh = sdesc(bh + 2 * s * G::CMA, G::CMA, 128);
-          const uint64_t dl = sdesc(bl + 2 * s * G::CMA, G::CMA, 128);
-          mma(tmem + 0, dh, dh, G::ID_GRAM, (c | s) != 0);    // Zh^T Zh
-          mma(tmem + 128, dh, dl, G::ID_GRAM, (c | s) != 0);  // Zh^T Zl
-        }
-        commit(&bars[j]);
-      }
-      ++nring[j];
-    }
-    {
-      const int jl = (nch - 1) & 1;
-      mbar_wait(&bars[jl], (nring[jl] - 1) & 1);
-      if (nch >= 2) {
-        const int jo = jl ^ 1;  // keep both parities in step
-        mbar_wait(&bars[jo], (nring[jo] - 1) & 1);
+#ifndef XL_REG_AUX
+#define XL_REG_AUX 56
+#define XL_REG_CONV 104
+#define XL_REG_MATH 176
+#endif
+  static_assert(128 * XL_REG_AUX + 128 * XL_REG_CONV + 256 * XL_REG_MATH <= 65536, "register budget");
+#if XL_USE_SETMAXNREG
+  if (warp >= W_MMA) {  // warpgroup 3: MMA issuer, producer, 2 idle warps
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(XL_REG_AUX));
+  } else if (warp < NCONV) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(XL_REG_CONV));
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(XL_REG_MATH));
+  }
+#endif
+  if (warp == W_PROD) {
+    // ------------------------------------------------------ producer ------
+    if (lane == 0) {
+      uint32_t i = 0;
+      for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
+        const char* Hb = reinterpret_cast<const char*>(p.H + b * (int64_t)p.M * KU);
+        for (int pass = 0; pass < (p.dbg ? 1 : 2); ++pass)
+          for (int c = 0; c < nch; ++c, ++i) {
+            const int s = i % NS;
+            if (i >= (uint32_t)NS) mbar_wait(&sm->stage_free[s], ((i / NS) - 1) & 1);
+            mbar_expect_tx(&sm->raw_full[s], G::SB);
+            bulk_g2s(ring + s * G::SB, Hb + (int64_t)c * G::SB, G::SB, &sm->raw_full[s],
+                     pass == 0 ? HINT_EVICT_LAST : HINT_EVICT_FIRST);
+          }
       }
     }
-    tc_after();
-    // Gs = 0.5 Dhh + 2^-11 Dc (row r); G = Gs + Gs^T below
-    if (32 * q < NC) {
-      constexpr int HC = NC / 2;
-      float a[16], x[16];
+  } else if (warp < NCONV) {
+    // ---------------------------------------------------- converters ------
+    uint32_t i = 0;
+    for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
+      float sz = 1.0f;
+      int have = 0;
+      for (int pass = 0; pass < (p.dbg ? 1 : 2); ++pass)
+        for (int c = 0; c < nch; ++c, ++i) {
+          const int s = i % NS;
+          uint8_t* st = ring + s * G::SB;
+          mbar_wait(&sm->raw_full[s], (i / NS) & 1);
+          float4 v[G::NB];
 #pragma unroll
-      for (int c0 = 0; c0 < HC; c0 += 16) {
-        if constexpr (HC % 16 == 0) {
-          tmem_ld16(tl + h * HC + c0, a);
-          tmem_ld16(tl + 128 + h * HC + c0, x);
-        } else {
-          tmem_ld8(tl + h * HC + c0, a);
-          tmem_ld8(tl + 128 + h * HC + c0, x);
+          for (int k = 0; k < G::NB; ++k) {
+            const int blk = warp * G::NB + k;               // 4 antennas x 32 components
+            const int rb = blk / (NC / 32), cs = blk % (NC / 32);
+            const int m = 4 * rb + (lane >> 3), cc = 32 * cs + 4 * (lane & 7);
+            v[k] = *reinterpret_cast<const float4*>(st + (m * NC + cc) * 4);
+          }
+          named_sync(BAR_CONV, 32 * NCONV);  // all raw reads done before in-place writes
+          if (pass == 0 && !have) {
+            float mx = 0.0f;
+#pragma unroll
+            for (int k = 0; k < G::NB; ++k)
+              mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[k].x), fabsf(v[k].y)), fmaxf(fabsf(v[k].z), fabsf(v[k].w))));
+            mx = warp_max(mx);
+            if (lane == 0) sm->conv_red[warp] = mx;
+            named_sync(BAR_CONV, 32 * NCONV);
+            mx = fmaxf(fmaxf(sm->conv_red[0], sm->conv_red[1]), fmaxf(sm->conv_red[2], sm->conv_red[3]));
+            named_sync(BAR_CONV, 32 * NCONV);
+            if (mx > 0.0f) {
+              sz = pow2_scale(mx, 11);  // first nonzero chunk: max |Z'| in [2^10, 2^11)
+              have = 1;
+            }
+          }
+          const float2 s2 = make_float2(sz, sz);
+#pragma unroll
+          for (int k = 0; k < G::NB; ++k) {
+            const int blk = warp * G::NB + k;
+            const int rb = blk / (NC / 32), cs = blk % (NC / 32);
+            const int m = 4 * rb + (lane >> 3), cc = 32 * cs + 4 * (lane & 7);
+            const float2 a = __fmul2_rn(make_float2(v[k].x, v[k].y), s2);
+            const float2 bq = __fmul2_rn(make_float2(v[k].z, v[k].w), s2);
+            const __half2 ha = __float22half2_rn(a), hb = __float22half2_rn(bq);
+            const float2 ra = __fadd2_rn(a, make_float2(-__low2float(ha), -__high2float(ha)));
+            const float2 rbq = __fadd2_rn(bq, make_float2(-__low2float(hb), -__high2float(hb)));
+            const __half2 la = __float22half2_rn(ra), lb = __float22half2_rn(rbq);
+            const int off = (m >> 3) * G::CMA + (cc >> 3) * 128 + (m & 7) * 16 + (cc & 7) * 2;
+            *reinterpret_cast<uint2*>(st + off) = make_uint2(h2u(ha), h2u(hb));
+            *reinterpret_cast<uint2*>(st + G::ZT + off) = make_uint2(h2u(la), h2u(lb));
+          }
+          fence_async_smem();
+          named_sync(BAR_CONV, 32 * NCONV);
+          if (warp == 0 && lane == 0) {
+            mbar_arrive(&sm->conv_full[s]);
+            if (pass == 0 && c == nch - 1) {
+              sm->sz_slot[0] = sz;
+              mbar_arrive(&sm->scale_ready);
+            }
+          }
         }
-        tmem_wait_ld();
-        if (r < NC) {
-          constexpr int W = (HC % 16 == 0) ? 16 : 8;
+    }
+  } else if (warp == W_MMA) {
+    // ------------------------------------------- streaming MMA issuer ------
+    if (lane == 0) {
+      uint32_t i = 0, k = 0, wc = 0;
+      uint32_t wuse[2] = {0, 0};
+      for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++k) {
+        for (int c = 0; c < nch; ++c, ++i) {  // Gram
+          const int s = i % NS;
+          mbar_wait(&sm->conv_full[s], (i / NS) & 1);
+          tc_after();
+          const uint32_t zh = su32(ring + s * G::SB), zl = zh + G::ZT;
 #pragma unroll
-          for (int i = 0; i < W; ++i) Gs[r * G::GLD + h * HC + c0 + i] = 0.5f * a[i] + x[i] * (1.0f / 2048.0f);
+          for (int ks = 0; ks < G::CH / 16; ++ks) {
+            const uint64_t dh = sdesc(zh + 2 * ks * G::CMA, G::CMA, 128);
+            const uint64_t dl = sdesc(zl + 2 * ks * G::CMA, G::CMA, 128);
+            mma(tmem + G::T_GRAM, dh, dh, G::ID_GRAM, (c | ks) != 0);
+            mma(tmem + G::T_GRAM, dh, dl, G::ID_GRAM, 1);
+            mma(tmem + G::T_GRAM, dl, dh, G::ID_GRAM, 1);
+          }
+          commit(&sm->stage_free[s]);
+        }
+        commit(&sm->gram_full);
+        if (p.dbg) continue;
+        mbar_wait(&sm->xe_ready, k & 1);
+        for (int c = 0; c < nch; ++c, ++i, ++wc) {  // W^T = Xe^T Z^T
+          const int s = i % NS;
+          const int j = wc & 1;
+          if (wuse[j] >= 1) mbar_wait(&sm->wfree[j], (wuse[j] - 1) & 1);
+          mbar_wait(&sm->conv_full[s], (i / NS) & 1);
+          tc_after();
+          const uint32_t zh = su32(ring + s * G::SB), zl = zh + G::ZT;
+          const uint32_t xh = su32(aeh), xl_ = su32(ael);
+          const uint32_t d = tmem + (j ? G::T_W1 : G::T_W0);
+#pragma unroll
+          for (int ks = 0; ks < NC / 16; ++ks) {
+            const uint64_t dxh = sdesc(xh + 256 * ks, 128, NC * 16), dxl = sdesc(xl_ + 256 * ks, 128, NC * 16);
+            const uint64_t dzh = sdesc(zh + 256 * ks, 128, G::CMA), dzl = sdesc(zl + 256 * ks, 128, G::CMA);
+            mma(d, dxh, dzh, G::ID_W, ks != 0);
+            mma(d, dxh, dzl, G::ID_W, 1);
+            mma(d, dxl, dzh, G::ID_W, 1);
+          }
+          commit(&sm->stage_free[s]);
+          commit(&sm->wfull[j]);
+          ++wuse[j];
         }
       }
     }
-    tc_before();
-    __syncthreads();
-
-    // diag, A scale 2^ea, A'' split
-    const float alpha_s = (float)(alpha * (double)sz * (double)sz);
-    float dmax = 0.0f;
-    for (int k = tid; k < KU; k += NTHREADS) {
-      const float d = 2.0f * Gs[2 * k * G::GLD + 2 * k] + 2.0f * Gs[(2 * k + 1) * G::GLD + 2 * k + 1] + alpha_s;
-      cd[k] = d;
-      dmax = fmaxf(dmax, d);
-    }
-    dmax = block_max(dmax, fred);
-    const float sa = pow2_scale(dmax, 14);  // diag(A'') < 2^14
-    build_A<KU>(Gs, aeh, ael, alpha_s, sa, p.dbgA ? p.dbgA + b * KU * KU : nullptr, 1.0f / (sz * sz));
-    fence_async_smem();
-    __syncthreads();
-
-    // ---------------------------------------------------------- PCG -------
+  } else if (warp < NCONV + NMATH) {
+    // ---------------------------------------------------------- math ------
+    const int mw = warp - NCONV;
+    const int q = warp & 3, h = mw >> 2;     // TMEM lane quadrant = warp % 4
+    const int r = 32 * q + lane;             // component row / output component
+    const bool act_row = r < NC;
+    const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
     const bool textbook = (p.method == XL_JACPCG && p.variant == XL_TEXTBOOK);
     const bool use_c = (p.method == XL_JACPCG);
-    const bool act_row = r < NC;
-    const float cr = act_row ? (use_c ? cd[r >> 1] * sa : 1.0f) : 1.0f;  // c'' (scaled)
-    float X[JH], R[JH], P[JH], rz[JH];
-#pragma unroll
-    for (int jj = 0; jj < JH; ++jj) {
-      const int jc = h * JH + jj;
-      const float e = (act_row && r == 2 * jc) ? 1.0f : 0.0f;
-      X[jj] = 0.0f;
-      if (textbook) {
-        R[jj] = e;
-        P[jj] = e / cr;
-        rz[jj] = 1.0f / (use_c ? cd[jc] * sa : 1.0f);
+    uint32_t k = 0, nq = 0, wc = 0;
+    uint32_t wuse[2] = {0, 0};
+    for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++k) {
+      const double alpha = p.xi_b ? p.xi_b[b] : p.xi;
+      mbar_wait(&sm->scale_ready, k & 1);
+      const float sz = sm->sz_slot[0];
+      mbar_wait(&sm->gram_full, k & 1);
+      tc_after();
+      // ---- A'' = sa (G + xi' I) from TMEM rows 2k, 2k+1 (lane pairs)
+      const float alpha_s = (float)(alpha * (double)sz * (double)sz);
+      float gv[HC];
+      if (32 * q < NC) {
+        tmem_ld<HC>(tl + G::T_GRAM + h * HC, gv);
+        tmem_wait_ld();
       } else {
-        R[jj] = use_c ? e / cr : e;
-        P[jj] = R[jj];
-        const float c0 = use_c ? cd[jc] * sa : 1.0f;
-        rz[jj] = use_c ? (1.0f / c0) * (1.0f / c0) : 1.0f;
-      }
-    }
-    int not_hpd = 0;
-    for (int t = 1; t <= p.T; ++t) {
-      // P scale + split into the B operand
-      float pm = 0.0f;
 #pragma unroll
-      for (int jj = 0; jj < JH; ++jj) pm = fmaxf(pm, fabsf(P[jj]));
-      const float sp = pow2_scale(block_max(pm, fred), 14);
+        for (int i2 = 0; i2 < HC; ++i2) gv[i2] = 0.0f;
+      }
+      tc_before();
+      const bool odd = lane & 1;
+      // pairs (ar, ai) for the columns of this half; diag into cdg
+#pragma unroll
+      for (int jp = 0; jp < HC / 2; ++jp) {
+        const float g0 = gv[2 * jp], g1 = gv[2 * jp + 1];
+        const float p0 = __shfl_xor_sync(0xffffffffu, g0, 1), p1 = __shfl_xor_sync(0xffffffffu, g1, 1);
+        const float ar = odd ? (p0 + g1) : (g0 + p1);
+        const float ai = odd ? (p1 - g0) : (g1 - p0);
+        gv[2 * jp] = ar;
+        gv[2 * jp + 1] = ai;
+        const int jc = (h * HC) / 2 + jp;
+        if (act_row && !odd && jc == (r >> 1)) sm->cdg[jc] = ar;
+      }
+      named_sync(BAR_MATH, NMT);
+      float dmax = 0.0f;
+      for (int kk = 0; kk < KU; ++kk) dmax = fmaxf(dmax, sm->cdg[kk] + alpha_s);
+      const bool range_bad = !isfinite(dmax);
+      const float sa = pow2_scale(dmax, 14);
+      const float gd = act_row ? sm->cdg[r >> 1] : 0.0f;  // Re A'_kk without xi
+      const float cr = act_row ? (use_c ? (gd + alpha_s) * sa : 1.0f) : 1.0f;
       if (act_row) {
+        const int kr = r >> 1;
+#pragma unroll
+        for (int jp = 0; jp < HC / 2; ++jp) {
+          const int jc = (h * HC) / 2 + jp;
+          float ar = gv[2 * jp], ai = gv[2 * jp + 1];
+          if (jc == kr) ar += alpha_s;
+          if (p.dbgA && !odd) {
+            const float inv = 1.0f / (sz * sz);
+            p.dbgA[(b * KU + kr) * KU + jc] = make_float2(ar * inv, ai * inv);
+          }
+          // row 2k: (ar, -ai); row 2k+1: (ai, ar)   at columns (2jc, 2jc+1)
+          const float e0 = (odd ? ai : ar) * sa, e1 = (odd ? ar : -ai) * sa;
+          __half h0, l0, h1, l1;
+          split(e0, h0, l0);
+          split(e1, h1, l1);
+          const int o = boff<KU>(r, 2 * jc);
+          *reinterpret_cast<uint32_t*>(aeh + o) = pack2(h0, h1);
+          *reinterpret_cast<uint32_t*>(ael + o) = pack2(l0, l1);
+        }
+      }
+      if (p.dbg == 1) {
+        named_sync(BAR_MATH, NMT);
+        if (tid == 32 * NCONV) p.status[b] = range_bad ? XL_STATUS_RANGE : 0;
+        continue;
+      }
+      // ---- PCG state
+      float X[JH], R[JH], P[JH], rz[JH];
+#pragma unroll
+      for (int jj = 0; jj < JH; ++jj) {
+        const int jc = h * JH + jj;
+        const float e = (act_row && r == 2 * jc) ? 1.0f : 0.0f;
+        const float c0 = use_c ? (sm->cdg[jc] + alpha_s) * sa : 1.0f;
+        X[jj] = 0.0f;
+        if (textbook) {
+          R[jj] = e;
+          P[jj] = e / cr;
+          rz[jj] = 1.0f / c0;
+        } else {
+          R[jj] = use_c ? e / cr : e;
+          P[jj] = R[jj];
+          rz[jj] = use_c ? (1.0f / c0) * (1.0f / c0) : 1.0f;
+        }
+      }
+      int not_hpd = 0;
+      const uint32_t uah = su32(aeh), ual = su32(ael), ubh = su32(pbh), ubl = su32(pbl);
+      for (int t = 1; t <= p.T; ++t) {
+        float pm = 0.0f;
+#pragma unroll
+        for (int jj = 0; jj < JH; ++jj) pm = fmaxf(pm, fabsf(P[jj]));
+        const float sp = pow2_scale(math_max(pm, sm), 14);
+        if (act_row) write_cols<KU>(P, sp, r, h, pbh, pbl);
+        fence_async_smem();
+        named_sync(BAR_MATH, NMT);
+        if (mw == 0 && lane == 0) issue_kxk<KU>(tmem + G::T_Q, uah, ual, ubh, ubl, &sm->q_full);
+        mbar_wait(&sm->q_full, nq & 1);
+        ++nq;
+        tc_after();
+        float Q[JH], cv[JH];
+        tmem_ld<JH>(tl + G::T_Q + h * JH, Q);
+        tmem_wait_ld();
+        tc_before();
+        const float isp = 1.0f / sp;
 #pragma unroll
         for (int jj = 0; jj < JH; ++jj) {
-          __half hh, ll;
-          split(P[jj] * sp, hh, ll);
-          const int o = boff<KU>(h * JH + jj, r);
-          *reinterpret_cast<__half*>(pbh + o) = hh;
-          *reinterpret_cast<__half*>(pbl + o) = ll;
+          Q[jj] = act_row ? Q[jj] * isp : 0.0f;
+          if (!textbook && use_c) Q[jj] = Q[jj] / cr;  // Algorithm 1: z = C^-1 P m
+          cv[jj] = P[jj] * Q[jj];
+        }
+        column_allreduce<JH>(cv, sm, q, h);  // curvature per column
+        float rn[JH];
+#pragma unroll
+        for (int jj = 0; jj < JH; ++jj) {
+          const bool act = rz[jj] > 0.0f;
+          if (cv[jj] <= 0.0f && act) not_hpd = 1;  // linsolve.py:277-279
+          const float al = act ? rz[jj] / (cv[jj] > 0.0f ? cv[jj] : 1.0f) : 0.0f;
+          X[jj] = X[jj] + al * P[jj];
+          R[jj] = R[jj] - al * Q[jj];
+          const float z = textbook ? R[jj] / cr : R[jj];
+          rn[jj] = R[jj] * z;
+        }
+        column_allreduce<JH>(rn, sm, q, h);  // new rz per column
+#pragma unroll
+        for (int jj = 0; jj < JH; ++jj) {
+          const bool act = rz[jj] > 0.0f;
+          const float be = act ? rn[jj] / rz[jj] : 0.0f;
+          const float z = textbook ? R[jj] / cr : R[jj];
+          P[jj] = z + be * P[jj];
+          rz[jj] = rn[jj];
+        }
+      }
+      // ---- beta / coupling: Q = G'' X'' with G'' = A'' - sa xi' I (diag only)
+      float xm = 0.0f;
+#pragma unroll
+      for (int jj = 0; jj < JH; ++jj) xm = fmaxf(xm, fabsf(X[jj]));
+      const float sx = pow2_scale(math_max(xm, sm), 14);
+      if (act_row && h == ((r >> 1) * 2) / HC) {  // owner of diagonal element (r, r)
+        __half hh, ll;
+        split(gd * sa, hh, ll);
+        const int o = boff<KU>(r, r);
+        *reinterpret_cast<__half*>(aeh + o) = hh;
+        *reinterpret_cast<__half*>(ael + o) = ll;
+      }
+      if (act_row) write_cols<KU>(X, sx, r, h, pbh, pbl);
+      fence_async_smem();
+      named_sync(BAR_MATH, NMT);
+      if (mw == 0 && lane == 0) issue_kxk<KU>(tmem + G::T_Q, uah, ual, ubh, ubl, &sm->q_full);
+      mbar_wait(&sm->q_full, nq & 1);
+      ++nq;
+      tc_after();
+      float GX[JH];
+      tmem_ld<JH>(tl + G::T_Q + h * JH, GX);
+      tmem_wait_ld();
+      tc_before();
+      const float isx = 1.0f / sx;
+#pragma unroll
+      for (int jj = 0; jj < JH; ++jj) GX[jj] = act_row ? GX[jj] * isx : 0.0f;
+      // kappa = sa sz^2: X_true = kappa X'', G X_true = GX
+      const double kappa = (double)sa * (double)sz * (double)sz;
+      double part = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < JH; ++jj) part += (double)X[jj] * (double)GX[jj];
+      const double fro2 = kappa * math_sum_d(part, sm);
+      double beta = 0.0;
+      int degenerate = 0;
+      if (fro2 > 0.0 && isfinite(fro2)) beta = sqrt(p.power / fro2);
+      else degenerate = 1;
+      {
+        float rs = 0.0f;
+#pragma unroll
+        for (int jj = 0; jj < JH; ++jj) rs += GX[jj] * GX[jj];
+        if (act_row) {
+          sm->rsq[h * NC + r] = rs;
+#pragma unroll
+          for (int jj = 0; jj < JH; ++jj)
+            if (h * JH + jj == (r >> 1)) sm->dgq[r] = GX[jj];
+        }
+      }
+      named_sync(BAR_MATH, NMT);
+      const int mt = tid - 32 * NCONV;  // 0..255
+      if (mt < KU) {
+        const double b2 = beta * beta;
+        const double tot = b2 * ((double)sm->rsq[2 * mt] + (double)sm->rsq[NC + 2 * mt] +
+                                 (double)sm->rsq[2 * mt + 1] + (double)sm->rsq[NC + 2 * mt + 1]);
+        const double sig = b2 * ((double)sm->dgq[2 * mt] * sm->dgq[2 * mt] +
+                                  (double)sm->dgq[2 * mt + 1] * sm->dgq[2 * mt + 1]);
+        const double g = sig / ((tot - sig) + p.sigma2);
+        if (p.gamma) p.gamma[b * KU + mt] = g;
+        sm->sse[mt] = log2(1.0 + g);
+      }
+      const bool any_not_hpd = math_max(not_hpd ? 1.0f : 0.0f, sm) > 0.0f;  // also orders sse
+      if (mt == 0) {
+        double s = 0.0;
+        for (int kk = 0; kk < KU; ++kk) s += sm->sse[kk];
+        p.sum_se[b] = s;
+        p.beta[b] = beta;
+        int st = XL_STATUS_OK;
+        if (range_bad) st = XL_STATUS_RANGE;
+        else if (any_not_hpd) st = XL_STATUS_NOT_HPD;
+        else if (degenerate) st = XL_STATUS_DEGENERATE;
+        p.status[b] = st;
+      }
+      if (p.X && act_row) {
+#pragma unroll
+        for (int jj = 0; jj < JH; ++jj) {
+          const int jc = h * JH + jj;
+          reinterpret_cast<float*>(p.X)[((b * KU + (r >> 1)) * KU + jc) * 2 + (r & 1)] = (float)(kappa * X[jj]);
+        }
+      }
+      // ---- Xe (A operand of W^T = Xe^T Z^T): element (row c2, col c) = Xe[c][c2]
+      //      Xe[2k][2j] = xr, Xe[2k+1][2j] = -xi, Xe[2k][2j+1] = xi, Xe[2k+1][2j+1] = xr
+      if (act_row) {
+        const int kr = r >> 1;
+#pragma unroll
+        for (int jj = 0; jj < JH; ++jj) {
+          const int jc = h * JH + jj;
+          const float v = X[jj] * sx;
+          __half h1, l1, h2, l2;
+          int o1, o2;
+          if (!(r & 1)) {  // xr
+            split(v, h1, l1);
+            h2 = h1;
+            l2 = l1;
+            o1 = boff<KU>(2 * jc, 2 * kr);
+            o2 = boff<KU>(2 * jc + 1, 2 * kr + 1);
+          } else {         // xi
+            split(-v, h1, l1);
+            split(v, h2, l2);
+            o1 = boff<KU>(2 * jc, 2 * kr + 1);
+            o2 = boff<KU>(2 * jc + 1, 2 * kr);
+          }
+          *reinterpret_cast<__half*>(aeh + o1) = h1;
+          *reinterpret_cast<__half*>(ael + o1) = l1;
+          *reinterpret_cast<__half*>(aeh + o2) = h2;
+          *reinterpret_cast<__half*>(ael + o2) = l2;
         }
       }
       fence_async_smem();
-      __syncthreads();
-      if (tid == 0) {
+      named_sync(BAR_MATH, NMT);
+      if (mt == 0) mbar_arrive(&sm->xe_ready);
+      // ---- W epilogue: lane row c2 = r, antennas [32h, 32h+32) of each chunk
+      const float wscale = (float)(beta * kappa / ((double)sz * (double)sx));
+      const float fscale = (float)(kappa / ((double)sz * (double)sx));
+      float* Wb = reinterpret_cast<float*>(p.W + b * (int64_t)p.M * KU);
+      float* Fb = p.F ? reinterpret_cast<float*>(p.F + b * (int64_t)p.M * KU) : nullptr;
+      for (int c = 0; c < (p.dbg ? 0 : nch); ++c, ++wc) {
+        const int j = wc & 1;
+        mbar_wait(&sm->wfull[j], wuse[j] & 1);
+        ++wuse[j];
         tc_after();
-        const uint32_t ah = su32(aeh), al = su32(ael), bh = su32(pbh), bl = su32(pbl);
-#pragma unroll
-        for (int s = 0; s < NC / 16; ++s) {
-          const uint64_t dah = sdesc(ah + 256 * s, 128, NC * 16), dal = sdesc(al + 256 * s, 128, NC * 16);
-          const uint64_t dbh = sdesc(bh + 256 * s, 128, NC * 16), dbl = sdesc(bl + 256 * s, 128, NC * 16);
-          mma(tmem + 0, dah, dbh, G::ID_P, s != 0);
-          mma(tmem + 128, dah, dbl, G::ID_P, s != 0);
-          mma(tmem + 128, dal, dbh, G::ID_P, 1);
-        }
-        commit(&bars[2]);
-      }
-      ++nq;
-      mbar_wait(&bars[2], (nq - 1) & 1);
-      tc_after();
-      float qa[JH], qx[JH], Q[JH];
-      tmem_ld<JH>(tl + h * JH, qa);
-      tmem_ld<JH>(tl + 128 + h * JH, qx);
-      tmem_wait_ld();
-      const float isp = 1.0f / sp;
-      float cv[JH];
-#pragma unroll
-      for (int jj = 0; jj < JH; ++jj) {
-        Q[jj] = act_row ? (qa[jj] + qx[jj] * (1.0f / 2048.0f)) * isp : 0.0f;
-        if (!textbook && use_c) Q[jj] = Q[jj] / cr;  // algorithm: z = C^-1 P m
-        cv[jj] = P[jj] * Q[jj];
-      }
-      tc_before();
-      column_allreduce<JH>(cv, red, q, h);  // curv_j
-      float alpha_j[JH], rn[JH];
-#pragma unroll
-      for (int jj = 0; jj < JH; ++jj) {
-        const bool act = rz[jj] > 0.0f;
-        if (cv[jj] <= 0.0f && act) not_hpd = 1;
-        alpha_j[jj] = act ? rz[jj] / (cv[jj] > 0.0f ? cv[jj] : 1.0f) : 0.0f;
-        X[jj] = X[jj] + alpha_j[jj] * P[jj];
-        R[jj] = R[jj] - alpha_j[jj] * Q[jj];
-        const float z = textbook ? R[jj] / cr : R[jj];
-        rn[jj] = R[jj] * z;
-      }
-      column_allreduce<JH>(rn, red, q, h);  // rz_new_j
-#pragma unroll
-      for (int jj = 0; jj < JH; ++jj) {
-        const bool act = rz[jj] > 0.0f;
-        const float be = act ? rn[jj] / rz[jj] : 0.0f;
-        const float z = textbook ? R[jj] / cr : R[jj];
-        P[jj] = z + be * P[jj];
-        rz[jj] = rn[jj];
-      }
-    }
-
-    // ------------------------------------------- beta, coupling, SINR -----
-    // Q = G'' X'' with G'' = sa * (Gs + Gs^T) (no alpha)
-    float xm = 0.0f;
-#pragma unroll
-    for (int jj = 0; jj < JH; ++jj) xm = fmaxf(xm, fabsf(X[jj]));
-    const float sx = pow2_scale(block_max(xm, fred), 14);
-    build_A<KU>(Gs, aeh, ael, 0.0f, sa, nullptr, 1.0f);
-    if (act_row) {
-#pragma unroll
-      for (int jj = 0; jj < JH; ++jj) {
-        __half hh, ll;
-        split(X[jj] * sx, hh, ll);
-        const int o = boff<KU>(h * JH + jj, r);
-        *reinterpret_cast<__half*>(pbh + o) = hh;
-        *reinterpret_cast<__half*>(pbl + o) = ll;
-      }
-    }
-    fence_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      tc_after();
-      const uint32_t ah = su32(aeh), al = su32(ael), bh = su32(pbh), bl = su32(pbl);
-#pragma unroll
-      for (int s = 0; s < NC / 16; ++s) {
-        const uint64_t dah = sdesc(ah + 256 * s, 128, NC * 16), dal = sdesc(al + 256 * s, 128, NC * 16);
-        const uint64_t dbh = sdesc(bh + 256 * s, 128, NC * 16), dbl = sdesc(bl + 256 * s, 128, NC * 16);
-        mma(tmem + 0, dah, dbh, G::ID_P, s != 0);
-        mma(tmem + 128, dah, dbl, G::ID_P, s != 0);
-        mma(tmem + 128, dal, dbh, G::ID_P, 1);
-      }
-      commit(&bars[2]);
-    }
-    ++nq;
-    mbar_wait(&bars[2], (nq - 1) & 1);
-    tc_after();
-    float GX[JH];
-    {
-      float qa[JH], qx[JH];
-      tmem_ld<JH>(tl + h * JH, qa);
-      tmem_ld<JH>(tl + 128 + h * JH, qx);
-      tmem_wait_ld();
-#pragma unroll
-      for (int jj = 0; jj < JH; ++jj) GX[jj] = act_row ? (qa[jj] + qx[jj] * (1.0f / 2048.0f)) / sx : 0.0f;
-    }
-    tc_before();
-    // kappa = sa * sz^2: X_true = kappa X'', G X_true = GX (exactly scaled)
-    const double kappa = (double)sa * (double)sz * (double)sz;
-    double part = 0.0;
-#pragma unroll
-    for (int jj = 0; jj < JH; ++jj) part += (double)X[jj] * (double)GX[jj];
-    const double fro2 = kappa * block_sum_d(part, dred);
-    double beta = 0.0;
-    int degenerate = 0;
-    if (fro2 > 0.0 && isfinite(fro2)) beta = sqrt(p.power / fro2);
-    else degenerate = 1;
-    // coupling B = beta * GX; row sums of |B|^2 and the diagonal
-    {
-      float rs = 0.0f;
-#pragma unroll
-      for (int jj = 0; jj < JH; ++jj) rs += GX[jj] * GX[jj];
-      if (act_row) {
-        rsq[h * NC + r] = rs;
-        const int jc = r >> 1;  // diagonal column of row r
-        if (jc >= h * JH && jc < (h + 1) * JH) {
-#pragma unroll
-          for (int jj = 0; jj < JH; ++jj)
-            if (h * JH + jj == jc) dgq[r] = GX[jj];
-        }
-      }
-    }
-    __syncthreads();
-    if (tid < KU) {
-      const int k = tid;
-      const double b2 = beta * beta;
-      const double tot = b2 * ((double)rsq[2 * k] + (double)rsq[NC + 2 * k] + (double)rsq[2 * k + 1] +
-                               (double)rsq[NC + 2 * k + 1]);
-      const double sig = b2 * ((double)dgq[2 * k] * dgq[2 * k] + (double)dgq[2 * k + 1] * dgq[2 * k + 1]);
-      const double g = sig / ((tot - sig) + p.sigma2);
-      if (p.gamma) p.gamma[b * KU + k] = g;
-      sse[k] = log2(1.0 + g);
-    }
-    __syncthreads();
-    not_hpd = __syncthreads_or(not_hpd);
-    range_bad = __syncthreads_or(range_bad);
-    if (tid == 0) {
-      double s = 0.0;
-      for (int k = 0; k < KU; ++k) s += sse[k];
-      p.sum_se[b] = s;
-      p.beta[b] = beta;
-      int st = XL_STATUS_OK;
-      if (range_bad) st = XL_STATUS_RANGE;
-      else if (not_hpd) st = XL_STATUS_NOT_HPD;
-      else if (degenerate) st = XL_STATUS_DEGENERATE;
-      p.status[b] = st;
-    }
-    if (p.X && act_row) {
-#pragma unroll
-      for (int jj = 0; jj < JH; ++jj) {
-        const int jc = h * JH + jj;
-        reinterpret_cast<float*>(p.X)[((b * KU + (r >> 1)) * KU + jc) * 2 + (r & 1)] = (float)(kappa * X[jj]);
-      }
-    }
-
-    // ------------------------------------------------------------ W -------
-    // Xe (real embedding of X'', scaled by sx) as the W B operand:
-    // Xe[2k][2j] = xr, Xe[2k+1][2j] = -xi, Xe[2k][2j+1] = xi, Xe[2k+1][2j+1] = xr
-    if (act_row) {
-      const int k = r >> 1;
-#pragma unroll
-      for (int jj = 0; jj < JH; ++jj) {
-        const int jc = h * JH + jj;
-        const float v = X[jj] * sx;
-        __half h1, l1, h2, l2;
-        int o1, o2;
-        if ((r & 1) == 0) {  // xr
-          split(v, h1, l1);
-          h2 = h1; l2 = l1;
-          o1 = boff<KU>(2 * jc, 2 * k);
-          o2 = boff<KU>(2 * jc + 1, 2 * k + 1);
-        } else {             // xi
-          split(-v, h1, l1);
-          split(v, h2, l2);
-          o1 = boff<KU>(2 * jc, 2 * k + 1);
-          o2 = boff<KU>(2 * jc + 1, 2 * k);
-        }
-        *reinterpret_cast<__half*>(aeh + o1) = h1;
-        *reinterpret_cast<__half*>(ael + o1) = l1;
-        *reinterpret_cast<__half*>(aeh + o2) = h2;
-        *reinterpret_cast<__half*>(ael + o2) = l2;
-      }
-    }
-    const float wscale = (float)(beta * kappa / ((double)sz * (double)sx));
-    const float fscale = (float)(kappa / ((double)sz * (double)sx));
-    __syncthreads();  // Gs / PB no longer needed; ring free for the W pass
-    for (int c = 0; c <= nch; ++c) {
-      if (c < nch) {
-        const int j = c & 1;
-        load_chunk<KU>(Hb, c * G::MA, zh[j], zl[j], sz, have_scale, flags, fred, pol_stream, range_bad);
-        fence_async_smem();
-        __syncthreads();
-        if (tid == 0) {
-          tc_after();
-          const uint32_t bh = su32(zh[j]), bl = su32(zl[j]), xh = su32(aeh), xl_ = su32(ael);
-          const uint32_t d0 = tmem + 256 * j;
-#pragma unroll
-          for (int s = 0; s < NC / 16; ++s) {
-            const uint64_t dzh = sdesc(bh + 256 * s, 128, G::CMA), dzl = sdesc(bl + 256 * s, 128, G::CMA);
-            const uint64_t dxh = sdesc(xh + 256 * s, 128, NC * 16), dxl = sdesc(xl_ + 256 * s, 128, NC * 16);
-            mma(d0, dzh, dxh, G::ID_W, s != 0);
-            mma(d0 + 128, dzh, dxl, G::ID_W, s != 0);
-            mma(d0 + 128, dzl, dxh, G::ID_W, 1);
-          }
-          commit(&bars[j]);
-        }
-        ++nring[j];
-      }
-      if (c >= 1) {  // epilogue of chunk c-1 (overlaps the MMAs of chunk c)
-        const int jp = (c - 1) & 1;
-        mbar_wait(&bars[jp], (nring[jp] - 1) & 1);
-        tc_after();
-        constexpr int HC = NC / 2;  // this thread: antenna row r, components [h*HC, h*HC+HC)
-        const int m = (c - 1) * G::MA + r;
-        float4* wrow = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.W + (b * (int64_t)p.M + m) * KU) + h * HC);
-        float4* frow = p.F ? reinterpret_cast<float4*>(reinterpret_cast<float*>(p.F + (b * (int64_t)p.M + m) * KU) + h * HC) : nullptr;
-        constexpr int CW = (HC % 16 == 0) ? 16 : 8;
-#pragma unroll
-        for (int c0 = 0; c0 < HC; c0 += CW) {
-          float a[16], x[16];
-          if constexpr (CW == 16) {
-            tmem_ld16(tl + 256 * jp + h * HC + c0, a);
-            tmem_ld16(tl + 256 * jp + 128 + h * HC + c0, x);
-          } else {
-            tmem_ld8(tl + 256 * jp + h * HC + c0, a);
-            tmem_ld8(tl + 256 * jp + 128 + h * HC + c0, x);
-          }
+        float d[32];
+        if (32 * q < NC) {
+          tmem_ld16(tl + (j ? G::T_W1 : G::T_W0) + 32 * h, d);
+          tmem_ld16(tl + (j ? G::T_W1 : G::T_W0) + 32 * h + 16, d + 16);
           tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < CW; i += 4) {
-            float d0 = a[i] + x[i] * (1.0f / 2048.0f), d1 = a[i + 1] + x[i + 1] * (1.0f / 2048.0f);
-            float d2 = a[i + 2] + x[i + 2] * (1.0f / 2048.0f), d3 = a[i + 3] + x[i + 3] * (1.0f / 2048.0f);
-            stg_hint(wrow + (c0 + i) / 4, make_float4(d0 * wscale, d1 * wscale, d2 * wscale, d3 * wscale), pol_stream);
-            if (frow) stg_hint(frow + (c0 + i) / 4, make_float4(d0 * fscale, d1 * fscale, d2 * fscale, d3 * fscale), pol_stream);
-          }
         }
         tc_before();
+        mbar_arrive(&sm->wfree[j]);
+        if (act_row) {
+          const int m0 = c * G::CH + 32 * h;
+#pragma unroll
+          for (int a = 0; a < 32; ++a) {
+            __stcs(Wb + (int64_t)(m0 + a) * NC + r, d[a] * wscale);
+            if (Fb) __stcs(Fb + (int64_t)(m0 + a) * NC + r, d[a] * fscale);
+          }
+        }
       }
     }
-    range_bad = __syncthreads_or(range_bad);
-    if (tid == 0 && range_bad) p.status[b] = XL_STATUS_RANGE;
   }
   __syncthreads();
   if (warp == 0) {
@@ -779,7 +793,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
 bool fused_supported(int dtype, int method, int M, int K) {
   if (dtype != XL_C64 || method == XL_DIRECT) return false;
   if (K != 16 && K != 32 && K != 64) return false;
-  return M >= 128 && M % 128 == 0;
+  return M >= 64 && M % 64 == 0;
 }
 
 size_t fused_ws_bytes(int, int, int64_t, int, int) { return 256; }
@@ -790,6 +804,7 @@ template <int KU>
 static int launch_k(const tc::Params& p, cudaStream_t st) {
   constexpr int smem = tc::Geo<KU>::SMEM;
   static_assert(smem <= 227 * 1024, "fused kernel smem");
+  static_assert(sizeof(tc::Small) <= 4096, "small region");
   cudaFuncSetAttribute(tc::fused_rzf_kernel<KU>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (g_num_sms == 0) {
     int dev = 0;
@@ -807,7 +822,8 @@ int launch_fused(int dtype, int method, int variant, const void* H, int64_t B, i
                  int32_t* status, void*, size_t, void* dbg_gram, cudaStream_t st) {
   (void)dtype;
   tc::Params p{(const float2*)H, B, M, xi, xi_per_batch, power, sigma2, T, method, variant,
-               (float2*)W, (float2*)F, beta, gamma, sum_se, (float2*)X, status, (float2*)dbg_gram};
+               (float2*)W, (float2*)F, beta, gamma, sum_se, (float2*)X, status, (float2*)dbg_gram, 0};
+  if (const char* e = getenv("XL_FUSED_DEBUG")) p.dbg = atoi(e);
   if (K == 64) return launch_k<64>(p, st);
   if (K == 32) return launch_k<32>(p, st);
   return launch_k<16>(p, st);
