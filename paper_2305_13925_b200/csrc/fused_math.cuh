@@ -1,0 +1,413 @@
+// Math-warp role of the fused tcgen05 precoder (included by fused_tc.cu).
+//
+// 8 warps = 2 per TMEM lane quadrant; thread (q, h, lane) owns component row
+// r = 32q + lane (interleaved re/im of user r/2) and the JH = K/2 right-hand
+// side columns of half h.  Register budget is the constraint (128 per
+// thread for 512-thread CTAs), so the PCG state lives where it is cheapest:
+//   P   (direction)      registers   (needed by every step)
+//   X   (iterate)        TMEM cols T_X   (updated once per iteration)
+//   R   (residual)       TMEM cols T_R
+//   Q = A P              TMEM cols T_Q   (tensor-core product)
+//   rz  (per column)     smem, double buffered by iteration parity
+// Column inner products are warp transpose-reductions + a fixed-order sum
+// over the 4 quadrant warps (deterministic).
+
+__device__ __forceinline__ void tmem_st8(uint32_t ta, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
+               "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+               "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+               "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+template <int KU>
+__device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* aeh, uint8_t* ael,
+                                          uint8_t* pbh, uint8_t* pbl, uint32_t tmem, int nch) {
+  using G = Geo<KU>;
+  constexpr int NC = G::NC, JH = G::JH, HC = G::HC;
+  static_assert(JH % 8 == 0 && HC % 16 == 0, "math tiling");
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int mw = warp - NCONV;
+  const int q = warp & 3, h = mw >> 2;  // TMEM lane quadrant = warp % 4
+  const int r = 32 * q + lane;          // component row / output component
+  const bool act_row = r < NC;
+  const bool quad_act = 32 * q < NC;    // warp-uniform (NC is a multiple of 32)
+  const bool odd = lane & 1;
+  const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+  const uint32_t tQ = tl + G::T_Q + h * JH, tX = tl + G::T_X + h * JH, tR = tl + G::T_R + h * JH;
+  const bool textbook = (p.method == XL_JACPCG && p.variant == XL_TEXTBOOK);
+  const bool use_c = (p.method == XL_JACPCG);
+  const int mt = tid - 32 * NCONV;  // 0..255
+  const uint32_t uah = su32(aeh), ual = su32(ael), ubh = su32(pbh), ubl = su32(pbl);
+  auto stamp = [&](uint32_t kk, int slot) {
+    if (p.trace && blockIdx.x == 0 && kk < 8 && mt == 0) p.trace[kk * 32 + slot] = clock64();
+  };
+  uint32_t k = 0, nq = 0, wc = 0;
+  uint32_t wuse[2] = {0, 0};
+  for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++k) {
+    const double alpha = p.xi_b ? p.xi_b[b] : p.xi;
+    mbar_wait(&sm->scale_ready, k & 1);
+    const float sz = sm->sz_slot[k & 1];
+    mbar_wait(&sm->gram_full, k & 1);
+    stamp(k, 0);
+    tc_after();
+    const float alpha_s = (float)(alpha * (double)sz * (double)sz);
+
+    // ---- (1) Re diag of A' = G[2k][2k] + G[2k+1][2k+1] (same order as below)
+    if (quad_act && h == (32 * q) / HC) {
+      float v[32];
+      tmem_ld16(tl + G::T_GRAM + 32 * q, v);
+      tmem_ld16(tl + G::T_GRAM + 32 * q + 16, v + 16);
+      tmem_wait_ld();
+      float dg = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) dg = (i == lane) ? v[i] : dg;
+      const float pd = __shfl_xor_sync(0xffffffffu, dg, 1);
+      if (!odd) sm->cdg[r >> 1] = dg + pd;
+    }
+    named_sync(BAR_MATH, NMT);
+    float dmax = 0.0f;
+    for (int kk = 0; kk < KU; ++kk) dmax = fmaxf(dmax, sm->cdg[kk] + alpha_s);
+    const bool range_bad = !isfinite(dmax);
+    const float sa = pow2_scale(dmax, 14);  // diag(A'') < 2^14
+    const float gd = act_row ? sm->cdg[r >> 1] : 0.0f;
+    const float cr = (act_row && use_c) ? (gd + alpha_s) * sa : 1.0f;
+    const float icr = 1.0f / cr;
+
+    // ---- (2) A'' split: row 2k = (ar, -ai), row 2k+1 = (ai, ar) per column pair
+    if (quad_act) {
+      const int kr = r >> 1;
+#pragma unroll 1
+      for (int c0 = 0; c0 < HC; c0 += 16) {
+        float v[16];
+        tmem_ld16(tl + G::T_GRAM + h * HC + c0, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int jp = 0; jp < 8; ++jp) {
+          const float g0 = v[2 * jp], g1 = v[2 * jp + 1];
+          const float p0 = __shfl_xor_sync(0xffffffffu, g0, 1), p1 = __shfl_xor_sync(0xffffffffu, g1, 1);
+          float ar = odd ? (p0 + g1) : (g0 + p1);
+          const float ai = odd ? (p1 - g0) : (g1 - p0);
+          const int jc = (h * HC + c0) / 2 + jp;
+          if (jc == kr) ar += alpha_s;
+          if (p.dbgA && !odd) {
+            const float inv = 1.0f / (sz * sz);
+            p.dbgA[(b * KU + kr) * KU + jc] = make_float2(ar * inv, ai * inv);
+          }
+          __half h0, l0, h1, l1;
+          split((odd ? ai : ar) * sa, h0, l0);
+          split((odd ? ar : -ai) * sa, h1, l1);
+          const int o = boff<KU>(r, 2 * jc);
+          *reinterpret_cast<uint32_t*>(aeh + o) = pack2(h0, h1);
+          *reinterpret_cast<uint32_t*>(ael + o) = pack2(l0, l1);
+        }
+      }
+    }
+    tc_before();
+    named_sync(BAR_MATH, NMT);  // every thread's Gram TMEM reads are complete
+    if (mt == 0) mbar_arrive(&sm->gram_free);  // the next Gram may accumulate
+    if (p.dbg == 1) {
+      if (mt == 0) p.status[b] = range_bad ? XL_STATUS_RANGE : 0;
+      continue;
+    }
+    stamp(k, 1);
+
+    // ---- (3) PCG (linsolve.py:217-294), K identity RHS, w0 = 0
+    float P[JH], A[JH];
+    {
+      float xz[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int c0 = 0; c0 < JH; c0 += 8) {
+        float rv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int jc = h * JH + c0 + i;
+          const float e = (act_row && r == 2 * jc) ? 1.0f : 0.0f;
+          rv[i] = (use_c && !textbook) ? e * icr : e;
+          P[c0 + i] = textbook ? e * icr : rv[i];
+        }
+        if (quad_act) {
+          tmem_st8(tX + c0, xz);
+          tmem_st8(tR + c0, rv);
+        }
+      }
+      if (mt < KU) {
+        const float c0 = use_c ? (sm->cdg[mt] + alpha_s) * sa : 1.0f;
+        const float ic = 1.0f / c0;
+        sm->rzs[0][mt] = textbook ? ic : (use_c ? ic * ic : 1.0f);
+      }
+      tmem_wait_st();
+    }
+    int not_hpd = 0;
+    for (int t = 1; t <= p.T; ++t) {
+      const int cur = (t - 1) & 1, nxt = t & 1;
+      float pm = 0.0f;
+#pragma unroll
+      for (int jj = 0; jj < JH; ++jj) pm = fmaxf(pm, fabsf(P[jj]));
+      const float sp = pow2_scale(math_max(pm, sm), 14);  // also orders rzs writes
+      if (t == 1) stamp(k, 5);
+      if (act_row) write_cols<KU>(P, sp, r, h, pbh, pbl);
+      fence_async_smem();
+      named_sync(BAR_MATH, NMT);
+      if (t == 1) stamp(k, 6);
+      if (mt == 0) issue_kxk<KU>(tmem + G::T_Q, uah, ual, ubh, ubl, &sm->q_full);
+      mbar_wait(&sm->q_full, nq & 1);
+      ++nq;
+      if (t == 1) stamp(k, 7);
+      tc_after();
+      const float isp = 1.0f / sp;
+      const float qs = (use_c && !textbook) ? isp * icr : isp;  // Algorithm 1: z = C^-1 P m
+      if (quad_act) {
+        tmem_ld<JH>(tQ, A);
+        tmem_wait_ld();
+      }
+#pragma unroll
+      for (int jj = 0; jj < JH; ++jj) A[jj] = act_row ? P[jj] * (A[jj] * qs) : 0.0f;
+      column_allreduce<JH>(A, sm, q, h);  // curvature m^H z per column
+      if (t == 1) stamp(k, 12);
+#pragma unroll
+      for (int jj = 0; jj < JH; ++jj) {
+        const float rzj = sm->rzs[cur][h * JH + jj];
+        const bool act = rzj > 0.0f;
+        if (A[jj] <= 0.0f && act) not_hpd = 1;  // linsolve.py:277-279
+        // fast division: the IEEE slow-path call would spill the live state
+        A[jj] = act ? __fdividef(rzj, A[jj] > 0.0f ? A[jj] : 1.0f) : 0.0f;  // alpha_j
+      }
+#pragma unroll
+      for (int c0 = 0; c0 < JH; c0 += 8) {
+        float qv[8], xv[8], rv[8];
+        if (quad_act) {
+          tmem_ld8(tQ + c0, qv);
+          tmem_ld8(tX + c0, xv);
+          tmem_ld8(tR + c0, rv);
+          tmem_wait_ld();
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float al = A[c0 + i];
+          xv[i] = xv[i] + al * P[c0 + i];
+          rv[i] = rv[i] - al * (qv[i] * qs);
+          const float z = textbook ? rv[i] * icr : rv[i];
+          A[c0 + i] = act_row ? rv[i] * z : 0.0f;  // new rz partial
+        }
+        if (quad_act) {
+          tmem_st8(tX + c0, xv);
+          tmem_st8(tR + c0, rv);
+        }
+      }
+      tmem_wait_st();
+      if (t == 1) stamp(k, 13);
+      column_allreduce<JH>(A, sm, q, h);  // new rz per column
+      if (t == 1) stamp(k, 14);
+#pragma unroll
+      for (int c0 = 0; c0 < JH; c0 += 8) {
+        float rv[8];
+        if (quad_act) {
+          tmem_ld8(tR + c0, rv);
+          tmem_wait_ld();
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float rzj = sm->rzs[cur][h * JH + c0 + i];
+          const float be = rzj > 0.0f ? __fdividef(A[c0 + i], rzj) : 0.0f;
+          const float z = textbook ? rv[i] * icr : rv[i];
+          P[c0 + i] = act_row ? z + be * P[c0 + i] : 0.0f;
+        }
+      }
+      if (q == 0 && lane == 0) {
+#pragma unroll
+        for (int jj = 0; jj < JH; ++jj) sm->rzs[nxt][h * JH + jj] = A[jj];
+      }
+      if (t == 1) stamp(k, 15);
+    }
+    tc_before();
+    stamp(k, 2);
+
+    // ---- (4) beta, coupling B = beta G X, SINR (precoder.py:64-70, metrics.py:47-58)
+    float xm = 0.0f;
+#pragma unroll
+    for (int c0 = 0; c0 < JH; c0 += 8) {
+      float xv[8];
+      if (quad_act) {
+        tmem_ld8(tX + c0, xv);
+        tmem_wait_ld();
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) xm = act_row ? fmaxf(xm, fabsf(xv[i])) : xm;
+    }
+    const float sx = pow2_scale(math_max(xm, sm), 14);
+    stamp(k, 19);
+    if (act_row && h == r / HC) {  // G'' = A'' - sa xi' I: only the diagonal changes
+      __half hh, ll;
+      split(gd * sa, hh, ll);
+      const int o = boff<KU>(r, r);
+      *reinterpret_cast<__half*>(aeh + o) = hh;
+      *reinterpret_cast<__half*>(ael + o) = ll;
+    }
+#pragma unroll
+    for (int c0 = 0; c0 < JH; c0 += 8) {
+      float xv[8];
+      if (quad_act) {
+        tmem_ld8(tX + c0, xv);
+        tmem_wait_ld();
+      }
+      if (act_row) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          __half hh, ll;
+          split(xv[i] * sx, hh, ll);
+          const int o = boff<KU>(h * JH + c0 + i, r);
+          *reinterpret_cast<__half*>(pbh + o) = hh;
+          *reinterpret_cast<__half*>(pbl + o) = ll;
+        }
+      }
+    }
+    fence_async_smem();
+    named_sync(BAR_MATH, NMT);
+    stamp(k, 20);
+    if (mt == 0) issue_kxk<KU>(tmem + G::T_Q, uah, ual, ubh, ubl, &sm->q_full);
+    mbar_wait(&sm->q_full, nq & 1);
+    ++nq;
+    stamp(k, 21);
+    tc_after();
+    float GX[JH];
+    if (quad_act) {
+      tmem_ld<JH>(tQ, GX);
+      tmem_wait_ld();
+    }
+    const float isx = 1.0f / sx;
+    // kappa = sa sz^2: X_true = kappa X'', G X_true = GX
+    const double kappa = (double)sa * (double)sz * (double)sz;
+    double part = 0.0;
+    float rs = 0.0f;
+#pragma unroll
+    for (int c0 = 0; c0 < JH; c0 += 8) {
+      float xv[8];
+      if (quad_act) {
+        tmem_ld8(tX + c0, xv);
+        tmem_wait_ld();
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float g = act_row ? GX[c0 + i] * isx : 0.0f;
+        GX[c0 + i] = g;
+        part += act_row ? (double)xv[i] * (double)g : 0.0;
+        rs += g * g;
+      }
+    }
+    const double fro2 = kappa * math_sum_d(part, sm);
+    stamp(k, 22);
+    double beta = 0.0;
+    int degenerate = 0;
+    if (fro2 > 0.0 && isfinite(fro2)) beta = sqrt(p.power / fro2);
+    else degenerate = 1;
+    if (act_row) {
+      sm->rsq[h * NC + r] = rs;
+#pragma unroll
+      for (int jj = 0; jj < JH; ++jj)
+        if (h * JH + jj == (r >> 1)) sm->dgq[r] = GX[jj];
+    }
+    named_sync(BAR_MATH, NMT);
+    if (mt < KU) {
+      const double b2 = beta * beta;
+      const double tot = b2 * ((double)sm->rsq[2 * mt] + (double)sm->rsq[NC + 2 * mt] +
+                               (double)sm->rsq[2 * mt + 1] + (double)sm->rsq[NC + 2 * mt + 1]);
+      const double sig = b2 * ((double)sm->dgq[2 * mt] * sm->dgq[2 * mt] +
+                                (double)sm->dgq[2 * mt + 1] * sm->dgq[2 * mt + 1]);
+      const double g = sig / ((tot - sig) + p.sigma2);
+      if (p.gamma) p.gamma[b * KU + mt] = g;
+      sm->sse[mt] = log2(1.0 + g);
+    }
+    const bool any_not_hpd = math_max(not_hpd ? 1.0f : 0.0f, sm) > 0.0f;  // also orders sse
+    stamp(k, 23);
+    if (mt == 0) {
+      double s = 0.0;
+      for (int kk = 0; kk < KU; ++kk) s += sm->sse[kk];
+      p.sum_se[b] = s;
+      p.beta[b] = beta;
+      int st = XL_STATUS_OK;
+      if (range_bad) st = XL_STATUS_RANGE;
+      else if (any_not_hpd) st = XL_STATUS_NOT_HPD;
+      else if (degenerate) st = XL_STATUS_DEGENERATE;
+      p.status[b] = st;
+    }
+
+    stamp(k, 28);
+    // ---- (5) X out (optional) and Xe = real embedding of X (A operand of
+    //      W^T = Xe^T Z^T): element (row c2, col c) = Xe[c][c2] with
+    //      Xe[2k][2j] = xr, Xe[2k+1][2j] = -xi, Xe[2k][2j+1] = xi, Xe[2k+1][2j+1] = xr
+    const int kr = r >> 1;
+#pragma unroll
+    for (int c0 = 0; c0 < JH; c0 += 8) {
+      float xv[8];
+      if (quad_act) {
+        tmem_ld8(tX + c0, xv);
+        tmem_wait_ld();
+      }
+      if (act_row) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int jc = h * JH + c0 + i;
+          if (p.X) reinterpret_cast<float*>(p.X)[((b * KU + kr) * KU + jc) * 2 + (r & 1)] = (float)(kappa * xv[i]);
+          const float v = xv[i] * sx;
+          __half h1, l1, h2, l2;
+          int o1, o2;
+          if (!odd) {  // xr
+            split(v, h1, l1);
+            h2 = h1;
+            l2 = l1;
+            o1 = boff<KU>(2 * jc, 2 * kr);
+            o2 = boff<KU>(2 * jc + 1, 2 * kr + 1);
+          } else {     // xi
+            split(-v, h1, l1);
+            split(v, h2, l2);
+            o1 = boff<KU>(2 * jc, 2 * kr + 1);
+            o2 = boff<KU>(2 * jc + 1, 2 * kr);
+          }
+          *reinterpret_cast<__half*>(aeh + o1) = h1;
+          *reinterpret_cast<__half*>(ael + o1) = l1;
+          *reinterpret_cast<__half*>(aeh + o2) = h2;
+          *reinterpret_cast<__half*>(ael + o2) = l2;
+        }
+      }
+    }
+    tc_before();
+    fence_async_smem();
+    named_sync(BAR_MATH, NMT);
+    if (mt == 0) mbar_arrive(&sm->xe_ready);
+    stamp(k, 3);
+
+    // ---- (6) W epilogue: lane row c2 = r, antennas [32h, 32h+32) of each chunk
+    const float wscale = (float)(beta * kappa / ((double)sz * (double)sx));
+    const float fscale = (float)(kappa / ((double)sz * (double)sx));
+    float* Wb = reinterpret_cast<float*>(p.W + b * (int64_t)p.M * KU);
+    float* Fb = p.F ? reinterpret_cast<float*>(p.F + b * (int64_t)p.M * KU) : nullptr;
+    for (int c = 0; c < (p.dbg ? 0 : nch); ++c, ++wc) {
+      const int j = wc & 1;
+      mbar_wait(&sm->wfull[j], wuse[j] & 1);
+      ++wuse[j];
+      tc_after();
+      float d[32];
+      if (quad_act) {
+        tmem_ld16(tl + (j ? G::T_W1 : G::T_W0) + 32 * h, d);
+        tmem_ld16(tl + (j ? G::T_W1 : G::T_W0) + 32 * h + 16, d + 16);
+        tmem_wait_ld();
+      }
+      tc_before();
+      mbar_arrive(&sm->wfree[j]);
+      if (act_row) {
+        const int64_t o0 = (int64_t)(c * G::CH + 32 * h) * NC + r;
+        float* wp = Wb + o0;
+#pragma unroll
+        for (int a = 0; a < 32; ++a) __stcs(wp + a * NC, d[a] * wscale);
+        if (Fb) {
+          float* fp = Fb + o0;
+#pragma unroll
+          for (int a = 0; a < 32; ++a) __stcs(fp + a * NC, d[a] * fscale);
+        }
+      }
+    }
+    stamp(k, 4);
+  }
+}

@@ -35,6 +35,7 @@
 #include <cuda_fp16.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "xl_common.cuh"
@@ -77,17 +78,19 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 // Wait for the phase with this parity to complete.  A bounded spin traps
 // instead of hanging the GPU if a pipeline accounting bug ever deadlocks.
+// try_wait carries a suspend-time hint so waiting warps sleep in hardware
+// instead of burning issue slots the converter / math warps need.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0, spins = 0;
   do {
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, P1;\n\t}\n"
         : "=r"(done)
-        : "r"(su32(bar)), "r"(parity)
+        : "r"(su32(bar)), "r"(parity), "r"(0x989680u)
         : "memory");
-    if (++spins > (1u << 28)) asm volatile("trap;");
+    if (++spins > (1u << 24)) asm volatile("trap;");
   } while (!done);
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
@@ -202,7 +205,7 @@ struct Geo {
   static constexpr int OFF_PB = OFF_AE + 2 * AEPART;
   static constexpr int PBPART = KU * NC * 2;
   static constexpr int OFF_SMALL = OFF_PB + 2 * PBPART;
-  static constexpr int SMEM = OFF_SMALL + 4096;
+  static constexpr int SMEM = OFF_SMALL + 8192;
   static constexpr int JH = KU / 2;          // PCG columns per math thread
   static constexpr int HC = NC / 2;          // Gram columns per math thread
   static constexpr int NB = NC / 8;          // converter float4 blocks per thread
@@ -210,7 +213,7 @@ struct Geo {
   static constexpr uint32_t ID_W = idesc(128, CH, 0, 0);
   static constexpr uint32_t ID_P = idesc(128, KU, 0, 0);
   // TMEM columns
-  static constexpr uint32_t T_GRAM = 0, T_Q = 128, T_W0 = 256, T_W1 = 320;
+  static constexpr uint32_t T_GRAM = 0, T_Q = 128, T_W0 = 256, T_W1 = 320, T_X = 384, T_R = 448;
 };
 
 struct Params {
@@ -230,6 +233,7 @@ struct Params {
   int32_t* status;
   float2* dbgA;  // optional [B][K][K] regularized Gram (tests)
   int dbg;       // bisection: 1 = Gram + A only, 2 = no W pass
+  long long* trace;  // optional per-phase clock64 stamps of CTA 0 (XL_FUSED_TRACE)
 };
 
 // Element (row n, col k) of an n x NC K-major operand tile (core rows = n).
@@ -240,7 +244,7 @@ __device__ __forceinline__ int boff(int n, int k) {
 
 struct Small {
   uint64_t raw_full[4], conv_full[4], stage_free[4];
-  uint64_t gram_full, q_full, xe_ready, scale_ready;
+  uint64_t gram_full, q_full, xe_ready, scale_ready, gram_free;
   uint64_t wfull[2], wfree[2];
   uint32_t tmem_slot;
   int pad0;
@@ -253,6 +257,7 @@ struct Small {
   float rsq[2 * 128];
   float dgq[128];
   double sse[64];
+  float rzs[2][64];
   int flags[4];
 };
 
@@ -323,6 +328,8 @@ __device__ __forceinline__ void issue_kxk(uint32_t tq, uint32_t ah, uint32_t al,
   commit(bar);
 }
 
+#include "fused_math.cuh"
+
 // ------------------------------------------------------------ kernel ----
 template <int KU>
 __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
@@ -349,6 +356,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
     mbar_init(&sm->q_full, 1);
     mbar_init(&sm->xe_ready, 1);
     mbar_init(&sm->scale_ready, 1);
+    mbar_init(&sm->gram_free, 1);
     for (int j = 0; j < 2; ++j) {
       mbar_init(&sm->wfull[j], 1);
       mbar_init(&sm->wfree[j], NMT);
@@ -364,6 +372,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
   tc_after();
   const uint32_t tmem = sm->tmem_slot;
 
+  // phase stamps (CTA 0, first 8 realizations) for pipeline analysis
+  auto stamp = [&](uint32_t kk, int slot) {
+    if (p.trace && blockIdx.x == 0 && kk < 8) p.trace[kk * 32 + slot] = clock64();
+  };
 #ifndef XL_REG_AUX
 #define XL_REG_AUX 56
 #define XL_REG_CONV 104
@@ -379,30 +391,47 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(XL_REG_MATH));
   }
 #endif
+  // Stream order of ring items (software pipeline across this CTA's
+  // realizations k = 0..nb-1):  G(0), then for every k: G(k+1), W(k).
+  // G(k+1) streams while the math warps run PCG(k); W(k) needs X(k).
+  const int64_t nb = p.B > (int64_t)blockIdx.x ? (p.B - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto for_items = [&](auto&& body) {  // body(kk, pass, b)
+    for (int64_t k = 0; k < nb; ++k)
+      for (int part = (k == 0 ? 0 : 1); part < 3; ++part) {
+        if (part == 1 && k + 1 >= nb) continue;
+        if (part == 2 && p.dbg) continue;
+        const int64_t kk = part == 1 ? k + 1 : k;
+        body((uint32_t)kk, part == 2 ? 1 : 0, (int64_t)blockIdx.x + kk * gridDim.x);
+      }
+  };
   if (warp == W_PROD) {
     // ------------------------------------------------------ producer ------
     if (lane == 0) {
       uint32_t i = 0;
-      for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
+      for_items([&](uint32_t kk, int pass, int64_t b) {
         const char* Hb = reinterpret_cast<const char*>(p.H + b * (int64_t)p.M * KU);
-        for (int pass = 0; pass < (p.dbg ? 1 : 2); ++pass)
-          for (int c = 0; c < nch; ++c, ++i) {
-            const int s = i % NS;
-            if (i >= (uint32_t)NS) mbar_wait(&sm->stage_free[s], ((i / NS) - 1) & 1);
-            mbar_expect_tx(&sm->raw_full[s], G::SB);
-            bulk_g2s(ring + s * G::SB, Hb + (int64_t)c * G::SB, G::SB, &sm->raw_full[s],
-                     pass == 0 ? HINT_EVICT_LAST : HINT_EVICT_FIRST);
-          }
-      }
+        for (int c = 0; c < nch; ++c, ++i) {
+          const int s = i % NS;
+          if (i >= (uint32_t)NS) mbar_wait(&sm->stage_free[s], ((i / NS) - 1) & 1);
+          mbar_expect_tx(&sm->raw_full[s], G::SB);
+          bulk_g2s(ring + s * G::SB, Hb + (int64_t)c * G::SB, G::SB, &sm->raw_full[s],
+                   pass == 0 ? HINT_EVICT_LAST : HINT_EVICT_FIRST);
+          if (c == 0 && pass == 0) stamp(kk, 16);
+          if (c == nch - 1) stamp(kk, 17 + pass);
+        }
+      });
     }
   } else if (warp < NCONV) {
     // ---------------------------------------------------- converters ------
     uint32_t i = 0;
-    for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
-      float sz = 1.0f;
-      int have = 0;
-      for (int pass = 0; pass < (p.dbg ? 1 : 2); ++pass)
-        for (int c = 0; c < nch; ++c, ++i) {
+    float sz_par[2] = {1.0f, 1.0f};
+    int have_par[2] = {0, 0};
+    for_items([&](uint32_t kc, int pass, int64_t) {
+      const int par = kc & 1;
+      if (pass == 0) { sz_par[par] = 1.0f; have_par[par] = 0; }
+      float sz = sz_par[par];
+      int have = have_par[par];
+      for (int c = 0; c < nch; ++c, ++i) {
           const int s = i % NS;
           uint8_t* st = ring + s * G::SB;
           mbar_wait(&sm->raw_full[s], (i / NS) & 1);
@@ -451,21 +480,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
           if (warp == 0 && lane == 0) {
             mbar_arrive(&sm->conv_full[s]);
             if (pass == 0 && c == nch - 1) {
-              sm->sz_slot[0] = sz;
+              sm->sz_slot[par] = sz;
               mbar_arrive(&sm->scale_ready);
             }
+            if (c == 0) stamp(kc, 24 + 2 * pass);
+            if (c == nch - 1) stamp(kc, 25 + 2 * pass);
           }
-        }
-    }
+      }
+      sz_par[par] = sz;
+      have_par[par] = have;
+    });
   } else if (warp == W_MMA) {
     // ------------------------------------------- streaming MMA issuer ------
     if (lane == 0) {
-      uint32_t i = 0, k = 0, wc = 0;
+      uint32_t i = 0, wc = 0;
       uint32_t wuse[2] = {0, 0};
-      for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++k) {
+      for_items([&](uint32_t k, int pass, int64_t) {
+       if (pass == 0) {
+        // the TMEM Gram accumulator is free once the math warps built A(k-1)
+        if (k >= 1) mbar_wait(&sm->gram_free, (k - 1) & 1);
         for (int c = 0; c < nch; ++c, ++i) {  // Gram
           const int s = i % NS;
           mbar_wait(&sm->conv_full[s], (i / NS) & 1);
+          if (c == 0) stamp(k, 8);
           tc_after();
           const uint32_t zh = su32(ring + s * G::SB), zl = zh + G::ZT;
 #pragma unroll
@@ -479,8 +516,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
           commit(&sm->stage_free[s]);
         }
         commit(&sm->gram_full);
-        if (p.dbg) continue;
+        stamp(k, 9);
+        return;
+       }
         mbar_wait(&sm->xe_ready, k & 1);
+        stamp(k, 10);
         for (int c = 0; c < nch; ++c, ++i, ++wc) {  // W^T = Xe^T Z^T
           const int s = i % NS;
           const int j = wc & 1;
@@ -502,284 +542,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
           commit(&sm->wfull[j]);
           ++wuse[j];
         }
-      }
+        stamp(k, 11);
+      });
     }
   } else if (warp < NCONV + NMATH) {
-    // ---------------------------------------------------------- math ------
-    const int mw = warp - NCONV;
-    const int q = warp & 3, h = mw >> 2;     // TMEM lane quadrant = warp % 4
-    const int r = 32 * q + lane;             // component row / output component
-    const bool act_row = r < NC;
-    const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
-    const bool textbook = (p.method == XL_JACPCG && p.variant == XL_TEXTBOOK);
-    const bool use_c = (p.method == XL_JACPCG);
-    uint32_t k = 0, nq = 0, wc = 0;
-    uint32_t wuse[2] = {0, 0};
-    for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++k) {
-      const double alpha = p.xi_b ? p.xi_b[b] : p.xi;
-      mbar_wait(&sm->scale_ready, k & 1);
-      const float sz = sm->sz_slot[0];
-      mbar_wait(&sm->gram_full, k & 1);
-      tc_after();
-      // ---- A'' = sa (G + xi' I) from TMEM rows 2k, 2k+1 (lane pairs)
-      const float alpha_s = (float)(alpha * (double)sz * (double)sz);
-      float gv[HC];
-      if (32 * q < NC) {
-        tmem_ld<HC>(tl + G::T_GRAM + h * HC, gv);
-        tmem_wait_ld();
-      } else {
-#pragma unroll
-        for (int i2 = 0; i2 < HC; ++i2) gv[i2] = 0.0f;
-      }
-      tc_before();
-      const bool odd = lane & 1;
-      // pairs (ar, ai) for the columns of this half; diag into cdg
-#pragma unroll
-      for (int jp = 0; jp < HC / 2; ++jp) {
-        const float g0 = gv[2 * jp], g1 = gv[2 * jp + 1];
-        const float p0 = __shfl_xor_sync(0xffffffffu, g0, 1), p1 = __shfl_xor_sync(0xffffffffu, g1, 1);
-        const float ar = odd ? (p0 + g1) : (g0 + p1);
-        const float ai = odd ? (p1 - g0) : (g1 - p0);
-        gv[2 * jp] = ar;
-        gv[2 * jp + 1] = ai;
-        const int jc = (h * HC) / 2 + jp;
-        if (act_row && !odd && jc == (r >> 1)) sm->cdg[jc] = ar;
-      }
-      named_sync(BAR_MATH, NMT);
-      float dmax = 0.0f;
-      for (int kk = 0; kk < KU; ++kk) dmax = fmaxf(dmax, sm->cdg[kk] + alpha_s);
-      const bool range_bad = !isfinite(dmax);
-      const float sa = pow2_scale(dmax, 14);
-      const float gd = act_row ? sm->cdg[r >> 1] : 0.0f;  // Re A'_kk without xi
-      const float cr = act_row ? (use_c ? (gd + alpha_s) * sa : 1.0f) : 1.0f;
-      if (act_row) {
-        const int kr = r >> 1;
-#pragma unroll
-        for (int jp = 0; jp < HC / 2; ++jp) {
-          const int jc = (h * HC) / 2 + jp;
-          float ar = gv[2 * jp], ai = gv[2 * jp + 1];
-          if (jc == kr) ar += alpha_s;
-          if (p.dbgA && !odd) {
-            const float inv = 1.0f / (sz * sz);
-            p.dbgA[(b * KU + kr) * KU + jc] = make_float2(ar * inv, ai * inv);
-          }
-          // row 2k: (ar, -ai); row 2k+1: (ai, ar)   at columns (2jc, 2jc+1)
-          const float e0 = (odd ? ai : ar) * sa, e1 = (odd ? ar : -ai) * sa;
-          __half h0, l0, h1, l1;
-          split(e0, h0, l0);
-          split(e1, h1, l1);
-          const int o = boff<KU>(r, 2 * jc);
-          *reinterpret_cast<uint32_t*>(aeh + o) = pack2(h0, h1);
-          *reinterpret_cast<uint32_t*>(ael + o) = pack2(l0, l1);
-        }
-      }
-      if (p.dbg == 1) {
-        named_sync(BAR_MATH, NMT);
-        if (tid == 32 * NCONV) p.status[b] = range_bad ? XL_STATUS_RANGE : 0;
-        continue;
-      }
-      // ---- PCG state
-      float X[JH], R[JH], P[JH], rz[JH];
-#pragma unroll
-      for (int jj = 0; jj < JH; ++jj) {
-        const int jc = h * JH + jj;
-        const float e = (act_row && r == 2 * jc) ? 1.0f : 0.0f;
-        const float c0 = use_c ? (sm->cdg[jc] + alpha_s) * sa : 1.0f;
-        X[jj] = 0.0f;
-        if (textbook) {
-          R[jj] = e;
-          P[jj] = e / cr;
-          rz[jj] = 1.0f / c0;
-        } else {
-          R[jj] = use_c ? e / cr : e;
-          P[jj] = R[jj];
-          rz[jj] = use_c ? (1.0f / c0) * (1.0f / c0) : 1.0f;
-        }
-      }
-      int not_hpd = 0;
-      const uint32_t uah = su32(aeh), ual = su32(ael), ubh = su32(pbh), ubl = su32(pbl);
-      for (int t = 1; t <= p.T; ++t) {
-        float pm = 0.0f;
-#pragma unroll
-        for (int jj = 0; jj < JH; ++jj) pm = fmaxf(pm, fabsf(P[jj]));
-        const float sp = pow2_scale(math_max(pm, sm), 14);
-        if (act_row) write_cols<KU>(P, sp, r, h, pbh, pbl);
-        fence_async_smem();
-        named_sync(BAR_MATH, NMT);
-        if (mw == 0 && lane == 0) issue_kxk<KU>(tmem + G::T_Q, uah, ual, ubh, ubl, &sm->q_full);
-        mbar_wait(&sm->q_full, nq & 1);
-        ++nq;
-        tc_after();
-        float Q[JH], cv[JH];
-        tmem_ld<JH>(tl + G::T_Q + h * JH, Q);
-        tmem_wait_ld();
-        tc_before();
-        const float isp = 1.0f / sp;
-#pragma unroll
-        for (int jj = 0; jj < JH; ++jj) {
-          Q[jj] = act_row ? Q[jj] * isp : 0.0f;
-          if (!textbook && use_c) Q[jj] = Q[jj] / cr;  // Algorithm 1: z = C^-1 P m
-          cv[jj] = P[jj] * Q[jj];
-        }
-        column_allreduce<JH>(cv, sm, q, h);  // curvature per column
-        float rn[JH];
-#pragma unroll
-        for (int jj = 0; jj < JH; ++jj) {
-          const bool act = rz[jj] > 0.0f;
-          if (cv[jj] <= 0.0f && act) not_hpd = 1;  // linsolve.py:277-279
-          const float al = act ? rz[jj] / (cv[jj] > 0.0f ? cv[jj] : 1.0f) : 0.0f;
-          X[jj] = X[jj] + al * P[jj];
-          R[jj] = R[jj] - al * Q[jj];
-          const float z = textbook ? R[jj] / cr : R[jj];
-          rn[jj] = R[jj] * z;
-        }
-        column_allreduce<JH>(rn, sm, q, h);  // new rz per column
-#pragma unroll
-        for (int jj = 0; jj < JH; ++jj) {
-          const bool act = rz[jj] > 0.0f;
-          const float be = act ? rn[jj] / rz[jj] : 0.0f;
-          const float z = textbook ? R[jj] / cr : R[jj];
-          P[jj] = z + be * P[jj];
-          rz[jj] = rn[jj];
-        }
-      }
-      // ---- beta / coupling: Q = G'' X'' with G'' = A'' - sa xi' I (diag only)
-      float xm = 0.0f;
-#pragma unroll
-      for (int jj = 0; jj < JH; ++jj) xm = fmaxf(xm, fabsf(X[jj]));
-      const float sx = pow2_scale(math_max(xm, sm), 14);
-      if (act_row && h == ((r >> 1) * 2) / HC) {  // owner of diagonal element (r, r)
-        __half hh, ll;
-        split(gd * sa, hh, ll);
-        const int o = boff<KU>(r, r);
-        *reinterpret_cast<__half*>(aeh + o) = hh;
-        *reinterpret_cast<__half*>(ael + o) = ll;
-      }
-      if (act_row) write_cols<KU>(X, sx, r, h, pbh, pbl);
-      fence_async_smem();
-      named_sync(BAR_MATH, NMT);
-      if (mw == 0 && lane == 0) issue_kxk<KU>(tmem + G::T_Q, uah, ual, ubh, ubl, &sm->q_full);
-      mbar_wait(&sm->q_full, nq & 1);
-      ++nq;
-      tc_after();
-      float GX[JH];
-      tmem_ld<JH>(tl + G::T_Q + h * JH, GX);
-      tmem_wait_ld();
-      tc_before();
-      const float isx = 1.0f / sx;
-#pragma unroll
-      for (int jj = 0; jj < JH; ++jj) GX[jj] = act_row ? GX[jj] * isx : 0.0f;
-      // kappa = sa sz^2: X_true = kappa X'', G X_true = GX
-      const double kappa = (double)sa * (double)sz * (double)sz;
-      double part = 0.0;
-#pragma unroll
-      for (int jj = 0; jj < JH; ++jj) part += (double)X[jj] * (double)GX[jj];
-      const double fro2 = kappa * math_sum_d(part, sm);
-      double beta = 0.0;
-      int degenerate = 0;
-      if (fro2 > 0.0 && isfinite(fro2)) beta = sqrt(p.power / fro2);
-      else degenerate = 1;
-      {
-        float rs = 0.0f;
-#pragma unroll
-        for (int jj = 0; jj < JH; ++jj) rs += GX[jj] * GX[jj];
-        if (act_row) {
-          sm->rsq[h * NC + r] = rs;
-#pragma unroll
-          for (int jj = 0; jj < JH; ++jj)
-            if (h * JH + jj == (r >> 1)) sm->dgq[r] = GX[jj];
-        }
-      }
-      named_sync(BAR_MATH, NMT);
-      const int mt = tid - 32 * NCONV;  // 0..255
-      if (mt < KU) {
-        const double b2 = beta * beta;
-        const double tot = b2 * ((double)sm->rsq[2 * mt] + (double)sm->rsq[NC + 2 * mt] +
-                                 (double)sm->rsq[2 * mt + 1] + (double)sm->rsq[NC + 2 * mt + 1]);
-        const double sig = b2 * ((double)sm->dgq[2 * mt] * sm->dgq[2 * mt] +
-                                  (double)sm->dgq[2 * mt + 1] * sm->dgq[2 * mt + 1]);
-        const double g = sig / ((tot - sig) + p.sigma2);
-        if (p.gamma) p.gamma[b * KU + mt] = g;
-        sm->sse[mt] = log2(1.0 + g);
-      }
-      const bool any_not_hpd = math_max(not_hpd ? 1.0f : 0.0f, sm) > 0.0f;  // also orders sse
-      if (mt == 0) {
-        double s = 0.0;
-        for (int kk = 0; kk < KU; ++kk) s += sm->sse[kk];
-        p.sum_se[b] = s;
-        p.beta[b] = beta;
-        int st = XL_STATUS_OK;
-        if (range_bad) st = XL_STATUS_RANGE;
-        else if (any_not_hpd) st = XL_STATUS_NOT_HPD;
-        else if (degenerate) st = XL_STATUS_DEGENERATE;
-        p.status[b] = st;
-      }
-      if (p.X && act_row) {
-#pragma unroll
-        for (int jj = 0; jj < JH; ++jj) {
-          const int jc = h * JH + jj;
-          reinterpret_cast<float*>(p.X)[((b * KU + (r >> 1)) * KU + jc) * 2 + (r & 1)] = (float)(kappa * X[jj]);
-        }
-      }
-      // ---- Xe (A operand of W^T = Xe^T Z^T): element (row c2, col c) = Xe[c][c2]
-      //      Xe[2k][2j] = xr, Xe[2k+1][2j] = -xi, Xe[2k][2j+1] = xi, Xe[2k+1][2j+1] = xr
-      if (act_row) {
-        const int kr = r >> 1;
-#pragma unroll
-        for (int jj = 0; jj < JH; ++jj) {
-          const int jc = h * JH + jj;
-          const float v = X[jj] * sx;
-          __half h1, l1, h2, l2;
-          int o1, o2;
-          if (!(r & 1)) {  // xr
-            split(v, h1, l1);
-            h2 = h1;
-            l2 = l1;
-            o1 = boff<KU>(2 * jc, 2 * kr);
-            o2 = boff<KU>(2 * jc + 1, 2 * kr + 1);
-          } else {         // xi
-            split(-v, h1, l1);
-            split(v, h2, l2);
-            o1 = boff<KU>(2 * jc, 2 * kr + 1);
-            o2 = boff<KU>(2 * jc + 1, 2 * kr);
-          }
-          *reinterpret_cast<__half*>(aeh + o1) = h1;
-          *reinterpret_cast<__half*>(ael + o1) = l1;
-          *reinterpret_cast<__half*>(aeh + o2) = h2;
-          *reinterpret_cast<__half*>(ael + o2) = l2;
-        }
-      }
-      fence_async_smem();
-      named_sync(BAR_MATH, NMT);
-      if (mt == 0) mbar_arrive(&sm->xe_ready);
-      // ---- W epilogue: lane row c2 = r, antennas [32h, 32h+32) of each chunk
-      const float wscale = (float)(beta * kappa / ((double)sz * (double)sx));
-      const float fscale = (float)(kappa / ((double)sz * (double)sx));
-      float* Wb = reinterpret_cast<float*>(p.W + b * (int64_t)p.M * KU);
-      float* Fb = p.F ? reinterpret_cast<float*>(p.F + b * (int64_t)p.M * KU) : nullptr;
-      for (int c = 0; c < (p.dbg ? 0 : nch); ++c, ++wc) {
-        const int j = wc & 1;
-        mbar_wait(&sm->wfull[j], wuse[j] & 1);
-        ++wuse[j];
-        tc_after();
-        float d[32];
-        if (32 * q < NC) {
-          tmem_ld16(tl + (j ? G::T_W1 : G::T_W0) + 32 * h, d);
-          tmem_ld16(tl + (j ? G::T_W1 : G::T_W0) + 32 * h + 16, d + 16);
-          tmem_wait_ld();
-        }
-        tc_before();
-        mbar_arrive(&sm->wfree[j]);
-        if (act_row) {
-          const int m0 = c * G::CH + 32 * h;
-#pragma unroll
-          for (int a = 0; a < 32; ++a) {
-            __stcs(Wb + (int64_t)(m0 + a) * NC + r, d[a] * wscale);
-            if (Fb) __stcs(Fb + (int64_t)(m0 + a) * NC + r, d[a] * fscale);
-          }
-        }
-      }
-    }
+    math_role<KU>(p, sm, aeh, ael, pbh, pbl, tmem, nch);
   }
   __syncthreads();
   if (warp == 0) {
@@ -804,7 +571,7 @@ template <int KU>
 static int launch_k(const tc::Params& p, cudaStream_t st) {
   constexpr int smem = tc::Geo<KU>::SMEM;
   static_assert(smem <= 227 * 1024, "fused kernel smem");
-  static_assert(sizeof(tc::Small) <= 4096, "small region");
+  static_assert(sizeof(tc::Small) <= 8192, "small region");
   cudaFuncSetAttribute(tc::fused_rzf_kernel<KU>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (g_num_sms == 0) {
     int dev = 0;
@@ -822,11 +589,35 @@ int launch_fused(int dtype, int method, int variant, const void* H, int64_t B, i
                  int32_t* status, void*, size_t, void* dbg_gram, cudaStream_t st) {
   (void)dtype;
   tc::Params p{(const float2*)H, B, M, xi, xi_per_batch, power, sigma2, T, method, variant,
-               (float2*)W, (float2*)F, beta, gamma, sum_se, (float2*)X, status, (float2*)dbg_gram, 0};
+               (float2*)W, (float2*)F, beta, gamma, sum_se, (float2*)X, status, (float2*)dbg_gram, 0,
+               nullptr};
   if (const char* e = getenv("XL_FUSED_DEBUG")) p.dbg = atoi(e);
-  if (K == 64) return launch_k<64>(p, st);
-  if (K == 32) return launch_k<32>(p, st);
-  return launch_k<16>(p, st);
+  // XL_FUSED_TRACE=1: synchronous per-phase clock64 dump of CTA 0 to stderr
+  // (development aid; never set in production runs).
+  static long long* trace = nullptr;
+  const bool tracing = getenv("XL_FUSED_TRACE") != nullptr;
+  if (tracing) {
+    if (!trace) cudaMalloc(&trace, 8 * 32 * sizeof(long long));
+    cudaMemsetAsync(trace, 0, 8 * 32 * sizeof(long long), st);
+    p.trace = trace;
+  }
+  int rc = K == 64 ? launch_k<64>(p, st) : K == 32 ? launch_k<32>(p, st) : launch_k<16>(p, st);
+  if (tracing && rc == XL_SUCCESS) {
+    long long h[8 * 32];
+    cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    const long long t0 = h[16];
+    static const char* names[32] = {"math:gram_full", "math:A_built", "math:pcg_done", "math:xe_ready",
+                                    "math:w_epi_done", "pcg1:sp", "pcg1:mma_issue", "pcg1:q_ready", "mma:gram_start", "mma:gram_full",
+                                    "mma:xe_wait_done", "mma:w_last", "pcg1:curv", "pcg1:upd", "pcg1:rz", "pcg1:P", "prod:first", "prod:G_last",
+                                    "prod:W_last", "beta:sx", "beta:issue", "beta:gx", "beta:fro2",
+                                    "conv:G_first", "conv:G_last", "conv:W_first", "conv:W_last",
+                                    "beta:gamma", 0, 0, 0};
+    for (int kk = 0; kk < 8; ++kk)
+      for (int s = 0; s < 32; ++s)
+        if (names[s] && h[kk * 32 + s]) fprintf(stderr, "trace b%d %-18s %10lld\n", kk, names[s], h[kk * 32 + s] - t0);
+  }
+  return rc;
 }
 
 }  // namespace xl
