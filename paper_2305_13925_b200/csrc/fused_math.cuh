@@ -2,15 +2,15 @@
 //
 // 8 warps = 2 per TMEM lane quadrant; thread (q, h, lane) owns component row
 // r = 32q + lane (interleaved re/im of user r/2) and the JH = K/2 right-hand
-// side columns of half h.  Register budget is the constraint (128 per
-// thread for 512-thread CTAs), so the PCG state lives where it is cheapest:
+// side columns of half h.  With 128 registers per thread the PCG state lives
+// where it is cheapest:
 //   P   (direction)      registers   (needed by every step)
-//   X   (iterate)        TMEM cols T_X   (updated once per iteration)
+//   X   (iterate)        TMEM cols T_X
 //   R   (residual)       TMEM cols T_R
 //   Q = A P              TMEM cols T_Q   (tensor-core product)
-//   rz  (per column)     smem, double buffered by iteration parity
-// Column inner products are warp transpose-reductions + a fixed-order sum
-// over the 4 quadrant warps (deterministic).
+// Per-column scalars (curvature, rz, alpha, beta) are finalised once per
+// column by 64 threads from warp transpose-reduction partials summed over the
+// 4 quadrant warps in a fixed order (deterministic), then broadcast via smem.
 
 __device__ __forceinline__ void tmem_st8(uint32_t ta, const float* v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
@@ -34,6 +34,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
   const bool act_row = r < NC;
   const bool quad_act = 32 * q < NC;    // warp-uniform (NC is a multiple of 32)
   const bool odd = lane & 1;
+  const int kr = r >> 1;
   const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
   const uint32_t tQ = tl + G::T_Q + h * JH, tX = tl + G::T_X + h * JH, tR = tl + G::T_R + h * JH;
   const bool textbook = (p.method == XL_JACPCG && p.variant == XL_TEXTBOOK);
@@ -43,7 +44,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
   auto stamp = [&](uint32_t kk, int slot) {
     if (p.trace && blockIdx.x == 0 && kk < 8 && mt == 0) p.trace[kk * 32 + slot] = clock64();
   };
-  uint32_t k = 0, nq = 0, wc = 0;
+  uint32_t k = 0, nq = 0, wc = 0, par = 0;
   uint32_t wuse[2] = {0, 0};
   for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++k) {
     const double alpha = p.xi_b ? p.xi_b[b] : p.xi;
@@ -64,20 +65,19 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
 #pragma unroll
       for (int i = 0; i < 32; ++i) dg = (i == lane) ? v[i] : dg;
       const float pd = __shfl_xor_sync(0xffffffffu, dg, 1);
-      if (!odd) sm->cdg[r >> 1] = dg + pd;
+      if (!odd) sm->cdg[kr] = dg + pd;
     }
     named_sync(BAR_MATH, NMT);
     float dmax = 0.0f;
     for (int kk = 0; kk < KU; ++kk) dmax = fmaxf(dmax, sm->cdg[kk] + alpha_s);
     const bool range_bad = !isfinite(dmax);
     const float sa = pow2_scale(dmax, 14);  // diag(A'') < 2^14
-    const float gd = act_row ? sm->cdg[r >> 1] : 0.0f;
+    const float gd = act_row ? sm->cdg[kr] : 0.0f;
     const float cr = (act_row && use_c) ? (gd + alpha_s) * sa : 1.0f;
     const float icr = 1.0f / cr;
 
     // ---- (2) A'' split: row 2k = (ar, -ai), row 2k+1 = (ai, ar) per column pair
     if (quad_act) {
-      const int kr = r >> 1;
 #pragma unroll 1
       for (int c0 = 0; c0 < HC; c0 += 16) {
         float v[16];
@@ -132,21 +132,28 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
           tmem_st8(tR + c0, rv);
         }
       }
-      if (mt < KU) {
+      if (mt < KU) {  // rz_j = r_j^H z_j of the unit residual (linsolve.py:268)
         const float c0 = use_c ? (sm->cdg[mt] + alpha_s) * sa : 1.0f;
         const float ic = 1.0f / c0;
-        sm->rzs[0][mt] = textbook ? ic : (use_c ? ic * ic : 1.0f);
+        sm->rzs[mt] = textbook ? ic : (use_c ? ic * ic : 1.0f);
       }
       tmem_wait_st();
     }
     int not_hpd = 0;
-    for (int t = 1; t <= p.T; ++t) {
-      const int cur = (t - 1) & 1, nxt = t & 1;
+    for (int t = 1; t <= p.T; ++t, par ^= 1) {
+      // (a) power-of-two scale of P for the fp16 split (one barrier: parity buffers)
       float pm = 0.0f;
 #pragma unroll
       for (int jj = 0; jj < JH; ++jj) pm = fmaxf(pm, fabsf(P[jj]));
-      const float sp = pow2_scale(math_max(pm, sm), 14);  // also orders rzs writes
+      pm = warp_max(pm);
+      if (lane == 0) sm->mred2[par][mw] = pm;
+      named_sync(BAR_MATH, NMT);
+      float pmax = sm->mred2[par][0];
+#pragma unroll
+      for (int w = 1; w < NMATH; ++w) pmax = fmaxf(pmax, sm->mred2[par][w]);
+      const float sp = pow2_scale(pmax, 14);
       if (t == 1) stamp(k, 5);
+      // (b) Q = A'' P on the tensor core
       if (act_row) write_cols<KU>(P, sp, r, h, pbh, pbl);
       fence_async_smem();
       named_sync(BAR_MATH, NMT);
@@ -162,18 +169,21 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
         tmem_ld<JH>(tQ, A);
         tmem_wait_ld();
       }
+      // (c) curvature m^H z per column
 #pragma unroll
       for (int jj = 0; jj < JH; ++jj) A[jj] = act_row ? P[jj] * (A[jj] * qs) : 0.0f;
-      column_allreduce<JH>(A, sm, q, h);  // curvature m^H z per column
-      if (t == 1) stamp(k, 12);
-#pragma unroll
-      for (int jj = 0; jj < JH; ++jj) {
-        const float rzj = sm->rzs[cur][h * JH + jj];
+      column_partials<JH>(A, sm->red, q, h);
+      named_sync(BAR_MATH, NMT);
+      if (mt < KU) {  // (d) alpha_j, NotHpd (linsolve.py:276-280)
+        const float curv = column_total<JH>(sm->red, mt);
+        const float rzj = sm->rzs[mt];
         const bool act = rzj > 0.0f;
-        if (A[jj] <= 0.0f && act) not_hpd = 1;  // linsolve.py:277-279
-        // fast division: the IEEE slow-path call would spill the live state
-        A[jj] = act ? __fdividef(rzj, A[jj] > 0.0f ? A[jj] : 1.0f) : 0.0f;  // alpha_j
+        if (curv <= 0.0f && act) not_hpd = 1;
+        sm->coef[0][mt] = act ? rzj / (curv > 0.0f ? curv : 1.0f) : 0.0f;
       }
+      named_sync(BAR_MATH, NMT);
+      if (t == 1) stamp(k, 12);
+      // (e) w += alpha m, r -= alpha Pm, rz partials (linsolve.py:281-284)
 #pragma unroll
       for (int c0 = 0; c0 < JH; c0 += 8) {
         float qv[8], xv[8], rv[8];
@@ -185,21 +195,30 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float al = A[c0 + i];
+          const float al = sm->coef[0][h * JH + c0 + i];
           xv[i] = xv[i] + al * P[c0 + i];
           rv[i] = rv[i] - al * (qv[i] * qs);
           const float z = textbook ? rv[i] * icr : rv[i];
-          A[c0 + i] = act_row ? rv[i] * z : 0.0f;  // new rz partial
+          A[c0 + i] = act_row ? rv[i] * z : 0.0f;
         }
         if (quad_act) {
           tmem_st8(tX + c0, xv);
           tmem_st8(tR + c0, rv);
         }
       }
+      column_partials<JH>(A, sm->red2, q, h);
       tmem_wait_st();
       if (t == 1) stamp(k, 13);
-      column_allreduce<JH>(A, sm, q, h);  // new rz per column
+      named_sync(BAR_MATH, NMT);
+      if (mt < KU) {  // (f) beta_j, rz update (linsolve.py:284-288)
+        const float rn = column_total<JH>(sm->red2, mt);
+        const float rzj = sm->rzs[mt];
+        sm->coef[1][mt] = rzj > 0.0f ? rn / rzj : 0.0f;
+        sm->rzs[mt] = rn;
+      }
+      named_sync(BAR_MATH, NMT);
       if (t == 1) stamp(k, 14);
+      // (g) m = z + beta m
 #pragma unroll
       for (int c0 = 0; c0 < JH; c0 += 8) {
         float rv[8];
@@ -209,15 +228,10 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float rzj = sm->rzs[cur][h * JH + c0 + i];
-          const float be = rzj > 0.0f ? __fdividef(A[c0 + i], rzj) : 0.0f;
+          const float be = sm->coef[1][h * JH + c0 + i];
           const float z = textbook ? rv[i] * icr : rv[i];
           P[c0 + i] = act_row ? z + be * P[c0 + i] : 0.0f;
         }
-      }
-      if (q == 0 && lane == 0) {
-#pragma unroll
-        for (int jj = 0; jj < JH; ++jj) sm->rzs[nxt][h * JH + jj] = A[jj];
       }
       if (t == 1) stamp(k, 15);
     }
@@ -306,9 +320,9 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
       sm->rsq[h * NC + r] = rs;
 #pragma unroll
       for (int jj = 0; jj < JH; ++jj)
-        if (h * JH + jj == (r >> 1)) sm->dgq[r] = GX[jj];
+        if (h * JH + jj == kr) sm->dgq[r] = GX[jj];
     }
-    named_sync(BAR_MATH, NMT);
+    const bool any_not_hpd = math_max(not_hpd ? 1.0f : 0.0f, sm) > 0.0f;  // also orders rsq/dgq
     if (mt < KU) {
       const double b2 = beta * beta;
       const double tot = b2 * ((double)sm->rsq[2 * mt] + (double)sm->rsq[NC + 2 * mt] +
@@ -317,11 +331,46 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
                                 (double)sm->dgq[2 * mt + 1] * sm->dgq[2 * mt + 1]);
       const double g = sig / ((tot - sig) + p.sigma2);
       if (p.gamma) p.gamma[b * KU + mt] = g;
+      // per-user SE in double (a 64-thread step; |error| << the 1e-4 bound)
       sm->sse[mt] = log2(1.0 + g);
     }
-    const bool any_not_hpd = math_max(not_hpd ? 1.0f : 0.0f, sm) > 0.0f;  // also orders sse
     stamp(k, 23);
+
+    // ---- (5) X out (optional) and Xe = real embedding of X as the A operand of
+    //      W^T = Xe^T Z^T: row c2 = 2j: (xr, -xi), row 2j+1: (xi, xr) at cols (2k, 2k+1)
+#pragma unroll
+    for (int c0 = 0; c0 < JH; c0 += 8) {
+      float xv[8];
+      if (quad_act) {
+        tmem_ld8(tX + c0, xv);
+        tmem_wait_ld();
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float v = xv[i] * sx;
+        const float pv = __shfl_xor_sync(0xffffffffu, v, 1);  // partner: xi for even, xr for odd
+        const int jc = h * JH + c0 + i;
+        if (act_row) {
+          if (p.X) reinterpret_cast<float*>(p.X)[((b * KU + kr) * KU + jc) * 2 + (r & 1)] = (float)(kappa * xv[i]);
+          __half h0, l0, h1, l1;
+          if (!odd) {  // v = xr, pv = xi: row 2jc = (xr, -xi)
+            split(v, h0, l0);
+            split(-pv, h1, l1);
+          } else {     // v = xi, pv = xr: row 2jc + 1 = (xi, xr)
+            split(v, h0, l0);
+            split(pv, h1, l1);
+          }
+          const int o = boff<KU>(2 * jc + (odd ? 1 : 0), 2 * kr);
+          *reinterpret_cast<uint32_t*>(aeh + o) = pack2(h0, h1);
+          *reinterpret_cast<uint32_t*>(ael + o) = pack2(l0, l1);
+        }
+      }
+    }
+    tc_before();
+    fence_async_smem();
+    named_sync(BAR_MATH, NMT);
     if (mt == 0) {
+      mbar_arrive(&sm->xe_ready);
       double s = 0.0;
       for (int kk = 0; kk < KU; ++kk) s += sm->sse[kk];
       p.sum_se[b] = s;
@@ -332,50 +381,6 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
       else if (degenerate) st = XL_STATUS_DEGENERATE;
       p.status[b] = st;
     }
-
-    stamp(k, 28);
-    // ---- (5) X out (optional) and Xe = real embedding of X (A operand of
-    //      W^T = Xe^T Z^T): element (row c2, col c) = Xe[c][c2] with
-    //      Xe[2k][2j] = xr, Xe[2k+1][2j] = -xi, Xe[2k][2j+1] = xi, Xe[2k+1][2j+1] = xr
-    const int kr = r >> 1;
-#pragma unroll
-    for (int c0 = 0; c0 < JH; c0 += 8) {
-      float xv[8];
-      if (quad_act) {
-        tmem_ld8(tX + c0, xv);
-        tmem_wait_ld();
-      }
-      if (act_row) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int jc = h * JH + c0 + i;
-          if (p.X) reinterpret_cast<float*>(p.X)[((b * KU + kr) * KU + jc) * 2 + (r & 1)] = (float)(kappa * xv[i]);
-          const float v = xv[i] * sx;
-          __half h1, l1, h2, l2;
-          int o1, o2;
-          if (!odd) {  // xr
-            split(v, h1, l1);
-            h2 = h1;
-            l2 = l1;
-            o1 = boff<KU>(2 * jc, 2 * kr);
-            o2 = boff<KU>(2 * jc + 1, 2 * kr + 1);
-          } else {     // xi
-            split(-v, h1, l1);
-            split(v, h2, l2);
-            o1 = boff<KU>(2 * jc, 2 * kr + 1);
-            o2 = boff<KU>(2 * jc + 1, 2 * kr);
-          }
-          *reinterpret_cast<__half*>(aeh + o1) = h1;
-          *reinterpret_cast<__half*>(ael + o1) = l1;
-          *reinterpret_cast<__half*>(aeh + o2) = h2;
-          *reinterpret_cast<__half*>(ael + o2) = l2;
-        }
-      }
-    }
-    tc_before();
-    fence_async_smem();
-    named_sync(BAR_MATH, NMT);
-    if (mt == 0) mbar_arrive(&sm->xe_ready);
     stamp(k, 3);
 
     // ---- (6) W epilogue: lane row c2 = r, antennas [32h, 32h+32) of each chunk

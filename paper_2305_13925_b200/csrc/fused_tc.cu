@@ -201,9 +201,14 @@ struct Geo {
   static constexpr int ZT = SB / 2;          // one fp16 tile
   static constexpr int CMA = NC * 16;        // antenna-group (core row group) stride
   static constexpr int OFF_AE = NS * SB + 2048;   // + slack for M-padded Gram reads
-  static constexpr int AEPART = 128 * NC * 2;     // A operand padded to 128 rows
+  // Math-written operand tiles (A'', G'', Xe, P / X columns) use padded core
+  // strides so per-row / per-column register stores are bank-conflict free:
+  // K-direction core stride LBOP = 144 B, 8-row group stride SBOP = 32 mod 128.
+  static constexpr int LBOP = 144;
+  static constexpr int SBOP = (NC / 8) * LBOP + 32;
+  static constexpr int AEPART = 16 * SBOP;        // A operand padded to 128 rows
   static constexpr int OFF_PB = OFF_AE + 2 * AEPART;
-  static constexpr int PBPART = KU * NC * 2;
+  static constexpr int PBPART = (KU / 8) * SBOP;
   static constexpr int OFF_SMALL = OFF_PB + 2 * PBPART;
   static constexpr int SMEM = OFF_SMALL + 8192;
   static constexpr int JH = KU / 2;          // PCG columns per math thread
@@ -236,10 +241,15 @@ struct Params {
   long long* trace;  // optional per-phase clock64 stamps of CTA 0 (XL_FUSED_TRACE)
 };
 
-// Element (row n, col k) of an n x NC K-major operand tile (core rows = n).
+// Element (row n, col k) of a padded n x NC K-major operand tile (core rows = n).
 template <int KU>
 __device__ __forceinline__ int boff(int n, int k) {
-  return (n >> 3) * (Geo<KU>::NC * 16) + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2;
+  return (n >> 3) * Geo<KU>::SBOP + (k >> 3) * Geo<KU>::LBOP + (n & 7) * 16 + (k & 7) * 2;
+}
+// smem descriptor of K-step s of a padded tile
+template <int KU>
+__device__ __forceinline__ uint64_t pdesc(uint32_t base, int s) {
+  return sdesc(base + 2 * s * Geo<KU>::LBOP, Geo<KU>::LBOP, Geo<KU>::SBOP);
 }
 
 struct Small {
@@ -257,7 +267,10 @@ struct Small {
   float rsq[2 * 128];
   float dgq[128];
   double sse[64];
-  float rzs[2][64];
+  float rzs[64];        // rz per column (owned by the finalising threads)
+  float coef[2][64];    // broadcast per-column alpha / beta
+  float mred2[2][8];    // per-iteration P max, parity buffered
+  float red2[8 * 32];
   int flags[4];
 };
 
@@ -283,17 +296,20 @@ __device__ __forceinline__ double math_sum_d(double v, Small* sm) {
   named_sync(BAR_MATH, NMT);
   return s;
 }
+// Column sums of per-thread partials: each warp transpose-reduces its 32
+// rows, lanes < JH publish one partial per column into red[quadrant][h][j].
+// The caller finalises (fixed quadrant order) after a math barrier.
 template <int JH>
-__device__ __forceinline__ void column_allreduce(float (&v)[JH], Small* sm, int q, int h) {
+__device__ __forceinline__ void column_partials(float (&v)[JH], float* red, int q, int h) {
   const int lane = threadIdx.x & 31;
   float t = warp_transpose_reduce<JH>(v);
-  if (lane < JH) sm->red[(q * 2 + h) * JH + lane] = t;
-  named_sync(BAR_MATH, NMT);
-#pragma unroll
-  for (int jj = 0; jj < JH; ++jj)
-    v[jj] = ((sm->red[(0 * 2 + h) * JH + jj] + sm->red[(1 * 2 + h) * JH + jj]) + sm->red[(2 * 2 + h) * JH + jj]) +
-            sm->red[(3 * 2 + h) * JH + jj];
-  named_sync(BAR_MATH, NMT);
+  if (lane < JH) red[(q * 2 + h) * JH + lane] = t;
+}
+template <int JH>
+__device__ __forceinline__ float column_total(const float* red, int j) {
+  const int h = j / JH, jj = j % JH;
+  return ((red[(0 * 2 + h) * JH + jj] + red[(1 * 2 + h) * JH + jj]) + red[(2 * 2 + h) * JH + jj]) +
+         red[(3 * 2 + h) * JH + jj];
 }
 
 // Write the JH columns of this thread's component row r of an NC x KU
@@ -319,8 +335,8 @@ __device__ __forceinline__ void issue_kxk(uint32_t tq, uint32_t ah, uint32_t al,
   tc_after();
 #pragma unroll
   for (int s = 0; s < G::NC / 16; ++s) {
-    const uint64_t dah = sdesc(ah + 256 * s, 128, G::NC * 16), dal = sdesc(al + 256 * s, 128, G::NC * 16);
-    const uint64_t dbh = sdesc(bh + 256 * s, 128, G::NC * 16), dbl = sdesc(bl + 256 * s, 128, G::NC * 16);
+    const uint64_t dah = pdesc<KU>(ah, s), dal = pdesc<KU>(al, s);
+    const uint64_t dbh = pdesc<KU>(bh, s), dbl = pdesc<KU>(bl, s);
     mma(tq, dah, dbh, G::ID_P, s != 0);
     mma(tq, dah, dbl, G::ID_P, 1);
     mma(tq, dal, dbh, G::ID_P, 1);
@@ -532,7 +548,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
           const uint32_t d = tmem + (j ? G::T_W1 : G::T_W0);
 #pragma unroll
           for (int ks = 0; ks < NC / 16; ++ks) {
-            const uint64_t dxh = sdesc(xh + 256 * ks, 128, NC * 16), dxl = sdesc(xl_ + 256 * ks, 128, NC * 16);
+            const uint64_t dxh = pdesc<KU>(xh, ks), dxl = pdesc<KU>(xl_, ks);
             const uint64_t dzh = sdesc(zh + 256 * ks, 128, G::CMA), dzl = sdesc(zl + 256 * ks, 128, G::CMA);
             mma(d, dxh, dzh, G::ID_W, ks != 0);
             mma(d, dxh, dzl, G::ID_W, 1);
