@@ -105,8 +105,12 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
       }
     }
     tc_before();
+    fence_async_smem();
     named_sync(BAR_MATH, NMT);  // every thread's Gram TMEM reads are complete
-    if (mt == 0) mbar_arrive(&sm->gram_free);  // the next Gram may accumulate
+    if (mt == 0) {
+      mbar_arrive(&sm->gram_free);  // the next Gram may accumulate
+      cp_A<KU>(tmem + G::T_XE, uah, ual);  // A'' -> TMEM (A operand of the PCG products)
+    }
     if (p.dbg == 1) {
       if (mt == 0) p.status[b] = range_bad ? XL_STATUS_RANGE : 0;
       continue;
@@ -158,7 +162,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
       fence_async_smem();
       named_sync(BAR_MATH, NMT);
       if (t == 1) stamp(k, 6);
-      if (mt == 0) issue_kxk<KU>(tmem + G::T_Q, uah, ual, ubh, ubl, &sm->q_full);
+      if (mt == 0) issue_kxk<KU>(tmem + G::T_Q, tmem + G::T_XE, ubh, ubl, &sm->q_full);
       mbar_wait(&sm->q_full, nq & 1);
       ++nq;
       if (t == 1) stamp(k, 7);
@@ -280,7 +284,10 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
     fence_async_smem();
     named_sync(BAR_MATH, NMT);
     stamp(k, 20);
-    if (mt == 0) issue_kxk<KU>(tmem + G::T_Q, uah, ual, ubh, ubl, &sm->q_full);
+    if (mt == 0) {
+      cp_A<KU>(tmem + G::T_XE, uah, ual);  // G'' (diagonal rewritten) -> TMEM
+      issue_kxk<KU>(tmem + G::T_Q, tmem + G::T_XE, ubh, ubl, &sm->q_full);
+    }
     mbar_wait(&sm->q_full, nq & 1);
     ++nq;
     stamp(k, 21);
@@ -388,28 +395,28 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
     const float fscale = (float)(kappa / ((double)sz * (double)sx));
     float* Wb = reinterpret_cast<float*>(p.W + b * (int64_t)p.M * KU);
     float* Fb = p.F ? reinterpret_cast<float*>(p.F + b * (int64_t)p.M * KU) : nullptr;
-    for (int c = 0; c < (p.dbg ? 0 : nch); ++c, ++wc) {
-      const int j = wc & 1;
+    for (int c = 0; c < ((p.dbg == 1 || p.dbg == 2) ? 0 : nch); ++c, ++wc) {
+      const int j = wc % G::NWB;
       mbar_wait(&sm->wfull[j], wuse[j] & 1);
       ++wuse[j];
       tc_after();
-      float d[32];
+      constexpr int WH = G::WH;
+      float d[WH];
       if (quad_act) {
-        tmem_ld16(tl + (j ? G::T_W1 : G::T_W0) + 32 * h, d);
-        tmem_ld16(tl + (j ? G::T_W1 : G::T_W0) + 32 * h + 16, d + 16);
+        tmem_ld<WH>(tl + (j ? G::T_W1 : G::T_W0) + WH * h, d);
         tmem_wait_ld();
       }
       tc_before();
       mbar_arrive(&sm->wfree[j]);
       if (act_row) {
-        const int64_t o0 = (int64_t)(c * G::CH + 32 * h) * NC + r;
+        const int64_t o0 = (int64_t)(c * G::CH + WH * h) * NC + r;
         float* wp = Wb + o0;
 #pragma unroll
-        for (int a = 0; a < 32; ++a) __stcs(wp + a * NC, d[a] * wscale);
+        for (int a = 0; a < WH; ++a) __stcs(wp + a * NC, d[a] * wscale);
         if (Fb) {
           float* fp = Fb + o0;
 #pragma unroll
-          for (int a = 0; a < 32; ++a) __stcs(fp + a * NC, d[a] * fscale);
+          for (int a = 0; a < WH; ++a) __stcs(fp + a * NC, d[a] * fscale);
         }
       }
     }

@@ -63,6 +63,17 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(id), "r"(acc));
 }
+// A operand from TMEM (K-major), B from smem.
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
+}
+// smem (K-major operand k-step: 128 rows x 16 fp16) -> TMEM 128 lanes x 8 columns
+__device__ __forceinline__ void tmem_cp(uint32_t taddr, uint64_t desc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(desc));
+}
 __device__ __forceinline__ void commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
                : "memory");
@@ -190,13 +201,23 @@ constexpr int NCONV = 4, NMATH = 8;
 constexpr int W_MMA = NCONV + NMATH, W_PROD = W_MMA + 1;
 constexpr int NTHREADS = 512;  // 16 warps = 4 warpgroups (setmaxnreg granularity)
 constexpr int BAR_CONV = 1, BAR_MATH = 2;
+// Converter warps: 0..3 plus the two spare warps of warpgroup 3 (14, 15).
+#ifndef XL_NCW
+#define XL_NCW 6
+#endif
+constexpr int NCW = XL_NCW;
+__device__ __forceinline__ bool is_converter(int w) { return w < NCONV || (NCW > NCONV && w >= 16 - (NCW - NCONV)); }
+__device__ __forceinline__ int conv_index(int w) { return w < NCONV ? w : NCONV + (w - (16 - (NCW - NCONV))); }
 constexpr int NMT = 32 * NMATH;               // math threads
 
 template <int KU>
 struct Geo {
   static constexpr int NC = 2 * KU;          // real components (interleaved re/im)
-  static constexpr int CH = 64;              // antennas per ring stage
-  static constexpr int NS = 3;               // ring depth
+#ifndef XL_CH
+#define XL_CH 64
+#endif
+  static constexpr int CH = XL_CH;           // antennas per ring stage
+  static constexpr int NS = (3 * 64) / CH;   // ring depth (96 KB ring for K = 64)
   static constexpr int SB = CH * NC * 4;     // stage bytes (raw fp32 == hi + lo fp16 tiles)
   static constexpr int ZT = SB / 2;          // one fp16 tile
   static constexpr int CMA = NC * 16;        // antenna-group (core row group) stride
@@ -213,12 +234,19 @@ struct Geo {
   static constexpr int SMEM = OFF_SMALL + 8192;
   static constexpr int JH = KU / 2;          // PCG columns per math thread
   static constexpr int HC = NC / 2;          // Gram columns per math thread
-  static constexpr int NB = NC / 8;          // converter float4 blocks per thread
+  static constexpr int NB = (CH / 4) * (NC / 32) / NCONV;  // converter float4 blocks per thread
+  static constexpr int WH = CH / 2;          // W epilogue antennas per math thread
   static constexpr uint32_t ID_GRAM = idesc(128, NC, 1, 1);
   static constexpr uint32_t ID_W = idesc(128, CH, 0, 0);
   static constexpr uint32_t ID_P = idesc(128, KU, 0, 0);
   // TMEM columns
-  static constexpr uint32_t T_GRAM = 0, T_Q = 128, T_W0 = 256, T_W1 = 320, T_X = 384, T_R = 448;
+  // TMEM columns.  T_XE holds the A operand of the K x K products (A'' / G'')
+  // and then of W^T (Xe), hi at T_XE and lo at T_XE + 64, copied in from smem
+  // by tcgen05.cp so the MMAs re-read only their B operand from smem.
+  static constexpr int NWB = (CH <= 32) ? 2 : 1;  // W accumulator buffers
+  static_assert(NWB * CH <= 64, "W accumulator columns");
+  static constexpr uint32_t T_GRAM = 0, T_Q = 128, T_W0 = 192, T_W1 = 192 + CH * (NWB - 1), T_X = 256,
+                            T_R = 320, T_XE = 384;
 };
 
 struct Params {
@@ -239,6 +267,7 @@ struct Params {
   float2* dbgA;  // optional [B][K][K] regularized Gram (tests)
   int dbg;       // bisection: 1 = Gram + A only, 2 = no W pass
   long long* trace;  // optional per-phase clock64 stamps of CTA 0 (XL_FUSED_TRACE)
+  int keep16;        // sixteenths of each realization's H kept L2-resident (evict_last)
 };
 
 // Element (row n, col k) of a padded n x NC K-major operand tile (core rows = n).
@@ -253,13 +282,13 @@ __device__ __forceinline__ uint64_t pdesc(uint32_t base, int s) {
 }
 
 struct Small {
-  uint64_t raw_full[4], conv_full[4], stage_free[4];
+  uint64_t raw_full[12], conv_full[12], stage_free[12];
   uint64_t gram_full, q_full, xe_ready, scale_ready, gram_free;
   uint64_t wfull[2], wfree[2];
   uint32_t tmem_slot;
   int pad0;
   float sz_slot[2];
-  float conv_red[4];
+  float conv_red[8];
   float mred[8];
   double dred[8];
   float cdg[64];        // Re diag of A' (no xi) per user
@@ -327,19 +356,30 @@ __device__ __forceinline__ void write_cols(const float* v, float s, int r, int h
   }
 }
 
-// K x K tensor-core product Q = A'' * Bop (3xFP16), issued by one thread.
+// Copy the padded K-major 128 x NC split operand (hi, lo) from smem into TMEM
+// columns [t, t + NC/2) and [t + 64, t + 64 + NC/2).  Ordered before later
+// tcgen05.mma of the same thread.
 template <int KU>
-__device__ __forceinline__ void issue_kxk(uint32_t tq, uint32_t ah, uint32_t al, uint32_t bh, uint32_t bl,
-                                          uint64_t* bar) {
+__device__ __forceinline__ void cp_A(uint32_t t, uint32_t ah, uint32_t al) {
+  tc_after();
+#pragma unroll
+  for (int s = 0; s < Geo<KU>::NC / 16; ++s) {
+    tmem_cp(t + 8 * s, pdesc<KU>(ah, s));
+    tmem_cp(t + 64 + 8 * s, pdesc<KU>(al, s));
+  }
+}
+
+// K x K tensor-core product Q = A'' * Bop (3xFP16) with A'' in TMEM, issued by one thread.
+template <int KU>
+__device__ __forceinline__ void issue_kxk(uint32_t tq, uint32_t ta, uint32_t bh, uint32_t bl, uint64_t* bar) {
   using G = Geo<KU>;
   tc_after();
 #pragma unroll
   for (int s = 0; s < G::NC / 16; ++s) {
-    const uint64_t dah = pdesc<KU>(ah, s), dal = pdesc<KU>(al, s);
     const uint64_t dbh = pdesc<KU>(bh, s), dbl = pdesc<KU>(bl, s);
-    mma(tq, dah, dbh, G::ID_P, s != 0);
-    mma(tq, dah, dbl, G::ID_P, 1);
-    mma(tq, dal, dbh, G::ID_P, 1);
+    mma_ts(tq, ta + 8 * s, dbh, G::ID_P, s != 0);
+    mma_ts(tq, ta + 8 * s, dbl, G::ID_P, 1);
+    mma_ts(tq, ta + 64 + 8 * s, dbh, G::ID_P, 1);
   }
   commit(bar);
 }
@@ -389,6 +429,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
   const uint32_t tmem = sm->tmem_slot;
 
   // phase stamps (CTA 0, first 8 realizations) for pipeline analysis
+  // per ring item i in [64, 128): 0 = load issued, 1 = raw landed, 2 = converted, 3 = MMAs issued
+  auto item_stamp = [&](uint32_t ii, int slot) {
+    if (p.trace && blockIdx.x == 0 && ii >= 64 && ii < 128) p.trace[256 + (ii - 64) * 4 + slot] = clock64();
+  };
   auto stamp = [&](uint32_t kk, int slot) {
     if (p.trace && blockIdx.x == 0 && kk < 8) p.trace[kk * 32 + slot] = clock64();
   };
@@ -415,7 +459,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
     for (int64_t k = 0; k < nb; ++k)
       for (int part = (k == 0 ? 0 : 1); part < 3; ++part) {
         if (part == 1 && k + 1 >= nb) continue;
-        if (part == 2 && p.dbg) continue;
+        if (part == 2 && (p.dbg == 1 || p.dbg == 2)) continue;
         const int64_t kk = part == 1 ? k + 1 : k;
         body((uint32_t)kk, part == 2 ? 1 : 0, (int64_t)blockIdx.x + kk * gridDim.x);
       }
@@ -424,21 +468,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
     // ------------------------------------------------------ producer ------
     if (lane == 0) {
       uint32_t i = 0;
+      const int keep_num = p.keep16;
       for_items([&](uint32_t kk, int pass, int64_t b) {
         const char* Hb = reinterpret_cast<const char*>(p.H + b * (int64_t)p.M * KU);
         for (int c = 0; c < nch; ++c, ++i) {
           const int s = i % NS;
           if (i >= (uint32_t)NS) mbar_wait(&sm->stage_free[s], ((i / NS) - 1) & 1);
+          item_stamp(i, 0);
           mbar_expect_tx(&sm->raw_full[s], G::SB);
+          // Two realizations per SM are in flight (Gram of k+1 overlaps PCG of
+          // k), which is more than L2 holds for all 148 SMs; keep only the
+          // first keep_num/16 of each realization's chunks L2-resident for
+          // the W re-read and stream the rest.
+          const bool keep = pass == 0 && c * 16 < nch * keep_num;
           bulk_g2s(ring + s * G::SB, Hb + (int64_t)c * G::SB, G::SB, &sm->raw_full[s],
-                   pass == 0 ? HINT_EVICT_LAST : HINT_EVICT_FIRST);
+                   keep ? HINT_EVICT_LAST : HINT_EVICT_FIRST);
           if (c == 0 && pass == 0) stamp(kk, 16);
           if (c == nch - 1) stamp(kk, 17 + pass);
         }
       });
     }
-  } else if (warp < NCONV) {
+  } else if (is_converter(warp)) {
     // ---------------------------------------------------- converters ------
+    const int cw = conv_index(warp);
     uint32_t i = 0;
     float sz_par[2] = {1.0f, 1.0f};
     int have_par[2] = {0, 0};
@@ -451,25 +503,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
           const int s = i % NS;
           uint8_t* st = ring + s * G::SB;
           mbar_wait(&sm->raw_full[s], (i / NS) & 1);
-          float4 v[G::NB];
+          if (warp == 0 && lane == 0) item_stamp(i, 1);
+          // blocks of 4 antennas x 32 components, round-robin over converter warps
+          constexpr int NBLK = (G::CH / 4) * (NC / 32), NBM = (NBLK + NCW - 1) / NCW;
+          float4 v[NBM];
 #pragma unroll
-          for (int k = 0; k < G::NB; ++k) {
-            const int blk = warp * G::NB + k;               // 4 antennas x 32 components
+          for (int k = 0; k < NBM; ++k) {
+            const int blk = cw + k * NCW;
             const int rb = blk / (NC / 32), cs = blk % (NC / 32);
             const int m = 4 * rb + (lane >> 3), cc = 32 * cs + 4 * (lane & 7);
-            v[k] = *reinterpret_cast<const float4*>(st + (m * NC + cc) * 4);
+            if (blk < NBLK) v[k] = *reinterpret_cast<const float4*>(st + (m * NC + cc) * 4);
+            else v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
           }
-          named_sync(BAR_CONV, 32 * NCONV);  // all raw reads done before in-place writes
+          named_sync(BAR_CONV, 32 * NCW);  // all raw reads done before in-place writes
           if (pass == 0 && !have) {
             float mx = 0.0f;
 #pragma unroll
-            for (int k = 0; k < G::NB; ++k)
+            for (int k = 0; k < NBM; ++k)
               mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[k].x), fabsf(v[k].y)), fmaxf(fabsf(v[k].z), fabsf(v[k].w))));
             mx = warp_max(mx);
-            if (lane == 0) sm->conv_red[warp] = mx;
-            named_sync(BAR_CONV, 32 * NCONV);
-            mx = fmaxf(fmaxf(sm->conv_red[0], sm->conv_red[1]), fmaxf(sm->conv_red[2], sm->conv_red[3]));
-            named_sync(BAR_CONV, 32 * NCONV);
+            if (lane == 0) sm->conv_red[cw] = mx;
+            named_sync(BAR_CONV, 32 * NCW);
+            mx = sm->conv_red[0];
+#pragma unroll
+            for (int w = 1; w < NCW; ++w) mx = fmaxf(mx, sm->conv_red[w]);
+            named_sync(BAR_CONV, 32 * NCW);
             if (mx > 0.0f) {
               sz = pow2_scale(mx, 11);  // first nonzero chunk: max |Z'| in [2^10, 2^11)
               have = 1;
@@ -477,8 +535,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
           }
           const float2 s2 = make_float2(sz, sz);
 #pragma unroll
-          for (int k = 0; k < G::NB; ++k) {
-            const int blk = warp * G::NB + k;
+          for (int k = 0; k < NBM; ++k) {
+            const int blk = cw + k * NCW;
+            if (blk >= NBLK || p.dbg == 3) continue;  // dbg 3: timing without conversion
             const int rb = blk / (NC / 32), cs = blk % (NC / 32);
             const int m = 4 * rb + (lane >> 3), cc = 32 * cs + 4 * (lane & 7);
             const float2 a = __fmul2_rn(make_float2(v[k].x, v[k].y), s2);
@@ -492,9 +551,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
             *reinterpret_cast<uint2*>(st + G::ZT + off) = make_uint2(h2u(la), h2u(lb));
           }
           fence_async_smem();
-          named_sync(BAR_CONV, 32 * NCONV);
+          named_sync(BAR_CONV, 32 * NCW);
           if (warp == 0 && lane == 0) {
             mbar_arrive(&sm->conv_full[s]);
+            item_stamp(i, 2);
             if (pass == 0 && c == nch - 1) {
               sm->sz_slot[par] = sz;
               mbar_arrive(&sm->scale_ready);
@@ -530,6 +590,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
             mma(tmem + G::T_GRAM, dl, dh, G::ID_GRAM, 1);
           }
           commit(&sm->stage_free[s]);
+          item_stamp(i, 3);
         }
         commit(&sm->gram_full);
         stamp(k, 9);
@@ -537,26 +598,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
        }
         mbar_wait(&sm->xe_ready, k & 1);
         stamp(k, 10);
+        cp_A<KU>(tmem + G::T_XE, su32(aeh), su32(ael));  // Xe -> TMEM (A operand)
         for (int c = 0; c < nch; ++c, ++i, ++wc) {  // W^T = Xe^T Z^T
           const int s = i % NS;
-          const int j = wc & 1;
+          const int j = wc % G::NWB;
           if (wuse[j] >= 1) mbar_wait(&sm->wfree[j], (wuse[j] - 1) & 1);
           mbar_wait(&sm->conv_full[s], (i / NS) & 1);
           tc_after();
           const uint32_t zh = su32(ring + s * G::SB), zl = zh + G::ZT;
-          const uint32_t xh = su32(aeh), xl_ = su32(ael);
           const uint32_t d = tmem + (j ? G::T_W1 : G::T_W0);
+          const uint32_t txe = tmem + G::T_XE;
 #pragma unroll
           for (int ks = 0; ks < NC / 16; ++ks) {
-            const uint64_t dxh = pdesc<KU>(xh, ks), dxl = pdesc<KU>(xl_, ks);
             const uint64_t dzh = sdesc(zh + 256 * ks, 128, G::CMA), dzl = sdesc(zl + 256 * ks, 128, G::CMA);
-            mma(d, dxh, dzh, G::ID_W, ks != 0);
-            mma(d, dxh, dzl, G::ID_W, 1);
-            mma(d, dxl, dzh, G::ID_W, 1);
+            mma_ts(d, txe + 8 * ks, dzh, G::ID_W, ks != 0);
+            mma_ts(d, txe + 8 * ks, dzl, G::ID_W, 1);
+            mma_ts(d, txe + 64 + 8 * ks, dzh, G::ID_W, 1);
           }
           commit(&sm->stage_free[s]);
           commit(&sm->wfull[j]);
           ++wuse[j];
+          item_stamp(i, 3);
         }
         stamp(k, 11);
       });
@@ -606,32 +668,39 @@ int launch_fused(int dtype, int method, int variant, const void* H, int64_t B, i
   (void)dtype;
   tc::Params p{(const float2*)H, B, M, xi, xi_per_batch, power, sigma2, T, method, variant,
                (float2*)W, (float2*)F, beta, gamma, sum_se, (float2*)X, status, (float2*)dbg_gram, 0,
-               nullptr};
+               nullptr, 8};
   if (const char* e = getenv("XL_FUSED_DEBUG")) p.dbg = atoi(e);
+  if (const char* e = getenv("XL_FUSED_KEEP16")) p.keep16 = atoi(e);
   // XL_FUSED_TRACE=1: synchronous per-phase clock64 dump of CTA 0 to stderr
   // (development aid; never set in production runs).
   static long long* trace = nullptr;
   const bool tracing = getenv("XL_FUSED_TRACE") != nullptr;
   if (tracing) {
-    if (!trace) cudaMalloc(&trace, 8 * 32 * sizeof(long long));
-    cudaMemsetAsync(trace, 0, 8 * 32 * sizeof(long long), st);
+    if (!trace) cudaMalloc(&trace, 512 * sizeof(long long));
+    cudaMemsetAsync(trace, 0, 512 * sizeof(long long), st);
     p.trace = trace;
   }
   int rc = K == 64 ? launch_k<64>(p, st) : K == 32 ? launch_k<32>(p, st) : launch_k<16>(p, st);
   if (tracing && rc == XL_SUCCESS) {
-    long long h[8 * 32];
+    long long h[512];
     cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     const long long t0 = h[16];
     static const char* names[32] = {"math:gram_full", "math:A_built", "math:pcg_done", "math:xe_ready",
-                                    "math:w_epi_done", "pcg1:sp", "pcg1:mma_issue", "pcg1:q_ready", "mma:gram_start", "mma:gram_full",
-                                    "mma:xe_wait_done", "mma:w_last", "pcg1:curv", "pcg1:upd", "pcg1:rz", "pcg1:P", "prod:first", "prod:G_last",
-                                    "prod:W_last", "beta:sx", "beta:issue", "beta:gx", "beta:fro2",
+                                    "math:w_epi_done", "pcg1:sp", "pcg1:mma_issue", "pcg1:q_ready",
+                                    "mma:gram_start", "mma:gram_full", "mma:xe_wait_done", "mma:w_last",
+                                    "pcg1:curv", "pcg1:upd", "pcg1:rz", "pcg1:P",
+                                    "prod:first", "prod:G_last", "prod:W_last", "beta:sx",
+                                    "beta:issue", "beta:gx", "beta:fro2", "beta:gamma",
                                     "conv:G_first", "conv:G_last", "conv:W_first", "conv:W_last",
-                                    "beta:gamma", 0, 0, 0};
+                                    0, 0, 0, 0};
     for (int kk = 0; kk < 8; ++kk)
       for (int s = 0; s < 32; ++s)
         if (names[s] && h[kk * 32 + s]) fprintf(stderr, "trace b%d %-18s %10lld\n", kk, names[s], h[kk * 32 + s] - t0);
+    for (int ii = 0; ii < 64; ++ii)
+      if (h[256 + ii * 4])
+        fprintf(stderr, "item %3d issue %9lld landed %9lld converted %9lld mma %9lld\n", ii + 64,
+                h[256 + ii * 4] - t0, h[256 + ii * 4 + 1] - t0, h[256 + ii * 4 + 2] - t0, h[256 + ii * 4 + 3] - t0);
   }
   return rc;
 }
