@@ -77,6 +77,8 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
     const float icr = 1.0f / cr;
 
     // ---- (2) A'' split: row 2k = (ar, -ai), row 2k+1 = (ai, ar) per column pair
+    // (the smem operand region held Xe(k-1) until the W pass copied it to TMEM)
+    if (k >= 1) mbar_wait(&sm->xe_consumed, (k - 1) & 1);
     if (quad_act) {
 #pragma unroll 1
       for (int c0 = 0; c0 < HC; c0 += 16) {
@@ -107,10 +109,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
     tc_before();
     fence_async_smem();
     named_sync(BAR_MATH, NMT);  // every thread's Gram TMEM reads are complete
-    if (mt == 0) {
-      mbar_arrive(&sm->gram_free);  // the next Gram may accumulate
-      cp_A<KU>(tmem + G::T_XE, uah, ual);  // A'' -> TMEM (A operand of the PCG products)
-    }
+    if (mt == 0) mbar_arrive(&sm->gram_free);  // the next Gram may accumulate
     if (p.dbg == 1) {
       if (mt == 0) p.status[b] = range_bad ? XL_STATUS_RANGE : 0;
       continue;
@@ -162,7 +161,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
       fence_async_smem();
       named_sync(BAR_MATH, NMT);
       if (t == 1) stamp(k, 6);
-      if (mt == 0) issue_kxk<KU>(tmem + G::T_Q, tmem + G::T_XE, ubh, ubl, &sm->q_full);
+      if (mt == 0) issue_kxk<KU>(tmem + G::T_Q, uah, ual, ubh, ubl, &sm->q_full);
       mbar_wait(&sm->q_full, nq & 1);
       ++nq;
       if (t == 1) stamp(k, 7);
@@ -284,10 +283,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
     fence_async_smem();
     named_sync(BAR_MATH, NMT);
     stamp(k, 20);
-    if (mt == 0) {
-      cp_A<KU>(tmem + G::T_XE, uah, ual);  // G'' (diagonal rewritten) -> TMEM
-      issue_kxk<KU>(tmem + G::T_Q, tmem + G::T_XE, ubh, ubl, &sm->q_full);
-    }
+    if (mt == 0) issue_kxk<KU>(tmem + G::T_Q, uah, ual, ubh, ubl, &sm->q_full);
     mbar_wait(&sm->q_full, nq & 1);
     ++nq;
     stamp(k, 21);
@@ -377,6 +373,9 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
     fence_async_smem();
     named_sync(BAR_MATH, NMT);
     if (mt == 0) {
+      // W^T scales for the converters' epilogue, published before xe_ready
+      sm->wsc[k & 1][0] = (float)(beta * kappa / ((double)sz * (double)sx));
+      sm->wsc[k & 1][1] = (float)(kappa / ((double)sz * (double)sx));
       mbar_arrive(&sm->xe_ready);
       double s = 0.0;
       for (int kk = 0; kk < KU; ++kk) s += sm->sse[kk];
@@ -389,37 +388,45 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
       p.status[b] = st;
     }
     stamp(k, 3);
+    // The W pass of this realization (TMA re-read, conversion, W^T MMAs and
+    // the TMEM -> HBM epilogue) now proceeds on the converter / MMA warps
+    // while these warps move on to the next realization.
+  }
+  (void)nch;
+  (void)wc;
+  (void)wuse;
+}
 
-    // ---- (6) W epilogue: lane row c2 = r, antennas [32h, 32h+32) of each chunk
-    const float wscale = (float)(beta * kappa / ((double)sz * (double)sx));
-    const float fscale = (float)(kappa / ((double)sz * (double)sx));
-    float* Wb = reinterpret_cast<float*>(p.W + b * (int64_t)p.M * KU);
-    float* Fb = p.F ? reinterpret_cast<float*>(p.F + b * (int64_t)p.M * KU) : nullptr;
-    for (int c = 0; c < ((p.dbg == 1 || p.dbg == 2) ? 0 : nch); ++c, ++wc) {
-      const int j = wc % G::NWB;
-      mbar_wait(&sm->wfull[j], wuse[j] & 1);
-      ++wuse[j];
-      tc_after();
-      constexpr int WH = G::WH;
-      float d[WH];
-      if (quad_act) {
-        tmem_ld<WH>(tl + (j ? G::T_W1 : G::T_W0) + WH * h, d);
-        tmem_wait_ld();
-      }
-      tc_before();
-      mbar_arrive(&sm->wfree[j]);
-      if (act_row) {
-        const int64_t o0 = (int64_t)(c * G::CH + WH * h) * NC + r;
-        float* wp = Wb + o0;
+// W^T epilogue of one chunk, run by converter warps 0-3 (TMEM lane quadrant =
+// warp): thread = output component c2 = 32 q + lane, CH antennas.
+template <int KU>
+__device__ __forceinline__ void w_epilogue(const Params& p, Small* sm, uint32_t tmem, int64_t b, int c,
+                                           uint32_t j, uint32_t parity, uint32_t kpar) {
+  using G = Geo<KU>;
+  constexpr int NC = G::NC, CH = G::CH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = 32 * warp + lane;
+  const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16) + (j ? G::T_W1 : G::T_W0);
+  mbar_wait(&sm->wfull[j], parity);
+  // the math warps published the scales before xe_ready, which these MMAs awaited
+  const float wscale = sm->wsc[kpar][0], fscale = sm->wsc[kpar][1];
+  tc_after();
+  float d[CH];
+  if (32 * warp < NC) {
+    tmem_ld<CH>(tl, d);
+    tmem_wait_ld();
+  }
+  tc_before();
+  mbar_arrive(&sm->wfree[j]);
+  if (r < NC) {
+    const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH) * NC + r;
+    float* wp = reinterpret_cast<float*>(p.W) + o0;
 #pragma unroll
-        for (int a = 0; a < WH; ++a) __stcs(wp + a * NC, d[a] * wscale);
-        if (Fb) {
-          float* fp = Fb + o0;
+    for (int a = 0; a < CH; ++a) __stcs(wp + a * NC, d[a] * wscale);
+    if (p.F) {
+      float* fp = reinterpret_cast<float*>(p.F) + o0;
 #pragma unroll
-          for (int a = 0; a < WH; ++a) __stcs(fp + a * NC, d[a] * fscale);
-        }
-      }
+      for (int a = 0; a < CH; ++a) __stcs(fp + a * NC, d[a] * fscale);
     }
-    stamp(k, 4);
   }
 }

@@ -285,6 +285,8 @@ struct Small {
   uint64_t raw_full[12], conv_full[12], stage_free[12];
   uint64_t gram_full, q_full, xe_ready, scale_ready, gram_free;
   uint64_t wfull[2], wfree[2];
+  uint64_t xe_consumed;  // Xe(b) copied smem -> TMEM: the smem region may hold A(b+1)
+  float wsc[2][2];       // per realization parity: W scale, F scale (for the converters' epilogue)
   uint32_t tmem_slot;
   int pad0;
   float sz_slot[2];
@@ -369,17 +371,21 @@ __device__ __forceinline__ void cp_A(uint32_t t, uint32_t ah, uint32_t al) {
   }
 }
 
-// K x K tensor-core product Q = A'' * Bop (3xFP16) with A'' in TMEM, issued by one thread.
+// K x K tensor-core product Q = A'' * Bop (3xFP16), both operands in smem
+// (the TMEM A slot holds Xe of the previous realization while its W pass
+// streams), issued by one thread.
 template <int KU>
-__device__ __forceinline__ void issue_kxk(uint32_t tq, uint32_t ta, uint32_t bh, uint32_t bl, uint64_t* bar) {
+__device__ __forceinline__ void issue_kxk(uint32_t tq, uint32_t ah, uint32_t al, uint32_t bh, uint32_t bl,
+                                          uint64_t* bar) {
   using G = Geo<KU>;
   tc_after();
 #pragma unroll
   for (int s = 0; s < G::NC / 16; ++s) {
+    const uint64_t dah = pdesc<KU>(ah, s), dal = pdesc<KU>(al, s);
     const uint64_t dbh = pdesc<KU>(bh, s), dbl = pdesc<KU>(bl, s);
-    mma_ts(tq, ta + 8 * s, dbh, G::ID_P, s != 0);
-    mma_ts(tq, ta + 8 * s, dbl, G::ID_P, 1);
-    mma_ts(tq, ta + 64 + 8 * s, dbh, G::ID_P, 1);
+    mma(tq, dah, dbh, G::ID_P, s != 0);
+    mma(tq, dah, dbl, G::ID_P, 1);
+    mma(tq, dal, dbh, G::ID_P, 1);
   }
   commit(bar);
 }
@@ -413,9 +419,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
     mbar_init(&sm->xe_ready, 1);
     mbar_init(&sm->scale_ready, 1);
     mbar_init(&sm->gram_free, 1);
+    mbar_init(&sm->xe_consumed, 1);
     for (int j = 0; j < 2; ++j) {
       mbar_init(&sm->wfull[j], 1);
-      mbar_init(&sm->wfree[j], NMT);
+      mbar_init(&sm->wfree[j], 32 * NCONV);  // converter warps 0-3 run the W epilogue
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -494,7 +501,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
     uint32_t i = 0;
     float sz_par[2] = {1.0f, 1.0f};
     int have_par[2] = {0, 0};
-    for_items([&](uint32_t kc, int pass, int64_t) {
+    uint32_t wcv = 0;                 // W chunk counter (same sequence as the MMA issuer)
+    uint32_t wuse_c[2] = {0, 0};
+    const bool epi = warp < NCONV;    // warps 0-3 also run the W^T epilogue
+    auto epilogue = [&](int64_t b, int c, uint32_t kc) {
+      const uint32_t j = wcv % G::NWB;
+      w_epilogue<KU>(p, sm, tmem, b, c, j, wuse_c[j] & 1, kc & 1);
+      ++wuse_c[j];
+      ++wcv;
+    };
+    for_items([&](uint32_t kc, int pass, int64_t bcur) {
       const int par = kc & 1;
       if (pass == 0) { sz_par[par] = 1.0f; have_par[par] = 0; }
       float sz = sz_par[par];
@@ -562,6 +578,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
             if (c == 0) stamp(kc, 24 + 2 * pass);
             if (c == nch - 1) stamp(kc, 25 + 2 * pass);
           }
+          // W^T epilogue of the previous chunk overlaps this chunk's MMAs
+          if (pass == 1 && epi && c >= 1) epilogue(bcur, c - 1, kc);
+      }
+      if (pass == 1 && epi) {
+        epilogue(bcur, nch - 1, kc);
+        if (warp == 0 && lane == 0) stamp(kc, 4);
       }
       sz_par[par] = sz;
       have_par[par] = have;
@@ -599,6 +621,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
         mbar_wait(&sm->xe_ready, k & 1);
         stamp(k, 10);
         cp_A<KU>(tmem + G::T_XE, su32(aeh), su32(ael));  // Xe -> TMEM (A operand)
+        commit(&sm->xe_consumed);  // smem Xe may now be overwritten by A(k+1)
         for (int c = 0; c < nch; ++c, ++i, ++wc) {  // W^T = Xe^T Z^T
           const int s = i % NS;
           const int j = wc % G::NWB;

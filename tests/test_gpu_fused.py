@@ -1,0 +1,149 @@
+"""GPU tests of the fused tcgen05 precoder kernel (complex64, K in {16, 32, 64}).
+
+Every case is checked against the CPU oracle (complex128) on the same H,
+with the north_star tolerances written here: W relative Frobenius <= 1e-4,
+sum-SE relative <= 1e-4 (the kernel reaches ~2e-6 / ~1e-6).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import xlmimo_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+import paper_2305_13925_b200 as X  # noqa: E402
+from paper_2305_13925_b200 import _lib as L  # noqa: E402
+from paper_2305_13925_b200 import batched as BT  # noqa: E402
+from paper_2305_13925_b200.errors import DegenerateChannelError  # noqa: E402
+
+W_TOL = 1e-4
+SE_TOL = 1e-4
+
+
+def relf(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def _check(H, out, alpha, power, method, T, variant):
+    Hn = H.cpu().numpy().astype(np.complex128)
+    W = out.W.cpu().numpy()
+    S = out.sum_se.cpu().numpy()
+    beta = out.beta.cpu().numpy()
+    gam = out.gamma.cpu().numpy() if out.gamma is not None else None
+    for b in range(H.shape[0]):
+        G, be, g, s = O.precoder_and_se(Hn[b], alpha, power, 1.0, method, T, variant)
+        assert relf(W[b], G) <= W_TOL, (b, relf(W[b], G))
+        assert abs(S[b] - s) <= SE_TOL * abs(s), (b, S[b], s)
+        assert abs(beta[b] - be) <= 1e-4 * be
+        if gam is not None:
+            np.testing.assert_allclose(gam[b], g, rtol=1e-3, atol=1e-6 * np.abs(g).max())
+
+
+@pytest.mark.parametrize("S,K", [(16, 64), (4, 32), (4, 16), (2, 64), (1, 16)])
+def test_fused_shapes_vs_oracle(S, K):
+    assert BT.uses_tensor_cores(torch.complex64, "jacpcg", 64 * S, K)
+    m = X.ChannelModel(S=S, K=K, p=0.6, r=0.7)
+    H = X.generate_channels(m, seed=21, first=5, B=5, dtype=torch.complex64)
+    alpha, power = K / 10.0, 10.0
+    out = BT.rzf_batched(H, alpha, power, T=4)
+    _check(H, out, alpha, power, "jacpcg", 4, "textbook")
+
+
+@pytest.mark.parametrize("method,variant", [("cg", "textbook"), ("jacpcg", "algorithm")])
+@pytest.mark.parametrize("T", [1, 3, 6])
+def test_fused_methods(method, variant, T):
+    m = X.ChannelModel(S=4, K=32, p=0.5, r=0.5)
+    H = X.generate_channels(m, seed=3, first=0, B=4, dtype=torch.complex64)
+    out = BT.rzf_batched(H, 3.2, 10.0, method=method, T=T, variant=variant)
+    _check(H, out, 3.2, 10.0, method, T, variant)
+
+
+def test_fused_snr_sweep_per_realization_xi():
+    """configs[1]-style SNR sweep in one batch via per-realization xi."""
+    m = X.ChannelModel(S=4, K=32, p=0.5, r=0.5)
+    snrs = np.array([-10.0, -5.0, 0.0, 5.0, 10.0, 15.0, 20.0])
+    Hone = X.generate_channels(m, seed=9, first=0, B=1, dtype=torch.complex64)
+    H = Hone.repeat(len(snrs), 1, 1).contiguous()
+    xi = torch.tensor(32.0 / 10 ** (snrs / 10), dtype=torch.float64, device="cuda")
+    out = BT.rzf_batched(H, xi, 1.0, T=4)
+    Hn = Hone[0].cpu().numpy().astype(np.complex128)
+    for i, a in enumerate(xi.cpu().numpy()):
+        G, _, _, s = O.precoder_and_se(Hn, a, 1.0, 1.0, "jacpcg", 4, "textbook")
+        assert relf(out.W[i].cpu().numpy(), G) <= W_TOL
+        assert abs(out.sum_se[i].item() - s) <= SE_TOL * s
+
+
+def test_fused_matches_general_path_and_debug_gram():
+    wl = X.CONFIGS["cfg3"]
+    H = X.generate_channels(wl.model, seed=2, first=0, B=6, dtype=torch.complex64)
+    lib = L.lib()
+    A = torch.zeros(6, wl.K, wl.K, dtype=torch.complex64, device="cuda")
+    lib.xl_debug_set_gram_out(A.data_ptr())
+    try:
+        f = BT.rzf_batched(H, wl.alpha(), wl.power(), T=wl.T, want_X=True, want_F=True)
+        torch.cuda.synchronize()
+    finally:
+        lib.xl_debug_set_gram_out(None)
+    g = BT.rzf_batched(H, wl.alpha(), wl.power(), T=wl.T, want_X=True, want_F=True, general=True)
+    Ag = BT.gram_batched(H, wl.alpha())
+    assert relf(A.cpu().numpy(), Ag.cpu().numpy()) < 1e-5
+    assert relf(f.X.cpu().numpy(), g.X.cpu().numpy()) < 1e-5
+    assert relf(f.W.cpu().numpy(), g.W.cpu().numpy()) < 1e-5
+    # F = G / beta (precoder.py:70)
+    np.testing.assert_allclose(f.W.cpu().numpy(), f.F.cpu().numpy() * f.beta.cpu().numpy()[:, None, None],
+                               rtol=1e-5, atol=1e-7)
+    assert torch.allclose(f.sum_se, g.sum_se, rtol=1e-5)
+
+
+def test_fused_degenerate_and_zero_subarrays():
+    m = X.ChannelModel(S=4, K=16, p=0.3, r=0.5)
+    H = X.generate_channels(m, seed=4, first=0, B=4, dtype=torch.complex64)
+    H[2] = 0
+    H[1, :128] = 0  # leading all-zero chunks: the fp16 scale comes from a later chunk
+    out = BT.rzf_batched(H, 1.6, 10.0, T=4, check=False)
+    st = out.status.cpu().tolist()
+    assert st[2] == 3 and st[0] == 0 and st[1] == 0 and st[3] == 0
+    with pytest.raises(DegenerateChannelError):
+        BT.rzf_batched(H, 1.6, 10.0, T=4)
+    keep = [0, 1, 3]
+    sub = H[keep].contiguous()
+    _check(sub, BT.rzf_batched(sub, 1.6, 10.0, T=4), 1.6, 10.0, "jacpcg", 4, "textbook")
+
+
+@pytest.mark.parametrize("scale", [1e-6, 1e6])
+def test_fused_scale_invariance(scale):
+    """Power-of-two pre-scaling: W is invariant to scaling H by c with xi by c^2."""
+    m = X.ChannelModel(S=4, K=32, p=0.5, r=0.5)
+    H = X.generate_channels(m, seed=8, first=0, B=3, dtype=torch.complex64)
+    base = BT.rzf_batched(H, 3.2, 10.0, T=4)
+    Hs = (H * scale).contiguous()
+    out = BT.rzf_batched(Hs, 3.2 * scale * scale, 10.0, T=4)
+    # W(cH, c^2 xi) = W(H, xi) exactly (beta absorbs c)
+    assert relf(out.W.cpu().numpy(), base.W.cpu().numpy()) < 1e-5
+    assert torch.allclose(out.sum_se, base.sum_se, rtol=1e-5)
+
+
+def test_fused_range_fallback():
+    """A chunk far above the first chunk's scale overflows the fp16 split:
+    the kernel flags XL_STATUS_RANGE and rzf_batched re-runs it on the
+    general kernels (check=True), matching the oracle."""
+    m = X.ChannelModel(S=4, K=16, p=1.0, r=0.5)
+    H = X.generate_channels(m, seed=5, first=0, B=2, dtype=torch.complex64)
+    H[0, 192:] *= 1e4
+    raw = BT.rzf_batched(H, 1.6, 10.0, T=4, check=False)
+    assert raw.status.cpu().tolist()[0] == L.XL_STATUS_RANGE
+    out = BT.rzf_batched(H, 1.6, 10.0, T=4)
+    assert out.status.cpu().tolist() == [0, 0]
+    _check(H, out, 1.6, 10.0, "jacpcg", 4, "textbook")
+
+
+def test_fused_determinism_and_batch_independence():
+    wl = X.CONFIGS["cfg3"]
+    H = X.generate_channels(wl.model, seed=1, first=0, B=300, dtype=torch.complex64)
+    a = BT.rzf_batched(H, wl.alpha(), wl.power(), T=wl.T)
+    b = BT.rzf_batched(H, wl.alpha(), wl.power(), T=wl.T)
+    assert torch.equal(a.W, b.W) and torch.equal(a.sum_se, b.sum_se)
+    sub = BT.rzf_batched(H[37:41].contiguous(), wl.alpha(), wl.power(), T=wl.T)
+    assert torch.equal(sub.W, a.W[37:41]) and torch.equal(sub.sum_se, a.sum_se[37:41])
