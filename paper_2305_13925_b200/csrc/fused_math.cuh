@@ -44,7 +44,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
   auto stamp = [&](uint32_t kk, int slot) {
     if (p.trace && blockIdx.x == 0 && kk < 8 && mt == 0) p.trace[kk * 32 + slot] = clock64();
   };
-  uint32_t k = 0, nq = 0, wc = 0, par = 0;
+  uint32_t k = 0, nq = 0, wc = 0;
   uint32_t wuse[2] = {0, 0};
   for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++k) {
     const double alpha = p.xi_b ? p.xi_b[b] : p.xi;
@@ -69,8 +69,12 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
     }
     named_sync(BAR_MATH, NMT);
     float dmax = 0.0f;
-    for (int kk = 0; kk < KU; ++kk) dmax = fmaxf(dmax, sm->cdg[kk] + alpha_s);
-    const bool range_bad = !isfinite(dmax);
+    bool range_bad = false;  // per entry: fmaxf would drop a NaN (inf - inf in the split)
+    for (int kk = 0; kk < KU; ++kk) {
+      const float d = sm->cdg[kk] + alpha_s;
+      range_bad |= !isfinite(d);
+      dmax = fmaxf(dmax, d);
+    }
     const float sa = pow2_scale(dmax, 14);  // diag(A'') < 2^14
     const float gd = act_row ? sm->cdg[kr] : 0.0f;
     const float cr = (act_row && use_c) ? (gd + alpha_s) * sa : 1.0f;
@@ -143,21 +147,22 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
       tmem_wait_st();
     }
     int not_hpd = 0;
-    for (int t = 1; t <= p.T; ++t, par ^= 1) {
-      // (a) power-of-two scale of P for the fp16 split (one barrier: parity buffers)
-      float pm = 0.0f;
+    for (int t = 1; t <= p.T; ++t) {
+      // (a) per-column power-of-two scale of P for the fp16 split: columns
+      // converge at different rates, and a converged column must keep its
+      // relative precision (a shared scale flushes it to zero -> curvature 0)
 #pragma unroll
-      for (int jj = 0; jj < JH; ++jj) pm = fmaxf(pm, fabsf(P[jj]));
-      pm = warp_max(pm);
-      if (lane == 0) sm->mred2[par][mw] = pm;
+      for (int jj = 0; jj < JH; ++jj) A[jj] = fabsf(P[jj]);
+      column_partials<JH, true>(A, sm->red, q, h);
       named_sync(BAR_MATH, NMT);
-      float pmax = sm->mred2[par][0];
-#pragma unroll
-      for (int w = 1; w < NMATH; ++w) pmax = fmaxf(pmax, sm->mred2[par][w]);
-      const float sp = pow2_scale(pmax, 14);
+      if (mt < KU) {
+        const float s = pow2_scale(column_max<JH>(sm->red, mt), 14);
+        sm->spc[mt] = make_float2(s, 1.0f / s);
+      }
+      named_sync(BAR_MATH, NMT);
       if (t == 1) stamp(k, 5);
       // (b) Q = A'' P on the tensor core
-      if (act_row) write_cols<KU>(P, sp, r, h, pbh, pbl);
+      if (act_row) write_cols<KU>(P, sm->spc, r, h, pbh, pbl);
       fence_async_smem();
       named_sync(BAR_MATH, NMT);
       if (t == 1) stamp(k, 6);
@@ -166,15 +171,17 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
       ++nq;
       if (t == 1) stamp(k, 7);
       tc_after();
-      const float isp = 1.0f / sp;
-      const float qs = (use_c && !textbook) ? isp * icr : isp;  // Algorithm 1: z = C^-1 P m
+      const float qs = (use_c && !textbook) ? icr : 1.0f;  // Algorithm 1: z = C^-1 P m
       if (quad_act) {
         tmem_ld<JH>(tQ, A);
         tmem_wait_ld();
       }
       // (c) curvature m^H z per column
 #pragma unroll
-      for (int jj = 0; jj < JH; ++jj) A[jj] = act_row ? P[jj] * (A[jj] * qs) : 0.0f;
+      for (int jj = 0; jj < JH; ++jj) {
+        A[jj] = A[jj] * sm->spc[h * JH + jj].y;  // undo the column scale (exact)
+        A[jj] = act_row ? P[jj] * (A[jj] * qs) : 0.0f;
+      }
       column_partials<JH>(A, sm->red, q, h);
       named_sync(BAR_MATH, NMT);
       if (mt < KU) {  // (d) alpha_j, NotHpd (linsolve.py:276-280)
@@ -200,7 +207,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
         for (int i = 0; i < 8; ++i) {
           const float al = sm->coef[0][h * JH + c0 + i];
           xv[i] = xv[i] + al * P[c0 + i];
-          rv[i] = rv[i] - al * (qv[i] * qs);
+          rv[i] = rv[i] - al * ((qv[i] * sm->spc[h * JH + c0 + i].y) * qs);
           const float z = textbook ? rv[i] * icr : rv[i];
           A[c0 + i] = act_row ? rv[i] * z : 0.0f;
         }
@@ -310,7 +317,8 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
         const float g = act_row ? GX[c0 + i] * isx : 0.0f;
         GX[c0 + i] = g;
         part += act_row ? (double)xv[i] * (double)g : 0.0;
-        rs += g * g;
+        // interference summed directly (j != k): total - signal cancels in fp32
+        rs += (h * JH + c0 + i == kr) ? 0.0f : g * g;
       }
     }
     const double fro2 = kappa * math_sum_d(part, sm);
@@ -328,11 +336,11 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
     const bool any_not_hpd = math_max(not_hpd ? 1.0f : 0.0f, sm) > 0.0f;  // also orders rsq/dgq
     if (mt < KU) {
       const double b2 = beta * beta;
-      const double tot = b2 * ((double)sm->rsq[2 * mt] + (double)sm->rsq[NC + 2 * mt] +
-                               (double)sm->rsq[2 * mt + 1] + (double)sm->rsq[NC + 2 * mt + 1]);
+      const double intf = b2 * ((double)sm->rsq[2 * mt] + (double)sm->rsq[NC + 2 * mt] +
+                                (double)sm->rsq[2 * mt + 1] + (double)sm->rsq[NC + 2 * mt + 1]);
       const double sig = b2 * ((double)sm->dgq[2 * mt] * sm->dgq[2 * mt] +
                                 (double)sm->dgq[2 * mt + 1] * sm->dgq[2 * mt + 1]);
-      const double g = sig / ((tot - sig) + p.sigma2);
+      const double g = sig / (intf + p.sigma2);  // metrics.py:52-56
       if (p.gamma) p.gamma[b * KU + mt] = g;
       // per-user SE in double (a 64-thread step; |error| << the 1e-4 bound)
       sm->sse[mt] = log2(1.0 + g);

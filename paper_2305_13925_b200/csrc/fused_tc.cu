@@ -176,13 +176,14 @@ __device__ __forceinline__ float warp_max(float v) {
 }
 // Sum each of N per-lane values over the 32 lanes; lane l returns the total
 // of column l % N.  Fixed butterfly order -> bit-reproducible.
-template <int N>
+template <int N, bool MAX = false>
 __device__ __forceinline__ float warp_transpose_reduce(float (&v)[N]) {
   const int lane = threadIdx.x & 31;
+  auto op = [](float a, float b) { return MAX ? fmaxf(a, b) : a + b; };
 #pragma unroll
   for (int o = 16; o >= N; o >>= 1)
 #pragma unroll
-    for (int i = 0; i < N; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+    for (int i = 0; i < N; ++i) v[i] = op(v[i], __shfl_xor_sync(0xffffffffu, v[i], o));
 #pragma unroll
   for (int half = N / 2; half >= 1; half >>= 1) {
     const bool up = (lane & half) != 0;
@@ -190,7 +191,7 @@ __device__ __forceinline__ float warp_transpose_reduce(float (&v)[N]) {
     for (int i = 0; i < half; ++i) {
       float send = up ? v[i] : v[i + half];
       float keep = up ? v[i + half] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+      v[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, half));
     }
   }
   return v[0];
@@ -300,7 +301,7 @@ struct Small {
   double sse[64];
   float rzs[64];        // rz per column (owned by the finalising threads)
   float coef[2][64];    // broadcast per-column alpha / beta
-  float mred2[2][8];    // per-iteration P max, parity buffered
+  float2 spc[64];       // per-column P scale (2^e, 2^-e) of the current iteration
   float red2[8 * 32];
   int flags[4];
 };
@@ -330,10 +331,10 @@ __device__ __forceinline__ double math_sum_d(double v, Small* sm) {
 // Column sums of per-thread partials: each warp transpose-reduces its 32
 // rows, lanes < JH publish one partial per column into red[quadrant][h][j].
 // The caller finalises (fixed quadrant order) after a math barrier.
-template <int JH>
+template <int JH, bool MAX = false>
 __device__ __forceinline__ void column_partials(float (&v)[JH], float* red, int q, int h) {
   const int lane = threadIdx.x & 31;
-  float t = warp_transpose_reduce<JH>(v);
+  float t = warp_transpose_reduce<JH, MAX>(v);
   if (lane < JH) red[(q * 2 + h) * JH + lane] = t;
 }
 template <int JH>
@@ -342,16 +343,24 @@ __device__ __forceinline__ float column_total(const float* red, int j) {
   return ((red[(0 * 2 + h) * JH + jj] + red[(1 * 2 + h) * JH + jj]) + red[(2 * 2 + h) * JH + jj]) +
          red[(3 * 2 + h) * JH + jj];
 }
+template <int JH>
+__device__ __forceinline__ float column_max(const float* red, int j) {
+  const int h = j / JH, jj = j % JH;
+  return fmaxf(fmaxf(red[(0 * 2 + h) * JH + jj], red[(1 * 2 + h) * JH + jj]),
+               fmaxf(red[(2 * 2 + h) * JH + jj], red[(3 * 2 + h) * JH + jj]));
+}
 
 // Write the JH columns of this thread's component row r of an NC x KU
-// matrix (scaled by s) as the split B operand (rows = columns j, K = r).
+// matrix (column j scaled by s[j].x) as the split B operand (rows = columns
+// j, K = r).
 template <int KU>
-__device__ __forceinline__ void write_cols(const float* v, float s, int r, int h, uint8_t* bh, uint8_t* bl) {
+__device__ __forceinline__ void write_cols(const float* v, const float2* s, int r, int h, uint8_t* bh,
+                                           uint8_t* bl) {
   constexpr int JH = Geo<KU>::JH;
 #pragma unroll
   for (int jj = 0; jj < JH; ++jj) {
     __half hh, ll;
-    split(v[jj] * s, hh, ll);
+    split(v[jj] * s[h * JH + jj].x, hh, ll);
     const int o = boff<KU>(h * JH + jj, r);
     *reinterpret_cast<__half*>(bh + o) = hh;
     *reinterpret_cast<__half*>(bl + o) = ll;

@@ -68,6 +68,23 @@ def _sensitivity(P, S, T, w0, name):
     return worst
 
 
+def _iterate_sensitivity(P, S, T, w0, name):
+    """Per-iterate version of _sensitivity (keep_iterates runs)."""
+    fns = {"textbook": lambda Q: O.jacpcg_solve(Q, S, T, w0=w0, variant="textbook", keep_iterates=True),
+           "algorithm": lambda Q: O.jacpcg_solve(Q, S, T, w0=w0, variant="algorithm", keep_iterates=True),
+           "cg": lambda Q: O.cg_solve(Q, S, T, w0=w0, keep_iterates=True)}
+    base = fns[name](P).iterates
+    worst = np.zeros(len(base))
+    for seed in range(3):
+        rng = np.random.default_rng(seed)
+        E = rng.standard_normal(P.shape) * 1e-16 * np.abs(P)
+        E = (E + E.T) / 2
+        its = fns[name](P + E).iterates
+        for t in range(min(len(its), len(base))):
+            worst[t] = max(worst[t], relf(its[t], base[t]))
+    return worst
+
+
 def test_solver_golden(golden):
     g = golden("solvers")
     for i in range(int(g["n_solver_cases"])):
@@ -99,8 +116,9 @@ def test_solver_golden(golden):
             if pre + name + "_iterates" in g:
                 ri = g[pre + name + "_iterates"]
                 assert len(o.iterates) == ri.shape[0]
-                for a, b in zip(o.iterates, ri):
-                    assert relf(a, b) < tol
+                sens = _iterate_sensitivity(P, S, T, w0, name)
+                for t, (a, b) in enumerate(zip(o.iterates, ri)):
+                    assert relf(a, b) < max(tol, 50 * sens[t]), (i, name, t, relf(a, b), sens[t])
         o = X.direct_solve(sysm)
         assert relf(o.w, g[pre + "direct_w"]) < 1e-11
         assert o.iterations == 0 and o.converged
@@ -189,7 +207,8 @@ def test_precoder_golden_c128(golden, tag):
         # interference = row total - signal (metrics.py:54) cancels when one user
         # dominates its row, so gamma inherits ~1e-8 relative round-off.
         np.testing.assert_allclose(out.gamma.cpu().numpy(), g[key[:-2] + "_gamma"], rtol=1e-7)
-        np.testing.assert_allclose(out.sum_se.cpu().numpy(), g[key[:-2] + "_sumse"], rtol=1e-10)
+        # SE inherits gamma's cancellation (see above): 1e-8 relative in complex128
+        np.testing.assert_allclose(out.sum_se.cpu().numpy(), g[key[:-2] + "_sumse"], rtol=1e-8)
         # G = beta F (precoder.py:70)
         np.testing.assert_allclose(W, out.F.cpu().numpy() * out.beta.cpu().numpy()[:, None, None],
                                    rtol=1e-14, atol=0)
