@@ -14,20 +14,28 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
          "-Xptxas", "-warn-spills"]
 
 
-def build(verbose=False, force=False):
+def build(verbose=False, force=False, out=None, extra=()):
+    """Compile the library (mtime-checked).  ``out``/``extra`` build a
+    development variant (e.g. ``-DXL_...``) elsewhere for A/B timing."""
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
     deps.append(os.path.join(os.path.dirname(HERE), "include", "xlmimo_b200.h"))
-    if (not force and os.path.exists(LIB)
-            and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in deps)):
-        return LIB
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    cmd = [NVCC, *FLAGS, "-o", LIB, *srcs]
+    lib = out or LIB
+    if (not force and out is None and os.path.exists(lib)
+            and os.path.getmtime(lib) >= max(os.path.getmtime(d) for d in deps)):
+        return lib
+    os.makedirs(os.path.dirname(os.path.abspath(lib)), exist_ok=True)
+    cmd = [NVCC, *FLAGS, *extra, "-o", lib, *srcs]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(verbose=True, force="--force" in sys.argv)
+    args = sys.argv[1:]
+    out = None
+    if "--out" in args:
+        out = args[args.index("--out") + 1]
+    build(verbose=True, force="--force" in args, out=out,
+          extra=[a for a in args if a.startswith("-D")])

@@ -42,7 +42,8 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
   const int mt = tid - 32 * NCONV;  // 0..255
   const uint32_t uah = su32(aeh), ual = su32(ael), ubh = su32(pbh), ubl = su32(pbl);
   auto stamp = [&](uint32_t kk, int slot) {
-    if (p.trace && blockIdx.x == 0 && kk < 8 && mt == 0) p.trace[kk * 32 + slot] = clock64();
+    if (p.trace && blockIdx.x == 0 && mt == 0 && kk >= (uint32_t)p.trace_k0 && kk < (uint32_t)p.trace_k0 + 8)
+      p.trace[(kk - p.trace_k0) * 32 + slot] = clock64();
   };
   uint32_t k = 0, nq = 0, wc = 0;
   uint32_t wuse[2] = {0, 0};
@@ -82,7 +83,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
 
     // ---- (2) A'' split: row 2k = (ar, -ai), row 2k+1 = (ai, ar) per column pair
     // (the smem operand region held Xe(k-1) until the W pass copied it to TMEM)
-    if (k >= 1) mbar_wait(&sm->xe_consumed, (k - 1) & 1);
+    if (k >= 1 && !(p.dbg & 3)) mbar_wait(&sm->xe_consumed, (k - 1) & 1);
     if (quad_act) {
 #pragma unroll 1
       for (int c0 = 0; c0 < HC; c0 += 16) {
@@ -101,12 +102,11 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
             const float inv = 1.0f / (sz * sz);
             p.dbgA[(b * KU + kr) * KU + jc] = make_float2(ar * inv, ai * inv);
           }
-          __half h0, l0, h1, l1;
-          split((odd ? ai : ar) * sa, h0, l0);
-          split((odd ? ar : -ai) * sa, h1, l1);
+          uint32_t hw, lw;
+          split2((odd ? ai : ar) * sa, (odd ? ar : -ai) * sa, hw, lw);
           const int o = boff<KU>(r, 2 * jc);
-          *reinterpret_cast<uint32_t*>(aeh + o) = pack2(h0, h1);
-          *reinterpret_cast<uint32_t*>(ael + o) = pack2(l0, l1);
+          *reinterpret_cast<uint32_t*>(aeh + o) = hw;
+          *reinterpret_cast<uint32_t*>(ael + o) = lw;
         }
       }
     }
@@ -114,7 +114,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
     fence_async_smem();
     named_sync(BAR_MATH, NMT);  // every thread's Gram TMEM reads are complete
     if (mt == 0) mbar_arrive(&sm->gram_free);  // the next Gram may accumulate
-    if (p.dbg == 1) {
+    if (p.dbg & 1) {
       if (mt == 0) p.status[b] = range_bad ? XL_STATUS_RANGE : 0;
       continue;
     }
@@ -278,12 +278,14 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
       }
       if (act_row) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          __half hh, ll;
-          split(xv[i] * sx, hh, ll);
-          const int o = boff<KU>(h * JH + c0 + i, r);
-          *reinterpret_cast<__half*>(pbh + o) = hh;
-          *reinterpret_cast<__half*>(pbl + o) = ll;
+        for (int i = 0; i < 8; i += 2) {
+          uint32_t hh, ll;
+          split2(xv[i] * sx, xv[i + 1] * sx, hh, ll);
+          const int o0 = boff<KU>(h * JH + c0 + i, r), o1 = boff<KU>(h * JH + c0 + i + 1, r);
+          *reinterpret_cast<unsigned short*>(pbh + o0) = (unsigned short)(hh & 0xffffu);
+          *reinterpret_cast<unsigned short*>(pbl + o0) = (unsigned short)(ll & 0xffffu);
+          *reinterpret_cast<unsigned short*>(pbh + o1) = (unsigned short)(hh >> 16);
+          *reinterpret_cast<unsigned short*>(pbl + o1) = (unsigned short)(ll >> 16);
         }
       }
     }
@@ -303,7 +305,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
     const float isx = 1.0f / sx;
     // kappa = sa sz^2: X_true = kappa X'', G X_true = GX
     const double kappa = (double)sa * (double)sz * (double)sz;
-    double part = 0.0;
+    float part = 0.0f;  // 32-term per-thread partial in fp32, cross-thread sum in fp64
     float rs = 0.0f;
 #pragma unroll
     for (int c0 = 0; c0 < JH; c0 += 8) {
@@ -316,12 +318,12 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
       for (int i = 0; i < 8; ++i) {
         const float g = act_row ? GX[c0 + i] * isx : 0.0f;
         GX[c0 + i] = g;
-        part += act_row ? (double)xv[i] * (double)g : 0.0;
+        part = act_row ? fmaf(xv[i], g, part) : part;
         // interference summed directly (j != k): total - signal cancels in fp32
         rs += (h * JH + c0 + i == kr) ? 0.0f : g * g;
       }
     }
-    const double fro2 = kappa * math_sum_d(part, sm);
+    const double fro2 = kappa * math_sum_d((double)part, sm);
     stamp(k, 22);
     double beta = 0.0;
     int degenerate = 0;
@@ -334,16 +336,24 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
         if (h * JH + jj == kr) sm->dgq[r] = GX[jj];
     }
     const bool any_not_hpd = math_max(not_hpd ? 1.0f : 0.0f, sm) > 0.0f;  // also orders rsq/dgq
-    if (mt < KU) {
-      const double b2 = beta * beta;
-      const double intf = b2 * ((double)sm->rsq[2 * mt] + (double)sm->rsq[NC + 2 * mt] +
-                                (double)sm->rsq[2 * mt + 1] + (double)sm->rsq[NC + 2 * mt + 1]);
-      const double sig = b2 * ((double)sm->dgq[2 * mt] * sm->dgq[2 * mt] +
-                                (double)sm->dgq[2 * mt + 1] * sm->dgq[2 * mt + 1]);
-      const double g = sig / (intf + p.sigma2);  // metrics.py:52-56
-      if (p.gamma) p.gamma[b * KU + mt] = g;
-      // per-user SE in double (a 64-thread step; |error| << the 1e-4 bound)
-      sm->sse[mt] = log2(1.0 + g);
+    if (mt < 64) {  // warps 4-5: per-user SINR / SE, then a fixed-order warp sum
+      double se = 0.0;
+      if (mt < KU) {
+        const double b2 = beta * beta;
+        const double intf = b2 * ((double)sm->rsq[2 * mt] + (double)sm->rsq[NC + 2 * mt] +
+                                  (double)sm->rsq[2 * mt + 1] + (double)sm->rsq[NC + 2 * mt + 1]);
+        const double sig = b2 * ((double)sm->dgq[2 * mt] * sm->dgq[2 * mt] +
+                                  (double)sm->dgq[2 * mt + 1] * sm->dgq[2 * mt + 1]);
+        const double g = sig / (intf + p.sigma2);  // metrics.py:52-56
+        if (p.gamma) p.gamma[b * KU + mt] = g;
+        se = log2(1.0 + g);
+      }
+      se = warp_sum(se);
+      if (lane == 0) sm->sse[mt >> 5] = se;
+      if (mt == 0) {  // W^T scales for the converters' epilogue, published before xe_ready
+        sm->wsc[k & 1][0] = (float)(beta * kappa / ((double)sz * (double)sx));
+        sm->wsc[k & 1][1] = (float)(kappa / ((double)sz * (double)sx));
+      }
     }
     stamp(k, 23);
 
@@ -363,31 +373,23 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
         const int jc = h * JH + c0 + i;
         if (act_row) {
           if (p.X) reinterpret_cast<float*>(p.X)[((b * KU + kr) * KU + jc) * 2 + (r & 1)] = (float)(kappa * xv[i]);
-          __half h0, l0, h1, l1;
-          if (!odd) {  // v = xr, pv = xi: row 2jc = (xr, -xi)
-            split(v, h0, l0);
-            split(-pv, h1, l1);
-          } else {     // v = xi, pv = xr: row 2jc + 1 = (xi, xr)
-            split(v, h0, l0);
-            split(pv, h1, l1);
-          }
+          // even: v = xr, pv = xi -> row 2jc = (xr, -xi); odd: row 2jc + 1 = (xi, xr)
+          uint32_t hw, lw;
+          split2(v, odd ? pv : -pv, hw, lw);
           const int o = boff<KU>(2 * jc + (odd ? 1 : 0), 2 * kr);
-          *reinterpret_cast<uint32_t*>(aeh + o) = pack2(h0, h1);
-          *reinterpret_cast<uint32_t*>(ael + o) = pack2(l0, l1);
+          *reinterpret_cast<uint32_t*>(aeh + o) = hw;
+          *reinterpret_cast<uint32_t*>(ael + o) = lw;
         }
       }
     }
+    stamp(k, 28);
     tc_before();
     fence_async_smem();
     named_sync(BAR_MATH, NMT);
+    stamp(k, 29);
     if (mt == 0) {
-      // W^T scales for the converters' epilogue, published before xe_ready
-      sm->wsc[k & 1][0] = (float)(beta * kappa / ((double)sz * (double)sx));
-      sm->wsc[k & 1][1] = (float)(kappa / ((double)sz * (double)sx));
       mbar_arrive(&sm->xe_ready);
-      double s = 0.0;
-      for (int kk = 0; kk < KU; ++kk) s += sm->sse[kk];
-      p.sum_se[b] = s;
+      p.sum_se[b] = sm->sse[0] + sm->sse[1];
       p.beta[b] = beta;
       int st = XL_STATUS_OK;
       if (range_bad) st = XL_STATUS_RANGE;
@@ -405,36 +407,45 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
   (void)wuse;
 }
 
-// W^T epilogue of one chunk, run by converter warps 0-3 (TMEM lane quadrant =
-// warp): thread = output component c2 = 32 q + lane, CH antennas.
+// W^T epilogue of one chunk, run by the four warps of lane quadrants 0-3
+// (converter warps 0-3, or the epilogue warpgroup with XL_EPI_WARPS): thread
+// = output component c2 = 32 q + lane, CH antennas, read from TMEM in EPI_PART
+// column pieces (the epilogue warpgroup runs with 64 registers).
 template <int KU>
 __device__ __forceinline__ void w_epilogue(const Params& p, Small* sm, uint32_t tmem, int64_t b, int c,
                                            uint32_t j, uint32_t parity, uint32_t kpar) {
   using G = Geo<KU>;
   constexpr int NC = G::NC, CH = G::CH;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int PART = XL_EPI_WARPS ? 32 : CH;
+  static_assert(CH % PART == 0, "epilogue pieces");
+  const int warp = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;  // lane quadrant
   const int r = 32 * warp + lane;
   const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16) + (j ? G::T_W1 : G::T_W0);
   mbar_wait(&sm->wfull[j], parity);
   // the math warps published the scales before xe_ready, which these MMAs awaited
   const float wscale = sm->wsc[kpar][0], fscale = sm->wsc[kpar][1];
   tc_after();
-  float d[CH];
-  if (32 * warp < NC) {
-    tmem_ld<CH>(tl, d);
-    tmem_wait_ld();
-  }
-  tc_before();
-  mbar_arrive(&sm->wfree[j]);
-  if (r < NC) {
-    const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH) * NC + r;
-    float* wp = reinterpret_cast<float*>(p.W) + o0;
+  const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH) * NC + r;
+  float* wp = reinterpret_cast<float*>(p.W) + o0;
+  float* fp = p.F ? reinterpret_cast<float*>(p.F) + o0 : nullptr;
+#pragma unroll 1
+  for (int a0 = 0; a0 < CH; a0 += PART) {
+    float d[PART];
+    if (32 * warp < NC) {
+      tmem_ld<PART>(tl + a0, d);
+      tmem_wait_ld();
+    }
+    if (a0 + PART == CH) {  // accumulator drained: the next W MMAs may overwrite it
+      tc_before();
+      mbar_arrive(&sm->wfree[j]);
+    }
+    if (r < NC && !(p.dbg & 8)) {  // dbg & 8: timing without the W stores
 #pragma unroll
-    for (int a = 0; a < CH; ++a) __stcs(wp + a * NC, d[a] * wscale);
-    if (p.F) {
-      float* fp = reinterpret_cast<float*>(p.F) + o0;
+      for (int a = 0; a < PART; ++a) __stcs(wp + (a0 + a) * NC, d[a] * wscale);
+      if (fp) {
 #pragma unroll
-      for (int a = 0; a < CH; ++a) __stcs(fp + a * NC, d[a] * fscale);
+        for (int a = 0; a < PART; ++a) __stcs(fp + (a0 + a) * NC, d[a] * fscale);
+      }
     }
   }
 }

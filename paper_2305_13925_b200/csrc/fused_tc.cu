@@ -104,6 +104,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (++spins > (1u << 24)) asm volatile("trap;");
   } while (!done);
 }
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t hint) {
   asm volatile(
@@ -149,14 +152,40 @@ __device__ __forceinline__ void tmem_ld(uint32_t ta, float* v) {
   }
 }
 
-constexpr uint64_t HINT_EVICT_FIRST = 0x12F0000000000000ull;
-constexpr uint64_t HINT_EVICT_LAST = 0x14F0000000000000ull;
+// L2 cache policies for the bulk loads, made by createpolicy (the opaque
+// 64-bit encoding is not assumed).
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 
 // ------------------------------------------------------------- helpers ----
 // x = hi + lo, hi = fp16(x), lo = fp16(x - hi)  (x pre-scaled into range)
+// Packed conversions only: cvt.rn.f16x2.f32 is an ALU op (F2FP), the scalar
+// cvt.rn.f16.f32 is a quarter-rate XU op (F2F) that stalled the math warps.
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __float22half2_rn(make_float2(a, b));
+  const float2 hf = __half22float2(h);
+  const __half2 l = __float22half2_rn(make_float2(a - hf.x, b - hf.y));
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
 __device__ __forceinline__ void split(float x, __half& hi, __half& lo) {
-  hi = __float2half_rn(x);
-  lo = __float2half_rn(x - __half2float(hi));
+  uint32_t h, l;
+  split2(x, 0.0f, h, l);
+  hi = __ushort_as_half((unsigned short)(h & 0xffffu));
+  lo = __ushort_as_half((unsigned short)(l & 0xffffu));
 }
 __device__ __forceinline__ uint32_t h2u(__half2 v) { return *reinterpret_cast<uint32_t*>(&v); }
 __device__ __forceinline__ uint32_t pack2(__half a, __half b) {
@@ -198,16 +227,35 @@ __device__ __forceinline__ float warp_transpose_reduce(float (&v)[N]) {
 }
 
 // ----------------------------------------------------------- geometry ----
+#ifndef XL_WSPLIT
+#define XL_WSPLIT 0           // W pass: extra converter warps take half the blocks
+#endif
+#ifndef XL_PF
+#define XL_PF 0               // L2 prefetch distance in 32 KB ring items (0: off)
+#endif
+#ifndef XL_WB_GRAM
+#define XL_WB_GRAM 0          // Gram TMEM columns double-buffer the W accumulator
+#endif
+#ifndef XL_WB_START
+#define XL_WB_START 4         // first W chunk that may use them (A(k+1) built by then)
+#endif
+#ifndef XL_CONV_ARRIVE_ALL
+#define XL_CONV_ARRIVE_ALL 1  // conv_full: per-warp arrivals instead of a CTA barrier
+#endif
 constexpr int NCONV = 4, NMATH = 8;
 constexpr int W_MMA = NCONV + NMATH, W_PROD = W_MMA + 1;
-constexpr int NTHREADS = 512;  // 16 warps = 4 warpgroups (setmaxnreg granularity)
+#ifndef XL_EPI_WARPS
+#define XL_EPI_WARPS 0  // 1: a fifth warpgroup (warps 16-19) runs the W^T epilogue
+#endif
+constexpr int NTHREADS = XL_EPI_WARPS ? 640 : 512;  // 4-5 warpgroups (setmaxnreg granularity)
+constexpr int W_EPI0 = 16;                          // first epilogue warp (lane quadrant 0)
 constexpr int BAR_CONV = 1, BAR_MATH = 2;
 // Converter warps: 0..3 plus the two spare warps of warpgroup 3 (14, 15).
 #ifndef XL_NCW
 #define XL_NCW 6
 #endif
 constexpr int NCW = XL_NCW;
-__device__ __forceinline__ bool is_converter(int w) { return w < NCONV || (NCW > NCONV && w >= 16 - (NCW - NCONV)); }
+__device__ __forceinline__ bool is_converter(int w) { return w < NCONV || (NCW > NCONV && w >= 16 - (NCW - NCONV) && w < 16); }
 __device__ __forceinline__ int conv_index(int w) { return w < NCONV ? w : NCONV + (w - (16 - (NCW - NCONV))); }
 constexpr int NMT = 32 * NMATH;               // math threads
 
@@ -244,10 +292,20 @@ struct Geo {
   // TMEM columns.  T_XE holds the A operand of the K x K products (A'' / G'')
   // and then of W^T (Xe), hi at T_XE and lo at T_XE + 64, copied in from smem
   // by tcgen05.cp so the MMAs re-read only their B operand from smem.
-  static constexpr int NWB = (CH <= 32) ? 2 : 1;  // W accumulator buffers
+  static constexpr int NWB = (CH <= 32) ? 2 : 1;  // W accumulator buffers at T_W0
   static_assert(NWB * CH <= 64, "W accumulator columns");
-  static constexpr uint32_t T_GRAM = 0, T_Q = 128, T_W0 = 192, T_W1 = 192 + CH * (NWB - 1), T_X = 256,
-                            T_R = 320, T_XE = 384;
+  // With one buffer at T_W0, the Gram columns serve as the second W buffer
+  // while W(k) streams: G(k+1) is consumed (A(k+1) built) early in W(k) and
+  // G(k+2) starts only after W(k).
+  static constexpr bool WB_GRAM = XL_WB_GRAM && NWB == 1 && CH <= 128;
+  static constexpr uint32_t T_GRAM = 0, T_Q = 128, T_W0 = 192, T_X = 256, T_R = 320, T_XE = 384;
+  static constexpr uint32_t T_W1 = NWB == 2 ? 192 + CH : T_GRAM;
+  // W accumulator buffer of chunk c (wc = running W chunk count)
+  __device__ static int wsel(int c, uint32_t wc) {
+    if (NWB == 2) return (int)(wc & 1);
+    if (!WB_GRAM) return 0;
+    return (c >= XL_WB_START && ((c - XL_WB_START) & 1) == 0) ? 1 : 0;
+  }
 };
 
 struct Params {
@@ -266,9 +324,11 @@ struct Params {
   float2* X;
   int32_t* status;
   float2* dbgA;  // optional [B][K][K] regularized Gram (tests)
-  int dbg;       // bisection: 1 = Gram + A only, 2 = no W pass
+  int dbg;       // timing bisection bits: 1 Gram + A only, 2 no W pass, 4 no conversion,
+                 // 8 no W stores, 16 no Gram MMAs (results invalid)
   long long* trace;  // optional per-phase clock64 stamps of CTA 0 (XL_FUSED_TRACE)
-  int keep16;        // sixteenths of each realization's H kept L2-resident (evict_last)
+  int l2mode;        // L2 policy of the G-pass loads: 0 evict_first, 1 normal, 2 evict_last
+  int trace_k0;      // first traced realization of CTA 0 (XL_FUSED_TRACE=k0+1)
 };
 
 // Element (row n, col k) of a padded n x NC K-major operand tile (core rows = n).
@@ -358,12 +418,14 @@ __device__ __forceinline__ void write_cols(const float* v, const float2* s, int 
                                            uint8_t* bl) {
   constexpr int JH = Geo<KU>::JH;
 #pragma unroll
-  for (int jj = 0; jj < JH; ++jj) {
-    __half hh, ll;
-    split(v[jj] * s[h * JH + jj].x, hh, ll);
-    const int o = boff<KU>(h * JH + jj, r);
-    *reinterpret_cast<__half*>(bh + o) = hh;
-    *reinterpret_cast<__half*>(bl + o) = ll;
+  for (int jj = 0; jj < JH; jj += 2) {
+    uint32_t hh, ll;
+    split2(v[jj] * s[h * JH + jj].x, v[jj + 1] * s[h * JH + jj + 1].x, hh, ll);
+    const int o0 = boff<KU>(h * JH + jj, r), o1 = boff<KU>(h * JH + jj + 1, r);
+    *reinterpret_cast<unsigned short*>(bh + o0) = (unsigned short)(hh & 0xffffu);
+    *reinterpret_cast<unsigned short*>(bl + o0) = (unsigned short)(ll & 0xffffu);
+    *reinterpret_cast<unsigned short*>(bh + o1) = (unsigned short)(hh >> 16);
+    *reinterpret_cast<unsigned short*>(bl + o1) = (unsigned short)(ll >> 16);
   }
 }
 
@@ -420,7 +482,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sm->raw_full[s], 1);
-      mbar_init(&sm->conv_full[s], 1);
+      mbar_init(&sm->conv_full[s], XL_CONV_ARRIVE_ALL ? NCW : 1);
       mbar_init(&sm->stage_free[s], 1);
     }
     mbar_init(&sm->gram_full, 1);
@@ -447,10 +509,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
   // phase stamps (CTA 0, first 8 realizations) for pipeline analysis
   // per ring item i in [64, 128): 0 = load issued, 1 = raw landed, 2 = converted, 3 = MMAs issued
   auto item_stamp = [&](uint32_t ii, int slot) {
-    if (p.trace && blockIdx.x == 0 && ii >= 64 && ii < 128) p.trace[256 + (ii - 64) * 4 + slot] = clock64();
+    const uint32_t i0 = 64 + 32 * (uint32_t)p.trace_k0;
+    if (p.trace && blockIdx.x == 0 && ii >= i0 && ii < i0 + 64) p.trace[256 + (ii - i0) * 8 + slot] = clock64();
   };
   auto stamp = [&](uint32_t kk, int slot) {
-    if (p.trace && blockIdx.x == 0 && kk < 8) p.trace[kk * 32 + slot] = clock64();
+    if (p.trace && blockIdx.x == 0 && kk >= (uint32_t)p.trace_k0 && kk < (uint32_t)p.trace_k0 + 8)
+      p.trace[(kk - p.trace_k0) * 32 + slot] = clock64();
   };
 #ifndef XL_REG_AUX
 #define XL_REG_AUX 56
@@ -458,7 +522,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
 #define XL_REG_MATH 176
 #endif
   static_assert(128 * XL_REG_AUX + 128 * XL_REG_CONV + 256 * XL_REG_MATH <= 65536, "register budget");
-#if XL_USE_SETMAXNREG
+#if XL_EPI_WARPS
+  // 640 threads: the launch bound leaves 96 registers per thread; the math
+  // warpgroups take 128 (inside their branch, so ptxas allocates for it) from
+  // the other three.
+  // setmaxnreg.inc draws only on registers released by .dec: the math warps'
+  // +32 x 256 comes from WG0/WG3 (96 -> 80) and the epilogue WG (96 -> 64).
+  if (warp < NCONV || (warp >= NCONV + NMATH && warp < W_EPI0)) asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
+  if (warp >= W_EPI0) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
+#elif XL_USE_SETMAXNREG
   if (warp >= W_MMA) {  // warpgroup 3: MMA issuer, producer, 2 idle warps
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(XL_REG_AUX));
   } else if (warp < NCONV) {
@@ -475,7 +547,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
     for (int64_t k = 0; k < nb; ++k)
       for (int part = (k == 0 ? 0 : 1); part < 3; ++part) {
         if (part == 1 && k + 1 >= nb) continue;
-        if (part == 2 && (p.dbg == 1 || p.dbg == 2)) continue;
+        if (part == 2 && (p.dbg & 3)) continue;
         const int64_t kk = part == 1 ? k + 1 : k;
         body((uint32_t)kk, part == 2 ? 1 : 0, (int64_t)blockIdx.x + kk * gridDim.x);
       }
@@ -484,21 +556,44 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
     // ------------------------------------------------------ producer ------
     if (lane == 0) {
       uint32_t i = 0;
-      const int keep_num = p.keep16;
+      const uint64_t pol_first = policy_evict_first();
+      const uint64_t pol_g = (p.l2mode & 3) == 0 ? pol_first : (p.l2mode & 3) == 1 ? policy_evict_normal()
+                                                                                  : policy_evict_last();
+      // L2 prefetch cursor XL_PF items ahead of the TMA loads (same order as
+      // for_items): the smem ring is too small to cover HBM latency on its
+      // own, so the loads that follow hit L2.
+      int64_t pk = 0;
+      int ppart = 0, pc = 0;
+      auto part_ok = [&](int64_t k, int part) {
+        if (part == 0) return k == 0;
+        if (part == 1) return k + 1 < nb;
+        return !(p.dbg & 3);
+      };
+      auto prefetch_next = [&]() {
+        if (pk >= nb) return;
+        const int64_t kk = ppart == 1 ? pk + 1 : pk;
+        const int64_t bb = (int64_t)blockIdx.x + kk * gridDim.x;
+        bulk_prefetch_l2(reinterpret_cast<const char*>(p.H + bb * (int64_t)p.M * KU) + (int64_t)pc * G::SB, G::SB);
+        if (++pc < nch) return;
+        pc = 0;
+        do {
+          if (++ppart == 3) { ppart = 0; ++pk; }
+        } while (pk < nb && !part_ok(pk, ppart));
+      };
+      for (int q = 0; q < XL_PF; ++q) prefetch_next();
       for_items([&](uint32_t kk, int pass, int64_t b) {
         const char* Hb = reinterpret_cast<const char*>(p.H + b * (int64_t)p.M * KU);
         for (int c = 0; c < nch; ++c, ++i) {
           const int s = i % NS;
+          prefetch_next();
           if (i >= (uint32_t)NS) mbar_wait(&sm->stage_free[s], ((i / NS) - 1) & 1);
           item_stamp(i, 0);
           mbar_expect_tx(&sm->raw_full[s], G::SB);
-          // Two realizations per SM are in flight (Gram of k+1 overlaps PCG of
-          // k), which is more than L2 holds for all 148 SMs; keep only the
-          // first keep_num/16 of each realization's chunks L2-resident for
-          // the W re-read and stream the rest.
-          const bool keep = pass == 0 && c * 16 < nch * keep_num;
+          // The W pass re-reads H about two passes later; the G-pass policy
+          // (l2mode) decides how hard L2 tries to keep it, the W-pass reads
+          // are dead after use.
           bulk_g2s(ring + s * G::SB, Hb + (int64_t)c * G::SB, G::SB, &sm->raw_full[s],
-                   keep ? HINT_EVICT_LAST : HINT_EVICT_FIRST);
+                   pass == 0 ? pol_g : pol_first);
           if (c == 0 && pass == 0) stamp(kk, 16);
           if (c == nch - 1) stamp(kk, 17 + pass);
         }
@@ -512,9 +607,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
     int have_par[2] = {0, 0};
     uint32_t wcv = 0;                 // W chunk counter (same sequence as the MMA issuer)
     uint32_t wuse_c[2] = {0, 0};
-    const bool epi = warp < NCONV;    // warps 0-3 also run the W^T epilogue
+    const bool epi = !XL_EPI_WARPS && warp < NCONV;  // warps 0-3 also run the W^T epilogue
     auto epilogue = [&](int64_t b, int c, uint32_t kc) {
-      const uint32_t j = wcv % G::NWB;
+      const uint32_t j = G::wsel(c, wcv);
       w_epilogue<KU>(p, sm, tmem, b, c, j, wuse_c[j] & 1, kc & 1);
       ++wuse_c[j];
       ++wcv;
@@ -529,15 +624,34 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
           uint8_t* st = ring + s * G::SB;
           mbar_wait(&sm->raw_full[s], (i / NS) & 1);
           if (warp == 0 && lane == 0) item_stamp(i, 1);
-          // blocks of 4 antennas x 32 components, round-robin over converter warps
-          constexpr int NBLK = (G::CH / 4) * (NC / 32), NBM = (NBLK + NCW - 1) / NCW;
+          // Half-blocks of 8 antennas x 32 components (two per 8x32 block),
+          // round-robin over converter warps.  Lane -> (row, 16-B half b,
+          // core matrix j) is chosen so both the float4 reads (8-lane phases:
+          // distinct (j, b)) and the uint2 core-matrix writes (16-lane
+          // phases: distinct (row, b)) are bank-conflict free.
+          // G pass: round-robin over the NCW warps.  W pass: warps 0-3 also
+          // run the W^T epilogue, so the two extra warps take half the blocks.
+          constexpr int NBLK = (G::CH / 8) * (NC / 32) * 2, NBG = (NBLK + NCW - 1) / NCW;
+          static_assert(NCW == NCONV + 2, "W-pass block split assumes two extra converter warps");
+          constexpr int NBM = (XL_WSPLIT && NBLK / 4 > NBG) ? NBLK / 4 : NBG;
+          auto blk_of = [&](int k) -> int {
+            if (pass == 0 || !XL_WSPLIT) return cw + k * NCW < NBLK ? cw + k * NCW : -1;
+            if (cw >= NCONV) return k < NBLK / 4 ? (cw - NCONV) + 2 * k : -1;
+            return k < NBLK / 8 ? NBLK / 2 + cw + NCONV * k : -1;
+          };
+          auto coords = [&](int blk, int& m, int& cc) {
+            const int it = blk & 1, cs = (blk >> 1) % (NC / 32), rb = (blk >> 1) / (NC / 32);
+            const int row = (lane >> 1) & 7, hb16 = lane & 1, j = (row + 2 * (lane >> 4) + it) & 3;
+            m = 8 * rb + row;
+            cc = 32 * cs + 8 * j + 4 * hb16;
+          };
           float4 v[NBM];
 #pragma unroll
           for (int k = 0; k < NBM; ++k) {
-            const int blk = cw + k * NCW;
-            const int rb = blk / (NC / 32), cs = blk % (NC / 32);
-            const int m = 4 * rb + (lane >> 3), cc = 32 * cs + 4 * (lane & 7);
-            if (blk < NBLK) v[k] = *reinterpret_cast<const float4*>(st + (m * NC + cc) * 4);
+            const int blk = blk_of(k);
+            int m, cc;
+            coords(blk, m, cc);
+            if (blk >= 0) v[k] = *reinterpret_cast<const float4*>(st + (m * NC + cc) * 4);
             else v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
           }
           named_sync(BAR_CONV, 32 * NCW);  // all raw reads done before in-place writes
@@ -561,10 +675,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
           const float2 s2 = make_float2(sz, sz);
 #pragma unroll
           for (int k = 0; k < NBM; ++k) {
-            const int blk = cw + k * NCW;
-            if (blk >= NBLK || p.dbg == 3) continue;  // dbg 3: timing without conversion
-            const int rb = blk / (NC / 32), cs = blk % (NC / 32);
-            const int m = 4 * rb + (lane >> 3), cc = 32 * cs + 4 * (lane & 7);
+            const int blk = blk_of(k);
+            if (blk < 0 || (p.dbg & 4)) continue;  // dbg & 4: timing without conversion
+            int m, cc;
+            coords(blk, m, cc);
             const float2 a = __fmul2_rn(make_float2(v[k].x, v[k].y), s2);
             const float2 bq = __fmul2_rn(make_float2(v[k].z, v[k].w), s2);
             const __half2 ha = __float22half2_rn(a), hb = __float22half2_rn(bq);
@@ -576,9 +690,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
             *reinterpret_cast<uint2*>(st + G::ZT + off) = make_uint2(h2u(la), h2u(lb));
           }
           fence_async_smem();
-          named_sync(BAR_CONV, 32 * NCW);
+          if (XL_CONV_ARRIVE_ALL) {  // one arrival per converter warp, no CTA-wide wait
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm->conv_full[s]);
+          } else {
+            named_sync(BAR_CONV, 32 * NCW);
+            if (warp == 0 && lane == 0) mbar_arrive(&sm->conv_full[s]);
+          }
           if (warp == 0 && lane == 0) {
-            mbar_arrive(&sm->conv_full[s]);
             item_stamp(i, 2);
             if (pass == 0 && c == nch - 1) {
               sm->sz_slot[par] = sz;
@@ -588,7 +707,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
             if (c == nch - 1) stamp(kc, 25 + 2 * pass);
           }
           // W^T epilogue of the previous chunk overlaps this chunk's MMAs
-          if (pass == 1 && epi && c >= 1) epilogue(bcur, c - 1, kc);
+          if (pass == 1 && epi && c >= 1) {
+            if (warp == 0 && lane == 0) item_stamp(i - 1, 4);
+            epilogue(bcur, c - 1, kc);
+            if (warp == 0 && lane == 0) item_stamp(i - 1, 5);
+          }
       }
       if (pass == 1 && epi) {
         epilogue(bcur, nch - 1, kc);
@@ -606,6 +729,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
        if (pass == 0) {
         // the TMEM Gram accumulator is free once the math warps built A(k-1)
         if (k >= 1) mbar_wait(&sm->gram_free, (k - 1) & 1);
+        // ... and the W epilogues that borrowed the Gram columns have drained them
+        if (G::WB_GRAM && wuse[1] >= 1) mbar_wait(&sm->wfree[1], (wuse[1] - 1) & 1);
         for (int c = 0; c < nch; ++c, ++i) {  // Gram
           const int s = i % NS;
           mbar_wait(&sm->conv_full[s], (i / NS) & 1);
@@ -614,6 +739,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
           const uint32_t zh = su32(ring + s * G::SB), zl = zh + G::ZT;
 #pragma unroll
           for (int ks = 0; ks < G::CH / 16; ++ks) {
+            if (p.dbg & 16) break;
             const uint64_t dh = sdesc(zh + 2 * ks * G::CMA, G::CMA, 128);
             const uint64_t dl = sdesc(zl + 2 * ks * G::CMA, G::CMA, 128);
             mma(tmem + G::T_GRAM, dh, dh, G::ID_GRAM, (c | ks) != 0);
@@ -633,7 +759,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
         commit(&sm->xe_consumed);  // smem Xe may now be overwritten by A(k+1)
         for (int c = 0; c < nch; ++c, ++i, ++wc) {  // W^T = Xe^T Z^T
           const int s = i % NS;
-          const int j = wc % G::NWB;
+          const int j = G::wsel(c, wc);
+          // first borrow of the Gram columns: A(k+1) must have been built from them
+          if (G::WB_GRAM && c == XL_WB_START && (int64_t)k + 1 < nb) mbar_wait(&sm->gram_free, (k + 1) & 1);
           if (wuse[j] >= 1) mbar_wait(&sm->wfree[j], (wuse[j] - 1) & 1);
           mbar_wait(&sm->conv_full[s], (i / NS) & 1);
           tc_after();
@@ -656,7 +784,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
       });
     }
   } else if (warp < NCONV + NMATH) {
+#if XL_EPI_WARPS
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");
+#endif
     math_role<KU>(p, sm, aeh, ael, pbh, pbl, tmem, nch);
+  } else if (XL_EPI_WARPS && warp >= W_EPI0) {
+    // ------------------------------------------ W^T epilogue warpgroup ------
+    uint32_t wcv = 0, wuse_e[2] = {0, 0};
+    for_items([&](uint32_t kc, int pass, int64_t bcur) {
+      if (pass != 1) return;
+      for (int c = 0; c < nch; ++c, ++wcv) {
+        const uint32_t j = G::wsel(c, wcv);
+        w_epilogue<KU>(p, sm, tmem, bcur, c, j, wuse_e[j] & 1, kc & 1);
+        ++wuse_e[j];
+      }
+      if (warp == W_EPI0 && lane == 0) stamp(kc, 4);
+    });
   }
   __syncthreads();
   if (warp == 0) {
@@ -700,21 +843,22 @@ int launch_fused(int dtype, int method, int variant, const void* H, int64_t B, i
   (void)dtype;
   tc::Params p{(const float2*)H, B, M, xi, xi_per_batch, power, sigma2, T, method, variant,
                (float2*)W, (float2*)F, beta, gamma, sum_se, (float2*)X, status, (float2*)dbg_gram, 0,
-               nullptr, 8};
+               nullptr, 0};  // l2mode 0: evict_first loads, st.global.cs W stores
   if (const char* e = getenv("XL_FUSED_DEBUG")) p.dbg = atoi(e);
-  if (const char* e = getenv("XL_FUSED_KEEP16")) p.keep16 = atoi(e);
+  if (const char* e = getenv("XL_FUSED_L2")) p.l2mode = atoi(e);
   // XL_FUSED_TRACE=1: synchronous per-phase clock64 dump of CTA 0 to stderr
   // (development aid; never set in production runs).
   static long long* trace = nullptr;
   const bool tracing = getenv("XL_FUSED_TRACE") != nullptr;
+  if (tracing) p.trace_k0 = atoi(getenv("XL_FUSED_TRACE")) > 1 ? atoi(getenv("XL_FUSED_TRACE")) - 1 : 0;
   if (tracing) {
-    if (!trace) cudaMalloc(&trace, 512 * sizeof(long long));
-    cudaMemsetAsync(trace, 0, 512 * sizeof(long long), st);
+    if (!trace) cudaMalloc(&trace, 1024 * sizeof(long long));
+    cudaMemsetAsync(trace, 0, 1024 * sizeof(long long), st);
     p.trace = trace;
   }
   int rc = K == 64 ? launch_k<64>(p, st) : K == 32 ? launch_k<32>(p, st) : launch_k<16>(p, st);
   if (tracing && rc == XL_SUCCESS) {
-    long long h[512];
+    long long h[1024];
     cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     const long long t0 = h[16];
@@ -725,14 +869,16 @@ int launch_fused(int dtype, int method, int variant, const void* H, int64_t B, i
                                     "prod:first", "prod:G_last", "prod:W_last", "beta:sx",
                                     "beta:issue", "beta:gx", "beta:fro2", "beta:gamma",
                                     "conv:G_first", "conv:G_last", "conv:W_first", "conv:W_last",
-                                    0, 0, 0, 0};
+                                    "xe:built", "xe:synced", 0, 0};
     for (int kk = 0; kk < 8; ++kk)
       for (int s = 0; s < 32; ++s)
         if (names[s] && h[kk * 32 + s]) fprintf(stderr, "trace b%d %-18s %10lld\n", kk, names[s], h[kk * 32 + s] - t0);
-    for (int ii = 0; ii < 64; ++ii)
-      if (h[256 + ii * 4])
-        fprintf(stderr, "item %3d issue %9lld landed %9lld converted %9lld mma %9lld\n", ii + 64,
-                h[256 + ii * 4] - t0, h[256 + ii * 4 + 1] - t0, h[256 + ii * 4 + 2] - t0, h[256 + ii * 4 + 3] - t0);
+    for (int ii = 0; ii < 64; ++ii) {
+      const long long* e = h + 256 + ii * 8;
+      if (e[0])
+        fprintf(stderr, "item %3d issue %9lld landed %9lld converted %9lld mma %9lld epi %9lld %9lld\n", ii + 64,
+                e[0] - t0, e[1] - t0, e[2] - t0, e[3] - t0, e[4] ? e[4] - t0 : 0, e[5] ? e[5] - t0 : 0);
+    }
   }
   return rc;
 }
