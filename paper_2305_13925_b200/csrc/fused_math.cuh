@@ -90,6 +90,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
         float v[16];
         tmem_ld16(tl + G::T_GRAM + h * HC + c0, v);
         tmem_wait_ld();
+        uint32_t hw[8], lw[8];
 #pragma unroll
         for (int jp = 0; jp < 8; ++jp) {
           const float g0 = v[2 * jp], g1 = v[2 * jp + 1];
@@ -102,11 +103,14 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
             const float inv = 1.0f / (sz * sz);
             p.dbgA[(b * KU + kr) * KU + jc] = make_float2(ar * inv, ai * inv);
           }
-          uint32_t hw, lw;
-          split2((odd ? ai : ar) * sa, (odd ? ar : -ai) * sa, hw, lw);
-          const int o = boff<KU>(r, 2 * jc);
-          *reinterpret_cast<uint32_t*>(aeh + o) = hw;
-          *reinterpret_cast<uint32_t*>(ael + o) = lw;
+          split2((odd ? ai : ar) * sa, (odd ? ar : -ai) * sa, hw[jp], lw[jp]);
+        }
+        // two whole 16-B core-matrix rows per thread (8-lane phases contiguous)
+#pragma unroll
+        for (int q4 = 0; q4 < 2; ++q4) {
+          const int o = boff<KU>(r, h * HC + c0 + 8 * q4);
+          *reinterpret_cast<uint4*>(aeh + o) = make_uint4(hw[4 * q4], hw[4 * q4 + 1], hw[4 * q4 + 2], hw[4 * q4 + 3]);
+          *reinterpret_cast<uint4*>(ael + o) = make_uint4(lw[4 * q4], lw[4 * q4 + 1], lw[4 * q4 + 2], lw[4 * q4 + 3]);
         }
       }
     }

@@ -271,11 +271,12 @@ struct Geo {
   static constexpr int ZT = SB / 2;          // one fp16 tile
   static constexpr int CMA = NC * 16;        // antenna-group (core row group) stride
   static constexpr int OFF_AE = NS * SB + 2048;   // + slack for M-padded Gram reads
-  // Math-written operand tiles (A'', G'', Xe, P / X columns) use padded core
-  // strides so per-row / per-column register stores are bank-conflict free:
-  // K-direction core stride LBOP = 144 B, 8-row group stride SBOP = 32 mod 128.
-  static constexpr int LBOP = 144;
-  static constexpr int SBOP = (NC / 8) * LBOP + 32;
+  // Math-written operand tiles (A'', G'', Xe, P / X columns) use a padded
+  // K-direction core stride LBOP = 160 B (== 32 mod 128): the per-column
+  // 16-bit stores of P / X and the paired-row 32-bit stores of Xe then hit
+  // distinct banks; A'' rows are written as whole 16-B core-matrix rows.
+  static constexpr int LBOP = 160;
+  static constexpr int SBOP = (NC / 8) * LBOP;
   static constexpr int AEPART = 16 * SBOP;        // A operand padded to 128 rows
   static constexpr int OFF_PB = OFF_AE + 2 * AEPART;
   static constexpr int PBPART = (KU / 8) * SBOP;
