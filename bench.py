@@ -312,16 +312,22 @@ def main():
         achieved, peak, unit = B * bytes_per / kern_s / 1e9, hbm, "GB/s"
     else:
         achieved, peak, unit = B * flops_per / kern_s / 1e12, tc_peak, "TFLOP/s"
+    # DRAM bytes per launch from the committed ncu --set full capture
+    # (bytes per precoder there x this launch's realizations), or null
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(f"{a.config}:{a.method}")
+            rec = json.load(f).get(f"{a.config}:{a.method}")
+        if rec and tc:
+            traffic = rec["dram_bytes_per_precoder"] * B
     roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
             "frac": achieved / peak, "traffic": traffic,
             "peak_source": f"{peak_src} (MEASURED_PEAKS.json)" if peak_src == "measured" else peak_src,
             "kernel": "xl_rzf fused precoder call" + (" (tcgen05)" if tc else " (SIMT path)"),
             "kernel_ms": kern_ms, "bytes_per_precoder": bytes_per,
+            "algorithmic_bytes_per_launch": B * bytes_per,
+            "traffic_source": "profiles/traffic.json" if traffic is not None else None,
             "flops_per_precoder": flops_per}
 
     cpu = None
