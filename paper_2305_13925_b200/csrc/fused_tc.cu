@@ -227,9 +227,6 @@ __device__ __forceinline__ float warp_transpose_reduce(float (&v)[N]) {
 }
 
 // ----------------------------------------------------------- geometry ----
-#ifndef XL_WSPLIT
-#define XL_WSPLIT 0           // W pass: extra converter warps take half the blocks
-#endif
 #ifndef XL_PF
 #define XL_PF 0               // L2 prefetch distance in 32 KB ring items (0: off)
 #endif
@@ -238,9 +235,6 @@ __device__ __forceinline__ float warp_transpose_reduce(float (&v)[N]) {
 #endif
 #ifndef XL_WB_START
 #define XL_WB_START 4         // first W chunk that may use them (A(k+1) built by then)
-#endif
-#ifndef XL_CONV_ARRIVE_ALL
-#define XL_CONV_ARRIVE_ALL 1  // conv_full: per-warp arrivals instead of a CTA barrier
 #endif
 constexpr int NCONV = 4, NMATH = 8;
 constexpr int W_MMA = NCONV + NMATH, W_PROD = W_MMA + 1;
@@ -268,8 +262,7 @@ struct Geo {
   static constexpr int CH = XL_CH;           // antennas per ring stage
   static constexpr int NS = (3 * 64) / CH;   // ring depth (96 KB ring for K = 64)
   static constexpr int SB = CH * NC * 4;     // stage bytes (raw fp32 == hi + lo fp16 tiles)
-  static constexpr int ZT = SB / 2;          // one fp16 tile
-  static constexpr int CMA = NC * 16;        // antenna-group (core row group) stride
+  static constexpr int CMA = NC * 16;        // one fp16 tile of an 8-antenna group (hi or lo)
   static constexpr int OFF_AE = NS * SB + 2048;   // + slack for M-padded Gram reads
   // Math-written operand tiles (A'', G'', Xe, P / X columns) use a padded
   // K-direction core stride LBOP = 160 B (== 32 mod 128): the per-column
@@ -483,7 +476,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sm->raw_full[s], 1);
-      mbar_init(&sm->conv_full[s], XL_CONV_ARRIVE_ALL ? NCW : 1);
+      mbar_init(&sm->conv_full[s], NCW);  // one arrival per converter warp
       mbar_init(&sm->stage_free[s], 1);
     }
     mbar_init(&sm->gram_full, 1);
@@ -625,42 +618,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
           uint8_t* st = ring + s * G::SB;
           mbar_wait(&sm->raw_full[s], (i / NS) & 1);
           if (warp == 0 && lane == 0) item_stamp(i, 1);
-          // Half-blocks of 8 antennas x 32 components (two per 8x32 block),
-          // round-robin over converter warps.  Lane -> (row, 16-B half b,
-          // core matrix j) is chosen so both the float4 reads (8-lane phases:
-          // distinct (j, b)) and the uint2 core-matrix writes (16-lane
-          // phases: distinct (row, b)) are bank-conflict free.
-          // G pass: round-robin over the NCW warps.  W pass: warps 0-3 also
-          // run the W^T epilogue, so the two extra warps take half the blocks.
-          constexpr int NBLK = (G::CH / 8) * (NC / 32) * 2, NBG = (NBLK + NCW - 1) / NCW;
-          static_assert(NCW == NCONV + 2, "W-pass block split assumes two extra converter warps");
-          constexpr int NBM = (XL_WSPLIT && NBLK / 4 > NBG) ? NBLK / 4 : NBG;
-          auto blk_of = [&](int k) -> int {
-            if (pass == 0 || !XL_WSPLIT) return cw + k * NCW < NBLK ? cw + k * NCW : -1;
-            if (cw >= NCONV) return k < NBLK / 4 ? (cw - NCONV) + 2 * k : -1;
-            return k < NBLK / 8 ? NBLK / 2 + cw + NCONV * k : -1;
-          };
-          auto coords = [&](int blk, int& m, int& cc) {
-            const int it = blk & 1, cs = (blk >> 1) % (NC / 32), rb = (blk >> 1) / (NC / 32);
-            const int row = (lane >> 1) & 7, hb16 = lane & 1, j = (row + 2 * (lane >> 4) + it) & 3;
-            m = 8 * rb + row;
+          // Group-interleaved stage: antenna group g (8 antennas) holds its raw
+          // fp32 rows at [GS g, GS (g+1)), GS = 8 NC 4 = 2 CMA, and after
+          // conversion its fp16 hi core matrices at GS g and lo at GS g + CMA,
+          // i.e. the same bytes: each warp converts its own groups in place, no
+          // CTA-wide barrier.  Warps 0-3 (which also run the W^T epilogue) take
+          // one group, the two extra warps two.  Lane -> (row, 16-B half,
+          // core matrix j) keeps the float4 reads (8-lane phases: distinct
+          // (j, half)) and the uint2 writes (16-lane phases: distinct
+          // (row, half)) bank-conflict free.
+          constexpr int NG = G::CH / 8, GS = 2 * G::CMA, NIT = NC / 16;
+          static_assert(NCW == NCONV + 2 && NG == NCONV + 2 * (NCW - NCONV), "group split");
+          const int g0 = cw < NCONV ? cw : NCONV + 2 * (cw - NCONV);
+          const int ng = cw < NCONV ? 1 : 2;
+          auto coords = [&](int it, int& row, int& cc) {
+            const int cs = it >> 1, ih = it & 1;
+            row = (lane >> 1) & 7;
+            const int hb16 = lane & 1, j = (row + 2 * (lane >> 4) + ih) & 3;
             cc = 32 * cs + 8 * j + 4 * hb16;
           };
-          float4 v[NBM];
-#pragma unroll
-          for (int k = 0; k < NBM; ++k) {
-            const int blk = blk_of(k);
-            int m, cc;
-            coords(blk, m, cc);
-            if (blk >= 0) v[k] = *reinterpret_cast<const float4*>(st + (m * NC + cc) * 4);
-            else v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-          named_sync(BAR_CONV, 32 * NCW);  // all raw reads done before in-place writes
-          if (pass == 0 && !have) {
+          if (pass == 0 && !have) {  // until the first non-zero chunk: CTA-wide max for the scale
             float mx = 0.0f;
+            for (int gi = 0; gi < ng; ++gi) {
+              const uint8_t* gb = st + (g0 + gi) * GS;
 #pragma unroll
-            for (int k = 0; k < NBM; ++k)
-              mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[k].x), fabsf(v[k].y)), fmaxf(fabsf(v[k].z), fabsf(v[k].w))));
+              for (int it = 0; it < NIT; ++it) {
+                int row, cc;
+                coords(it, row, cc);
+                const float4 x = *reinterpret_cast<const float4*>(gb + (row * NC + cc) * 4);
+                mx = fmaxf(mx, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
+              }
+            }
             mx = warp_max(mx);
             if (lane == 0) sm->conv_red[cw] = mx;
             named_sync(BAR_CONV, 32 * NCW);
@@ -674,30 +662,35 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
             }
           }
           const float2 s2 = make_float2(sz, sz);
+          for (int gi = 0; gi < ng; ++gi) {
+            uint8_t* gb = st + (g0 + gi) * GS;
+            float4 v[NIT];
 #pragma unroll
-          for (int k = 0; k < NBM; ++k) {
-            const int blk = blk_of(k);
-            if (blk < 0 || (p.dbg & 4)) continue;  // dbg & 4: timing without conversion
-            int m, cc;
-            coords(blk, m, cc);
-            const float2 a = __fmul2_rn(make_float2(v[k].x, v[k].y), s2);
-            const float2 bq = __fmul2_rn(make_float2(v[k].z, v[k].w), s2);
-            const __half2 ha = __float22half2_rn(a), hb = __float22half2_rn(bq);
-            const float2 ra = __fadd2_rn(a, make_float2(-__low2float(ha), -__high2float(ha)));
-            const float2 rbq = __fadd2_rn(bq, make_float2(-__low2float(hb), -__high2float(hb)));
-            const __half2 la = __float22half2_rn(ra), lb = __float22half2_rn(rbq);
-            const int off = (m >> 3) * G::CMA + (cc >> 3) * 128 + (m & 7) * 16 + (cc & 7) * 2;
-            *reinterpret_cast<uint2*>(st + off) = make_uint2(h2u(ha), h2u(hb));
-            *reinterpret_cast<uint2*>(st + G::ZT + off) = make_uint2(h2u(la), h2u(lb));
+            for (int it = 0; it < NIT; ++it) {
+              int row, cc;
+              coords(it, row, cc);
+              v[it] = *reinterpret_cast<const float4*>(gb + (row * NC + cc) * 4);
+            }
+            __syncwarp();  // the whole group is in registers before it is overwritten
+            if (p.dbg & 4) continue;  // dbg & 4: timing without conversion
+#pragma unroll
+            for (int it = 0; it < NIT; ++it) {
+              int row, cc;
+              coords(it, row, cc);
+              const float2 a = __fmul2_rn(make_float2(v[it].x, v[it].y), s2);
+              const float2 bq = __fmul2_rn(make_float2(v[it].z, v[it].w), s2);
+              const __half2 ha = __float22half2_rn(a), hb = __float22half2_rn(bq);
+              const float2 ra = __fadd2_rn(a, make_float2(-__low2float(ha), -__high2float(ha)));
+              const float2 rbq = __fadd2_rn(bq, make_float2(-__low2float(hb), -__high2float(hb)));
+              const __half2 la = __float22half2_rn(ra), lb = __float22half2_rn(rbq);
+              const int off = (cc >> 3) * 128 + row * 16 + (cc & 7) * 2;
+              *reinterpret_cast<uint2*>(gb + off) = make_uint2(h2u(ha), h2u(hb));
+              *reinterpret_cast<uint2*>(gb + G::CMA + off) = make_uint2(h2u(la), h2u(lb));
+            }
           }
           fence_async_smem();
-          if (XL_CONV_ARRIVE_ALL) {  // one arrival per converter warp, no CTA-wide wait
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm->conv_full[s]);
-          } else {
-            named_sync(BAR_CONV, 32 * NCW);
-            if (warp == 0 && lane == 0) mbar_arrive(&sm->conv_full[s]);
-          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm->conv_full[s]);  // one arrival per converter warp
           if (warp == 0 && lane == 0) {
             item_stamp(i, 2);
             if (pass == 0 && c == nch - 1) {
@@ -737,12 +730,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
           mbar_wait(&sm->conv_full[s], (i / NS) & 1);
           if (c == 0) stamp(k, 8);
           tc_after();
-          const uint32_t zh = su32(ring + s * G::SB), zl = zh + G::ZT;
+          // group-interleaved stage: antenna-group (K) stride GS = 2 CMA, lo at + CMA
+          const uint32_t zh = su32(ring + s * G::SB), zl = zh + G::CMA;
 #pragma unroll
           for (int ks = 0; ks < G::CH / 16; ++ks) {
             if (p.dbg & 16) break;
-            const uint64_t dh = sdesc(zh + 2 * ks * G::CMA, G::CMA, 128);
-            const uint64_t dl = sdesc(zl + 2 * ks * G::CMA, G::CMA, 128);
+            const uint64_t dh = sdesc(zh + 4 * ks * G::CMA, 2 * G::CMA, 128);
+            const uint64_t dl = sdesc(zl + 4 * ks * G::CMA, 2 * G::CMA, 128);
             mma(tmem + G::T_GRAM, dh, dh, G::ID_GRAM, (c | ks) != 0);
             mma(tmem + G::T_GRAM, dh, dl, G::ID_GRAM, 1);
             mma(tmem + G::T_GRAM, dl, dh, G::ID_GRAM, 1);
@@ -766,12 +760,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
           if (wuse[j] >= 1) mbar_wait(&sm->wfree[j], (wuse[j] - 1) & 1);
           mbar_wait(&sm->conv_full[s], (i / NS) & 1);
           tc_after();
-          const uint32_t zh = su32(ring + s * G::SB), zl = zh + G::ZT;
+          const uint32_t zh = su32(ring + s * G::SB), zl = zh + G::CMA;
           const uint32_t d = tmem + (j ? G::T_W1 : G::T_W0);
           const uint32_t txe = tmem + G::T_XE;
 #pragma unroll
           for (int ks = 0; ks < NC / 16; ++ks) {
-            const uint64_t dzh = sdesc(zh + 256 * ks, 128, G::CMA), dzl = sdesc(zl + 256 * ks, 128, G::CMA);
+            const uint64_t dzh = sdesc(zh + 256 * ks, 128, 2 * G::CMA), dzl = sdesc(zl + 256 * ks, 128, 2 * G::CMA);
             mma_ts(d, txe + 8 * ks, dzh, G::ID_W, ks != 0);
             mma_ts(d, txe + 8 * ks, dzl, G::ID_W, 1);
             mma_ts(d, txe + 64 + 8 * ks, dzh, G::ID_W, 1);
