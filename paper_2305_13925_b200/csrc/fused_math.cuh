@@ -47,7 +47,10 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
   };
   uint32_t k = 0, nq = 0, wc = 0;
   uint32_t wuse[2] = {0, 0};
-  for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++k) {
+  for (;; ++k) {
+    mbar_wait(&sm->bq_full[k & 3], (k >> 2) & 1);  // realization claimed by the producer
+    const int64_t b = sm->bq[k & 3];
+    if (b < 0) break;
     const double alpha = p.xi_b ? p.xi_b[b] : p.xi;
     mbar_wait(&sm->scale_ready, k & 1);
     const float sz = sm->sz_slot[k & 1];
@@ -411,45 +414,38 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
   (void)wuse;
 }
 
-// W^T epilogue of one chunk, run by the four warps of lane quadrants 0-3
-// (converter warps 0-3, or the epilogue warpgroup with XL_EPI_WARPS): thread
-// = output component c2 = 32 q + lane, CH antennas, read from TMEM in EPI_PART
-// column pieces (the epilogue warpgroup runs with 64 registers).
+// W^T epilogue of one chunk, run by converter warps 0-3 (TMEM lane quadrant =
+// warp): thread = output component c2 = 32 q + lane, CH antennas; 128-B
+// coalesced streaming stores per antenna.  (Staging the tile in the consumed
+// ring stage for one bulk store measured 6% slower: it holds the stage longer.)
 template <int KU>
 __device__ __forceinline__ void w_epilogue(const Params& p, Small* sm, uint32_t tmem, int64_t b, int c,
                                            uint32_t j, uint32_t parity, uint32_t kpar) {
   using G = Geo<KU>;
   constexpr int NC = G::NC, CH = G::CH;
-  constexpr int PART = XL_EPI_WARPS ? 32 : CH;
-  static_assert(CH % PART == 0, "epilogue pieces");
-  const int warp = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;  // lane quadrant
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;  // warps 0-3 = lane quadrants
   const int r = 32 * warp + lane;
   const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16) + (j ? G::T_W1 : G::T_W0);
   mbar_wait(&sm->wfull[j], parity);
   // the math warps published the scales before xe_ready, which these MMAs awaited
   const float wscale = sm->wsc[kpar][0], fscale = sm->wsc[kpar][1];
   tc_after();
-  const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH) * NC + r;
-  float* wp = reinterpret_cast<float*>(p.W) + o0;
-  float* fp = p.F ? reinterpret_cast<float*>(p.F) + o0 : nullptr;
-#pragma unroll 1
-  for (int a0 = 0; a0 < CH; a0 += PART) {
-    float d[PART];
-    if (32 * warp < NC) {
-      tmem_ld<PART>(tl + a0, d);
-      tmem_wait_ld();
-    }
-    if (a0 + PART == CH) {  // accumulator drained: the next W MMAs may overwrite it
-      tc_before();
-      mbar_arrive(&sm->wfree[j]);
-    }
-    if (r < NC && !(p.dbg & 8)) {  // dbg & 8: timing without the W stores
+  float d[CH];
+  if (32 * warp < NC) {
+    tmem_ld<CH>(tl, d);
+    tmem_wait_ld();
+  }
+  tc_before();
+  mbar_arrive(&sm->wfree[j]);
+  if (r < NC && !(p.dbg & 8)) {  // dbg & 8: timing without the W stores
+    const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH) * NC + r;
+    float* wp = reinterpret_cast<float*>(p.W) + o0;
 #pragma unroll
-      for (int a = 0; a < PART; ++a) __stcs(wp + (a0 + a) * NC, d[a] * wscale);
-      if (fp) {
+    for (int a = 0; a < CH; ++a) __stcs(wp + a * NC, d[a] * wscale);
+    if (p.F) {
+      float* fp = reinterpret_cast<float*>(p.F) + o0;
 #pragma unroll
-        for (int a = 0; a < PART; ++a) __stcs(fp + (a0 + a) * NC, d[a] * fscale);
-      }
+      for (int a = 0; a < CH; ++a) __stcs(fp + a * NC, d[a] * fscale);
     }
   }
 }

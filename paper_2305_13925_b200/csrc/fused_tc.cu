@@ -39,6 +39,7 @@
 #include <stdlib.h>
 
 #include "xl_common.cuh"
+#include <algorithm>
 #include "fused_tc.cuh"
 
 namespace xl {
@@ -103,9 +104,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     if (++spins > (1u << 24)) asm volatile("trap;");
   } while (!done);
-}
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t hint) {
@@ -227,22 +225,9 @@ __device__ __forceinline__ float warp_transpose_reduce(float (&v)[N]) {
 }
 
 // ----------------------------------------------------------- geometry ----
-#ifndef XL_PF
-#define XL_PF 0               // L2 prefetch distance in 32 KB ring items (0: off)
-#endif
-#ifndef XL_WB_GRAM
-#define XL_WB_GRAM 0          // Gram TMEM columns double-buffer the W accumulator
-#endif
-#ifndef XL_WB_START
-#define XL_WB_START 4         // first W chunk that may use them (A(k+1) built by then)
-#endif
 constexpr int NCONV = 4, NMATH = 8;
 constexpr int W_MMA = NCONV + NMATH, W_PROD = W_MMA + 1;
-#ifndef XL_EPI_WARPS
-#define XL_EPI_WARPS 0  // 1: a fifth warpgroup (warps 16-19) runs the W^T epilogue
-#endif
-constexpr int NTHREADS = XL_EPI_WARPS ? 640 : 512;  // 4-5 warpgroups (setmaxnreg granularity)
-constexpr int W_EPI0 = 16;                          // first epilogue warp (lane quadrant 0)
+constexpr int NTHREADS = 512;  // 16 warps = 4 warpgroups (setmaxnreg granularity)
 constexpr int BAR_CONV = 1, BAR_MATH = 2;
 // Converter warps: 0..3 plus the two spare warps of warpgroup 3 (14, 15).
 #ifndef XL_NCW
@@ -288,18 +273,10 @@ struct Geo {
   // by tcgen05.cp so the MMAs re-read only their B operand from smem.
   static constexpr int NWB = (CH <= 32) ? 2 : 1;  // W accumulator buffers at T_W0
   static_assert(NWB * CH <= 64, "W accumulator columns");
-  // With one buffer at T_W0, the Gram columns serve as the second W buffer
-  // while W(k) streams: G(k+1) is consumed (A(k+1) built) early in W(k) and
-  // G(k+2) starts only after W(k).
-  static constexpr bool WB_GRAM = XL_WB_GRAM && NWB == 1 && CH <= 128;
-  static constexpr uint32_t T_GRAM = 0, T_Q = 128, T_W0 = 192, T_X = 256, T_R = 320, T_XE = 384;
-  static constexpr uint32_t T_W1 = NWB == 2 ? 192 + CH : T_GRAM;
-  // W accumulator buffer of chunk c (wc = running W chunk count)
-  __device__ static int wsel(int c, uint32_t wc) {
-    if (NWB == 2) return (int)(wc & 1);
-    if (!WB_GRAM) return 0;
-    return (c >= XL_WB_START && ((c - XL_WB_START) & 1) == 0) ? 1 : 0;
-  }
+  static constexpr uint32_t T_GRAM = 0, T_Q = 128, T_W0 = 192, T_W1 = 192 + CH * (NWB - 1), T_X = 256,
+                            T_R = 320, T_XE = 384;
+  // W accumulator buffer of the wc-th W chunk
+  __device__ static int wsel(uint32_t wc) { return (int)(wc % NWB); }
 };
 
 struct Params {
@@ -323,6 +300,7 @@ struct Params {
   long long* trace;  // optional per-phase clock64 stamps of CTA 0 (XL_FUSED_TRACE)
   int l2mode;        // L2 policy of the G-pass loads: 0 evict_first, 1 normal, 2 evict_last
   int trace_k0;      // first traced realization of CTA 0 (XL_FUSED_TRACE=k0+1)
+  int* counter;      // realization claim counter (workspace, zeroed per launch)
 };
 
 // Element (row n, col k) of a padded n x NC K-major operand tile (core rows = n).
@@ -341,6 +319,8 @@ struct Small {
   uint64_t gram_full, q_full, xe_ready, scale_ready, gram_free;
   uint64_t wfull[2], wfree[2];
   uint64_t xe_consumed;  // Xe(b) copied smem -> TMEM: the smem region may hold A(b+1)
+  uint64_t bq_full[4];   // realization index of pipeline slot k & 3 published
+  long long bq[4];
   float wsc[2][2];       // per realization parity: W scale, F scale (for the converters' epilogue)
   uint32_t tmem_slot;
   int pad0;
@@ -485,6 +465,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
     mbar_init(&sm->scale_ready, 1);
     mbar_init(&sm->gram_free, 1);
     mbar_init(&sm->xe_consumed, 1);
+    for (int q = 0; q < 4; ++q) mbar_init(&sm->bq_full[q], 1);
     for (int j = 0; j < 2; ++j) {
       mbar_init(&sm->wfull[j], 1);
       mbar_init(&sm->wfree[j], 32 * NCONV);  // converter warps 0-3 run the W epilogue
@@ -499,6 +480,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
   __syncthreads();
   tc_after();
   const uint32_t tmem = sm->tmem_slot;
+  auto cta_stamp = [&](int slot) {  // per-CTA globaltimer / clock64 (XL_FUSED_TRACE)
+    if (p.trace && threadIdx.x == 0 && blockIdx.x < 256) {
+      uint64_t ns;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+      p.trace[1024 + blockIdx.x * 4 + 2 * slot] = (long long)ns;
+      p.trace[1024 + blockIdx.x * 4 + 2 * slot + 1] = clock64();
+    }
+  };
+  cta_stamp(0);
 
   // phase stamps (CTA 0, first 8 realizations) for pipeline analysis
   // per ring item i in [64, 128): 0 = load issued, 1 = raw landed, 2 = converted, 3 = MMAs issued
@@ -516,15 +506,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
 #define XL_REG_MATH 176
 #endif
   static_assert(128 * XL_REG_AUX + 128 * XL_REG_CONV + 256 * XL_REG_MATH <= 65536, "register budget");
-#if XL_EPI_WARPS
-  // 640 threads: the launch bound leaves 96 registers per thread; the math
-  // warpgroups take 128 (inside their branch, so ptxas allocates for it) from
-  // the other three.
-  // setmaxnreg.inc draws only on registers released by .dec: the math warps'
-  // +32 x 256 comes from WG0/WG3 (96 -> 80) and the epilogue WG (96 -> 64).
-  if (warp < NCONV || (warp >= NCONV + NMATH && warp < W_EPI0)) asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
-  if (warp >= W_EPI0) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
-#elif XL_USE_SETMAXNREG
+#if XL_USE_SETMAXNREG
   if (warp >= W_MMA) {  // warpgroup 3: MMA issuer, producer, 2 idle warps
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(XL_REG_AUX));
   } else if (warp < NCONV) {
@@ -534,17 +516,35 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
   }
 #endif
   // Stream order of ring items (software pipeline across this CTA's
-  // realizations k = 0..nb-1):  G(0), then for every k: G(k+1), W(k).
+  // realizations k = 0, 1, ...):  G(0), then for every k: G(k+1), W(k).
   // G(k+1) streams while the math warps run PCG(k); W(k) needs X(k).
-  const int64_t nb = p.B > (int64_t)blockIdx.x ? (p.B - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  // Realizations are claimed dynamically (atomic counter in the workspace):
+  // the producer claims b_k just before streaming G(k) and publishes it in
+  // the bq ring (4 slots: every role is within 2 realizations of the
+  // producer); b_k < 0 ends the sequence.  This evens out per-SM speed
+  // differences (static striding left an 11% spread of CTA end times).
+  const bool is_prod = (warp == W_PROD && lane == 0);
+  auto real_of = [&](uint32_t k) -> int64_t {  // b_k, or -1 past the end
+    if (is_prod) {
+      const int64_t b = (int64_t)atomicAdd(p.counter, 1);
+      sm->bq[k & 3] = b < p.B ? b : -1;
+      mbar_arrive(&sm->bq_full[k & 3]);
+    } else {
+      mbar_wait(&sm->bq_full[k & 3], (k >> 2) & 1);
+    }
+    return sm->bq[k & 3];
+  };
   auto for_items = [&](auto&& body) {  // body(kk, pass, b)
-    for (int64_t k = 0; k < nb; ++k)
-      for (int part = (k == 0 ? 0 : 1); part < 3; ++part) {
-        if (part == 1 && k + 1 >= nb) continue;
-        if (part == 2 && (p.dbg & 3)) continue;
-        const int64_t kk = part == 1 ? k + 1 : k;
-        body((uint32_t)kk, part == 2 ? 1 : 0, (int64_t)blockIdx.x + kk * gridDim.x);
-      }
+    int64_t bk = real_of(0);
+    if (bk < 0) return;
+    body(0u, 0, bk);
+    for (uint32_t k = 0;; ++k) {
+      const int64_t bn = real_of(k + 1);
+      if (bn >= 0) body(k + 1, 0, bn);
+      if (!(p.dbg & 3)) body(k, 1, bk);
+      if (bn < 0) break;
+      bk = bn;
+    }
   };
   if (warp == W_PROD) {
     // ------------------------------------------------------ producer ------
@@ -553,33 +553,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
       const uint64_t pol_first = policy_evict_first();
       const uint64_t pol_g = (p.l2mode & 3) == 0 ? pol_first : (p.l2mode & 3) == 1 ? policy_evict_normal()
                                                                                   : policy_evict_last();
-      // L2 prefetch cursor XL_PF items ahead of the TMA loads (same order as
-      // for_items): the smem ring is too small to cover HBM latency on its
-      // own, so the loads that follow hit L2.
-      int64_t pk = 0;
-      int ppart = 0, pc = 0;
-      auto part_ok = [&](int64_t k, int part) {
-        if (part == 0) return k == 0;
-        if (part == 1) return k + 1 < nb;
-        return !(p.dbg & 3);
-      };
-      auto prefetch_next = [&]() {
-        if (pk >= nb) return;
-        const int64_t kk = ppart == 1 ? pk + 1 : pk;
-        const int64_t bb = (int64_t)blockIdx.x + kk * gridDim.x;
-        bulk_prefetch_l2(reinterpret_cast<const char*>(p.H + bb * (int64_t)p.M * KU) + (int64_t)pc * G::SB, G::SB);
-        if (++pc < nch) return;
-        pc = 0;
-        do {
-          if (++ppart == 3) { ppart = 0; ++pk; }
-        } while (pk < nb && !part_ok(pk, ppart));
-      };
-      for (int q = 0; q < XL_PF; ++q) prefetch_next();
       for_items([&](uint32_t kk, int pass, int64_t b) {
         const char* Hb = reinterpret_cast<const char*>(p.H + b * (int64_t)p.M * KU);
         for (int c = 0; c < nch; ++c, ++i) {
           const int s = i % NS;
-          prefetch_next();
           if (i >= (uint32_t)NS) mbar_wait(&sm->stage_free[s], ((i / NS) - 1) & 1);
           item_stamp(i, 0);
           mbar_expect_tx(&sm->raw_full[s], G::SB);
@@ -601,9 +578,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
     int have_par[2] = {0, 0};
     uint32_t wcv = 0;                 // W chunk counter (same sequence as the MMA issuer)
     uint32_t wuse_c[2] = {0, 0};
-    const bool epi = !XL_EPI_WARPS && warp < NCONV;  // warps 0-3 also run the W^T epilogue
+    const bool epi = warp < NCONV;  // warps 0-3 also run the W^T epilogue
     auto epilogue = [&](int64_t b, int c, uint32_t kc) {
-      const uint32_t j = G::wsel(c, wcv);
+      const uint32_t j = G::wsel(wcv);
       w_epilogue<KU>(p, sm, tmem, b, c, j, wuse_c[j] & 1, kc & 1);
       ++wuse_c[j];
       ++wcv;
@@ -723,8 +700,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
        if (pass == 0) {
         // the TMEM Gram accumulator is free once the math warps built A(k-1)
         if (k >= 1) mbar_wait(&sm->gram_free, (k - 1) & 1);
-        // ... and the W epilogues that borrowed the Gram columns have drained them
-        if (G::WB_GRAM && wuse[1] >= 1) mbar_wait(&sm->wfree[1], (wuse[1] - 1) & 1);
         for (int c = 0; c < nch; ++c, ++i) {  // Gram
           const int s = i % NS;
           mbar_wait(&sm->conv_full[s], (i / NS) & 1);
@@ -754,9 +729,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
         commit(&sm->xe_consumed);  // smem Xe may now be overwritten by A(k+1)
         for (int c = 0; c < nch; ++c, ++i, ++wc) {  // W^T = Xe^T Z^T
           const int s = i % NS;
-          const int j = G::wsel(c, wc);
-          // first borrow of the Gram columns: A(k+1) must have been built from them
-          if (G::WB_GRAM && c == XL_WB_START && (int64_t)k + 1 < nb) mbar_wait(&sm->gram_free, (k + 1) & 1);
+          const int j = G::wsel(wc);
           if (wuse[j] >= 1) mbar_wait(&sm->wfree[j], (wuse[j] - 1) & 1);
           mbar_wait(&sm->conv_full[s], (i / NS) & 1);
           tc_after();
@@ -779,24 +752,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
       });
     }
   } else if (warp < NCONV + NMATH) {
-#if XL_EPI_WARPS
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");
-#endif
     math_role<KU>(p, sm, aeh, ael, pbh, pbl, tmem, nch);
-  } else if (XL_EPI_WARPS && warp >= W_EPI0) {
-    // ------------------------------------------ W^T epilogue warpgroup ------
-    uint32_t wcv = 0, wuse_e[2] = {0, 0};
-    for_items([&](uint32_t kc, int pass, int64_t bcur) {
-      if (pass != 1) return;
-      for (int c = 0; c < nch; ++c, ++wcv) {
-        const uint32_t j = G::wsel(c, wcv);
-        w_epilogue<KU>(p, sm, tmem, bcur, c, j, wuse_e[j] & 1, kc & 1);
-        ++wuse_e[j];
-      }
-      if (warp == W_EPI0 && lane == 0) stamp(kc, 4);
-    });
   }
   __syncthreads();
+  cta_stamp(1);
   if (warp == 0) {
     tc_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -834,11 +793,13 @@ static int launch_k(const tc::Params& p, cudaStream_t st) {
 int launch_fused(int dtype, int method, int variant, const void* H, int64_t B, int M, int K,
                  double xi, const double* xi_per_batch, double power, int T, double sigma2,
                  void* W, void* F, double* beta, double* gamma, double* sum_se, void* X,
-                 int32_t* status, void*, size_t, void* dbg_gram, cudaStream_t st) {
+                 int32_t* status, void* ws, size_t ws_bytes, void* dbg_gram, cudaStream_t st) {
   (void)dtype;
   tc::Params p{(const float2*)H, B, M, xi, xi_per_batch, power, sigma2, T, method, variant,
                (float2*)W, (float2*)F, beta, gamma, sum_se, (float2*)X, status, (float2*)dbg_gram, 0,
                nullptr, 0};  // l2mode 0: evict_first loads, st.global.cs W stores
+  p.counter = static_cast<int*>(ws);
+  if (ws_bytes < sizeof(int) || cudaMemsetAsync(ws, 0, sizeof(int), st) != cudaSuccess) return check_launch("fused counter");
   if (const char* e = getenv("XL_FUSED_DEBUG")) p.dbg = atoi(e);
   if (const char* e = getenv("XL_FUSED_L2")) p.l2mode = atoi(e);
   // XL_FUSED_TRACE=1: synchronous per-phase clock64 dump of CTA 0 to stderr
@@ -847,14 +808,14 @@ int launch_fused(int dtype, int method, int variant, const void* H, int64_t B, i
   const bool tracing = getenv("XL_FUSED_TRACE") != nullptr;
   if (tracing) p.trace_k0 = atoi(getenv("XL_FUSED_TRACE")) > 1 ? atoi(getenv("XL_FUSED_TRACE")) - 1 : 0;
   if (tracing) {
-    if (!trace) cudaMalloc(&trace, 1024 * sizeof(long long));
-    cudaMemsetAsync(trace, 0, 1024 * sizeof(long long), st);
+    if (!trace) cudaMalloc(&trace, 2048 * sizeof(long long));
+    cudaMemsetAsync(trace, 0, 2048 * sizeof(long long), st);
     p.trace = trace;
   }
   int rc = K == 64 ? launch_k<64>(p, st) : K == 32 ? launch_k<32>(p, st) : launch_k<16>(p, st);
   if (tracing && rc == XL_SUCCESS) {
-    long long h[1024];
-    cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st);
+    static long long h[2048];
+    cudaMemcpyAsync(h, trace, sizeof(long long) * 2048, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     const long long t0 = h[16];
     static const char* names[32] = {"math:gram_full", "math:A_built", "math:pcg_done", "math:xe_ready",
@@ -868,6 +829,21 @@ int launch_fused(int dtype, int method, int variant, const void* H, int64_t B, i
     for (int kk = 0; kk < 8; ++kk)
       for (int s = 0; s < 32; ++s)
         if (names[s] && h[kk * 32 + s]) fprintf(stderr, "trace b%d %-18s %10lld\n", kk, names[s], h[kk * 32 + s] - t0);
+    {  // per-CTA wall time and effective SM clock
+      long long t0n = h[1024], t1n = h[1024 + 2], mn = 1LL << 62, mx = 0;
+      double clk = 0;
+      int n = 0;
+      for (int b = 0; b < 256 && h[1024 + 4 * b]; ++b, ++n) {
+        const long long* e = h + 1024 + 4 * b;
+        t0n = std::min(t0n, e[0]);
+        t1n = std::max(t1n, e[2]);
+        mn = std::min(mn, e[2] - e[0]);
+        mx = std::max(mx, e[2] - e[0]);
+        clk += (double)(e[3] - e[1]) / (double)(e[2] - e[0]);
+      }
+      if (n) fprintf(stderr, "ctas %d: span %.3f ms, per-CTA %.3f..%.3f ms, mean SM clock %.0f MHz\n", n, (t1n - t0n) * 1e-6,
+                     mn * 1e-6, mx * 1e-6, 1e3 * clk / n);
+    }
     for (int ii = 0; ii < 64; ++ii) {
       const long long* e = h + 256 + ii * 8;
       if (e[0])
