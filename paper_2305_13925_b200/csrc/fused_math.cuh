@@ -42,7 +42,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
   const int mt = tid - 32 * NCONV;  // 0..255
   const uint32_t uah = su32(aeh), ual = su32(ael), ubh = su32(pbh), ubl = su32(pbl);
   auto stamp = [&](uint32_t kk, int slot) {
-    if (p.trace && blockIdx.x == 0 && mt == 0 && kk >= (uint32_t)p.trace_k0 && kk < (uint32_t)p.trace_k0 + 8)
+    if (XL_TRACE && p.trace && blockIdx.x == 0 && mt == 0 && kk >= (uint32_t)p.trace_k0 && kk < (uint32_t)p.trace_k0 + 8)
       p.trace[(kk - p.trace_k0) * 32 + slot] = clock64();
   };
   uint32_t k = 0, nq = 0, wc = 0;

@@ -230,6 +230,9 @@ constexpr int W_MMA = NCONV + NMATH, W_PROD = W_MMA + 1;
 constexpr int NTHREADS = 512;  // 16 warps = 4 warpgroups (setmaxnreg granularity)
 constexpr int BAR_CONV = 1, BAR_MATH = 2;
 // Converter warps: 0..3 plus the two spare warps of warpgroup 3 (14, 15).
+#ifndef XL_TRACE
+#define XL_TRACE 1  // clock64 phase stamps, enabled at run time by XL_FUSED_TRACE=<k0+1>
+#endif
 #ifndef XL_NCW
 #define XL_NCW 6
 #endif
@@ -481,7 +484,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
   tc_after();
   const uint32_t tmem = sm->tmem_slot;
   auto cta_stamp = [&](int slot) {  // per-CTA globaltimer / clock64 (XL_FUSED_TRACE)
-    if (p.trace && threadIdx.x == 0 && blockIdx.x < 256) {
+    if (XL_TRACE && p.trace && threadIdx.x == 0 && blockIdx.x < 256) {
       uint64_t ns;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
       p.trace[1024 + blockIdx.x * 4 + 2 * slot] = (long long)ns;
@@ -494,10 +497,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
   // per ring item i in [64, 128): 0 = load issued, 1 = raw landed, 2 = converted, 3 = MMAs issued
   auto item_stamp = [&](uint32_t ii, int slot) {
     const uint32_t i0 = 64 + 32 * (uint32_t)p.trace_k0;
-    if (p.trace && blockIdx.x == 0 && ii >= i0 && ii < i0 + 64) p.trace[256 + (ii - i0) * 8 + slot] = clock64();
+    if (XL_TRACE && p.trace && blockIdx.x == 0 && ii >= i0 && ii < i0 + 64) p.trace[256 + (ii - i0) * 8 + slot] = clock64();
   };
   auto stamp = [&](uint32_t kk, int slot) {
-    if (p.trace && blockIdx.x == 0 && kk >= (uint32_t)p.trace_k0 && kk < (uint32_t)p.trace_k0 + 8)
+    if (XL_TRACE && p.trace && blockIdx.x == 0 && kk >= (uint32_t)p.trace_k0 && kk < (uint32_t)p.trace_k0 + 8)
       p.trace[(kk - p.trace_k0) * 32 + slot] = clock64();
   };
 #ifndef XL_REG_AUX
@@ -805,7 +808,7 @@ int launch_fused(int dtype, int method, int variant, const void* H, int64_t B, i
   // XL_FUSED_TRACE=1: synchronous per-phase clock64 dump of CTA 0 to stderr
   // (development aid; never set in production runs).
   static long long* trace = nullptr;
-  const bool tracing = getenv("XL_FUSED_TRACE") != nullptr;
+  const bool tracing = XL_TRACE && getenv("XL_FUSED_TRACE") != nullptr;
   if (tracing) p.trace_k0 = atoi(getenv("XL_FUSED_TRACE")) > 1 ? atoi(getenv("XL_FUSED_TRACE")) - 1 : 0;
   if (tracing) {
     if (!trace) cudaMalloc(&trace, 2048 * sizeof(long long));
