@@ -169,7 +169,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
       named_sync(BAR_MATH, NMT);
       if (t == 1) stamp(k, 5);
       // (b) Q = A'' P on the tensor core
-      if (act_row) write_cols<KU>(P, sm->spc, r, h, pbh, pbl);
+      if (act_row) write_cols<KU>(P, [&](int j) { return sm->spc[j].x; }, r, h, pbh, pbl);
       fence_async_smem();
       named_sync(BAR_MATH, NMT);
       if (t == 1) stamp(k, 6);
@@ -223,12 +223,12 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
           tmem_st8(tR + c0, rv);
         }
       }
-      column_partials<JH>(A, sm->red2, q, h);
+      column_partials<JH>(A, sm->red, q, h);  // (d) finished reading red before the last barrier
       tmem_wait_st();
       if (t == 1) stamp(k, 13);
       named_sync(BAR_MATH, NMT);
       if (mt < KU) {  // (f) beta_j, rz update (linsolve.py:284-288)
-        const float rn = column_total<JH>(sm->red2, mt);
+        const float rn = column_total<JH>(sm->red, mt);
         const float rzj = sm->rzs[mt];
         sm->coef[1][mt] = rzj > 0.0f ? rn / rzj : 0.0f;
         sm->rzs[mt] = rn;
@@ -283,17 +283,13 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
         tmem_ld8(tX + c0, xv);
         tmem_wait_ld();
       }
-      if (act_row) {
+      if (act_row) {  // X columns c0..c0+7 as one 16-B row segment of the MN-major B tile
+        uint32_t hw[4], lw[4];
 #pragma unroll
-        for (int i = 0; i < 8; i += 2) {
-          uint32_t hh, ll;
-          split2(xv[i] * sx, xv[i + 1] * sx, hh, ll);
-          const int o0 = boff<KU>(h * JH + c0 + i, r), o1 = boff<KU>(h * JH + c0 + i + 1, r);
-          *reinterpret_cast<unsigned short*>(pbh + o0) = (unsigned short)(hh & 0xffffu);
-          *reinterpret_cast<unsigned short*>(pbl + o0) = (unsigned short)(ll & 0xffffu);
-          *reinterpret_cast<unsigned short*>(pbh + o1) = (unsigned short)(hh >> 16);
-          *reinterpret_cast<unsigned short*>(pbl + o1) = (unsigned short)(ll >> 16);
-        }
+        for (int i = 0; i < 4; ++i) split2(xv[2 * i] * sx, xv[2 * i + 1] * sx, hw[i], lw[i]);
+        const int o = (r >> 3) * G::LBOB + ((h * JH + c0) / 8) * 128 + (r & 7) * 16;
+        *reinterpret_cast<uint4*>(pbh + o) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(pbl + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
       }
     }
     fence_async_smem();
@@ -337,20 +333,22 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
     if (fro2 > 0.0 && isfinite(fro2)) beta = sqrt(p.power / fro2);
     else degenerate = 1;
     if (act_row) {
-      sm->rsq[h * NC + r] = rs;
+      sm->rsq()[h * NC + r] = rs;
 #pragma unroll
       for (int jj = 0; jj < JH; ++jj)
-        if (h * JH + jj == kr) sm->dgq[r] = GX[jj];
+        if (h * JH + jj == kr) sm->dgq()[r] = GX[jj];
     }
     const bool any_not_hpd = math_max(not_hpd ? 1.0f : 0.0f, sm) > 0.0f;  // also orders rsq/dgq
     if (mt < 64) {  // warps 4-5: per-user SINR / SE, then a fixed-order warp sum
       double se = 0.0;
       if (mt < KU) {
         const double b2 = beta * beta;
-        const double intf = b2 * ((double)sm->rsq[2 * mt] + (double)sm->rsq[NC + 2 * mt] +
-                                  (double)sm->rsq[2 * mt + 1] + (double)sm->rsq[NC + 2 * mt + 1]);
-        const double sig = b2 * ((double)sm->dgq[2 * mt] * sm->dgq[2 * mt] +
-                                  (double)sm->dgq[2 * mt + 1] * sm->dgq[2 * mt + 1]);
+        const float* rsq = sm->rsq();
+        const float* dgq = sm->dgq();
+        const double intf = b2 * ((double)rsq[2 * mt] + (double)rsq[NC + 2 * mt] +
+                                  (double)rsq[2 * mt + 1] + (double)rsq[NC + 2 * mt + 1]);
+        const double sig = b2 * ((double)dgq[2 * mt] * dgq[2 * mt] +
+                                  (double)dgq[2 * mt + 1] * dgq[2 * mt + 1]);
         const double g = sig / (intf + p.sigma2);  // metrics.py:52-56
         if (p.gamma) p.gamma[b * KU + mt] = g;
         se = log2(1.0 + g);
@@ -420,13 +418,14 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
 // ring stage for one bulk store measured 6% slower: it holds the stage longer.)
 template <int KU>
 __device__ __forceinline__ void w_epilogue(const Params& p, Small* sm, uint32_t tmem, int64_t b, int c,
-                                           uint32_t j, uint32_t parity, uint32_t kpar) {
+                                           uint32_t j, uint32_t parity, uint32_t kpar, long long* tr = nullptr) {
   using G = Geo<KU>;
   constexpr int NC = G::NC, CH = G::CH;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;  // warps 0-3 = lane quadrants
   const int r = 32 * warp + lane;
   const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16) + (j ? G::T_W1 : G::T_W0);
   mbar_wait(&sm->wfull[j], parity);
+  if (XL_TRACE && tr && threadIdx.x == 0) tr[6] = clock64();
   // the math warps published the scales before xe_ready, which these MMAs awaited
   const float wscale = sm->wsc[kpar][0], fscale = sm->wsc[kpar][1];
   tc_after();
@@ -437,6 +436,7 @@ __device__ __forceinline__ void w_epilogue(const Params& p, Small* sm, uint32_t 
   }
   tc_before();
   mbar_arrive(&sm->wfree[j]);
+  if (XL_TRACE && tr && threadIdx.x == 0) tr[7] = clock64();
   if (r < NC && !(p.dbg & 8)) {  // dbg & 8: timing without the W stores
     const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH) * NC + r;
     float* wp = reinterpret_cast<float*>(p.W) + o0;

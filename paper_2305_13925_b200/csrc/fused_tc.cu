@@ -230,6 +230,9 @@ constexpr int W_MMA = NCONV + NMATH, W_PROD = W_MMA + 1;
 constexpr int NTHREADS = 512;  // 16 warps = 4 warpgroups (setmaxnreg granularity)
 constexpr int BAR_CONV = 1, BAR_MATH = 2;
 // Converter warps: 0..3 plus the two spare warps of warpgroup 3 (14, 15).
+#ifndef XL_NS_MAX
+#define XL_NS_MAX 3  // ring depth cap (4 stages measured 3% slower at K = 64)
+#endif
 #ifndef XL_TRACE
 #define XL_TRACE 1  // clock64 phase stamps, enabled at run time by XL_FUSED_TRACE=<k0+1>
 #endif
@@ -248,28 +251,36 @@ struct Geo {
 #define XL_CH 64
 #endif
   static constexpr int CH = XL_CH;           // antennas per ring stage
-  static constexpr int NS = (3 * 64) / CH;   // ring depth (96 KB ring for K = 64)
   static constexpr int SB = CH * NC * 4;     // stage bytes (raw fp32 == hi + lo fp16 tiles)
   static constexpr int CMA = NC * 16;        // one fp16 tile of an 8-antenna group (hi or lo)
-  static constexpr int OFF_AE = NS * SB + 2048;   // + slack for M-padded Gram reads
-  // Math-written operand tiles (A'', G'', Xe, P / X columns) use a padded
-  // K-direction core stride LBOP = 160 B (== 32 mod 128): the per-column
-  // 16-bit stores of P / X and the paired-row 32-bit stores of Xe then hit
-  // distinct banks; A'' rows are written as whole 16-B core-matrix rows.
-  static constexpr int LBOP = 160;
-  static constexpr int SBOP = (NC / 8) * LBOP;
-  static constexpr int AEPART = 16 * SBOP;        // A operand padded to 128 rows
+  // Math-written operand tiles, canonical SWIZZLE_NONE layouts, no padding:
+  //  A (A'', G'', Xe; K-major, 128 rows x NC): element (n, k) at
+  //    (n/8) SBOA + (k/8) 128 + (n%8) 16 + (k%8) 2 -- rows written as whole
+  //    16-B core-matrix rows (uint4), conflict-free;
+  //  B (P, X; MN-major, K = NC components x N = KU columns): element (k, n) at
+  //    (k/8) LBOB + (n/8) 128 + (k%8) 16 + (n%8) 2 -- a thread (component k)
+  //    writes 8 consecutive columns as one 16-B store, conflict-free.
+  static constexpr int SBOA = NC * 16;
+  static constexpr int AEPART = 16 * SBOA;        // A operand tile (128 rows)
+  static constexpr int LBOB = KU * 16;
+  static constexpr int PBPART = (NC / 8) * LBOB;  // B operand tile
+  static constexpr int SMALL_BYTES = 3072;
+  static constexpr int SLACK = NC < 128 ? 2048 : 0;  // M-padded Gram reads past the last tile
+  static constexpr int SMEM_MAX = 227 * 1024;
+  static constexpr int NS_FIT = (SMEM_MAX - 2 * AEPART - 2 * PBPART - SMALL_BYTES - SLACK) / SB;
+  static constexpr int NS = NS_FIT < XL_NS_MAX ? NS_FIT : XL_NS_MAX;  // ring depth: 4 x 32 KB at K = 64
+  static_assert(NS >= 3, "ring depth");
+  static constexpr int OFF_AE = NS * SB + SLACK;
   static constexpr int OFF_PB = OFF_AE + 2 * AEPART;
-  static constexpr int PBPART = (KU / 8) * SBOP;
   static constexpr int OFF_SMALL = OFF_PB + 2 * PBPART;
-  static constexpr int SMEM = OFF_SMALL + 8192;
+  static constexpr int SMEM = OFF_SMALL + SMALL_BYTES;
   static constexpr int JH = KU / 2;          // PCG columns per math thread
   static constexpr int HC = NC / 2;          // Gram columns per math thread
   static constexpr int NB = (CH / 4) * (NC / 32) / NCONV;  // converter float4 blocks per thread
   static constexpr int WH = CH / 2;          // W epilogue antennas per math thread
   static constexpr uint32_t ID_GRAM = idesc(128, NC, 1, 1);
   static constexpr uint32_t ID_W = idesc(128, CH, 0, 0);
-  static constexpr uint32_t ID_P = idesc(128, KU, 0, 0);
+  static constexpr uint32_t ID_P = idesc(128, KU, 0, 1);  // A'' K-major, P/X MN-major
   // TMEM columns
   // TMEM columns.  T_XE holds the A operand of the K x K products (A'' / G'')
   // and then of W^T (Xe), hi at T_XE and lo at T_XE + 64, copied in from smem
@@ -306,19 +317,24 @@ struct Params {
   int* counter;      // realization claim counter (workspace, zeroed per launch)
 };
 
-// Element (row n, col k) of a padded n x NC K-major operand tile (core rows = n).
+// Element (row n, col k) of the K-major A operand tile (core rows = n).
 template <int KU>
 __device__ __forceinline__ int boff(int n, int k) {
-  return (n >> 3) * Geo<KU>::SBOP + (k >> 3) * Geo<KU>::LBOP + (n & 7) * 16 + (k & 7) * 2;
+  return (n >> 3) * Geo<KU>::SBOA + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2;
 }
-// smem descriptor of K-step s of a padded tile
+// smem descriptor of K-step s (16 elements) of the A tile
 template <int KU>
 __device__ __forceinline__ uint64_t pdesc(uint32_t base, int s) {
-  return sdesc(base + 2 * s * Geo<KU>::LBOP, Geo<KU>::LBOP, Geo<KU>::SBOP);
+  return sdesc(base + 2 * s * 128, 128, Geo<KU>::SBOA);
+}
+// ... and of the MN-major B tile (K-group stride LBOB, N-core stride 128)
+template <int KU>
+__device__ __forceinline__ uint64_t bdesc(uint32_t base, int s) {
+  return sdesc(base + 2 * s * Geo<KU>::LBOB, Geo<KU>::LBOB, 128);
 }
 
 struct Small {
-  uint64_t raw_full[12], conv_full[12], stage_free[12];
+  uint64_t raw_full[8], conv_full[8], stage_free[8];
   uint64_t gram_full, q_full, xe_ready, scale_ready, gram_free;
   uint64_t wfull[2], wfree[2];
   uint64_t xe_consumed;  // Xe(b) copied smem -> TMEM: the smem region may hold A(b+1)
@@ -331,17 +347,16 @@ struct Small {
   float conv_red[8];
   float mred[8];
   double dred[8];
+  double sse[2];        // per-warp sum-SE partials
   float cdg[64];        // Re diag of A' (no xi) per user
-  float red[8 * 32];    // column reductions (4 quadrants x 2 halves x JH)
-  float rsq[2 * 128];
-  float dgq[128];
-  double sse[64];
+  float red[8 * 32];    // PCG column partials (4 quadrants x 2 halves x JH); beta step: rsq[2][128]
   float rzs[64];        // rz per column (owned by the finalising threads)
-  float coef[2][64];    // broadcast per-column alpha / beta
+  float coef[2][64];    // broadcast per-column alpha / beta; beta step: dgq[128]
   float2 spc[64];       // per-column P scale (2^e, 2^-e) of the current iteration
-  float red2[8 * 32];
-  int flags[4];
+  __device__ float* rsq() { return red; }
+  __device__ float* dgq() { return &coef[0][0]; }
 };
+static_assert(sizeof(Small) <= 3072, "small region");
 
 __device__ __forceinline__ float math_max(float v, Small* sm) {
   const int mw = (threadIdx.x >> 5) - NCONV, lane = threadIdx.x & 31;
@@ -387,26 +402,26 @@ __device__ __forceinline__ float column_max(const float* red, int j) {
                fmaxf(red[(2 * 2 + h) * JH + jj], red[(3 * 2 + h) * JH + jj]));
 }
 
-// Write the JH columns of this thread's component row r of an NC x KU
-// matrix (column j scaled by s[j].x) as the split B operand (rows = columns
-// j, K = r).
-template <int KU>
-__device__ __forceinline__ void write_cols(const float* v, const float2* s, int r, int h, uint8_t* bh,
-                                           uint8_t* bl) {
+// Write the JH columns of this thread's component row r (column j scaled by
+// scl(j)) as the split MN-major B operand: 8 columns per 16-B store.
+template <int KU, typename Scale>
+__device__ __forceinline__ void write_cols(const float* v, Scale scl, int r, int h, uint8_t* bh, uint8_t* bl) {
   constexpr int JH = Geo<KU>::JH;
 #pragma unroll
-  for (int jj = 0; jj < JH; jj += 2) {
-    uint32_t hh, ll;
-    split2(v[jj] * s[h * JH + jj].x, v[jj + 1] * s[h * JH + jj + 1].x, hh, ll);
-    const int o0 = boff<KU>(h * JH + jj, r), o1 = boff<KU>(h * JH + jj + 1, r);
-    *reinterpret_cast<unsigned short*>(bh + o0) = (unsigned short)(hh & 0xffffu);
-    *reinterpret_cast<unsigned short*>(bl + o0) = (unsigned short)(ll & 0xffffu);
-    *reinterpret_cast<unsigned short*>(bh + o1) = (unsigned short)(hh >> 16);
-    *reinterpret_cast<unsigned short*>(bl + o1) = (unsigned short)(ll >> 16);
+  for (int g = 0; g < JH / 8; ++g) {
+    uint32_t hw[4], lw[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int jj = 8 * g + 2 * i;
+      split2(v[jj] * scl(h * JH + jj), v[jj + 1] * scl(h * JH + jj + 1), hw[i], lw[i]);
+    }
+    const int o = (r >> 3) * Geo<KU>::LBOB + ((h * JH) / 8 + g) * 128 + (r & 7) * 16;
+    *reinterpret_cast<uint4*>(bh + o) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    *reinterpret_cast<uint4*>(bl + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
   }
 }
 
-// Copy the padded K-major 128 x NC split operand (hi, lo) from smem into TMEM
+// Copy the K-major 128 x NC split A operand (hi, lo) from smem into TMEM
 // columns [t, t + NC/2) and [t + 64, t + 64 + NC/2).  Ordered before later
 // tcgen05.mma of the same thread.
 template <int KU>
@@ -430,7 +445,7 @@ __device__ __forceinline__ void issue_kxk(uint32_t tq, uint32_t ah, uint32_t al,
 #pragma unroll
   for (int s = 0; s < G::NC / 16; ++s) {
     const uint64_t dah = pdesc<KU>(ah, s), dal = pdesc<KU>(al, s);
-    const uint64_t dbh = pdesc<KU>(bh, s), dbl = pdesc<KU>(bl, s);
+    const uint64_t dbh = bdesc<KU>(bh, s), dbl = bdesc<KU>(bl, s);
     mma(tq, dah, dbh, G::ID_P, s != 0);
     mma(tq, dah, dbl, G::ID_P, 1);
     mma(tq, dal, dbh, G::ID_P, 1);
@@ -582,9 +597,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
     uint32_t wcv = 0;                 // W chunk counter (same sequence as the MMA issuer)
     uint32_t wuse_c[2] = {0, 0};
     const bool epi = warp < NCONV;  // warps 0-3 also run the W^T epilogue
-    auto epilogue = [&](int64_t b, int c, uint32_t kc) {
+    auto epilogue = [&](int64_t b, int c, uint32_t kc, uint32_t item) {
       const uint32_t j = G::wsel(wcv);
-      w_epilogue<KU>(p, sm, tmem, b, c, j, wuse_c[j] & 1, kc & 1);
+      const uint32_t i0 = 64 + 32 * (uint32_t)p.trace_k0;
+      long long* tr = (XL_TRACE && p.trace && blockIdx.x == 0 && item >= i0 && item < i0 + 64)
+                          ? p.trace + 256 + (item - i0) * 8 : nullptr;
+      w_epilogue<KU>(p, sm, tmem, b, c, j, wuse_c[j] & 1, kc & 1, tr);
       ++wuse_c[j];
       ++wcv;
     };
@@ -683,12 +701,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
           // W^T epilogue of the previous chunk overlaps this chunk's MMAs
           if (pass == 1 && epi && c >= 1) {
             if (warp == 0 && lane == 0) item_stamp(i - 1, 4);
-            epilogue(bcur, c - 1, kc);
+            epilogue(bcur, c - 1, kc, i - 1);
             if (warp == 0 && lane == 0) item_stamp(i - 1, 5);
           }
       }
       if (pass == 1 && epi) {
-        epilogue(bcur, nch - 1, kc);
+        epilogue(bcur, nch - 1, kc, i - 1);
         if (warp == 0 && lane == 0) stamp(kc, 4);
       }
       sz_par[par] = sz;
@@ -781,7 +799,6 @@ template <int KU>
 static int launch_k(const tc::Params& p, cudaStream_t st) {
   constexpr int smem = tc::Geo<KU>::SMEM;
   static_assert(smem <= 227 * 1024, "fused kernel smem");
-  static_assert(sizeof(tc::Small) <= 8192, "small region");
   cudaFuncSetAttribute(tc::fused_rzf_kernel<KU>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (g_num_sms == 0) {
     int dev = 0;
@@ -850,8 +867,9 @@ int launch_fused(int dtype, int method, int variant, const void* H, int64_t B, i
     for (int ii = 0; ii < 64; ++ii) {
       const long long* e = h + 256 + ii * 8;
       if (e[0])
-        fprintf(stderr, "item %3d issue %9lld landed %9lld converted %9lld mma %9lld epi %9lld %9lld\n", ii + 64,
-                e[0] - t0, e[1] - t0, e[2] - t0, e[3] - t0, e[4] ? e[4] - t0 : 0, e[5] ? e[5] - t0 : 0);
+        fprintf(stderr, "item %3d issue %9lld landed %9lld converted %9lld mma %9lld epi %9lld %9lld full %9lld ld %9lld\n", ii + 64,
+                e[0] - t0, e[1] - t0, e[2] - t0, e[3] - t0, e[4] ? e[4] - t0 : 0, e[5] ? e[5] - t0 : 0,
+                e[6] ? e[6] - t0 : 0, e[7] ? e[7] - t0 : 0);
     }
   }
   return rc;
