@@ -164,12 +164,13 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
       named_sync(BAR_MATH, NMT);
       if (mt < KU) {
         const float s = pow2_scale(column_max<JH>(sm->red, mt), 14);
-        sm->spc[mt] = make_float2(s, 1.0f / s);
+        sm->spx[mt] = s;
+        sm->spy[mt] = 1.0f / s;
       }
       named_sync(BAR_MATH, NMT);
       if (t == 1) stamp(k, 5);
       // (b) Q = A'' P on the tensor core
-      if (act_row) write_cols<KU>(P, [&](int j) { return sm->spc[j].x; }, r, h, pbh, pbl);
+      if (act_row) write_cols<KU>(P, sm->spx, 1.0f, r, h, pbh, pbl);
       fence_async_smem();
       named_sync(BAR_MATH, NMT);
       if (t == 1) stamp(k, 6);
@@ -185,9 +186,15 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
       }
       // (c) curvature m^H z per column
 #pragma unroll
-      for (int jj = 0; jj < JH; ++jj) {
-        A[jj] = A[jj] * sm->spc[h * JH + jj].y;  // undo the column scale (exact)
-        A[jj] = act_row ? P[jj] * (A[jj] * qs) : 0.0f;
+      for (int c0 = 0; c0 < JH; c0 += 8) {
+        float sy[8];
+        lds8(sm->spy + h * JH + c0, sy);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int jj = c0 + i;
+          A[jj] = A[jj] * sy[i];  // undo the column scale (exact)
+          A[jj] = act_row ? P[jj] * (A[jj] * qs) : 0.0f;
+        }
       }
       column_partials<JH>(A, sm->red, q, h);
       named_sync(BAR_MATH, NMT);
@@ -203,18 +210,20 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
       // (e) w += alpha m, r -= alpha Pm, rz partials (linsolve.py:281-284)
 #pragma unroll
       for (int c0 = 0; c0 < JH; c0 += 8) {
-        float qv[8], xv[8], rv[8];
+        float qv[8], xv[8], rv[8], al8[8], sy[8];
         if (quad_act) {
           tmem_ld8(tQ + c0, qv);
           tmem_ld8(tX + c0, xv);
           tmem_ld8(tR + c0, rv);
-          tmem_wait_ld();
         }
+        lds8(sm->coef[0] + h * JH + c0, al8);
+        lds8(sm->spy + h * JH + c0, sy);
+        if (quad_act) tmem_wait_ld();
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float al = sm->coef[0][h * JH + c0 + i];
+          const float al = al8[i];
           xv[i] = xv[i] + al * P[c0 + i];
-          rv[i] = rv[i] - al * ((qv[i] * sm->spc[h * JH + c0 + i].y) * qs);
+          rv[i] = rv[i] - al * ((qv[i] * sy[i]) * qs);
           const float z = textbook ? rv[i] * icr : rv[i];
           A[c0 + i] = act_row ? rv[i] * z : 0.0f;
         }
@@ -238,14 +247,13 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
       // (g) m = z + beta m
 #pragma unroll
       for (int c0 = 0; c0 < JH; c0 += 8) {
-        float rv[8];
-        if (quad_act) {
-          tmem_ld8(tR + c0, rv);
-          tmem_wait_ld();
-        }
+        float rv[8], be8[8];
+        if (quad_act) tmem_ld8(tR + c0, rv);
+        lds8(sm->coef[1] + h * JH + c0, be8);
+        if (quad_act) tmem_wait_ld();
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float be = sm->coef[1][h * JH + c0 + i];
+          const float be = be8[i];
           const float z = textbook ? rv[i] * icr : rv[i];
           P[c0 + i] = act_row ? z + be * P[c0 + i] : 0.0f;
         }
@@ -413,14 +421,19 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
 }
 
 // W^T epilogue of one chunk, run by converter warps 0-3 (TMEM lane quadrant =
-// warp): thread = output component c2 = 32 q + lane, CH antennas; 128-B
-// coalesced streaming stores per antenna.  (Staging the tile in the consumed
-// ring stage for one bulk store measured 6% slower: it holds the stage longer.)
+// warp): thread = output component c2 = 32 q + lane, CH antennas.
+// XL_WSTAGE: each half of the tile (CH/2 antennas x NC components, row-major ==
+// the W rows in HBM) is written to its own smem staging buffer and leaves with
+// one 1-D bulk store, so the warps do not sit in the ~1 k-cycle store drain
+// (the per-SM store path moves ~32 B/cycle); a buffer is reused once the
+// previous chunk's store of it has been read out.  Otherwise 128-B coalesced
+// streaming stores per antenna.
 template <int KU>
-__device__ __forceinline__ void w_epilogue(const Params& p, Small* sm, uint32_t tmem, int64_t b, int c,
-                                           uint32_t j, uint32_t parity, uint32_t kpar, long long* tr = nullptr) {
+__device__ __forceinline__ void w_epilogue(const Params& p, Small* sm, uint32_t tmem, uint8_t* wstg, int64_t b,
+                                           int c, uint32_t j, uint32_t parity, uint32_t kpar,
+                                           long long* tr = nullptr) {
   using G = Geo<KU>;
-  constexpr int NC = G::NC, CH = G::CH;
+  constexpr int NC = G::NC, CH = G::CH, HALF = CH / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;  // warps 0-3 = lane quadrants
   const int r = 32 * warp + lane;
   const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16) + (j ? G::T_W1 : G::T_W0);
@@ -437,15 +450,30 @@ __device__ __forceinline__ void w_epilogue(const Params& p, Small* sm, uint32_t 
   tc_before();
   mbar_arrive(&sm->wfree[j]);
   if (XL_TRACE && tr && threadIdx.x == 0) tr[7] = clock64();
-  if (r < NC && !(p.dbg & 8)) {  // dbg & 8: timing without the W stores
-    const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH) * NC + r;
-    float* wp = reinterpret_cast<float*>(p.W) + o0;
+  const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH) * NC;
+  if (p.F && r < NC) {
+    float* fp = reinterpret_cast<float*>(p.F) + o0 + r;
+#pragma unroll
+    for (int a = 0; a < CH; ++a) __stcs(fp + a * NC, d[a] * fscale);
+  }
+  if (XL_WSTAGE) {
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      float* buf = reinterpret_cast<float*>(wstg + hf * HALF * NC * 4);
+      if (threadIdx.x == 0) bulk_wait_read<1>();  // this buffer's previous store has been read
+      named_sync(BAR_EPI, 32 * NCONV);
+      if (r < NC) {
+#pragma unroll
+        for (int a = 0; a < HALF; ++a) buf[a * NC + r] = d[hf * HALF + a] * wscale;
+      }
+      fence_async_smem();
+      named_sync(BAR_EPI, 32 * NCONV);
+      if (threadIdx.x == 0 && !(p.dbg & 8))
+        bulk_s2g(reinterpret_cast<float*>(p.W) + o0 + (int64_t)hf * HALF * NC, buf, HALF * NC * 4);
+    }
+  } else if (r < NC && !(p.dbg & 8)) {  // dbg & 8: timing without the W stores
+    float* wp = reinterpret_cast<float*>(p.W) + o0 + r;
 #pragma unroll
     for (int a = 0; a < CH; ++a) __stcs(wp + a * NC, d[a] * wscale);
-    if (p.F) {
-      float* fp = reinterpret_cast<float*>(p.F) + o0;
-#pragma unroll
-      for (int a = 0; a < CH; ++a) __stcs(fp + a * NC, d[a] * fscale);
-    }
   }
 }

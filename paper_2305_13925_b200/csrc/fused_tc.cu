@@ -105,6 +105,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (++spins > (1u << 24)) asm volatile("trap;");
   } while (!done);
 }
+// smem -> global 1-D bulk store, completion tracked by bulk groups
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(su32(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// wait until at most N committed bulk stores are still reading shared memory
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t hint) {
   asm volatile(
@@ -228,8 +237,11 @@ __device__ __forceinline__ float warp_transpose_reduce(float (&v)[N]) {
 constexpr int NCONV = 4, NMATH = 8;
 constexpr int W_MMA = NCONV + NMATH, W_PROD = W_MMA + 1;
 constexpr int NTHREADS = 512;  // 16 warps = 4 warpgroups (setmaxnreg granularity)
-constexpr int BAR_CONV = 1, BAR_MATH = 2;
+constexpr int BAR_CONV = 1, BAR_MATH = 2, BAR_EPI = 3;
 // Converter warps: 0..3 plus the two spare warps of warpgroup 3 (14, 15).
+#ifndef XL_WSTAGE
+#define XL_WSTAGE 0  // 1: W^T tiles leave through a smem staging area + bulk stores (measured no faster)
+#endif
 #ifndef XL_NS_MAX
 #define XL_NS_MAX 3  // ring depth cap (4 stages measured 3% slower at K = 64)
 #endif
@@ -267,12 +279,15 @@ struct Geo {
   static constexpr int SMALL_BYTES = 3072;
   static constexpr int SLACK = NC < 128 ? 2048 : 0;  // M-padded Gram reads past the last tile
   static constexpr int SMEM_MAX = 227 * 1024;
-  static constexpr int NS_FIT = (SMEM_MAX - 2 * AEPART - 2 * PBPART - SMALL_BYTES - SLACK) / SB;
+  // W^T staging for the epilogue's bulk stores: two buffers of CH/2 antennas
+  static constexpr int WSTG = XL_WSTAGE ? SB : 0;
+  static constexpr int NS_FIT = (SMEM_MAX - 2 * AEPART - 2 * PBPART - SMALL_BYTES - SLACK - WSTG) / SB;
   static constexpr int NS = NS_FIT < XL_NS_MAX ? NS_FIT : XL_NS_MAX;  // ring depth: 4 x 32 KB at K = 64
   static_assert(NS >= 3, "ring depth");
   static constexpr int OFF_AE = NS * SB + SLACK;
   static constexpr int OFF_PB = OFF_AE + 2 * AEPART;
-  static constexpr int OFF_SMALL = OFF_PB + 2 * PBPART;
+  static constexpr int OFF_WSTG = OFF_PB + 2 * PBPART;
+  static constexpr int OFF_SMALL = OFF_WSTG + WSTG;
   static constexpr int SMEM = OFF_SMALL + SMALL_BYTES;
   static constexpr int JH = KU / 2;          // PCG columns per math thread
   static constexpr int HC = NC / 2;          // Gram columns per math thread
@@ -351,8 +366,9 @@ struct Small {
   float cdg[64];        // Re diag of A' (no xi) per user
   float red[8 * 32];    // PCG column partials (4 quadrants x 2 halves x JH); beta step: rsq[2][128]
   float rzs[64];        // rz per column (owned by the finalising threads)
-  float coef[2][64];    // broadcast per-column alpha / beta; beta step: dgq[128]
-  float2 spc[64];       // per-column P scale (2^e, 2^-e) of the current iteration
+  alignas(16) float coef[2][64];  // broadcast per-column alpha / beta; beta step: dgq[128]
+  alignas(16) float spx[64];  // per-column P scale 2^e (current iteration)
+  alignas(16) float spy[64];  // ... and its inverse 2^-e
   __device__ float* rsq() { return red; }
   __device__ float* dgq() { return &coef[0][0]; }
 };
@@ -402,18 +418,30 @@ __device__ __forceinline__ float column_max(const float* red, int j) {
                fmaxf(red[(2 * 2 + h) * JH + jj], red[(3 * 2 + h) * JH + jj]));
 }
 
+// 8 consecutive floats of a 32-B aligned smem array (two LDS.128)
+__device__ __forceinline__ void lds8(const float* a, float (&o)[8]) {
+  const float4 x = reinterpret_cast<const float4*>(a)[0], y = reinterpret_cast<const float4*>(a)[1];
+  o[0] = x.x; o[1] = x.y; o[2] = x.z; o[3] = x.w; o[4] = y.x; o[5] = y.y; o[6] = y.z; o[7] = y.w;
+}
+
 // Write the JH columns of this thread's component row r (column j scaled by
-// scl(j)) as the split MN-major B operand: 8 columns per 16-B store.
-template <int KU, typename Scale>
-__device__ __forceinline__ void write_cols(const float* v, Scale scl, int r, int h, uint8_t* bh, uint8_t* bl) {
+// scl[j], or by sc1 when scl is null) as the split MN-major B operand: 8
+// columns per 16-B store.
+template <int KU>
+__device__ __forceinline__ void write_cols(const float* v, const float* scl, float sc1, int r, int h, uint8_t* bh,
+                                           uint8_t* bl) {
   constexpr int JH = Geo<KU>::JH;
 #pragma unroll
   for (int g = 0; g < JH / 8; ++g) {
+    float sv[8];
+    if (scl) lds8(scl + h * JH + 8 * g, sv);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sv[i] = scl ? sv[i] : sc1;
     uint32_t hw[4], lw[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int jj = 8 * g + 2 * i;
-      split2(v[jj] * scl(h * JH + jj), v[jj + 1] * scl(h * JH + jj + 1), hw[i], lw[i]);
+      split2(v[jj] * sv[2 * i], v[jj + 1] * sv[2 * i + 1], hw[i], lw[i]);
     }
     const int o = (r >> 3) * Geo<KU>::LBOB + ((h * JH) / 8 + g) * 128 + (r & 7) * 16;
     *reinterpret_cast<uint4*>(bh + o) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
@@ -466,6 +494,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
   uint8_t* ael = aeh + G::AEPART;
   uint8_t* pbh = smem + G::OFF_PB;
   uint8_t* pbl = pbh + G::PBPART;
+  uint8_t* wstg = smem + G::OFF_WSTG;
   Small* sm = reinterpret_cast<Small*>(smem + G::OFF_SMALL);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -602,7 +631,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
       const uint32_t i0 = 64 + 32 * (uint32_t)p.trace_k0;
       long long* tr = (XL_TRACE && p.trace && blockIdx.x == 0 && item >= i0 && item < i0 + 64)
                           ? p.trace + 256 + (item - i0) * 8 : nullptr;
-      w_epilogue<KU>(p, sm, tmem, b, c, j, wuse_c[j] & 1, kc & 1, tr);
+      w_epilogue<KU>(p, sm, tmem, wstg, b, c, j, wuse_c[j] & 1, kc & 1, tr);
       ++wuse_c[j];
       ++wcv;
     };
@@ -775,6 +804,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
   } else if (warp < NCONV + NMATH) {
     math_role<KU>(p, sm, aeh, ael, pbh, pbl, tmem, nch);
   }
+  // the epilogue's W bulk stores (issued by warp 0 lane 0) complete before exit
+  if (XL_WSTAGE && warp == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
   cta_stamp(1);
   if (warp == 0) {
