@@ -20,6 +20,24 @@ __device__ void load(const char* src, size_t bytes, char* buf, uint64_t* bar, ui
 __global__ void k(const char* X, size_t xs, const char* Y, size_t ys, int mode) {
   extern __shared__ __align__(1024) char smem[];
   uint64_t* bar = (uint64_t*)smem;
+  if (mode >= 3) {  // mode 3: X load (evict_last) then all threads write Y with st.global.cs; 4: same, no X reload gap
+    const size_t xper = xs / gridDim.x, yper = ys / gridDim.x;
+    uint64_t last;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(last));
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar)));
+      asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    uint32_t ph = 0;
+    if (threadIdx.x == 0) load(X + blockIdx.x * xper, xper, smem + 1024, bar, ph, last);
+    __syncthreads();
+    float4* yw = (float4*)(const_cast<char*>(Y) + blockIdx.x * yper);
+    for (size_t i = threadIdx.x; i < yper / 16; i += blockDim.x) __stcs(yw + i, make_float4(1.f, 2.f, 3.f, 4.f));
+    __syncthreads();
+    if (threadIdx.x == 0) load(X + blockIdx.x * xper, xper, smem + 1024, bar, ph, last);
+    return;
+  }
   if (threadIdx.x != 0) return;
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar)));
   asm volatile("fence.mbarrier_init.release.cluster;");
@@ -30,7 +48,7 @@ __global__ void k(const char* X, size_t xs, const char* Y, size_t ys, int mode) 
   uint32_t ph = 0;
   const size_t xper = xs / gridDim.x, yper = ys / gridDim.x;
   load(X + blockIdx.x * xper, xper, smem + 1024, bar, ph, mode == 0 ? last : normal);
-  if (mode != 2) load(Y + blockIdx.x * yper, yper, smem + 1024, bar, ph, first);
+  if (mode == 0 || mode == 1) load(Y + blockIdx.x * yper, yper, smem + 1024, bar, ph, first);
   load(X + blockIdx.x * xper, xper, smem + 1024, bar, ph, first);
 }
 int main(int argc, char** argv) {
@@ -39,9 +57,10 @@ int main(int argc, char** argv) {
   xs = xs / (148 * 32768) * 148 * 32768; ys = ys / (148 * 32768) * 148 * 32768;
   char *X, *Y; cudaMalloc(&X, xs); cudaMalloc(&Y, ys); cudaMemset(X, 1, xs); cudaMemset(Y, 2, ys);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 + 32768);
-  k<<<148, 32, 1024 + 32768>>>(X, xs, Y, ys, mode);
+  const int nt = mode >= 3 ? 256 : 32;
+  k<<<148, nt, 1024 + 32768>>>(X, xs, Y, ys, mode);
   cudaDeviceSynchronize();
-  k<<<148, 32, 1024 + 32768>>>(X, xs, Y, ys, mode);
+  k<<<148, nt, 1024 + 32768>>>(X, xs, Y, ys, mode);
   printf("X %zu MB Y %zu MB mode %d: %s\n", xs >> 20, ys >> 20, mode, cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
