@@ -104,12 +104,22 @@ cgemm_kernel(const cplx<R>* __restrict__ A, int64_t sA, int lda,
           double xi = diag_add ? diag_add[b] : diag_scalar;
           Cb[(int64_t)i * ldc + i] = mk<R>((R)((double)v.x + xi), (R)0);
         }
+      } else if (EPI == EPI_GXF) {  // (A - xi I) X and Re<X, (A - xi I) X>
+        const double xi = diag_add ? diag_add[b] : diag_scalar;
+        const C x = Bb[(int64_t)i * ldb + j];
+        v.x = (R)((double)v.x - xi * (double)x.x);
+        v.y = (R)((double)v.y - xi * (double)x.y);
+        Cb[(int64_t)i * ldc + j] = v;
+        local += (double)x.x * (double)v.x + (double)x.y * (double)v.y;
+      } else if (EPI == EPI_BSCALE) {  // per-batch scale (beta)
+        const R sc = (R)diag_add[b];
+        Cb[(int64_t)i * ldc + j] = cscale(v, sc);
       } else {
         Cb[(int64_t)i * ldc + j] = v;
         if (EPI == EPI_FNORM) local += (double)cabs2(v);
       }
     }
-  if (EPI == EPI_FNORM) {
+  if (EPI == EPI_FNORM || EPI == EPI_GXF) {
     // fixed-order block reduction -> one partial per (b, tile)
     __shared__ double red[NT / 32];
     local = warp_sum(local);
@@ -141,6 +151,8 @@ int launch_cgemm(bool conjA, int epi, const void* A, int64_t sA, int lda,
     else cgemm_kernel<R, true, EPI_STORE><<<grid, NT, 0, st>>>(XL_GEMM_ARGS);
   } else {
     if (epi == EPI_FNORM) cgemm_kernel<R, false, EPI_FNORM><<<grid, NT, 0, st>>>(XL_GEMM_ARGS);
+    else if (epi == EPI_GXF) cgemm_kernel<R, false, EPI_GXF><<<grid, NT, 0, st>>>(XL_GEMM_ARGS);
+    else if (epi == EPI_BSCALE) cgemm_kernel<R, false, EPI_BSCALE><<<grid, NT, 0, st>>>(XL_GEMM_ARGS);
     else cgemm_kernel<R, false, EPI_STORE><<<grid, NT, 0, st>>>(XL_GEMM_ARGS);
   }
 #undef XL_GEMM_ARGS
@@ -187,6 +199,27 @@ __global__ void beta_scale_kernel(cplx<R>* __restrict__ W, cplx<R>* __restrict__
   }
 }
 
+// beta = sqrt(power / ||F||^2) only (||F||^2 from per-tile partials).
+__global__ void beta_kernel(int64_t B, const double* __restrict__ partial, int nparts, double power,
+                            double* __restrict__ beta, int32_t* __restrict__ status) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double tr = 0.0;
+  for (int p = 0; p < nparts; ++p) tr += partial[b * nparts + p];
+  double bt = 0.0;
+  if (!(tr > 0.0)) {
+    if (status && status[b] == XL_STATUS_OK) status[b] = XL_STATUS_DEGENERATE;
+  } else {
+    bt = sqrt(power / tr);
+  }
+  beta[b] = bt;
+}
+int launch_beta_from_partials(int64_t B, const double* partial, int nparts, double power, double* beta,
+                              int32_t* status, cudaStream_t st) {
+  beta_kernel<<<(unsigned)((B + 255) / 256), 256, 0, st>>>(B, partial, nparts, power, beta, status);
+  return check_launch("beta");
+}
+
 template <typename R>
 int launch_beta_scale(void* W, void* F, int64_t B, int64_t per, const double* partial,
                       int nparts, double power, double* beta, int32_t* status,
@@ -208,16 +241,17 @@ template int launch_beta_scale<double>(void*, void*, int64_t, int64_t, const dou
 template <typename R>
 __global__ void sinr_kernel(const cplx<R>* __restrict__ Bc, int K, double sigma2,
                             double* __restrict__ gamma, double* __restrict__ se,
-                            double* __restrict__ sum_se) {
+                            double* __restrict__ sum_se, const double* __restrict__ bscale) {
   const int64_t b = blockIdx.x;
+  const double s2 = bscale ? bscale[b] * bscale[b] : 1.0;  // B = beta * Bc
   extern __shared__ double sse[];
   const cplx<R>* Bb = Bc + b * (int64_t)K * K;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int k = warp; k < K; k += nw) {
     double tot = 0.0;
     for (int j = lane; j < K; j += 32) tot += (double)cabs2(Bb[(int64_t)k * K + j]);
-    tot = warp_sum(tot);
-    double sig = (double)cabs2(Bb[(int64_t)k * K + k]);
+    tot = warp_sum(tot) * s2;
+    double sig = (double)cabs2(Bb[(int64_t)k * K + k]) * s2;
     double g = sig / ((tot - sig) + sigma2);
     double s = log2(1.0 + g);
     if (lane == 0) {
@@ -236,13 +270,13 @@ __global__ void sinr_kernel(const cplx<R>* __restrict__ Bc, int K, double sigma2
 
 template <typename R>
 int launch_sinr(const void* Bc, int64_t B, int K, double sigma2, double* gamma,
-                double* se, double* sum_se, cudaStream_t st) {
+                double* se, double* sum_se, cudaStream_t st, const double* bscale) {
   sinr_kernel<R><<<(unsigned)B, 256, K * sizeof(double), st>>>(
-      (const cplx<R>*)Bc, K, sigma2, gamma, se, sum_se);
+      (const cplx<R>*)Bc, K, sigma2, gamma, se, sum_se, bscale);
   return check_launch("sinr");
 }
-template int launch_sinr<float>(const void*, int64_t, int, double, double*, double*, double*, cudaStream_t);
-template int launch_sinr<double>(const void*, int64_t, int, double, double*, double*, double*, cudaStream_t);
+template int launch_sinr<float>(const void*, int64_t, int, double, double*, double*, double*, cudaStream_t, const double*);
+template int launch_sinr<double>(const void*, int64_t, int, double, double*, double*, double*, cudaStream_t, const double*);
 
 // ---------------------------------------------------------------------------
 // Ergodic-SE partials {sum, sum of squares, n} per chunk (metrics.py:61-68).

@@ -5,7 +5,7 @@
 
 namespace xl {
 
-enum { EPI_STORE = 0, EPI_GRAM = 1, EPI_FNORM = 2 };
+enum { EPI_STORE = 0, EPI_GRAM = 1, EPI_FNORM = 2, EPI_GXF = 3, EPI_BSCALE = 4 };
 
 template <typename R>
 int launch_cgemm(bool conjA, int epi, const void* A, int64_t sA, int lda,
@@ -21,7 +21,9 @@ int launch_beta_scale(void* W, void* F, int64_t B, int64_t per, const double* pa
                       cudaStream_t st);
 template <typename R>
 int launch_sinr(const void* Bc, int64_t B, int K, double sigma2, double* gamma,
-                double* se, double* sum_se, cudaStream_t st);
+                double* se, double* sum_se, cudaStream_t st, const double* bscale = nullptr);
+int launch_beta_from_partials(int64_t B, const double* partial, int nparts, double power, double* beta,
+                              int32_t* status, cudaStream_t st);
 int launch_se_partials(const double* s, int64_t B, int64_t chunk, double* out, cudaStream_t st);
 
 // PCG / CG / Jac-PCG (linsolve.py:183-294) and Cholesky (linsolve.py:109-119).

@@ -118,8 +118,9 @@ static size_t simt_rzf_ws(int dtype, int64_t B, int M, int K) {
   size_t cs = csize(dtype), kk = (size_t)B * K * K * cs;
   size_t sws = xl_solve_workspace_bytes(dtype, B, K, K);
   if (sws < kk) sws = kk;
+  const int tiles = gemm_tiles(M, K) > gemm_tiles(K, K) ? gemm_tiles(M, K) : gemm_tiles(K, K);
   return align_up(kk) + align_up(kk) + align_up(sws) +
-         align_up((size_t)B * gemm_tiles(M, K) * sizeof(double)) + align_up((size_t)B * 4);
+         align_up((size_t)B * tiles * sizeof(double)) + align_up((size_t)B * 4);
 }
 
 size_t xl_rzf_workspace_bytes(int dtype, int method, int64_t B, int32_t M, int32_t K) {
@@ -167,15 +168,33 @@ static int rzf_impl(bool allow_fused, int dtype, int method, int variant, const 
   size_t sws = xl_solve_workspace_bytes(dtype, B, K, K);
   if (sws < kk) sws = kk;
   void* sw = p; p += align_up(sws);
-  double* part = (double*)p; p += align_up((size_t)B * gemm_tiles(M, K) * sizeof(double));
+  const int ptiles = gemm_tiles(M, K) > gemm_tiles(K, K) ? gemm_tiles(M, K) : gemm_tiles(K, K);
+  double* part = (double*)p; p += align_up((size_t)B * ptiles * sizeof(double));
   int32_t* iters = (int32_t*)p;
   void* Xo = X ? X : Xw;
   int e;
   if ((e = xl_gram(dtype, H, B, M, K, xi, xi_per_batch, A, stream))) return e;
   if ((e = xl_solve(dtype, method, variant, A, B, K, nullptr, K, nullptr, nullptr, method == XL_CG,
                     T, -1.0, Xo, iters, nullptr, nullptr, status, sw, sws, stream))) return e;
-  return apply_precoder(dtype, H, Xo, B, M, K, power, sigma2, W, F, beta, gamma, sum_se, status,
-                        part, sw, st);
+  // Coupling and ||F||^2 from the K x K side: GX = (A - xi I) X,
+  // ||F||_F^2 = Re tr(X^H GX) (precoder.py:64-70 with F = H X), beta, then
+  // W = beta H X in one pass and B = H^H W = beta GX (metrics.py:35-44):
+  // 8 K^3 instead of 8 M K^2 flops for the coupling, no separate F pass.
+  const int64_t sH = (int64_t)M * K, sK = (int64_t)K * K;
+  const int np = gemm_tiles(K, K);
+  void* GX = sw;  // the solver workspace is free again (>= B K K)
+  if (dtype == XL_C64) {
+    if ((e = launch_cgemm<float>(false, EPI_GXF, A, sK, K, Xo, sK, K, GX, sK, K, B, K, K, K, xi_per_batch, xi, part, st))) return e;
+    if ((e = launch_beta_from_partials(B, part, np, power, beta, status, st))) return e;
+    if ((e = launch_cgemm<float>(false, EPI_BSCALE, H, sH, K, Xo, sK, K, W, sH, K, B, M, K, K, beta, 0, nullptr, st))) return e;
+    if (F && (e = launch_cgemm<float>(false, EPI_STORE, H, sH, K, Xo, sK, K, F, sH, K, B, M, K, K, nullptr, 0, nullptr, st))) return e;
+    return launch_sinr<float>(GX, B, K, sigma2, gamma, nullptr, sum_se, st, beta);
+  }
+  if ((e = launch_cgemm<double>(false, EPI_GXF, A, sK, K, Xo, sK, K, GX, sK, K, B, K, K, K, xi_per_batch, xi, part, st))) return e;
+  if ((e = launch_beta_from_partials(B, part, np, power, beta, status, st))) return e;
+  if ((e = launch_cgemm<double>(false, EPI_BSCALE, H, sH, K, Xo, sK, K, W, sH, K, B, M, K, K, beta, 0, nullptr, st))) return e;
+  if (F && (e = launch_cgemm<double>(false, EPI_STORE, H, sH, K, Xo, sK, K, F, sH, K, B, M, K, K, nullptr, 0, nullptr, st))) return e;
+  return launch_sinr<double>(GX, B, K, sigma2, gamma, nullptr, sum_se, st, beta);
 }
 
 int xl_rzf(int dtype, int method, int variant, const void* H, int64_t B, int32_t M,
