@@ -329,6 +329,17 @@ def main():
             "algorithmic_bytes_per_launch": B * bytes_per,
             "traffic_source": "profiles/traffic.json" if traffic is not None else None,
             "flops_per_precoder": flops_per}
+    # SURVEY.md section 8(d)'s convention, for comparison: c64 priced as
+    # 3xTF32 (TF32 ~ BF16 / 2, so BF16 / 6), which makes cfg3 tensor-bound;
+    # the 3xFP16 split used here runs at the FP16 (= BF16) rate, hence the
+    # primary "roofline" above is the HBM bound.
+    if tc:
+        p3 = bf16 / 6.0
+        t_roof = max(flops_per / (p3 * 1e12), bytes_per / (hbm * 1e9))
+        roof["survey_convention"] = {
+            "bound": "tensor" if flops_per / (p3 * 1e12) > bytes_per / (hbm * 1e9) else "hbm",
+            "tensor_peak_tflops": p3, "roofline_precoders_per_s": 1.0 / t_roof,
+            "frac": (B / kern_s) * t_roof}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
