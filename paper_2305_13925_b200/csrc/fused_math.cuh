@@ -87,6 +87,64 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
     // ---- (2) A'' split: row 2k = (ar, -ai), row 2k+1 = (ai, ar) per column pair
     // (the smem operand region held Xe(k-1) until the W pass copied it to TMEM)
     if (k >= 1 && !(p.dbg & 3)) mbar_wait(&sm->xe_consumed, (k - 1) & 1);
+#if XL_GRAM2
+    // The Gram pass accumulated U = Zh^T (Zh + 2 Zl) (two products instead of
+    // three); G = (U + U^T) / 2.  U goes through smem (rows padded to NC + 4
+    // floats: conflict-free 16-B row accesses and 4-B column accesses; the
+    // buffer spans the A'' and P tiles, both idle here), each thread forms
+    // its half-row of G, and the A'' rows are written after everyone's reads.
+    {
+      constexpr int UP = NC + 4;
+      float* ub = reinterpret_cast<float*>(aeh);
+      static_assert(NC * UP * 4 <= 2 * G::AEPART + 2 * G::PBPART, "U staging");
+      if (quad_act) {
+#pragma unroll 1
+        for (int c0 = 0; c0 < HC; c0 += 16) {
+          float v[16];
+          tmem_ld16(tl + G::T_GRAM + h * HC + c0, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; e += 4)
+            *reinterpret_cast<float4*>(ub + r * UP + h * HC + c0 + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+        }
+      }
+      named_sync(BAR_MATH, NMT);
+      uint32_t hw[HC / 2], lw[HC / 2];
+      if (quad_act) {
+#pragma unroll
+        for (int c0 = 0; c0 < HC; c0 += 4) {
+          const float4 own = *reinterpret_cast<const float4*>(ub + r * UP + h * HC + c0);
+          const float gv[4] = {own.x, own.y, own.z, own.w};
+          float g[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) g[e] = 0.5f * (gv[e] + ub[(h * HC + c0 + e) * UP + r]);
+#pragma unroll
+          for (int jp = 0; jp < 2; ++jp) {
+            const float g0 = g[2 * jp], g1 = g[2 * jp + 1];
+            const float p0 = __shfl_xor_sync(0xffffffffu, g0, 1), p1 = __shfl_xor_sync(0xffffffffu, g1, 1);
+            float ar = odd ? (p0 + g1) : (g0 + p1);
+            const float ai = odd ? (p1 - g0) : (g1 - p0);
+            const int jc = (h * HC + c0) / 2 + jp;
+            if (jc == kr) ar += alpha_s;
+            if (p.dbgA && !odd) {
+              const float inv = 1.0f / (sz * sz);
+              p.dbgA[(b * KU + kr) * KU + jc] = make_float2(ar * inv, ai * inv);
+            }
+            split2((odd ? ai : ar) * sa, (odd ? ar : -ai) * sa, hw[c0 / 2 + jp], lw[c0 / 2 + jp]);
+          }
+        }
+      }
+      named_sync(BAR_MATH, NMT);  // U reads done before A'' overwrites the buffer
+      if (quad_act) {
+#pragma unroll
+        for (int q8 = 0; q8 < HC / 8; ++q8) {
+          const int o = boff<KU>(r, h * HC + 8 * q8);
+          *reinterpret_cast<uint4*>(aeh + o) = make_uint4(hw[4 * q8], hw[4 * q8 + 1], hw[4 * q8 + 2], hw[4 * q8 + 3]);
+          *reinterpret_cast<uint4*>(ael + o) = make_uint4(lw[4 * q8], lw[4 * q8 + 1], lw[4 * q8 + 2], lw[4 * q8 + 3]);
+        }
+      }
+    }
+#else
     if (quad_act) {
 #pragma unroll 1
       for (int c0 = 0; c0 < HC; c0 += 16) {
@@ -117,6 +175,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
         }
       }
     }
+#endif
     tc_before();
     fence_async_smem();
     named_sync(BAR_MATH, NMT);  // every thread's Gram TMEM reads are complete

@@ -242,6 +242,9 @@ constexpr int BAR_CONV = 1, BAR_MATH = 2, BAR_EPI = 3;
 #ifndef XL_WSTAGE
 #define XL_WSTAGE 0  // 1: W^T tiles leave through a smem staging area + bulk stores (measured no faster)
 #endif
+#ifndef XL_GRAM2
+#define XL_GRAM2 1  // Gram pass accumulates U = Zh^T (Zh + 2 Zl): 2 MMAs per K-step instead of 3
+#endif
 #ifndef XL_NS_MAX
 #define XL_NS_MAX 3  // ring depth cap (4 stages measured 3% slower at K = 64)
 #endif
@@ -709,7 +712,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
               const __half2 ha = __float22half2_rn(a), hb = __float22half2_rn(bq);
               const float2 ra = __fadd2_rn(a, make_float2(-__low2float(ha), -__high2float(ha)));
               const float2 rbq = __fadd2_rn(bq, make_float2(-__low2float(hb), -__high2float(hb)));
-              const __half2 la = __float22half2_rn(ra), lb = __float22half2_rn(rbq);
+              // Gram pass with XL_GRAM2: the lo tile holds 2 Zl (exact)
+              const float2 l2 = (XL_GRAM2 && pass == 0) ? make_float2(2.0f, 2.0f) : make_float2(1.0f, 1.0f);
+              const __half2 la = __float22half2_rn(__fmul2_rn(ra, l2)), lb = __float22half2_rn(__fmul2_rn(rbq, l2));
               const int off = (cc >> 3) * 128 + row * 16 + (cc & 7) * 2;
               *reinterpret_cast<uint2*>(gb + off) = make_uint2(h2u(ha), h2u(hb));
               *reinterpret_cast<uint2*>(gb + G::CMA + off) = make_uint2(h2u(la), h2u(lb));
@@ -763,8 +768,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
             const uint64_t dh = sdesc(zh + 4 * ks * G::CMA, 2 * G::CMA, 128);
             const uint64_t dl = sdesc(zl + 4 * ks * G::CMA, 2 * G::CMA, 128);
             mma(tmem + G::T_GRAM, dh, dh, G::ID_GRAM, (c | ks) != 0);
-            mma(tmem + G::T_GRAM, dh, dl, G::ID_GRAM, 1);
-            mma(tmem + G::T_GRAM, dl, dh, G::ID_GRAM, 1);
+            mma(tmem + G::T_GRAM, dh, dl, G::ID_GRAM, 1);            // XL_GRAM2: dl holds 2 Zl
+            if (!XL_GRAM2) mma(tmem + G::T_GRAM, dl, dh, G::ID_GRAM, 1);
           }
           commit(&sm->stage_free[s]);
           item_stamp(i, 3);

@@ -86,8 +86,12 @@ def _check(H, out, alpha, power, method, T, variant):
         G, be, g, s = O.precoder_and_se(Hn[b], alpha, power, 1.0, method, T, variant)
         wt, st = W_TOL, SE_TOL
         if variant == "algorithm" or method == "cg":
+            # the diverging Algorithm-1 recurrence amplifies round-off
+            # chaotically: two fp32-level executions differ by up to ~30x the
+            # distance of one of them from the complex128 oracle
+            fac = 30 if variant == "algorithm" else 10
             ws, ss = _fp32_sensitivity(Hn[b], alpha, power, method, T, variant)
-            wt, st = max(W_TOL, 10 * ws), max(SE_TOL, 10 * ss)
+            wt, st = max(W_TOL, fac * ws), max(SE_TOL, fac * ss)
         assert relf(W[b], G) <= wt, (b, relf(W[b], G), wt)
         assert abs(S[b] - s) <= st * abs(s), (b, S[b], s, st)
         if variant == "algorithm":
