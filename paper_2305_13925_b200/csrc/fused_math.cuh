@@ -536,3 +536,78 @@ __device__ __forceinline__ void w_epilogue(const Params& p, Small* sm, uint32_t 
     for (int a = 0; a < CH; ++a) __stcs(wp + a * NC, d[a] * wscale);
   }
 }
+
+// 20-warp layout (K = 64): half of one chunk's W^T epilogue, CH/2 antennas
+// starting at a0, TMEM lane quadrant warp & 3; two warps share a quadrant.
+template <int KU>
+__device__ __forceinline__ void w_epilogue_half(const Params& p, Small* sm, uint32_t tmem, int64_t b, int c,
+                                                uint32_t j, uint32_t parity, uint32_t kpar, int a0,
+                                                long long* tr = nullptr) {
+  using G = Geo<KU>;
+  constexpr int NC = G::NC, CH = G::CH, HALF = CH / 2;
+  const int q = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
+  const int r = 32 * q + lane;
+  const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + (j ? G::T_W1 : G::T_W0) + a0;
+  mbar_wait(&sm->wfull[j], parity);
+  if (XL_TRACE && tr && threadIdx.x == 0) tr[6] = clock64();
+  const float wscale = sm->wsc[kpar][0], fscale = sm->wsc[kpar][1];
+  tc_after();
+  float d[HALF];
+  if (32 * q < NC) {
+    tmem_ld<HALF>(tl, d);
+    tmem_wait_ld();
+  }
+  tc_before();
+  mbar_arrive(&sm->wfree[j]);
+  if (XL_TRACE && tr && threadIdx.x == 0) tr[7] = clock64();
+  if (r < NC && !(p.dbg & 8)) {
+    const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH + a0) * NC + r;
+    float* wp = reinterpret_cast<float*>(p.W) + o0;
+#pragma unroll
+    for (int a = 0; a < HALF; ++a) __stcs(wp + a * NC, d[a] * wscale);
+    if (p.F) {
+      float* fp = reinterpret_cast<float*>(p.F) + o0;
+#pragma unroll
+      for (int a = 0; a < HALF; ++a) __stcs(fp + a * NC, d[a] * fscale);
+    }
+  }
+}
+
+// Whole-chunk W^T epilogue in two 32-antenna halves (register-lean: the
+// 20-warp layout gives the streaming warps 64 registers); the accumulator is
+// released after the second TMEM read.
+template <int KU>
+__device__ __forceinline__ void w_epilogue_halves(const Params& p, Small* sm, uint32_t tmem, int64_t b, int c,
+                                                  uint32_t j, uint32_t parity, uint32_t kpar) {
+  using G = Geo<KU>;
+  constexpr int NC = G::NC, CH = G::CH, HALF = CH / 2;
+  const int q = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
+  const int r = 32 * q + lane;
+  const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + (j ? G::T_W1 : G::T_W0);
+  mbar_wait(&sm->wfull[j], parity);
+  const float wscale = sm->wsc[kpar][0], fscale = sm->wsc[kpar][1];
+  tc_after();
+  const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH) * NC + r;
+#pragma unroll 1
+  for (int a0 = 0; a0 < CH; a0 += HALF) {
+    float d[HALF];
+    if (32 * q < NC) {
+      tmem_ld<HALF>(tl + a0, d);
+      tmem_wait_ld();
+    }
+    if (a0 + HALF == CH) {
+      tc_before();
+      mbar_arrive(&sm->wfree[j]);
+    }
+    if (r < NC && !(p.dbg & 8)) {
+      float* wp = reinterpret_cast<float*>(p.W) + o0 + (int64_t)a0 * NC;
+#pragma unroll
+      for (int a = 0; a < HALF; ++a) __stcs(wp + a * NC, d[a] * wscale);
+      if (p.F) {
+        float* fp = reinterpret_cast<float*>(p.F) + o0 + (int64_t)a0 * NC;
+#pragma unroll
+        for (int a = 0; a < HALF; ++a) __stcs(fp + a * NC, d[a] * fscale);
+      }
+    }
+  }
+}

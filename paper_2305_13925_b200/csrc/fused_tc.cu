@@ -236,7 +236,6 @@ __device__ __forceinline__ float warp_transpose_reduce(float (&v)[N]) {
 // ----------------------------------------------------------- geometry ----
 constexpr int NCONV = 4, NMATH = 8;
 constexpr int W_MMA = NCONV + NMATH, W_PROD = W_MMA + 1;
-constexpr int NTHREADS = 512;  // 16 warps = 4 warpgroups (setmaxnreg granularity)
 constexpr int BAR_CONV = 1, BAR_MATH = 2, BAR_EPI = 3;
 // Converter warps: 0..3 plus the two spare warps of warpgroup 3 (14, 15).
 #ifndef XL_WSTAGE
@@ -251,12 +250,34 @@ constexpr int BAR_CONV = 1, BAR_MATH = 2, BAR_EPI = 3;
 #ifndef XL_TRACE
 #define XL_TRACE 1  // clock64 phase stamps, enabled at run time by XL_FUSED_TRACE=<k0+1>
 #endif
-#ifndef XL_NCW
-#define XL_NCW 6
+#ifndef XL_WB_GRAM
+#define XL_WB_GRAM 1   // Gram TMEM columns double-buffer the W accumulator during W passes
 #endif
-constexpr int NCW = XL_NCW;
-__device__ __forceinline__ bool is_converter(int w) { return w < NCONV || (NCW > NCONV && w >= 16 - (NCW - NCONV) && w < 16); }
-__device__ __forceinline__ int conv_index(int w) { return w < NCONV ? w : NCONV + (w - (16 - (NCW - NCONV))); }
+#ifndef XL_WB_START
+#define XL_WB_START 2  // first W chunk that may use them (A(k+1) is usually built by then)
+#endif
+#ifndef XL_W20_EPI4
+#define XL_W20_EPI4 0  // 1: 20 warps but the W^T epilogue only on warps 0-3 (measured 6% slower)
+#endif
+#ifndef XL_W20
+#define XL_W20 1  // K = 64: a fifth warpgroup (warps 16-19) converts and drains W^T too
+#endif
+// Warp layout per K.  16 warps: converters 0-3 (one 8-antenna group per chunk,
+// plus the W^T epilogue) and 14, 15 (two groups).  20 warps (K = 64): eight
+// converters 0-3 and 16-19, one group each, each draining half of the W^T
+// accumulator of its lane quadrant; setmaxnreg moves registers from the
+// streaming warpgroups (64) to the math warpgroups (136).
+template <int KU>
+struct Lay {
+  static constexpr bool W20 = XL_W20 && KU == 64;
+  static constexpr int NT = W20 ? 640 : 512;
+  static constexpr int NCW = W20 ? 8 : 6;     // converter warps
+  static constexpr int NEPI = W20 ? 8 : 4;    // W^T epilogue warps
+  __device__ static bool is_conv(int w) { return w < NCONV || (W20 ? (w >= 16 && w < 20) : (w == 14 || w == 15)); }
+  __device__ static int conv_idx(int w) { return w < NCONV ? w : (W20 ? w - 12 : w - 10); }
+  __device__ static int g0(int cw) { return W20 ? cw : (cw < NCONV ? cw : NCONV + 2 * (cw - NCONV)); }
+  __device__ static int ng(int cw) { return (W20 || cw < NCONV) ? 1 : 2; }
+};
 constexpr int NMT = 32 * NMATH;               // math threads
 
 template <int KU>
@@ -305,10 +326,18 @@ struct Geo {
   // by tcgen05.cp so the MMAs re-read only their B operand from smem.
   static constexpr int NWB = (CH <= 32) ? 2 : 1;  // W accumulator buffers at T_W0
   static_assert(NWB * CH <= 64, "W accumulator columns");
-  static constexpr uint32_t T_GRAM = 0, T_Q = 128, T_W0 = 192, T_W1 = 192 + CH * (NWB - 1), T_X = 256,
-                            T_R = 320, T_XE = 384;
-  // W accumulator buffer of the wc-th W chunk
-  __device__ static int wsel(uint32_t wc) { return (int)(wc % NWB); }
+  // XL_WB_GRAM: with one buffer at T_W0, the Gram columns (free once A(k+1)
+  // is built, and until G(k+2) starts) are the second W buffer of W(k) from
+  // chunk XL_WB_START on.
+  static constexpr bool WB_GRAM = XL_WB_GRAM && NWB == 1;
+  static constexpr uint32_t T_GRAM = 0, T_Q = 128, T_W0 = 192, T_X = 256, T_R = 320, T_XE = 384;
+  static constexpr uint32_t T_W1 = NWB == 2 ? 192 + CH : T_GRAM;
+  // W accumulator buffer of chunk c, the wc-th W chunk of the CTA
+  __device__ static int wsel(int c, uint32_t wc) {
+    if (NWB == 2) return (int)(wc & 1);
+    if (!WB_GRAM) return 0;
+    return (c >= XL_WB_START && ((c - XL_WB_START) & 1) == 0) ? 1 : 0;
+  }
 };
 
 struct Params {
@@ -488,7 +517,7 @@ __device__ __forceinline__ void issue_kxk(uint32_t tq, uint32_t ah, uint32_t al,
 
 // ------------------------------------------------------------ kernel ----
 template <int KU>
-__global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
+__global__ void __launch_bounds__(Lay<KU>::NT, 1) fused_rzf_kernel(Params p) {
   using G = Geo<KU>;
   constexpr int NC = G::NC, JH = G::JH, HC = G::HC, NS = G::NS;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -506,7 +535,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sm->raw_full[s], 1);
-      mbar_init(&sm->conv_full[s], NCW);  // one arrival per converter warp
+      mbar_init(&sm->conv_full[s], Lay<KU>::NCW);  // one arrival per converter warp
       mbar_init(&sm->stage_free[s], 1);
     }
     mbar_init(&sm->gram_full, 1);
@@ -518,7 +547,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
     for (int q = 0; q < 4; ++q) mbar_init(&sm->bq_full[q], 1);
     for (int j = 0; j < 2; ++j) {
       mbar_init(&sm->wfull[j], 1);
-      mbar_init(&sm->wfree[j], 32 * NCONV);  // converter warps 0-3 run the W epilogue
+      mbar_init(&sm->wfree[j], 32 * ((Lay<KU>::W20 && XL_W20_EPI4) ? NCONV : Lay<KU>::NEPI));  // the W epilogue warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -556,6 +585,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
 #define XL_REG_MATH 176
 #endif
   static_assert(128 * XL_REG_AUX + 128 * XL_REG_CONV + 256 * XL_REG_MATH <= 65536, "register budget");
+  if (Lay<KU>::W20 && (warp < NCONV || warp >= NCONV + NMATH))
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");  // 640 threads launch with 96 each
 #if XL_USE_SETMAXNREG
   if (warp >= W_MMA) {  // warpgroup 3: MMA issuer, producer, 2 idle warps
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(XL_REG_AUX));
@@ -584,14 +615,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
     }
     return sm->bq[k & 3];
   };
-  auto for_items = [&](auto&& body) {  // body(kk, pass, b)
+  auto for_items = [&](auto&& body) {  // body(kk, pass, b, W pass: realization k+1 exists)
     int64_t bk = real_of(0);
     if (bk < 0) return;
-    body(0u, 0, bk);
+    body(0u, 0, bk, false);
     for (uint32_t k = 0;; ++k) {
       const int64_t bn = real_of(k + 1);
-      if (bn >= 0) body(k + 1, 0, bn);
-      if (!(p.dbg & 3)) body(k, 1, bk);
+      if (bn >= 0) body(k + 1, 0, bn, false);
+      if (!(p.dbg & 3)) body(k, 1, bk, bn >= 0);
       if (bn < 0) break;
       bk = bn;
     }
@@ -603,7 +634,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
       const uint64_t pol_first = policy_evict_first();
       const uint64_t pol_g = (p.l2mode & 3) == 0 ? pol_first : (p.l2mode & 3) == 1 ? policy_evict_normal()
                                                                                   : policy_evict_last();
-      for_items([&](uint32_t kk, int pass, int64_t b) {
+      for_items([&](uint32_t kk, int pass, int64_t b, bool) {
         const char* Hb = reinterpret_cast<const char*>(p.H + b * (int64_t)p.M * KU);
         for (int c = 0; c < nch; ++c, ++i) {
           const int s = i % NS;
@@ -620,25 +651,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
         }
       });
     }
-  } else if (is_converter(warp)) {
+  } else if (Lay<KU>::is_conv(warp)) {
     // ---------------------------------------------------- converters ------
-    const int cw = conv_index(warp);
+    const int cw = Lay<KU>::conv_idx(warp);
+    constexpr int NCW = Lay<KU>::NCW;
     uint32_t i = 0;
     float sz_par[2] = {1.0f, 1.0f};
     int have_par[2] = {0, 0};
     uint32_t wcv = 0;                 // W chunk counter (same sequence as the MMA issuer)
     uint32_t wuse_c[2] = {0, 0};
-    const bool epi = warp < NCONV;  // warps 0-3 also run the W^T epilogue
+    const bool epi = (Lay<KU>::W20 && !XL_W20_EPI4) || warp < NCONV;  // the W^T epilogue warps
     auto epilogue = [&](int64_t b, int c, uint32_t kc, uint32_t item) {
-      const uint32_t j = G::wsel(wcv);
+      const uint32_t j = G::wsel(c, wcv);
       const uint32_t i0 = 64 + 32 * (uint32_t)p.trace_k0;
       long long* tr = (XL_TRACE && p.trace && blockIdx.x == 0 && item >= i0 && item < i0 + 64)
                           ? p.trace + 256 + (item - i0) * 8 : nullptr;
-      w_epilogue<KU>(p, sm, tmem, wstg, b, c, j, wuse_c[j] & 1, kc & 1, tr);
+      if (Lay<KU>::W20 && XL_W20_EPI4)  // warps 0-3 drain the whole chunk in two halves
+        w_epilogue_halves<KU>(p, sm, tmem, b, c, j, wuse_c[j] & 1, kc & 1);
+      else if (Lay<KU>::W20)  // lane quadrant warp & 3; warps 0-3 the first antenna half, 16-19 the second
+        w_epilogue_half<KU>(p, sm, tmem, b, c, j, wuse_c[j] & 1, kc & 1, warp >= 16 ? G::CH / 2 : 0, tr);
+      else
+        w_epilogue<KU>(p, sm, tmem, wstg, b, c, j, wuse_c[j] & 1, kc & 1, tr);
       ++wuse_c[j];
       ++wcv;
     };
-    for_items([&](uint32_t kc, int pass, int64_t bcur) {
+    for_items([&](uint32_t kc, int pass, int64_t bcur, bool) {
       const int par = kc & 1;
       if (pass == 0) { sz_par[par] = 1.0f; have_par[par] = 0; }
       float sz = sz_par[par];
@@ -658,9 +695,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
           // (j, half)) and the uint2 writes (16-lane phases: distinct
           // (row, half)) bank-conflict free.
           constexpr int NG = G::CH / 8, GS = 2 * G::CMA, NIT = NC / 16;
-          static_assert(NCW == NCONV + 2 && NG == NCONV + 2 * (NCW - NCONV), "group split");
-          const int g0 = cw < NCONV ? cw : NCONV + 2 * (cw - NCONV);
-          const int ng = cw < NCONV ? 1 : 2;
+          static_assert(NG == (Lay<KU>::W20 ? 8 : NCONV + 2 * 2), "group split");
+          const int g0 = Lay<KU>::g0(cw), ng = Lay<KU>::ng(cw);
           auto coords = [&](int it, int& row, int& cc) {
             const int cs = it >> 1, ih = it & 1;
             row = (lane >> 1) & 7;
@@ -751,10 +787,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
     if (lane == 0) {
       uint32_t i = 0, wc = 0;
       uint32_t wuse[2] = {0, 0};
-      for_items([&](uint32_t k, int pass, int64_t) {
+      for_items([&](uint32_t k, int pass, int64_t, bool has_next) {
        if (pass == 0) {
         // the TMEM Gram accumulator is free once the math warps built A(k-1)
         if (k >= 1) mbar_wait(&sm->gram_free, (k - 1) & 1);
+        // ... and W epilogues that borrowed the Gram columns have drained them
+        if (G::WB_GRAM && wuse[1] >= 1) mbar_wait(&sm->wfree[1], (wuse[1] - 1) & 1);
         for (int c = 0; c < nch; ++c, ++i) {  // Gram
           const int s = i % NS;
           mbar_wait(&sm->conv_full[s], (i / NS) & 1);
@@ -784,7 +822,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
         commit(&sm->xe_consumed);  // smem Xe may now be overwritten by A(k+1)
         for (int c = 0; c < nch; ++c, ++i, ++wc) {  // W^T = Xe^T Z^T
           const int s = i % NS;
-          const int j = G::wsel(wc);
+          const int j = G::wsel(c, wc);
+          // first borrow of the Gram columns in W(k): A(k+1) has been built from them
+          if (G::WB_GRAM && c == XL_WB_START && has_next) mbar_wait(&sm->gram_free, (k + 1) & 1);
           if (wuse[j] >= 1) mbar_wait(&sm->wfree[j], (wuse[j] - 1) & 1);
           mbar_wait(&sm->conv_full[s], (i / NS) & 1);
           tc_after();
@@ -807,6 +847,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_rzf_kernel(Params p) {
       });
     }
   } else if (warp < NCONV + NMATH) {
+    if (Lay<KU>::W20) asm volatile("setmaxnreg.inc.sync.aligned.u32 136;");
     math_role<KU>(p, sm, aeh, ael, pbh, pbl, tmem, nch);
   }
   // the epilogue's W bulk stores (issued by warp 0 lane 0) complete before exit
@@ -842,7 +883,8 @@ static int launch_k(const tc::Params& p, cudaStream_t st) {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   int64_t grid = p.B < g_num_sms ? p.B : g_num_sms;
-  tc::fused_rzf_kernel<KU><<<(unsigned)grid, tc::NTHREADS, smem, st>>>(p);
+  if (const char* e = getenv("XL_FUSED_GRID")) grid = grid < atoi(e) ? grid : atoi(e);  // scaling experiments
+  tc::fused_rzf_kernel<KU><<<(unsigned)grid, tc::Lay<KU>::NT, smem, st>>>(p);
   return check_launch("fused_rzf_tc");
 }
 
