@@ -479,20 +479,16 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
   (void)wuse;
 }
 
-// W^T epilogue of one chunk, run by converter warps 0-3 (TMEM lane quadrant =
-// warp): thread = output component c2 = 32 q + lane, CH antennas.
-// XL_WSTAGE: each half of the tile (CH/2 antennas x NC components, row-major ==
-// the W rows in HBM) is written to its own smem staging buffer and leaves with
-// one 1-D bulk store, so the warps do not sit in the ~1 k-cycle store drain
-// (the per-SM store path moves ~32 B/cycle); a buffer is reused once the
-// previous chunk's store of it has been read out.  Otherwise 128-B coalesced
-// streaming stores per antenna.
+// W^T epilogue of one chunk (16-warp layout), run by converter warps 0-3
+// (TMEM lane quadrant = warp): thread = output component c2 = 32 q + lane, CH
+// antennas; 128-B coalesced streaming stores per antenna.  (Staging the tile in
+// smem for 1-D bulk stores measured no faster: the per-SM store path, ~32 B per
+// cycle, sets the pace, not the issuing warps.)
 template <int KU>
-__device__ __forceinline__ void w_epilogue(const Params& p, Small* sm, uint32_t tmem, uint8_t* wstg, int64_t b,
-                                           int c, uint32_t j, uint32_t parity, uint32_t kpar,
-                                           long long* tr = nullptr) {
+__device__ __forceinline__ void w_epilogue(const Params& p, Small* sm, uint32_t tmem, int64_t b, int c,
+                                           uint32_t j, uint32_t parity, uint32_t kpar, long long* tr = nullptr) {
   using G = Geo<KU>;
-  constexpr int NC = G::NC, CH = G::CH, HALF = CH / 2;
+  constexpr int NC = G::NC, CH = G::CH;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;  // warps 0-3 = lane quadrants
   const int r = 32 * warp + lane;
   const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16) + (j ? G::T_W1 : G::T_W0);
@@ -509,31 +505,16 @@ __device__ __forceinline__ void w_epilogue(const Params& p, Small* sm, uint32_t 
   tc_before();
   mbar_arrive(&sm->wfree[j]);
   if (XL_TRACE && tr && threadIdx.x == 0) tr[7] = clock64();
-  const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH) * NC;
-  if (p.F && r < NC) {
-    float* fp = reinterpret_cast<float*>(p.F) + o0 + r;
-#pragma unroll
-    for (int a = 0; a < CH; ++a) __stcs(fp + a * NC, d[a] * fscale);
-  }
-  if (XL_WSTAGE) {
-#pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
-      float* buf = reinterpret_cast<float*>(wstg + hf * HALF * NC * 4);
-      if (threadIdx.x == 0) bulk_wait_read<1>();  // this buffer's previous store has been read
-      named_sync(BAR_EPI, 32 * NCONV);
-      if (r < NC) {
-#pragma unroll
-        for (int a = 0; a < HALF; ++a) buf[a * NC + r] = d[hf * HALF + a] * wscale;
-      }
-      fence_async_smem();
-      named_sync(BAR_EPI, 32 * NCONV);
-      if (threadIdx.x == 0 && !(p.dbg & 8))
-        bulk_s2g(reinterpret_cast<float*>(p.W) + o0 + (int64_t)hf * HALF * NC, buf, HALF * NC * 4);
-    }
-  } else if (r < NC && !(p.dbg & 8)) {  // dbg & 8: timing without the W stores
-    float* wp = reinterpret_cast<float*>(p.W) + o0 + r;
+  if (r < NC && !(p.dbg & 8)) {  // dbg & 8: timing without the W stores
+    const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH) * NC + r;
+    float* wp = reinterpret_cast<float*>(p.W) + o0;
 #pragma unroll
     for (int a = 0; a < CH; ++a) __stcs(wp + a * NC, d[a] * wscale);
+    if (p.F) {
+      float* fp = reinterpret_cast<float*>(p.F) + o0;
+#pragma unroll
+      for (int a = 0; a < CH; ++a) __stcs(fp + a * NC, d[a] * fscale);
+    }
   }
 }
 
@@ -569,45 +550,6 @@ __device__ __forceinline__ void w_epilogue_half(const Params& p, Small* sm, uint
       float* fp = reinterpret_cast<float*>(p.F) + o0;
 #pragma unroll
       for (int a = 0; a < HALF; ++a) __stcs(fp + a * NC, d[a] * fscale);
-    }
-  }
-}
-
-// Whole-chunk W^T epilogue in two 32-antenna halves (register-lean: the
-// 20-warp layout gives the streaming warps 64 registers); the accumulator is
-// released after the second TMEM read.
-template <int KU>
-__device__ __forceinline__ void w_epilogue_halves(const Params& p, Small* sm, uint32_t tmem, int64_t b, int c,
-                                                  uint32_t j, uint32_t parity, uint32_t kpar) {
-  using G = Geo<KU>;
-  constexpr int NC = G::NC, CH = G::CH, HALF = CH / 2;
-  const int q = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
-  const int r = 32 * q + lane;
-  const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + (j ? G::T_W1 : G::T_W0);
-  mbar_wait(&sm->wfull[j], parity);
-  const float wscale = sm->wsc[kpar][0], fscale = sm->wsc[kpar][1];
-  tc_after();
-  const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH) * NC + r;
-#pragma unroll 1
-  for (int a0 = 0; a0 < CH; a0 += HALF) {
-    float d[HALF];
-    if (32 * q < NC) {
-      tmem_ld<HALF>(tl + a0, d);
-      tmem_wait_ld();
-    }
-    if (a0 + HALF == CH) {
-      tc_before();
-      mbar_arrive(&sm->wfree[j]);
-    }
-    if (r < NC && !(p.dbg & 8)) {
-      float* wp = reinterpret_cast<float*>(p.W) + o0 + (int64_t)a0 * NC;
-#pragma unroll
-      for (int a = 0; a < HALF; ++a) __stcs(wp + a * NC, d[a] * wscale);
-      if (p.F) {
-        float* fp = reinterpret_cast<float*>(p.F) + o0 + (int64_t)a0 * NC;
-#pragma unroll
-        for (int a = 0; a < HALF; ++a) __stcs(fp + a * NC, d[a] * fscale);
-      }
     }
   }
 }

@@ -105,15 +105,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (++spins > (1u << 24)) asm volatile("trap;");
   } while (!done);
 }
-// smem -> global 1-D bulk store, completion tracked by bulk groups
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(su32(src)), "r"(bytes)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-// wait until at most N committed bulk stores are still reading shared memory
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t hint) {
   asm volatile(
@@ -238,9 +229,6 @@ constexpr int NCONV = 4, NMATH = 8;
 constexpr int W_MMA = NCONV + NMATH, W_PROD = W_MMA + 1;
 constexpr int BAR_CONV = 1, BAR_MATH = 2, BAR_EPI = 3;
 // Converter warps: 0..3 plus the two spare warps of warpgroup 3 (14, 15).
-#ifndef XL_WSTAGE
-#define XL_WSTAGE 0  // 1: W^T tiles leave through a smem staging area + bulk stores (measured no faster)
-#endif
 #ifndef XL_GRAM2
 #define XL_GRAM2 1  // Gram pass accumulates U = Zh^T (Zh + 2 Zl): 2 MMAs per K-step instead of 3
 #endif
@@ -255,9 +243,6 @@ constexpr int BAR_CONV = 1, BAR_MATH = 2, BAR_EPI = 3;
 #endif
 #ifndef XL_WB_START
 #define XL_WB_START 2  // first W chunk that may use them (A(k+1) is usually built by then)
-#endif
-#ifndef XL_W20_EPI4
-#define XL_W20_EPI4 0  // 1: 20 warps but the W^T epilogue only on warps 0-3 (measured 6% slower)
 #endif
 #ifndef XL_W20
 #define XL_W20 1  // K = 64: a fifth warpgroup (warps 16-19) converts and drains W^T too
@@ -303,15 +288,12 @@ struct Geo {
   static constexpr int SMALL_BYTES = 3072;
   static constexpr int SLACK = NC < 128 ? 2048 : 0;  // M-padded Gram reads past the last tile
   static constexpr int SMEM_MAX = 227 * 1024;
-  // W^T staging for the epilogue's bulk stores: two buffers of CH/2 antennas
-  static constexpr int WSTG = XL_WSTAGE ? SB : 0;
-  static constexpr int NS_FIT = (SMEM_MAX - 2 * AEPART - 2 * PBPART - SMALL_BYTES - SLACK - WSTG) / SB;
+  static constexpr int NS_FIT = (SMEM_MAX - 2 * AEPART - 2 * PBPART - SMALL_BYTES - SLACK) / SB;
   static constexpr int NS = NS_FIT < XL_NS_MAX ? NS_FIT : XL_NS_MAX;  // ring depth: 4 x 32 KB at K = 64
   static_assert(NS >= 3, "ring depth");
   static constexpr int OFF_AE = NS * SB + SLACK;
   static constexpr int OFF_PB = OFF_AE + 2 * AEPART;
-  static constexpr int OFF_WSTG = OFF_PB + 2 * PBPART;
-  static constexpr int OFF_SMALL = OFF_WSTG + WSTG;
+  static constexpr int OFF_SMALL = OFF_PB + 2 * PBPART;
   static constexpr int SMEM = OFF_SMALL + SMALL_BYTES;
   static constexpr int JH = KU / 2;          // PCG columns per math thread
   static constexpr int HC = NC / 2;          // Gram columns per math thread
@@ -526,7 +508,6 @@ __global__ void __launch_bounds__(Lay<KU>::NT, 1) fused_rzf_kernel(Params p) {
   uint8_t* ael = aeh + G::AEPART;
   uint8_t* pbh = smem + G::OFF_PB;
   uint8_t* pbl = pbh + G::PBPART;
-  uint8_t* wstg = smem + G::OFF_WSTG;
   Small* sm = reinterpret_cast<Small*>(smem + G::OFF_SMALL);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -547,7 +528,7 @@ __global__ void __launch_bounds__(Lay<KU>::NT, 1) fused_rzf_kernel(Params p) {
     for (int q = 0; q < 4; ++q) mbar_init(&sm->bq_full[q], 1);
     for (int j = 0; j < 2; ++j) {
       mbar_init(&sm->wfull[j], 1);
-      mbar_init(&sm->wfree[j], 32 * ((Lay<KU>::W20 && XL_W20_EPI4) ? NCONV : Lay<KU>::NEPI));  // the W epilogue warps
+      mbar_init(&sm->wfree[j], 32 * Lay<KU>::NEPI);  // the W epilogue warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -579,23 +560,10 @@ __global__ void __launch_bounds__(Lay<KU>::NT, 1) fused_rzf_kernel(Params p) {
     if (XL_TRACE && p.trace && blockIdx.x == 0 && kk >= (uint32_t)p.trace_k0 && kk < (uint32_t)p.trace_k0 + 8)
       p.trace[(kk - p.trace_k0) * 32 + slot] = clock64();
   };
-#ifndef XL_REG_AUX
-#define XL_REG_AUX 56
-#define XL_REG_CONV 104
-#define XL_REG_MATH 176
-#endif
-  static_assert(128 * XL_REG_AUX + 128 * XL_REG_CONV + 256 * XL_REG_MATH <= 65536, "register budget");
+  // 20-warp layout: 640 threads launch with 96 registers each; the streaming
+  // warpgroups give theirs down to 64 so the math warpgroups can take 136
   if (Lay<KU>::W20 && (warp < NCONV || warp >= NCONV + NMATH))
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");  // 640 threads launch with 96 each
-#if XL_USE_SETMAXNREG
-  if (warp >= W_MMA) {  // warpgroup 3: MMA issuer, producer, 2 idle warps
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(XL_REG_AUX));
-  } else if (warp < NCONV) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(XL_REG_CONV));
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(XL_REG_MATH));
-  }
-#endif
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
   // Stream order of ring items (software pipeline across this CTA's
   // realizations k = 0, 1, ...):  G(0), then for every k: G(k+1), W(k).
   // G(k+1) streams while the math warps run PCG(k); W(k) needs X(k).
@@ -660,18 +628,16 @@ __global__ void __launch_bounds__(Lay<KU>::NT, 1) fused_rzf_kernel(Params p) {
     int have_par[2] = {0, 0};
     uint32_t wcv = 0;                 // W chunk counter (same sequence as the MMA issuer)
     uint32_t wuse_c[2] = {0, 0};
-    const bool epi = (Lay<KU>::W20 && !XL_W20_EPI4) || warp < NCONV;  // the W^T epilogue warps
+    const bool epi = Lay<KU>::W20 || warp < NCONV;  // the W^T epilogue warps
     auto epilogue = [&](int64_t b, int c, uint32_t kc, uint32_t item) {
       const uint32_t j = G::wsel(c, wcv);
       const uint32_t i0 = 64 + 32 * (uint32_t)p.trace_k0;
       long long* tr = (XL_TRACE && p.trace && blockIdx.x == 0 && item >= i0 && item < i0 + 64)
                           ? p.trace + 256 + (item - i0) * 8 : nullptr;
-      if (Lay<KU>::W20 && XL_W20_EPI4)  // warps 0-3 drain the whole chunk in two halves
-        w_epilogue_halves<KU>(p, sm, tmem, b, c, j, wuse_c[j] & 1, kc & 1);
-      else if (Lay<KU>::W20)  // lane quadrant warp & 3; warps 0-3 the first antenna half, 16-19 the second
+      if (Lay<KU>::W20)  // lane quadrant warp & 3; warps 0-3 the first antenna half, 16-19 the second
         w_epilogue_half<KU>(p, sm, tmem, b, c, j, wuse_c[j] & 1, kc & 1, warp >= 16 ? G::CH / 2 : 0, tr);
       else
-        w_epilogue<KU>(p, sm, tmem, wstg, b, c, j, wuse_c[j] & 1, kc & 1, tr);
+        w_epilogue<KU>(p, sm, tmem, b, c, j, wuse_c[j] & 1, kc & 1, tr);
       ++wuse_c[j];
       ++wcv;
     };
@@ -850,8 +816,6 @@ __global__ void __launch_bounds__(Lay<KU>::NT, 1) fused_rzf_kernel(Params p) {
     if (Lay<KU>::W20) asm volatile("setmaxnreg.inc.sync.aligned.u32 136;");
     math_role<KU>(p, sm, aeh, ael, pbh, pbl, tmem, nch);
   }
-  // the epilogue's W bulk stores (issued by warp 0 lane 0) complete before exit
-  if (XL_WSTAGE && warp == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
   cta_stamp(1);
   if (warp == 0) {
