@@ -157,6 +157,12 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+// a fraction f of the lines (by address) evict_last, the rest evict_first
+__device__ __forceinline__ uint64_t policy_keep_fraction(float f) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;" : "=l"(pol) : "f"(f));
+  return pol;
+}
 __device__ __forceinline__ uint64_t policy_evict_normal() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
@@ -600,8 +606,10 @@ __global__ void __launch_bounds__(Lay<KU>::NT, 1) fused_rzf_kernel(Params p) {
     if (lane == 0) {
       uint32_t i = 0;
       const uint64_t pol_first = policy_evict_first();
-      const uint64_t pol_g = (p.l2mode & 3) == 0 ? pol_first : (p.l2mode & 3) == 1 ? policy_evict_normal()
-                                                                                  : policy_evict_last();
+      const uint64_t pol_g = (p.l2mode & 32) ? policy_keep_fraction(((p.l2mode & 15) + 1) / 16.0f)
+                             : (p.l2mode & 3) == 0 ? pol_first
+                             : (p.l2mode & 3) == 1 ? policy_evict_normal()
+                                                   : policy_evict_last();
       for_items([&](uint32_t kk, int pass, int64_t b, bool) {
         const char* Hb = reinterpret_cast<const char*>(p.H + b * (int64_t)p.M * KU);
         for (int c = 0; c < nch; ++c, ++i) {
