@@ -35,6 +35,7 @@ typedef struct CUstream_st* xl_stream_t; /* == cudaStream_t */
 
 enum { XL_C64 = 0, XL_C128 = 1 };
 enum { XL_JACPCG = 0, XL_CG = 1, XL_DIRECT = 2 };          /* precoder.py:109-115 */
+enum { XL_JOR = 3, XL_GS = 4 };  /* stationary splittings, ITERATIVE_SOLVERS linsolve.py:310-315 */
 enum { XL_TEXTBOOK = 0, XL_ALGORITHM = 1 };                /* linsolve.py:209-213 */
 
 enum {
@@ -90,6 +91,19 @@ int xl_solve(int dtype, int method, int variant, const void* A, int64_t B,
              double eps, void* X, int32_t* iterations, double* trace,
              void* iterates, int32_t* status, void* workspace,
              size_t ws_bytes, xl_stream_t stream);
+
+/* Stationary iterative solvers on the same batched layout and workspace
+ * (xl_solve_workspace_bytes):
+ *   XL_JOR: w <- w + omega (s - P w) / diag(P)  -- replaces jor_solve (linsolve.py:154-176)
+ *   XL_GS : (D + Lo) w' = s - Up w              -- replaces gs_solve  (linsolve.py:128-151)
+ * A zero diagonal entry sets status XL_STATUS_SPLITTING (_check_diag :120-125);
+ * omega <= 0 or T < 1 -> XL_ERR_CONFIG (ConfigurationError).  S, w0, eps, X,
+ * iterations, trace, iterates, status as in xl_solve. */
+int xl_solve_stationary(int dtype, int method, const void* A, int64_t B, int32_t K,
+                        const void* S, int32_t R, const void* w0, double omega,
+                        int32_t T, double eps, void* X, int32_t* iterations,
+                        double* trace, void* iterates, int32_t* status,
+                        void* workspace, size_t ws_bytes, xl_stream_t stream);
 
 /* The fused hot path, per realization b:
  *   A = H^H H + xi I; X ~= A^{-1} (Jac-PCG / CG with T iterations, identity

@@ -211,6 +211,66 @@ def jacpcg_solve(P, rhs, T, eps=None, w0=None, precond_diag=None,
 # precoder.py / metrics.py restatement
 # ---------------------------------------------------------------------------
 
+def _check_diag(P):
+    """linsolve.py:120-125: exact zero on the (complex) diagonal."""
+    d = np.diag(P)
+    if np.any(d == 0):
+        raise OracleError("SplittingError", f"zero diagonal entry at index {int(np.argmin(np.abs(d)))}")
+    return d
+
+
+def gs_solve(P, rhs, T, w0=None, eps=None, keep_iterates=False):
+    """linsolve.py:128-151: Gauss-Seidel, w' = (D + Lo)^{-1} (s - Up w).
+
+    The reference calls scipy's solve_triangular; this restatement does the
+    forward substitution explicitly (row i: w_i = (r_i - sum_{l<i} P_il w_l) / P_ii).
+    """
+    if T < 1:
+        raise OracleError("ConfigurationError", f"iteration count T must be >= 1, got {T}")
+    P = np.asarray(P, dtype=complex)
+    _check_diag(P)
+    s2, w, was_1d, snorm2 = _prepare(rhs, w0)
+    n = P.shape[0]
+    Up = np.triu(P, 1)
+    trace = [_ls_error(P, w, s2, snorm2)]
+    iterates, it = [], 0
+    for t in range(1, T + 1):
+        r = s2 - Up @ w
+        wn = np.empty_like(r)
+        for i in range(n):
+            wn[i] = (r[i] - P[i, :i] @ wn[:i]) / P[i, i]
+        w = wn
+        it = t
+        trace.append(_ls_error(P, w, s2, snorm2))
+        if keep_iterates:
+            iterates.append(w.copy())
+        if eps is not None and np.sqrt(trace[-1]) <= eps:
+            break
+    return _finish(w, was_1d, it, trace, _converged_flag(trace, eps), iterates)
+
+
+def jor_solve(P, rhs, T, omega=0.5, w0=None, eps=None, keep_iterates=False):
+    """linsolve.py:154-176: Jacobi over-relaxation w <- w + omega (s - P w) / d."""
+    if T < 1:
+        raise OracleError("ConfigurationError", f"iteration count T must be >= 1, got {T}")
+    if omega <= 0:
+        raise OracleError("ConfigurationError", f"relaxation omega must be positive, got {omega}")
+    P = np.asarray(P, dtype=complex)
+    d = _check_diag(P)[:, None]
+    s2, w, was_1d, snorm2 = _prepare(rhs, w0)
+    trace = [_ls_error(P, w, s2, snorm2)]
+    iterates, it = [], 0
+    for t in range(1, T + 1):
+        w = w + omega * ((s2 - P @ w) / d)
+        it = t
+        trace.append(_ls_error(P, w, s2, snorm2))
+        if keep_iterates:
+            iterates.append(w.copy())
+        if eps is not None and np.sqrt(trace[-1]) <= eps:
+            break
+    return _finish(w, was_1d, it, trace, _converged_flag(trace, eps), iterates)
+
+
 def gram_regularized(H, xi):
     """precoder.py:53-61: P = H^H H + xi I, symmetrised; rhs = I."""
     if xi <= 0:

@@ -17,7 +17,7 @@ from .errors import (AssemblyError, ConfigurationError, DegenerateChannelError, 
                      GeometryInfeasibleError, ModelError, NotHpdError,
                      SplittingError, UnsupportedTopologyError, XlMimoError)
 from .linsolve import (ITERATIVE_SOLVERS, HpdSystem, SolverOutcome, cg_solve,  # noqa: F401
-                       direct_solve, jacpcg_solve)
+                       direct_solve, gs_solve, jacpcg_solve, jor_solve)
 from .metrics import LinkReport, coupling_matrix, sinr_eq9, sum_se  # noqa: F401
 from .precoder import (BlockPrecoder, PrecoderBlock, assemble_precoder,  # noqa: F401
                        build_precoder, gram_regularized, rzf_block, rzf_direct,

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_native",
 
 XL_C64, XL_C128 = 0, 1
 XL_JACPCG, XL_CG, XL_DIRECT = 0, 1, 2
+XL_JOR, XL_GS = 3, 4
 XL_TEXTBOOK, XL_ALGORITHM = 0, 1
 XL_SUCCESS, XL_ERR_CONFIG, XL_ERR_CUDA, XL_ERR_UNSUPPORTED, XL_ERR_WORKSPACE = 0, 1, 2, 3, 4
 XL_STATUS_RANGE = 6
@@ -60,6 +61,8 @@ _SIGNATURES = {
     "xl_solve_workspace_bytes": (_sz, [_int, _i64, _i32, _i32]),
     "xl_solve": (_int, [_int, _int, _int, _p, _i64, _i32, _p, _i32, _p, _p, _i32,
                         _i32, _f64, _p, _p, _p, _p, _p, _p, _sz, _p]),
+    "xl_solve_stationary": (_int, [_int, _int, _p, _i64, _i32, _p, _i32, _p, _f64, _i32, _f64,
+                                   _p, _p, _p, _p, _p, _p, _sz, _p]),
     "xl_rzf_workspace_bytes": (_sz, [_int, _int, _i64, _i32, _i32]),
     "xl_rzf": (_int, [_int, _int, _int, _p, _i64, _i32, _i32, _f64, _p, _f64, _i32,
                       _f64, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),

@@ -21,6 +21,8 @@ from .errors import ConfigurationError
 
 METHODS = {"jacpcg": L.XL_JACPCG, "cg": L.XL_CG, "direct": L.XL_DIRECT}
 VARIANTS = {"textbook": L.XL_TEXTBOOK, "algorithm": L.XL_ALGORITHM}
+# solve_batched also runs the stationary splittings (linsolve.py:128-176)
+SOLVE_METHODS = dict(METHODS, jor=L.XL_JOR, gs=L.XL_GS)
 
 
 def dtype_code(dt: torch.dtype) -> int:
@@ -196,11 +198,17 @@ def solve_batched(A: torch.Tensor, method: str = "jacpcg", T: int = 5, variant: 
                   S: torch.Tensor | None = None, w0: torch.Tensor | None = None,
                   precond: torch.Tensor | None = None, precond_identity: bool = False,
                   eps: float | None = None, trace: bool = False, iterates: bool = False,
-                  check: bool = True, stream=None) -> SolveBatch:
-    """Batched A_b X_b = S_b (S = identity when None): linsolve.py:109-294."""
+                  check: bool = True, stream=None, omega: float = 0.5) -> SolveBatch:
+    """Batched A_b X_b = S_b (S = identity when None): linsolve.py:109-294;
+    method "jor" (relaxation omega) / "gs" run the stationary splittings
+    (linsolve.py:128-176)."""
     lib = L.lib()
-    if method not in METHODS:
+    if method not in SOLVE_METHODS:
         raise ConfigurationError(f"unknown solver {method!r}")
+    if method in ("jor", "gs") and int(T) < 1:
+        raise ConfigurationError(f"iteration count T must be >= 1, got {T}")
+    if method == "jor" and not omega > 0:
+        raise ConfigurationError(f"relaxation omega must be positive, got {omega}")
     if variant not in VARIANTS:
         raise ConfigurationError(f"unknown PCG variant {variant!r}")
     _check_tensor(A, "A", 3)
@@ -230,11 +238,19 @@ def solve_batched(A: torch.Tensor, method: str = "jacpcg", T: int = 5, variant: 
     itr = torch.empty(B, Tn, K, R, dtype=A.dtype, device=dev) if iterates else None
     nbytes = int(lib.xl_solve_workspace_bytes(dc, B, K, R))
     ws = _WS.get(dev, nbytes)
-    rc = lib.xl_solve(dc, METHODS[method], VARIANTS[variant], L.ptr(A), B, K, L.ptr(S), R,
-                      L.ptr(w0), L.ptr(precond), int(bool(precond_identity)), int(T),
-                      -1.0 if eps is None else float(eps), L.ptr(X), L.ptr(its), L.ptr(tr),
-                      L.ptr(itr), L.ptr(st), L.ptr(ws), ws.numel(), L.stream_ptr(stream))
-    L.check(rc, "xl_solve")
+    if method in ("jor", "gs"):
+        rc = lib.xl_solve_stationary(dc, SOLVE_METHODS[method], L.ptr(A), B, K, L.ptr(S), R,
+                                     L.ptr(w0), float(omega), int(T),
+                                     -1.0 if eps is None else float(eps), L.ptr(X), L.ptr(its),
+                                     L.ptr(tr), L.ptr(itr), L.ptr(st), L.ptr(ws), ws.numel(),
+                                     L.stream_ptr(stream))
+        L.check(rc, "xl_solve_stationary")
+    else:
+        rc = lib.xl_solve(dc, METHODS[method], VARIANTS[variant], L.ptr(A), B, K, L.ptr(S), R,
+                          L.ptr(w0), L.ptr(precond), int(bool(precond_identity)), int(T),
+                          -1.0 if eps is None else float(eps), L.ptr(X), L.ptr(its), L.ptr(tr),
+                          L.ptr(itr), L.ptr(st), L.ptr(ws), ws.numel(), L.stream_ptr(stream))
+        L.check(rc, "xl_solve")
     if check:
         L.raise_status(st.cpu().numpy(), "solve_batched")
     return SolveBatch(X, its, st, tr, itr)

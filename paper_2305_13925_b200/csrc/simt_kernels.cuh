@@ -37,6 +37,7 @@ struct SolveArgs {
   int T; double eps;             // eps < 0 -> None
   void* X; int32_t* iterations; double* trace; void* iterates; int32_t* status;
   void* ws; size_t ws_bytes;
+  double omega = 0.5;            // XL_JOR relaxation
 };
 template <typename R> size_t solve_ws_bytes(int64_t B, int K, int Rcols);
 template <typename R> int launch_solve(const SolveArgs& a, cudaStream_t st);

@@ -23,7 +23,8 @@ constexpr int ST = 256;  // threads per solver CTA
 template <typename C> __device__ __forceinline__ auto dotc_re(C a, C b) { return a.x * b.x + a.y * b.y; }
 
 // out[:, j] = A * in[:, j], j < Rc; A row-major K x K; in/out column-major.
-template <typename R>
+// UPPER: only the strict upper triangle of A (Gauss-Seidel's Up, linsolve.py:139).
+template <typename R, bool UPPER = false>
 __device__ void cta_gemm(const cplx<R>* __restrict__ A, const cplx<R>* in, cplx<R>* out,
                          int K, int Rc, cplx<R> (*As)[33], cplx<R> (*Ms)[33]) {
   using C = cplx<R>;
@@ -41,7 +42,7 @@ __device__ void cta_gemm(const cplx<R>* __restrict__ A, const cplx<R>* in, cplx<
         for (int p = 0; p < 2; ++p) {
           int e = tid + p * ST, r = e / 16, l = e % 16;
           C va = mk<R>(0, 0), vm = mk<R>(0, 0);
-          if (i0 + r < K && l0 + l < K) va = A[(int64_t)(i0 + r) * K + l0 + l];
+          if (i0 + r < K && l0 + l < K && (!UPPER || l0 + l > i0 + r)) va = A[(int64_t)(i0 + r) * K + l0 + l];
           if (j0 + r < Rc && l0 + l < K) vm = in[(int64_t)(j0 + r) * K + l0 + l];
           As[l][r] = va;
           Ms[l][r] = vm;
@@ -390,6 +391,149 @@ chol_kernel(SolveArgs a) {
   if (tid == 0) a.iterations[b] = 0;
 }
 
+// numpy's complex division (Smith's scaling, multiply by the reciprocal), so a
+// real divisor gives the same rounding as the reference's (s - P w) / d.
+template <typename R>
+__device__ __forceinline__ cplx<R> cdiv_np(cplx<R> a, cplx<R> d) {
+  const R ar = fabs(d.x), ai = fabs(d.y);
+  if (ar >= ai) {
+    const R rat = d.y / d.x, scl = (R)1 / (d.x + d.y * rat);
+    return mk<R>((a.x + a.y * rat) * scl, (a.y - a.x * rat) * scl);
+  }
+  const R rat = d.x / d.y, scl = (R)1 / (d.y + d.x * rat);
+  return mk<R>((a.x * rat + a.y) * scl, (a.y * rat - a.x) * scl);
+}
+
+// Stationary splittings, one CTA per realization (linsolve.py:128-176):
+//   XL_JOR: w <- w + omega * (s - P w) / diag(P)                  (:154-176)
+//   XL_GS : w <- (D + Lo)^{-1} (s - Up w), forward substitution    (:128-151)
+// Zero diagonal -> SplittingError (_check_diag :120-125).  Trace, eps stop and
+// iterates as in the Krylov kernel; no curvature checks (the reference has none).
+template <typename R>
+__global__ void __launch_bounds__(ST)
+stationary_kernel(SolveArgs a, double omega) {
+  using C = cplx<R>;
+  const int64_t b = blockIdx.x;
+  const int K = a.K, Rc = a.R;
+  const C* A = (const C*)a.A + b * (int64_t)K * K;
+  const C* S = a.S ? (const C*)a.S + b * (int64_t)K * Rc : nullptr;
+  const int64_t per = (int64_t)K * Rc;
+  C* Xw = (C*)a.ws + b * 4 * per;
+  C* Qw = Xw + per;
+  C* Rw = Qw + per;
+  __shared__ C As[16][33], Ms[16][33];
+  extern __shared__ double dyn[];
+  double* colpart = dyn;
+  __shared__ int zero_diag;
+  __shared__ double snorm2, sh_tr;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool gs = a.method == XL_GS;
+  const bool want_trace = a.trace != nullptr || a.eps >= 0.0;
+  if (tid == 0) zero_diag = 0;
+  __syncthreads();
+  for (int i = tid; i < K; i += ST) {
+    const C d = A[(int64_t)i * K + i];
+    if (d.x == (R)0 && d.y == (R)0) zero_diag = 1;
+  }
+  for (int j = warp; j < Rc; j += ST / 32) {  // ||S||^2 (linsolve.py:84-85)
+    double acc = 0.0;
+    for (int i = lane; i < K; i += 32) acc += (double)cabs2(rhs_at<R>(S, i, j, Rc));
+    acc = warp_sum(acc);
+    if (lane == 0) colpart[j] = acc;
+  }
+  __syncthreads();
+  if (zero_diag) {
+    if (tid == 0) { a.status[b] = XL_STATUS_SPLITTING; a.iterations[b] = 0; }
+    return;
+  }
+  if (tid == 0) {
+    double t = 0.0;
+    for (int j = 0; j < Rc; ++j) t += colpart[j];
+    snorm2 = t > 0.0 ? t : 1.0;
+  }
+  for (int64_t e = tid; e < per; e += ST) {
+    const int j = (int)(e / K), i = (int)(e % K);
+    Xw[e] = a.w0 ? ((const C*)a.w0)[b * per + (int64_t)i * Rc + j] : mk<R>(0, 0);
+  }
+  __syncthreads();
+  {
+    const double t0 = residual_norm2<R>(A, Xw, Qw, S, K, Rc, As, Ms, colpart);
+    if (a.trace && tid == 0) a.trace[b * (a.T + 1)] = t0 / snorm2;
+  }
+  int it = 0;
+  for (int t = 1; t <= a.T; ++t) {
+    if (!gs) {
+      cta_gemm<R>(A, Xw, Qw, K, Rc, As, Ms);  // P w
+      for (int64_t e = tid; e < per; e += ST) {
+        const int j = (int)(e / K), i = (int)(e % K);
+        const C u = cdiv_np<R>(csub(rhs_at<R>(S, i, j, Rc), Qw[e]), A[(int64_t)i * K + i]);
+        C x = Xw[e];
+        x.x = x.x + (R)omega * u.x;
+        x.y = x.y + (R)omega * u.y;
+        Xw[e] = x;
+      }
+    } else {
+      cta_gemm<R, true>(A, Xw, Qw, K, Rc, As, Ms);  // Up w
+      for (int64_t e = tid; e < per; e += ST) {
+        const int j = (int)(e / K), i = (int)(e % K);
+        Rw[e] = csub(rhs_at<R>(S, i, j, Rc), Qw[e]);
+      }
+      __syncthreads();
+      // (D + Lo) w = rhs: one warp per RHS column, lanes own rows l = lane + 32 m;
+      // step i finalises w_i and eliminates it from the rows below.
+      for (int j = warp; j < Rc; j += ST / 32) {
+        C* rj = Rw + (int64_t)j * K;
+        C* xj = Xw + (int64_t)j * K;
+        for (int i = 0; i < K; ++i) {
+          C wi = mk<R>(0, 0);
+          if (lane == (i & 31)) {
+            wi = cdiv_np<R>(rj[i], A[(int64_t)i * K + i]);
+            xj[i] = wi;
+          }
+          wi.x = __shfl_sync(0xffffffffu, wi.x, i & 31);
+          wi.y = __shfl_sync(0xffffffffu, wi.y, i & 31);
+          for (int l = i + 1 + ((lane - (i + 1)) & 31); l < K; l += 32) {
+            const C p = A[(int64_t)l * K + i];
+            C v = rj[l];
+            v.x = v.x - (p.x * wi.x - p.y * wi.y);
+            v.y = v.y - (p.x * wi.y + p.y * wi.x);
+            rj[l] = v;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    it = t;
+    double trt = 0.0;
+    if (want_trace) {
+      trt = residual_norm2<R>(A, Xw, Qw, S, K, Rc, As, Ms, colpart) / snorm2;
+      if (a.trace && tid == 0) a.trace[b * (a.T + 1) + t] = trt;
+    }
+    if (a.iterates) {
+      C* dst = (C*)a.iterates + (b * a.T + (t - 1)) * per;
+      for (int64_t e = tid; e < per; e += ST) {
+        const int j = (int)(e / K), i = (int)(e % K);
+        dst[(int64_t)i * Rc + j] = Xw[e];
+      }
+    }
+    if (tid == 0) sh_tr = trt;
+    __syncthreads();
+    if (a.eps >= 0.0 && sqrt(sh_tr) <= a.eps) break;  // linsolve.py:148-149, 173-174
+    __syncthreads();
+  }
+  __syncthreads();
+  C* Xo = (C*)a.X + b * per;
+  for (int64_t e = tid; e < per; e += ST) {
+    const int i = (int)(e / Rc), j = (int)(e % Rc);
+    Xo[e] = Xw[(int64_t)j * K + i];
+  }
+  if (tid == 0) {
+    a.iterations[b] = it;
+    if (a.trace)
+      for (int t = it + 1; t <= a.T; ++t) a.trace[b * (a.T + 1) + t] = __longlong_as_double(0x7ff8000000000000ll);
+  }
+}
+
 template <typename R> size_t solve_ws_bytes(int64_t B, int K, int Rc) {
   size_t per = (size_t)K * Rc;
   size_t pcg = 4 * per;
@@ -405,8 +549,9 @@ template <typename R> int launch_solve(const SolveArgs& a, cudaStream_t st) {
   size_t dyn = (size_t)a.R * sizeof(double) + ((size_t)a.R + a.K) * sizeof(R) + 16;
   if (dyn > 48 * 1024) { set_error("solve: too many columns (R=%d)", a.R); return XL_ERR_UNSUPPORTED; }
   if (a.method == XL_DIRECT) chol_kernel<R><<<(unsigned)a.B, ST, dyn, st>>>(a);
+  else if (a.method == XL_JOR || a.method == XL_GS) stationary_kernel<R><<<(unsigned)a.B, ST, dyn, st>>>(a, a.omega);
   else pcg_kernel<R><<<(unsigned)a.B, ST, dyn, st>>>(a);
-  return check_launch(a.method == XL_DIRECT ? "chol" : "pcg");
+  return check_launch(a.method == XL_DIRECT ? "chol" : a.method == XL_JOR || a.method == XL_GS ? "stationary" : "pcg");
 }
 
 template size_t solve_ws_bytes<float>(int64_t, int, int);

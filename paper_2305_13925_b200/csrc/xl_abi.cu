@@ -110,6 +110,24 @@ int xl_solve(int dtype, int method, int variant, const void* A, int64_t B, int32
   return dtype == XL_C64 ? launch_solve<float>(a, st) : launch_solve<double>(a, st);
 }
 
+int xl_solve_stationary(int dtype, int method, const void* A, int64_t B, int32_t K,
+                        const void* S, int32_t R, const void* w0, double omega, int32_t T,
+                        double eps, void* X, int32_t* iterations, double* trace, void* iterates,
+                        int32_t* status, void* workspace, size_t ws_bytes, xl_stream_t stream) {
+  if (int e = check_dtype(dtype)) return e;
+  if (method != XL_JOR && method != XL_GS) { set_error("unknown stationary method %d", method); return XL_ERR_CONFIG; }
+  if (T < 1) { set_error("iteration count T must be >= 1, got %d", T); return XL_ERR_CONFIG; }
+  if (method == XL_JOR && !(omega > 0)) { set_error("relaxation omega must be positive, got %g", omega); return XL_ERR_CONFIG; }
+  if (K < 1 || R < 1 || B < 0) { set_error("bad sizes"); return XL_ERR_CONFIG; }
+  if (!S && R != K) { set_error("identity RHS needs R == K"); return XL_ERR_CONFIG; }
+  if (B == 0) return XL_SUCCESS;
+  SolveArgs a{method, XL_TEXTBOOK, A, B, K, S, R, w0, nullptr, 0, T, eps,
+              X, iterations, trace, iterates, status, workspace, ws_bytes};
+  a.omega = omega;
+  cudaStream_t st = (cudaStream_t)stream;
+  return dtype == XL_C64 ? launch_solve<float>(a, st) : launch_solve<double>(a, st);
+}
+
 // ---------------------------------------------------------------------------
 // Fused precoder.  Workspace (SIMT path): A | X | solver ws (reused for the
 // coupling matrix) | ||F||^2 partials | iterations.

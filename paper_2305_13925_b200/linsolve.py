@@ -6,8 +6,8 @@ batched sm_100a solver (csrc/simt_solve.cu) with B = 1.  Numpy inputs are
 promoted to complex128 exactly like the reference (linsolve.py:74, 222, 262);
 a complex64 torch tensor keeps the fp32 path.
 
-gs_solve / jor_solve are outside the B200 hot path
-and raise ConfigurationError naming the supported solvers.
+gs_solve / jor_solve run the stationary-splitting
+kernel of the same file (xl_solve_stationary).
 """
 
 from __future__ import annotations
@@ -69,7 +69,7 @@ def _to_dev(x, dt):
 
 
 def _run(sys: HpdSystem, method, T, eps=None, w0=None, precond=None, precond_identity=False,
-         keep_iterates=False, variant="textbook") -> SolverOutcome:
+         keep_iterates=False, variant="textbook", omega=0.5) -> SolverOutcome:
     s = np.asarray(sys.rhs, dtype=complex)
     was_1d = s.ndim == 1
     s2 = s[:, None] if was_1d else s
@@ -86,7 +86,7 @@ def _run(sys: HpdSystem, method, T, eps=None, w0=None, precond=None, precond_ide
     C = torch.from_numpy(np.asarray(precond, dtype=np.float64))[None].to(A.device) if precond is not None else None
     res = BT.solve_batched(A, method, T=max(T, 1), variant=variant, S=S, w0=W0, precond=C,
                            precond_identity=precond_identity, eps=eps, trace=True,
-                           iterates=keep_iterates, check=True)
+                           iterates=keep_iterates, check=True, omega=omega)
     its = int(res.iterations[0].item())
     trace = res.trace[0].cpu().numpy()[: (its + 1) if method != "direct" else 1]
     X = res.X[0].cpu().numpy()
@@ -137,18 +137,36 @@ def jacpcg_solve(sys: HpdSystem, T: int, eps: float | None = None, w0=None,
                 variant=variant)
 
 
-def _out_of_scope(name):
-    def fn(*_a, **_k):
-        raise ConfigurationError(
-            f"solver {name!r} is not on the B200 path; supported: cg, jacpcg (+ direct)")
-    fn.__name__ = f"{name}_solve"
-    return fn
+def _check_diag(P) -> None:
+    """Zero diagonal entry -> SplittingError (linsolve.py:120-125)."""
+    d = np.diag(np.asarray(P))
+    if np.any(d == 0):
+        raise SplittingError(f"zero diagonal entry at index {int(np.argmin(np.abs(d)))}")
 
 
-gs_solve = _out_of_scope("gs")
-jor_solve = _out_of_scope("jor")
+def gs_solve(sys: HpdSystem, T: int, w0=None, eps: float | None = None,
+             keep_iterates: bool = False) -> SolverOutcome:
+    """Gauss-Seidel sweeps (D + Lo) w' = s - Up w (linsolve.py:128-151)."""
+    if T < 1:
+        raise ConfigurationError(f"iteration count T must be >= 1, got {T}")
+    _check_diag(sys.P)
+    return _run(sys, "gs", T, eps, w0, keep_iterates=keep_iterates)
 
-ITERATIVE_SOLVERS = {
+
+def jor_solve(sys: HpdSystem, T: int, omega: float = 0.5, w0=None,
+              eps: float | None = None, keep_iterates: bool = False) -> SolverOutcome:
+    """Jacobi over-relaxation w <- w + omega D^-1 (s - P w) (linsolve.py:154-176)."""
+    if T < 1:
+        raise ConfigurationError(f"iteration count T must be >= 1, got {T}")
+    if omega <= 0:
+        raise ConfigurationError(f"relaxation omega must be positive, got {omega}")
+    _check_diag(sys.P)
+    return _run(sys, "jor", T, eps, w0, keep_iterates=keep_iterates, omega=omega)
+
+
+ITERATIVE_SOLVERS = {  # linsolve.py:310-315
+    "gs": gs_solve,
+    "jor": jor_solve,
     "cg": cg_solve,
     "jacpcg": jacpcg_solve,
 }

@@ -24,7 +24,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 import xlmimo  # noqa: E402
 from xlmimo.channel import assemble_blocks, build_correlation, psd_sqrt  # noqa: E402
 from xlmimo.errors import XlMimoError  # noqa: E402
-from xlmimo.linsolve import HpdSystem, cg_solve, direct_solve, jacpcg_solve  # noqa: E402
+from xlmimo.linsolve import HpdSystem, cg_solve, direct_solve, gs_solve, jacpcg_solve, jor_solve  # noqa: E402
 from xlmimo.metrics import sinr_eq9, sum_se  # noqa: E402
 from xlmimo.precoder import BlockPrecoder, rzf_direct, rzf_iterative  # noqa: E402
 
@@ -119,6 +119,60 @@ def solver_cases():
     return out
 
 
+def stationary_cases():
+    """linsolve.py:128-176 pins: JOR (two omegas) and Gauss-Seidel on the same
+    system families as solver_cases, plus their error paths."""
+    rng = np.random.default_rng(20261020)
+    out = {}
+    idx = 0
+    for n in (4, 8, 16, 32):
+        for rep in range(2):
+            P = random_hpd(rng, n, cond_cap=20.0 if rep == 0 else 1e3)
+            if rep == 1:  # diagonally weighted: JOR/GS behave differently from the Krylov solvers
+                d = np.sqrt(np.logspace(0, 2, n))
+                P = (d[:, None] * P) * d[None, :]
+                P = (P + P.conj().T) / 2.0
+            for rhs_kind in ("eye", "vec", "multi"):
+                S = np.eye(n, dtype=complex) if rhs_kind == "eye" else (
+                    crandn(rng, n) if rhs_kind == "vec" else crandn(rng, n, 3))
+                w0 = None if rhs_kind != "multi" else 0.1 * crandn(rng, n, 3)
+                T = 6
+                sysm = HpdSystem(P=P, rhs=S)
+                pre = f"s{idx}_"
+                out[pre + "P"] = P
+                out[pre + "S"] = S
+                out[pre + "T"] = np.int64(T)
+                if w0 is not None:
+                    out[pre + "w0"] = w0
+                for name, fn in (
+                    ("jor05", lambda: jor_solve(sysm, T, omega=0.5, w0=w0, keep_iterates=True)),
+                    ("jor10", lambda: jor_solve(sysm, T, omega=1.0, w0=w0, keep_iterates=True)),
+                    ("gs", lambda: gs_solve(sysm, T, w0=w0, keep_iterates=True)),
+                    ("gseps", lambda: gs_solve(sysm, 40, w0=w0, eps=1e-5)),
+                ):
+                    o = fn()
+                    out[pre + name + "_w"] = o.w
+                    out[pre + name + "_trace"] = o.residual_trace
+                    out[pre + name + "_it"] = np.int64(o.iterations)
+                    out[pre + name + "_conv"] = np.bool_(o.converged)
+                    if o.iterates:
+                        out[pre + name + "_iterates"] = np.stack(o.iterates)
+                idx += 1
+    out["n_cases"] = np.int64(idx)
+    for name, fn in (
+        ("gs_zero_diag", lambda: gs_solve(HpdSystem(P=np.diag([0.0, 1.0]), rhs=np.ones(2)), 1)),
+        ("jor_zero_diag", lambda: jor_solve(HpdSystem(P=np.diag([1.0, 0.0]), rhs=np.ones(2)), 1)),
+        ("jor_omega", lambda: jor_solve(HpdSystem(P=np.eye(2), rhs=np.ones(2)), 1, omega=0.0)),
+        ("gs_T0", lambda: gs_solve(HpdSystem(P=np.eye(2), rhs=np.ones(2)), 0)),
+    ):
+        try:
+            fn()
+            out["err_" + name] = np.str_("none")
+        except XlMimoError as exc:
+            out["err_" + name] = np.str_(type(exc).__name__)
+    return out
+
+
 def precoder_cases():
     """precoder.py / metrics.py pins on BASELINE-model and random channels."""
     out = {}
@@ -201,14 +255,22 @@ def channel_cases():
     return out
 
 
-def main():
-    np.savez_compressed(os.path.join(HERE, "golden_solvers.npz"), **solver_cases())
-    np.savez_compressed(os.path.join(HERE, "golden_precoders.npz"), **precoder_cases())
-    np.savez_compressed(os.path.join(HERE, "golden_channel.npz"), **channel_cases())
+FIXTURES = {
+    "solvers": solver_cases,
+    "precoders": precoder_cases,
+    "channel": channel_cases,
+    "stationary": stationary_cases,
+}
+
+
+def main(names=None):
+    """python tests/golden/make_golden.py [fixture ...]  (default: all)"""
+    for name in names or FIXTURES:
+        np.savez_compressed(os.path.join(HERE, f"golden_{name}.npz"), **FIXTURES[name]())
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:])
