@@ -174,6 +174,17 @@ int xl_channel_generate(int dtype, uint64_t seed, int64_t first, int64_t B,
 int xl_se_partials(const double* sum_se, int64_t B, int64_t chunk,
                    double* partials, xl_stream_t stream);
 
+/* BER detection chain of ber_montecarlo (metrics.py:124-140) for a batch of
+ * channel draws: Y = Bc s + n with s = QPSK(bits) ((1-2b0) + j(1-2b1))/sqrt(2)
+ * (metrics.py:73-77), genie scaling by diag(Bc) with zero gains replaced by 1,
+ * hard decisions b = (Re < 0, Im < 0) (metrics.py:80-83), and the number of
+ * bit errors per draw.  Bc [B][K][K] (coupling, e.g. sinr's B = H^H G);
+ * bits [B][K][nsym][2] int8 in {0,1}; noise [B][K][nsym]; errors [B] int64
+ * (overwritten). */
+int xl_ber_errors(int dtype, const void* Bc, const int8_t* bits, const void* noise,
+                  int64_t B, int32_t K, int32_t nsym, int64_t* errors,
+                  xl_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -42,6 +42,9 @@ struct SolveArgs {
 template <typename R> size_t solve_ws_bytes(int64_t B, int K, int Rcols);
 template <typename R> int launch_solve(const SolveArgs& a, cudaStream_t st);
 
+int launch_ber(int dtype, const void* Bc, const int8_t* bits, const void* noise, int64_t B, int K,
+               int nsym, int64_t* errors, cudaStream_t st);
+
 int launch_channel(int dtype, uint64_t seed, int64_t first, int64_t B, int S, int Ms,
                    int K, double p, const double* Rsqrt, double gain_scale, double dmin,
                    double dmax, void* H, int32_t* status, cudaStream_t st);

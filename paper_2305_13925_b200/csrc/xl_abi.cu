@@ -296,4 +296,12 @@ int xl_se_partials(const double* sum_se, int64_t B, int64_t chunk, double* parti
   return launch_se_partials(sum_se, B, chunk, partials, (cudaStream_t)stream);
 }
 
+int xl_ber_errors(int dtype, const void* Bc, const int8_t* bits, const void* noise, int64_t B,
+                  int32_t K, int32_t nsym, int64_t* errors, xl_stream_t stream) {
+  if (int e = check_dtype(dtype)) return e;
+  if (K < 1 || nsym < 1 || B < 0) { set_error("bad sizes"); return XL_ERR_CONFIG; }
+  if (B == 0) return XL_SUCCESS;
+  return launch_ber(dtype, Bc, bits, noise, B, K, nsym, errors, (cudaStream_t)stream);
+}
+
 }  // extern "C"

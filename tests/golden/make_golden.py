@@ -173,6 +173,91 @@ def stationary_cases():
     return out
 
 
+def telemetry_cases():
+    """metrics.py:93-185 pins.
+
+    convergence_trace: the reference function itself on its default
+    configuration (trials = 6, T_max = 8), plus the central-subarray channel
+    Hc and QPSK right-hand side of every trial, extracted with the same
+    seed_stream / draw_trial sequence the function uses.
+    ber_montecarlo: one SNR point's inner loop, made of the reference's own
+    functions (draw_trial, _precoders_for_trial, coupling_matrix,
+    qpsk_modulate, qpsk_detect): coupling matrices, bits, noise and the error
+    counts, plus the reference function's own report for the same settings.
+    """
+    from xlmimo.config import ExperimentConfig
+    from xlmimo.metrics import (_precoders_for_trial, ber_montecarlo, convergence_trace,
+                                coupling_matrix, qpsk_detect, qpsk_modulate)
+    from xlmimo.scenario import build_scenario, draw_trial
+    from xlmimo.seeding import seed_stream
+
+    out = {}
+    cfg = ExperimentConfig()
+    cfg.run.trials, cfg.run.t_max = 6, 8
+    methods = ["gs", "jor", "cg", "jacpcg"]
+    med = convergence_trace(cfg, methods=methods)
+    scen = build_scenario(cfg)
+    Hc, S = [], []
+    for trial in range(cfg.run.trials):
+        rng = seed_stream(cfg.run.seed, trial)
+        draw = draw_trial(scen, rng)
+        bits = rng.integers(0, 2, size=(scen.K, 2), dtype=np.int8)
+        Hc.append(draw.realization.Hc)
+        S.append(qpsk_modulate(bits))
+    out["conv_Hc"] = np.stack(Hc)
+    out["conv_S"] = np.stack(S)
+    out["conv_xi"] = np.float64(cfg.power.xi)
+    out["conv_omega"] = np.float64(cfg.solver.omega)
+    out["conv_variant"] = np.str_(cfg.solver.pcg_variant)
+    out["conv_T"] = np.int64(cfg.run.t_max)
+    out["conv_methods"] = np.array(methods)
+    for m in methods:
+        out["conv_median_" + m] = med[m]
+
+    # BER: one grid point, the reference's loop body (metrics.py:124-140)
+    cfg = ExperimentConfig()
+    cfg.run.symbols_per_channel = 64
+    nsym = cfg.run.symbols_per_channel
+    grid = np.array([4.0, 10.0])
+    bmethods = ["direct", "jacpcg", "jor"]
+    scen = build_scenario(cfg)
+    K = scen.K
+    cfg.run.bits_per_point = 3 * 2 * K * nsym  # three channel draws per point
+    rep = ber_montecarlo(cfg, bmethods, snr_grid_db=grid)
+    sigma2 = cfg.power.sigma2_watts
+    for ig, snr_db in enumerate(grid):
+        snr = 10.0 ** (snr_db / 10.0)
+        xi, power = 1.0 / snr, sigma2 * snr
+        for trial in range(3):
+            rng = seed_stream(cfg.run.seed, trial * grid.size + ig)
+            draw = draw_trial(scen, rng)
+            pre = _precoders_for_trial(draw.realization, xi, power, bmethods, cfg.solver.T,
+                                       cfg.solver.omega, cfg.solver.pcg_variant)
+            bits = rng.integers(0, 2, size=(K, nsym, 2), dtype=np.int8)
+            noise = np.sqrt(sigma2 / 2.0) * (rng.standard_normal((K, nsym))
+                                             + 1j * rng.standard_normal((K, nsym)))
+            key = f"ber_p{ig}_t{trial}_"
+            out[key + "bits"] = bits
+            out[key + "noise"] = noise
+            out[key + "H"] = draw.realization.H
+            for m in bmethods:
+                Bm = coupling_matrix(draw.realization, pre[m])
+                gain = np.diag(Bm).copy()
+                gain[gain == 0] = 1.0
+                Y = Bm @ qpsk_modulate(bits) + noise
+                out[key + m + "_B"] = Bm
+                out[key + m + "_G"] = pre[m].G
+                out[key + m + "_errors"] = np.int64(np.count_nonzero(qpsk_detect(Y / gain[:, None]) != bits))
+    out["ber_grid"] = grid
+    out["ber_methods"] = np.array(bmethods)
+    out["ber_nsym"] = np.int64(nsym)
+    out["ber_sigma2"] = np.float64(sigma2)
+    for m in bmethods:
+        out["ber_report_errors_" + m] = rep.bit_errors[m]
+    out["ber_report_bits"] = np.int64(rep.bits_simulated)
+    return out
+
+
 def precoder_cases():
     """precoder.py / metrics.py pins on BASELINE-model and random channels."""
     out = {}
@@ -260,6 +345,7 @@ FIXTURES = {
     "precoders": precoder_cases,
     "channel": channel_cases,
     "stationary": stationary_cases,
+    "telemetry": telemetry_cases,
 }
 
 
