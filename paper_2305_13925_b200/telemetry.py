@@ -108,15 +108,10 @@ def ber_point_batched(H: torch.Tensor, xi, power: float, methods, bits: torch.Te
     """One SNR point on B paired draws (metrics.py:124-140) with single-block
     precoders: {method: errors [B]}.  Iterative methods use rzf_batched
     (jacpcg / cg / direct) or the stationary solvers (jor / gs)."""
+    from .blocks import precode_batched
     out = {}
     for m in methods:
-        if m in ("jacpcg", "cg", "direct"):
-            G = BT.rzf_batched(H, xi, power, method=m, T=T, variant=variant, want_gamma=False,
-                               check=True).W
-        else:
-            A = BT.gram_batched(H, xi, stream=stream)
-            X = BT.solve_batched(A, m, T=T, omega=omega, check=True, stream=stream).X
-            G = BT.apply_precoder_batched(H, X, power, check=True, stream=stream).W
+        G = precode_batched(H, xi, power, m, T=T, omega=omega, variant=variant, stream=stream).W
         Bc = BT.sinr_batched(H, G, 1.0, stream=stream).coupling
         out[m] = ber_errors_batched(Bc, bits, noise, stream=stream)
     return out

@@ -258,6 +258,42 @@ def telemetry_cases():
     return out
 
 
+def block_cases():
+    """precoder.py:118-146 + metrics.py:35-58 pins for the S=3/L=2 block
+    topology: the reference's own draws (default
+    configuration), build_precoder for every method with per-block beta, and
+    sinr_eq9 on the block coupling."""
+    from xlmimo.config import ExperimentConfig
+    from xlmimo.precoder import build_precoder
+    from xlmimo.scenario import build_scenario, draw_trial
+    from xlmimo.seeding import seed_stream
+
+    cfg = ExperimentConfig()
+    scen = build_scenario(cfg)
+    xi, power, sigma2 = cfg.power.xi, cfg.power.tx_power_watts, cfg.power.sigma2_watts
+    methods = ["direct", "jacpcg", "cg", "jor", "gs"]
+    out = {"xi": np.float64(xi), "power": np.float64(power), "sigma2": np.float64(sigma2),
+           "T": np.int64(cfg.solver.T), "omega": np.float64(cfg.solver.omega),
+           "variant": np.str_(cfg.solver.pcg_variant), "methods": np.array(methods)}
+    n = 0
+    for trial in range(8):
+        draw = draw_trial(scen, seed_stream(cfg.run.seed, trial))
+        r = draw.realization
+        key = f"r{trial}_"
+        out[key + "H1"], out[key + "Hc"], out[key + "H2"], out[key + "H"] = r.H1, r.Hc, r.H2, r.H
+        for m in methods:
+            bp = build_precoder(r, xi, power, m, T=cfg.solver.T, omega=cfg.solver.omega,
+                                pcg_variant=cfg.solver.pcg_variant)
+            rep = sinr_eq9(r, bp, sigma2)
+            out[key + m + "_G"] = bp.G
+            out[key + m + "_betas"] = np.array([bp.beta_1, bp.beta_c, bp.beta_2])
+            out[key + m + "_gamma"] = rep.gamma
+            out[key + m + "_sumse"] = np.float64(rep.sum_se)
+        n += 1
+    out["n"] = np.int64(n)
+    return out
+
+
 def precoder_cases():
     """precoder.py / metrics.py pins on BASELINE-model and random channels."""
     out = {}
@@ -346,6 +382,7 @@ FIXTURES = {
     "channel": channel_cases,
     "stationary": stationary_cases,
     "telemetry": telemetry_cases,
+    "blocks": block_cases,
 }
 
 

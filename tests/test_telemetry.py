@@ -152,3 +152,70 @@ def test_gpu_ber_point_vs_oracle(method):
         F = Hn[b] @ Xs
         G = np.sqrt(power / np.vdot(F, F).real) * F
         assert got[b] == _np_errors(Hn[b].conj().T @ G, bits[b], noise[b]), b
+
+
+# ------------------------------------------------------- block topology -----
+
+def test_oracle_blocks_golden(golden):
+    """Oracle per-block RZF + stacked coupling reproduce the reference's
+    build_precoder / sinr_eq9 on its own draws (pins the oracle for next-2)."""
+    g = golden("blocks")
+    xi, power, sigma2, T, omega = (float(g["xi"]), float(g["power"]), float(g["sigma2"]),
+                                   int(g["T"]), float(g["omega"]))
+    for t in range(int(g["n"])):
+        k = f"r{t}_"
+        H1, Hc, H2, H = g[k + "H1"], g[k + "Hc"], g[k + "H2"], g[k + "H"]
+        for m in g["methods"]:
+            m = str(m)
+            Gs, betas = [], []
+            for Hb in (H1, Hc, H2):
+                P = O.gram_regularized(Hb, xi)
+                Kb = Hb.shape[1]
+                Xs = {"direct": lambda: O.direct_solve(P, np.eye(Kb)).w,
+                      "jacpcg": lambda: O.jacpcg_solve(P, np.eye(Kb), T, variant=str(g["variant"])).w,
+                      "cg": lambda: O.cg_solve(P, np.eye(Kb), T).w,
+                      "jor": lambda: O.jor_solve(P, np.eye(Kb), T, omega=omega).w,
+                      "gs": lambda: O.gs_solve(P, np.eye(Kb), T).w}[m]()
+                F = Hb @ Xs
+                beta = np.sqrt(power / np.vdot(F, F).real)
+                Gs.append(beta * F)
+                betas.append(beta)
+            K1 = H1.shape[1]
+            G = np.zeros_like(H)
+            G[:H1.shape[0], :K1] = Gs[0]
+            G[H1.shape[0]:H1.shape[0] + Hc.shape[0]] = Gs[1]
+            G[H1.shape[0] + Hc.shape[0]:, K1:] = Gs[2]
+            assert np.linalg.norm(G - g[k + m + "_G"]) / np.linalg.norm(g[k + m + "_G"]) < 1e-10, (t, m)
+            np.testing.assert_allclose(betas, g[k + m + "_betas"], rtol=1e-10)
+            gam, _, s = O.sinr_single_block(H, G, sigma2)
+            np.testing.assert_allclose(gam, g[k + m + "_gamma"], rtol=1e-8)
+            assert abs(s - float(g[k + m + "_sumse"])) < 1e-9 * abs(s)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dt", ["c128", "c64"])
+def test_gpu_block_precoder_golden(golden, dt):
+    """build_precoder_batched + block_sinr_batched on the reference's draws
+    (all 8 in one batch) against the reference's block precoders and SINR."""
+    import torch
+    from paper_2305_13925_b200 import blocks as BK
+    g = golden("blocks")
+    cdt = torch.complex128 if dt == "c128" else torch.complex64
+    n = int(g["n"])
+    stack = lambda name: torch.stack([torch.from_numpy(g[f"r{t}_{name}"]) for t in range(n)]).to("cuda", cdt)
+    H1, Hc, H2 = stack("H1"), stack("Hc"), stack("H2")
+    xi, power, sigma2 = float(g["xi"]), float(g["power"]), float(g["sigma2"])
+    tol_g = 1e-10 if dt == "c128" else 1e-4
+    for m in g["methods"]:
+        m = str(m)
+        pre = BK.build_precoder_batched(H1, Hc, H2, xi, power, m, T=int(g["T"]), omega=float(g["omega"]),
+                                        variant=str(g["variant"]))
+        rep = BK.block_sinr_batched(H1, Hc, H2, pre, sigma2)
+        G = pre.G.cpu().numpy()
+        betas = torch.stack([pre.beta_1, pre.beta_c, pre.beta_2], 1).cpu().numpy()
+        for t in range(n):
+            ref = g[f"r{t}_{m}_G"]
+            assert np.linalg.norm(G[t] - ref) / np.linalg.norm(ref) < tol_g, (m, t)
+            np.testing.assert_allclose(betas[t], g[f"r{t}_{m}_betas"], rtol=10 * tol_g)
+            np.testing.assert_allclose(rep.gamma[t].cpu().numpy(), g[f"r{t}_{m}_gamma"], rtol=100 * tol_g)
+            assert abs(rep.sum_se[t].item() - float(g[f"r{t}_{m}_sumse"])) < 10 * tol_g * float(g[f"r{t}_{m}_sumse"])
