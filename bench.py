@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--method", default="jacpcg")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-chunk", type=int, default=256,
+                    help="realizations per HostPipeline chunk (fill/drain ~ 1/number of chunks)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -275,7 +277,7 @@ def main():
     # ---------------- e2e: host buffers through the pipelined public API ----
     e2e = None
     if a.e2e_steps > 0:
-        pipe = BT.HostPipeline(M, K, dtype=dt, chunk=min(2048, B), device=dev)
+        pipe = BT.HostPipeline(M, K, dtype=dt, chunk=min(a.e2e_chunk, B), device=dev)
         Hh = torch.empty(B, M, K, dtype=dt, pin_memory=True)
         Hh.copy_(H)
         Wh = torch.empty_like(Hh, pin_memory=True)
@@ -300,7 +302,7 @@ def main():
         e2e = {"value": B * world / (ems / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": B * M * K * csz,
                "d2h_bytes_per_step": B * M * K * csz + B * (8 + 4),
-               "ms_per_step": ems, "path": "HostPipeline (3 streams, 2048-realization chunks)"}
+               "ms_per_step": ems, "path": f"HostPipeline (3 streams, {min(a.e2e_chunk, B)}-realization chunks)"}
         del Hh, Wh
 
     # ---------------- roofline of the fused precoder call -------------------
