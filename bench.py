@@ -84,7 +84,7 @@ class ClockSampler:
 
     def __init__(self, index):
         self.samples, self.reasons, self.max_mhz = [], set(), None
-        self.power, self.limit_w = [], None
+        self.limit_w = None
         self.stop_ev = threading.Event()
         try:
             import pynvml
@@ -100,7 +100,6 @@ class ClockSampler:
         while not self.stop_ev.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1e3)
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if r & bit and name != "gpu_idle":
@@ -123,7 +122,6 @@ class ClockSampler:
     def summary(self):
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "power_w": statistics.median(self.power) if self.power else None,
                 "power_limit_w": self.limit_w,
                 "samples": len(self.samples)}
 
