@@ -86,7 +86,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
 
     // ---- (2) A'' split: row 2k = (ar, -ai), row 2k+1 = (ai, ar) per column pair
     // (the smem operand region held Xe(k-1) until the W pass copied it to TMEM)
-    if (k >= 1 && !(p.dbg & 3)) mbar_wait(&sm->xe_consumed, (k - 1) & 1);
+    if (k >= 1 && !(dbg_bits(p) & 3)) mbar_wait(&sm->xe_consumed, (k - 1) & 1);
 #if XL_GRAM2
     // The Gram pass accumulated U = Zh^T (Zh + 2 Zl) (two products instead of
     // three); G = (U + U^T) / 2.  U goes through smem (rows padded to NC + 4
@@ -180,7 +180,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
     fence_async_smem();
     named_sync(BAR_MATH, NMT);  // every thread's Gram TMEM reads are complete
     if (mt == 0) mbar_arrive(&sm->gram_free);  // the next Gram may accumulate
-    if (p.dbg & 1) {
+    if (dbg_bits(p) & 1) {
       if (mt == 0) p.status[b] = range_bad ? XL_STATUS_RANGE : 0;
       continue;
     }
@@ -505,7 +505,7 @@ __device__ __forceinline__ void w_epilogue(const Params& p, Small* sm, uint32_t 
   tc_before();
   mbar_arrive(&sm->wfree[j]);
   if (XL_TRACE && tr && threadIdx.x == 0) tr[7] = clock64();
-  if (r < NC && !(p.dbg & 8)) {  // dbg & 8: timing without the W stores
+  if (r < NC && !(dbg_bits(p) & 8)) {  // dbg & 8: timing without the W stores
     const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH) * NC + r;
     float* wp = reinterpret_cast<float*>(p.W) + o0;
 #pragma unroll
@@ -541,7 +541,7 @@ __device__ __forceinline__ void w_epilogue_half(const Params& p, Small* sm, uint
   tc_before();
   mbar_arrive(&sm->wfree[j]);
   if (XL_TRACE && tr && threadIdx.x == 0) tr[7] = clock64();
-  if (r < NC && !(p.dbg & 8)) {
+  if (r < NC && !(dbg_bits(p) & 8)) {
     const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH + a0) * NC + r;
     float* wp = reinterpret_cast<float*>(p.W) + o0;
 #pragma unroll

@@ -241,8 +241,15 @@ constexpr int BAR_CONV = 1, BAR_MATH = 2, BAR_EPI = 3;
 #ifndef XL_NS_MAX
 #define XL_NS_MAX 3  // ring depth cap (4 stages measured 3% slower at K = 64)
 #endif
+// Development hooks (timing bisection bits, phase traces, L2-policy and grid
+// experiments; read from XL_FUSED_* environment variables).  Off in the
+// product build, where every hook folds away at compile time; tools build a
+// variant with -DXL_DEV_HOOKS=1 (build_ext.py --out ... -DXL_DEV_HOOKS=1).
+#ifndef XL_DEV_HOOKS
+#define XL_DEV_HOOKS 0
+#endif
 #ifndef XL_TRACE
-#define XL_TRACE 1  // clock64 phase stamps, enabled at run time by XL_FUSED_TRACE=<k0+1>
+#define XL_TRACE XL_DEV_HOOKS  // clock64 phase stamps, enabled at run time by XL_FUSED_TRACE=<k0+1>
 #endif
 #ifndef XL_WB_GRAM
 #define XL_WB_GRAM 1   // Gram TMEM columns double-buffer the W accumulator during W passes
@@ -351,6 +358,8 @@ struct Params {
   int trace_k0;      // first traced realization of CTA 0 (XL_FUSED_TRACE=k0+1)
   int* counter;      // realization claim counter (workspace, zeroed per launch)
 };
+// the bisection bits, compile-time 0 in the product build
+__device__ __forceinline__ int dbg_bits(const Params& p) { return XL_DEV_HOOKS ? p.dbg : 0; }
 
 // Element (row n, col k) of the K-major A operand tile (core rows = n).
 template <int KU>
@@ -596,7 +605,7 @@ __global__ void __launch_bounds__(Lay<KU>::NT, 1) fused_rzf_kernel(Params p) {
     for (uint32_t k = 0;; ++k) {
       const int64_t bn = real_of(k + 1);
       if (bn >= 0) body(k + 1, 0, bn, false);
-      if (!(p.dbg & 3)) body(k, 1, bk, bn >= 0);
+      if (!(dbg_bits(p) & 3)) body(k, 1, bk, bn >= 0);
       if (bn < 0) break;
       bk = bn;
     }
@@ -606,9 +615,10 @@ __global__ void __launch_bounds__(Lay<KU>::NT, 1) fused_rzf_kernel(Params p) {
     if (lane == 0) {
       uint32_t i = 0;
       const uint64_t pol_first = policy_evict_first();
-      const uint64_t pol_g = (p.l2mode & 32) ? policy_keep_fraction(((p.l2mode & 15) + 1) / 16.0f)
-                             : (p.l2mode & 3) == 0 ? pol_first
-                             : (p.l2mode & 3) == 1 ? policy_evict_normal()
+      const int l2m = XL_DEV_HOOKS ? p.l2mode : 0;
+      const uint64_t pol_g = (l2m & 32) ? policy_keep_fraction(((l2m & 15) + 1) / 16.0f)
+                             : (l2m & 3) == 0 ? pol_first
+                             : (l2m & 3) == 1 ? policy_evict_normal()
                                                    : policy_evict_last();
       for_items([&](uint32_t kk, int pass, int64_t b, bool) {
         const char* Hb = reinterpret_cast<const char*>(p.H + b * (int64_t)p.M * KU);
@@ -712,7 +722,7 @@ __global__ void __launch_bounds__(Lay<KU>::NT, 1) fused_rzf_kernel(Params p) {
               v[it] = *reinterpret_cast<const float4*>(gb + (row * NC + cc) * 4);
             }
             __syncwarp();  // the whole group is in registers before it is overwritten
-            if (p.dbg & 4) continue;  // dbg & 4: timing without conversion
+            if (dbg_bits(p) & 4) continue;  // dbg & 4: timing without conversion
 #pragma unroll
             for (int it = 0; it < NIT; ++it) {
               int row, cc;
@@ -776,7 +786,7 @@ __global__ void __launch_bounds__(Lay<KU>::NT, 1) fused_rzf_kernel(Params p) {
           const uint32_t zh = su32(ring + s * G::SB), zl = zh + G::CMA;
 #pragma unroll
           for (int ks = 0; ks < G::CH / 16; ++ks) {
-            if (p.dbg & 16) break;
+            if (dbg_bits(p) & 16) break;
             const uint64_t dh = sdesc(zh + 4 * ks * G::CMA, 2 * G::CMA, 128);
             const uint64_t dl = sdesc(zl + 4 * ks * G::CMA, 2 * G::CMA, 128);
             mma(tmem + G::T_GRAM, dh, dh, G::ID_GRAM, (c | ks) != 0);
@@ -855,7 +865,8 @@ static int launch_k(const tc::Params& p, cudaStream_t st) {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   int64_t grid = p.B < g_num_sms ? p.B : g_num_sms;
-  if (const char* e = getenv("XL_FUSED_GRID")) grid = grid < atoi(e) ? grid : atoi(e);  // scaling experiments
+  if (XL_DEV_HOOKS)
+    if (const char* e = getenv("XL_FUSED_GRID")) grid = grid < atoi(e) ? grid : atoi(e);  // scaling experiments
   tc::fused_rzf_kernel<KU><<<(unsigned)grid, tc::Lay<KU>::NT, smem, st>>>(p);
   return check_launch("fused_rzf_tc");
 }
@@ -870,8 +881,10 @@ int launch_fused(int dtype, int method, int variant, const void* H, int64_t B, i
                nullptr, 0};  // l2mode 0: evict_first loads, st.global.cs W stores
   p.counter = static_cast<int*>(ws);
   if (ws_bytes < sizeof(int) || cudaMemsetAsync(ws, 0, sizeof(int), st) != cudaSuccess) return check_launch("fused counter");
-  if (const char* e = getenv("XL_FUSED_DEBUG")) p.dbg = atoi(e);
-  if (const char* e = getenv("XL_FUSED_L2")) p.l2mode = atoi(e);
+  if (XL_DEV_HOOKS) {
+    if (const char* e = getenv("XL_FUSED_DEBUG")) p.dbg = atoi(e);
+    if (const char* e = getenv("XL_FUSED_L2")) p.l2mode = atoi(e);
+  }
   // XL_FUSED_TRACE=1: synchronous per-phase clock64 dump of CTA 0 to stderr
   // (development aid; never set in production runs).
   static long long* trace = nullptr;

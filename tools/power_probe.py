@@ -1,7 +1,10 @@
 """Effective SM clock and board power of the fused cfg3 kernel under several
 XL_FUSED_* settings (development aid).  For each setting: run the kernel in a
 loop for ~3 s sampling NVML power / clock, then one traced launch whose
-clock64 / globaltimer ratio gives the effective SM clock."""
+clock64 / globaltimer ratio gives the effective SM clock.
+The XL_FUSED_* settings need the development-hooks build
+(build_ext.py --out variants/dev.so -DXL_DEV_HOOKS=1; run via tools/with_lib.sh).
+"""
 import os, sys, subprocess, threading, time, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

@@ -1,5 +1,8 @@
 """Time the fused cfg3 call (check=False) under the current XL_FUSED_* env;
-prints precoders/s.  Development aid for A/B experiments."""
+prints precoders/s.  Development aid for A/B experiments.
+The XL_FUSED_* settings need the development-hooks build
+(build_ext.py --out variants/dev.so -DXL_DEV_HOOKS=1; run via tools/with_lib.sh).
+"""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
