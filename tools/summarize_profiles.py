@@ -69,7 +69,8 @@ def full():
     h, u, v = r[0], r[1], r[2]
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
-    open("/tmp/_src.csv", "w").write(src)
+    with open("/tmp/_src.csv", "w") as f:
+        f.write(src)
     stalls = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_stalls.py"), "/tmp/_src.csv", "16"],
                             capture_output=True, text=True).stdout
     B = 4096
