@@ -497,23 +497,32 @@ __device__ __forceinline__ void w_epilogue(const Params& p, Small* sm, uint32_t 
   // the math warps published the scales before xe_ready, which these MMAs awaited
   const float wscale = sm->wsc[kpar][0], fscale = sm->wsc[kpar][1];
   tc_after();
-  float d[CH];
-  if (32 * warp < NC) {
-    tmem_ld<CH>(tl, d);
-    tmem_wait_ld();
-  }
-  tc_before();
-  mbar_arrive(&sm->wfree[j]);
-  if (XL_TRACE && tr && threadIdx.x == 0) tr[7] = clock64();
-  if (r < NC && !(dbg_bits(p) & 8)) {  // dbg & 8: timing without the W stores
-    const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH) * NC + r;
-    float* wp = reinterpret_cast<float*>(p.W) + o0;
+  // two halves of CH/2 antennas keep the register footprint at CH/2 (the
+  // converter state lives alongside); the buffer is released after the
+  // second TMEM load, before its stores
+  constexpr int HALF = CH / 2;
+  const int64_t o0 = (b * (int64_t)p.M + (int64_t)c * CH) * NC + r;
+  float* wp = reinterpret_cast<float*>(p.W) + o0;
+  float* fp = p.F ? reinterpret_cast<float*>(p.F) + o0 : nullptr;
 #pragma unroll
-    for (int a = 0; a < CH; ++a) __stcs(wp + a * NC, d[a] * wscale);
-    if (p.F) {
-      float* fp = reinterpret_cast<float*>(p.F) + o0;
+  for (int hf = 0; hf < 2; ++hf) {
+    float d[HALF];
+    if (32 * warp < NC) {
+      tmem_ld<HALF>(tl + hf * HALF, d);
+      tmem_wait_ld();
+    }
+    if (hf == 1) {
+      tc_before();
+      mbar_arrive(&sm->wfree[j]);
+      if (XL_TRACE && tr && threadIdx.x == 0) tr[7] = clock64();
+    }
+    if (r < NC && !(dbg_bits(p) & 8)) {  // dbg & 8: timing without the W stores
 #pragma unroll
-      for (int a = 0; a < CH; ++a) __stcs(fp + a * NC, d[a] * fscale);
+      for (int a = 0; a < HALF; ++a) __stcs(wp + (hf * HALF + a) * NC, d[a] * wscale);
+      if (fp) {
+#pragma unroll
+        for (int a = 0; a < HALF; ++a) __stcs(fp + (hf * HALF + a) * NC, d[a] * fscale);
+      }
     }
   }
 }

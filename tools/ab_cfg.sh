@@ -1,0 +1,9 @@
+L=paper_2305_13925_b200/_native/libxlmimo_b200.so
+cp $L /tmp/orig.so
+for rep in 1 2; do
+  for v in old new; do
+    cp variants/$v.so $L
+    echo "$v cfg2: $(python tools/time_fused.py cfg2 65536 2>&1 | tail -1)   cfg3: $(python tools/time_fused.py cfg3 32768 2>&1 | tail -1)"
+  done
+done
+cp /tmp/orig.so $L
