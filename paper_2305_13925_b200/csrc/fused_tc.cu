@@ -356,6 +356,7 @@ struct Params {
   long long* trace;  // optional per-phase clock64 stamps of CTA 0 (XL_FUSED_TRACE)
   int l2mode;        // L2 policy of the G-pass loads: 0 evict_first, 1 normal, 2 evict_last
   int trace_k0;      // first traced realization of CTA 0 (XL_FUSED_TRACE=k0+1)
+  int stagger_ns;    // dev: odd CTAs start this much later (phase-offset experiment)
   int* counter;      // realization claim counter (workspace, zeroed per launch)
 };
 // the bisection bits, compile-time 0 in the product build
@@ -614,6 +615,14 @@ __global__ void __launch_bounds__(Lay<KU>::NT, 1) fused_rzf_kernel(Params p) {
     // ------------------------------------------------------ producer ------
     if (lane == 0) {
       uint32_t i = 0;
+      if (XL_DEV_HOOKS && p.stagger_ns > 0 && (blockIdx.x % 2) == 1) {
+        uint64_t t0, t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        do {
+          __nanosleep(1000);
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        } while (t1 - t0 < (uint64_t)p.stagger_ns);
+      }
       const uint64_t pol_first = policy_evict_first();
       const int l2m = XL_DEV_HOOKS ? p.l2mode : 0;
       const uint64_t pol_g = (l2m & 32) ? policy_keep_fraction(((l2m & 15) + 1) / 16.0f)
@@ -884,6 +893,7 @@ int launch_fused(int dtype, int method, int variant, const void* H, int64_t B, i
   if (XL_DEV_HOOKS) {
     if (const char* e = getenv("XL_FUSED_DEBUG")) p.dbg = atoi(e);
     if (const char* e = getenv("XL_FUSED_L2")) p.l2mode = atoi(e);
+    if (const char* e = getenv("XL_FUSED_STAGGER")) p.stagger_ns = atoi(e);
   }
   // XL_FUSED_TRACE=1: synchronous per-phase clock64 dump of CTA 0 to stderr
   // (development aid; never set in production runs).
