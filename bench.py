@@ -159,9 +159,18 @@ def cpu_baseline(cfg_name, method, seconds):
     with cf.ProcessPoolExecutor(cores, mp_context=ctx) as ex:
         res = list(ex.map(_cpu_worker, [(seconds, cfg_name, method, 7, 10_000 + 16 * i, 16)
                                         for i in range(cores)]))
+        # also one core alone (the rest of the pool idle)
+        n1, el1 = ex.submit(_cpu_worker, (min(4.0, seconds), cfg_name, method, 7, 10_000, 16)).result()
     n = sum(r[0] for r in res)
     el = max(r[1] for r in res)
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((l.split(":", 1)[1].strip() for l in f if l.startswith("model name")), "")
+    except OSError:
+        pass
     return {"value": n / el, "unit": UNIT, "cores": cores, "kind": "port",
+            "single_core_value": n1 / el1, "cpu_model": model,
             "sample": f"{n} {cfg_name} precoders ({method}, T={_T(cfg_name)}) + SINR/SE, "
                       f"complex128 oracle, {cores} processes x 1 BLAS thread, {el:.1f} s"}
 
