@@ -42,6 +42,14 @@ struct SolveArgs {
 template <typename R> size_t solve_ws_bytes(int64_t B, int K, int Rcols);
 template <typename R> int launch_solve(const SolveArgs& a, cudaStream_t st);
 
+// gemm_tc.cu: tensor-core Gram / W for the general path at large K (3xTF32 c64, ZGEMM c128)
+bool tc_general_supported(int dtype, int M, int K);
+size_t tc_gram_ws_bytes(int dtype, int64_t Bc, int M, int K);
+int tc_gram(int dtype, const void* H, int64_t Bc, int M, int K, const double* xi_b, double xi, void* A,
+            void* ws, cudaStream_t st);
+int tc_apply(int dtype, const void* H, const void* X, const double* beta, int64_t Bc, int M, int K, void* W,
+             void* F, void* ws, cudaStream_t st, bool resplit);
+
 int launch_ber(int dtype, const void* Bc, const int8_t* bits, const void* noise, int64_t B, int K,
                int nsym, int64_t* errors, cudaStream_t st);
 

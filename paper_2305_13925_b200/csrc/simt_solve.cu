@@ -100,7 +100,7 @@ __device__ double residual_norm2(const cplx<R>* A, const cplx<R>* X, cplx<R>* Q,
 }
 
 template <typename R>
-__global__ void __launch_bounds__(ST)
+__global__ void __launch_bounds__(ST, sizeof(R) == 4 ? 4 : 2)
 pcg_kernel(SolveArgs a) {
   using C = cplx<R>;
   const int64_t b = blockIdx.x;

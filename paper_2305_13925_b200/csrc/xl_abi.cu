@@ -141,18 +141,111 @@ static size_t simt_rzf_ws(int dtype, int64_t B, int M, int K) {
          align_up((size_t)B * tiles * sizeof(double)) + align_up((size_t)B * 4);
 }
 
+// Large K: the general path runs its Gram / W products on the tensor cores
+// (gemm_tc.cu).  Their split operands [Zh | Zl] take twice the bytes of H; they
+// are kept for the whole batch (up to 32 GiB, i.e. 16 GiB of H) so the W
+// products reuse them, else built per sub-batch for the Gram and again for W.
+static int64_t tc_chunk_size(int dtype, int64_t B, int M, int K) {
+  if (dtype == XL_C128) return B;
+  const int64_t per = (int64_t)M * 4 * K * 4;  // split rows [Zh | Zl] per realization
+  int64_t c = ((int64_t)32 << 30) / per;
+  if (c < 1) c = 1;
+  return c < B ? c : B;
+}
+
+static size_t general_ws(int dtype, int64_t B, int M, int K) {
+  size_t w = simt_rzf_ws(dtype, B, M, K);
+  if (tc_general_supported(dtype, M, K)) w += align_up(tc_gram_ws_bytes(dtype, tc_chunk_size(dtype, B, M, K), M, K));
+  return w;
+}
+
 size_t xl_rzf_workspace_bytes(int dtype, int method, int64_t B, int32_t M, int32_t K) {
   if (fused_supported(dtype, method, M, K)) return fused_ws_bytes(dtype, method, B, M, K);
-  return simt_rzf_ws(dtype, B, M, K);
+  return general_ws(dtype, B, M, K);
 }
 
 size_t xl_rzf_general_workspace_bytes(int dtype, int method, int64_t B, int32_t M, int32_t K) {
   (void)method;
-  return simt_rzf_ws(dtype, B, M, K);
+  return general_ws(dtype, B, M, K);
 }
 
 static void* g_dbg_gram = nullptr;
 void xl_debug_set_gram_out(void* A) { g_dbg_gram = A; }
+
+// The general path over B realizations (workspace: simt_rzf_ws(B) + the
+// tensor-core sub-batch buffers).
+static int general_path(int dtype, int method, int variant, const void* H, int64_t B, int32_t M, int32_t K,
+                         double xi, const double* xi_per_batch, double power, int32_t T, double sigma2, void* W,
+                         void* F, double* beta, double* gamma, double* sum_se, void* X, int32_t* status,
+                         void* workspace, cudaStream_t st) {
+  const bool tc = tc_general_supported(dtype, M, K);
+  const size_t cs = csize(dtype), kk = (size_t)B * K * K * cs;
+  char* p = (char*)workspace;
+  void* A = p; p += align_up(kk);
+  void* Xw = p; p += align_up(kk);
+  size_t sws = xl_solve_workspace_bytes(dtype, B, K, K);
+  if (sws < kk) sws = kk;
+  void* sw = p; p += align_up(sws);
+  const int ptiles = gemm_tiles(M, K) > gemm_tiles(K, K) ? gemm_tiles(M, K) : gemm_tiles(K, K);
+  double* part = (double*)p; p += align_up((size_t)B * ptiles * sizeof(double));
+  int32_t* iters = (int32_t*)p; p += align_up((size_t)B * 4);
+  void* tcws = p;  // gemm_tc.cu: cuBLAS workspace + split operands
+  void* Xo = X ? X : Xw;
+  const xl_stream_t stream = (xl_stream_t)st;
+  int e;
+  const int64_t Bc = tc ? tc_chunk_size(dtype, B, M, K) : B;
+  const int64_t oH = (int64_t)M * K * (int64_t)cs, oK = (int64_t)K * K * (int64_t)cs;
+  if (tc) {
+    for (int64_t b0 = 0; b0 < B; b0 += Bc) {
+      const int64_t nb = B - b0 < Bc ? B - b0 : Bc;
+      if ((e = tc_gram(dtype, (const char*)H + b0 * oH, nb, M, K, xi_per_batch ? xi_per_batch + b0 : nullptr, xi,
+                       (char*)A + b0 * oK, tcws, st)))
+        return e;
+    }
+  } else if ((e = xl_gram(dtype, H, B, M, K, xi, xi_per_batch, A, stream))) {
+    return e;
+  }
+  // W = beta H X on the tensor cores, per sub-batch (the split rows are rebuilt:
+  // the Gram sub-batches have overwritten them)
+  auto tc_w = [&]() -> int {
+    for (int64_t b0 = 0; b0 < B; b0 += Bc) {
+      const int64_t nb = B - b0 < Bc ? B - b0 : Bc;
+      if (int r = tc_apply(dtype, (const char*)H + b0 * oH, (const char*)Xo + b0 * oK, beta + b0, nb, M, K,
+                           (char*)W + b0 * oH, F ? (char*)F + b0 * oH : nullptr, tcws, st, Bc < B))
+        return r;
+    }
+    return XL_SUCCESS;
+  };
+  if ((e = xl_solve(dtype, method, variant, A, B, K, nullptr, K, nullptr, nullptr, method == XL_CG,
+                    T, -1.0, Xo, iters, nullptr, nullptr, status, sw, sws, stream))) return e;
+  // Coupling and ||F||^2 from the K x K side (SURVEY K3/K4): GX = (A - xi I) X,
+  // ||F||_F^2 = Re tr(X^H GX) (precoder.py:64-70 with F = H X), beta, then
+  // W = beta H X in one pass and B = H^H W = beta GX (metrics.py:35-44):
+  // 8 K^3 instead of 8 M K^2 flops for the coupling, no separate F pass.
+  const int64_t sH = (int64_t)M * K, sK = (int64_t)K * K;
+  const int np = gemm_tiles(K, K);
+  void* GX = sw;  // the solver workspace is free again (>= B K K)
+  if (dtype == XL_C64) {
+    if ((e = launch_cgemm<float>(false, EPI_GXF, A, sK, K, Xo, sK, K, GX, sK, K, B, K, K, K, xi_per_batch, xi, part, st))) return e;
+    if ((e = launch_beta_from_partials(B, part, np, power, beta, status, st))) return e;
+    if (tc) {
+      if ((e = tc_w())) return e;
+    } else {
+      if ((e = launch_cgemm<float>(false, EPI_BSCALE, H, sH, K, Xo, sK, K, W, sH, K, B, M, K, K, beta, 0, nullptr, st))) return e;
+      if (F && (e = launch_cgemm<float>(false, EPI_STORE, H, sH, K, Xo, sK, K, F, sH, K, B, M, K, K, nullptr, 0, nullptr, st))) return e;
+    }
+    return launch_sinr<float>(GX, B, K, sigma2, gamma, nullptr, sum_se, st, beta);
+  }
+  if ((e = launch_cgemm<double>(false, EPI_GXF, A, sK, K, Xo, sK, K, GX, sK, K, B, K, K, K, xi_per_batch, xi, part, st))) return e;
+  if ((e = launch_beta_from_partials(B, part, np, power, beta, status, st))) return e;
+  if (tc) {
+    if ((e = tc_w())) return e;
+  } else {
+    if ((e = launch_cgemm<double>(false, EPI_BSCALE, H, sH, K, Xo, sK, K, W, sH, K, B, M, K, K, beta, 0, nullptr, st))) return e;
+    if (F && (e = launch_cgemm<double>(false, EPI_STORE, H, sH, K, Xo, sK, K, F, sH, K, B, M, K, K, nullptr, 0, nullptr, st))) return e;
+  }
+  return launch_sinr<double>(GX, B, K, sigma2, gamma, nullptr, sum_se, st, beta);
+}
 
 static int rzf_impl(bool allow_fused, int dtype, int method, int variant, const void* H, int64_t B,
                     int32_t M, int32_t K, double xi, const double* xi_per_batch, double power,
@@ -169,7 +262,7 @@ static int rzf_impl(bool allow_fused, int dtype, int method, int variant, const 
   if (B == 0) return XL_SUCCESS;
   cudaStream_t st = (cudaStream_t)stream;
   const bool fused = allow_fused && fused_supported(dtype, method, M, K);
-  const size_t need = fused ? fused_ws_bytes(dtype, method, B, M, K) : simt_rzf_ws(dtype, B, M, K);
+  const size_t need = fused ? fused_ws_bytes(dtype, method, B, M, K) : general_ws(dtype, B, M, K);
   if (ws_bytes < need) { set_error("rzf: workspace too small"); return XL_ERR_WORKSPACE; }
   if (cudaMemsetAsync(status, 0, (size_t)B * sizeof(int32_t), st) != cudaSuccess) return check_launch("memset");
 
@@ -178,41 +271,9 @@ static int rzf_impl(bool allow_fused, int dtype, int method, int variant, const 
                         sigma2, W, F, beta, gamma, sum_se, X, status, workspace, ws_bytes,
                         g_dbg_gram, st);
 
-  // ---- general SIMT path: Gram -> solve -> F = H X (+||F||^2) -> beta, W -> B = H^H W -> SINR
-  const size_t cs = csize(dtype), kk = (size_t)B * K * K * cs;
-  char* p = (char*)workspace;
-  void* A = p; p += align_up(kk);
-  void* Xw = p; p += align_up(kk);
-  size_t sws = xl_solve_workspace_bytes(dtype, B, K, K);
-  if (sws < kk) sws = kk;
-  void* sw = p; p += align_up(sws);
-  const int ptiles = gemm_tiles(M, K) > gemm_tiles(K, K) ? gemm_tiles(M, K) : gemm_tiles(K, K);
-  double* part = (double*)p; p += align_up((size_t)B * ptiles * sizeof(double));
-  int32_t* iters = (int32_t*)p;
-  void* Xo = X ? X : Xw;
-  int e;
-  if ((e = xl_gram(dtype, H, B, M, K, xi, xi_per_batch, A, stream))) return e;
-  if ((e = xl_solve(dtype, method, variant, A, B, K, nullptr, K, nullptr, nullptr, method == XL_CG,
-                    T, -1.0, Xo, iters, nullptr, nullptr, status, sw, sws, stream))) return e;
-  // Coupling and ||F||^2 from the K x K side (SURVEY K3/K4): GX = (A - xi I) X,
-  // ||F||_F^2 = Re tr(X^H GX) (precoder.py:64-70 with F = H X), beta, then
-  // W = beta H X in one pass and B = H^H W = beta GX (metrics.py:35-44):
-  // 8 K^3 instead of 8 M K^2 flops for the coupling, no separate F pass.
-  const int64_t sH = (int64_t)M * K, sK = (int64_t)K * K;
-  const int np = gemm_tiles(K, K);
-  void* GX = sw;  // the solver workspace is free again (>= B K K)
-  if (dtype == XL_C64) {
-    if ((e = launch_cgemm<float>(false, EPI_GXF, A, sK, K, Xo, sK, K, GX, sK, K, B, K, K, K, xi_per_batch, xi, part, st))) return e;
-    if ((e = launch_beta_from_partials(B, part, np, power, beta, status, st))) return e;
-    if ((e = launch_cgemm<float>(false, EPI_BSCALE, H, sH, K, Xo, sK, K, W, sH, K, B, M, K, K, beta, 0, nullptr, st))) return e;
-    if (F && (e = launch_cgemm<float>(false, EPI_STORE, H, sH, K, Xo, sK, K, F, sH, K, B, M, K, K, nullptr, 0, nullptr, st))) return e;
-    return launch_sinr<float>(GX, B, K, sigma2, gamma, nullptr, sum_se, st, beta);
-  }
-  if ((e = launch_cgemm<double>(false, EPI_GXF, A, sK, K, Xo, sK, K, GX, sK, K, B, K, K, K, xi_per_batch, xi, part, st))) return e;
-  if ((e = launch_beta_from_partials(B, part, np, power, beta, status, st))) return e;
-  if ((e = launch_cgemm<double>(false, EPI_BSCALE, H, sH, K, Xo, sK, K, W, sH, K, B, M, K, K, beta, 0, nullptr, st))) return e;
-  if (F && (e = launch_cgemm<double>(false, EPI_STORE, H, sH, K, Xo, sK, K, F, sH, K, B, M, K, K, nullptr, 0, nullptr, st))) return e;
-  return launch_sinr<double>(GX, B, K, sigma2, gamma, nullptr, sum_se, st, beta);
+  // ---- general path: Gram -> solve -> GX, beta -> W = beta H X -> SINR
+  return general_path(dtype, method, variant, H, B, M, K, xi, xi_per_batch, power, T, sigma2, W, F, beta,
+                      gamma, sum_se, X, status, workspace, st);
 }
 
 int xl_rzf(int dtype, int method, int variant, const void* H, int64_t B, int32_t M,

@@ -286,6 +286,26 @@ def test_c64_vs_oracle(cfg, B, method):
         assert abs(S[b] - s) / abs(s) <= 1e-4, (cfg, method, b, S[b], s)
 
 
+@pytest.mark.parametrize("cfg,B,tol", [("cfg5", 2, 1e-4), ("cfg5_c128", 1, 1e-10), ("cfg4", 3, 1e-4)])
+def test_large_k_tensor_core_general_path(cfg, B, tol):
+    """K >= 96: the general path's Gram and W run on the tensor cores
+    (3xTF32 for complex64, ZGEMM for complex128; gemm_tc.cu), in sub-batches."""
+    wl = X.CONFIGS[cfg]
+    H = X.generate_channels(wl.model, seed=2, first=77, B=B, dtype=wl.dtype)
+    Hn = H.cpu().numpy().astype(np.complex128)
+    for method in ("jacpcg", "direct"):
+        out = BT.rzf_batched(H, wl.alpha(), wl.power(), method=method, T=wl.T, want_F=True)
+        W, F, S = out.W.cpu().numpy(), out.F.cpu().numpy(), out.sum_se.cpu().numpy()
+        beta, gam = out.beta.cpu().numpy(), out.gamma.cpu().numpy()
+        for b in range(B):
+            Gr, br, gr, s = O.precoder_and_se(Hn[b], wl.alpha(), wl.power(), 1.0, method, wl.T, "textbook")
+            assert relf(W[b], Gr) <= tol, (cfg, method, b, relf(W[b], Gr))
+            assert relf(F[b], Gr / br) <= tol, (cfg, method, b)
+            assert abs(beta[b] - br) <= tol * br
+            assert abs(S[b] - s) <= max(tol, 1e-8) * abs(s), (cfg, method, b, S[b], s)
+            np.testing.assert_allclose(gam[b], gr, rtol=max(10 * tol, 1e-8))
+
+
 def test_c128_cfg1_full_batch():
     """configs[0]: 100 realizations, complex128, Jac-PCG T=4 and direct at 1e-10."""
     wl = X.CONFIGS["cfg1"]
