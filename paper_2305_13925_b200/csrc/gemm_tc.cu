@@ -162,6 +162,195 @@ __global__ void herm_add_kernel(double2* __restrict__ A, int K, const double* __
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Jac-PCG / CG on the real embedding for the rzf path at large K (identity
+// right-hand sides, w0 = 0, fixed T): the K complex columns are K real columns
+// of length n2 = 2K (column j = the complex column interleaved re/im, so the
+// column-major real view IS the column-major complex state), A'' the real
+// embedding of the Hermitian A (column 2j = A[:, j], column 2j+1 = i A[:, j]).
+// Each iteration: Q = A'' P as two 3xTF32 GEMMs (E1 = [A''h | A''h] against the
+// split P rows [Ph ; Pl], plus E2 = A''l against Ph), then one CTA per
+// realization updates X, R, P with the per-column scalars of linsolve.py:217-294
+// (textbook: z = r / c; Algorithm 1: r and Pm pre-divided by C; CG: C = I).
+// Real inner products of the embedded columns are the complex Re(a^H b).
+// ---------------------------------------------------------------------------
+
+struct PcgState {
+  float* E1;  // n2 x 2 n2 (col-major) per realization
+  float* E2;  // n2 x n2
+  float* SP;  // 2 n2 x K: [Ph ; Pl] per column
+  float* Q;   // n2 x K
+  float* P;   // n2 x K
+  float* X;   // n2 x K
+  float* R;   // n2 x K
+  float* C;   // n2: preconditioner diagonal per real component (c_i twice)
+  float* rz;  // K
+};
+
+__device__ __forceinline__ float warp_sum_f(float v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// build E1 / E2 from A (K x K complex row-major, Hermitian), C, and the initial state
+__global__ void pcg_init_kernel(const float2* __restrict__ A, PcgState s, int K, int method, int variant,
+                                int32_t* __restrict__ status) {
+  const int64_t b = blockIdx.x;
+  const int n2 = 2 * K;
+  const float2* a = A + b * (int64_t)K * K;
+  float* e1 = s.E1 + b * (int64_t)n2 * 2 * n2;
+  float* e2 = s.E2 + b * (int64_t)n2 * n2;
+  float* c = s.C + b * (int64_t)n2;
+  const bool use_c = method == XL_JACPCG;
+  const bool textbook = use_c && variant == XL_TEXTBOOK;
+  __shared__ int zero_diag;
+  if (threadIdx.x == 0) zero_diag = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < K; i += blockDim.x) {
+    const float d = use_c ? a[(int64_t)i * K + i].x : 1.0f;
+    if (d == 0.0f) zero_diag = 1;
+    c[2 * i] = d;
+    c[2 * i + 1] = d;
+  }
+  // A''(r, col): col 2j = A[:, j] (re/im interleaved), col 2j+1 = i A[:, j]; A[i][j] = conj(A[j][i])
+  for (int64_t e = threadIdx.x; e < (int64_t)n2 * n2; e += blockDim.x) {
+    const int col = (int)(e / n2), r = (int)(e % n2);
+    const int j = col >> 1, i = r >> 1;
+    const float2 aij = a[(int64_t)i * K + j];
+    float v;
+    if ((col & 1) == 0) v = (r & 1) == 0 ? aij.x : aij.y;   // A_ij
+    else v = (r & 1) == 0 ? -aij.y : aij.x;                 // i A_ij
+    const float h = tf32_rn(v), l = v - h;
+    e1[(int64_t)col * n2 + r] = h;
+    e1[(int64_t)(n2 + col) * n2 + r] = h;
+    e2[(int64_t)col * n2 + r] = l;
+  }
+  __syncthreads();
+  if (zero_diag) {
+    if (threadIdx.x == 0) status[b] = XL_STATUS_SPLITTING;
+  }
+  // r = S - A w = I (Algorithm 1: C^-1 I), z, m = z, x = 0, rz (linsolve.py:224-229, 264-268)
+  const int64_t per = (int64_t)n2 * K;
+  float* P = s.P + b * per;
+  float* X = s.X + b * per;
+  float* R = s.R + b * per;
+  float* SP = s.SP + b * 2 * per;
+  for (int64_t e = threadIdx.x; e < per; e += blockDim.x) {
+    const int j = (int)(e / n2), r = (int)(e % n2);
+    const float ci = c[r];
+    const bool one = r == 2 * j;
+    const float rv = one ? ((use_c && !textbook) ? 1.0f / ci : 1.0f) : 0.0f;
+    const float zv = textbook ? rv / ci : rv;
+    R[e] = rv;
+    X[e] = 0.0f;
+    P[e] = zv;
+    const float h = tf32_rn(zv);
+    SP[(int64_t)j * 2 * n2 + r] = h;
+    SP[(int64_t)j * 2 * n2 + n2 + r] = zv - h;
+  }
+  for (int j = threadIdx.x; j < K; j += blockDim.x) {
+    const float ci = c[2 * j];
+    s.rz[b * K + j] = textbook ? 1.0f / ci : ((use_c) ? (1.0f / ci) * (1.0f / ci) : 1.0f);
+  }
+}
+
+// one PCG step after Q = A'' P (linsolve.py:275-288): one warp per column, the
+// column's q, p, x, r held in registers (float4 per lane, n2 <= 512) so each is
+// read and written once
+constexpr int PCG_V = 4;  // float4 per lane and vector: n2 <= 32 * 4 * PCG_V
+__global__ void pcg_update_kernel(PcgState s, int K, int method, int variant, int32_t* __restrict__ status) {
+  const int64_t b = blockIdx.x;
+  const int n2 = 2 * K, nq = n2 / 4;
+  const int64_t per = (int64_t)n2 * K;
+  const bool use_c = method == XL_JACPCG;
+  const bool textbook = use_c && variant == XL_TEXTBOOK;
+  const float4* c4 = reinterpret_cast<const float4*>(s.C + b * (int64_t)n2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __shared__ int not_hpd;
+  if (threadIdx.x == 0) not_hpd = 0;
+  __syncthreads();
+  for (int j = warp; j < K; j += nw) {
+    const int64_t o = b * per + (int64_t)j * n2;
+    const float4* q4 = reinterpret_cast<const float4*>(s.Q + o);
+    float4* p4 = reinterpret_cast<float4*>(s.P + o);
+    float4* x4 = reinterpret_cast<float4*>(s.X + o);
+    float4* r4 = reinterpret_cast<float4*>(s.R + o);
+    float4* sp4 = reinterpret_cast<float4*>(s.SP + b * 2 * per + (int64_t)j * 2 * n2);
+    const float rzj = s.rz[b * K + j];
+    const bool act = rzj > 0.0f;
+    float4 qv[PCG_V], pv[PCG_V], cv[PCG_V];
+    float curv = 0.0f;
+#pragma unroll
+    for (int t = 0; t < PCG_V; ++t) {
+      const int i = lane + 32 * t;
+      if (i < nq) {
+        qv[t] = q4[i];
+        pv[t] = p4[i];
+        cv[t] = use_c ? c4[i] : make_float4(1.f, 1.f, 1.f, 1.f);
+        if (use_c && !textbook) {
+          qv[t].x = qv[t].x / cv[t].x; qv[t].y = qv[t].y / cv[t].y;
+          qv[t].z = qv[t].z / cv[t].z; qv[t].w = qv[t].w / cv[t].w;
+        }
+        curv += pv[t].x * qv[t].x + pv[t].y * qv[t].y + pv[t].z * qv[t].z + pv[t].w * qv[t].w;
+      }
+    }
+    curv = warp_sum_f(curv);
+    if (curv <= 0.0f && act && lane == 0) not_hpd = 1;
+    const float al = act ? rzj / (curv > 0.0f ? curv : 1.0f) : 0.0f;
+    float acc = 0.0f;
+    float4 rv[PCG_V];
+#pragma unroll
+    for (int t = 0; t < PCG_V; ++t) {
+      const int i = lane + 32 * t;
+      if (i < nq) {
+        float4 xv = x4[i];
+        rv[t] = r4[i];
+        xv.x += al * pv[t].x; xv.y += al * pv[t].y; xv.z += al * pv[t].z; xv.w += al * pv[t].w;
+        rv[t].x -= al * qv[t].x; rv[t].y -= al * qv[t].y; rv[t].z -= al * qv[t].z; rv[t].w -= al * qv[t].w;
+        x4[i] = xv;
+        r4[i] = rv[t];
+        if (textbook)
+          acc += rv[t].x * (rv[t].x / cv[t].x) + rv[t].y * (rv[t].y / cv[t].y) + rv[t].z * (rv[t].z / cv[t].z) +
+                 rv[t].w * (rv[t].w / cv[t].w);
+        else
+          acc += rv[t].x * rv[t].x + rv[t].y * rv[t].y + rv[t].z * rv[t].z + rv[t].w * rv[t].w;
+      }
+    }
+    acc = warp_sum_f(acc);
+    const float be = act ? acc / rzj : 0.0f;
+#pragma unroll
+    for (int t = 0; t < PCG_V; ++t) {
+      const int i = lane + 32 * t;
+      if (i < nq) {
+        float4 m;
+        m.x = (textbook ? rv[t].x / cv[t].x : rv[t].x) + be * pv[t].x;
+        m.y = (textbook ? rv[t].y / cv[t].y : rv[t].y) + be * pv[t].y;
+        m.z = (textbook ? rv[t].z / cv[t].z : rv[t].z) + be * pv[t].z;
+        m.w = (textbook ? rv[t].w / cv[t].w : rv[t].w) + be * pv[t].w;
+        p4[i] = m;
+        const float4 h = make_float4(tf32_rn(m.x), tf32_rn(m.y), tf32_rn(m.z), tf32_rn(m.w));
+        sp4[i] = h;
+        sp4[nq + i] = make_float4(m.x - h.x, m.y - h.y, m.z - h.z, m.w - h.w);
+      }
+    }
+    if (lane == 0) s.rz[b * K + j] = acc;
+  }
+  __syncthreads();
+  if (not_hpd && threadIdx.x == 0 && status[b] == 0) status[b] = XL_STATUS_NOT_HPD;
+}
+
+// column-major embedded X (n2 x K) -> row-major complex X (K x K)
+__global__ void pcg_store_x_kernel(const float* __restrict__ Xs, float2* __restrict__ X, int K) {
+  const int64_t b = blockIdx.y;
+  const int n2 = 2 * K;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < K * K; e += gridDim.x * blockDim.x) {
+    const int i = e / K, j = e % K;
+    const float* col = Xs + b * (int64_t)n2 * K + (int64_t)j * n2;
+    X[b * (int64_t)K * K + e] = make_float2(col[2 * i], col[2 * i + 1]);
+  }
+}
+
 unsigned grid_for(int64_t n, int t) {
   int64_t g = (n + t - 1) / t;
   return (unsigned)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
@@ -173,6 +362,8 @@ bool tc_general_supported(int dtype, int M, int K) {
   (void)M;
   return K >= 96 && (dtype == XL_C128 || (2 * K) % 4 == 0);
 }
+
+bool tc_pcg_supported(int K) { return K % 2 == 0 && 2 * K <= 32 * 4 * PCG_V; }
 
 size_t tc_gram_ws_bytes(int dtype, int64_t Bc, int M, int K) {
   if (dtype == XL_C128) return CUBLAS_WS;
@@ -287,6 +478,61 @@ int tc_apply(int dtype, const void* H, const void* X, const double* beta, int64_
     return check_launch("tc F");
   }
   return XL_SUCCESS;
+}
+
+
+size_t tc_pcg_ws_bytes(int64_t B, int K) {
+  const size_t n2 = 2 * (size_t)K;
+  return align_up((size_t)B * n2 * 2 * n2 * 4) + align_up((size_t)B * n2 * n2 * 4) +
+         align_up((size_t)B * 2 * n2 * K * 4) + 4 * align_up((size_t)B * n2 * K * 4) +
+         align_up((size_t)B * n2 * 4) + align_up((size_t)B * K * 4);
+}
+
+// X ~= A^{-1} for B realizations (complex64, identity RHS, w0 = 0, T iterations);
+// status gets NotHpd / Splitting like pcg_kernel.  cws: the CUBLAS_WS bytes
+// shared with tc_gram / tc_apply; bufs: tc_pcg_ws_bytes(B, K).
+int tc_pcg(int method, int variant, const void* A, int64_t B, int K, int T, void* X, int32_t* status, void* cws,
+           void* bufs, cudaStream_t st) {
+  cublasHandle_t h = handle_for_device();
+  if (!h) { set_error("cublasCreate failed"); return XL_ERR_CUDA; }
+  cublasSetStream(h, st);
+  cublasSetWorkspace(h, cws, CUBLAS_WS);
+  char* p = (char*)bufs;
+  const int n2 = 2 * K;
+  PcgState s;
+  s.E1 = (float*)p; p += align_up((size_t)B * n2 * 2 * n2 * 4);
+  s.E2 = (float*)p; p += align_up((size_t)B * n2 * n2 * 4);
+  s.SP = (float*)p; p += align_up((size_t)B * 2 * n2 * K * 4);
+  s.Q = (float*)p; p += align_up((size_t)B * n2 * K * 4);
+  s.P = (float*)p; p += align_up((size_t)B * n2 * K * 4);
+  s.X = (float*)p; p += align_up((size_t)B * n2 * K * 4);
+  s.R = (float*)p; p += align_up((size_t)B * n2 * K * 4);
+  s.C = (float*)p; p += align_up((size_t)B * n2 * 4);
+  s.rz = (float*)p;
+  pcg_init_kernel<<<(unsigned)B, 256, 0, st>>>((const float2*)A, s, K, method, variant, status);
+  if (int e = check_launch("tc pcg init")) return e;
+  const float one = 1.0f, zero = 0.0f;
+  for (int t = 1; t <= T; ++t) {
+    // Q = [A''h | A''h] [Ph ; Pl] + A''l Ph
+    int e = cublas_check(cublasGemmStridedBatchedEx(h, CUBLAS_OP_N, CUBLAS_OP_N, n2, K, 2 * n2, &one, s.E1, CUDA_R_32F,
+                                                    n2, (long long)n2 * 2 * n2, s.SP, CUDA_R_32F, 2 * n2,
+                                                    (long long)2 * n2 * K, &zero, s.Q, CUDA_R_32F, n2,
+                                                    (long long)n2 * K, (int)B, CUBLAS_COMPUTE_32F_FAST_TF32,
+                                                    CUBLAS_GEMM_DEFAULT),
+                         "tc pcg hh+hl");
+    if (e) return e;
+    e = cublas_check(cublasGemmStridedBatchedEx(h, CUBLAS_OP_N, CUBLAS_OP_N, n2, K, n2, &one, s.E2, CUDA_R_32F, n2,
+                                                (long long)n2 * n2, s.SP, CUDA_R_32F, 2 * n2, (long long)2 * n2 * K,
+                                                &one, s.Q, CUDA_R_32F, n2, (long long)n2 * K, (int)B,
+                                                CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT),
+                     "tc pcg lh");
+    if (e) return e;
+    pcg_update_kernel<<<(unsigned)B, 256, 0, st>>>(s, K, method, variant, status);
+    if ((e = check_launch("tc pcg update"))) return e;
+  }
+  const unsigned gx = grid_for((int64_t)K * K, 256);
+  pcg_store_x_kernel<<<dim3(gx > 64 ? 64 : gx, (unsigned)B), 256, 0, st>>>(s.X, (float2*)X, K);
+  return check_launch("tc pcg store");
 }
 
 }  // namespace xl

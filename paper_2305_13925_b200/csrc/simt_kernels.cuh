@@ -50,6 +50,11 @@ int tc_gram(int dtype, const void* H, int64_t Bc, int M, int K, const double* xi
 int tc_apply(int dtype, const void* H, const void* X, const double* beta, int64_t Bc, int M, int K, void* W,
              void* F, void* ws, cudaStream_t st, bool resplit);
 
+size_t tc_pcg_ws_bytes(int64_t B, int K);
+bool tc_pcg_supported(int K);
+int tc_pcg(int method, int variant, const void* A, int64_t B, int K, int T, void* X, int32_t* status, void* cws,
+           void* bufs, cudaStream_t st);
+
 int launch_ber(int dtype, const void* Bc, const int8_t* bits, const void* noise, int64_t B, int K,
                int nsym, int64_t* errors, cudaStream_t st);
 

@@ -155,7 +155,10 @@ static int64_t tc_chunk_size(int dtype, int64_t B, int M, int K) {
 
 static size_t general_ws(int dtype, int64_t B, int M, int K) {
   size_t w = simt_rzf_ws(dtype, B, M, K);
-  if (tc_general_supported(dtype, M, K)) w += align_up(tc_gram_ws_bytes(dtype, tc_chunk_size(dtype, B, M, K), M, K));
+  if (tc_general_supported(dtype, M, K)) {
+    w += align_up(tc_gram_ws_bytes(dtype, tc_chunk_size(dtype, B, M, K), M, K));
+    if (dtype == XL_C64 && tc_pcg_supported(K)) w += align_up(tc_pcg_ws_bytes(B, K));
+  }
   return w;
 }
 
@@ -189,7 +192,8 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   const int ptiles = gemm_tiles(M, K) > gemm_tiles(K, K) ? gemm_tiles(M, K) : gemm_tiles(K, K);
   double* part = (double*)p; p += align_up((size_t)B * ptiles * sizeof(double));
   int32_t* iters = (int32_t*)p; p += align_up((size_t)B * 4);
-  void* tcws = p;  // gemm_tc.cu: cuBLAS workspace + split operands
+  void* tcws = p;  // gemm_tc.cu: cuBLAS workspace + split operands (+ the tensor-core PCG state)
+  void* pcgws = tc ? (void*)(p + align_up(tc_gram_ws_bytes(dtype, tc_chunk_size(dtype, B, M, K), M, K))) : nullptr;
   void* Xo = X ? X : Xw;
   const xl_stream_t stream = (xl_stream_t)st;
   int e;
@@ -216,8 +220,12 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
     }
     return XL_SUCCESS;
   };
-  if ((e = xl_solve(dtype, method, variant, A, B, K, nullptr, K, nullptr, nullptr, method == XL_CG,
-                    T, -1.0, Xo, iters, nullptr, nullptr, status, sw, sws, stream))) return e;
+  if (tc && dtype == XL_C64 && method != XL_DIRECT && tc_pcg_supported(K)) {
+    if ((e = tc_pcg(method, variant, A, B, K, T, Xo, status, tcws, pcgws, st))) return e;
+  } else if ((e = xl_solve(dtype, method, variant, A, B, K, nullptr, K, nullptr, nullptr, method == XL_CG,
+                           T, -1.0, Xo, iters, nullptr, nullptr, status, sw, sws, stream))) {
+    return e;
+  }
   // Coupling and ||F||^2 from the K x K side: GX = (A - xi I) X,
   // ||F||_F^2 = Re tr(X^H GX) (precoder.py:64-70 with F = H X), beta, then
   // W = beta H X in one pass and B = H^H W = beta GX (metrics.py:35-44):

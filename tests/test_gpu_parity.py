@@ -306,6 +306,28 @@ def test_large_k_tensor_core_general_path(cfg, B, tol):
             np.testing.assert_allclose(gam[b], gr, rtol=max(10 * tol, 1e-8))
 
 
+def test_large_k_pcg_variants_vs_oracle():
+    """The tensor-core Jac-PCG / CG of the large-K general path (gemm_tc.cu
+    tc_pcg) against the complex128 oracle for all three recurrences on the
+    same regularized Gram matrices; Algorithm 1 amplifies round-off (SURVEY
+    F2), so its bound is looser."""
+    wl = X.CONFIGS["cfg4"]
+    H = X.generate_channels(wl.model, seed=5, first=3, B=2, dtype=torch.complex64)
+    Hn = H.cpu().numpy().astype(np.complex128)
+    for method, variant, tol in (("jacpcg", "textbook", 1e-4), ("cg", "textbook", 1e-3),
+                                 ("jacpcg", "algorithm", 1e-2)):
+        out = BT.rzf_batched(H, wl.alpha(), wl.power(), method=method, T=wl.T, variant=variant,
+                             want_X=True)
+        Xg = out.X.cpu().numpy()
+        for b in range(2):
+            P = O.gram_regularized(Hn[b], wl.alpha())
+            K = P.shape[0]
+            o = (O.cg_solve(P, np.eye(K), wl.T) if method == "cg"
+                 else O.jacpcg_solve(P, np.eye(K), wl.T, variant=variant))
+            assert relf(Xg[b], o.w) <= tol, (method, variant, b, relf(Xg[b], o.w))
+        assert (out.status == 0).all()
+
+
 def test_c128_cfg1_full_batch():
     """configs[0]: 100 realizations, complex128, Jac-PCG T=4 and direct at 1e-10."""
     wl = X.CONFIGS["cfg1"]
