@@ -101,7 +101,7 @@ def _check(H, out, alpha, power, method, T, variant):
             np.testing.assert_allclose(gam[b], g, rtol=max(1e-3, 10 * wt), atol=1e-6 * np.abs(g).max())
 
 
-@pytest.mark.parametrize("S,K", [(16, 64), (4, 32), (4, 16), (2, 64), (1, 16)])
+@pytest.mark.parametrize("S,K", [(16, 64), (4, 32), (4, 16), (2, 64), (1, 16), (64, 64), (48, 32)])
 def test_fused_shapes_vs_oracle(S, K):
     assert BT.uses_tensor_cores(torch.complex64, "jacpcg", 64 * S, K)
     m = X.ChannelModel(S=S, K=K, p=0.6, r=0.7)
@@ -198,6 +198,23 @@ def test_fused_range_fallback():
     out = BT.rzf_batched(H, 1.6, 10.0, T=4)
     assert out.status.cpu().tolist() == [0, 0]
     _check(H, out, 1.6, 10.0, "jacpcg", 4, "textbook")
+
+
+@pytest.mark.parametrize("B", [1, 147, 149, 297])
+def test_fused_odd_batch_sizes(B):
+    """Dynamic realization claiming at batch sizes around the grid (148 CTAs)."""
+    m = X.ChannelModel(S=4, K=64, p=0.5, r=0.5)
+    H = X.generate_channels(m, seed=8, first=11, B=B, dtype=torch.complex64)
+    out = BT.rzf_batched(H, 6.4, 10.0, T=4)
+    assert (out.status == 0).all()
+    idx = sorted({0, B // 2, B - 1})
+    sub = BT.rzf_batched(H[idx].contiguous(), 6.4, 10.0, T=4)
+    assert torch.equal(sub.W, out.W[idx]) and torch.equal(sub.sum_se, out.sum_se[idx])
+    Hn = H[idx].cpu().numpy().astype(np.complex128)
+    for i, b in enumerate(idx):
+        G, _, _, s = O.precoder_and_se(Hn[i], 6.4, 10.0, 1.0, "jacpcg", 4, "textbook")
+        assert relf(out.W[b].cpu().numpy(), G) <= 1e-4
+        assert abs(out.sum_se[b].item() - s) <= 1e-4 * abs(s)
 
 
 def test_fused_determinism_and_batch_independence():
