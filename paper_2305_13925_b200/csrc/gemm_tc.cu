@@ -19,7 +19,6 @@
 // Reference ops replaced: precoder.py:59-60 (H^H H + xi I, symmetrised) and
 // precoder.py:88-91 + 64-70 (F = H X, G = beta F).
 #include <cublas_v2.h>
-#include <mutex>
 
 #include "xl_common.cuh"
 #include "simt_kernels.cuh"
@@ -32,14 +31,16 @@ constexpr size_t CUBLAS_WS = 32u << 20;  // cuBLAS workspace carved from the cal
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// One cuBLAS handle per (host thread, device): set stream / workspace calls on
+// a handle are not safe against another thread using it concurrently.
 cublasHandle_t handle_for_device() {
-  static std::mutex mu;
-  static cublasHandle_t handles[64] = {};
+  thread_local cublasHandle_t handles[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
-  if (!handles[dev]) {
-    if (cublasCreate(&handles[dev]) != CUBLAS_STATUS_SUCCESS) return nullptr;
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!handles[dev] && cublasCreate(&handles[dev]) != CUBLAS_STATUS_SUCCESS) {
+    handles[dev] = nullptr;
+    return nullptr;
   }
   return handles[dev];
 }
