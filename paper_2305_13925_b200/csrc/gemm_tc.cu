@@ -352,6 +352,64 @@ __global__ void pcg_store_x_kernel(const float* __restrict__ Xs, float2* __restr
   }
 }
 
+PcgState pcg_state(char* p, int64_t B, int K) {
+  const size_t n2 = 2 * (size_t)K;
+  PcgState s;
+  s.E1 = (float*)p; p += align_up((size_t)B * n2 * 2 * n2 * 4);
+  s.E2 = (float*)p; p += align_up((size_t)B * n2 * n2 * 4);
+  s.SP = (float*)p; p += align_up((size_t)B * 2 * n2 * K * 4);
+  s.Q = (float*)p; p += align_up((size_t)B * n2 * K * 4);
+  s.P = (float*)p; p += align_up((size_t)B * n2 * K * 4);
+  s.X = (float*)p; p += align_up((size_t)B * n2 * K * 4);
+  s.R = (float*)p; p += align_up((size_t)B * n2 * K * 4);
+  s.C = (float*)p; p += align_up((size_t)B * n2 * 4);
+  s.rz = (float*)p;
+  return s;
+}
+
+// [Xh ; Xl] split of the embedded X state (for the GX product)
+__global__ void split_x_kernel(PcgState s, int K) {
+  const int64_t b = blockIdx.y;
+  const int n2 = 2 * K;
+  const int64_t per = (int64_t)n2 * K;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per; e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e / n2), r = (int)(e % n2);
+    const float v = s.X[b * per + e];
+    const float h = tf32_rn(v);
+    s.SP[b * 2 * per + (int64_t)j * 2 * n2 + r] = h;
+    s.SP[b * 2 * per + (int64_t)j * 2 * n2 + n2 + r] = v - h;
+  }
+}
+
+// GX = A'' X - xi X -> complex row-major K x K, and Re tr(X^H GX) = ||F||^2 / ...
+// per realization in double, fixed order (one CTA per realization)
+__global__ void gx_finish_kernel(PcgState s, int K, const double* __restrict__ xi_b, double xi,
+                                 float2* __restrict__ GX, double* __restrict__ part) {
+  const int64_t b = blockIdx.x;
+  const int n2 = 2 * K;
+  const int64_t per = (int64_t)n2 * K;
+  const double x0 = xi_b ? xi_b[b] : xi;
+  double local = 0.0;
+  for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+    const int i = e / K, j = e % K;
+    const int64_t o = b * per + (int64_t)j * n2 + 2 * i;
+    const float xr = s.X[o], xim = s.X[o + 1];
+    const float gr = (float)((double)s.Q[o] - x0 * (double)xr);
+    const float gi = (float)((double)s.Q[o + 1] - x0 * (double)xim);
+    GX[b * (int64_t)K * K + e] = make_float2(gr, gi);
+    local += (double)xr * (double)gr + (double)xim * (double)gi;
+  }
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    part[b] = t;
+  }
+}
+
 unsigned grid_for(int64_t n, int t) {
   int64_t g = (n + t - 1) / t;
   return (unsigned)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
@@ -500,16 +558,7 @@ int tc_pcg(int method, int variant, const void* A, int64_t B, int K, int T, void
   cublasSetWorkspace(h, cws, CUBLAS_WS);
   char* p = (char*)bufs;
   const int n2 = 2 * K;
-  PcgState s;
-  s.E1 = (float*)p; p += align_up((size_t)B * n2 * 2 * n2 * 4);
-  s.E2 = (float*)p; p += align_up((size_t)B * n2 * n2 * 4);
-  s.SP = (float*)p; p += align_up((size_t)B * 2 * n2 * K * 4);
-  s.Q = (float*)p; p += align_up((size_t)B * n2 * K * 4);
-  s.P = (float*)p; p += align_up((size_t)B * n2 * K * 4);
-  s.X = (float*)p; p += align_up((size_t)B * n2 * K * 4);
-  s.R = (float*)p; p += align_up((size_t)B * n2 * K * 4);
-  s.C = (float*)p; p += align_up((size_t)B * n2 * 4);
-  s.rz = (float*)p;
+  const PcgState s = pcg_state(p, B, K);
   pcg_init_kernel<<<(unsigned)B, 256, 0, st>>>((const float2*)A, s, K, method, variant, status);
   if (int e = check_launch("tc pcg init")) return e;
   const float one = 1.0f, zero = 0.0f;
@@ -534,6 +583,39 @@ int tc_pcg(int method, int variant, const void* A, int64_t B, int K, int T, void
   const unsigned gx = grid_for((int64_t)K * K, 256);
   pcg_store_x_kernel<<<dim3(gx > 64 ? 64 : gx, (unsigned)B), 256, 0, st>>>(s.X, (float2*)X, K);
   return check_launch("tc pcg store");
+}
+
+
+// After tc_pcg (same cws / bufs): GX = (A - xi I) X as complex row-major K x K
+// (the coupling up to beta) and one ||F||^2 partial per realization in part[B]
+// (= Re tr(X^H GX)), on the tensor cores.
+int tc_gx(const double* xi_b, double xi, int64_t B, int K, void* GX, double* part, void* cws, void* bufs,
+          cudaStream_t st) {
+  cublasHandle_t h = handle_for_device();
+  if (!h) { set_error("cublasCreate failed"); return XL_ERR_CUDA; }
+  cublasSetStream(h, st);
+  cublasSetWorkspace(h, cws, CUBLAS_WS);
+  const int n2 = 2 * K;
+  const PcgState s = pcg_state((char*)bufs, B, K);
+  const unsigned gx = grid_for((int64_t)n2 * K, 256);
+  split_x_kernel<<<dim3(gx > 64 ? 64 : gx, (unsigned)B), 256, 0, st>>>(s, K);
+  if (int e = check_launch("tc gx split")) return e;
+  const float one = 1.0f, zero = 0.0f;
+  int e = cublas_check(cublasGemmStridedBatchedEx(h, CUBLAS_OP_N, CUBLAS_OP_N, n2, K, 2 * n2, &one, s.E1, CUDA_R_32F,
+                                                  n2, (long long)n2 * 2 * n2, s.SP, CUDA_R_32F, 2 * n2,
+                                                  (long long)2 * n2 * K, &zero, s.Q, CUDA_R_32F, n2,
+                                                  (long long)n2 * K, (int)B, CUBLAS_COMPUTE_32F_FAST_TF32,
+                                                  CUBLAS_GEMM_DEFAULT),
+                       "tc gx hh+hl");
+  if (e) return e;
+  e = cublas_check(cublasGemmStridedBatchedEx(h, CUBLAS_OP_N, CUBLAS_OP_N, n2, K, n2, &one, s.E2, CUDA_R_32F, n2,
+                                              (long long)n2 * n2, s.SP, CUDA_R_32F, 2 * n2, (long long)2 * n2 * K,
+                                              &one, s.Q, CUDA_R_32F, n2, (long long)n2 * K, (int)B,
+                                              CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT),
+                   "tc gx lh");
+  if (e) return e;
+  gx_finish_kernel<<<(unsigned)B, 256, 0, st>>>(s, K, xi_b, xi, (float2*)GX, part);
+  return check_launch("tc gx finish");
 }
 
 }  // namespace xl

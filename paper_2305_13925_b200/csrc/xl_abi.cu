@@ -220,7 +220,8 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
     }
     return XL_SUCCESS;
   };
-  if (tc && dtype == XL_C64 && method != XL_DIRECT && tc_pcg_supported(K)) {
+  const bool tcp = tc && dtype == XL_C64 && method != XL_DIRECT && tc_pcg_supported(K);
+  if (tcp) {
     if ((e = tc_pcg(method, variant, A, B, K, T, Xo, status, tcws, pcgws, st))) return e;
   } else if ((e = xl_solve(dtype, method, variant, A, B, K, nullptr, K, nullptr, nullptr, method == XL_CG,
                            T, -1.0, Xo, iters, nullptr, nullptr, status, sw, sws, stream))) {
@@ -234,8 +235,13 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   const int np = gemm_tiles(K, K);
   void* GX = sw;  // the solver workspace is free again (>= B K K)
   if (dtype == XL_C64) {
-    if ((e = launch_cgemm<float>(false, EPI_GXF, A, sK, K, Xo, sK, K, GX, sK, K, B, K, K, K, xi_per_batch, xi, part, st))) return e;
-    if ((e = launch_beta_from_partials(B, part, np, power, beta, status, st))) return e;
+    if (tcp) {  // GX and the ||F||^2 partials on the tensor cores from the PCG state
+      if ((e = tc_gx(xi_per_batch, xi, B, K, GX, part, tcws, pcgws, st))) return e;
+      if ((e = launch_beta_from_partials(B, part, 1, power, beta, status, st))) return e;
+    } else {
+      if ((e = launch_cgemm<float>(false, EPI_GXF, A, sK, K, Xo, sK, K, GX, sK, K, B, K, K, K, xi_per_batch, xi, part, st))) return e;
+      if ((e = launch_beta_from_partials(B, part, np, power, beta, status, st))) return e;
+    }
     if (tc) {
       if ((e = tc_w())) return e;
     } else {
