@@ -306,6 +306,23 @@ def test_large_k_tensor_core_general_path(cfg, B, tol):
             np.testing.assert_allclose(gam[b], gr, rtol=max(10 * tol, 1e-8))
 
 
+@pytest.mark.parametrize("M,K", [(1000, 96), (640, 320), (130, 128)])
+def test_large_k_odd_shapes(M, K):
+    """Tensor-core general path at shapes off the BASELINE grid: K = 96 (n2 not a
+    multiple of 128), K = 320 (tensor-core Gram / W with the SIMT Jac-PCG), M not a
+    multiple of 64, per-realization xi."""
+    rng = np.random.default_rng(M + K)
+    Hn = (rng.standard_normal((2, M, K)) + 1j * rng.standard_normal((2, M, K))) / np.sqrt(2)
+    H = torch.from_numpy(Hn.astype(np.complex64)).to(DEV)
+    xi = torch.tensor([K / 10.0, K / 3.0], dtype=torch.float64, device=DEV)
+    out = BT.rzf_batched(H, xi, 10.0, method="jacpcg", T=4)
+    Hq = H.cpu().numpy().astype(np.complex128)
+    for b in range(2):
+        Gr, br, gr, s = O.precoder_and_se(Hq[b], float(xi[b]), 10.0, 1.0, "jacpcg", 4, "textbook")
+        assert relf(out.W[b].cpu().numpy(), Gr) <= 1e-4, (M, K, b)
+        assert abs(out.sum_se[b].item() - s) <= 1e-4 * abs(s)
+
+
 def test_large_k_pcg_variants_vs_oracle():
     """The tensor-core Jac-PCG / CG of the large-K general path (gemm_tc.cu
     tc_pcg) against the complex128 oracle for all three recurrences on the
