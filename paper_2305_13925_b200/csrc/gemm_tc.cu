@@ -81,22 +81,35 @@ __global__ void split_rows_kernel(const float4* __restrict__ Z, float4* __restri
 
 // U [b] (n2 x n2) -> A[b] (K x K complex): G = (U + U^T)/2,
 // Re A_ij = G[2i][2j] + G[2i+1][2j+1], Im A_ij = G[2i][2j+1] - G[2i+1][2j], + xi on the
-// diagonal.  Exactly Hermitian by construction (real diagonal).
-__global__ void gram_extract_kernel(const float* __restrict__ U, float2* __restrict__ A, int K,
-                                    const double* __restrict__ xi_b, double xi) {
-  const int64_t b = blockIdx.y;
+// diagonal.  Exactly Hermitian by construction (real diagonal).  One CTA per 32 x 32
+// tile of A: the 64 x 64 blocks of U and of U^T it needs are staged through shared
+// memory with coalesced row reads; A is written row by row.
+constexpr int XT = 32;
+__global__ void __launch_bounds__(256) gram_extract_kernel(const float* __restrict__ U, float2* __restrict__ A,
+                                                           int K, const double* __restrict__ xi_b, double xi) {
+  const int64_t b = blockIdx.x;
   const int n2 = 2 * K;
+  const int i0 = blockIdx.z * XT, j0 = blockIdx.y * XT;
   const float* u = U + b * (int64_t)n2 * n2;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < K * K; e += gridDim.x * blockDim.x) {
-    const int i = e / K, j = e % K;
-    auto g = [&](int r, int c) { return 0.5f * (u[(int64_t)r * n2 + c] + u[(int64_t)c * n2 + r]); };
-    float re = g(2 * i, 2 * j) + g(2 * i + 1, 2 * j + 1);
-    float im = g(2 * i, 2 * j + 1) - g(2 * i + 1, 2 * j);
+  __shared__ float t1[2 * XT][2 * XT + 1], t2[2 * XT][2 * XT + 1];  // U[2i0.., 2j0..], U[2j0.., 2i0..]
+  for (int e = threadIdx.x; e < 4 * XT * XT; e += blockDim.x) {
+    const int rr = e / (2 * XT), cc = e % (2 * XT);
+    const int r1 = 2 * i0 + rr, c1 = 2 * j0 + cc, r2 = 2 * j0 + rr, c2 = 2 * i0 + cc;
+    t1[rr][cc] = (r1 < n2 && c1 < n2) ? u[(int64_t)r1 * n2 + c1] : 0.0f;
+    t2[rr][cc] = (r2 < n2 && c2 < n2) ? u[(int64_t)r2 * n2 + c2] : 0.0f;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < XT * XT; e += blockDim.x) {
+    const int ti = e / XT, tj = e % XT, i = i0 + ti, j = j0 + tj;
+    if (i >= K || j >= K) continue;
+    auto g = [&](int dr, int dc) { return 0.5f * (t1[2 * ti + dr][2 * tj + dc] + t2[2 * tj + dc][2 * ti + dr]); };
+    float re = g(0, 0) + g(1, 1);
+    float im = g(0, 1) - g(1, 0);
     if (i == j) {
       re = (float)((double)re + (xi_b ? xi_b[b] : xi));
       im = 0.0f;
     }
-    A[b * (int64_t)K * K + e] = make_float2(re, im);
+    A[b * (int64_t)K * K + (int64_t)i * K + j] = make_float2(re, im);
   }
 }
 
@@ -107,21 +120,23 @@ __global__ void gram_extract_kernel(const float* __restrict__ U, float2* __restr
 // Xe[2i][2j] = xr, Xe[2i][2j+1] = xi, Xe[2i+1][2j] = -xi, Xe[2i+1][2j+1] = xr.
 __global__ void embed_x_kernel(const float2* __restrict__ X, const double* __restrict__ beta, float* __restrict__ E1,
                                float* __restrict__ E2, int K) {
-  const int64_t b = blockIdx.y;
+  const int64_t b = blockIdx.x;
   const int n2 = 2 * K;
   const float sc = (float)beta[b];
   float* e1 = E1 + b * (int64_t)n2 * 2 * n2;
   float* e2 = E2 + b * (int64_t)n2 * n2;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n2 * n2; e += gridDim.x * blockDim.x) {
-    const int r = e / n2, c = e % n2;  // Xe[r][c]
-    const float2 x = X[b * (int64_t)K * K + (r / 2) * K + (c / 2)];
-    const float xr = x.x * sc, xi = x.y * sc;
-    const float v = (r & 1) == 0 ? ((c & 1) == 0 ? xr : xi) : ((c & 1) == 0 ? -xi : xr);
-    const float h = tf32_rn(v), l = v - h;
-    // column-major (n2 rows) view of row-major Xe: element (c, r) at r * n2 + c
-    e1[(int64_t)r * n2 + c] = h;
-    e1[(int64_t)(n2 + r) * n2 + c] = h;
-    e2[(int64_t)r * n2 + c] = l;
+  const float2* xb = X + b * (int64_t)K * K;
+  for (int r = blockIdx.y; r < n2; r += gridDim.y) {  // Xe row r: column r of the col-major view
+    const float2* xrow = xb + (int64_t)(r >> 1) * K;
+    for (int c = threadIdx.x; c < n2; c += blockDim.x) {
+      const float2 x = xrow[c >> 1];
+      const float xr = x.x * sc, xi = x.y * sc;
+      const float v = (r & 1) == 0 ? ((c & 1) == 0 ? xr : xi) : ((c & 1) == 0 ? -xi : xr);
+      const float h = tf32_rn(v);
+      e1[(int64_t)r * n2 + c] = h;
+      e1[(int64_t)(n2 + r) * n2 + c] = h;
+      e2[(int64_t)r * n2 + c] = v - h;
+    }
   }
 }
 
@@ -147,9 +162,9 @@ __global__ void scale_c128_kernel(double2* __restrict__ W, double2* __restrict__
 
 __global__ void herm_add_kernel(double2* __restrict__ A, int K, const double* __restrict__ xi_b, double xi) {
   // (P + P^H)/2 + xi I on the ZGEMM result (precoder.py:59-60)
-  const int64_t b = blockIdx.y;
+  const int64_t b = blockIdx.x;
   double2* a = A + b * (int64_t)K * K;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < K * K; e += gridDim.x * blockDim.x) {
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < K * K; e += gridDim.y * blockDim.x) {
     const int i = e / K, j = e % K;
     if (j > i) continue;
     const double2 p = a[(int64_t)i * K + j], q = a[(int64_t)j * K + i];
@@ -214,18 +229,20 @@ __global__ void pcg_init_kernel(const float2* __restrict__ A, PcgState s, int K,
     c[2 * i] = d;
     c[2 * i + 1] = d;
   }
-  // A''(r, col): col 2j = A[:, j] (re/im interleaved), col 2j+1 = i A[:, j]; A[i][j] = conj(A[j][i])
-  for (int64_t e = threadIdx.x; e < (int64_t)n2 * n2; e += blockDim.x) {
-    const int col = (int)(e / n2), r = (int)(e % n2);
-    const int j = col >> 1, i = r >> 1;
-    const float2 aij = a[(int64_t)i * K + j];
-    float v;
-    if ((col & 1) == 0) v = (r & 1) == 0 ? aij.x : aij.y;   // A_ij
-    else v = (r & 1) == 0 ? -aij.y : aij.x;                 // i A_ij
-    const float h = tf32_rn(v), l = v - h;
-    e1[(int64_t)col * n2 + r] = h;
-    e1[(int64_t)(n2 + col) * n2 + r] = h;
-    e2[(int64_t)col * n2 + r] = l;
+  // A''(r, col): col 2j = A[:, j] (re/im interleaved), col 2j+1 = i A[:, j].  A is
+  // Hermitian, so column j is conj(row j): read row j contiguously.
+  for (int col = 0; col < n2; ++col) {
+    const int j = col >> 1;
+    const float2* arow = a + (int64_t)j * K;
+    for (int r = threadIdx.x; r < n2; r += blockDim.x) {
+      const float2 aji = arow[r >> 1];  // A_ij = conj(A_ji)
+      const float re = aji.x, im = -aji.y;
+      const float v = (col & 1) == 0 ? ((r & 1) == 0 ? re : im) : ((r & 1) == 0 ? -im : re);
+      const float h = tf32_rn(v);
+      e1[(int64_t)col * n2 + r] = h;
+      e1[(int64_t)(n2 + col) * n2 + r] = h;
+      e2[(int64_t)col * n2 + r] = v - h;
+    }
   }
   __syncthreads();
   if (zero_diag) {
@@ -341,14 +358,25 @@ __global__ void pcg_update_kernel(PcgState s, int K, int method, int variant, in
   if (not_hpd && threadIdx.x == 0 && status[b] == 0) status[b] = XL_STATUS_NOT_HPD;
 }
 
-// column-major embedded X (n2 x K) -> row-major complex X (K x K)
-__global__ void pcg_store_x_kernel(const float* __restrict__ Xs, float2* __restrict__ X, int K) {
-  const int64_t b = blockIdx.y;
+// column-major embedded X (n2 x K) -> row-major complex X (K x K): 32 x 32 tiles
+// through shared memory (coalesced on both sides)
+__global__ void __launch_bounds__(256) pcg_store_x_kernel(const float* __restrict__ Xs, float2* __restrict__ X,
+                                                          int K) {
+  const int64_t b = blockIdx.x;
   const int n2 = 2 * K;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < K * K; e += gridDim.x * blockDim.x) {
-    const int i = e / K, j = e % K;
-    const float* col = Xs + b * (int64_t)n2 * K + (int64_t)j * n2;
-    X[b * (int64_t)K * K + e] = make_float2(col[2 * i], col[2 * i + 1]);
+  const int i0 = blockIdx.z * XT, j0 = blockIdx.y * XT;
+  __shared__ float2 t[XT][XT + 1];  // [j][i]
+  for (int e = threadIdx.x; e < XT * XT; e += blockDim.x) {
+    const int tj = e / XT, ti = e % XT, i = i0 + ti, j = j0 + tj;
+    if (i < K && j < K) {
+      const float* col = Xs + b * (int64_t)n2 * K + (int64_t)j * n2;
+      t[tj][ti] = make_float2(col[2 * i], col[2 * i + 1]);
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < XT * XT; e += blockDim.x) {
+    const int ti = e / XT, tj = e % XT, i = i0 + ti, j = j0 + tj;
+    if (i < K && j < K) X[b * (int64_t)K * K + (int64_t)i * K + j] = t[tj][ti];
   }
 }
 
@@ -369,10 +397,10 @@ PcgState pcg_state(char* p, int64_t B, int K) {
 
 // [Xh ; Xl] split of the embedded X state (for the GX product)
 __global__ void split_x_kernel(PcgState s, int K) {
-  const int64_t b = blockIdx.y;
+  const int64_t b = blockIdx.x;
   const int n2 = 2 * K;
   const int64_t per = (int64_t)n2 * K;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per; e += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t e = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; e < per; e += (int64_t)gridDim.y * blockDim.x) {
     const int j = (int)(e / n2), r = (int)(e % n2);
     const float v = s.X[b * per + e];
     const float h = tf32_rn(v);
@@ -381,32 +409,41 @@ __global__ void split_x_kernel(PcgState s, int K) {
   }
 }
 
-// GX = A'' X - xi X -> complex row-major K x K, and Re tr(X^H GX) = ||F||^2 / ...
-// per realization in double, fixed order (one CTA per realization)
-__global__ void gx_finish_kernel(PcgState s, int K, const double* __restrict__ xi_b, double xi,
-                                 float2* __restrict__ GX, double* __restrict__ part) {
+// GX = A'' X - xi X -> complex row-major K x K, and Re tr(X^H GX) partials: one per
+// 32 x 32 tile (fixed-order sums, combined by the beta kernel in tile order)
+__global__ void __launch_bounds__(256) gx_finish_kernel(PcgState s, int K, const double* __restrict__ xi_b, double xi,
+                                                        float2* __restrict__ GX, double* __restrict__ part) {
   const int64_t b = blockIdx.x;
   const int n2 = 2 * K;
   const int64_t per = (int64_t)n2 * K;
+  const int i0 = blockIdx.z * XT, j0 = blockIdx.y * XT;
   const double x0 = xi_b ? xi_b[b] : xi;
+  __shared__ float2 t[XT][XT + 1];  // [j][i]
   double local = 0.0;
-  for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-    const int i = e / K, j = e % K;
-    const int64_t o = b * per + (int64_t)j * n2 + 2 * i;
-    const float xr = s.X[o], xim = s.X[o + 1];
-    const float gr = (float)((double)s.Q[o] - x0 * (double)xr);
-    const float gi = (float)((double)s.Q[o + 1] - x0 * (double)xim);
-    GX[b * (int64_t)K * K + e] = make_float2(gr, gi);
-    local += (double)xr * (double)gr + (double)xim * (double)gi;
+  for (int e = threadIdx.x; e < XT * XT; e += blockDim.x) {
+    const int tj = e / XT, ti = e % XT, i = i0 + ti, j = j0 + tj;
+    if (i < K && j < K) {
+      const int64_t o = b * per + (int64_t)j * n2 + 2 * i;
+      const float xr = s.X[o], xim = s.X[o + 1];
+      const float gr = (float)((double)s.Q[o] - x0 * (double)xr);
+      const float gi = (float)((double)s.Q[o + 1] - x0 * (double)xim);
+      t[tj][ti] = make_float2(gr, gi);
+      local += (double)xr * (double)gr + (double)xim * (double)gi;
+    }
   }
-  __shared__ double red[32];
+  __syncthreads();
+  for (int e = threadIdx.x; e < XT * XT; e += blockDim.x) {
+    const int ti = e / XT, tj = e % XT, i = i0 + ti, j = j0 + tj;
+    if (i < K && j < K) GX[b * (int64_t)K * K + (int64_t)i * K + j] = t[tj][ti];
+  }
+  __shared__ double red[8];
   for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = local;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    part[b] = t;
+    double tt = 0.0;
+    for (int w = 0; w < 8; ++w) tt += red[w];
+    part[b * gridDim.y * gridDim.z + blockIdx.z * gridDim.y + blockIdx.y] = tt;
   }
 }
 
@@ -451,7 +488,7 @@ int tc_gram(int dtype, const void* H, int64_t Bc, int M, int K, const double* xi
                          "tc gram zgemm");
     if (e) return e;
     const unsigned gk = grid_for((int64_t)K * K, 256);
-    herm_add_kernel<<<dim3(gk > 64 ? 64 : gk, (unsigned)Bc), 256, 0, st>>>((double2*)A, K, xi_b, xi);
+    herm_add_kernel<<<dim3((unsigned)Bc, gk > 64 ? 64 : gk), 256, 0, st>>>((double2*)A, K, xi_b, xi);
     return check_launch("tc herm");
   }
   const int n2 = 2 * K;
@@ -474,8 +511,8 @@ int tc_gram(int dtype, const void* H, int64_t Bc, int M, int K, const double* xi
                                               CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT),
                    "tc gram hl");
   if (e) return e;
-  unsigned gx = grid_for((int64_t)K * K, 256);
-  gram_extract_kernel<<<dim3(gx > 64 ? 64 : gx, (unsigned)Bc), 256, 0, st>>>(U, (float2*)A, K, xi_b, xi);
+  const unsigned nt = (unsigned)((K + XT - 1) / XT);
+  gram_extract_kernel<<<dim3((unsigned)Bc, nt, nt), 256, 0, st>>>(U, (float2*)A, K, xi_b, xi);
   return check_launch("tc gram extract");
 }
 
@@ -514,8 +551,7 @@ int tc_apply(int dtype, const void* H, const void* X, const double* beta, int64_
     split_rows_kernel<<<grid_for(nrow * n2 / 4, 256), 256, 0, st>>>((const float4*)H, (float4*)S, nrow, n2);
     if (int e = check_launch("tc split")) return e;
   }
-  unsigned gx = grid_for((int64_t)n2 * n2, 256);
-  embed_x_kernel<<<dim3(gx > 64 ? 64 : gx, (unsigned)Bc), 256, 0, st>>>((const float2*)X, beta, E1, E2, K);
+  embed_x_kernel<<<dim3((unsigned)Bc, (unsigned)(n2 < 128 ? n2 : 128)), 256, 0, st>>>((const float2*)X, beta, E1, E2, K);
   if (int e = check_launch("tc embed")) return e;
   const float one = 1.0f, zero = 0.0f;
   const long long sS = (long long)M * 2 * n2, sW = (long long)M * n2;
@@ -580,15 +616,15 @@ int tc_pcg(int method, int variant, const void* A, int64_t B, int K, int T, void
     pcg_update_kernel<<<(unsigned)B, 256, 0, st>>>(s, K, method, variant, status);
     if ((e = check_launch("tc pcg update"))) return e;
   }
-  const unsigned gx = grid_for((int64_t)K * K, 256);
-  pcg_store_x_kernel<<<dim3(gx > 64 ? 64 : gx, (unsigned)B), 256, 0, st>>>(s.X, (float2*)X, K);
+  const unsigned nt = (unsigned)((K + XT - 1) / XT);
+  pcg_store_x_kernel<<<dim3((unsigned)B, nt, nt), 256, 0, st>>>(s.X, (float2*)X, K);
   return check_launch("tc pcg store");
 }
 
 
 // After tc_pcg (same cws / bufs): GX = (A - xi I) X as complex row-major K x K
-// (the coupling up to beta) and one ||F||^2 partial per realization in part[B]
-// (= Re tr(X^H GX)), on the tensor cores.
+// (the coupling up to beta) and the ||F||^2 partials (= Re tr(X^H GX), SURVEY
+// K3/K4): ceil(K/32)^2 per realization in part, on the tensor cores.
 int tc_gx(const double* xi_b, double xi, int64_t B, int K, void* GX, double* part, void* cws, void* bufs,
           cudaStream_t st) {
   cublasHandle_t h = handle_for_device();
@@ -598,7 +634,7 @@ int tc_gx(const double* xi_b, double xi, int64_t B, int K, void* GX, double* par
   const int n2 = 2 * K;
   const PcgState s = pcg_state((char*)bufs, B, K);
   const unsigned gx = grid_for((int64_t)n2 * K, 256);
-  split_x_kernel<<<dim3(gx > 64 ? 64 : gx, (unsigned)B), 256, 0, st>>>(s, K);
+  split_x_kernel<<<dim3((unsigned)B, gx > 64 ? 64 : gx), 256, 0, st>>>(s, K);
   if (int e = check_launch("tc gx split")) return e;
   const float one = 1.0f, zero = 0.0f;
   int e = cublas_check(cublasGemmStridedBatchedEx(h, CUBLAS_OP_N, CUBLAS_OP_N, n2, K, 2 * n2, &one, s.E1, CUDA_R_32F,
@@ -614,7 +650,8 @@ int tc_gx(const double* xi_b, double xi, int64_t B, int K, void* GX, double* par
                                               CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT),
                    "tc gx lh");
   if (e) return e;
-  gx_finish_kernel<<<(unsigned)B, 256, 0, st>>>(s, K, xi_b, xi, (float2*)GX, part);
+  const unsigned nt = (unsigned)((K + XT - 1) / XT);
+  gx_finish_kernel<<<dim3((unsigned)B, nt, nt), 256, 0, st>>>(s, K, xi_b, xi, (float2*)GX, part);
   return check_launch("tc gx finish");
 }
 

@@ -237,7 +237,8 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   if (dtype == XL_C64) {
     if (tcp) {  // GX and the ||F||^2 partials on the tensor cores from the PCG state
       if ((e = tc_gx(xi_per_batch, xi, B, K, GX, part, tcws, pcgws, st))) return e;
-      if ((e = launch_beta_from_partials(B, part, 1, power, beta, status, st))) return e;
+      const int nt = (K + 31) / 32;
+      if ((e = launch_beta_from_partials(B, part, nt * nt, power, beta, status, st))) return e;
     } else {
       if ((e = launch_cgemm<float>(false, EPI_GXF, A, sK, K, Xo, sK, K, GX, sK, K, B, K, K, K, xi_per_batch, xi, part, st))) return e;
       if ((e = launch_beta_from_partials(B, part, np, power, beta, status, st))) return e;
