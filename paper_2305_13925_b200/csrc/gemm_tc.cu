@@ -447,6 +447,187 @@ __global__ void __launch_bounds__(256) gx_finish_kernel(PcgState s, int K, const
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// complex128: the same recurrences with ZGEMM (FP64 tensor cores) for Q = A P
+// directly on the complex state (no split: DMMA products are exact fp64).  The
+// state is the column-major complex K x K matrix (column j = RHS j), read as
+// real n2-vectors by the update kernel.
+// ---------------------------------------------------------------------------
+struct PcgState64 {
+  double* Q;
+  double* P;
+  double* X;
+  double* R;
+  double* C;
+  double* rz;
+};
+
+PcgState64 pcg_state64(char* p, int64_t B, int K) {
+  const size_t n2 = 2 * (size_t)K;
+  PcgState64 s;
+  s.Q = (double*)p; p += align_up((size_t)B * n2 * K * 8);
+  s.P = (double*)p; p += align_up((size_t)B * n2 * K * 8);
+  s.X = (double*)p; p += align_up((size_t)B * n2 * K * 8);
+  s.R = (double*)p; p += align_up((size_t)B * n2 * K * 8);
+  s.C = (double*)p; p += align_up((size_t)B * n2 * 8);
+  s.rz = (double*)p;
+  return s;
+}
+
+__global__ void pcg_init64_kernel(const double2* __restrict__ A, PcgState64 s, int K, int method, int variant,
+                                  int32_t* __restrict__ status) {
+  const int64_t b = blockIdx.x;
+  const int n2 = 2 * K;
+  const double2* a = A + b * (int64_t)K * K;
+  double* c = s.C + b * (int64_t)n2;
+  const bool use_c = method == XL_JACPCG;
+  const bool textbook = use_c && variant == XL_TEXTBOOK;
+  __shared__ int zero_diag;
+  if (threadIdx.x == 0) zero_diag = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < K; i += blockDim.x) {
+    const double d = use_c ? a[(int64_t)i * K + i].x : 1.0;
+    if (d == 0.0) zero_diag = 1;
+    c[2 * i] = d;
+    c[2 * i + 1] = d;
+  }
+  __syncthreads();
+  if (zero_diag && threadIdx.x == 0) status[b] = XL_STATUS_SPLITTING;
+  const int64_t per = (int64_t)n2 * K;
+  for (int64_t e = threadIdx.x; e < per; e += blockDim.x) {
+    const int j = (int)(e / n2), r = (int)(e % n2);
+    const double ci = c[r];
+    const double rv = r == 2 * j ? ((use_c && !textbook) ? 1.0 / ci : 1.0) : 0.0;
+    s.R[b * per + e] = rv;
+    s.X[b * per + e] = 0.0;
+    s.P[b * per + e] = textbook ? rv / ci : rv;
+  }
+  for (int j = threadIdx.x; j < K; j += blockDim.x) {
+    const double ci = c[2 * j];
+    s.rz[b * K + j] = textbook ? 1.0 / ci : (use_c ? (1.0 / ci) * (1.0 / ci) : 1.0);
+  }
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+constexpr int PCG_V64 = 8;  // double2 per lane and vector: n2 <= 32 * 2 * PCG_V64
+__global__ void __launch_bounds__(256) pcg_update64_kernel(PcgState64 s, int K, int method, int variant,
+                                                           int32_t* __restrict__ status) {
+  const int64_t b = blockIdx.x;
+  const int n2 = 2 * K, nq = n2 / 2;
+  const int64_t per = (int64_t)n2 * K;
+  const bool use_c = method == XL_JACPCG;
+  const bool textbook = use_c && variant == XL_TEXTBOOK;
+  const double2* c2 = reinterpret_cast<const double2*>(s.C + b * (int64_t)n2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __shared__ int not_hpd;
+  if (threadIdx.x == 0) not_hpd = 0;
+  __syncthreads();
+  for (int j = warp; j < K; j += nw) {
+    const int64_t o = b * per + (int64_t)j * n2;
+    const double2* q2 = reinterpret_cast<const double2*>(s.Q + o);
+    double2* p2 = reinterpret_cast<double2*>(s.P + o);
+    double2* x2 = reinterpret_cast<double2*>(s.X + o);
+    double2* r2 = reinterpret_cast<double2*>(s.R + o);
+    const double rzj = s.rz[b * K + j];
+    const bool act = rzj > 0.0;
+    double2 qv[PCG_V64], pv[PCG_V64], cv[PCG_V64];
+    double curv = 0.0;
+#pragma unroll
+    for (int t = 0; t < PCG_V64; ++t) {
+      const int i = lane + 32 * t;
+      if (i < nq) {
+        qv[t] = q2[i];
+        pv[t] = p2[i];
+        cv[t] = use_c ? c2[i] : make_double2(1.0, 1.0);
+        if (use_c && !textbook) { qv[t].x /= cv[t].x; qv[t].y /= cv[t].y; }
+        curv += pv[t].x * qv[t].x + pv[t].y * qv[t].y;
+      }
+    }
+    curv = warp_sum_d(curv);
+    if (curv <= 0.0 && act && lane == 0) not_hpd = 1;
+    const double al = act ? rzj / (curv > 0.0 ? curv : 1.0) : 0.0;
+    double acc = 0.0;
+    double2 rv[PCG_V64];
+#pragma unroll
+    for (int t = 0; t < PCG_V64; ++t) {
+      const int i = lane + 32 * t;
+      if (i < nq) {
+        double2 xv = x2[i];
+        rv[t] = r2[i];
+        xv.x += al * pv[t].x; xv.y += al * pv[t].y;
+        rv[t].x -= al * qv[t].x; rv[t].y -= al * qv[t].y;
+        x2[i] = xv;
+        r2[i] = rv[t];
+        acc += textbook ? rv[t].x * (rv[t].x / cv[t].x) + rv[t].y * (rv[t].y / cv[t].y)
+                        : rv[t].x * rv[t].x + rv[t].y * rv[t].y;
+      }
+    }
+    acc = warp_sum_d(acc);
+    const double be = act ? acc / rzj : 0.0;
+#pragma unroll
+    for (int t = 0; t < PCG_V64; ++t) {
+      const int i = lane + 32 * t;
+      if (i < nq) {
+        double2 m;
+        m.x = (textbook ? rv[t].x / cv[t].x : rv[t].x) + be * pv[t].x;
+        m.y = (textbook ? rv[t].y / cv[t].y : rv[t].y) + be * pv[t].y;
+        p2[i] = m;
+      }
+    }
+    if (lane == 0) s.rz[b * K + j] = acc;
+  }
+  __syncthreads();
+  if (not_hpd && threadIdx.x == 0 && status[b] == 0) status[b] = XL_STATUS_NOT_HPD;
+}
+
+// column-major complex (column j contiguous) -> row-major K x K, 32 x 32 tiles;
+// with Q given: GX = Q - xi X and the Re tr(X^H GX) partials per tile
+__global__ void __launch_bounds__(256) cm_to_rm64_kernel(const double* __restrict__ Xs, const double* __restrict__ Qs,
+                                                         int K, const double* __restrict__ xi_b, double xi,
+                                                         double2* __restrict__ out, double* __restrict__ part) {
+  const int64_t b = blockIdx.x;
+  const int64_t per = 2 * (int64_t)K * K;
+  const int i0 = blockIdx.z * XT, j0 = blockIdx.y * XT;
+  const double x0 = Qs ? (xi_b ? xi_b[b] : xi) : 0.0;
+  __shared__ double2 t[XT][XT + 1];
+  double local = 0.0;
+  for (int e = threadIdx.x; e < XT * XT; e += blockDim.x) {
+    const int tj = e / XT, ti = e % XT, i = i0 + ti, j = j0 + tj;
+    if (i < K && j < K) {
+      const int64_t o = b * per + (int64_t)j * 2 * K + 2 * i;
+      const double xr = Xs[o], xim = Xs[o + 1];
+      if (Qs) {
+        const double gr = Qs[o] - x0 * xr, gi = Qs[o + 1] - x0 * xim;
+        t[tj][ti] = make_double2(gr, gi);
+        local += xr * gr + xim * gi;
+      } else {
+        t[tj][ti] = make_double2(xr, xim);
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < XT * XT; e += blockDim.x) {
+    const int ti = e / XT, tj = e % XT, i = i0 + ti, j = j0 + tj;
+    if (i < K && j < K) out[b * (int64_t)K * K + (int64_t)i * K + j] = t[tj][ti];
+  }
+  if (part) {
+    __shared__ double red[8];
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = local;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tt = 0.0;
+      for (int w = 0; w < 8; ++w) tt += red[w];
+      part[b * gridDim.y * gridDim.z + blockIdx.z * gridDim.y + blockIdx.y] = tt;
+    }
+  }
+}
+
 unsigned grid_for(int64_t n, int t) {
   int64_t g = (n + t - 1) / t;
   return (unsigned)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
@@ -653,6 +834,62 @@ int tc_gx(const double* xi_b, double xi, int64_t B, int K, void* GX, double* par
   const unsigned nt = (unsigned)((K + XT - 1) / XT);
   gx_finish_kernel<<<dim3((unsigned)B, nt, nt), 256, 0, st>>>(s, K, xi_b, xi, (float2*)GX, part);
   return check_launch("tc gx finish");
+}
+
+
+size_t tc_pcg64_ws_bytes(int64_t B, int K) {
+  const size_t n2 = 2 * (size_t)K;
+  return 4 * align_up((size_t)B * n2 * K * 8) + align_up((size_t)B * n2 * 8) + align_up((size_t)B * K * 8);
+}
+
+bool tc_pcg64_supported(int K) { return 2 * K <= 32 * 2 * PCG_V64; }
+
+// complex128 Jac-PCG / CG for the rzf path (identity RHS, w0 = 0, T iterations):
+// Q = A P per iteration as one ZGEMM (OP_T of the column-major view of row-major
+// A is A), then the per-column update; X out row-major.
+int tc_pcg64(int method, int variant, const void* A, int64_t B, int K, int T, void* X, int32_t* status, void* cws,
+             void* bufs, cudaStream_t st) {
+  cublasHandle_t h = handle_for_device();
+  if (!h) { set_error("cublasCreate failed"); return XL_ERR_CUDA; }
+  cublasSetStream(h, st);
+  cublasSetWorkspace(h, cws, CUBLAS_WS);
+  const PcgState64 s = pcg_state64((char*)bufs, B, K);
+  pcg_init64_kernel<<<(unsigned)B, 256, 0, st>>>((const double2*)A, s, K, method, variant, status);
+  if (int e = check_launch("tc pcg64 init")) return e;
+  const cuDoubleComplex one = make_cuDoubleComplex(1, 0), zero = make_cuDoubleComplex(0, 0);
+  const long long sk = (long long)K * K;
+  for (int t = 1; t <= T; ++t) {
+    int e = cublas_check(cublasZgemmStridedBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, K, K, K, &one,
+                                                   (const cuDoubleComplex*)A, K, sk, (const cuDoubleComplex*)s.P, K,
+                                                   sk, &zero, (cuDoubleComplex*)s.Q, K, sk, (int)B),
+                         "tc pcg64 zgemm");
+    if (e) return e;
+    pcg_update64_kernel<<<(unsigned)B, 256, 0, st>>>(s, K, method, variant, status);
+    if ((e = check_launch("tc pcg64 update"))) return e;
+  }
+  const unsigned nt = (unsigned)((K + XT - 1) / XT);
+  cm_to_rm64_kernel<<<dim3((unsigned)B, nt, nt), 256, 0, st>>>(s.X, nullptr, K, nullptr, 0.0, (double2*)X, nullptr);
+  return check_launch("tc pcg64 store");
+}
+
+// After tc_pcg64: GX = (A - xi I) X and the ||F||^2 partials per 32 x 32 tile.
+int tc_gx64(const void* A, const double* xi_b, double xi, int64_t B, int K, void* GX, double* part, void* cws,
+            void* bufs, cudaStream_t st) {
+  cublasHandle_t h = handle_for_device();
+  if (!h) { set_error("cublasCreate failed"); return XL_ERR_CUDA; }
+  cublasSetStream(h, st);
+  cublasSetWorkspace(h, cws, CUBLAS_WS);
+  const PcgState64 s = pcg_state64((char*)bufs, B, K);
+  const cuDoubleComplex one = make_cuDoubleComplex(1, 0), zero = make_cuDoubleComplex(0, 0);
+  const long long sk = (long long)K * K;
+  int e = cublas_check(cublasZgemmStridedBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, K, K, K, &one, (const cuDoubleComplex*)A,
+                                                 K, sk, (const cuDoubleComplex*)s.X, K, sk, &zero,
+                                                 (cuDoubleComplex*)s.Q, K, sk, (int)B),
+                       "tc gx64 zgemm");
+  if (e) return e;
+  const unsigned nt = (unsigned)((K + XT - 1) / XT);
+  cm_to_rm64_kernel<<<dim3((unsigned)B, nt, nt), 256, 0, st>>>(s.X, s.Q, K, xi_b, xi, (double2*)GX, part);
+  return check_launch("tc gx64 finish");
 }
 
 }  // namespace xl

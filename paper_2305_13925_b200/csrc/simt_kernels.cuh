@@ -52,6 +52,12 @@ int tc_apply(int dtype, const void* H, const void* X, const double* beta, int64_
 
 size_t tc_pcg_ws_bytes(int64_t B, int K);
 bool tc_pcg_supported(int K);
+size_t tc_pcg64_ws_bytes(int64_t B, int K);
+bool tc_pcg64_supported(int K);
+int tc_pcg64(int method, int variant, const void* A, int64_t B, int K, int T, void* X, int32_t* status, void* cws,
+             void* bufs, cudaStream_t st);
+int tc_gx64(const void* A, const double* xi_b, double xi, int64_t B, int K, void* GX, double* part, void* cws,
+            void* bufs, cudaStream_t st);
 int tc_gx(const double* xi_b, double xi, int64_t B, int K, void* GX, double* part, void* cws, void* bufs,
           cudaStream_t st);
 int tc_pcg(int method, int variant, const void* A, int64_t B, int K, int T, void* X, int32_t* status, void* cws,

@@ -158,6 +158,7 @@ static size_t general_ws(int dtype, int64_t B, int M, int K) {
   if (tc_general_supported(dtype, M, K)) {
     w += align_up(tc_gram_ws_bytes(dtype, tc_chunk_size(dtype, B, M, K), M, K));
     if (dtype == XL_C64 && tc_pcg_supported(K)) w += align_up(tc_pcg_ws_bytes(B, K));
+    if (dtype == XL_C128 && tc_pcg64_supported(K)) w += align_up(tc_pcg64_ws_bytes(B, K));
   }
   return w;
 }
@@ -221,8 +222,11 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
     return XL_SUCCESS;
   };
   const bool tcp = tc && dtype == XL_C64 && method != XL_DIRECT && tc_pcg_supported(K);
+  const bool tcp64 = tc && dtype == XL_C128 && method != XL_DIRECT && tc_pcg64_supported(K);
   if (tcp) {
     if ((e = tc_pcg(method, variant, A, B, K, T, Xo, status, tcws, pcgws, st))) return e;
+  } else if (tcp64) {
+    if ((e = tc_pcg64(method, variant, A, B, K, T, Xo, status, tcws, pcgws, st))) return e;
   } else if ((e = xl_solve(dtype, method, variant, A, B, K, nullptr, K, nullptr, nullptr, method == XL_CG,
                            T, -1.0, Xo, iters, nullptr, nullptr, status, sw, sws, stream))) {
     return e;
@@ -251,8 +255,14 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
     }
     return launch_sinr<float>(GX, B, K, sigma2, gamma, nullptr, sum_se, st, beta);
   }
-  if ((e = launch_cgemm<double>(false, EPI_GXF, A, sK, K, Xo, sK, K, GX, sK, K, B, K, K, K, xi_per_batch, xi, part, st))) return e;
-  if ((e = launch_beta_from_partials(B, part, np, power, beta, status, st))) return e;
+  if (tcp64) {
+    if ((e = tc_gx64(A, xi_per_batch, xi, B, K, GX, part, tcws, pcgws, st))) return e;
+    const int nt = (K + 31) / 32;
+    if ((e = launch_beta_from_partials(B, part, nt * nt, power, beta, status, st))) return e;
+  } else {
+    if ((e = launch_cgemm<double>(false, EPI_GXF, A, sK, K, Xo, sK, K, GX, sK, K, B, K, K, K, xi_per_batch, xi, part, st))) return e;
+    if ((e = launch_beta_from_partials(B, part, np, power, beta, status, st))) return e;
+  }
   if (tc) {
     if ((e = tc_w())) return e;
   } else {

@@ -345,6 +345,25 @@ def test_large_k_pcg_variants_vs_oracle():
         assert (out.status == 0).all()
 
 
+def test_large_k_pcg_c128_variants_vs_oracle():
+    """complex128 large-K rzf path (ZGEMM Gram / W, ZGEMM-based Jac-PCG / CG and
+    GX): all three recurrences at the c128 tolerance."""
+    rng = np.random.default_rng(17)
+    M, K, T = 512, 128, 5
+    Hn = (rng.standard_normal((2, M, K)) + 1j * rng.standard_normal((2, M, K))) / np.sqrt(2)
+    H = torch.from_numpy(Hn).to(DEV)
+    xi, power = K / 10.0, 10.0
+    for method, variant in (("jacpcg", "textbook"), ("cg", "textbook"), ("jacpcg", "algorithm")):
+        out = BT.rzf_batched(H, xi, power, method=method, T=T, variant=variant, want_X=True)
+        for b in range(2):
+            Gr, br, gr, s = O.precoder_and_se(Hn[b], xi, power, 1.0, method, T, variant)
+            tol = max(1e-10, 100 * _sensitivity(O.gram_regularized(Hn[b], xi), np.eye(K), T, None,
+                                                "cg" if method == "cg" else variant))
+            assert relf(out.W[b].cpu().numpy(), Gr) <= tol, (method, variant, b, relf(out.W[b].cpu().numpy(), Gr))
+            assert abs(out.sum_se[b].item() - s) <= max(1e-8, tol) * abs(s)
+        assert (out.status == 0).all()
+
+
 def test_c128_cfg1_full_batch():
     """configs[0]: 100 realizations, complex128, Jac-PCG T=4 and direct at 1e-10."""
     wl = X.CONFIGS["cfg1"]
