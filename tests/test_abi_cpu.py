@@ -60,6 +60,18 @@ def test_host_side_validation_without_device(lib):
     assert lib.xl_rzf(*rz) == L.XL_ERR_CONFIG                                            # sigma2 = 0
     assert b"noise power" in lib.xl_last_error()
     assert lib.xl_se_partials(None, 4, 0, None, None) == L.XL_ERR_CONFIG
+    # stationary solvers (linsolve.py:128-176): T < 1, omega <= 0, unknown method
+    st = [0, L.XL_JOR, None, 1, 4, None, 4, None, 0.5, 0, -1.0] + [None] * 6 + [0, None]
+    assert lib.xl_solve_stationary(*st) == L.XL_ERR_CONFIG                               # T = 0
+    st[9] = 2
+    st[8] = 0.0
+    assert lib.xl_solve_stationary(*st) == L.XL_ERR_CONFIG                               # omega = 0
+    assert b"omega" in lib.xl_last_error()
+    st[1] = L.XL_JACPCG
+    assert lib.xl_solve_stationary(*st) == L.XL_ERR_CONFIG                               # not JOR/GS
+    # BER chain: bad sizes / dtype
+    assert lib.xl_ber_errors(0, None, None, None, 1, 0, 8, None, None) == L.XL_ERR_CONFIG
+    assert lib.xl_ber_errors(9, None, None, None, 1, 4, 8, None, None) == L.XL_ERR_CONFIG
 
 
 def test_status_mapping_to_reference_exceptions():
@@ -77,4 +89,7 @@ def test_status_mapping_to_reference_exceptions():
 
 def test_workspace_queries(lib):
     assert lib.xl_rzf_workspace_bytes(0, 0, 16, 1024, 64) > 0
+    # large K: the tensor-core general path also holds the split rows of H (2x its bytes)
+    M, K, B = 4096, 128, 64
+    assert lib.xl_rzf_workspace_bytes(0, 0, B, M, K) >= 2 * B * M * K * 8
     assert lib.xl_solve_workspace_bytes(1, 16, 64, 64) == 16 * 4 * 64 * 64 * 16
