@@ -47,16 +47,23 @@ def _check_tensor(t, name, ndim, dt=None):
 
 
 class _Workspace:
-    """Per-device scratch buffer that only grows (no per-call cudaMalloc)."""
+    """Per-(device, stream) scratch buffer that only grows (no per-call
+    cudaMalloc).  Keyed by stream so concurrent calls on different streams never
+    share scratch; allocated on that stream, so the caching allocator's reuse
+    after a grow is stream-ordered."""
 
     def __init__(self):
         self.buf = {}
 
-    def get(self, device, nbytes: int) -> torch.Tensor:
-        key = torch.device(device).index
+    def get(self, device, nbytes: int, stream=None) -> torch.Tensor:
+        dev = torch.device(device)
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        key = (dev.index, s.cuda_stream)
         cur = self.buf.get(key)
         if cur is None or cur.numel() < nbytes:
-            cur = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            self.buf.pop(key, None)
+            with torch.cuda.stream(s):
+                cur = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=dev)
             self.buf[key] = cur
         return cur
 
@@ -143,7 +150,7 @@ def rzf_batched(H: torch.Tensor, xi, power: float, method: str = "jacpcg", T: in
     else:
         nbytes = int(lib.xl_rzf_workspace_bytes(dc, METHODS[method], B, M, K))
         fn = lib.xl_rzf
-    ws = _WS.get(H.device, nbytes)
+    ws = _WS.get(H.device, nbytes, stream)
     rc = fn(dc, METHODS[method], VARIANTS[variant], L.ptr(H), B, M, K, xs,
             L.ptr(xt), float(power), int(T), float(sigma2), L.ptr(out.W),
             L.ptr(out.F), L.ptr(out.beta), L.ptr(out.gamma), L.ptr(out.sum_se),
@@ -237,7 +244,7 @@ def solve_batched(A: torch.Tensor, method: str = "jacpcg", T: int = 5, variant: 
     tr = torch.empty(B, Tn + 1, dtype=torch.float64, device=dev) if trace else None
     itr = torch.empty(B, Tn, K, R, dtype=A.dtype, device=dev) if iterates else None
     nbytes = int(lib.xl_solve_workspace_bytes(dc, B, K, R))
-    ws = _WS.get(dev, nbytes)
+    ws = _WS.get(dev, nbytes, stream)
     if method in ("jor", "gs"):
         rc = lib.xl_solve_stationary(dc, SOLVE_METHODS[method], L.ptr(A), B, K, L.ptr(S), R,
                                      L.ptr(w0), float(omega), int(T),
@@ -266,7 +273,7 @@ def apply_precoder_batched(H: torch.Tensor, X: torch.Tensor, power: float, sigma
     out = alloc_outputs(H, True, want_F, False)
     dc = dtype_code(H.dtype)
     nbytes = int(lib.xl_apply_precoder_workspace_bytes(dc, B, M, K))
-    ws = _WS.get(H.device, nbytes)
+    ws = _WS.get(H.device, nbytes, stream)
     L.check(lib.xl_apply_precoder(dc, L.ptr(H), L.ptr(X), B, M, K, float(power), float(sigma2),
                                   L.ptr(out.W), L.ptr(out.F), L.ptr(out.beta), L.ptr(out.gamma),
                                   L.ptr(out.sum_se), L.ptr(out.status), L.ptr(ws), ws.numel(),
