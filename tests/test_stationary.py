@@ -164,3 +164,67 @@ def test_gpu_rzf_iterative_stationary(solver):
     assert relf(blk.F, F) < 1e-10
     assert abs(blk.beta - beta) / beta < 1e-10
     assert relf(blk.G, beta * F) < 1e-10
+
+
+# ------------------------------------------ known answers (test_linsolve.py) --
+
+def _rand_hpd(rng, n, cond_cap=10.0):
+    A = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    Q, _ = np.linalg.qr(A)
+    P = (Q * rng.uniform(1.0, cond_cap, size=n)) @ Q.conj().T
+    return (P + P.conj().T) / 2.0
+
+
+@pytest.mark.gpu
+def test_gpu_gs_known_answers():
+    """Gauss-Seidel pins of the reference's suite (test_linsolve.py:60-96), on the GPU."""
+    import paper_2305_13925_b200 as X
+    from paper_2305_13925_b200.errors import ConfigurationError, SplittingError
+    sysm = lambda P, s: X.HpdSystem(P=np.asarray(P, dtype=complex), rhs=np.asarray(s, dtype=complex))
+    out = X.gs_solve(sysm(np.eye(3), [1.0, 2.0, 3.0]), T=1)           # identity: one sweep
+    np.testing.assert_allclose(out.w, [1.0, 2.0, 3.0])
+    assert out.residual_trace[-1] == 0.0
+    out = X.gs_solve(sysm([[2.0, 1.0], [1.0, 2.0]], [3.0, 3.0]), T=1)  # hand-computed sweep
+    np.testing.assert_allclose(out.w, [1.5, 0.75])
+    rng = np.random.default_rng(2)
+    for _ in range(5):                                                 # converges to direct
+        P = _rand_hpd(rng, 16)
+        s = rng.standard_normal(16) + 1j * rng.standard_normal(16)
+        ref = np.linalg.solve(P, s)
+        out = X.gs_solve(sysm(P, s), T=300)
+        assert np.linalg.norm(out.w - ref) < 1e-8 * np.linalg.norm(ref)
+        assert out.converged
+    with pytest.raises(SplittingError):
+        X.gs_solve(sysm([[0.0, 1.0], [1.0, 0.0]], [1.0, 1.0]), T=1)
+    out = X.gs_solve(sysm(np.eye(2), [1.0, 1.0]), T=4)
+    assert len(out.residual_trace) == out.iterations + 1
+    with pytest.raises(ConfigurationError):
+        X.gs_solve(sysm(np.eye(2), [1.0, 1.0]), T=0)
+    P = _rand_hpd(np.random.default_rng(3), 8, 100.0)                  # eps early stop
+    s = np.random.default_rng(4).standard_normal(8) + 0j
+    out = X.gs_solve(sysm(P, s), T=500, eps=1e-6)
+    assert out.iterations < 500 and out.converged
+    assert np.sqrt(out.residual_trace[-1]) <= 1e-6
+
+
+@pytest.mark.gpu
+def test_gpu_jor_known_answers():
+    """JOR pins of the reference's suite (test_linsolve.py:99-122), on the GPU."""
+    import paper_2305_13925_b200 as X
+    from paper_2305_13925_b200.errors import ConfigurationError
+    sysm = lambda P, s: X.HpdSystem(P=np.asarray(P, dtype=complex), rhs=np.asarray(s, dtype=complex))
+    out = X.jor_solve(sysm([[2.0, 1.0], [1.0, 2.0]], [3.0, 3.0]), T=2, omega=1.0, keep_iterates=True)
+    np.testing.assert_allclose(out.iterates[0], [1.5, 1.5])
+    np.testing.assert_allclose(out.iterates[1], [0.75, 0.75])
+    out = X.jor_solve(sysm(np.diag([2.0, 5.0]), [4.0, 10.0]), T=1, omega=1.0)
+    np.testing.assert_allclose(out.w, [2.0, 2.0])
+    assert out.residual_trace[-1] == 0.0
+    P = _rand_hpd(np.random.default_rng(5), 8, 100.0)                  # divergence flagged
+    d = np.sqrt(np.diag(P).real)
+    lam_max = np.linalg.eigvalsh(P / np.outer(d, d))[-1]
+    s = np.random.default_rng(6).standard_normal(8) + 0j
+    out = X.jor_solve(sysm(P, s), T=50, omega=2.5 / lam_max)
+    assert not out.converged
+    assert out.residual_trace[-1] > out.residual_trace[0]
+    with pytest.raises(ConfigurationError):
+        X.jor_solve(sysm(np.eye(2), [1.0, 1.0]), T=1, omega=0.0)
