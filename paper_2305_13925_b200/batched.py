@@ -339,6 +339,45 @@ def combine_se_partials(partials) -> tuple[float, float]:
     return mean, math.sqrt(var) / math.sqrt(n)
 
 
+class GraphedRzf:
+    """A fixed-shape ``rzf_batched`` call captured once into a CUDA graph and
+    replayed: the whole precoder chain (fused kernel, or the general path's
+    kernels and library GEMMs) leaves the host in one launch, for callers whose
+    host thread is the bottleneck (tools/time_graph.py: with back-to-back calls
+    the GPU time dominates and replay gains nothing at cfg1-cfg3 sizes).
+
+        g = GraphedRzf(B, M, K, torch.complex64, xi, power)
+        out = g.run(H)      # copies H into the captured input, replays, returns
+                            # the captured outputs (valid until the next run)
+    """
+
+    def __init__(self, B: int, M: int, K: int, dtype, xi, power: float, method: str = "jacpcg",
+                 T: int = 4, variant: str = "textbook", sigma2: float = 1.0, want_gamma: bool = True,
+                 device=None):
+        dev = torch.device(device or "cuda")
+        self.stream = torch.cuda.Stream(dev)
+        self.H = torch.zeros(B, M, K, dtype=dtype, device=dev)
+        self.H[:, 0, :] = 1  # a valid input for the warm-up
+        self.out = alloc_outputs(self.H, want_gamma=want_gamma)
+        kw = dict(method=method, T=T, variant=variant, sigma2=sigma2, out=self.out, check=False,
+                  stream=self.stream)
+        self._xi = xi.to(dev).contiguous() if isinstance(xi, torch.Tensor) else xi
+        self.stream.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(self.stream):   # warm-up: workspace, modules, library handles
+            rzf_batched(self.H, self._xi, power, **kw)
+        self.stream.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            rzf_batched(self.H, self._xi, power, **kw)
+
+    def run(self, H: torch.Tensor, check: bool = True) -> PrecoderBatch:
+        self.H.copy_(H)
+        self.graph.replay()
+        if check:
+            L.raise_status(self.out.status.cpu().numpy(), "GraphedRzf")
+        return self.out
+
+
 class HostPipeline:
     """Host-buffer front end of the hot path: H (pinned host) -> W (pinned host).
 
