@@ -12,14 +12,6 @@
 // column by 64 threads from warp transpose-reduction partials summed over the
 // 4 quadrant warps in a fixed order (deterministic), then broadcast via smem.
 
-__device__ __forceinline__ void tmem_st8(uint32_t ta, const float* v) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
-               "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-               "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-               "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
-               : "memory");
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 template <int KU>
 __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* aeh, uint8_t* ael,

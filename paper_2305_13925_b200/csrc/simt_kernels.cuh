@@ -60,6 +60,10 @@ int tc_gx64(const void* A, const double* xi_b, double xi, int64_t B, int K, void
             void* bufs, cudaStream_t st);
 int tc_gx(const double* xi_b, double xi, int64_t B, int K, void* GX, double* part, void* cws, void* bufs,
           cudaStream_t st);
+// cluster_pcg.cu: fused 2-CTA-cluster Jac-PCG / CG + GX for K = 128 (complex64)
+bool cpcg_supported(int K);
+int cpcg_solve(int method, int variant, const void* A, int64_t B, int K, int T, double xi, const double* xi_b,
+               void* X, void* GX, double* part, int32_t* status, cudaStream_t st);
 int tc_pcg(int method, int variant, const void* A, int64_t B, int K, int T, void* X, int32_t* status, void* cws,
            void* bufs, cudaStream_t st);
 

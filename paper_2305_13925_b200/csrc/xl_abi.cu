@@ -221,9 +221,17 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
     }
     return XL_SUCCESS;
   };
-  const bool tcp = tc && dtype == XL_C64 && method != XL_DIRECT && tc_pcg_supported(K);
+  // K = 128 (complex64): the fused 2-CTA-cluster solver keeps the PCG state on
+  // chip and also returns GX and the ||F||^2 partials (cluster_pcg.cu)
+  const bool cpc = tc && dtype == XL_C64 && method != XL_DIRECT && cpcg_supported(K);
+  const bool tcp = tc && dtype == XL_C64 && method != XL_DIRECT && !cpc && tc_pcg_supported(K);
   const bool tcp64 = tc && dtype == XL_C128 && method != XL_DIRECT && tc_pcg64_supported(K);
-  if (tcp) {
+  const int64_t sH = (int64_t)M * K, sK = (int64_t)K * K;
+  const int np = gemm_tiles(K, K);
+  void* GX = sw;  // the solver workspace is free again (>= B K K)
+  if (cpc) {
+    if ((e = cpcg_solve(method, variant, A, B, K, T, xi, xi_per_batch, Xo, GX, part, status, st))) return e;
+  } else if (tcp) {
     if ((e = tc_pcg(method, variant, A, B, K, T, Xo, status, tcws, pcgws, st))) return e;
   } else if (tcp64) {
     if ((e = tc_pcg64(method, variant, A, B, K, T, Xo, status, tcws, pcgws, st))) return e;
@@ -235,11 +243,10 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   // ||F||_F^2 = Re tr(X^H GX) (precoder.py:64-70 with F = H X), beta, then
   // W = beta H X in one pass and B = H^H W = beta GX (metrics.py:35-44):
   // 8 K^3 instead of 8 M K^2 flops for the coupling, no separate F pass.
-  const int64_t sH = (int64_t)M * K, sK = (int64_t)K * K;
-  const int np = gemm_tiles(K, K);
-  void* GX = sw;  // the solver workspace is free again (>= B K K)
   if (dtype == XL_C64) {
-    if (tcp) {  // GX and the ||F||^2 partials on the tensor cores from the PCG state
+    if (cpc) {
+      if ((e = launch_beta_from_partials(B, part, 2, power, beta, status, st))) return e;
+    } else if (tcp) {  // GX and the ||F||^2 partials on the tensor cores from the PCG state
       if ((e = tc_gx(xi_per_batch, xi, B, K, GX, part, tcws, pcgws, st))) return e;
       const int nt = (K + 31) / 32;
       if ((e = launch_beta_from_partials(B, part, nt * nt, power, beta, status, st))) return e;

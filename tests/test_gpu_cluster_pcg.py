@@ -1,0 +1,103 @@
+"""GPU parity of the fused 2-CTA-cluster Jac-PCG (cluster_pcg.cu, K = 128
+complex64) that the large-K rzf path uses in place of the split-GEMM solver.
+
+Checks: W / beta / SE against the complex128 oracle (north_star tolerances,
+W relative Frobenius <= 1e-4), agreement with the split-GEMM solver it
+replaces (XL_LARGE_K_SOLVER=gemm selects that one per call), bit-identical
+repeat calls (the pair's scalars are summed in a fixed order), many clusters
+per launch, and per-realization xi.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import xlmimo_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+import paper_2305_13925_b200 as X  # noqa: E402
+from paper_2305_13925_b200 import batched as BT  # noqa: E402
+
+DEV = "cuda"
+
+
+def relf(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def _run(H, xi, power, method="jacpcg", T=5, variant="textbook", solver=None, **kw):
+    old = os.environ.get("XL_LARGE_K_SOLVER")
+    try:
+        if solver:
+            os.environ["XL_LARGE_K_SOLVER"] = solver
+        else:
+            os.environ.pop("XL_LARGE_K_SOLVER", None)
+        out = BT.rzf_batched(H, xi, power, method=method, T=T, variant=variant, **kw)
+        torch.cuda.synchronize()
+        return out
+    finally:
+        if old is None:
+            os.environ.pop("XL_LARGE_K_SOLVER", None)
+        else:
+            os.environ["XL_LARGE_K_SOLVER"] = old
+
+
+@pytest.mark.parametrize("method,variant,tol", [("jacpcg", "textbook", 1e-4), ("cg", "textbook", 1e-3),
+                                                ("jacpcg", "algorithm", 1e-2)])
+def test_cluster_pcg_vs_oracle_cfg4_channel(method, variant, tol):
+    wl = X.CONFIGS["cfg4"]
+    H = X.generate_channels(wl.model, seed=11, first=5, B=3, dtype=torch.complex64)
+    Hn = H.cpu().numpy().astype(np.complex128)
+    out = _run(H, wl.alpha(), wl.power(), method=method, T=wl.T, variant=variant, want_X=True)
+    W, S, beta = out.W.cpu().numpy(), out.sum_se.cpu().numpy(), out.beta.cpu().numpy()
+    assert (out.status.cpu().numpy() == 0).all()
+    for b in range(3):
+        Gr, br, gr, s = O.precoder_and_se(Hn[b], wl.alpha(), wl.power(), 1.0, method, wl.T, variant)
+        assert relf(W[b], Gr) <= tol, (method, variant, b, relf(W[b], Gr))
+        assert abs(beta[b] - br) <= tol * br
+        assert abs(S[b] - s) <= max(tol, 1e-4) * abs(s), (method, variant, b, S[b], s)
+
+
+def test_cluster_pcg_matches_split_gemm_solver():
+    """Same Gram, two solvers: the on-chip cluster solver and the split-GEMM
+    tc_pcg + tc_gx chain agree to the 3xFP16 / 3xTF32 rounding level."""
+    rng = np.random.default_rng(7)
+    B, M, K = 40, 384, 128
+    Hn = (rng.standard_normal((B, M, K)) + 1j * rng.standard_normal((B, M, K))) / np.sqrt(2)
+    H = torch.from_numpy(Hn.astype(np.complex64)).to(DEV)
+    xi = torch.from_numpy(rng.uniform(K / 30, K / 3, size=B)).to(DEV)
+    a = _run(H, xi, 10.0, T=5, want_X=True)
+    g = _run(H, xi, 10.0, T=5, want_X=True, solver="gemm")
+    for b in range(B):
+        assert relf(a.X[b].cpu().numpy(), g.X[b].cpu().numpy()) <= 2e-5, b
+        assert relf(a.W[b].cpu().numpy(), g.W[b].cpu().numpy()) <= 2e-5, b
+    np.testing.assert_allclose(a.beta.cpu().numpy(), g.beta.cpu().numpy(), rtol=2e-5)
+    np.testing.assert_allclose(a.sum_se.cpu().numpy(), g.sum_se.cpu().numpy(), rtol=2e-5)
+    np.testing.assert_allclose(a.gamma.cpu().numpy(), g.gamma.cpu().numpy(), rtol=1e-4)
+    # spot-check against the oracle with the per-realization xi
+    Hq = H.cpu().numpy().astype(np.complex128)
+    for b in (0, B - 1):
+        Gr, br, gr, s = O.precoder_and_se(Hq[b], float(xi[b]), 10.0, 1.0, "jacpcg", 5, "textbook")
+        assert relf(a.W[b].cpu().numpy(), Gr) <= 1e-4
+        assert abs(a.sum_se[b].item() - s) <= 1e-4 * abs(s)
+
+
+def test_cluster_pcg_deterministic_and_many_clusters():
+    """Hundreds of clusters (several waves) and bit-identical repeat calls."""
+    wl = X.CONFIGS["cfg4"]
+    rng = np.random.default_rng(3)
+    B, M, K = 300, 256, 128
+    Hn = (rng.standard_normal((B, M, K)) + 1j * rng.standard_normal((B, M, K))) / np.sqrt(2)
+    H = torch.from_numpy(Hn.astype(np.complex64)).to(DEV)
+    o1 = _run(H, wl.alpha(), wl.power(), T=5, want_X=True)
+    o2 = _run(H, wl.alpha(), wl.power(), T=5, want_X=True)
+    assert torch.equal(o1.X, o2.X) and torch.equal(o1.W, o2.W)
+    assert torch.equal(o1.sum_se, o2.sum_se) and torch.equal(o1.beta, o2.beta)
+    Hq = H.cpu().numpy().astype(np.complex128)
+    for b in (0, 149, 299):
+        Gr, br, gr, s = O.precoder_and_se(Hq[b], wl.alpha(), wl.power(), 1.0, "jacpcg", 5, "textbook")
+        assert relf(o1.W[b].cpu().numpy(), Gr) <= 1e-4, b
