@@ -697,6 +697,15 @@ int tc_gram(int dtype, const void* H, int64_t Bc, int M, int K, const double* xi
   return check_launch("tc gram extract");
 }
 
+// A = (U + U^T)/2 re-assembled as the complex Hermitian H^H H + xi I from the
+// fp32 real Gram U of Bc realizations (stream_tc.cu's Gram uses it too)
+int tc_gram_extract(const float* U, int64_t Bc, int K, const double* xi_b, double xi, void* A, cudaStream_t st) {
+  const unsigned nt = (unsigned)((K + XT - 1) / XT);
+  gram_extract_kernel<<<dim3((unsigned)Bc, nt, nt), 256, 0, st>>>(U, (float2*)A, K, xi_b, xi);
+  return check_launch("tc gram extract");
+}
+size_t tc_cublas_ws_bytes() { return CUBLAS_WS; }
+
 // W = beta H X for Bc realizations; their split rows are in ws from tc_gram
 // unless resplit; F = W / beta when requested.
 int tc_apply(int dtype, const void* H, const void* X, const double* beta, int64_t Bc, int M, int K, void* W,

@@ -60,6 +60,13 @@ int tc_gx64(const void* A, const double* xi_b, double xi, int64_t B, int K, void
             void* bufs, cudaStream_t st);
 int tc_gx(const double* xi_b, double xi, int64_t B, int K, void* GX, double* part, void* cws, void* bufs,
           cudaStream_t st);
+// stream_tc.cu: streaming tcgen05 Gram / W for K = 128 complex64 (M % 64 == 0)
+bool stc_supported(int dtype, int M, int K);
+int stc_gram(const void* H, int64_t B, int M, int K, float* sz, float* U, cudaStream_t st);
+int stc_apply(const void* H, const void* X, const double* beta, const float* sz, int64_t B, int M, int K, void* W,
+              void* F, cudaStream_t st);
+int tc_gram_extract(const float* U, int64_t Bc, int K, const double* xi_b, double xi, void* A, cudaStream_t st);
+size_t tc_cublas_ws_bytes();
 // cluster_pcg.cu: fused 2-CTA-cluster Jac-PCG / CG + GX for K = 128 (complex64)
 bool cpcg_supported(int K);
 int cpcg_solve(int method, int variant, const void* A, int64_t B, int K, int T, double xi, const double* xi_b,

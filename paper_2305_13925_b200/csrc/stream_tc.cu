@@ -1,0 +1,404 @@
+// Streaming tcgen05 Gram and W products for the large-K rzf path (complex64,
+// K = 128, M % 64 == 0): the B200-native replacement of the split-operand
+// library GEMMs (gemm_tc.cu tc_gram / tc_apply) for the cfg4 shape.
+//
+//   zmax_kernel   per realization max |Re|, |Im| of H -> exact power-of-two
+//                 scale sz (max |sz H| in [2^10, 2^11)) for the fp16 split;
+//   gram_kernel   U = Zh^T (Zh + 2 Zl) over all M antennas, Z = sz [Re H, Im H]
+//                 interleaved (M x 2K real), written fp32 row-major as U / sz^2;
+//                 gram_extract_kernel then forms A = (U + U^T)/2 + xi I
+//                 (gram_regularized, precoder.py:53-61) exactly as after the
+//                 library GEMMs;
+//   w_kernel      W^T = beta Xe^T Z^T per realization and output half
+//                 (rzf_iterative F = H X, precoder.py:90, with _power_scale's
+//                 beta folded in, precoder.py:64-70), F = W / beta optional.
+//
+// Both streaming kernels are warp-specialised like the fused K <= 64 kernel
+// (fused_tc.cu): one producer thread issues 1-D bulk copies (TMA) of 64-antenna
+// raw fp32 chunks (64 KiB) into a 3-stage ring, 8 converter warps split each
+// chunk in place into fp16 hi / lo core-matrix tiles (x = hi + lo, ~22
+// mantissa bits), one thread issues tcgen05.mma with fp32 accumulation in
+// TMEM.  Stage layout: an 8-antenna group g holds its raw rows at 8 KiB g and,
+// after conversion, its hi tile at 8 KiB g and lo at 8 KiB g + 4 KiB (core
+// matrix = 8 antennas x 8 components, 128 B): MN-major operands for the Gram
+// (K = antennas), K-major B operand for W^T (K = components).
+#include <cuda_fp16.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "xl_common.cuh"
+
+namespace xl {
+namespace stc {
+
+#include "tc_ptx.cuh"
+
+constexpr int KU = 128, NC = 2 * KU;      // users, real components
+constexpr int CH = 64;                    // antennas per ring stage
+constexpr int SB = CH * NC * 4;           // stage bytes (64 KiB)
+constexpr int NS = 3;                     // ring depth
+constexpr int CMA = NC * 16;              // one fp16 tile of an 8-antenna group (4 KiB)
+constexpr int GS = 2 * CMA;               // group stride (raw 8 KiB == hi + lo)
+constexpr int NCONV = 8;                  // converter warps (one 8-antenna group each)
+constexpr int W_PROD = 0, W_MMA = 1, W_CONV0 = 2;
+constexpr int NT = 32 * (W_CONV0 + NCONV);  // 320 threads
+constexpr int NIT = NC / 16;              // float4 per lane per group
+constexpr int SMALL = 2048;
+constexpr int SMEM = NS * SB + SMALL;
+static_assert(SMEM <= 227 * 1024, "stream smem");
+constexpr int BAR_CONV = 1;
+
+struct Small {
+  uint64_t raw_full[NS], conv_full[NS], stage_free[NS];
+  uint64_t acc_full[2], acc_free[2];
+  uint64_t done, cp_done;
+  uint32_t tmem_slot;
+  float rmax[2][128];  // W: per-row partial maxima of the two k halves
+};
+static_assert(sizeof(Small) <= SMALL, "small region");
+
+// ------------------------------------------------------------- helpers ----
+// Converter lane -> (antenna row in group, component column) of iteration it:
+// float4 reads and 8-B core-matrix writes bank-conflict free (fused_tc.cu).
+__device__ __forceinline__ void coords(int lane, int it, int& row, int& cc) {
+  const int cs = it >> 1, ih = it & 1;
+  row = (lane >> 1) & 7;
+  const int hb16 = lane & 1, j = (row + 2 * (lane >> 4) + ih) & 3;
+  cc = 32 * cs + 8 * j + 4 * hb16;
+}
+
+// Split the raw fp32 group at gb in place into hi / (lmul * lo) fp16 tiles.
+__device__ __forceinline__ void convert_group(uint8_t* gb, int lane, float sz, float lmul) {
+  float4 v[NIT];
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    int row, cc;
+    coords(lane, it, row, cc);
+    v[it] = *reinterpret_cast<const float4*>(gb + (row * NC + cc) * 4);
+  }
+  __syncwarp();  // the whole group is in registers before it is overwritten
+  const float2 s2 = make_float2(sz, sz), l2 = make_float2(lmul, lmul);
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    int row, cc;
+    coords(lane, it, row, cc);
+    const float2 a = __fmul2_rn(make_float2(v[it].x, v[it].y), s2);
+    const float2 bq = __fmul2_rn(make_float2(v[it].z, v[it].w), s2);
+    const __half2 ha = __float22half2_rn(a), hb = __float22half2_rn(bq);
+    const float2 ra = __fadd2_rn(a, make_float2(-__low2float(ha), -__high2float(ha)));
+    const float2 rb = __fadd2_rn(bq, make_float2(-__low2float(hb), -__high2float(hb)));
+    const __half2 la = __float22half2_rn(__fmul2_rn(ra, l2)), lb = __float22half2_rn(__fmul2_rn(rb, l2));
+    const int off = (cc >> 3) * 128 + row * 16 + (cc & 7) * 2;
+    *reinterpret_cast<uint2*>(gb + off) = make_uint2(h2u(ha), h2u(hb));
+    *reinterpret_cast<uint2*>(gb + CMA + off) = make_uint2(h2u(la), h2u(lb));
+  }
+}
+
+// Producer (one thread): chunk c of realization b into stage c % NS.
+__device__ __forceinline__ void produce(const float2* H, int64_t b, int M, uint8_t* ring, Small* sm) {
+  const uint64_t pol = policy_evict_first();
+  const int nch = M / CH;
+  const char* src = reinterpret_cast<const char*>(H + b * (int64_t)M * KU);
+  for (int c = 0; c < nch; ++c) {
+    const int s = c % NS;
+    if (c >= NS) mbar_wait(&sm->stage_free[s], ((c / NS) - 1) & 1);
+    mbar_expect_tx(&sm->raw_full[s], SB);
+    bulk_g2s(ring + s * SB, src + (int64_t)c * SB, SB, &sm->raw_full[s], pol);
+  }
+}
+
+__device__ __forceinline__ void init_ring(Small* sm) {
+  for (int s = 0; s < NS; ++s) {
+    mbar_init(&sm->raw_full[s], 1);
+    mbar_init(&sm->conv_full[s], NCONV);
+    mbar_init(&sm->stage_free[s], 1);
+  }
+  for (int j = 0; j < 2; ++j) {
+    mbar_init(&sm->acc_full[j], 1);
+    mbar_init(&sm->acc_free[j], 32 * NCONV);
+  }
+  mbar_init(&sm->done, 1);
+  mbar_init(&sm->cp_done, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// ----------------------------------------------------------- zmax ---------
+// grid (B), 512 threads: sz[b] = 2^e with max |sz H_b| in [2^10, 2^11)
+__global__ void __launch_bounds__(512) zmax_kernel(const float4* __restrict__ H, int64_t per4, float* __restrict__ sz) {
+  const int64_t b = blockIdx.x;
+  const float4* h = H + b * per4;
+  float m = 0.0f;
+  for (int64_t i = threadIdx.x; i < per4; i += 4 * 512) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = (i + u * 512 < per4) ? __ldcs(h + i + u * 512) : make_float4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+  }
+  __shared__ float red[16];
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = red[0];
+    for (int w = 1; w < 16; ++w) t = fmaxf(t, red[w]);
+    sz[b] = pow2_scale(t, 11);
+  }
+}
+
+// ----------------------------------------------------------- Gram ---------
+// One CTA per realization.  TMEM: U rows [0, 128) at columns [0, 256), rows
+// [128, 256) at [256, 512); per K-step (16 antennas) 4 MMAs of 128 x 256 x 16.
+constexpr uint32_t ID_GRAM = idesc(128, NC, 1, 1);
+
+__global__ void __launch_bounds__(NT, 1) gram_kernel(const float2* __restrict__ H, int M, const float* __restrict__ szv,
+                                                     float* __restrict__ U) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* ring = smem;
+  Small* sm = reinterpret_cast<Small*>(smem + NS * SB);
+  const int64_t b = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nch = M / CH;
+  if (tid == 0) init_ring(sm);
+  if (warp == W_MMA) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm->tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = sm->tmem_slot;
+  const float sz = szv[b];
+  if (warp == W_PROD) {
+    if (lane == 0) produce(H, b, M, ring, sm);
+  } else if (warp == W_MMA) {
+    if (lane == 0) {
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % NS;
+        mbar_wait(&sm->conv_full[s], (c / NS) & 1);
+        tc_after();
+        const uint32_t zh = su32(ring + s * SB), zl = zh + CMA;
+#pragma unroll
+        for (int ks = 0; ks < CH / 16; ++ks) {
+          const uint32_t o = 4 * ks * CMA;  // two groups per K-step
+          const uint64_t bh = sdesc(zh + o, GS, 128), bl = sdesc(zl + o, GS, 128);
+          const uint64_t a0 = bh, a1 = sdesc(zh + o + 16 * 128, GS, 128);
+          mma(tmem, a0, bh, ID_GRAM, (c | ks) != 0);
+          mma(tmem, a0, bl, ID_GRAM, 1);  // the lo tile holds 2 Zl
+          mma(tmem + 256, a1, bh, ID_GRAM, (c | ks) != 0);
+          mma(tmem + 256, a1, bl, ID_GRAM, 1);
+        }
+        commit(&sm->stage_free[s]);
+      }
+      commit(&sm->done);
+    }
+  } else {
+    const int cw = warp - W_CONV0;
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % NS;
+      mbar_wait(&sm->raw_full[s], (c / NS) & 1);
+      convert_group(ring + s * SB + cw * GS, lane, sz, 2.0f);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm->conv_full[s]);
+    }
+    // epilogue: warp (quadrant q, half hf) writes U rows hf 128 + 32 q + lane
+    mbar_wait(&sm->done, 0);
+    tc_after();
+    const int q = warp & 3, hf = cw >> 2;
+    const float isz = 1.0f / sz;  // two exact multiplies: sz^2 may overflow
+    const int row = hf * 128 + 32 * q + lane;
+    float4* urow = reinterpret_cast<float4*>(U + (b * NC + row) * (int64_t)NC);
+    const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 256 * hf;
+#pragma unroll 1
+    for (int c0 = 0; c0 < NC; c0 += 32) {
+      float v[32];
+      tmem_ld16(ta + c0, v);
+      tmem_ld16(ta + c0 + 16, v + 16);
+      tmem_wait_ld();
+#pragma unroll
+      for (int e = 0; e < 32; e += 4) urow[(c0 + e) / 4] = make_float4(v[e] * isz * isz, v[e + 1] * isz * isz, v[e + 2] * isz * isz, v[e + 3] * isz * isz);
+    }
+  }
+  tc_before();
+  __syncthreads();
+  if (warp == W_MMA) {
+    tc_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// -------------------------------------------------------------- W ---------
+// CTA (b, half): output components m in [128 half, 128 half + 128).
+// A operand Xe^T rows (row 2j: (Re X_ij, -Im X_ij) at k = (2i, 2i+1); row
+// 2j+1: (Im X_ij, Re X_ij)), scaled per row by 2^e (max < 2^14), split and
+// copied into TMEM (hi [0, 128), lo [128, 256)); accumulators (64 antennas)
+// double-buffered at [256, 320) and [320, 384).
+constexpr uint32_t T_AH = 0, T_AL = 128, T_ACC = 256;
+constexpr uint32_t ID_W = idesc(128, CH, 0, 0);
+constexpr int SBOA = NC * 16;  // K-major staging: 8-row group stride
+
+__global__ void __launch_bounds__(NT, 1) w_kernel(const float2* __restrict__ H, int M, const float* __restrict__ szv,
+                                                  const float2* __restrict__ X, const double* __restrict__ beta,
+                                                  float* __restrict__ W, float* __restrict__ F) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* ring = smem;
+  Small* sm = reinterpret_cast<Small*>(smem + NS * SB);
+  const int64_t b = (int64_t)blockIdx.x >> 1;
+  const int half = blockIdx.x & 1;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nch = M / CH;
+  if (tid == 0) init_ring(sm);
+  if (warp == W_MMA) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm->tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = sm->tmem_slot;
+  const float sz = szv[b];
+  const int q = warp & 3, cw = warp - W_CONV0, kh = cw >> 2;
+  const int r = 32 * q + lane;            // local output component (TMEM lane)
+  const int m = 128 * half + r;           // global output component
+  const int j = m >> 1;                   // user column of X
+  const bool odd = m & 1;
+  float srow = 1.0f;
+  // ---- build the split, row-scaled Xe^T half in the ring (converter warps)
+  if (warp >= W_CONV0) {
+    const float2* xc = X + b * (int64_t)KU * KU + j;  // X[i][j], i = 64 kh .. 64 kh + 63
+    float mx = 0.0f;
+#pragma unroll 4
+    for (int i = 64 * kh; i < 64 * kh + 64; ++i) {
+      const float2 v = xc[(int64_t)i * KU];
+      mx = fmaxf(mx, fmaxf(fabsf(v.x), fabsf(v.y)));
+    }
+    sm->rmax[kh][r] = mx;
+    named_sync(BAR_CONV, 32 * NCONV);
+    srow = pow2_scale(fmaxf(sm->rmax[0][r], sm->rmax[1][r]), 14);
+#pragma unroll 2
+    for (int i0 = 64 * kh; i0 < 64 * kh + 64; i0 += 4) {  // 4 users = 8 components = one core-matrix row
+      uint32_t hw[4], lw[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 v = xc[(int64_t)(i0 + u) * KU];
+        split2((odd ? v.y : v.x) * srow, (odd ? v.x : -v.y) * srow, hw[u], lw[u]);
+      }
+      const int k = 2 * i0;
+      const int o = (r >> 3) * SBOA + (k >> 3) * 128 + (r & 7) * 16;
+      *reinterpret_cast<uint4*>(ring + o) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      *reinterpret_cast<uint4*>(ring + 16 * SBOA + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+    fence_async_smem();
+  }
+  __syncthreads();
+  if (tid == 32 * W_MMA) {
+    tc_after();
+    const uint32_t ua = su32(ring);
+#pragma unroll
+    for (int s = 0; s < NC / 16; ++s) {
+      tmem_cp(tmem + T_AH + 8 * s, sdesc(ua + 2 * s * 128, 128, SBOA));
+      tmem_cp(tmem + T_AL + 8 * s, sdesc(ua + 16 * SBOA + 2 * s * 128, 128, SBOA));
+    }
+    commit(&sm->cp_done);
+  }
+  if (warp == W_PROD) {
+    if (lane == 0) {
+      mbar_wait(&sm->cp_done, 0);  // the staging tile (ring) has been copied
+      produce(H, b, M, ring, sm);
+    }
+  } else if (warp == W_MMA) {
+    if (lane == 0) {
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % NS, jb = c & 1;
+        if (c >= 2) mbar_wait(&sm->acc_free[jb], ((c >> 1) - 1) & 1);
+        mbar_wait(&sm->conv_full[s], (c / NS) & 1);
+        tc_after();
+        const uint32_t zh = su32(ring + s * SB), zl = zh + CMA;
+        const uint32_t d = tmem + T_ACC + CH * jb;
+#pragma unroll
+        for (int ks = 0; ks < NC / 16; ++ks) {
+          const uint64_t dzh = sdesc(zh + 256 * ks, 128, GS), dzl = sdesc(zl + 256 * ks, 128, GS);
+          mma_ts(d, tmem + T_AH + 8 * ks, dzh, ID_W, ks != 0);
+          mma_ts(d, tmem + T_AH + 8 * ks, dzl, ID_W, 1);
+          mma_ts(d, tmem + T_AL + 8 * ks, dzh, ID_W, 1);
+        }
+        commit(&sm->stage_free[s]);
+        commit(&sm->acc_full[jb]);
+      }
+    }
+  } else {
+    // converters: split chunk c, then drain the accumulator of chunk c - 1
+    // (warps of antenna half kh: antennas 32 kh .. 32 kh + 31 of the chunk)
+    const double bt = beta[b];
+    const float wmul = (float)(bt / ((double)srow * (double)sz));
+    const float fmul = 1.0f / (srow * sz);
+    const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16) + T_ACC + 32 * kh;
+    auto drain = [&](int c) {
+      const int jb = c & 1;
+      mbar_wait(&sm->acc_full[jb], (c >> 1) & 1);
+      tc_after();
+      float v[32];
+      tmem_ld16(tq + CH * jb, v);
+      tmem_ld16(tq + CH * jb + 16, v + 16);
+      tmem_wait_ld();
+      tc_before();
+      mbar_arrive(&sm->acc_free[jb]);
+      const int64_t n0 = (int64_t)c * CH + 32 * kh;
+      float* wp = W + (b * (int64_t)M + n0) * NC + m;
+#pragma unroll
+      for (int n = 0; n < 32; ++n) __stcs(wp + (int64_t)n * NC, v[n] * wmul);
+      if (F) {
+        float* fp = F + (b * (int64_t)M + n0) * NC + m;
+#pragma unroll
+        for (int n = 0; n < 32; ++n) __stcs(fp + (int64_t)n * NC, v[n] * fmul);
+      }
+    };
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % NS;
+      mbar_wait(&sm->raw_full[s], (c / NS) & 1);
+      convert_group(ring + s * SB + cw * GS, lane, sz, 1.0f);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm->conv_full[s]);
+      if (c >= 1) drain(c - 1);
+    }
+    drain(nch - 1);
+  }
+  tc_before();
+  __syncthreads();
+  if (warp == W_MMA) {
+    tc_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+}  // namespace stc
+
+bool stc_supported(int dtype, int M, int K) {
+  if (dtype != XL_C64 || K != stc::KU || M < stc::CH || M % stc::CH != 0) return false;
+  const char* e = getenv("XL_LARGE_K_GEMM");  // "library": the split-operand library GEMMs (A/B, tests)
+  return !(e && e[0] == 'l');
+}
+
+// sz[b] for B realizations, then U (B x 2K x 2K fp32) for the Gram
+int stc_gram(const void* H, int64_t B, int M, int K, float* sz, float* U, cudaStream_t st) {
+  if (!stc_supported(XL_C64, M, K)) { set_error("stream Gram: unsupported shape"); return XL_ERR_UNSUPPORTED; }
+  stc::zmax_kernel<<<(unsigned)B, 512, 0, st>>>((const float4*)H, (int64_t)M * K / 2, sz);
+  if (int e = check_launch("stream zmax")) return e;
+  cudaFuncSetAttribute(stc::gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, stc::SMEM);
+  stc::gram_kernel<<<(unsigned)B, stc::NT, stc::SMEM, st>>>((const float2*)H, M, sz, U);
+  return check_launch("stream gram");
+}
+
+// W = beta H X (and F = H X when F is non-null) with the scales from stc_gram
+int stc_apply(const void* H, const void* X, const double* beta, const float* sz, int64_t B, int M, int K, void* W,
+              void* F, cudaStream_t st) {
+  if (!stc_supported(XL_C64, M, K)) { set_error("stream W: unsupported shape"); return XL_ERR_UNSUPPORTED; }
+  cudaFuncSetAttribute(stc::w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, stc::SMEM);
+  stc::w_kernel<<<(unsigned)(2 * B), stc::NT, stc::SMEM, st>>>((const float2*)H, M, sz, (const float2*)X, beta,
+                                                               (float*)W, (float*)F);
+  return check_launch("stream W");
+}
+
+}  // namespace xl

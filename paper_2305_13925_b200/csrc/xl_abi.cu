@@ -153,10 +153,24 @@ static int64_t tc_chunk_size(int dtype, int64_t B, int M, int K) {
   return c < B ? c : B;
 }
 
+// K = 128 complex64 with M % 64 == 0: the streaming Gram / W kernels
+// (stream_tc.cu) need the fp32 real Gram U of a sub-batch (after the cuBLAS
+// workspace the split-GEMM solver may still use) and one scale per realization.
+constexpr int64_t STC_SUB = 4096;
+static size_t stc_ws(int64_t B, int K) {
+  const int64_t nb = B < STC_SUB ? B : STC_SUB;
+  return tc_cublas_ws_bytes() + align_up((size_t)nb * 4 * K * K * 4);
+}
+// bytes of the tensor-core region that precedes the PCG buffers
+static size_t tc_region(int dtype, int64_t B, int M, int K) {
+  return stc_supported(dtype, M, K) ? stc_ws(B, K) : tc_gram_ws_bytes(dtype, tc_chunk_size(dtype, B, M, K), M, K);
+}
+
 static size_t general_ws(int dtype, int64_t B, int M, int K) {
   size_t w = simt_rzf_ws(dtype, B, M, K);
   if (tc_general_supported(dtype, M, K)) {
-    w += align_up(tc_gram_ws_bytes(dtype, tc_chunk_size(dtype, B, M, K), M, K));
+    if (stc_supported(dtype, M, K)) w += align_up((size_t)B * 4);  // sz[B]
+    w += align_up(tc_region(dtype, B, M, K));
     if (dtype == XL_C64 && tc_pcg_supported(K)) w += align_up(tc_pcg_ws_bytes(B, K));
     if (dtype == XL_C128 && tc_pcg64_supported(K)) w += align_up(tc_pcg64_ws_bytes(B, K));
   }
@@ -193,14 +207,25 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   const int ptiles = gemm_tiles(M, K) > gemm_tiles(K, K) ? gemm_tiles(M, K) : gemm_tiles(K, K);
   double* part = (double*)p; p += align_up((size_t)B * ptiles * sizeof(double));
   int32_t* iters = (int32_t*)p; p += align_up((size_t)B * 4);
+  const bool sc = tc && stc_supported(dtype, M, K);
+  float* szb = nullptr;
+  if (sc) { szb = (float*)p; p += align_up((size_t)B * 4); }
   void* tcws = p;  // gemm_tc.cu: cuBLAS workspace + split operands (+ the tensor-core PCG state)
-  void* pcgws = tc ? (void*)(p + align_up(tc_gram_ws_bytes(dtype, tc_chunk_size(dtype, B, M, K), M, K))) : nullptr;
+  void* pcgws = tc ? (void*)(p + align_up(tc_region(dtype, B, M, K))) : nullptr;
   void* Xo = X ? X : Xw;
   const xl_stream_t stream = (xl_stream_t)st;
   int e;
   const int64_t Bc = tc ? tc_chunk_size(dtype, B, M, K) : B;
   const int64_t oH = (int64_t)M * K * (int64_t)cs, oK = (int64_t)K * K * (int64_t)cs;
-  if (tc) {
+  if (sc) {  // streaming tcgen05 Gram per sub-batch, U after the cuBLAS workspace
+    float* U = (float*)((char*)tcws + tc_cublas_ws_bytes());
+    for (int64_t b0 = 0; b0 < B; b0 += STC_SUB) {
+      const int64_t nb = B - b0 < STC_SUB ? B - b0 : STC_SUB;
+      if ((e = stc_gram((const char*)H + b0 * oH, nb, M, K, szb + b0, U, st))) return e;
+      if ((e = tc_gram_extract(U, nb, K, xi_per_batch ? xi_per_batch + b0 : nullptr, xi, (char*)A + b0 * oK, st)))
+        return e;
+    }
+  } else if (tc) {
     for (int64_t b0 = 0; b0 < B; b0 += Bc) {
       const int64_t nb = B - b0 < Bc ? B - b0 : Bc;
       if ((e = tc_gram(dtype, (const char*)H + b0 * oH, nb, M, K, xi_per_batch ? xi_per_batch + b0 : nullptr, xi,
@@ -213,6 +238,7 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   // W = beta H X on the tensor cores, per sub-batch (the split rows are rebuilt:
   // the Gram sub-batches have overwritten them)
   auto tc_w = [&]() -> int {
+    if (sc) return stc_apply(H, Xo, beta, szb, B, M, K, W, F, st);
     for (int64_t b0 = 0; b0 < B; b0 += Bc) {
       const int64_t nb = B - b0 < Bc ? B - b0 : Bc;
       if (int r = tc_apply(dtype, (const char*)H + b0 * oH, (const char*)Xo + b0 * oK, beta + b0, nb, M, K,

@@ -101,3 +101,49 @@ def test_cluster_pcg_deterministic_and_many_clusters():
     for b in (0, 149, 299):
         Gr, br, gr, s = O.precoder_and_se(Hq[b], wl.alpha(), wl.power(), 1.0, "jacpcg", 5, "textbook")
         assert relf(o1.W[b].cpu().numpy(), Gr) <= 1e-4, b
+
+
+def _run_env(env, fn):
+    old = {k: os.environ.get(k) for k in env}
+    try:
+        for k, v in env.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+        out = fn()
+        torch.cuda.synchronize()
+        return out
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("method", ["jacpcg", "direct"])
+def test_streaming_gram_w_match_library_gemms(method):
+    """stream_tc.cu (tcgen05 Gram / W with the in-smem 3xFP16 split) against the
+    split-operand library GEMMs it replaces (XL_LARGE_K_GEMM=library) and the
+    complex128 oracle; F = W / beta and a wide per-user gain spread (the
+    per-realization scale and the per-row X scales)."""
+    rng = np.random.default_rng(21)
+    B, M, K = 6, 640, 128
+    Hn = (rng.standard_normal((B, M, K)) + 1j * rng.standard_normal((B, M, K))) / np.sqrt(2)
+    Hn *= 10.0 ** rng.uniform(-2, 1, size=(B, 1, K))  # 60 dB of user gain spread
+    Hn[1] *= 1e-6                                      # a tiny realization (scale 2^e far from 1)
+    H = torch.from_numpy(Hn.astype(np.complex64)).to(DEV)
+    xi = torch.from_numpy(rng.uniform(0.05, 2.0, size=B) * np.abs(Hn).mean(axis=(1, 2)) ** 2 * M).to(DEV)
+    f = lambda: BT.rzf_batched(H, xi, 10.0, method=method, T=6, want_F=True, want_X=True)
+    s = _run_env({"XL_LARGE_K_GEMM": None}, f)
+    lib = _run_env({"XL_LARGE_K_GEMM": "library"}, f)
+    Hq = H.cpu().numpy().astype(np.complex128)
+    for b in range(B):
+        Gr, br, gr, se = O.precoder_and_se(Hq[b], float(xi[b]), 10.0, 1.0, method, 6, "textbook")
+        Ws, Wl = s.W[b].cpu().numpy(), lib.W[b].cpu().numpy()
+        assert relf(Ws, Gr) <= 1e-4, (b, relf(Ws, Gr))
+        assert relf(Ws, Wl) <= 2e-5, (b, relf(Ws, Wl))
+        assert relf(s.F[b].cpu().numpy(), Gr / br) <= 1e-4
+        assert abs(s.beta[b].item() - br) <= 1e-4 * br
+        assert abs(s.sum_se[b].item() - se) <= 1e-4 * abs(se)
