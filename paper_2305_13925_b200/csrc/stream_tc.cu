@@ -2,9 +2,10 @@
 // K = 128, M % 64 == 0): the B200-native replacement of the split-operand
 // library GEMMs (gemm_tc.cu tc_gram / tc_apply) for the cfg4 shape.
 //
-//   zmax_kernel   per realization max |Re|, |Im| of H -> exact power-of-two
-//                 scale sz (max |sz H| in [2^10, 2^11)) for the fp16 split;
 //   gram_kernel   U = Zh^T (Zh + 2 Zl) over all M antennas, Z = sz [Re H, Im H]
+//                 (sz: power of two from the first non-zero chunk; realizations
+//                 whose later chunks would overflow fp16 are flagged and redone
+//                 with the exact max from zmax_kernel)
 //                 interleaved (M x 2K real), written fp32 row-major as U / sz^2;
 //                 gram_extract_kernel then forms A = (U + U^T)/2 + xi I
 //                 (gram_regularized, precoder.py:53-61) exactly as after the
@@ -53,7 +54,7 @@ struct Small {
   uint64_t acc_full[2], acc_free[2];
   uint64_t done, cp_done;
   uint32_t tmem_slot;
-  float rmax[2][128];  // W: per-row partial maxima of the two k halves
+  float rmax[2][128];  // W: per-row partial maxima of the two k halves; Gram: converter maxima
 };
 static_assert(sizeof(Small) <= SMALL, "small region");
 
@@ -67,15 +68,24 @@ __device__ __forceinline__ void coords(int lane, int it, int& row, int& cc) {
   cc = 32 * cs + 8 * j + 4 * hb16;
 }
 
-// Split the raw fp32 group at gb in place into hi / (lmul * lo) fp16 tiles.
-__device__ __forceinline__ void convert_group(uint8_t* gb, int lane, float sz, float lmul) {
-  float4 v[NIT];
+// Raw fp32 group at gb -> registers (lane's share)
+__device__ __forceinline__ void load_group(const uint8_t* gb, int lane, float4 (&v)[NIT]) {
 #pragma unroll
   for (int it = 0; it < NIT; ++it) {
     int row, cc;
     coords(lane, it, row, cc);
     v[it] = *reinterpret_cast<const float4*>(gb + (row * NC + cc) * 4);
   }
+}
+__device__ __forceinline__ float group_max(const float4 (&v)[NIT]) {
+  float mx = 0.0f;
+#pragma unroll
+  for (int it = 0; it < NIT; ++it)
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[it].x), fabsf(v[it].y)), fmaxf(fabsf(v[it].z), fabsf(v[it].w))));
+  return warp_max(mx);
+}
+// Split the group (loaded by load_group) in place into hi / (lmul * lo) fp16 tiles.
+__device__ __forceinline__ void store_group(uint8_t* gb, int lane, const float4 (&v)[NIT], float sz, float lmul) {
   __syncwarp();  // the whole group is in registers before it is overwritten
   const float2 s2 = make_float2(sz, sz), l2 = make_float2(lmul, lmul);
 #pragma unroll
@@ -123,9 +133,12 @@ __device__ __forceinline__ void init_ring(Small* sm) {
 }
 
 // ----------------------------------------------------------- zmax ---------
-// grid (B), 512 threads: sz[b] = 2^e with max |sz H_b| in [2^10, 2^11)
-__global__ void __launch_bounds__(512) zmax_kernel(const float4* __restrict__ H, int64_t per4, float* __restrict__ sz) {
+// grid (B), 512 threads: sz[b] = 2^e with max |sz H_b| in [2^10, 2^11), for the
+// realizations flagged in only[b] (the Gram's first-chunk scale overflowed)
+__global__ void __launch_bounds__(512) zmax_kernel(const float4* __restrict__ H, int64_t per4, float* __restrict__ sz,
+                                                   const int* __restrict__ only) {
   const int64_t b = blockIdx.x;
+  if (only && only[b] == 0) return;
   const float4* h = H + b * per4;
   float m = 0.0f;
   for (int64_t i = threadIdx.x; i < per4; i += 4 * 512) {
@@ -151,12 +164,19 @@ __global__ void __launch_bounds__(512) zmax_kernel(const float4* __restrict__ H,
 // [128, 256) at [256, 512); per K-step (16 antennas) 4 MMAs of 128 x 256 x 16.
 constexpr uint32_t ID_GRAM = idesc(128, NC, 1, 1);
 
-__global__ void __launch_bounds__(NT, 1) gram_kernel(const float2* __restrict__ H, int M, const float* __restrict__ szv,
-                                                     float* __restrict__ U) {
+// Scale: fixup == 0: sz from the first non-zero chunk (max |sz Z| in [2^10,
+// 2^11), one more read of H saved); a later group with max |sz Z| >= 2^15
+// (fp16 overflow) flags rflag[b] and the fixup launch (fixup == 1, only the
+// flagged realizations, sz from zmax_kernel) recomputes U.
+constexpr float RANGE_MAX = 32768.0f;
+
+__global__ void __launch_bounds__(NT, 1) gram_kernel(const float2* __restrict__ H, int M, float* __restrict__ szv,
+                                                     float* __restrict__ U, int* __restrict__ rflag, int fixup) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
   Small* sm = reinterpret_cast<Small*>(smem + NS * SB);
   const int64_t b = blockIdx.x;
+  if (fixup && rflag[b] == 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nch = M / CH;
   if (tid == 0) init_ring(sm);
@@ -168,7 +188,7 @@ __global__ void __launch_bounds__(NT, 1) gram_kernel(const float2* __restrict__ 
   __syncthreads();
   tc_after();
   const uint32_t tmem = sm->tmem_slot;
-  const float sz = szv[b];
+  float sz = fixup ? szv[b] : 1.0f;
   if (warp == W_PROD) {
     if (lane == 0) produce(H, b, M, ring, sm);
   } else if (warp == W_MMA) {
@@ -194,13 +214,35 @@ __global__ void __launch_bounds__(NT, 1) gram_kernel(const float2* __restrict__ 
     }
   } else {
     const int cw = warp - W_CONV0;
+    bool have = fixup != 0, over = false;
     for (int c = 0; c < nch; ++c) {
       const int s = c % NS;
       mbar_wait(&sm->raw_full[s], (c / NS) & 1);
-      convert_group(ring + s * SB + cw * GS, lane, sz, 2.0f);
+      uint8_t* gb = ring + s * SB + cw * GS;
+      float4 v[NIT];
+      load_group(gb, lane, v);
+      const float gm = group_max(v);
+      if (!have) {  // until the first non-zero chunk: max over the converter warps
+        if (lane == 0) sm->rmax[0][cw] = gm;
+        named_sync(BAR_CONV, 32 * NCONV);
+        float mx = sm->rmax[0][0];
+#pragma unroll
+        for (int w = 1; w < NCONV; ++w) mx = fmaxf(mx, sm->rmax[0][w]);
+        named_sync(BAR_CONV, 32 * NCONV);
+        if (mx > 0.0f) {
+          sz = pow2_scale(mx, 11);
+          have = true;
+        }
+      }
+      over |= !(gm * sz < RANGE_MAX);  // also catches inf / NaN
+      store_group(gb, lane, v, sz, 2.0f);
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm->conv_full[s]);
+    }
+    if (!fixup) {
+      if (over && lane == 0) rflag[b] = 1;
+      if (tid == 32 * W_CONV0) szv[b] = sz;
     }
     // epilogue: warp (quadrant q, half hf) writes U rows hf 128 + 32 q + lane
     mbar_wait(&sm->done, 0);
@@ -357,7 +399,10 @@ __global__ void __launch_bounds__(NT, 1) w_kernel(const float2* __restrict__ H, 
     for (int c = 0; c < nch; ++c) {
       const int s = c % NS;
       mbar_wait(&sm->raw_full[s], (c / NS) & 1);
-      convert_group(ring + s * SB + cw * GS, lane, sz, 1.0f);
+      uint8_t* gb = ring + s * SB + cw * GS;
+      float4 v[NIT];
+      load_group(gb, lane, v);
+      store_group(gb, lane, v, sz, 1.0f);
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm->conv_full[s]);
@@ -381,14 +426,18 @@ bool stc_supported(int dtype, int M, int K) {
   return !(e && e[0] == 'l');
 }
 
-// sz[b] for B realizations, then U (B x 2K x 2K fp32) for the Gram
-int stc_gram(const void* H, int64_t B, int M, int K, float* sz, float* U, cudaStream_t st) {
+// U (B x 2K x 2K fp32) for the Gram and the split scales sz[b] (rflag: B ints
+// of scratch): first-chunk scales, then the fixup of the flagged realizations
+int stc_gram(const void* H, int64_t B, int M, int K, float* sz, float* U, int* rflag, cudaStream_t st) {
   if (!stc_supported(XL_C64, M, K)) { set_error("stream Gram: unsupported shape"); return XL_ERR_UNSUPPORTED; }
-  stc::zmax_kernel<<<(unsigned)B, 512, 0, st>>>((const float4*)H, (int64_t)M * K / 2, sz);
-  if (int e = check_launch("stream zmax")) return e;
+  if (cudaMemsetAsync(rflag, 0, (size_t)B * sizeof(int), st) != cudaSuccess) return check_launch("stream flags");
   cudaFuncSetAttribute(stc::gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, stc::SMEM);
-  stc::gram_kernel<<<(unsigned)B, stc::NT, stc::SMEM, st>>>((const float2*)H, M, sz, U);
-  return check_launch("stream gram");
+  stc::gram_kernel<<<(unsigned)B, stc::NT, stc::SMEM, st>>>((const float2*)H, M, sz, U, rflag, 0);
+  if (int e = check_launch("stream gram")) return e;
+  stc::zmax_kernel<<<(unsigned)B, 512, 0, st>>>((const float4*)H, (int64_t)M * K / 2, sz, rflag);
+  if (int e = check_launch("stream zmax")) return e;
+  stc::gram_kernel<<<(unsigned)B, stc::NT, stc::SMEM, st>>>((const float2*)H, M, sz, U, rflag, 1);
+  return check_launch("stream gram fixup");
 }
 
 // W = beta H X (and F = H X when F is non-null) with the scales from stc_gram

@@ -169,7 +169,7 @@ static size_t tc_region(int dtype, int64_t B, int M, int K) {
 static size_t general_ws(int dtype, int64_t B, int M, int K) {
   size_t w = simt_rzf_ws(dtype, B, M, K);
   if (tc_general_supported(dtype, M, K)) {
-    if (stc_supported(dtype, M, K)) w += align_up((size_t)B * 4);  // sz[B]
+    if (stc_supported(dtype, M, K)) w += 2 * align_up((size_t)B * 4);  // sz[B], range flags[B]
     w += align_up(tc_region(dtype, B, M, K));
     if (dtype == XL_C64 && tc_pcg_supported(K)) w += align_up(tc_pcg_ws_bytes(B, K));
     if (dtype == XL_C128 && tc_pcg64_supported(K)) w += align_up(tc_pcg64_ws_bytes(B, K));
@@ -209,7 +209,11 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   int32_t* iters = (int32_t*)p; p += align_up((size_t)B * 4);
   const bool sc = tc && stc_supported(dtype, M, K);
   float* szb = nullptr;
-  if (sc) { szb = (float*)p; p += align_up((size_t)B * 4); }
+  int* rflag = nullptr;
+  if (sc) {
+    szb = (float*)p; p += align_up((size_t)B * 4);
+    rflag = (int*)p; p += align_up((size_t)B * 4);
+  }
   void* tcws = p;  // gemm_tc.cu: cuBLAS workspace + split operands (+ the tensor-core PCG state)
   void* pcgws = tc ? (void*)(p + align_up(tc_region(dtype, B, M, K))) : nullptr;
   void* Xo = X ? X : Xw;
@@ -221,7 +225,7 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
     float* U = (float*)((char*)tcws + tc_cublas_ws_bytes());
     for (int64_t b0 = 0; b0 < B; b0 += STC_SUB) {
       const int64_t nb = B - b0 < STC_SUB ? B - b0 : STC_SUB;
-      if ((e = stc_gram((const char*)H + b0 * oH, nb, M, K, szb + b0, U, st))) return e;
+      if ((e = stc_gram((const char*)H + b0 * oH, nb, M, K, szb + b0, U, rflag + b0, st))) return e;
       if ((e = tc_gram_extract(U, nb, K, xi_per_batch ? xi_per_batch + b0 : nullptr, xi, (char*)A + b0 * oK, st)))
         return e;
     }

@@ -126,13 +126,16 @@ def _run_env(env, fn):
 def test_streaming_gram_w_match_library_gemms(method):
     """stream_tc.cu (tcgen05 Gram / W with the in-smem 3xFP16 split) against the
     split-operand library GEMMs it replaces (XL_LARGE_K_GEMM=library) and the
-    complex128 oracle; F = W / beta and a wide per-user gain spread (the
-    per-realization scale and the per-row X scales)."""
+    complex128 oracle; F = W / beta, a wide per-user gain spread (the per-row X
+    scales), a realization whose later antennas overflow the first chunk's
+    fp16 scale (flag + fixup launch) and one with leading zero chunks."""
     rng = np.random.default_rng(21)
     B, M, K = 6, 640, 128
     Hn = (rng.standard_normal((B, M, K)) + 1j * rng.standard_normal((B, M, K))) / np.sqrt(2)
     Hn *= 10.0 ** rng.uniform(-2, 1, size=(B, 1, K))  # 60 dB of user gain spread
     Hn[1] *= 1e-6                                      # a tiny realization (scale 2^e far from 1)
+    Hn[2, 256:] *= 300.0                               # later chunks overflow the first chunk's scale: fixup
+    Hn[3, :128] = 0.0                                  # leading zero chunks: scale from the first non-zero one
     H = torch.from_numpy(Hn.astype(np.complex64)).to(DEV)
     xi = torch.from_numpy(rng.uniform(0.05, 2.0, size=B) * np.abs(Hn).mean(axis=(1, 2)) ** 2 * M).to(DEV)
     f = lambda: BT.rzf_batched(H, xi, 10.0, method=method, T=6, want_F=True, want_X=True)
