@@ -17,16 +17,18 @@
 //   - the column maxima of P are combined across the pair through DSMEM
 //     (per-column power-of-two scale for the fp16 split, as in the fused
 //     kernel: converged columns keep their relative precision);
-//   - each CTA writes its 128 rows of the scaled, split P into the B operand
-//     tile of BOTH CTAs (st.shared::cluster), so each holds all 2K rows;
+//   - each CTA writes its 128 rows of the scaled, split P into its B operand
+//     tile and bulk-copies them (cp.async.bulk shared::cta -> shared::cluster,
+//     mbarrier completion) into the peer's, so each holds all 2K rows;
 //   - Q_c = A''_c P on the tensor cores (48 tcgen05.mma, M = 128, N = K, from
 //     TMEM x smem), one elected thread per CTA;
 //   - per-column curvature and rz partials are summed over the CTA's rows in
-//     a fixed order, exchanged through DSMEM and added rank 0 + rank 1 in
-//     both CTAs: the scalars are bit-identical in the pair and deterministic.
-// Exchange slots are double-buffered by round parity: a round's writes into
-// the peer are issued only after the previous round's cluster barrier, which
-// the peer passes only after reading the slot of the round before.
+//     a fixed order, exchanged through DSMEM (st.async completing on the
+//     peer's mbarrier) and added rank 0 + rank 1 in both CTAs: the scalars
+//     are bit-identical in the pair and deterministic.
+// No cluster-wide barrier inside the solve: every exchange completes on an
+// mbarrier of the receiver, and the causal chain of the exchanges orders each
+// buffer's reuse (see pair_round / product).
 //
 // Scaling: A'' = sa A with sa = 2^e (diag(A'') < 2^14); iterates are those of
 // the unscaled recurrence up to rounding (X = sa X'').
@@ -60,10 +62,12 @@ constexpr uint32_t ID_P = idesc(128, KU, 0, 1);  // A'' K-major (TMEM), P MN-maj
 
 struct Small {
   uint64_t q_full, cp_done;
+  uint64_t pbar;                  // the peer's rows of the B tile have landed (bulk copy)
+  uint64_t xbar[2];               // the peer's column partials have landed (per round parity)
   uint32_t tmem_slot;
   int zero_diag, not_hpd, pad;
   float red[4 * 4 * JH];          // per (quadrant, column block) column partials
-  float xch[2][2][KU];            // [round parity][source rank][column]
+  float xin[2][KU];               // the peer's column partials [round parity][column]
   alignas(16) float coef[2][KU];  // alpha, beta
   alignas(16) float spx[KU];      // per-column B scale 2^e ...
   alignas(16) float spy[KU];      // ... and 2^-e
@@ -97,19 +101,20 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
-__device__ __forceinline__ void st_cluster_f32(uint32_t a, float v) {
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+// 4 bytes into the peer's smem, completing tx bytes on the peer's mbarrier
+__device__ __forceinline__ void st_async_f32(uint32_t a, float v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(a),
+               "r"(__float_as_uint(v)), "r"(bar)
+               : "memory");
 }
-__device__ __forceinline__ void st_cluster_v4(uint32_t a, uint4 v) {
-  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+// bulk copy (async proxy) of local smem into the peer's, completing on the peer's mbarrier
+__device__ __forceinline__ void bulk_s2s(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "r"(src), "r"(bytes), "r"(bar)
                : "memory");
 }
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// generic-proxy smem writes (own and the peer's) -> visible to the tensor core
-__device__ __forceinline__ void fence_async_cluster() {
-  asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
 }
 
 // per-thread column values -> red[(q * 4 + h) * JH + j] (warp transpose-reduce)
@@ -132,28 +137,29 @@ __device__ __forceinline__ void lds8(const float* a, float (&o)[8]) {
   o[0] = x.x; o[1] = x.y; o[2] = x.z; o[3] = x.w; o[4] = y.x; o[5] = y.y; o[6] = y.z; o[7] = y.w;
 }
 
-// One cross-CTA round: thread j < K publishes the CTA partial of column j into
-// slot [par][rank] of both CTAs; after the cluster barrier both read the pair
-// total (rank 0 first: identical bits in both CTAs).
+// One cross-CTA round n (threads j < K; the caller synchronises the CTA after
+// it): the CTA partial of column j goes to the peer's slot xin[n & 1][j] by
+// st.async, completing on the peer's xbar[n & 1]; the pair total adds rank 0's
+// partial first, so both CTAs hold identical bits.  Slot reuse is safe without
+// a cluster barrier: a CTA sends round n + 2 only after receiving the peer's
+// round n + 1, which the peer sends after reading round n.
 template <bool MAX>
-__device__ __forceinline__ float pair_round(Small* sm, uint32_t rank, uint32_t peer_xch, int par, int j) {
-  float own = 0.0f;
-  if (j < KU) {
-    own = col_total<MAX>(sm->red, j);
-    sm->xch[par][rank][j] = own;
-    st_cluster_f32(peer_xch + 4u * (uint32_t)((par * 2 + (int)rank) * KU + j), own);
-  }
-  cluster_sync();
+__device__ __forceinline__ float pair_round(Small* sm, uint32_t rank, uint32_t peer_xin, uint32_t peer_xbar, uint32_t n,
+                                            int j) {
   if (j >= KU) return 0.0f;
-  const float a = sm->xch[par][0][j], b = sm->xch[par][1][j];
+  const int par = n & 1;
+  const float own = col_total<MAX>(sm->red, j);
+  if (j == 0) mbar_expect_tx(&sm->xbar[par], KU * 4);
+  st_async_f32(peer_xin + 4u * (uint32_t)(par * KU + j), own, peer_xbar + 8u * par);
+  mbar_wait(&sm->xbar[par], (n >> 1) & 1);
+  const float other = sm->xin[par][j];
+  const float a = rank == 0 ? own : other, b = rank == 0 ? other : own;
   return MAX ? fmaxf(a, b) : a + b;
 }
 
 // Write this thread's JH columns of component row rg (column j scaled by
-// spx[j]) as 16-B core-matrix rows of the split MN-major B tile, into the
-// local tile and the peer's.
-__device__ __forceinline__ void write_b(const float (&v)[JH], const float* spx, int rg, int h, uint8_t* bh,
-                                        uint32_t peer_bh) {
+// spx[j]) as 16-B core-matrix rows of the split MN-major B tile.
+__device__ __forceinline__ void write_b(const float (&v)[JH], const float* spx, int rg, int h, uint8_t* bh) {
 #pragma unroll
   for (int g = 0; g < JH / 8; ++g) {
     float sv[8];
@@ -165,8 +171,6 @@ __device__ __forceinline__ void write_b(const float (&v)[JH], const float* spx, 
     const uint4 H4 = make_uint4(hw[0], hw[1], hw[2], hw[3]), L4 = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     *reinterpret_cast<uint4*>(bh + o) = H4;
     *reinterpret_cast<uint4*>(bh + PART + o) = L4;
-    st_cluster_v4(peer_bh + (uint32_t)o, H4);
-    st_cluster_v4(peer_bh + (uint32_t)(PART + o), L4);
   }
 }
 
@@ -199,11 +203,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) cluster_pcg_k
   const bool use_c = p.method == XL_JACPCG;
   const bool textbook = use_c && p.variant == XL_TEXTBOOK;
   const uint32_t peer_pb = mapa(su32(pb), peer);
-  const uint32_t peer_xch = mapa(su32(&sm->xch[0][0][0]), peer);
+  const uint32_t peer_xin = mapa(su32(&sm->xin[0][0]), peer);
+  const uint32_t peer_xbar = mapa(su32(&sm->xbar[0]), peer);
+  const uint32_t peer_pbar = mapa(su32(&sm->pbar), peer);
 
   if (tid == 0) {
     mbar_init(&sm->q_full, 1);
     mbar_init(&sm->cp_done, 1);
+    mbar_init(&sm->pbar, 1);
+    mbar_init(&sm->xbar[0], 1);
+    mbar_init(&sm->xbar[1], 1);
     sm->not_hpd = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -296,8 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) cluster_pcg_k
   mbar_wait(&sm->cp_done, 0);  // the staging tile is free for P
   tc_after();
   cluster_sync();  // the peer has started and finished its own staging copy
-  int par = 0;
-  uint32_t nq = 0;
+  uint32_t nr = 0, nq = 0;  // cross-CTA rounds, tensor-core products
   const uint32_t upb = su32(pb);
 
   // column max of v over the pair -> spx / spy (power-of-two scale, < 2^14)
@@ -306,8 +314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) cluster_pcg_k
     for (int jj = 0; jj < JH; ++jj) A[jj] = fabsf(v[jj]);
     col_partials<true>(A, sm->red, q, h);
     __syncthreads();
-    const float m = pair_round<true>(sm, rank, peer_xch, par, tid);
-    par ^= 1;
+    const float m = pair_round<true>(sm, rank, peer_xin, peer_xbar, nr++, tid);
     if (tid < KU) {
       const float s = pow2_scale(m, 14);
       sm->spx[tid] = s;
@@ -315,13 +322,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) cluster_pcg_k
     }
     __syncthreads();
   };
-  // write v (scaled) into both B tiles, then Q = A'' v
+  // write v (scaled) into the local B tile, bulk-copy this CTA's 128 rows into
+  // the peer's tile (they are contiguous: 16 K-groups of LBOB bytes, hi and
+  // lo), then Q = A'' v once the peer's rows have landed.  The peer's previous
+  // product has finished reading its tile: it sent this iteration's scale
+  // partial only after that.
   auto product = [&](const float (&v)[JH]) {
-    write_b(v, sm->spx, rg, h, pb, peer_pb);
+    write_b(v, sm->spx, rg, h, pb);
     fence_async_smem();
-    fence_async_cluster();
-    cluster_sync();
-    if (tid == 0) issue_q(tmem, upb, &sm->q_full);
+    __syncthreads();
+    if (tid == 0) {
+      constexpr uint32_t HALF = (ROWS / 8) * LBOB;
+      const uint32_t off = rank * HALF;
+      mbar_expect_tx(&sm->pbar, 2 * HALF);
+      bulk_s2s(peer_pb + off, upb + off, HALF, peer_pbar);
+      bulk_s2s(peer_pb + PART + off, upb + PART + off, HALF, peer_pbar);
+      mbar_wait(&sm->pbar, nq & 1);
+      issue_q(tmem, upb, &sm->q_full);
+    }
     mbar_wait(&sm->q_full, nq & 1);
     ++nq;
     tc_after();
@@ -344,8 +362,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) cluster_pcg_k
     col_partials(A, sm->red, q, h);
     __syncthreads();
     {
-      const float curv = pair_round<false>(sm, rank, peer_xch, par, tid);
-      par ^= 1;
+      const float curv = pair_round<false>(sm, rank, peer_xin, peer_xbar, nr++, tid);
       if (tid < KU) {  // alpha_j, NotHpd (linsolve.py:277-280)
         const float rzj = sm->rzs[tid];
         const bool act = rzj > 0.0f;
@@ -378,8 +395,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) cluster_pcg_k
     tmem_wait_st();
     __syncthreads();
     {
-      const float rn = pair_round<false>(sm, rank, peer_xch, par, tid);
-      par ^= 1;
+      const float rn = pair_round<false>(sm, rank, peer_xin, peer_xbar, nr++, tid);
       if (tid < KU) {  // beta_j, rz update (linsolve.py:284-288)
         const float rzj = sm->rzs[tid];
         sm->coef[1][tid] = rzj > 0.0f ? rn / rzj : 0.0f;
