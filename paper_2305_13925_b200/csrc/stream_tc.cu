@@ -52,7 +52,7 @@ constexpr int BAR_CONV = 1;
 struct Small {
   uint64_t raw_full[NS], conv_full[NS], stage_free[NS];
   uint64_t acc_full[2], acc_free[2];
-  uint64_t done, cp_done;
+  uint64_t done, cp_done;  // done: Gram accumulator complete / W: X columns staged
   uint32_t tmem_slot;
   float rmax[2][128];  // W: per-row partial maxima of the two k halves; Gram: converter maxima
 };
@@ -306,24 +306,35 @@ __global__ void __launch_bounds__(NT, 1) w_kernel(const float2* __restrict__ H, 
   const int j = m >> 1;                   // user column of X
   const bool odd = m & 1;
   float srow = 1.0f;
-  // ---- build the split, row-scaled Xe^T half in the ring (converter warps)
+  // ---- stage this half's 64 columns of X (512 B of each row i) in the ring
+  // above the Xe^T tiles with bulk copies, then build the split, row-scaled
+  // Xe^T half from smem (converter warps)
+  float2* xs = reinterpret_cast<float2*>(ring + 32 * SBOA);  // xs[i * 64 + jl]
+  if (tid == 32 * W_PROD) {
+    constexpr uint32_t RB = 64 * sizeof(float2);
+    mbar_expect_tx(&sm->done, KU * RB);
+    const float2* xsrc = X + b * (int64_t)KU * KU + 64 * half;
+    const uint64_t pol = policy_evict_first();
+    for (int i = 0; i < KU; ++i) bulk_g2s(xs + i * 64, xsrc + (int64_t)i * KU, RB, &sm->done, pol);
+  }
   if (warp >= W_CONV0) {
-    const float2* xc = X + b * (int64_t)KU * KU + j;  // X[i][j], i = 64 kh .. 64 kh + 63
+    const int jl = r >> 1;  // j - 64 half
+    mbar_wait(&sm->done, 0);
     float mx = 0.0f;
-#pragma unroll 4
+#pragma unroll 8
     for (int i = 64 * kh; i < 64 * kh + 64; ++i) {
-      const float2 v = xc[(int64_t)i * KU];
+      const float2 v = xs[i * 64 + jl];
       mx = fmaxf(mx, fmaxf(fabsf(v.x), fabsf(v.y)));
     }
     sm->rmax[kh][r] = mx;
     named_sync(BAR_CONV, 32 * NCONV);
     srow = pow2_scale(fmaxf(sm->rmax[0][r], sm->rmax[1][r]), 14);
-#pragma unroll 2
+#pragma unroll 4
     for (int i0 = 64 * kh; i0 < 64 * kh + 64; i0 += 4) {  // 4 users = 8 components = one core-matrix row
       uint32_t hw[4], lw[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const float2 v = xc[(int64_t)(i0 + u) * KU];
+        const float2 v = xs[(i0 + u) * 64 + jl];
         split2((odd ? v.y : v.x) * srow, (odd ? v.x : -v.y) * srow, hw[u], lw[u]);
       }
       const int k = 2 * i0;
