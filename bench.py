@@ -231,33 +231,56 @@ def main():
     from paper_2305_13925_b200.distributed import ergodic_se
 
     wl = X.CONFIGS[a.config]
-    B = a.batch or wl.B
     M, K, T = wl.M, wl.K, wl.T
     dt = wl.dtype
     csz = 8 if dt == torch.complex64 else 16
+    # cfg4 (configs[3]): 65536 realizations over all GPUs, generated on device in
+    # chunks of 2048 per GPU inside the step (they do not fit HBM at once: 256 GiB);
+    # other configs: the rank's batch is resident in HBM, precoded in sub-batches
+    # of at most 16 GiB of H (cfg5: 4 x 2048)
+    gen_in_step = wl.chunk is not None
+    if gen_in_step:
+        B = a.batch or wl.B // world
+        sub = min(wl.chunk, B)
+    else:
+        B = a.batch or wl.B
+        sub = B if B * M * K * csz <= 16 * 2**30 else 2048
+    assert B % sub == 0, "batch must be a multiple of the sub-batch"
     first = rank * B
-    H = X.generate_channels(wl.model, seed=0, first=first, B=B, dtype=dt, device=dev)
-    out = BT.alloc_outputs(H, want_gamma=True)
     alpha, power = wl.alpha(), wl.power()
     lib = L.lib()
     tc = X.uses_tensor_cores(dt, a.method, M, K)
+    H = X.generate_channels(wl.model, seed=0, first=first, B=sub if gen_in_step else B, dtype=dt, device=dev)
+    out = BT.alloc_outputs(H[:sub], want_gamma=True)
+    se_all = torch.empty(B, dtype=torch.float64, device=dev)
+    st_all = torch.empty(B, dtype=torch.int32, device=dev)
 
     def step(record=None):
-        if record is not None:
-            record[0].record()
-        BT.rzf_batched(H, alpha, power, method=a.method, T=T, variant="textbook", sigma2=1.0,
-                       out=out, check=False)
-        if record is not None:
-            record[1].record()
-        return ergodic_se(out.sum_se, chunk=2048, group=None if world > 1 else False)
+        for c0 in range(0, B, sub):
+            if gen_in_step:
+                X.generate_channels(wl.model, seed=0, first=first + c0, B=sub, dtype=dt, device=dev, out=H,
+                                    check=False)
+                Hc = H
+            else:
+                Hc = H[c0:c0 + sub]
+            if record is not None:
+                record[c0 // sub][0].record()
+            BT.rzf_batched(Hc, alpha, power, method=a.method, T=T, variant="textbook", sigma2=1.0,
+                           out=out, check=False)
+            if record is not None:
+                record[c0 // sub][1].record()
+            if sub < B:
+                se_all[c0:c0 + sub].copy_(out.sum_se)
+                st_all[c0:c0 + sub].copy_(out.status)
+        return ergodic_se(out.sum_se if sub == B else se_all, chunk=2048, group=None if world > 1 else False)
 
     for _ in range(a.warmup):
         step()
     torch.cuda.synchronize()
-    L.raise_status(out.status.cpu().numpy(), "bench warm-up")
+    L.raise_status((out.status if sub == B else st_all).cpu().numpy(), "bench warm-up")
 
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(a.steps)]
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(B // sub)] for _ in range(a.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -273,7 +296,8 @@ def main():
     if world > 1:
         dist.barrier()
     ms = t0.elapsed_time(t1)
-    kern_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev)
+    # the precoder calls of one step (without the in-step channel generation)
+    kern_ms = statistics.mean(sum(e0.elapsed_time(e1) for e0, e1 in evs) for evs in ev)
     if world > 1:
         tt = torch.tensor([ms, kern_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -286,11 +310,11 @@ def main():
     if a.e2e_steps > 0:
         # pinned host buffers for H and W: bound them to ~1/3 of host RAM across
         # the ranks of this node (a rate metric: a smaller sample is still valid)
-        Be = B
+        Be = H.shape[0]
         try:
             import psutil
             cap = int(psutil.virtual_memory().total / 3 / max(world, 1) / (2 * M * K * csz))
-            Be = max(256, min(B, cap))
+            Be = max(256, min(Be, cap))
         except Exception:  # noqa: BLE001
             pass
         pipe = BT.HostPipeline(M, K, dtype=dt, chunk=min(a.e2e_chunk, Be), device=dev)
@@ -370,7 +394,8 @@ def main():
     roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
             "frac": achieved / peak, "traffic": traffic,
             "peak_source": f"{peak_src} (MEASURED_PEAKS.json)" if peak_src == "measured" else peak_src,
-            "kernel": "xl_rzf fused precoder call" + (" (tcgen05)" if tc else " (SIMT path)"),
+            "kernel": ("xl_rzf precoder call" + (" (tcgen05)" if tc else " (SIMT path)")
+                       + (f", {B // sub} calls of {sub} per step" if sub < B else "")),
             "kernel_ms": kern_ms, "bytes_per_precoder": bytes_per,
             "algorithmic_bytes_per_launch": B * bytes_per,
             "traffic_source": "profiles/traffic.json" if traffic is not None else None,
@@ -394,10 +419,14 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "higher_is_better": True, "scaling": "strong" if gen_in_step else "weak", "vs_baseline": None,
                 "dtype": "c64" if dt == torch.complex64 else "c128", "data": "synthetic",
                 "config": {"workload": f"{a.config}: M={M}, K={K}, T={T}, {a.method}, "
-                                       f"{B} realizations per GPU",
+                                       f"{B} realizations per GPU"
+                                       + (f", generated on device in chunks of {sub} inside the step"
+                                          if gen_in_step else
+                                          (f", precoded in sub-batches of {sub}" if sub < B else "")),
+                           "sub_batch": sub, "channel_generation_timed": gen_in_step,
                            "M": M, "K": K, "T": T, "batch_per_gpu": B,
                            "global_batch": B * world, "method": a.method,
                            "parallelism": f"realization-sharded x{world}",
