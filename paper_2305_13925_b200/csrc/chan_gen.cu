@@ -9,9 +9,11 @@
 // b_lo, b_hi) -- identical to oracle/xlmimo_oracle.py::generate_channels, so
 // realization b is the same on any GPU count / chunking.
 //
-// One CTA per (realization, subarray): every CTA re-derives the users'
-// gains/visibility (a few Philox calls) so H rows are written coalesced
-// (row m = s*Ms + i holds all K users contiguously) without a workspace.
+// chan_real_kernel (S * K <= 2^14, every BASELINE config): one CTA per
+// realization draws the users' gains / visibility once and walks the
+// subarrays.  chan_kernel (larger S * K): one CTA per (realization, subarray),
+// every CTA re-deriving the users' gains / visibility.  Both write H rows
+// coalesced (row m = s*Ms + i holds all K users contiguously), no workspace.
 #include <math.h>
 
 #include "xl_common.cuh"
@@ -87,14 +89,18 @@ chan_kernel(uint64_t seed, int64_t first, int S, int Ms, int K, double p,
   const int half = Ms / 2;
   for (int kc = 0; kc < K; kc += KCH) {
     const int kn = min(KCH, K - kc);
-    // g[i][k - kc]: Philox (j = s*half + t) -> g[2t], g[2t+1]
+    // g[i][k - kc]: Philox (j = s*half + t) -> g[2t], g[2t+1]; counter-based, so
+    // users that do not see subarray s (amp 0, their rows are zero) are skipped
     for (int e = tid; e < half * kn; e += blockDim.x) {
       int kk = e / half, t = e % half, k = kc + kk;
+      if (amp[k] == (R)0) continue;
       uint4 z = philox4x32_10(make_uint4((uint32_t)(s * half + t), (uint32_t)k | (PURPOSE_FADE << 24), b_lo, b_hi), k0, k1);
-      double r0 = sqrt(-log(u01(z.x))), th0 = 2.0 * M_PI * u01(z.y);
-      double r1 = sqrt(-log(u01(z.z))), th1 = 2.0 * M_PI * u01(z.w);
-      g[(2 * t) * KCH + kk] = mk<R>((R)(r0 * cos(th0)), (R)(r0 * sin(th0)));
-      g[(2 * t + 1) * KCH + kk] = mk<R>((R)(r1 * cos(th1)), (R)(r1 * sin(th1)));
+      double r0 = sqrt(-log(u01(z.x))), r1 = sqrt(-log(u01(z.z)));
+      double s0, c0, s1, c1;  // theta = 2 pi u
+      sincospi(2.0 * u01(z.y), &s0, &c0);
+      sincospi(2.0 * u01(z.w), &s1, &c1);
+      g[(2 * t) * KCH + kk] = mk<R>((R)(r0 * c0), (R)(r0 * s0));
+      g[(2 * t + 1) * KCH + kk] = mk<R>((R)(r1 * c1), (R)(r1 * s1));
     }
     __syncthreads();
     for (int e = tid; e < Ms * kn; e += blockDim.x) {
@@ -116,12 +122,156 @@ chan_kernel(uint64_t seed, int64_t first, int S, int Ms, int K, double p,
   }
 }
 
+// Box-Muller pair from two Philox words: complex64 in fp32 (logf / sincospif,
+// ~1e-7 relative: far inside the c64 parity bound), complex128 in fp64 (the
+// oracle's arithmetic).
+__device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& re, float& im) {
+  const float u = __fmaf_rn((float)a, 2.3283064365386963e-10f, 1.1641532182693481e-10f);
+  const float v = __fmaf_rn((float)b, 2.3283064365386963e-10f, 1.1641532182693481e-10f);
+  const float r = sqrtf(-logf(u));
+  float sn, cs;
+  sincospif(2.0f * v, &sn, &cs);
+  re = r * cs;
+  im = r * sn;
+}
+__device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, double& re, double& im) {
+  const double r = sqrt(-log(u01(a)));
+  double sn, cs;
+  sincospi(2.0 * u01(b), &sn, &cs);
+  re = r * cs;
+  im = r * sn;
+}
+
+// One CTA per realization (S * K <= VIS_BITS): the users' gains and visibility
+// masks are drawn once per realization (not once per subarray), then the CTA
+// walks the subarrays; fading is drawn only for the visible (user, subarray)
+// pairs (counter-based stream: the same values as chan_kernel / the oracle).
+constexpr int VIS_BITS = 1 << 14;
+template <typename R>
+__global__ void __launch_bounds__(256)
+chan_real_kernel(uint64_t seed, int64_t first, int S, int Ms, int K, double p,
+                 const double* __restrict__ Rsqrt, double beta_bar, double dmin, double dmax,
+                 cplx<R>* __restrict__ H, int32_t* __restrict__ status) {
+  using C = cplx<R>;
+  const int64_t bl = blockIdx.x;
+  const uint64_t bg = (uint64_t)(first + bl);
+  const uint32_t b_lo = (uint32_t)bg, b_hi = (uint32_t)(bg >> 32);
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  const int M = S * Ms;
+  extern __shared__ double smem[];
+  R* rs = (R*)smem;                        // Ms x Ms
+  R* amp = rs + Ms * Ms;                   // K
+  uint32_t* vis = (uint32_t*)(amp + ((K + 1) & ~1));  // [K][ceil(S/32)] visibility bits
+  const int sw = (S + 31) / 32;
+  C* g = (C*)(vis + ((K * sw + 3) & ~3));  // Ms x KCH (16-B aligned for double2)
+  const int tid = threadIdx.x;
+  for (int e = tid; e < Ms * Ms; e += blockDim.x) rs[(e % Ms) * Ms + e / Ms] = (R)Rsqrt[e];  // transposed
+  const int nq = (S + 3) / 4;
+  for (int k = tid; k < K; k += blockDim.x) {
+    uint4 x = philox4x32_10(make_uint4(0u, (uint32_t)k | (PURPOSE_DIST << 24), b_lo, b_hi), k0, k1);
+    double d = dmin + (dmax - dmin) * u01(x.x);
+    double bdb = -35.3 - 37.6 * log10(d);
+    double gain = pow(10.0, bdb / 10.0) / beta_bar;
+    bool found = false;
+    for (int att = 0; att < MAX_VIS_ATTEMPTS && !found; ++att) {
+      for (int w = 0; w < sw; ++w) vis[k * sw + w] = 0u;
+      for (int q = 0; q < nq; ++q) {
+        uint4 y = philox4x32_10(make_uint4((uint32_t)(att * nq + q), (uint32_t)k | (PURPOSE_VIS << 24), b_lo, b_hi), k0, k1);
+        uint32_t wv[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          int ss = 4 * q + e;
+          if (ss < S && u01(wv[e]) < p) {
+            vis[k * sw + (ss >> 5)] |= 1u << (ss & 31);
+            found = true;
+          }
+        }
+      }
+    }
+    if (!found) status[bl] = XL_STATUS_NO_VISIBLE;
+    amp[k] = found ? (R)sqrt(gain) : (R)0;
+  }
+  __syncthreads();
+  // per subarray: compact the users that see it, draw their fading, then
+  // y = R^{1/2} g as a register-tiled (Ms x Ms) x (Ms x users) product
+  // (thread = one user x 16 rows; the R^{1/2} column is a warp broadcast)
+  const int half = Ms / 2;
+  int* vlist = (int*)(g + (size_t)Ms * KCH);  // K compacted user indices
+  __shared__ int nvis;
+  for (int s = 0; s < S; ++s) {
+    if (tid == 0) {
+      int n = 0;
+      for (int k = 0; k < K; ++k)
+        if ((vis[k * sw + (s >> 5)] >> (s & 31)) & 1u) vlist[n++] = k;
+      nvis = n;
+    }
+    // zero rows of the users that do not see subarray s (coalesced, masked)
+    for (int e = tid; e < Ms * K; e += blockDim.x) {
+      const int i = e / K, k = e % K;
+      if (!((vis[k * sw + (s >> 5)] >> (s & 31)) & 1u)) H[(bl * M + (int64_t)s * Ms + i) * K + k] = mk<R>(0, 0);
+    }
+    __syncthreads();
+    const int nv = nvis;
+    for (int vc = 0; vc < nv; vc += KCH) {
+      const int kn = min(KCH, nv - vc);
+      for (int e = tid; e < half * kn; e += blockDim.x) {
+        const int kk = e / half, t = e % half, k = vlist[vc + kk];
+        uint4 z = philox4x32_10(make_uint4((uint32_t)(s * half + t), (uint32_t)k | (PURPOSE_FADE << 24), b_lo, b_hi), k0, k1);
+        R r0, i0, r1, i1;
+        box_muller(z.x, z.y, r0, i0);
+        box_muller(z.z, z.w, r1, i1);
+        g[(2 * t) * KCH + kk] = mk<R>(r0, i0);
+        g[(2 * t + 1) * KCH + kk] = mk<R>(r1, i1);
+      }
+      __syncthreads();
+      for (int w = tid; w < KCH * (Ms / 16); w += blockDim.x) {
+        const int kk = w % KCH, i0 = 16 * (w / KCH);
+        if (kk >= kn) continue;
+        R ar[16], ai[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) ar[u] = ai[u] = (R)0;
+#pragma unroll 4
+        for (int j = 0; j < Ms; ++j) {
+          const C gj = g[j * KCH + kk];
+          const R* col = rs + j * Ms + i0;  // R^{1/2} stored transposed: col[u] = R^{1/2}[i0 + u][j]
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            ar[u] += col[u] * gj.x;
+            ai[u] += col[u] * gj.y;
+          }
+        }
+        const int k = vlist[vc + kk];
+        const R a = amp[k];
+        C* hp = H + (bl * M + (int64_t)s * Ms + i0) * K + k;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) hp[(int64_t)u * K] = mk<R>(ar[u] * a, ai[u] * a);
+      }
+      __syncthreads();
+    }
+  }
+}
+
 int launch_channel(int dtype, uint64_t seed, int64_t first, int64_t B, int S, int Ms,
                    int K, double p, const double* Rsqrt, double beta_bar, double dmin,
                    double dmax, void* H, int32_t* status, cudaStream_t st) {
   if (S > 65535 || (Ms & 1)) { set_error("channel: unsupported S/Ms"); return XL_ERR_UNSUPPORTED; }
-  dim3 grid((unsigned)B, (unsigned)S);
   size_t rsz = dtype == XL_C64 ? 4 : 8;
+  if ((int64_t)S * K <= VIS_BITS && Ms % 16 == 0 && B <= 0x7fffffff) {  // one CTA per realization
+    const int sw = (S + 31) / 32;
+    size_t smem = rsz * ((size_t)Ms * Ms + ((K + 1) & ~1)) + 4 * (size_t)((K * sw + 3) & ~3) +
+                  2 * rsz * (size_t)Ms * KCH + 4 * (size_t)K;
+    if (dtype == XL_C64) {
+      cudaFuncSetAttribute(chan_real_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      chan_real_kernel<float><<<(unsigned)B, 256, smem, st>>>(seed, first, S, Ms, K, p, Rsqrt, beta_bar, dmin, dmax,
+                                                              (float2*)H, status);
+    } else {
+      cudaFuncSetAttribute(chan_real_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      chan_real_kernel<double><<<(unsigned)B, 256, smem, st>>>(seed, first, S, Ms, K, p, Rsqrt, beta_bar, dmin, dmax,
+                                                               (double2*)H, status);
+    }
+    return check_launch("channel_generate");
+  }
+  dim3 grid((unsigned)B, (unsigned)S);
   size_t smem = rsz * ((size_t)Ms * Ms + ((K + 1) & ~1)) + 2 * rsz * (size_t)Ms * KCH;
   if (dtype == XL_C64) {
     cudaFuncSetAttribute(chan_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
