@@ -148,7 +148,7 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, double& re, d
 // pairs (counter-based stream: the same values as chan_kernel / the oracle).
 constexpr int VIS_BITS = 1 << 14;
 template <typename R>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 chan_real_kernel(uint64_t seed, int64_t first, int S, int Ms, int K, double p,
                  const double* __restrict__ Rsqrt, double beta_bar, double dmin, double dmax,
                  cplx<R>* __restrict__ H, int32_t* __restrict__ status) {
@@ -194,21 +194,34 @@ chan_real_kernel(uint64_t seed, int64_t first, int S, int Ms, int K, double p,
   __syncthreads();
   // per subarray: compact the users that see it, draw their fading, then
   // y = R^{1/2} g as a register-tiled (Ms x Ms) x (Ms x users) product
-  // (thread = one user x 16 rows; the R^{1/2} column is a warp broadcast)
+  // (thread = one user x 8 rows; the R^{1/2} column is a warp broadcast)
   const int half = Ms / 2;
   int* vlist = (int*)(g + (size_t)Ms * KCH);  // K compacted user indices
   __shared__ int nvis;
   for (int s = 0; s < S; ++s) {
-    if (tid == 0) {
+    if (tid < 32) {  // warp 0: ballot compaction in user order
       int n = 0;
-      for (int k = 0; k < K; ++k)
-        if ((vis[k * sw + (s >> 5)] >> (s & 31)) & 1u) vlist[n++] = k;
-      nvis = n;
+      for (int k0 = 0; k0 < K; k0 += 32) {
+        const int k = k0 + tid;
+        const bool v = k < K && ((vis[k * sw + (s >> 5)] >> (s & 31)) & 1u);
+        const unsigned bal = __ballot_sync(0xffffffffu, v);
+        if (v) vlist[n + __popc(bal & ((1u << tid) - 1u))] = k;
+        n += __popc(bal);
+      }
+      if (tid == 0) nvis = n;
     }
     // zero rows of the users that do not see subarray s (coalesced, masked)
-    for (int e = tid; e < Ms * K; e += blockDim.x) {
-      const int i = e / K, k = e % K;
-      if (!((vis[k * sw + (s >> 5)] >> (s & 31)) & 1u)) H[(bl * M + (int64_t)s * Ms + i) * K + k] = mk<R>(0, 0);
+    if (blockDim.x % K == 0) {  // a fixed user per thread
+      const int k = tid % K;
+      if (!((vis[k * sw + (s >> 5)] >> (s & 31)) & 1u)) {
+        C* hp = H + (bl * M + (int64_t)s * Ms) * K + k;
+        for (int i = tid / K; i < Ms; i += blockDim.x / K) hp[(int64_t)i * K] = mk<R>(0, 0);
+      }
+    } else {
+      for (int e = tid; e < Ms * K; e += blockDim.x) {
+        const int i = e / K, k = e % K;
+        if (!((vis[k * sw + (s >> 5)] >> (s & 31)) & 1u)) H[(bl * M + (int64_t)s * Ms + i) * K + k] = mk<R>(0, 0);
+      }
     }
     __syncthreads();
     const int nv = nvis;
@@ -224,18 +237,19 @@ chan_real_kernel(uint64_t seed, int64_t first, int S, int Ms, int K, double p,
         g[(2 * t + 1) * KCH + kk] = mk<R>(r1, i1);
       }
       __syncthreads();
-      for (int w = tid; w < KCH * (Ms / 16); w += blockDim.x) {
-        const int kk = w % KCH, i0 = 16 * (w / KCH);
+      constexpr int TR = 8;  // rows per thread
+      for (int w = tid; w < KCH * (Ms / TR); w += blockDim.x) {
+        const int kk = w % KCH, i0 = TR * (w / KCH);
         if (kk >= kn) continue;
-        R ar[16], ai[16];
+        R ar[TR], ai[TR];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) ar[u] = ai[u] = (R)0;
+        for (int u = 0; u < TR; ++u) ar[u] = ai[u] = (R)0;
 #pragma unroll 4
         for (int j = 0; j < Ms; ++j) {
           const C gj = g[j * KCH + kk];
           const R* col = rs + j * Ms + i0;  // R^{1/2} stored transposed: col[u] = R^{1/2}[i0 + u][j]
 #pragma unroll
-          for (int u = 0; u < 16; ++u) {
+          for (int u = 0; u < TR; ++u) {
             ar[u] += col[u] * gj.x;
             ai[u] += col[u] * gj.y;
           }
@@ -244,7 +258,7 @@ chan_real_kernel(uint64_t seed, int64_t first, int S, int Ms, int K, double p,
         const R a = amp[k];
         C* hp = H + (bl * M + (int64_t)s * Ms + i0) * K + k;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) hp[(int64_t)u * K] = mk<R>(ar[u] * a, ai[u] * a);
+        for (int u = 0; u < TR; ++u) hp[(int64_t)u * K] = mk<R>(ar[u] * a, ai[u] * a);
       }
       __syncthreads();
     }
@@ -256,7 +270,7 @@ int launch_channel(int dtype, uint64_t seed, int64_t first, int64_t B, int S, in
                    double dmax, void* H, int32_t* status, cudaStream_t st) {
   if (S > 65535 || (Ms & 1)) { set_error("channel: unsupported S/Ms"); return XL_ERR_UNSUPPORTED; }
   size_t rsz = dtype == XL_C64 ? 4 : 8;
-  if ((int64_t)S * K <= VIS_BITS && Ms % 16 == 0 && B <= 0x7fffffff) {  // one CTA per realization
+  if ((int64_t)S * K <= VIS_BITS && Ms % 8 == 0 && B <= 0x7fffffff) {  // one CTA per realization
     const int sw = (S + 31) / 32;
     size_t smem = rsz * ((size_t)Ms * Ms + ((K + 1) & ~1)) + 4 * (size_t)((K * sw + 3) & ~3) +
                   2 * rsz * (size_t)Ms * KCH + 4 * (size_t)K;
