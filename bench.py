@@ -314,7 +314,7 @@ def main():
         try:
             import psutil
             cap = int(psutil.virtual_memory().total / 3 / max(world, 1) / (2 * M * K * csz))
-            Be = max(256, min(Be, cap))
+            Be = min(Be, max(256, cap))
         except Exception:  # noqa: BLE001
             pass
         pipe = BT.HostPipeline(M, K, dtype=dt, chunk=min(a.e2e_chunk, Be), device=dev)
@@ -394,7 +394,7 @@ def main():
     roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
             "frac": achieved / peak, "traffic": traffic,
             "peak_source": f"{peak_src} (MEASURED_PEAKS.json)" if peak_src == "measured" else peak_src,
-            "kernel": ("xl_rzf precoder call" + (" (tcgen05)" if tc else " (SIMT path)")
+            "kernel": ("xl_rzf precoder call" + (" (tcgen05)" if tc else " (general path)")
                        + (f", {B // sub} calls of {sub} per step" if sub < B else "")),
             "kernel_ms": kern_ms, "bytes_per_precoder": bytes_per,
             "algorithmic_bytes_per_launch": B * bytes_per,

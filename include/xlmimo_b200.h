@@ -62,7 +62,9 @@ const char* xl_last_error(void);
 /* Number of kernels this library has launched in the process so far
  * (benchmark accounting of "our" launches). */
 uint64_t xl_launch_count(void);
-/* 1 when the fused tcgen05 kernel serves (dtype, method, M, K), else 0. */
+/* 1 when our tcgen05 kernels serve the whole rzf call for (dtype, method,
+ * M, K) -- the fused kernel (K in {16, 32, 64}) or the streaming Gram / W +
+ * cluster Jac-PCG chain (K = 128, M % 64 == 0) -- else 0. */
 int xl_rzf_uses_tensor_cores(int dtype, int method, int32_t M, int32_t K);
 
 /* Batched regularized Gram A_b = H_b^H H_b + xi_b I, Hermitian by

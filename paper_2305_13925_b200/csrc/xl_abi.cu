@@ -72,7 +72,9 @@ uint64_t xl_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RE
 const char* xl_last_error(void) { return g_err; }
 
 int xl_rzf_uses_tensor_cores(int dtype, int method, int32_t M, int32_t K) {
-  return fused_supported(dtype, method, M, K) ? 1 : 0;
+  if (fused_supported(dtype, method, M, K)) return 1;
+  // K = 128: streaming tcgen05 Gram / W + the cluster Jac-PCG / CG
+  return (method != XL_DIRECT && stc_supported(dtype, M, K) && cpcg_supported(K)) ? 1 : 0;
 }
 
 int xl_gram(int dtype, const void* H, int64_t B, int32_t M, int32_t K, double xi,
