@@ -150,3 +150,22 @@ def test_streaming_gram_w_match_library_gemms(method):
         assert relf(s.F[b].cpu().numpy(), Gr / br) <= 1e-4
         assert abs(s.beta[b].item() - br) <= 1e-4 * br
         assert abs(s.sum_se[b].item() - se) <= 1e-4 * abs(se)
+
+
+@pytest.mark.parametrize("B,M,T", [(1, 64, 1), (3, 64, 2), (4100, 64, 3)])
+def test_k128_edge_shapes(B, M, T):
+    """One 64-antenna chunk, T = 1, a single realization, and a batch past the
+    streaming Gram's 4096-realization sub-batch (U workspace reuse)."""
+    K = 128
+    g = torch.Generator(device=DEV).manual_seed(B + M + T)
+    H = torch.complex(torch.randn(B, M, K, device=DEV, generator=g),
+                      torch.randn(B, M, K, device=DEV, generator=g)) * 0.7
+    H = H.to(torch.complex64)
+    xi = K / 10.0
+    out = _run(H, xi, 10.0, T=T)
+    assert (out.status.cpu().numpy() == 0).all()
+    Hq = H.cpu().numpy().astype(np.complex128)
+    for b in sorted({0, B // 2, B - 1}):
+        Gr, br, gr, s = O.precoder_and_se(Hq[b], xi, 10.0, 1.0, "jacpcg", T, "textbook")
+        assert relf(out.W[b].cpu().numpy(), Gr) <= 1e-4, (B, M, T, b)
+        assert abs(out.sum_se[b].item() - s) <= 1e-4 * abs(s)
