@@ -441,8 +441,8 @@ def test_se_partials_vs_oracle():
 @pytest.mark.parametrize("cfg,B", [("cfg1", 100), ("cfg3", 64), ("cfg4", 4)])
 def test_graphed_rzf_matches_direct_calls(cfg, B):
     """CUDA-graph replay of the whole precoder chain (fused kernel, SIMT general
-    path, tensor-core large-K path with library GEMMs) gives the same bits as
-    the direct call, on two different inputs."""
+    path, the K = 128 tcgen05 chain with its 2-CTA clusters and DSMEM bulk
+    copies) gives the same bits as the direct call, on two different inputs."""
     wl = X.CONFIGS[cfg]
     g = BT.GraphedRzf(B, wl.M, wl.K, wl.dtype, wl.alpha(), wl.power(), T=wl.T)
     for seed in (0, 1):
