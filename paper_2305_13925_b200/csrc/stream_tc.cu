@@ -302,8 +302,7 @@ __global__ void __launch_bounds__(NT, 1) w_kernel(const float2* __restrict__ H, 
   const float sz = szv[b];
   const int q = warp & 3, cw = warp - W_CONV0, kh = cw >> 2;
   const int r = 32 * q + lane;            // local output component (TMEM lane)
-  const int m = 128 * half + r;           // global output component
-  const int j = m >> 1;                   // user column of X
+  const int m = 128 * half + r;           // global output component (user column m / 2 of X)
   const bool odd = m & 1;
   float srow = 1.0f;
   // ---- stage this half's 64 columns of X (512 B of each row i) in the ring
