@@ -62,7 +62,8 @@ int tc_gx(const double* xi_b, double xi, int64_t B, int K, void* GX, double* par
           cudaStream_t st);
 // stream_tc.cu: streaming tcgen05 Gram / W for K = 128 complex64 (M % 64 == 0)
 bool stc_supported(int dtype, int M, int K);
-int stc_gram(const void* H, int64_t B, int M, int K, float* sz, float* U, int* rflag, cudaStream_t st);
+int stc_gram(const void* H, int64_t B, int M, int K, double xi, const double* xi_b, float* sz, void* A, int* rflag,
+             cudaStream_t st);
 int stc_apply(const void* H, const void* X, const double* beta, const float* sz, int64_t B, int M, int K, void* W,
               void* F, cudaStream_t st);
 int tc_gram_extract(const float* U, int64_t Bc, int K, const double* xi_b, double xi, void* A, cudaStream_t st);

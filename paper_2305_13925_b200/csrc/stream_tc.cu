@@ -3,13 +3,13 @@
 // library GEMMs (gemm_tc.cu tc_gram / tc_apply) for the cfg4 shape.
 //
 //   gram_kernel   U = Zh^T (Zh + 2 Zl) over all M antennas, Z = sz [Re H, Im H]
+//                 in TMEM, emitted as A = (U + U^T)/2 + xi I (complex K x K)
 //                 (sz: power of two from the first non-zero chunk; realizations
 //                 whose later chunks would overflow fp16 are flagged and redone
 //                 with the exact max from zmax_kernel)
-//                 interleaved (M x 2K real), written fp32 row-major as U / sz^2;
-//                 gram_extract_kernel then forms A = (U + U^T)/2 + xi I
-//                 (gram_regularized, precoder.py:53-61) exactly as after the
-//                 library GEMMs;
+//                 interleaved (M x 2K real) -- the arithmetic of
+//                 gram_extract_kernel after the library GEMMs
+//                 (gram_regularized, precoder.py:53-61);
 //   w_kernel      W^T = beta Xe^T Z^T per realization and output half
 //                 (rzf_iterative F = H X, precoder.py:90, with _power_scale's
 //                 beta folded in, precoder.py:64-70), F = W / beta optional.
@@ -171,7 +171,8 @@ constexpr uint32_t ID_GRAM = idesc(128, NC, 1, 1);
 constexpr float RANGE_MAX = 32768.0f;
 
 __global__ void __launch_bounds__(NT, 1) gram_kernel(const float2* __restrict__ H, int M, float* __restrict__ szv,
-                                                     float* __restrict__ U, int* __restrict__ rflag, int fixup) {
+                                                     float2* __restrict__ A, double xi, const double* __restrict__ xi_b,
+                                                     int* __restrict__ rflag, int fixup) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
   Small* sm = reinterpret_cast<Small*>(smem + NS * SB);
@@ -244,22 +245,62 @@ __global__ void __launch_bounds__(NT, 1) gram_kernel(const float2* __restrict__ 
       if (over && lane == 0) rflag[b] = 1;
       if (tid == 32 * W_CONV0) szv[b] = sz;
     }
-    // epilogue: warp (quadrant q, half hf) writes U rows hf 128 + 32 q + lane
+    // epilogue: A = (U + U^T)/2 + xi I as complex K x K, straight from TMEM
+    // (gram_regularized, precoder.py:53-61; the arithmetic of gram_extract_kernel).
+    // U block (I, J) (rows 128 I.., cols 128 J..) sits at TMEM lanes 0..127,
+    // columns 256 I + 128 J.  Per user-block pair (0,0), (0,1), (1,1): the
+    // transposed partner block U(J, I) is staged in the (idle) ring with a padded
+    // row stride, each thread (row r of block I, column half p) combines its own
+    // row with the staged column, lane pairs (2i, 2i+1) form the complex entries;
+    // block (1,0) is the conjugate transpose of (0,1).
     mbar_wait(&sm->done, 0);
     tc_after();
-    const int q = warp & 3, hf = cw >> 2;
+    const int q = warp & 3, p = cw >> 2;
+    const int r = 32 * q + lane;
     const float isz = 1.0f / sz;  // two exact multiplies: sz^2 may overflow
-    const int row = hf * 128 + 32 * q + lane;
-    float4* urow = reinterpret_cast<float4*>(U + (b * NC + row) * (int64_t)NC);
-    const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 256 * hf;
+    const double xi_v = xi_b ? xi_b[b] : xi;
+    constexpr int SP = 129;       // staged row stride (floats): conflict-free both ways
+    float* S = reinterpret_cast<float*>(ring);
+    const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+    const bool odd = lane & 1;
+    float2* Ab = A + b * (int64_t)KU * KU;
+    const int blocks[3][2] = {{0, 0}, {0, 1}, {1, 1}};
 #pragma unroll 1
-    for (int c0 = 0; c0 < NC; c0 += 32) {
-      float v[32];
-      tmem_ld16(ta + c0, v);
-      tmem_ld16(ta + c0 + 16, v + 16);
-      tmem_wait_ld();
+    for (int bi = 0; bi < 3; ++bi) {
+      const int I = blocks[bi][0], J = blocks[bi][1];
+      // stage U(J, I): TMEM lane c = row c of block J, columns 256 J + 128 I ..
+#pragma unroll 1
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        float v[16];
+        tmem_ld16(tl + 256 * J + 128 * I + 64 * p + c0, v);
+        tmem_wait_ld();
 #pragma unroll
-      for (int e = 0; e < 32; e += 4) urow[(c0 + e) / 4] = make_float4(v[e] * isz * isz, v[e + 1] * isz * isz, v[e + 2] * isz * isz, v[e + 3] * isz * isz);
+        for (int e = 0; e < 16; ++e) S[r * SP + 64 * p + c0 + e] = v[e];
+      }
+      named_sync(BAR_CONV, 32 * NCONV);
+#pragma unroll 1
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        float v[16];
+        tmem_ld16(tl + 256 * I + 128 * J + 64 * p + c0, v);  // own row r of U(I, J)
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+          const int c = 64 * p + c0 + e;
+          const float g0 = 0.5f * (v[e] + S[c * SP + r]) * isz * isz;
+          const float g1 = 0.5f * (v[e + 1] + S[(c + 1) * SP + r]) * isz * isz;
+          const float p0 = __shfl_xor_sync(0xffffffffu, g0, 1), p1 = __shfl_xor_sync(0xffffffffu, g1, 1);
+          float re = odd ? (p0 + g1) : (g0 + p1);
+          float im = odd ? (p1 - g0) : (g1 - p0);
+          const int i = 64 * I + (r >> 1), j = 64 * J + (c >> 1);
+          if (i == j) {
+            re = (float)((double)re + xi_v);
+            im = 0.0f;
+          }
+          if (!odd) Ab[(int64_t)i * KU + j] = make_float2(re, im);
+          else if (I != J) Ab[(int64_t)j * KU + i] = make_float2(re, -im);
+        }
+      }
+      named_sync(BAR_CONV, 32 * NCONV);  // staged block consumed
     }
   }
   tc_before();
@@ -436,17 +477,18 @@ bool stc_supported(int dtype, int M, int K) {
   return !(e && e[0] == 'l');
 }
 
-// U (B x 2K x 2K fp32) for the Gram and the split scales sz[b] (rflag: B ints
-// of scratch): first-chunk scales, then the fixup of the flagged realizations
-int stc_gram(const void* H, int64_t B, int M, int K, float* sz, float* U, int* rflag, cudaStream_t st) {
+// A = H^H H + xi I (B x K x K complex64) and the split scales sz[b] (rflag: B
+// ints of scratch): first-chunk scales, then the fixup of the flagged realizations
+int stc_gram(const void* H, int64_t B, int M, int K, double xi, const double* xi_b, float* sz, void* A, int* rflag,
+             cudaStream_t st) {
   if (!stc_supported(XL_C64, M, K)) { set_error("stream Gram: unsupported shape"); return XL_ERR_UNSUPPORTED; }
   if (cudaMemsetAsync(rflag, 0, (size_t)B * sizeof(int), st) != cudaSuccess) return check_launch("stream flags");
   cudaFuncSetAttribute(stc::gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, stc::SMEM);
-  stc::gram_kernel<<<(unsigned)B, stc::NT, stc::SMEM, st>>>((const float2*)H, M, sz, U, rflag, 0);
+  stc::gram_kernel<<<(unsigned)B, stc::NT, stc::SMEM, st>>>((const float2*)H, M, sz, (float2*)A, xi, xi_b, rflag, 0);
   if (int e = check_launch("stream gram")) return e;
   stc::zmax_kernel<<<(unsigned)B, 512, 0, st>>>((const float4*)H, (int64_t)M * K / 2, sz, rflag);
   if (int e = check_launch("stream zmax")) return e;
-  stc::gram_kernel<<<(unsigned)B, stc::NT, stc::SMEM, st>>>((const float2*)H, M, sz, U, rflag, 1);
+  stc::gram_kernel<<<(unsigned)B, stc::NT, stc::SMEM, st>>>((const float2*)H, M, sz, (float2*)A, xi, xi_b, rflag, 1);
   return check_launch("stream gram fixup");
 }
 

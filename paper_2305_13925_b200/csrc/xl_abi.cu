@@ -156,13 +156,9 @@ static int64_t tc_chunk_size(int dtype, int64_t B, int M, int K) {
 }
 
 // K = 128 complex64 with M % 64 == 0: the streaming Gram / W kernels
-// (stream_tc.cu) need the fp32 real Gram U of a sub-batch (after the cuBLAS
-// workspace the split-GEMM solver may still use) and one scale per realization.
-constexpr int64_t STC_SUB = 4096;
-static size_t stc_ws(int64_t B, int K) {
-  const int64_t nb = B < STC_SUB ? B : STC_SUB;
-  return tc_cublas_ws_bytes() + align_up((size_t)nb * 4 * K * K * 4);
-}
+// (stream_tc.cu) need one split scale and one range flag per realization
+// (below) and only the cuBLAS workspace the split-GEMM solver may still use.
+static size_t stc_ws(int64_t, int) { return tc_cublas_ws_bytes(); }
 // bytes of the tensor-core region that precedes the PCG buffers
 static size_t tc_region(int dtype, int64_t B, int M, int K) {
   return stc_supported(dtype, M, K) ? stc_ws(B, K) : tc_gram_ws_bytes(dtype, tc_chunk_size(dtype, B, M, K), M, K);
@@ -223,14 +219,8 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   int e;
   const int64_t Bc = tc ? tc_chunk_size(dtype, B, M, K) : B;
   const int64_t oH = (int64_t)M * K * (int64_t)cs, oK = (int64_t)K * K * (int64_t)cs;
-  if (sc) {  // streaming tcgen05 Gram per sub-batch, U after the cuBLAS workspace
-    float* U = (float*)((char*)tcws + tc_cublas_ws_bytes());
-    for (int64_t b0 = 0; b0 < B; b0 += STC_SUB) {
-      const int64_t nb = B - b0 < STC_SUB ? B - b0 : STC_SUB;
-      if ((e = stc_gram((const char*)H + b0 * oH, nb, M, K, szb + b0, U, rflag + b0, st))) return e;
-      if ((e = tc_gram_extract(U, nb, K, xi_per_batch ? xi_per_batch + b0 : nullptr, xi, (char*)A + b0 * oK, st)))
-        return e;
-    }
+  if (sc) {  // streaming tcgen05 Gram, A emitted from TMEM
+    if ((e = stc_gram(H, B, M, K, xi, xi_per_batch, szb, A, rflag, st))) return e;
   } else if (tc) {
     for (int64_t b0 = 0; b0 < B; b0 += Bc) {
       const int64_t nb = B - b0 < Bc ? B - b0 : Bc;
