@@ -9,4 +9,4 @@ timeout 600 python bench.py > gpurun_out/${R}_bench.log 2>&1; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${R}_bench_ref.log 2>&1; echo "ref rc=$?"; tail -1 gpurun_out/${R}_bench_ref.log | cut -c1-200
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/${R}_launches.csv python bench.py --e2e-steps 0 --no-cpu-baseline --steps 2 --warmup 3 > gpurun_out/${R}_ncu_launch.log 2>&1
-echo "launch list rc=$?"; python tools/launch_summary.py gpurun_out/${R}_launches.csv | head -8
+echo "launch list rc=$?"; python tools/launch_summary.py gpurun_out/${R}_launches.csv > gpurun_out/${R}_launches.txt; head -8 gpurun_out/${R}_launches.txt
