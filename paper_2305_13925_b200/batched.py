@@ -73,9 +73,11 @@ _WS = _Workspace()
 
 def _xi_args(xi, B, device):
     if isinstance(xi, torch.Tensor):
-        xt = xi.to(device=device, dtype=torch.float64).contiguous()
+        xt = xi.to(device=device, dtype=torch.float64).reshape(-1).contiguous()
         if xt.numel() != B:
             raise ConfigurationError("per-realization xi must have B entries")
+        if B and not bool((xt > 0).all()):   # precoder.py:55-56, per realization
+            raise ConfigurationError("regularization xi must be positive for every realization")
         return 0.0, xt
     xi = float(xi)
     if not xi > 0:
@@ -144,6 +146,8 @@ def rzf_batched(H: torch.Tensor, xi, power: float, method: str = "jacpcg", T: in
     xs, xt = _xi_args(xi, B, H.device)
     if out is None:
         out = alloc_outputs(H, want_gamma, want_F, want_X)
+    else:
+        _check_out(out, H)
     if general:
         nbytes = int(lib.xl_rzf_general_workspace_bytes(dc, METHODS[method], B, M, K))
         fn = lib.xl_rzf_general
@@ -161,16 +165,40 @@ def rzf_batched(H: torch.Tensor, xi, power: float, method: str = "jacpcg", T: in
         st = out.status.cpu().numpy()
         redo = (st == L.XL_STATUS_RANGE).nonzero()[0]
         if redo.size:
-            _rerun_general(H, redo, xi, power, method, T, variant, sigma2, out, stream)
+            _rerun_general(H, redo, xt if xt is not None else xs, power, method, T, variant, sigma2,
+                           out, stream)
             st = out.status.cpu().numpy()
         L.raise_status(st, "rzf_batched")
     return out
 
 
+def _check_out(out: PrecoderBatch, H: torch.Tensor):
+    """Caller-provided outputs: shapes, dtypes, device and contiguity are
+    checked before their raw pointers reach the kernels."""
+    B, M, K = H.shape
+    f64 = torch.float64
+    want = {"W": ((B, M, K), H.dtype), "beta": ((B,), f64), "sum_se": ((B,), f64),
+            "status": ((B,), torch.int32), "gamma": ((B, K), f64), "F": ((B, M, K), H.dtype),
+            "X": ((B, K, K), H.dtype)}
+    for name, (shape, dt) in want.items():
+        t = getattr(out, name)
+        if t is None:
+            if name in ("W", "beta", "sum_se", "status"):
+                raise ConfigurationError(f"out.{name} is required")
+            continue
+        _check_tensor(t, f"out.{name}", len(shape), dt)
+        if tuple(t.shape) != shape:
+            raise ConfigurationError(f"out.{name} must have shape {shape}, got {tuple(t.shape)}")
+        if t.device != H.device:
+            raise ConfigurationError(f"out.{name} must live on {H.device}")
+
+
 def _rerun_general(H, idx, xi, power, method, T, variant, sigma2, out, stream):
-    """Re-run flagged realizations on the general GPU kernels and scatter back."""
+    """Re-run flagged realizations on the general GPU kernels and scatter back.
+
+    ``xi`` is the scalar or the device float64 copy made by ``_xi_args``."""
     it = torch.from_numpy(idx).to(H.device)
-    xsub = xi[it] if isinstance(xi, torch.Tensor) else xi
+    xsub = xi.index_select(0, it) if isinstance(xi, torch.Tensor) else xi
     sub = rzf_batched(H.index_select(0, it).contiguous(), xsub, power, method, T, variant, sigma2,
                       want_gamma=out.gamma is not None, want_F=out.F is not None,
                       want_X=out.X is not None, check=False, stream=stream, general=True)
@@ -403,6 +431,11 @@ class HostPipeline:
             sigma2=1.0):
         B = H_host.shape[0]
         n = (B + self.chunk - 1) // self.chunk
+        xi_dev = None
+        if isinstance(xi, torch.Tensor):   # per-realization xi: one device copy, sliced per chunk
+            xi_dev = xi.reshape(-1).to(device=self.device, dtype=torch.float64)
+            if xi_dev.numel() != B:
+                raise ConfigurationError("per-realization xi must have B entries")
         ev_h = [torch.cuda.Event() for _ in range(2)]
         ev_c = [torch.cuda.Event() for _ in range(2)]
         ev_hfree = [torch.cuda.Event() for _ in range(2)]
@@ -426,7 +459,8 @@ class HostPipeline:
                 view = out if nb == self.chunk else PrecoderBatch(
                     W=out.W[:nb], beta=out.beta[:nb], sum_se=out.sum_se[:nb],
                     status=out.status[:nb])
-                rzf_batched(Hd[:nb], xi, power, method=method, T=T, variant=variant,
+                xc = xi_dev[lo:hi] if xi_dev is not None else xi
+                rzf_batched(Hd[:nb], xc, power, method=method, T=T, variant=variant,
                             sigma2=sigma2, want_gamma=False, out=view, check=False,
                             stream=self.s_comp)
                 ev_c[j].record(self.s_comp)
@@ -441,3 +475,25 @@ class HostPipeline:
                 started_w[j] = True
         self.s_d2h.synchronize()
         self.s_comp.synchronize()
+        self._rerun_range(H_host, W_host, sum_se_host, status_host, xi, power, method, T, variant,
+                          sigma2)
+
+    def _rerun_range(self, H_host, W_host, sum_se_host, status_host, xi, power, method, T,
+                     variant, sigma2):
+        """The rzf_batched(check=True) contract on host buffers: realizations
+        the fused kernel flagged XL_STATUS_RANGE are re-run on the general
+        kernels and their W / sum-SE / status scattered back."""
+        st = status_host[: H_host.shape[0]].numpy()
+        redo = (st == L.XL_STATUS_RANGE).nonzero()[0]
+        if not redo.size:
+            return
+        it = torch.from_numpy(redo)
+        Hd = H_host.index_select(0, it).to(self.device)
+        xsub = xi
+        if isinstance(xi, torch.Tensor):
+            xsub = xi.reshape(-1).to(torch.float64).cpu().index_select(0, it)
+        sub = rzf_batched(Hd, xsub, power, method, T, variant, sigma2, want_gamma=False,
+                          check=False, general=True)
+        W_host.index_copy_(0, it, sub.W.cpu())
+        sum_se_host.index_copy_(0, it, sub.sum_se.cpu())
+        status_host.index_copy_(0, it, sub.status.cpu())

@@ -56,13 +56,18 @@ def _worker(rank, world, port, out):
         allp = D.gather_partials(parts)
         mean, sem = D.combine_partials_device(allp)
         out[rank] = (first, count, float(mean), float(sem), allp.shape[0])
-        # equal-size shards go through the single all_gather path
-        eq = _partials(_sum_se_oracle(rank * 4, 4), CHUNK)
-        m2, s2 = D.combine_partials_device(D.gather_partials_fixed(eq))
+        # the public combine path on ragged shards (the shards
+        # hold different chunk counts; gather_partials pads them)
+        m2, s2 = D.ergodic_from_partials(parts)
         out[world + rank] = (float(m2), float(s2))
         # the public entry point with group=False never communicates
-        m3, _ = D.combine_partials_device(parts)
+        m3, _ = D.ergodic_from_partials(parts, group=False)
         out[2 * world + rank] = float(m3)
+        # bench timing helpers: barrier + timed region + max over ranks
+        import time
+        with D.DeviceTimer("cpu") as t:
+            time.sleep(0.05 + 0.15 * rank)
+        out[3 * world + rank] = (t.ms, D.max_over_ranks([rank + 1.0, 10.0 - rank]))
     finally:
         dist.destroy_process_group()
 
@@ -105,9 +110,21 @@ def test_gloo_two_ranks_ergodic_se():
         assert abs(sem - rs) <= 1e-9 * rs, (sem, rs)
         assert nchunks == sum(-(-D.shard_range(TOTAL, world, q)[1] // CHUNK) for q in range(world))
     assert out[0][2:4] == out[1][2:4]  # bit-identical on both ranks
-    m_eq = O.sum_se(_sum_se_oracle(0, 8))[0]
     for r in range(world):
-        assert abs(out[world + r][0] - m_eq) <= 1e-12 * abs(m_eq)
+        assert abs(out[world + r][0] - rm) <= 1e-12 * abs(rm)
+        assert abs(out[world + r][1] - rs) <= 1e-9 * rs
+        ms, mx = out[3 * world + r]
+        assert ms >= 200.0 * 0.9, ms          # the slower rank's 0.2 s on every rank
+        assert mx == [2.0, 10.0]
     # rank-local combine sees only its own shard
     m0 = O.sum_se(x[:D.shard_range(TOTAL, world, 0)[1]])[0]
     assert abs(out[2 * world] - m0) <= 1e-12 * abs(m0)
+
+
+def test_rank_batch_weak_and_strong():
+    assert [D.rank_batch("weak", 100, 4, r) for r in range(4)] == [(0, 100), (100, 100), (200, 100), (300, 100)]
+    got = [D.rank_batch("strong", 32768, 8, r) for r in range(8)]
+    assert got[0] == (0, 4096) and got[7] == (28672, 4096)
+    assert sum(c for _, c in [D.rank_batch("strong", 4097, 2, r) for r in range(2)]) == 4097
+    with pytest.raises(ValueError):
+        D.rank_batch("other", 1, 1, 0)
