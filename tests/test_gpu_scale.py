@@ -11,10 +11,12 @@
 - an 80 dB per-user gain spread through the fused K <= 64 kernel.
 
 Tolerances (north_star): W relative Frobenius <= 1e-4 (c64) / <= 1e-10
-(c128), sum-SE relative <= 1e-4.  Exceptions are stated where they apply:
-unpreconditioned CG on the ill-conditioned cfg5 channel (r = 0.9) amplifies
-fp32 round-off beyond 1e-4 -- its c64 bound is the measured worst case
-("fp32 sensitivity of CG"), and c128 meets 1e-10.
+(c128), sum-SE relative <= 1e-4.  One stated exception: unpreconditioned CG
+in complex64 at T = 4-5 on the cfg2 grid amplifies round-off beyond 1e-4 in
+ANY complex64 execution (an independent numpy complex64 run of the same
+recurrence lands up to 7e-3 (W) / 4e-2 (SE) from the complex128 oracle at
+T = 5, 20 dB); those points are held to 2x that per-realization distance
+(DESIGN.md section 4).  CG at cfg5 and every Jac-PCG / direct point meet 1e-4.
 
 Measured maxima are appended to $XL_PARITY_LOG (JSON lines) when set.
 """
@@ -32,6 +34,7 @@ pytestmark = pytest.mark.gpu
 
 import paper_2305_13925_b200 as X  # noqa: E402
 from paper_2305_13925_b200 import trials as TR  # noqa: E402
+from fp32_ref import _fp32_sensitivity  # noqa: E402
 
 
 def relf(a, b):
@@ -96,9 +99,10 @@ def test_config_sample_vs_oracle(cfg, n, method, wtol, stol):
     assert be.max() <= max(wtol, 1e-10) * 10
 
 
-# measured worst cases of unpreconditioned CG in complex64 on the ill-conditioned
-# cfg5 channel (r = 0.9, T = 6): fp32 round-off amplified by the recurrence
-CG_C64_CFG5_BOUND = 5e-3
+# unpreconditioned CG in complex64 on the ill-conditioned cfg5 channel
+# (r = 0.9, T = 6): measured max 1.0e-5 over 64 realizations (r02), so the
+# north_star bound holds as is
+CG_C64_CFG5_BOUND = 1e-4
 
 
 @pytest.mark.timeout(1800)
@@ -125,19 +129,29 @@ def test_cfg2_paired_grid_vs_oracle():
     assert len(pts) == 63
     g = TR.se_grid_batched(H, pts, keep_W=True)
     Hn = H.cpu().numpy().astype(np.complex128)
-    worst = {}
+    worst, bad, fp32 = {}, {}, {}
     for p in pts:
         xi, power = TR.default_xi(wl.K, p.snr_db), 10.0 ** (p.snr_db / 10.0)
         W = g.W[p].cpu().numpy().astype(np.complex128)
         se = g.sum_se[p].cpu().numpy()
+        k = (p.method, p.T, p.snr_db)
         for b in range(Hn.shape[0]):
             G, _, _, s = O.precoder_and_se(Hn[b], xi, power, 1.0, p.method, max(p.T, 1), "textbook")
             e, es = relf(W[b], G), abs(se[b] - s) / abs(s)
-            k = (p.method, p.T, p.snr_db)
             worst[k] = max(worst.get(k, (0, 0))[0], e), max(worst.get(k, (0, 0))[1], es)
-    _log(test="cfg2_grid", worst={f"{m}:T{t}:{s:g}": v for (m, t, s), v in worst.items()})
-    bad = {k: v for k, v in worst.items() if v[0] > 1e-4 or v[1] > 1e-4}
+            if e <= 1e-4 and es <= 1e-4:
+                continue
+            # unpreconditioned CG only: bounded by 2x an independent complex64
+            # execution of the same recurrence on the same realization
+            fw, fs = _fp32_sensitivity(Hn[b], xi, power, p.method, max(p.T, 1), "textbook")
+            fp32[k] = max(fp32.get(k, (0, 0))[0], fw), max(fp32.get(k, (0, 0))[1], fs)
+            if p.method != "cg" or e > 2 * max(fw, 1e-4) or es > 2 * max(fs, 1e-4):
+                bad[k] = (e, es, fw, fs)
+    _log(test="cfg2_grid", worst={f"{m}:T{t}:{s:g}": v for (m, t, s), v in worst.items()},
+         fp32_cg={f"{m}:T{t}:{s:g}": v for (m, t, s), v in fp32.items()})
     assert not bad, bad
+    # Jac-PCG and direct meet the north_star bound at every point
+    assert all(v[0] <= 1e-4 and v[1] <= 1e-4 for (m, _, _), v in worst.items() if m != "cg")
     # paired: the ergodic SE increases with SNR for every method
     erg = g.ergodic()
     for m, T in [("jacpcg", 4), ("cg", 4), ("direct", 0)]:
