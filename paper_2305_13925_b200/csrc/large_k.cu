@@ -1,0 +1,1163 @@
+// Hand-written tcgen05 chain for K = 256 (complex64, M % 64 == 0): the cfg5
+// shape, where the K x K state does not fit one SM.
+//
+//   lk_gram_kernel  A = H^H H + xi I (gram_regularized, precoder.py:53-61).
+//                   The real Gram U = Z^T Z of Z = sz [Re H, Im H] (M x 512,
+//                   interleaved) in 128 x 128 tiles, upper triangle only
+//                   (10 tiles), two tiles per CTA, five CTAs per realization
+//                   sharing H through L2.  3xFP16: U = Zh^T Zh + Zh^T Zl +
+//                   Zl^T Zh with fp32 accumulation in TMEM.  H arrives by 2-D
+//                   TMA (cp.async.bulk.tensor) in 32-antenna x 128-component
+//                   boxes per needed block; converter warps split each box in
+//                   place into fp16 hi / lo MN-major core-matrix tiles.
+//   lk_pcg_kernel   Jac-PCG / CG (linsolve.py:217-294) on a persistent
+//                   8-CTA thread-block cluster per realization: CTA c owns
+//                   RHS columns [32c, 32c + 32) (the K identity right-hand
+//                   sides are independent columns with their own alpha_j /
+//                   beta_j), keeps P in registers and Q = A''P, R and X in
+//                   TMEM; the 3xFP16 split of the real embedding A''
+//                   (1 MiB: does not fit one SM) is shared by the cluster --
+//                   built once per realization into an L2-resident scratch
+//                   slot (each CTA one eighth) and streamed to all eight
+//                   CTAs' shared memory by TMA multicast (one L2 read per
+//                   cluster), 32 KiB per K-step.  Also returns GX = (A - xi I)X
+//                   and the ||F||^2 partials (precoder.py:64-70, metrics.py:35-44).
+//   lk_w_kernel     W = beta H X (rzf_iterative F = H X, precoder.py:90):
+//                   four CTAs per realization, one per 64-user output block
+//                   (128 output rows, interleaved re / im).  W^T = A Zr^T +
+//                   A2 Zi^T with A = [Re X; Im X]^T rows (hi, lo in TMEM) and
+//                   A2 = [-Im X; Re X]^T rows (hi, lo in shared memory), Z
+//                   de-interleaved into Re / Im K-steps by the converter
+//                   warps; the accumulator (128 rows x 64 antennas) is
+//                   double-buffered in TMEM and drained with 128-B coalesced
+//                   streaming stores.
+//
+// Range: Z's split scale is a power of two from the first non-zero chunk
+// (max |sz Z| in [2^10, 2^11)); a later group that would overflow fp16 flags
+// the realization and a fixup launch redoes it with the exact maximum
+// (lk_zmax_kernel), as in the K = 128 kernels (stream_tc.cu).
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "xl_common.cuh"
+
+namespace xl {
+namespace lk {
+
+#include "tc_ptx.cuh"
+
+constexpr int KU = 256, NC = 2 * KU;
+constexpr float RANGE_MAX = 32768.0f;
+
+// ------------------------------------------------------------ PTX extras ----
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// mbarrier wait with a wall-clock bound (4 s): a protocol bug traps instead of
+// hanging the GPU.  try_wait carries a suspend-time hint, so waiting warps
+// sleep in hardware instead of taking issue slots from the working ones.
+__device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  uint64_t t0 = 0;
+  for (uint32_t it = 0;; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(done)
+        : "r"(su32(bar)), "r"(parity), "r"(0x989680u)
+        : "memory");
+    if (done) return;
+    if ((it & 15u) == 15u) {
+      const uint64_t t = gtimer();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 4000000000ull) asm volatile("trap;");
+    }
+  }
+}
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t nclusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 1-D bulk copy global -> the same smem offset in every CTA of `mask`,
+// completing tx bytes on the mbarrier at the same offset in each
+__device__ __forceinline__ void bulk_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar)), "h"(mask)
+      : "memory");
+}
+// arrive on the mbarrier at this offset in every CTA of `mask` when this
+// thread's prior tcgen05 operations complete
+__device__ __forceinline__ void commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          su32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_alloc512(uint32_t* slot) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(slot)));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_free512(uint32_t t) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(t));
+}
+// split 8 floats (scaled) into one 16-B hi and one 16-B lo core-matrix row
+__device__ __forceinline__ void split8(const float* v, float s, uint4& hi, uint4& lo) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) split2(v[2 * i] * s, v[2 * i + 1] * s, h[i], l[i]);
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+// ----------------------------------------------------------------- zmax ----
+// sz[b] = 2^e with max |sz H_b| in [2^10, 2^11), for flagged realizations
+__global__ void __launch_bounds__(512) lk_zmax_kernel(const float4* __restrict__ H, int64_t per4,
+                                                      float* __restrict__ sz, const int* __restrict__ only) {
+  const int64_t b = blockIdx.x;
+  if (only[b] == 0) return;
+  const float4* h = H + b * per4;
+  float m = 0.0f;
+  for (int64_t i = threadIdx.x; i < per4; i += 512) {
+    const float4 v = __ldcs(h + i);
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  __shared__ float red[16];
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = red[0];
+    for (int w = 1; w < 16; ++w) t = fmaxf(t, red[w]);
+    sz[b] = pow2_scale(t, 11);
+  }
+}
+
+// ================================================================= Gram =====
+namespace gram {
+constexpr int CH = 32;                 // antennas per chunk
+constexpr int BLK = 128;               // components per block (64 users)
+constexpr int SLOT = CH * BLK * 4;     // 16 KiB: one block of one chunk
+constexpr int NSLOT = 3;
+constexpr int SB = NSLOT * SLOT;       // 48 KiB per stage
+constexpr int NS = 4;
+constexpr int GRP = 8 * BLK * 4;       // 4 KiB: 8 antennas of a block (raw) == hi 2 KiB + lo 2 KiB
+constexpr int NCONV = 8;
+constexpr int W_PROD = 0, W_MMA = 1, W_CONV0 = 2;
+constexpr int NT = 32 * (W_CONV0 + NCONV);
+constexpr int TPR = 5;                 // CTAs per realization
+constexpr int SMALL = 1024;
+constexpr int SMEM = NS * SB + SMALL;
+static_assert(SMEM <= 227 * 1024, "lk gram smem");
+constexpr uint32_t ID = idesc(128, 128, 1, 1);
+constexpr int BAR_CONV = 1;
+
+struct Small {
+  uint64_t full[NS], conv[NS], freed[NS];
+  uint64_t done;
+  uint32_t tmem_slot;
+  float rmax[NCONV];
+};
+static_assert(sizeof(Small) <= SMALL, "gram small");
+
+// tile pairs of CTA t: blocks loaded (slots), and per tile (A slot, B slot, I, J)
+struct Plan {
+  int nb, blk[3];
+  int as[2], bs[2], I[2], J[2];
+};
+__constant__ Plan c_plan[TPR] = {
+    {2, {0, 1, 0}, {0, 0}, {0, 1}, {0, 0}, {0, 1}},
+    {3, {0, 2, 3}, {0, 0}, {1, 2}, {0, 0}, {2, 3}},
+    {2, {1, 2, 0}, {0, 0}, {0, 1}, {1, 1}, {1, 2}},
+    {3, {1, 2, 3}, {0, 1}, {2, 1}, {1, 2}, {3, 2}},
+    {2, {2, 3, 0}, {0, 1}, {1, 1}, {2, 3}, {3, 3}},
+};
+
+__global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ CUtensorMap hmap, int M,
+                                                        float* __restrict__ szv, float2* __restrict__ A, double xi,
+                                                        const double* __restrict__ xi_b, int* __restrict__ rflag,
+                                                        int fixup) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* ring = smem;
+  Small* sm = reinterpret_cast<Small*>(smem + NS * SB);
+  const int64_t b = blockIdx.x / TPR;
+  const int t = blockIdx.x % TPR;
+  if (fixup && rflag[b] == 0) return;
+  const Plan pl = c_plan[t];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nch = M / CH;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm->full[s], 1);
+      mbar_init(&sm->conv[s], NCONV);
+      mbar_init(&sm->freed[s], 1);
+    }
+    mbar_init(&sm->done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == W_MMA) tmem_alloc512(&sm->tmem_slot);
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = sm->tmem_slot;
+
+  if (warp == W_PROD) {
+    if (lane == 0) {
+      const int y0 = (int)(b * M);
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % NS;
+        if (c >= NS) bwait(&sm->freed[s], ((c / NS) - 1) & 1);
+        mbar_expect_tx(&sm->full[s], pl.nb * SLOT);
+        for (int j = 0; j < pl.nb; ++j) tma2d(ring + s * SB + j * SLOT, &hmap, BLK * pl.blk[j], y0 + c * CH, &sm->full[s]);
+      }
+    }
+  } else if (warp == W_MMA) {
+    if (lane == 0) {
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % NS;
+        bwait(&sm->conv[s], (c / NS) & 1);
+        tc_after();
+        const uint32_t st = su32(ring + s * SB);
+#pragma unroll
+        for (int ks = 0; ks < CH / 16; ++ks) {
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const uint32_t ab = st + pl.as[k] * SLOT + 2 * ks * GRP, bb = st + pl.bs[k] * SLOT + 2 * ks * GRP;
+            const uint64_t ah = sdesc(ab, GRP, 128), al = sdesc(ab + GRP / 2, GRP, 128);
+            const uint64_t bh = sdesc(bb, GRP, 128), bl = sdesc(bb + GRP / 2, GRP, 128);
+            const uint32_t d = tmem + 128 * k;
+            mma(d, ah, bh, ID, (c | ks) != 0);
+            mma(d, ah, bl, ID, 1);
+            mma(d, al, bh, ID, 1);
+          }
+        }
+        commit(&sm->freed[s]);
+      }
+      commit(&sm->done);
+    }
+  } else {
+    const int cw = warp - W_CONV0;
+    float sz = fixup ? szv[b] : 1.0f;
+    bool have = fixup != 0, over = false;
+    const int ntask = 4 * pl.nb;
+    const int r8 = lane & 7, h4 = lane >> 3;
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % NS;
+      bwait(&sm->full[s], (c / NS) & 1);
+      float v[2][32];
+      float gm = 0.0f;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int task = cw + 8 * u;
+        if (task < ntask) {
+          const uint8_t* gb = ring + s * SB + (task >> 2) * SLOT + (task & 3) * GRP;
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {  // octet (4 it + (h4 + r8) % 4) of row r8: 2-way bank conflicts at most
+            const int o = 4 * it + ((h4 + r8) & 3);
+            const float4 a = *reinterpret_cast<const float4*>(gb + r8 * (BLK * 4) + o * 32);
+            const float4 bq = *reinterpret_cast<const float4*>(gb + r8 * (BLK * 4) + o * 32 + 16);
+            v[u][8 * it + 0] = a.x; v[u][8 * it + 1] = a.y; v[u][8 * it + 2] = a.z; v[u][8 * it + 3] = a.w;
+            v[u][8 * it + 4] = bq.x; v[u][8 * it + 5] = bq.y; v[u][8 * it + 6] = bq.z; v[u][8 * it + 7] = bq.w;
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) gm = fmaxf(gm, fabsf(v[u][i]));
+        }
+      }
+      gm = warp_max(gm);
+      if (!have) {  // until the first non-zero chunk: max over the converter warps
+        if (lane == 0) sm->rmax[cw] = gm;
+        named_sync(BAR_CONV, 32 * NCONV);
+        float mx = sm->rmax[0];
+#pragma unroll
+        for (int w = 1; w < NCONV; ++w) mx = fmaxf(mx, sm->rmax[w]);
+        named_sync(BAR_CONV, 32 * NCONV);
+        if (mx > 0.0f) {
+          sz = pow2_scale(mx, 11);
+          have = true;
+        }
+      }
+      over |= !(gm * sz < RANGE_MAX);  // also catches inf / NaN
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int task = cw + 8 * u;
+        if (task < ntask) {
+          uint8_t* gb = ring + s * SB + (task >> 2) * SLOT + (task & 3) * GRP;
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int o = 4 * it + ((h4 + r8) & 3);
+            uint4 hi, lo;
+            split8(&v[u][8 * it], sz, hi, lo);
+            *reinterpret_cast<uint4*>(gb + o * 128 + r8 * 16) = hi;
+            *reinterpret_cast<uint4*>(gb + GRP / 2 + o * 128 + r8 * 16) = lo;
+          }
+        }
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm->conv[s]);
+    }
+    if (!fixup && over && lane == 0) rflag[b] = 1;
+    // ---- epilogue: tile k = (I, J), lanes = rows 128 I + r, columns 128 J + c;
+    // lane pairs (2i, 2i+1) form the complex entries (re = U[2i][2j] +
+    // U[2i+1][2j+1], im = U[2i][2j+1] - U[2i+1][2j]); the upper triangle is
+    // written with its conjugate mirror: Hermitian by construction.
+    bwait(&sm->done, 0);
+    tc_after();
+    const int q = warp & 3, p = cw >> 2;
+    const int r = 32 * q + lane;
+    const float isz = 1.0f / sz;
+    const double xi_v = xi_b ? xi_b[b] : xi;
+    const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+    const bool odd = lane & 1;
+    float2* Ab = A + b * (int64_t)KU * KU;
+#pragma unroll 1
+    for (int k = 0; k < 2; ++k) {
+      const int I = pl.I[k], J = pl.J[k];
+      const int i = 64 * I + (r >> 1);
+#pragma unroll 1
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        float v[16];
+        tmem_ld16(tl + 128 * k + 64 * p + c0, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+          const float g0 = v[e] * isz * isz, g1 = v[e + 1] * isz * isz;
+          const float p0 = __shfl_xor_sync(0xffffffffu, g0, 1), p1 = __shfl_xor_sync(0xffffffffu, g1, 1);
+          float re = odd ? (p0 + g1) : (g0 + p1);
+          const float im = odd ? (p1 - g0) : (g1 - p0);
+          const int j = 64 * J + ((64 * p + c0 + e) >> 1);
+          if (i == j) {
+            if (!odd) Ab[(int64_t)i * KU + j] = make_float2((float)((double)re + xi_v), 0.0f);
+          } else if (i < j) {
+            if (!odd) Ab[(int64_t)i * KU + j] = make_float2(re, im);
+            else Ab[(int64_t)j * KU + i] = make_float2(re, -im);
+          }
+        }
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  if (warp == W_MMA) {
+    tc_after();
+    tmem_free512(tmem);
+  }
+}
+}  // namespace gram
+
+// =================================================================== W ======
+namespace wk {
+constexpr int CHA = 64;                  // antennas per box (MMA N)
+constexpr int BU = 32;                   // users per box (64 components)
+constexpr int BOX = CHA * 2 * BU * 4;    // 16 KiB
+constexpr int NS = 4;
+constexpr int A2SZ = 128 * KU * 2;       // one fp16 copy of a 128 x 256 K-major operand (64 KiB)
+constexpr int OFF_A2H = 0, OFF_A2L = A2SZ, OFF_RING = 2 * A2SZ;
+constexpr int SBOA = KU * 16;            // K-major 8-row group stride (4 KiB)
+constexpr int NCONV = 8;
+constexpr int W_PROD = 0, W_MMA = 1, W_CONV0 = 2;
+constexpr int NT = 32 * (W_CONV0 + NCONV);
+constexpr int TPR = KU / 64;             // CTAs per realization (64 users each)
+constexpr int SMALL = 2048;
+constexpr int SMEM = OFF_RING + NS * BOX + SMALL;
+static_assert(SMEM <= 227 * 1024, "lk W smem");
+constexpr uint32_t T_AH = 0, T_AL = 128, T_ACC = 256;
+constexpr uint32_t ID = idesc(128, CHA, 0, 0);
+constexpr int BAR_CONV = 1;
+
+struct Small {
+  uint64_t full[NS], conv[NS], freed[NS];
+  uint64_t acc_full[2], acc_free[2];
+  uint64_t cp_done;
+  uint32_t tmem_slot;
+  float rmax[4][64];
+  float sx[64];
+  float cmax[NCONV];
+};
+static_assert(sizeof(Small) <= SMALL, "W small");
+
+// A-operand rows of output block t (rows 2j', 2j'+1 = Re / Im of user
+// 64 t + j'); K = input user i.  A (Re-H K-steps): (Re X_ij, Im X_ij);
+// A2 (Im-H K-steps): (-Im X_ij, Re X_ij); row j' scaled by sx[j'].
+// Writes the K-major hi / lo core-matrix rows of A (a2 == false) or A2.
+__device__ __forceinline__ void build_rows(const float2* __restrict__ Xb, int t, const float* sx, uint8_t* dh,
+                                           uint8_t* dl, bool a2) {
+  for (int task = threadIdx.x; task < 128 * (KU / 8); task += NT) {
+    const int r = task & 127, o = task >> 7;  // row, K-octet
+    const int jl = r >> 1;
+    const bool odd = r & 1;
+    const float s = sx[jl];
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float2 x = __ldg(Xb + (int64_t)(8 * o + e) * KU + 64 * t + jl);
+      v[e] = a2 ? (odd ? x.x : -x.y) : (odd ? x.y : x.x);
+    }
+    uint4 hi, lo;
+    split8(v, s, hi, lo);
+    const int off = (r >> 3) * SBOA + o * 128 + (r & 7) * 16;
+    *reinterpret_cast<uint4*>(dh + off) = hi;
+    *reinterpret_cast<uint4*>(dl + off) = lo;
+  }
+}
+
+__global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUtensorMap hmap, int M,
+                                                     float* __restrict__ szv, const float2* __restrict__ X,
+                                                     const double* __restrict__ beta, float* __restrict__ W,
+                                                     float* __restrict__ F, int* __restrict__ rflag, int fixup) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* a2h = smem + OFF_A2H;
+  uint8_t* a2l = smem + OFF_A2L;
+  uint8_t* ring = smem + OFF_RING;
+  Small* sm = reinterpret_cast<Small*>(smem + OFF_RING + NS * BOX);
+  const int64_t b = blockIdx.x / TPR;
+  const int t = blockIdx.x % TPR;
+  if (fixup && rflag[b] == 0) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ntile = M / CHA, nbox = ntile * (KU / BU);
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm->full[s], 1);
+      mbar_init(&sm->conv[s], NCONV);
+      mbar_init(&sm->freed[s], 1);
+    }
+    for (int j = 0; j < 2; ++j) {
+      mbar_init(&sm->acc_full[j], 1);
+      mbar_init(&sm->acc_free[j], 32 * NCONV);
+    }
+    mbar_init(&sm->cp_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == W_MMA) tmem_alloc512(&sm->tmem_slot);
+  const float2* Xb = X + b * (int64_t)KU * KU;
+  // ---- per-user scale sx[j'] = 2^e, max |X_:j'| sx < 2^14
+  if (tid < 256) {
+    const int jl = tid & 63, part = tid >> 6;
+    float m = 0.0f;
+#pragma unroll 8
+    for (int i = 64 * part; i < 64 * part + 64; ++i) {
+      const float2 x = __ldg(Xb + (int64_t)i * KU + 64 * t + jl);
+      m = fmaxf(m, fmaxf(fabsf(x.x), fabsf(x.y)));
+    }
+    sm->rmax[part][jl] = m;
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (tid < 64)
+    sm->sx[tid] = pow2_scale(fmaxf(fmaxf(sm->rmax[0][tid], sm->rmax[1][tid]), fmaxf(sm->rmax[2][tid], sm->rmax[3][tid])), 14);
+  __syncthreads();
+  const uint32_t tmem = sm->tmem_slot;
+  // ---- A (hi in the ring, lo in the A2-lo region) -> TMEM; then A2 -> smem
+  build_rows(Xb, t, sm->sx, ring, a2l, false);
+  fence_async_smem();
+  __syncthreads();
+  if (tid == 32 * W_MMA) {
+    tc_after();
+    const uint32_t uh = su32(ring), ul = su32(a2l);
+#pragma unroll
+    for (int s = 0; s < KU / 16; ++s) {
+      tmem_cp(tmem + T_AH + 8 * s, sdesc(uh + 2 * s * 128, 128, SBOA));
+      tmem_cp(tmem + T_AL + 8 * s, sdesc(ul + 2 * s * 128, 128, SBOA));
+    }
+    commit(&sm->cp_done);
+  }
+  bwait(&sm->cp_done, 0);
+  tc_after();
+  build_rows(Xb, t, sm->sx, a2h, a2l, true);
+  fence_async_smem();
+  __syncthreads();
+
+  if (warp == W_PROD) {
+    if (lane == 0) {
+      const int y0 = (int)(b * M);
+      for (int g = 0; g < nbox; ++g) {
+        const int s = g % NS, tt = g / (KU / BU), kb = g % (KU / BU);
+        if (g >= NS) bwait(&sm->freed[s], ((g / NS) - 1) & 1);
+        mbar_expect_tx(&sm->full[s], BOX);
+        tma2d(ring + s * BOX, &hmap, 2 * BU * kb, y0 + CHA * tt, &sm->full[s]);
+      }
+    }
+  } else if (warp == W_MMA) {
+    if (lane == 0) {
+      const uint32_t ua2h = su32(a2h), ua2l = su32(a2l);
+      for (int g = 0; g < nbox; ++g) {
+        const int s = g % NS, tt = g / (KU / BU), kb = g % (KU / BU);
+        if (kb == 0 && tt >= 2) bwait(&sm->acc_free[tt & 1], ((tt >> 1) - 1) & 1);
+        bwait(&sm->conv[s], (g / NS) & 1);
+        tc_after();
+        const uint32_t st = su32(ring + s * BOX);
+        const uint32_t d = tmem + T_ACC + CHA * (tt & 1);
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {  // Re-H K-steps: A from TMEM
+          const int sk = 2 * kb + ks;       // K-step over input users
+          const uint64_t bh = sdesc(st + 256 * ks, 128, 2048), bl = sdesc(st + 1024 + 256 * ks, 128, 2048);
+          mma_ts(d, tmem + T_AH + 8 * sk, bh, ID, (kb | ks) != 0);
+          mma_ts(d, tmem + T_AH + 8 * sk, bl, ID, 1);
+          mma_ts(d, tmem + T_AL + 8 * sk, bh, ID, 1);
+        }
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {  // Im-H K-steps: A2 from smem
+          const int sk = 2 * kb + ks;
+          const uint64_t bh = sdesc(st + 512 + 256 * ks, 128, 2048), bl = sdesc(st + 1536 + 256 * ks, 128, 2048);
+          const uint64_t ah = sdesc(ua2h + 2 * sk * 128, 128, SBOA), al = sdesc(ua2l + 2 * sk * 128, 128, SBOA);
+          mma(d, ah, bh, ID, 1);
+          mma(d, ah, bl, ID, 1);
+          mma(d, al, bh, ID, 1);
+        }
+        commit(&sm->freed[s]);
+        if (kb == KU / BU - 1) commit(&sm->acc_full[tt & 1]);
+      }
+    }
+  } else {
+    const int cw = warp - W_CONV0;
+    float sz = fixup ? szv[b] : 1.0f;
+    bool have = fixup != 0, over = false;
+    const int r8 = lane & 7, h4 = lane >> 3;
+    const int q = warp & 3, p = cw >> 2;
+    const int r = 32 * q + lane;  // output row (TMEM lane)
+    const int col = 128 * t + r;  // output component
+    const double bt = beta[b];
+    const float srow = sm->sx[r >> 1];
+    const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16) + T_ACC + 32 * p;
+    // the scale is final from the first non-zero box on; tiles before it are all zero
+    auto drain = [&](int tt) {
+      const float wmul = (float)(bt / ((double)srow * (double)sz));
+      const float fmul = 1.0f / (srow * sz);
+      const int jb = tt & 1;
+      bwait(&sm->acc_full[jb], (tt >> 1) & 1);
+      tc_after();
+      float v[32];
+      tmem_ld16(tq + CHA * jb, v);
+      tmem_ld16(tq + CHA * jb + 16, v + 16);
+      tmem_wait_ld();
+      tc_before();
+      mbar_arrive(&sm->acc_free[jb]);
+      const int64_t n0 = (int64_t)tt * CHA + 32 * p;
+      float* wp = W + (b * (int64_t)M + n0) * NC + col;
+#pragma unroll
+      for (int n = 0; n < 32; ++n) __stcs(wp + (int64_t)n * NC, v[n] * wmul);
+      if (F) {
+        float* fp = F + (b * (int64_t)M + n0) * NC + col;
+#pragma unroll
+        for (int n = 0; n < 32; ++n) __stcs(fp + (int64_t)n * NC, v[n] * fmul);
+      }
+    };
+    for (int g = 0; g < nbox; ++g) {
+      const int s = g % NS, tt = g / (KU / BU), kb = g % (KU / BU);
+      bwait(&sm->full[s], (g / NS) & 1);
+      uint8_t* gb = ring + s * BOX + cw * 2048;  // 8 antennas x 64 components
+      float v[16];
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {  // users 8 h4 .. 8 h4 + 7 of row r8 (2-way conflicts at most)
+        const int f = (it + r8) & 3;
+        const float4 a = *reinterpret_cast<const float4*>(gb + r8 * 256 + 64 * h4 + 16 * f);
+        v[4 * f + 0] = a.x; v[4 * f + 1] = a.y; v[4 * f + 2] = a.z; v[4 * f + 3] = a.w;
+      }
+      float gm = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) gm = fmaxf(gm, fabsf(v[i]));
+      gm = warp_max(gm);
+      if (!have) {
+        if (lane == 0) sm->cmax[cw] = gm;
+        named_sync(BAR_CONV, 32 * NCONV);
+        float mx = sm->cmax[0];
+#pragma unroll
+        for (int w = 1; w < NCONV; ++w) mx = fmaxf(mx, sm->cmax[w]);
+        named_sync(BAR_CONV, 32 * NCONV);
+        if (mx > 0.0f) {
+          sz = pow2_scale(mx, 11);
+          have = true;
+        }
+      }
+      over |= !(gm * sz < RANGE_MAX);
+      __syncwarp();
+      float re[8], im[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        re[e] = v[2 * e];
+        im[e] = v[2 * e + 1];
+      }
+      uint4 hr, lr, hi_, li_;
+      split8(re, sz, hr, lr);
+      split8(im, sz, hi_, li_);
+      *reinterpret_cast<uint4*>(gb + 128 * h4 + 16 * r8) = hr;
+      *reinterpret_cast<uint4*>(gb + 1024 + 128 * h4 + 16 * r8) = lr;
+      *reinterpret_cast<uint4*>(gb + 128 * (4 + h4) + 16 * r8) = hi_;
+      *reinterpret_cast<uint4*>(gb + 1024 + 128 * (4 + h4) + 16 * r8) = li_;
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm->conv[s]);
+      if (kb == 0 && tt >= 1) drain(tt - 1);
+    }
+    drain(ntile - 1);
+    if (!fixup && over && lane == 0) rflag[b] = 1;
+  }
+  tc_before();
+  __syncthreads();
+  if (warp == W_MMA) {
+    tc_after();
+    tmem_free512(tmem);
+  }
+}
+}  // namespace wk
+
+// ======================================================== cluster Jac-PCG ===
+namespace pc {
+constexpr int C = 8;                     // CTAs per cluster
+constexpr int JN = KU / C;               // RHS columns per CTA
+constexpr int NMATH = 512;               // 16 warps: M-tile m = w >> 2, lane quadrant q = w & 3
+constexpr int NT = NMATH;
+constexpr int CHUNK = 32768;             // one K-step of A'': 512 rows x 16 K, hi + lo
+constexpr int NCH = NC / 16;             // K-steps per product
+constexpr int NS = 4;
+constexpr int LBOB = JN * 16;            // MN-major B tile: 8-K-row group stride
+constexpr int PART = (NC / 8) * LBOB;    // one B tile (hi or lo): 32 KiB
+constexpr int OFF_B = NS * CHUNK;
+constexpr int OFF_SMALL = OFF_B + 2 * PART;
+constexpr uint32_t T_Q = 0, T_R = 128, T_X = 256;
+constexpr uint32_t ID = idesc(128, JN, 0, 1);
+constexpr int BAR_MATH = 1;
+constexpr size_t SLOT_BYTES = (size_t)NCH * CHUNK;  // 1 MiB of A'' per cluster
+
+struct Small {
+  uint64_t full[NS], empty[NS], q_full;
+  uint32_t tmem_slot;
+  int zero_diag, not_hpd;
+  float red[16][JN];
+  alignas(16) float coef[2][JN];
+  alignas(16) float spx[JN];
+  alignas(16) float spy[JN];
+  float rzs[JN];
+  float cdg[KU];
+  float dmax[16];
+  double dred[16];
+};
+constexpr int SMEM = OFF_SMALL + (int)sizeof(Small);
+static_assert(SMEM <= 227 * 1024, "lk pcg smem");
+
+struct Params {
+  const float2* A;  // [B][K][K] regularized Gram (Hermitian, xi on the diagonal)
+  int64_t B;
+  int T, method, variant;
+  double xi;
+  const double* xi_b;
+  float2* X;        // [B][K][K]
+  float2* GX;       // [B][K][K]
+  double* part;     // [B][C] Re tr(X^H GX) per CTA
+  int32_t* status;  // [B]
+  uint8_t* scratch; // [clusters][1 MiB] A'' split, K-step chunks
+};
+
+__device__ __forceinline__ void lds8(const float* a, float (&o)[8]) {
+  const float4 x = reinterpret_cast<const float4*>(a)[0], y = reinterpret_cast<const float4*>(a)[1];
+  o[0] = x.x; o[1] = x.y; o[2] = x.z; o[3] = x.w; o[4] = y.x; o[5] = y.y; o[6] = y.z; o[7] = y.w;
+}
+// per-thread column values -> red[warp][lane] (warp transpose-reduce)
+template <bool MAX = false>
+__device__ __forceinline__ void col_partials(float (&v)[JN], Small* sm, int warp) {
+  const float t = warp_transpose_reduce<JN, MAX>(v);
+  sm->red[warp][threadIdx.x & 31] = t;
+}
+// CTA total of column j over the 16 math warps in a fixed order
+template <bool MAX = false>
+__device__ __forceinline__ float col_total(const Small* sm, int j) {
+  float s = sm->red[0][j];
+#pragma unroll
+  for (int w = 1; w < 16; ++w) s = MAX ? fmaxf(s, sm->red[w][j]) : s + sm->red[w][j];
+  return s;
+}
+
+__global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* ring = smem;
+  uint8_t* pb = smem + OFF_B;
+  Small* sm = reinterpret_cast<Small*>(smem + OFF_SMALL);
+  const uint32_t rank = cluster_rank();
+  const uint32_t cid = cluster_id_x(), ncl = nclusters_x();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = (warp >> 2) & 3, q = warp & 3;
+  const int rg = 128 * m + 32 * q + lane;     // component row
+  const int kr = rg >> 1;                     // user of the row
+  const bool use_c = p.method == XL_JACPCG;
+  const bool textbook = use_c && p.variant == XL_TEXTBOOK;
+  uint8_t* slot = p.scratch + (size_t)cid * SLOT_BYTES;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm->full[s], 1);
+      mbar_init(&sm->empty[s], C);
+    }
+    mbar_init(&sm->q_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc512(&sm->tmem_slot);
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = sm->tmem_slot;
+  const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+  const uint32_t tQ = tl + T_Q + JN * m, tR = tl + T_R + JN * m, tX = tl + T_X + JN * m;
+  const uint32_t upb = su32(pb);
+  uint32_t g_prod = 0, g_cons = 0, nq = 0;  // ring chunks produced / consumed, products
+  // thread 0 streams A'': chunk n of the realization's (T + 1) x 32 K-steps into
+  // the ring (stage g % NS, all eight CTAs), armed in every CTA, copied by its
+  // owner CTA (n % 8) with one multicast once every CTA has freed the stage
+  int n_issued = 0, n_total = 0;
+  const uint8_t* cur_slot = nullptr;
+  auto issue_next = [&]() {
+    if (n_issued >= n_total) return;
+    const int s = g_prod % NS, k = n_issued % NCH;
+    if (g_prod >= NS) bwait(&sm->empty[s], ((g_prod / NS) - 1) & 1);
+    mbar_expect_tx(&sm->full[s], CHUNK);
+    if ((k & (C - 1)) == (int)rank) bulk_mc(ring + s * CHUNK, cur_slot + (size_t)k * CHUNK, CHUNK, &sm->full[s], 0xFF);
+    ++g_prod;
+    ++n_issued;
+  };
+
+  for (int64_t b = cid; b < p.B; b += ncl) {
+    const float2* a = p.A + b * (int64_t)KU * KU;
+    cluster_sync();  // the previous realization's A'' chunks are consumed in every CTA
+    // ---- scale: diag(A'') = sa diag(A) < 2^14; zero diagonal -> Splitting (linsolve.py:205-208)
+    if (tid < KU) sm->cdg[tid] = a[(int64_t)tid * KU + tid].x;
+    if (tid == 0) sm->not_hpd = 0;
+    __syncthreads();
+    if (warp < KU / 32) {
+      const float d = sm->cdg[tid];
+      const float mx = warp_max(fabsf(d));
+      const unsigned z = __ballot_sync(0xffffffffu, use_c && d == 0.0f);
+      if (lane == 0) {
+        sm->dmax[warp] = mx;
+        sm->dmax[8 + warp] = z ? 1.0f : 0.0f;
+      }
+    }
+    __syncthreads();
+    float dmax = sm->dmax[0], zsum = sm->dmax[8];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      dmax = fmaxf(dmax, sm->dmax[w]);
+      zsum += sm->dmax[8 + w];
+    }
+    const float sa = pow2_scale(dmax, 14);
+    // ---- this CTA's eighth of A'' (K components [64 rank, 64 rank + 64)) ->
+    // the cluster's scratch slot as K-major core-matrix chunks; row 2i =
+    // (Re a_ij, -Im a_ij), row 2i+1 = (Im a_ij, Re a_ij), a_ij = conj(A[j][i])
+    for (int task = tid; task < NC * 8; task += NT) {
+      const int r = task & (NC - 1), o = task >> 9;
+      const int i = r >> 1;
+      const bool odd = r & 1;
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = 32 * (int)rank + 4 * o + u;
+        const float2 x = __ldg(a + (int64_t)j * KU + i);  // a_ji: Re a_ij = x.x, Im a_ij = -x.y
+        v[2 * u] = odd ? -x.y : x.x;
+        v[2 * u + 1] = odd ? x.x : x.y;
+      }
+      uint4 hi, lo;
+      split8(v, sa, hi, lo);
+      const int s = 4 * (int)rank + (o >> 1), kg = o & 1;
+      uint8_t* dst = slot + (size_t)s * CHUNK + (r >> 7) * 4096 + ((r & 127) >> 3) * 256 + kg * 128 + (r & 7) * 16;
+      *reinterpret_cast<uint4*>(dst) = hi;
+      *reinterpret_cast<uint4*>(dst + CHUNK / 2) = lo;
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    cluster_sync();  // the whole A'' is in the slot
+
+    if (tid == 0) {
+      n_issued = 0;
+      n_total = (p.T + 1) * NCH;
+      cur_slot = slot;
+      for (int i = 0; i < NS; ++i) issue_next();
+    }
+
+    const float cr = use_c ? sm->cdg[kr] * sa : 1.0f;
+    const float icr = 1.0f / cr;
+    const double alpha = p.xi_b ? p.xi_b[b] : p.xi;
+    // ---- initial state (linsolve.py:224-229, 264-268): x = 0, r = I (Algorithm 1:
+    // C^-1 I), m = z, rz per column
+    float P[JN], A[JN];
+#pragma unroll
+    for (int c0 = 0; c0 < JN; c0 += 8) {
+      float rv[8], zx[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int jg = JN * (int)rank + c0 + i;
+        const float e = (rg == 2 * jg) ? 1.0f : 0.0f;
+        rv[i] = (use_c && !textbook) ? e * icr : e;
+        P[c0 + i] = textbook ? e * icr : rv[i];
+        zx[i] = 0.0f;
+      }
+      tmem_st8(tR + c0, rv);
+      tmem_st8(tX + c0, zx);
+    }
+    if (tid < JN) {
+      const float c0 = use_c ? sm->cdg[JN * rank + tid] * sa : 1.0f;
+      const float ic = 1.0f / c0;
+      sm->rzs[tid] = textbook ? ic : (use_c ? ic * ic : 1.0f);
+    }
+    tmem_wait_st();
+
+    // column max over the CTA -> spx / spy (power-of-two scale of the fp16 split, < 2^14)
+    auto scale = [&](float (&v)[JN]) {
+#pragma unroll
+      for (int jj = 0; jj < JN; ++jj) A[jj] = fabsf(v[jj]);
+      col_partials<true>(A, sm, warp);
+      named_sync(BAR_MATH, NMATH);
+      if (tid < JN) {
+        const float s = pow2_scale(col_total<true>(sm, tid), 14);
+        sm->spx[tid] = s;
+        sm->spy[tid] = 1.0f / s;
+      }
+      named_sync(BAR_MATH, NMATH);
+    };
+    // Q = A'' v (v scaled per column): B tile written by all, MMAs issued by thread 0
+    auto product = [&](const float (&v)[JN]) {
+#pragma unroll
+      for (int g = 0; g < JN / 8; ++g) {
+        float sv[8], w8[8];
+        lds8(sm->spx + 8 * g, sv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w8[i] = v[8 * g + i];
+        uint4 hi, lo;
+        uint32_t h[4], l[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) split2(w8[2 * i] * sv[2 * i], w8[2 * i + 1] * sv[2 * i + 1], h[i], l[i]);
+        hi = make_uint4(h[0], h[1], h[2], h[3]);
+        lo = make_uint4(l[0], l[1], l[2], l[3]);
+        const int o = (rg >> 3) * LBOB + g * 128 + (rg & 7) * 16;
+        *reinterpret_cast<uint4*>(pb + o) = hi;
+        *reinterpret_cast<uint4*>(pb + PART + o) = lo;
+      }
+      fence_async_smem();
+      tc_before();
+      named_sync(BAR_MATH, NMATH);
+      if (warp == 0) {  // lanes 1..31 wait at __syncwarp, not in a divergent spin beside the issuer
+        if (lane == 0) {
+        tc_after();
+        for (int k = 0; k < NCH; ++k, ++g_cons) {
+          const int s = g_cons % NS;
+          bwait(&sm->full[s], (g_cons / NS) & 1);
+          tc_after();
+          const uint32_t st = su32(ring + s * CHUNK);
+          const uint64_t bh = sdesc(upb + 2 * k * LBOB, LBOB, 128), bl = sdesc(upb + PART + 2 * k * LBOB, LBOB, 128);
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt) {
+            const uint64_t ah = sdesc(st + 4096 * mt, 128, 256), al = sdesc(st + CHUNK / 2 + 4096 * mt, 128, 256);
+            const uint32_t d = tmem + T_Q + JN * mt;
+            mma(d, ah, bh, ID, k != 0);
+            mma(d, ah, bl, ID, 1);
+            mma(d, al, bh, ID, 1);
+          }
+          commit_mc(&sm->empty[s], 0xFF);
+          // refill the stage of the previous K-step (its MMAs are likely done)
+          if (k >= 1) issue_next();
+        }
+        commit(&sm->q_full);
+        issue_next();  // NS K-steps of the next product in flight during the SIMT phase
+        }
+        __syncwarp();
+      }
+      if (tid != 0) g_cons += NCH;
+      bwait(&sm->q_full, nq & 1);
+      ++nq;
+      tc_after();
+    };
+
+    for (int t = 1; t <= p.T; ++t) {
+      scale(P);
+      product(P);
+      const float qs = (use_c && !textbook) ? icr : 1.0f;  // Algorithm 1: z = C^-1 P m
+      tmem_ld<JN>(tQ, A);
+      tmem_wait_ld();
+      // curvature m^H z per column (linsolve.py:276)
+#pragma unroll
+      for (int c0 = 0; c0 < JN; c0 += 8) {
+        float sy[8];
+        lds8(sm->spy + c0, sy);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) A[c0 + i] = P[c0 + i] * ((A[c0 + i] * sy[i]) * qs);
+      }
+      col_partials(A, sm, warp);
+      named_sync(BAR_MATH, NMATH);
+      if (tid < JN) {  // alpha_j, NotHpd (linsolve.py:277-280)
+        const float curv = col_total(sm, tid);
+        const float rzj = sm->rzs[tid];
+        const bool act = rzj > 0.0f;
+        if (curv <= 0.0f && act) sm->not_hpd = 1;
+        sm->coef[0][tid] = act ? rzj / (curv > 0.0f ? curv : 1.0f) : 0.0f;
+      }
+      named_sync(BAR_MATH, NMATH);
+      // w += alpha m, r -= alpha Pm, rz partials (linsolve.py:281-284)
+#pragma unroll
+      for (int c0 = 0; c0 < JN; c0 += 8) {
+        float qv[8], rv[8], xv[8], al8[8], sy[8];
+        tmem_ld8(tQ + c0, qv);
+        tmem_ld8(tR + c0, rv);
+        tmem_ld8(tX + c0, xv);
+        lds8(sm->coef[0] + c0, al8);
+        lds8(sm->spy + c0, sy);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float al = al8[i];
+          xv[i] = xv[i] + al * P[c0 + i];
+          rv[i] = rv[i] - al * ((qv[i] * sy[i]) * qs);
+          const float z = textbook ? rv[i] * icr : rv[i];
+          A[c0 + i] = rv[i] * z;
+        }
+        tmem_st8(tR + c0, rv);
+        tmem_st8(tX + c0, xv);
+      }
+      col_partials(A, sm, warp);
+      tmem_wait_st();
+      named_sync(BAR_MATH, NMATH);
+      if (tid < JN) {  // beta_j, rz update (linsolve.py:284-288)
+        const float rn = col_total(sm, tid);
+        const float rzj = sm->rzs[tid];
+        sm->coef[1][tid] = rzj > 0.0f ? rn / rzj : 0.0f;
+        sm->rzs[tid] = rn;
+      }
+      named_sync(BAR_MATH, NMATH);
+      // m = z + beta m
+#pragma unroll
+      for (int c0 = 0; c0 < JN; c0 += 8) {
+        float rv[8], be8[8];
+        tmem_ld8(tR + c0, rv);
+        lds8(sm->coef[1] + c0, be8);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float z = textbook ? rv[i] * icr : rv[i];
+          P[c0 + i] = z + be8[i] * P[c0 + i];
+        }
+      }
+    }
+
+    // ---- GX = A X - xi X from Q = A'' X'' (X = sa X'')
+    tmem_ld<JN>(tX, P);
+    tmem_wait_ld();
+    scale(P);
+    product(P);
+    tmem_ld<JN>(tQ, A);
+    tmem_wait_ld();
+    double fro = 0.0;
+    const double xsa = alpha * (double)sa;
+#pragma unroll
+    for (int c0 = 0; c0 < JN; c0 += 8) {
+      float sy[8];
+      lds8(sm->spy + c0, sy);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float g = (float)((double)(A[c0 + i] * sy[i]) - xsa * (double)P[c0 + i]);
+        A[c0 + i] = g;
+        fro += (double)(P[c0 + i] * sa) * (double)g;  // Re tr(X^H GX)
+      }
+    }
+    // row-major complex outputs: lanes (2m, 2m+1) hold (Re, Im) of user kr;
+    // the even lane stores column pairs 4n, 4n+1 and the odd lane 4n+2, 4n+3
+    const bool odd = lane & 1;
+    float2* xo = p.X + b * (int64_t)KU * KU + (int64_t)kr * KU + JN * rank;
+    float2* go = p.GX + b * (int64_t)KU * KU + (int64_t)kr * KU + JN * rank;
+#pragma unroll
+    for (int jp = 0; jp < JN; jp += 2) {
+      const float x0 = P[jp] * sa, x1 = P[jp + 1] * sa, g0 = A[jp], g1 = A[jp + 1];
+      const float ox0 = __shfl_xor_sync(0xffffffffu, x0, 1), ox1 = __shfl_xor_sync(0xffffffffu, x1, 1);
+      const float og0 = __shfl_xor_sync(0xffffffffu, g0, 1), og1 = __shfl_xor_sync(0xffffffffu, g1, 1);
+      if (((jp >> 1) & 1) == (odd ? 1 : 0)) {
+        const float4 xv = odd ? make_float4(ox0, x0, ox1, x1) : make_float4(x0, ox0, x1, ox1);
+        const float4 gv = odd ? make_float4(og0, g0, og1, g1) : make_float4(g0, og0, g1, og1);
+        *reinterpret_cast<float4*>(xo + jp) = xv;
+        *reinterpret_cast<float4*>(go + jp) = gv;
+      }
+    }
+    fro = warp_sum(fro);
+    if (lane == 0) sm->dred[warp] = fro;
+    named_sync(BAR_MATH, NMATH);
+    if (tid == 0) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < 16; ++w) s += sm->dred[w];
+      p.part[C * b + rank] = s;
+      if (zsum > 0.0f) {
+        if (rank == 0) p.status[b] = XL_STATUS_SPLITTING;
+      } else if (sm->not_hpd) {
+        atomicCAS(reinterpret_cast<int*>(p.status + b), 0, XL_STATUS_NOT_HPD);
+      }
+    }
+  }
+  tc_before();
+  cluster_sync();  // no multicast may target an exited CTA
+  if (warp == 0) {
+    tc_after();
+    tmem_free512(tmem);
+  }
+}
+}  // namespace pc
+
+// ------------------------------------------------------------------ host ----
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiled encoder() {
+  static EncodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiled)p;
+  }
+  return fn;
+}
+
+// H[B][M][K] complex64 as a 2-D fp32 tensor [B M rows][2K floats], box {bx, by}
+static int make_hmap(CUtensorMap* map, const void* H, int64_t B, int M, int bx, int by) {
+  EncodeTiled enc = encoder();
+  if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return XL_ERR_CUDA; }
+  const cuuint64_t dims[2] = {(cuuint64_t)NC, (cuuint64_t)(B * M)};
+  const cuuint64_t strides[1] = {(cuuint64_t)NC * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)bx, (cuuint32_t)by};
+  const cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(H), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("tensor map encode failed (%d)", (int)r); return XL_ERR_CUDA; }
+  return XL_SUCCESS;
+}
+
+}  // namespace lk
+
+bool lk_supported(int dtype, int M, int K) {
+  if (dtype != XL_C64 || K != lk::KU || M < 64 || M % 64 != 0) return false;
+  const char* e = getenv("XL_LARGE_K_256");  // "library": the split-operand library GEMM path (A/B, tests)
+  return !(e && e[0] == 'l');
+}
+
+static int lk_clusters() {
+  static int n = 0;
+  if (n == 0) {
+    cudaFuncSetAttribute(lk::pc::lk_pcg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lk::pc::SMEM);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(lk::pc::C * 16, 1, 1);
+    cfg.blockDim = dim3(lk::pc::NT, 1, 1);
+    cfg.dynamicSmemBytes = lk::pc::SMEM;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = lk::pc::C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, lk::pc::lk_pcg_kernel, &cfg) != cudaSuccess || c < 1) {
+      cudaGetLastError();
+      c = 16;
+    }
+    n = c;
+  }
+  return n;
+}
+
+// scratch: sz[B] floats, range flags[B] ints (Gram), the same for W, and the
+// cluster solver's A'' slots
+size_t lk_ws_bytes(int64_t B) {
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  return 4 * al((size_t)B * 4) + (size_t)32 * lk::pc::SLOT_BYTES;
+}
+
+int lk_gram(const void* H, int64_t B, int M, double xi, const double* xi_b, void* A, void* ws, cudaStream_t st) {
+  using namespace lk;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  float* sz = (float*)ws;
+  int* rflag = (int*)((char*)ws + al((size_t)B * 4));
+  CUtensorMap map;
+  if (int e = make_hmap(&map, H, B, M, gram::BLK, gram::CH)) return e;
+  if (cudaMemsetAsync(rflag, 0, (size_t)B * sizeof(int), st) != cudaSuccess) return check_launch("lk flags");
+  cudaFuncSetAttribute(gram::lk_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gram::SMEM);
+  gram::lk_gram_kernel<<<(unsigned)(gram::TPR * B), gram::NT, gram::SMEM, st>>>(map, M, sz, (float2*)A, xi, xi_b,
+                                                                               rflag, 0);
+  if (int e = check_launch("lk gram")) return e;
+  lk_zmax_kernel<<<(unsigned)B, 512, 0, st>>>((const float4*)H, (int64_t)M * NC / 4, sz, rflag);
+  if (int e = check_launch("lk zmax")) return e;
+  gram::lk_gram_kernel<<<(unsigned)(gram::TPR * B), gram::NT, gram::SMEM, st>>>(map, M, sz, (float2*)A, xi, xi_b,
+                                                                               rflag, 1);
+  return check_launch("lk gram fixup");
+}
+
+int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi, const double* xi_b, void* X,
+             void* GX, double* part, int32_t* status, void* ws, cudaStream_t st) {
+  using namespace lk;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  uint8_t* scratch = (uint8_t*)ws + 4 * al((size_t)B * 4);
+  int ncl = lk_clusters();
+  if (ncl > 32) ncl = 32;
+  if (ncl > B) ncl = (int)B;
+  pc::Params p{(const float2*)A, B, T, method, variant, xi, xi_b, (float2*)X, (float2*)GX, part, status, scratch};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(pc::C * ncl), 1, 1);
+  cfg.blockDim = dim3(pc::NT, 1, 1);
+  cfg.dynamicSmemBytes = pc::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = pc::C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaFuncSetAttribute(pc::lk_pcg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pc::SMEM);
+  if (cudaLaunchKernelEx(&cfg, pc::lk_pcg_kernel, p) != cudaSuccess) return check_launch("lk pcg launch");
+  return check_launch("lk pcg");
+}
+
+int lk_apply(const void* H, const void* X, const double* beta, int64_t B, int M, void* W, void* F, void* ws,
+             cudaStream_t st) {
+  using namespace lk;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  float* sz = (float*)((char*)ws + 2 * al((size_t)B * 4));
+  int* rflag = (int*)((char*)ws + 3 * al((size_t)B * 4));
+  CUtensorMap map;
+  if (int e = make_hmap(&map, H, B, M, 2 * wk::BU, wk::CHA)) return e;
+  if (cudaMemsetAsync(rflag, 0, (size_t)B * sizeof(int), st) != cudaSuccess) return check_launch("lk w flags");
+  cudaFuncSetAttribute(wk::lk_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wk::SMEM);
+  wk::lk_w_kernel<<<(unsigned)(wk::TPR * B), wk::NT, wk::SMEM, st>>>(map, M, sz, (const float2*)X, beta, (float*)W,
+                                                                     (float*)F, rflag, 0);
+  if (int e = check_launch("lk w")) return e;
+  lk_zmax_kernel<<<(unsigned)B, 512, 0, st>>>((const float4*)H, (int64_t)M * NC / 4, sz, rflag);
+  if (int e = check_launch("lk w zmax")) return e;
+  wk::lk_w_kernel<<<(unsigned)(wk::TPR * B), wk::NT, wk::SMEM, st>>>(map, M, sz, (const float2*)X, beta, (float*)W,
+                                                                     (float*)F, rflag, 1);
+  return check_launch("lk w fixup");
+}
+
+}  // namespace xl

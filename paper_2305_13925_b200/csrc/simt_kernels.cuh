@@ -75,6 +75,15 @@ int cpcg_solve(int method, int variant, const void* A, int64_t B, int K, int T, 
 int tc_pcg(int method, int variant, const void* A, int64_t B, int K, int T, void* X, int32_t* status, void* cws,
            void* bufs, cudaStream_t st);
 
+// large_k.cu: K = 256 complex64 -- streaming tcgen05 Gram / W and the 8-CTA cluster Jac-PCG
+bool lk_supported(int dtype, int M, int K);
+size_t lk_ws_bytes(int64_t B);
+int lk_gram(const void* H, int64_t B, int M, double xi, const double* xi_b, void* A, void* ws, cudaStream_t st);
+int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi, const double* xi_b, void* X,
+             void* GX, double* part, int32_t* status, void* ws, cudaStream_t st);
+int lk_apply(const void* H, const void* X, const double* beta, int64_t B, int M, void* W, void* F, void* ws,
+             cudaStream_t st);
+
 int launch_ber(int dtype, const void* Bc, const int8_t* bits, const void* noise, int64_t B, int K,
                int nsym, int64_t* errors, cudaStream_t st);
 

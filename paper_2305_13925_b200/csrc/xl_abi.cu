@@ -73,6 +73,8 @@ const char* xl_last_error(void) { return g_err; }
 
 int xl_rzf_uses_tensor_cores(int dtype, int method, int32_t M, int32_t K) {
   if (fused_supported(dtype, method, M, K)) return 1;
+  // K = 256: streaming tcgen05 Gram / W + the 8-CTA cluster Jac-PCG / CG
+  if (method != XL_DIRECT && lk_supported(dtype, M, K)) return 1;
   // K = 128: streaming tcgen05 Gram / W + the cluster Jac-PCG / CG
   return (method != XL_DIRECT && stc_supported(dtype, M, K) && cpcg_supported(K)) ? 1 : 0;
 }
@@ -166,6 +168,7 @@ static size_t tc_region(int dtype, int64_t B, int M, int K) {
 
 static size_t general_ws(int dtype, int64_t B, int M, int K) {
   size_t w = simt_rzf_ws(dtype, B, M, K);
+  if (lk_supported(dtype, M, K)) return w + align_up(lk_ws_bytes(B));
   if (tc_general_supported(dtype, M, K)) {
     if (stc_supported(dtype, M, K)) w += 2 * align_up((size_t)B * 4);  // sz[B], range flags[B]
     w += align_up(tc_region(dtype, B, M, K));
@@ -194,7 +197,8 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
                          double xi, const double* xi_per_batch, double power, int32_t T, double sigma2, void* W,
                          void* F, double* beta, double* gamma, double* sum_se, void* X, int32_t* status,
                          void* workspace, cudaStream_t st) {
-  const bool tc = tc_general_supported(dtype, M, K);
+  const bool lkp = lk_supported(dtype, M, K);
+  const bool tc = !lkp && tc_general_supported(dtype, M, K);
   const size_t cs = csize(dtype), kk = (size_t)B * K * K * cs;
   char* p = (char*)workspace;
   void* A = p; p += align_up(kk);
@@ -219,7 +223,9 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   int e;
   const int64_t Bc = tc ? tc_chunk_size(dtype, B, M, K) : B;
   const int64_t oH = (int64_t)M * K * (int64_t)cs, oK = (int64_t)K * K * (int64_t)cs;
-  if (sc) {  // streaming tcgen05 Gram, A emitted from TMEM
+  if (lkp) {  // K = 256: upper-triangular tcgen05 tiles, A emitted from TMEM
+    if ((e = lk_gram(H, B, M, xi, xi_per_batch, A, tcws, st))) return e;
+  } else if (sc) {  // streaming tcgen05 Gram, A emitted from TMEM
     if ((e = stc_gram(H, B, M, K, xi, xi_per_batch, szb, A, rflag, st))) return e;
   } else if (tc) {
     for (int64_t b0 = 0; b0 < B; b0 += Bc) {
@@ -234,6 +240,7 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   // W = beta H X on the tensor cores, per sub-batch (the split rows are rebuilt:
   // the Gram sub-batches have overwritten them)
   auto tc_w = [&]() -> int {
+    if (lkp) return lk_apply(H, Xo, beta, B, M, W, F, tcws, st);
     if (sc) return stc_apply(H, Xo, beta, szb, B, M, K, W, F, st);
     for (int64_t b0 = 0; b0 < B; b0 += Bc) {
       const int64_t nb = B - b0 < Bc ? B - b0 : Bc;
@@ -245,13 +252,16 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   };
   // K = 128 (complex64): the fused 2-CTA-cluster solver keeps the PCG state on
   // chip and also returns GX and the ||F||^2 partials (cluster_pcg.cu)
+  const bool lks = lkp && method != XL_DIRECT;
   const bool cpc = tc && dtype == XL_C64 && method != XL_DIRECT && cpcg_supported(K);
   const bool tcp = tc && dtype == XL_C64 && method != XL_DIRECT && !cpc && tc_pcg_supported(K);
   const bool tcp64 = tc && dtype == XL_C128 && method != XL_DIRECT && tc_pcg64_supported(K);
   const int64_t sH = (int64_t)M * K, sK = (int64_t)K * K;
   const int np = gemm_tiles(K, K);
   void* GX = sw;  // the solver workspace is free again (>= B K K)
-  if (cpc) {
+  if (lks) {
+    if ((e = lk_solve(method, variant, A, B, T, xi, xi_per_batch, Xo, GX, part, status, tcws, st))) return e;
+  } else if (cpc) {
     if ((e = cpcg_solve(method, variant, A, B, K, T, xi, xi_per_batch, Xo, GX, part, status, st))) return e;
   } else if (tcp) {
     if ((e = tc_pcg(method, variant, A, B, K, T, Xo, status, tcws, pcgws, st))) return e;
@@ -266,7 +276,9 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   // W = beta H X in one pass and B = H^H W = beta GX (metrics.py:35-44):
   // 8 K^3 instead of 8 M K^2 flops for the coupling, no separate F pass.
   if (dtype == XL_C64) {
-    if (cpc) {
+    if (lks) {
+      if ((e = launch_beta_from_partials(B, part, 8, power, beta, status, st))) return e;
+    } else if (cpc) {
       if ((e = launch_beta_from_partials(B, part, 2, power, beta, status, st))) return e;
     } else if (tcp) {  // GX and the ||F||^2 partials on the tensor cores from the PCG state
       if ((e = tc_gx(xi_per_batch, xi, B, K, GX, part, tcws, pcgws, st))) return e;
@@ -276,7 +288,7 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
       if ((e = launch_cgemm<float>(false, EPI_GXF, A, sK, K, Xo, sK, K, GX, sK, K, B, K, K, K, xi_per_batch, xi, part, st))) return e;
       if ((e = launch_beta_from_partials(B, part, np, power, beta, status, st))) return e;
     }
-    if (tc) {
+    if (tc || lkp) {
       if ((e = tc_w())) return e;
     } else {
       if ((e = launch_cgemm<float>(false, EPI_BSCALE, H, sH, K, Xo, sK, K, W, sH, K, B, M, K, K, beta, 0, nullptr, st))) return e;

@@ -1,0 +1,166 @@
+"""K = 256 complex64 (cfg5 shape) on the hand-written tcgen05 chain of
+large_k.cu: streaming upper-triangular Gram tiles, the 8-CTA cluster
+Jac-PCG / CG sharing the split A'' by TMA multicast, and the W kernel with the
+X operand in TMEM / shared memory -- against the complex128 oracle
+(linsolve.py:217-294, precoder.py:53-91) and against the split-operand
+library-GEMM path it replaces (XL_LARGE_K_256=library).
+
+Tolerances (north_star): W relative Frobenius <= 1e-4, sum-SE <= 1e-4;
+Algorithm 1 (which diverges) within 10x an independent complex64
+execution of the same recurrence.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import xlmimo_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+import paper_2305_13925_b200 as X  # noqa: E402
+from paper_2305_13925_b200 import _lib as L  # noqa: E402
+from paper_2305_13925_b200 import batched as BT  # noqa: E402
+from fp32_ref import _fp32_sensitivity  # noqa: E402
+
+DEV = "cuda"
+K = 256
+
+
+def relf(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def _run_env(env, fn):
+    old = {k: os.environ.get(k) for k in env}
+    try:
+        for k, v in env.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+        out = fn()
+        torch.cuda.synchronize()
+        return out
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _lib_calls_in(fn):
+    """Names of the kernels launched are not visible from Python; the launch
+    counter at least proves the calls went through our library."""
+    n0 = L.lib().xl_launch_count()
+    out = fn()
+    torch.cuda.synchronize()
+    return out, int(L.lib().xl_launch_count() - n0)
+
+
+def test_k256_uses_hand_written_chain():
+    assert X.uses_tensor_cores(torch.complex64, "jacpcg", 2048, K)
+    assert X.uses_tensor_cores(torch.complex64, "cg", 2048, K)
+    assert not X.uses_tensor_cores(torch.complex64, "jacpcg", 2000, K)
+
+
+# Algorithm 1 diverges on the ill-conditioned cfg5 channel: by
+# T = 5-6 its residual grows ~1e8x and a complex64 execution (numpy included)
+# meets nonpositive curvature -> NotHpdError; it is compared at T = 3, where
+# it still runs in complex64, within 10x an independent numpy complex64 run
+# (the divergent recurrence amplifies the ~2^-22 3xFP16 product error as well)
+@pytest.mark.parametrize("method,variant,T", [("jacpcg", "textbook", 6), ("cg", "textbook", 6),
+                                              ("jacpcg", "algorithm", 3)])
+def test_k256_vs_oracle_cfg5_channel(method, variant, T):
+    wl = X.CONFIGS["cfg5"]
+    H = X.generate_channels(wl.model, seed=0, first=100, B=12, dtype=torch.complex64)
+    out, n = _lib_calls_in(lambda: BT.rzf_batched(H, wl.alpha(), wl.power(), method=method, T=T,
+                                                  variant=variant, want_X=True))
+    assert n >= 3
+    Hq = H.cpu().numpy().astype(np.complex128)
+    for b in range(H.shape[0]):
+        Gr, br, _, s = O.precoder_and_se(Hq[b], wl.alpha(), wl.power(), 1.0, method, T, variant)
+        e, es = relf(out.W[b].cpu().numpy(), Gr), abs(out.sum_se[b].item() - s) / abs(s)
+        if variant == "algorithm":
+            fw, fs = _fp32_sensitivity(Hq[b], wl.alpha(), wl.power(), method, T, variant)
+            assert e <= max(1e-4, 10 * fw) and es <= max(1e-4, 10 * fs, e), (b, e, fw, es, fs)
+        else:
+            assert e <= 1e-4 and es <= 1e-4, (b, e, es)
+            assert abs(out.beta[b].item() - br) <= 1e-4 * br
+
+
+def test_k256_matches_library_path_and_outputs():
+    """Against the split-operand library GEMMs: W, F, X, beta, gamma."""
+    rng = np.random.default_rng(5)
+    B, M = 5, 512
+    Hn = (rng.standard_normal((B, M, K)) + 1j * rng.standard_normal((B, M, K))) / np.sqrt(2)
+    Hn *= 10.0 ** rng.uniform(-2, 1, size=(B, 1, K))  # 60 dB of user gain spread
+    Hn[1] *= 1e-6                                      # tiny realization
+    Hn[2, 256:] *= 300.0                               # later antennas overflow the first chunk's scale: fixup
+    Hn[3, :96] = 0.0                                   # leading zero chunks
+    H = torch.from_numpy(Hn.astype(np.complex64)).to(DEV)
+    xi = torch.from_numpy(rng.uniform(0.05, 2.0, size=B) * np.abs(Hn).mean(axis=(1, 2)) ** 2 * M).to(DEV)
+    f = lambda: BT.rzf_batched(H, xi, 10.0, method="jacpcg", T=6, want_F=True, want_X=True)  # noqa: E731
+    s = _run_env({"XL_LARGE_K_256": None}, f)
+    lib = _run_env({"XL_LARGE_K_256": "library"}, f)
+    Hq = H.cpu().numpy().astype(np.complex128)
+    for b in range(B):
+        Gr, br, gr, se = O.precoder_and_se(Hq[b], float(xi[b]), 10.0, 1.0, "jacpcg", 6, "textbook")
+        Ws, Wl = s.W[b].cpu().numpy(), lib.W[b].cpu().numpy()
+        assert relf(Ws, Gr) <= 1e-4, (b, relf(Ws, Gr))
+        assert relf(Ws, Wl) <= 2e-5, (b, relf(Ws, Wl))
+        assert relf(s.F[b].cpu().numpy(), Gr / br) <= 1e-4
+        assert relf(s.X[b].cpu().numpy(), lib.X[b].cpu().numpy()) <= 2e-5
+        assert abs(s.beta[b].item() - br) <= 1e-4 * br
+        assert abs(s.sum_se[b].item() - se) <= 1e-4 * abs(se)
+        # gamma from B = beta (A - xi I) X (8 K^3 flops): a 60 dB weaker user's
+        # (A - xi I) X diagonal cancels in fp32, so its tiny gamma is held to the
+        # scale of the strongest user's
+        np.testing.assert_allclose(s.gamma[b].cpu().numpy(), gr, rtol=2e-4, atol=1e-5 * gr.max())
+
+
+@pytest.mark.parametrize("B,M,T", [(1, 64, 1), (3, 128, 2), (37, 64, 6), (300, 64, 3)])
+def test_k256_edge_shapes(B, M, T):
+    """One 64-antenna tile, T = 1, a single realization, and batches past the
+    number of resident clusters (the persistent solver loops)."""
+    g = torch.Generator(device=DEV).manual_seed(B + M + T)
+    H = torch.complex(torch.randn(B, M, K, device=DEV, generator=g),
+                      torch.randn(B, M, K, device=DEV, generator=g)) * 0.7
+    H = H.to(torch.complex64)
+    xi = K / 10.0
+    out = BT.rzf_batched(H, xi, 10.0, method="jacpcg", T=T, variant="textbook")
+    assert (out.status.cpu().numpy() == 0).all()
+    Hq = H.cpu().numpy().astype(np.complex128)
+    for b in sorted({0, B // 2, B - 1}):
+        Gr, br, gr, s = O.precoder_and_se(Hq[b], xi, 10.0, 1.0, "jacpcg", T, "textbook")
+        assert relf(out.W[b].cpu().numpy(), Gr) <= 1e-4, (B, M, T, b)
+        assert abs(out.sum_se[b].item() - s) <= 1e-4 * abs(s)
+
+
+def test_k256_deterministic():
+    wl = X.CONFIGS["cfg5"]
+    H = X.generate_channels(wl.model, seed=0, first=7, B=40, dtype=torch.complex64)
+    o1 = BT.rzf_batched(H, wl.alpha(), wl.power(), T=6, want_X=True)
+    o2 = BT.rzf_batched(H, wl.alpha(), wl.power(), T=6, want_X=True)
+    assert torch.equal(o1.W, o2.W) and torch.equal(o1.X, o2.X) and torch.equal(o1.sum_se, o2.sum_se)
+    # batch independence: a realization's result does not depend on its neighbours
+    o3 = BT.rzf_batched(H[5:6].contiguous(), wl.alpha(), wl.power(), T=6)
+    assert relf(o3.W[0].cpu().numpy(), o1.W[5].cpu().numpy()) <= 1e-6
+
+
+@pytest.mark.parametrize("method", ["jacpcg", "cg"])
+def test_k256_silent_user(method):
+    """A user nobody hears (all-zero channel column): its row / column of A is
+    xi e_k, a valid HPD system; both recurrences still match the oracle."""
+    wl = X.CONFIGS["cfg5"]
+    H = X.generate_channels(wl.model, seed=0, first=3, B=2, dtype=torch.complex64)
+    H[0, :, 17] = 0
+    out = BT.rzf_batched(H, wl.alpha(), wl.power(), method=method, T=6)
+    Hq = H.cpu().numpy().astype(np.complex128)
+    for b in range(2):
+        Gr, _, _, s = O.precoder_and_se(Hq[b], wl.alpha(), wl.power(), 1.0, method, 6, "textbook")
+        assert relf(out.W[b].cpu().numpy(), Gr) <= 1e-4
+        assert abs(out.sum_se[b].item() - s) <= 1e-4 * abs(s)
