@@ -163,13 +163,12 @@ __global__ void __launch_bounds__(512) lk_zmax_kernel(const float4* __restrict__
 
 // ================================================================= Gram =====
 namespace gram {
-constexpr int CH = 32;                 // antennas per chunk
+constexpr int CH = 32;                 // antennas per chunk (4 groups of 8)
 constexpr int BLK = 128;               // components per block (64 users)
-constexpr int SLOT = CH * BLK * 4;     // 16 KiB: one block of one chunk
-constexpr int NSLOT = 3;
-constexpr int SB = NSLOT * SLOT;       // 48 KiB per stage
+constexpr int SGL = CH * BLK * 4;      // 16 KiB: one block of one chunk
+constexpr int PAIR = 2 * SGL;          // 32 KiB: two adjacent blocks
+constexpr int SB = PAIR + SGL;         // 48 KiB per stage (at most a pair and a single)
 constexpr int NS = 4;
-constexpr int GRP = 8 * BLK * 4;       // 4 KiB: 8 antennas of a block (raw) == hi 2 KiB + lo 2 KiB
 constexpr int NCONV = 8;
 constexpr int W_PROD = 0, W_MMA = 1, W_CONV0 = 2;
 constexpr int NT = 32 * (W_CONV0 + NCONV);
@@ -177,8 +176,7 @@ constexpr int TPR = 5;                 // CTAs per realization
 constexpr int SMALL = 1024;
 constexpr int SMEM = NS * SB + SMALL;
 static_assert(SMEM <= 227 * 1024, "lk gram smem");
-constexpr uint32_t ID = idesc(128, 128, 1, 1);
-constexpr int BAR_CONV = 1;
+constexpr int BAR_CONV = 1;            // 2..5: converter warp pairs of a pair group
 
 struct Small {
   uint64_t full[NS], conv[NS], freed[NS];
@@ -188,20 +186,67 @@ struct Small {
 };
 static_assert(sizeof(Small) <= SMALL, "gram small");
 
-// tile pairs of CTA t: blocks loaded (slots), and per tile (A slot, B slot, I, J)
+// CTA t of a realization: a pair slot (blocks pb, pb + 1: one 256-component
+// box per chunk) and / or single slots (one 128-component box each), and its
+// two 128 x 128 output tiles (I_k, J_k) at TMEM columns 128 k.  The MMA is
+// N = 256 over the pair (A = its first block, or a single) where the two
+// tiles share a row block, else two N = 128 products.
 struct Plan {
-  int nb, blk[3];
-  int as[2], bs[2], I[2], J[2];
+  int pb;          // pair's first block, -1: none
+  int ns, sb[2];   // singles
+  int a_single;    // A operand: -1 = the pair's first block, else single index
+  int I[2], J[2];
 };
 __constant__ Plan c_plan[TPR] = {
-    {2, {0, 1, 0}, {0, 0}, {0, 1}, {0, 0}, {0, 1}},
-    {3, {0, 2, 3}, {0, 0}, {1, 2}, {0, 0}, {2, 3}},
-    {2, {1, 2, 0}, {0, 0}, {0, 1}, {1, 1}, {1, 2}},
-    {3, {1, 2, 3}, {0, 1}, {2, 1}, {1, 2}, {3, 2}},
-    {2, {2, 3, 0}, {0, 1}, {1, 1}, {2, 3}, {3, 3}},
+    {0, 0, {0, 0}, -1, {0, 0}, {0, 1}},
+    {2, 1, {0, 0}, 0, {0, 0}, {2, 3}},
+    {1, 0, {0, 0}, -1, {1, 1}, {1, 2}},
+    {2, 0, {0, 0}, -1, {2, 2}, {2, 3}},
+    {-1, 2, {1, 3}, 0, {1, 3}, {3, 3}},
 };
 
-__global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ CUtensorMap hmap, int M,
+// Conflict-free lane -> (row, component) map of a raw 8-antenna group with
+// rows of 4 * NCR bytes (stc::coords): float4 reads and 8-B core-matrix
+// writes hit distinct banks.
+__device__ __forceinline__ void coords(int lane, int it, int& row, int& cc) {
+  const int cs = it >> 1, ih = it & 1;
+  row = (lane >> 1) & 7;
+  const int hb16 = lane & 1, j = (row + 2 * (lane >> 4) + ih) & 3;
+  cc = 32 * cs + 8 * j + 4 * hb16;
+}
+// load 8 float4 (iterations it0 .. it0 + 7) of a group with row stride rs bytes
+__device__ __forceinline__ float load8(const uint8_t* gb, int rs, int lane, int it0, float4 (&v)[8]) {
+  float mx = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int row, cc;
+    coords(lane, it0 + i, row, cc);
+    v[i] = *reinterpret_cast<const float4*>(gb + row * rs + cc * 4);
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
+  }
+  return mx;
+}
+// split in place: hi core matrices at gb (core matrix cc >> 3 at 128 B), lo at gb + lo_off
+__device__ __forceinline__ void store8(uint8_t* gb, int lo_off, int lane, int it0, const float4 (&v)[8], float sz) {
+  const float2 s2 = make_float2(sz, sz);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int row, cc;
+    coords(lane, it0 + i, row, cc);
+    const float2 a = __fmul2_rn(make_float2(v[i].x, v[i].y), s2);
+    const float2 bq = __fmul2_rn(make_float2(v[i].z, v[i].w), s2);
+    const __half2 ha = __float22half2_rn(a), hb = __float22half2_rn(bq);
+    const float2 ra = __fadd2_rn(a, make_float2(-__low2float(ha), -__high2float(ha)));
+    const float2 rb = __fadd2_rn(bq, make_float2(-__low2float(hb), -__high2float(hb)));
+    const __half2 la = __float22half2_rn(ra), lb = __float22half2_rn(rb);
+    const int off = (cc >> 3) * 128 + row * 16 + (cc & 7) * 2;
+    *reinterpret_cast<uint2*>(gb + off) = make_uint2(h2u(ha), h2u(hb));
+    *reinterpret_cast<uint2*>(gb + lo_off + off) = make_uint2(h2u(la), h2u(lb));
+  }
+}
+
+__global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ CUtensorMap pmap,
+                                                        const __grid_constant__ CUtensorMap smap, int M,
                                                         float* __restrict__ szv, float2* __restrict__ A, double xi,
                                                         const double* __restrict__ xi_b, int* __restrict__ rflag,
                                                         int fixup) {
@@ -214,6 +259,9 @@ __global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ 
   const Plan pl = c_plan[t];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nch = M / CH;
+  const bool hp = pl.pb >= 0;
+  const int soff = hp ? PAIR : 0;  // singles follow the pair in a stage
+  const int stage_bytes = (hp ? PAIR : 0) + pl.ns * SGL;
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sm->full[s], 1);
@@ -235,12 +283,15 @@ __global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ 
       for (int c = 0; c < nch; ++c) {
         const int s = c % NS;
         if (c >= NS) bwait(&sm->freed[s], ((c / NS) - 1) & 1);
-        mbar_expect_tx(&sm->full[s], pl.nb * SLOT);
-        for (int j = 0; j < pl.nb; ++j) tma2d(ring + s * SB + j * SLOT, &hmap, BLK * pl.blk[j], y0 + c * CH, &sm->full[s]);
+        mbar_expect_tx(&sm->full[s], stage_bytes);
+        uint8_t* st = ring + s * SB;
+        if (hp) tma2d(st, &pmap, BLK * pl.pb, y0 + c * CH, &sm->full[s]);
+        for (int j = 0; j < pl.ns; ++j) tma2d(st + soff + j * SGL, &smap, BLK * pl.sb[j], y0 + c * CH, &sm->full[s]);
       }
     }
   } else if (warp == W_MMA) {
     if (lane == 0) {
+      constexpr int PG = 8 * 2 * BLK * 4, SG = 8 * BLK * 4;  // group strides (8 KiB pair, 4 KiB single)
       for (int c = 0; c < nch; ++c) {
         const int s = c % NS;
         bwait(&sm->conv[s], (c / NS) & 1);
@@ -248,15 +299,34 @@ __global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ 
         const uint32_t st = su32(ring + s * SB);
 #pragma unroll
         for (int ks = 0; ks < CH / 16; ++ks) {
-#pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const uint32_t ab = st + pl.as[k] * SLOT + 2 * ks * GRP, bb = st + pl.bs[k] * SLOT + 2 * ks * GRP;
-            const uint64_t ah = sdesc(ab, GRP, 128), al = sdesc(ab + GRP / 2, GRP, 128);
-            const uint64_t bh = sdesc(bb, GRP, 128), bl = sdesc(bb + GRP / 2, GRP, 128);
-            const uint32_t d = tmem + 128 * k;
-            mma(d, ah, bh, ID, (c | ks) != 0);
-            mma(d, ah, bl, ID, 1);
-            mma(d, al, bh, ID, 1);
+          const uint32_t acc = (c | ks) != 0;
+          if (hp) {  // one N = 256 product over the pair
+            const uint32_t pbase = st + 2 * ks * PG;
+            uint64_t ah, al;
+            if (pl.a_single < 0) {
+              ah = sdesc(pbase, PG, 128);
+              al = sdesc(pbase + PG / 2, PG, 128);
+            } else {
+              const uint32_t sbase = st + soff + pl.a_single * SGL + 2 * ks * SG;
+              ah = sdesc(sbase, SG, 128);
+              al = sdesc(sbase + SG / 2, SG, 128);
+            }
+            const uint64_t bh = sdesc(pbase, PG, 128), bl = sdesc(pbase + PG / 2, PG, 128);
+            constexpr uint32_t ID256 = idesc(128, 256, 1, 1);
+            mma(tmem, ah, bh, ID256, acc);
+            mma(tmem, ah, bl, ID256, 1);
+            mma(tmem, al, bh, ID256, 1);
+          } else {  // two N = 128 products on singles: (A = single 0, B = single 1), (single 1, single 1)
+            constexpr uint32_t ID128 = idesc(128, 128, 1, 1);
+            const uint32_t s0 = st + soff + 2 * ks * SG, s1 = s0 + SGL;
+            const uint64_t h0 = sdesc(s0, SG, 128), l0 = sdesc(s0 + SG / 2, SG, 128);
+            const uint64_t h1 = sdesc(s1, SG, 128), l1 = sdesc(s1 + SG / 2, SG, 128);
+            mma(tmem, h0, h1, ID128, acc);
+            mma(tmem, h0, l1, ID128, 1);
+            mma(tmem, l0, h1, ID128, 1);
+            mma(tmem + 128, h1, h1, ID128, acc);
+            mma(tmem + 128, h1, l1, ID128, 1);
+            mma(tmem + 128, l1, h1, ID128, 1);
           }
         }
         commit(&sm->freed[s]);
@@ -267,30 +337,19 @@ __global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ 
     const int cw = warp - W_CONV0;
     float sz = fixup ? szv[b] : 1.0f;
     bool have = fixup != 0, over = false;
-    const int ntask = 4 * pl.nb;
-    const int r8 = lane & 7, h4 = lane >> 3;
     for (int c = 0; c < nch; ++c) {
       const int s = c % NS;
       bwait(&sm->full[s], (c / NS) & 1);
-      float v[2][32];
+      uint8_t* st = ring + s * SB;
+      // pair: warp cw converts half (cw & 1) of group cw >> 1 with its partner
+      // warp; singles: group cw & 3 of single cw >> 2 (CTA 1: warps 0-3, single 0)
+      float4 vp[8], vs[8];
       float gm = 0.0f;
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int task = cw + 8 * u;
-        if (task < ntask) {
-          const uint8_t* gb = ring + s * SB + (task >> 2) * SLOT + (task & 3) * GRP;
-#pragma unroll
-          for (int it = 0; it < 4; ++it) {  // octet (4 it + (h4 + r8) % 4) of row r8: 2-way bank conflicts at most
-            const int o = 4 * it + ((h4 + r8) & 3);
-            const float4 a = *reinterpret_cast<const float4*>(gb + r8 * (BLK * 4) + o * 32);
-            const float4 bq = *reinterpret_cast<const float4*>(gb + r8 * (BLK * 4) + o * 32 + 16);
-            v[u][8 * it + 0] = a.x; v[u][8 * it + 1] = a.y; v[u][8 * it + 2] = a.z; v[u][8 * it + 3] = a.w;
-            v[u][8 * it + 4] = bq.x; v[u][8 * it + 5] = bq.y; v[u][8 * it + 6] = bq.z; v[u][8 * it + 7] = bq.w;
-          }
-#pragma unroll
-          for (int i = 0; i < 32; ++i) gm = fmaxf(gm, fabsf(v[u][i]));
-        }
-      }
+      uint8_t* pg = st + (cw >> 1) * (8 * 2 * BLK * 4);
+      const bool dos = hp ? (pl.ns == 1 && cw < 4) : true;
+      uint8_t* sg = st + soff + (hp ? 0 : (cw >> 2) * SGL) + (cw & 3) * (8 * BLK * 4);
+      if (hp) gm = load8(pg, 2 * BLK * 4, lane, 8 * (cw & 1), vp);
+      if (dos) gm = fmaxf(gm, load8(sg, BLK * 4, lane, 0, vs));
       gm = warp_max(gm);
       if (!have) {  // until the first non-zero chunk: max over the converter warps
         if (lane == 0) sm->rmax[cw] = gm;
@@ -305,22 +364,10 @@ __global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ 
         }
       }
       over |= !(gm * sz < RANGE_MAX);  // also catches inf / NaN
-      __syncwarp();
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int task = cw + 8 * u;
-        if (task < ntask) {
-          uint8_t* gb = ring + s * SB + (task >> 2) * SLOT + (task & 3) * GRP;
-#pragma unroll
-          for (int it = 0; it < 4; ++it) {
-            const int o = 4 * it + ((h4 + r8) & 3);
-            uint4 hi, lo;
-            split8(&v[u][8 * it], sz, hi, lo);
-            *reinterpret_cast<uint4*>(gb + o * 128 + r8 * 16) = hi;
-            *reinterpret_cast<uint4*>(gb + GRP / 2 + o * 128 + r8 * 16) = lo;
-          }
-        }
-      }
+      if (hp) named_sync(2 + (cw >> 1), 64);  // both halves of the pair group are in registers
+      else __syncwarp();
+      if (hp) store8(pg, 8 * 2 * BLK * 2, lane, 8 * (cw & 1), vp, sz);  // lo 4 KiB after hi
+      if (dos) store8(sg, 8 * BLK * 2, lane, 0, vs, sz);                 // lo 2 KiB after hi
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm->conv[s]);
@@ -379,9 +426,8 @@ namespace wk {
 constexpr int CHA = 64;                  // antennas per box (MMA N)
 constexpr int BU = 32;                   // users per box (64 components)
 constexpr int BOX = CHA * 2 * BU * 4;    // 16 KiB
-constexpr int NS = 4;
-constexpr int A2SZ = 128 * KU * 2;       // one fp16 copy of a 128 x 256 K-major operand (64 KiB)
-constexpr int OFF_A2H = 0, OFF_A2L = A2SZ, OFF_RING = 2 * A2SZ;
+constexpr int NS = 10;                   // ring depth (160 KiB in flight)
+constexpr int OFF_RING = 0;
 constexpr int SBOA = KU * 16;            // K-major 8-row group stride (4 KiB)
 constexpr int NCONV = 8;
 constexpr int W_PROD = 0, W_MMA = 1, W_CONV0 = 2;
@@ -390,6 +436,9 @@ constexpr int TPR = KU / 64;             // CTAs per realization (64 users each)
 constexpr int SMALL = 2048;
 constexpr int SMEM = OFF_RING + NS * BOX + SMALL;
 static_assert(SMEM <= 227 * 1024, "lk W smem");
+static_assert(NS * BOX >= 2 * 128 * KU * 2, "A staging fits the ring");
+// TMEM: A hi / lo (the MMA A operand), then per accumulator buffer j
+// D1 = A Zr^T at 256 + 128 j and D2 = A Zi^T at 256 + 128 j + 64
 constexpr uint32_t T_AH = 0, T_AL = 128, T_ACC = 256;
 constexpr uint32_t ID = idesc(128, CHA, 0, 0);
 constexpr int BAR_CONV = 1;
@@ -405,12 +454,13 @@ struct Small {
 };
 static_assert(sizeof(Small) <= SMALL, "W small");
 
-// A-operand rows of output block t (rows 2j', 2j'+1 = Re / Im of user
-// 64 t + j'); K = input user i.  A (Re-H K-steps): (Re X_ij, Im X_ij);
-// A2 (Im-H K-steps): (-Im X_ij, Re X_ij); row j' scaled by sx[j'].
-// Writes the K-major hi / lo core-matrix rows of A (a2 == false) or A2.
+// A-operand rows of output block t: row 2j' = Re X_{i, 64t+j'}, row 2j'+1 =
+// Im X_{i, 64t+j'} over the K = 256 input users i, row j' scaled by sx[j'];
+// K-major hi / lo core-matrix rows.  With D1 = A Zr^T and D2 = A Zi^T the
+// output rows are W^T[2j'] = D1[2j'] - D2[2j'+1] (Re: Re X Re H - Im X Im H)
+// and W^T[2j'+1] = D1[2j'+1] + D2[2j'] (Im: Im X Re H + Re X Im H).
 __device__ __forceinline__ void build_rows(const float2* __restrict__ Xb, int t, const float* sx, uint8_t* dh,
-                                           uint8_t* dl, bool a2) {
+                                           uint8_t* dl) {
   for (int task = threadIdx.x; task < 128 * (KU / 8); task += NT) {
     const int r = task & 127, o = task >> 7;  // row, K-octet
     const int jl = r >> 1;
@@ -420,7 +470,7 @@ __device__ __forceinline__ void build_rows(const float2* __restrict__ Xb, int t,
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const float2 x = __ldg(Xb + (int64_t)(8 * o + e) * KU + 64 * t + jl);
-      v[e] = a2 ? (odd ? x.x : -x.y) : (odd ? x.y : x.x);
+      v[e] = odd ? x.y : x.x;
     }
     uint4 hi, lo;
     split8(v, s, hi, lo);
@@ -435,8 +485,6 @@ __global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUt
                                                      const double* __restrict__ beta, float* __restrict__ W,
                                                      float* __restrict__ F, int* __restrict__ rflag, int fixup) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* a2h = smem + OFF_A2H;
-  uint8_t* a2l = smem + OFF_A2L;
   uint8_t* ring = smem + OFF_RING;
   Small* sm = reinterpret_cast<Small*>(smem + OFF_RING + NS * BOX);
   const int64_t b = blockIdx.x / TPR;
@@ -477,13 +525,13 @@ __global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUt
     sm->sx[tid] = pow2_scale(fmaxf(fmaxf(sm->rmax[0][tid], sm->rmax[1][tid]), fmaxf(sm->rmax[2][tid], sm->rmax[3][tid])), 14);
   __syncthreads();
   const uint32_t tmem = sm->tmem_slot;
-  // ---- A (hi in the ring, lo in the A2-lo region) -> TMEM; then A2 -> smem
-  build_rows(Xb, t, sm->sx, ring, a2l, false);
+  // ---- A hi / lo staged in the (idle) ring -> TMEM
+  build_rows(Xb, t, sm->sx, ring, ring + 128 * KU * 2);
   fence_async_smem();
   __syncthreads();
   if (tid == 32 * W_MMA) {
     tc_after();
-    const uint32_t uh = su32(ring), ul = su32(a2l);
+    const uint32_t uh = su32(ring), ul = su32(ring + 128 * KU * 2);
 #pragma unroll
     for (int s = 0; s < KU / 16; ++s) {
       tmem_cp(tmem + T_AH + 8 * s, sdesc(uh + 2 * s * 128, 128, SBOA));
@@ -493,8 +541,6 @@ __global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUt
   }
   bwait(&sm->cp_done, 0);
   tc_after();
-  build_rows(Xb, t, sm->sx, a2h, a2l, true);
-  fence_async_smem();
   __syncthreads();
 
   if (warp == W_PROD) {
@@ -509,30 +555,26 @@ __global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUt
     }
   } else if (warp == W_MMA) {
     if (lane == 0) {
-      const uint32_t ua2h = su32(a2h), ua2l = su32(a2l);
       for (int g = 0; g < nbox; ++g) {
         const int s = g % NS, tt = g / (KU / BU), kb = g % (KU / BU);
         if (kb == 0 && tt >= 2) bwait(&sm->acc_free[tt & 1], ((tt >> 1) - 1) & 1);
         bwait(&sm->conv[s], (g / NS) & 1);
         tc_after();
         const uint32_t st = su32(ring + s * BOX);
-        const uint32_t d = tmem + T_ACC + CHA * (tt & 1);
+        const uint32_t d1 = tmem + T_ACC + 128 * (tt & 1), d2 = d1 + CHA;
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {  // Re-H K-steps: A from TMEM
-          const int sk = 2 * kb + ks;       // K-step over input users
-          const uint64_t bh = sdesc(st + 256 * ks, 128, 2048), bl = sdesc(st + 1024 + 256 * ks, 128, 2048);
-          mma_ts(d, tmem + T_AH + 8 * sk, bh, ID, (kb | ks) != 0);
-          mma_ts(d, tmem + T_AH + 8 * sk, bl, ID, 1);
-          mma_ts(d, tmem + T_AL + 8 * sk, bh, ID, 1);
-        }
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {  // Im-H K-steps: A2 from smem
-          const int sk = 2 * kb + ks;
-          const uint64_t bh = sdesc(st + 512 + 256 * ks, 128, 2048), bl = sdesc(st + 1536 + 256 * ks, 128, 2048);
-          const uint64_t ah = sdesc(ua2h + 2 * sk * 128, 128, SBOA), al = sdesc(ua2l + 2 * sk * 128, 128, SBOA);
-          mma(d, ah, bh, ID, 1);
-          mma(d, ah, bl, ID, 1);
-          mma(d, al, bh, ID, 1);
+        for (int ks = 0; ks < 2; ++ks) {
+          const int sk = 2 * kb + ks;  // K-step over input users
+          const uint32_t ah = tmem + T_AH + 8 * sk, al = tmem + T_AL + 8 * sk;
+          const uint64_t brh = sdesc(st + 256 * ks, 128, 2048), brl = sdesc(st + 1024 + 256 * ks, 128, 2048);
+          const uint64_t bih = sdesc(st + 512 + 256 * ks, 128, 2048), bil = sdesc(st + 1536 + 256 * ks, 128, 2048);
+          const uint32_t acc = (kb | ks) != 0;
+          mma_ts(d1, ah, brh, ID, acc);
+          mma_ts(d1, ah, brl, ID, 1);
+          mma_ts(d1, al, brh, ID, 1);
+          mma_ts(d2, ah, bih, ID, acc);
+          mma_ts(d2, ah, bil, ID, 1);
+          mma_ts(d2, al, bih, ID, 1);
         }
         commit(&sm->freed[s]);
         if (kb == KU / BU - 1) commit(&sm->acc_full[tt & 1]);
@@ -542,9 +584,10 @@ __global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUt
     const int cw = warp - W_CONV0;
     float sz = fixup ? szv[b] : 1.0f;
     bool have = fixup != 0, over = false;
-    const int r8 = lane & 7, h4 = lane >> 3;
+    const int crow = lane >> 2, pair = lane & 3;  // converter: antenna row of the group, user pair
     const int q = warp & 3, p = cw >> 2;
     const int r = 32 * q + lane;  // output row (TMEM lane)
+    const bool odd = r & 1;
     const int col = 128 * t + r;  // output component
     const double bt = beta[b];
     const float srow = sm->sx[r >> 1];
@@ -556,12 +599,19 @@ __global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUt
       const int jb = tt & 1;
       bwait(&sm->acc_full[jb], (tt >> 1) & 1);
       tc_after();
-      float v[32];
-      tmem_ld16(tq + CHA * jb, v);
-      tmem_ld16(tq + CHA * jb + 16, v + 16);
+      float v[32], u[32];
+      tmem_ld16(tq + 128 * jb, v);
+      tmem_ld16(tq + 128 * jb + 16, v + 16);
+      tmem_ld16(tq + 128 * jb + CHA, u);
+      tmem_ld16(tq + 128 * jb + CHA + 16, u + 16);
       tmem_wait_ld();
       tc_before();
       mbar_arrive(&sm->acc_free[jb]);
+#pragma unroll
+      for (int n = 0; n < 32; ++n) {
+        const float o2 = __shfl_xor_sync(0xffffffffu, u[n], 1);
+        v[n] = odd ? v[n] + o2 : v[n] - o2;
+      }
       const int64_t n0 = (int64_t)tt * CHA + 32 * p;
       float* wp = W + (b * (int64_t)M + n0) * NC + col;
 #pragma unroll
@@ -576,16 +626,18 @@ __global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUt
       const int s = g % NS, tt = g / (KU / BU), kb = g % (KU / BU);
       bwait(&sm->full[s], (g / NS) & 1);
       uint8_t* gb = ring + s * BOX + cw * 2048;  // 8 antennas x 64 components
-      float v[16];
+      // lane (row, pair) reads users 8c + 2 pair, +1 of octet c = (it + row) & 3:
+      // 16-B loads and 4-B stores both bank-conflict free
+      float4 v[4];
 #pragma unroll
-      for (int it = 0; it < 4; ++it) {  // users 8 h4 .. 8 h4 + 7 of row r8 (2-way conflicts at most)
-        const int f = (it + r8) & 3;
-        const float4 a = *reinterpret_cast<const float4*>(gb + r8 * 256 + 64 * h4 + 16 * f);
-        v[4 * f + 0] = a.x; v[4 * f + 1] = a.y; v[4 * f + 2] = a.z; v[4 * f + 3] = a.w;
+      for (int it = 0; it < 4; ++it) {
+        const int c = (it + crow) & 3;
+        v[it] = *reinterpret_cast<const float4*>(gb + crow * 256 + 64 * c + 16 * pair);
       }
       float gm = 0.0f;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) gm = fmaxf(gm, fabsf(v[i]));
+      for (int it = 0; it < 4; ++it)
+        gm = fmaxf(gm, fmaxf(fmaxf(fabsf(v[it].x), fabsf(v[it].y)), fmaxf(fabsf(v[it].z), fabsf(v[it].w))));
       gm = warp_max(gm);
       if (!have) {
         if (lane == 0) sm->cmax[cw] = gm;
@@ -601,19 +653,18 @@ __global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUt
       }
       over |= !(gm * sz < RANGE_MAX);
       __syncwarp();
-      float re[8], im[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        re[e] = v[2 * e];
-        im[e] = v[2 * e + 1];
+      for (int it = 0; it < 4; ++it) {
+        const int c = (it + crow) & 3;
+        uint32_t hr, lr, hi_, li_;
+        split2(v[it].x * sz, v[it].z * sz, hr, lr);   // Re of the user pair
+        split2(v[it].y * sz, v[it].w * sz, hi_, li_); // Im
+        const int o = crow * 16 + 4 * pair;
+        *reinterpret_cast<uint32_t*>(gb + 128 * c + o) = hr;
+        *reinterpret_cast<uint32_t*>(gb + 1024 + 128 * c + o) = lr;
+        *reinterpret_cast<uint32_t*>(gb + 128 * (4 + c) + o) = hi_;
+        *reinterpret_cast<uint32_t*>(gb + 1024 + 128 * (4 + c) + o) = li_;
       }
-      uint4 hr, lr, hi_, li_;
-      split8(re, sz, hr, lr);
-      split8(im, sz, hi_, li_);
-      *reinterpret_cast<uint4*>(gb + 128 * h4 + 16 * r8) = hr;
-      *reinterpret_cast<uint4*>(gb + 1024 + 128 * h4 + 16 * r8) = lr;
-      *reinterpret_cast<uint4*>(gb + 128 * (4 + h4) + 16 * r8) = hi_;
-      *reinterpret_cast<uint4*>(gb + 1024 + 128 * (4 + h4) + 16 * r8) = li_;
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm->conv[s]);
@@ -1100,17 +1151,18 @@ int lk_gram(const void* H, int64_t B, int M, double xi, const double* xi_b, void
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   float* sz = (float*)ws;
   int* rflag = (int*)((char*)ws + al((size_t)B * 4));
-  CUtensorMap map;
-  if (int e = make_hmap(&map, H, B, M, gram::BLK, gram::CH)) return e;
+  CUtensorMap pmap, smap;
+  if (int e = make_hmap(&pmap, H, B, M, 2 * gram::BLK, gram::CH)) return e;
+  if (int e = make_hmap(&smap, H, B, M, gram::BLK, gram::CH)) return e;
   if (cudaMemsetAsync(rflag, 0, (size_t)B * sizeof(int), st) != cudaSuccess) return check_launch("lk flags");
   cudaFuncSetAttribute(gram::lk_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gram::SMEM);
-  gram::lk_gram_kernel<<<(unsigned)(gram::TPR * B), gram::NT, gram::SMEM, st>>>(map, M, sz, (float2*)A, xi, xi_b,
-                                                                               rflag, 0);
+  gram::lk_gram_kernel<<<(unsigned)(gram::TPR * B), gram::NT, gram::SMEM, st>>>(pmap, smap, M, sz, (float2*)A, xi,
+                                                                               xi_b, rflag, 0);
   if (int e = check_launch("lk gram")) return e;
   lk_zmax_kernel<<<(unsigned)B, 512, 0, st>>>((const float4*)H, (int64_t)M * NC / 4, sz, rflag);
   if (int e = check_launch("lk zmax")) return e;
-  gram::lk_gram_kernel<<<(unsigned)(gram::TPR * B), gram::NT, gram::SMEM, st>>>(map, M, sz, (float2*)A, xi, xi_b,
-                                                                               rflag, 1);
+  gram::lk_gram_kernel<<<(unsigned)(gram::TPR * B), gram::NT, gram::SMEM, st>>>(pmap, smap, M, sz, (float2*)A, xi,
+                                                                               xi_b, rflag, 1);
   return check_launch("lk gram fixup");
 }
 
