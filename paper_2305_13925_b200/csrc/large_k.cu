@@ -686,24 +686,29 @@ __global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUt
 namespace pc {
 constexpr int C = 8;                     // CTAs per cluster
 constexpr int JN = KU / C;               // RHS columns per CTA
-constexpr int NMATH = 512;               // 16 warps: M-tile m = w >> 2, lane quadrant q = w & 3
-constexpr int NT = NMATH;
-constexpr int CHUNK = 32768;             // one K-step of A'': 512 rows x 16 K, hi + lo
-constexpr int NCH = NC / 16;             // K-steps per product
+constexpr int NT = 512;                  // 16 warps: accumulator tile w >> 2, lane quadrant w & 3
+constexpr int TILE = 128 * 16 * 2;       // one 128-row x 16-K fp16 K-major operand tile (4 KiB)
+constexpr int CHUNK = 8 * TILE;          // one K-step of users: Ar, Ai (2 row tiles each) x hi, lo: 32 KiB
+constexpr int NCH = KU / 16;             // K-steps per product
 constexpr int NS = 4;
 constexpr int LBOB = JN * 16;            // MN-major B tile: 8-K-row group stride
-constexpr int PART = (NC / 8) * LBOB;    // one B tile (hi or lo): 32 KiB
+constexpr int PART = (KU / 8) * LBOB;    // one B tile (Pr or Pi, hi or lo): 16 KiB
 constexpr int OFF_B = NS * CHUNK;
-constexpr int OFF_SMALL = OFF_B + 2 * PART;
+constexpr int OFF_SMALL = OFF_B + 4 * PART;
+// TMEM: Q accumulator tiles (Re users 0-127, Re 128-255, Im 0-127, Im 128-255)
+// x 32 columns, then R and X in the same arrangement
 constexpr uint32_t T_Q = 0, T_R = 128, T_X = 256;
 constexpr uint32_t ID = idesc(128, JN, 0, 1);
+constexpr uint32_t ID_NEG = ID | (1u << 13);  // negate A: -Ai Pi
 constexpr int BAR_MATH = 1;
-constexpr size_t SLOT_BYTES = (size_t)NCH * CHUNK;  // 1 MiB of A'' per cluster
+constexpr size_t SLOT_BYTES = (size_t)NCH * CHUNK;  // 512 KiB of split A per cluster
+// chunk layout: [Ar hi | Ar lo | Ai hi | Ai lo] x [row tile 0 | row tile 1]
+__host__ __device__ constexpr int tile_off(int ai, int lo, int m) { return ((2 * ai + lo) * 2 + m) * TILE; }
 
 struct Small {
   uint64_t full[NS], empty[NS], q_full;
   uint32_t tmem_slot;
-  int zero_diag, not_hpd;
+  int not_hpd;
   float red[16][JN];
   alignas(16) float coef[2][JN];
   alignas(16) float spx[JN];
@@ -715,6 +720,7 @@ struct Small {
 };
 constexpr int SMEM = OFF_SMALL + (int)sizeof(Small);
 static_assert(SMEM <= 227 * 1024, "lk pcg smem");
+static_assert(NS * CHUNK >= KU * (2 * JN + 1) * 4, "X / GX staging fits the ring");
 
 struct Params {
   const float2* A;  // [B][K][K] regularized Gram (Hermitian, xi on the diagonal)
@@ -726,7 +732,7 @@ struct Params {
   float2* GX;       // [B][K][K]
   double* part;     // [B][C] Re tr(X^H GX) per CTA
   int32_t* status;  // [B]
-  uint8_t* scratch; // [clusters][1 MiB] A'' split, K-step chunks
+  uint8_t* scratch; // [clusters][512 KiB] split (Re A, Im A), K-step chunks
 };
 
 __device__ __forceinline__ void lds8(const float* a, float (&o)[8]) {
@@ -739,7 +745,7 @@ __device__ __forceinline__ void col_partials(float (&v)[JN], Small* sm, int warp
   const float t = warp_transpose_reduce<JN, MAX>(v);
   sm->red[warp][threadIdx.x & 31] = t;
 }
-// CTA total of column j over the 16 math warps in a fixed order
+// CTA total of column j over the 16 warps in a fixed order
 template <bool MAX = false>
 __device__ __forceinline__ float col_total(const Small* sm, int j) {
   float s = sm->red[0][j];
@@ -748,6 +754,12 @@ __device__ __forceinline__ float col_total(const Small* sm, int j) {
   return s;
 }
 
+// One cluster of 8 CTAs per realization (persistent over b); CTA c owns RHS
+// columns [32c, 32c + 32).  Thread (tile tau = warp >> 2, quadrant q, lane)
+// owns component (user u = 128 (tau & 1) + 32 q + lane, part = tau >> 1:
+// 0 = Re, 1 = Im) of its 32 columns: P in registers, Q / R / X in TMEM.
+// Q = A P as complex products of the streamed split Re A / Im A tiles:
+// Re Q = Ar Pr - Ai Pi, Im Q = Ar Pi + Ai Pr (3xFP16 each: 24 MMAs per K-step).
 __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
@@ -756,9 +768,9 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
   const uint32_t rank = cluster_rank();
   const uint32_t cid = cluster_id_x(), ncl = nclusters_x();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int m = (warp >> 2) & 3, q = warp & 3;
-  const int rg = 128 * m + 32 * q + lane;     // component row
-  const int kr = rg >> 1;                     // user of the row
+  const int tau = warp >> 2, q = warp & 3;
+  const int u = 128 * (tau & 1) + 32 * q + lane;  // user of the thread's component
+  const int part = tau >> 1;                      // 0: Re, 1: Im
   const bool use_c = p.method == XL_JACPCG;
   const bool textbook = use_c && p.variant == XL_TEXTBOOK;
   uint8_t* slot = p.scratch + (size_t)cid * SLOT_BYTES;
@@ -776,28 +788,28 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
   tc_after();
   const uint32_t tmem = sm->tmem_slot;
   const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
-  const uint32_t tQ = tl + T_Q + JN * m, tR = tl + T_R + JN * m, tX = tl + T_X + JN * m;
+  const uint32_t tQ = tl + T_Q + JN * tau, tR = tl + T_R + JN * tau, tX = tl + T_X + JN * tau;
   const uint32_t upb = su32(pb);
   uint32_t g_prod = 0, g_cons = 0, nq = 0;  // ring chunks produced / consumed, products
-  // thread 0 streams A'': chunk n of the realization's (T + 1) x 32 K-steps into
-  // the ring (stage g % NS, all eight CTAs), armed in every CTA, copied by its
-  // owner CTA (n % 8) with one multicast once every CTA has freed the stage
+  // thread 0 streams the split A: chunk n of the realization's (T + 1) x 16
+  // K-steps into the ring (stage g % NS of all eight CTAs), armed in every
+  // CTA, copied by its owner CTA (n % 8) with one multicast once every CTA has
+  // freed the stage
   int n_issued = 0, n_total = 0;
-  const uint8_t* cur_slot = nullptr;
   auto issue_next = [&]() {
     if (n_issued >= n_total) return;
     const int s = g_prod % NS, k = n_issued % NCH;
     if (g_prod >= NS) bwait(&sm->empty[s], ((g_prod / NS) - 1) & 1);
     mbar_expect_tx(&sm->full[s], CHUNK);
-    if ((k & (C - 1)) == (int)rank) bulk_mc(ring + s * CHUNK, cur_slot + (size_t)k * CHUNK, CHUNK, &sm->full[s], 0xFF);
+    if ((k & (C - 1)) == (int)rank) bulk_mc(ring + s * CHUNK, slot + (size_t)k * CHUNK, CHUNK, &sm->full[s], 0xFF);
     ++g_prod;
     ++n_issued;
   };
 
   for (int64_t b = cid; b < p.B; b += ncl) {
     const float2* a = p.A + b * (int64_t)KU * KU;
-    cluster_sync();  // the previous realization's A'' chunks are consumed in every CTA
-    // ---- scale: diag(A'') = sa diag(A) < 2^14; zero diagonal -> Splitting (linsolve.py:205-208)
+    cluster_sync();  // the previous realization's chunks are consumed in every CTA
+    // ---- scale: diag(A) sa < 2^14; zero diagonal -> Splitting (linsolve.py:205-208)
     if (tid < KU) sm->cdg[tid] = a[(int64_t)tid * KU + tid].x;
     if (tid == 0) sm->not_hpd = 0;
     __syncthreads();
@@ -818,39 +830,37 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       zsum += sm->dmax[8 + w];
     }
     const float sa = pow2_scale(dmax, 14);
-    // ---- this CTA's eighth of A'' (K components [64 rank, 64 rank + 64)) ->
-    // the cluster's scratch slot as K-major core-matrix chunks; row 2i =
-    // (Re a_ij, -Im a_ij), row 2i+1 = (Im a_ij, Re a_ij), a_ij = conj(A[j][i])
-    for (int task = tid; task < NC * 8; task += NT) {
-      const int r = task & (NC - 1), o = task >> 9;
-      const int i = r >> 1;
-      const bool odd = r & 1;
-      float v[8];
+    // ---- this CTA's two K-step chunks (users k in [32 rank, 32 rank + 32)) of
+    // the split (Re A, Im A) -> the cluster's scratch slot, K-major core
+    // matrices; a_ik = conj(A[k][i]) (A Hermitian): Re = A[k][i].x, Im = -A[k][i].y
+    for (int task = tid; task < 2 * KU * 2; task += NT) {
+      const int i = task & (KU - 1), ko = task >> 8;  // row, K-octet (0..3) of the CTA's 32 users
+      float vr[8], vi[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = 32 * (int)rank + 4 * o + u;
-        const float2 x = __ldg(a + (int64_t)j * KU + i);  // a_ji: Re a_ij = x.x, Im a_ij = -x.y
-        v[2 * u] = odd ? -x.y : x.x;
-        v[2 * u + 1] = odd ? x.x : x.y;
+      for (int e = 0; e < 8; ++e) {
+        const float2 x = __ldg(a + (int64_t)(32 * (int)rank + 8 * ko + e) * KU + i);
+        vr[e] = x.x;
+        vi[e] = -x.y;
       }
-      uint4 hi, lo;
-      split8(v, sa, hi, lo);
-      const int s = 4 * (int)rank + (o >> 1), kg = o & 1;
-      uint8_t* dst = slot + (size_t)s * CHUNK + (r >> 7) * 4096 + ((r & 127) >> 3) * 256 + kg * 128 + (r & 7) * 16;
-      *reinterpret_cast<uint4*>(dst) = hi;
-      *reinterpret_cast<uint4*>(dst + CHUNK / 2) = lo;
+      uint4 hr, lr, hi_, li_;
+      split8(vr, sa, hr, lr);
+      split8(vi, sa, hi_, li_);
+      const int s = 2 * (int)rank + (ko >> 1), kg = ko & 1, m = i >> 7;
+      uint8_t* dst = slot + (size_t)s * CHUNK + ((i & 127) >> 3) * 256 + kg * 128 + (i & 7) * 16;
+      *reinterpret_cast<uint4*>(dst + tile_off(0, 0, m)) = hr;
+      *reinterpret_cast<uint4*>(dst + tile_off(0, 1, m)) = lr;
+      *reinterpret_cast<uint4*>(dst + tile_off(1, 0, m)) = hi_;
+      *reinterpret_cast<uint4*>(dst + tile_off(1, 1, m)) = li_;
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");
-    cluster_sync();  // the whole A'' is in the slot
-
+    cluster_sync();  // the whole split A is in the slot
     if (tid == 0) {
       n_issued = 0;
       n_total = (p.T + 1) * NCH;
-      cur_slot = slot;
       for (int i = 0; i < NS; ++i) issue_next();
     }
 
-    const float cr = use_c ? sm->cdg[kr] * sa : 1.0f;
+    const float cr = use_c ? sm->cdg[u] * sa : 1.0f;
     const float icr = 1.0f / cr;
     const double alpha = p.xi_b ? p.xi_b[b] : p.xi;
     // ---- initial state (linsolve.py:224-229, 264-268): x = 0, r = I (Algorithm 1:
@@ -862,7 +872,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int jg = JN * (int)rank + c0 + i;
-        const float e = (rg == 2 * jg) ? 1.0f : 0.0f;
+        const float e = (part == 0 && u == jg) ? 1.0f : 0.0f;
         rv[i] = (use_c && !textbook) ? e * icr : e;
         P[c0 + i] = textbook ? e * icr : rv[i];
         zx[i] = 0.0f;
@@ -882,58 +892,68 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
 #pragma unroll
       for (int jj = 0; jj < JN; ++jj) A[jj] = fabsf(v[jj]);
       col_partials<true>(A, sm, warp);
-      named_sync(BAR_MATH, NMATH);
+      named_sync(BAR_MATH, NT);
       if (tid < JN) {
         const float s = pow2_scale(col_total<true>(sm, tid), 14);
         sm->spx[tid] = s;
         sm->spy[tid] = 1.0f / s;
       }
-      named_sync(BAR_MATH, NMATH);
+      named_sync(BAR_MATH, NT);
     };
-    // Q = A'' v (v scaled per column): B tile written by all, MMAs issued by thread 0
+    // Q = A v (v scaled per column): B tiles (Pr, Pi; hi, lo) written by all,
+    // MMAs issued by thread 0
     auto product = [&](const float (&v)[JN]) {
 #pragma unroll
       for (int g = 0; g < JN / 8; ++g) {
         float sv[8], w8[8];
         lds8(sm->spx + 8 * g, sv);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) w8[i] = v[8 * g + i];
+        for (int i = 0; i < 8; ++i) w8[i] = v[8 * g + i] * sv[i];
         uint4 hi, lo;
-        uint32_t h[4], l[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) split2(w8[2 * i] * sv[2 * i], w8[2 * i + 1] * sv[2 * i + 1], h[i], l[i]);
-        hi = make_uint4(h[0], h[1], h[2], h[3]);
-        lo = make_uint4(l[0], l[1], l[2], l[3]);
-        const int o = (rg >> 3) * LBOB + g * 128 + (rg & 7) * 16;
-        *reinterpret_cast<uint4*>(pb + o) = hi;
-        *reinterpret_cast<uint4*>(pb + PART + o) = lo;
+        split8(w8, 1.0f, hi, lo);
+        const int o = (u >> 3) * LBOB + g * 128 + (u & 7) * 16;
+        *reinterpret_cast<uint4*>(pb + (2 * part) * PART + o) = hi;
+        *reinterpret_cast<uint4*>(pb + (2 * part + 1) * PART + o) = lo;
       }
       fence_async_smem();
       tc_before();
-      named_sync(BAR_MATH, NMATH);
+      named_sync(BAR_MATH, NT);
       if (warp == 0) {  // lanes 1..31 wait at __syncwarp, not in a divergent spin beside the issuer
         if (lane == 0) {
-        tc_after();
-        for (int k = 0; k < NCH; ++k, ++g_cons) {
-          const int s = g_cons % NS;
-          bwait(&sm->full[s], (g_cons / NS) & 1);
           tc_after();
-          const uint32_t st = su32(ring + s * CHUNK);
-          const uint64_t bh = sdesc(upb + 2 * k * LBOB, LBOB, 128), bl = sdesc(upb + PART + 2 * k * LBOB, LBOB, 128);
+          for (int k = 0; k < NCH; ++k, ++g_cons) {
+            const int s = g_cons % NS;
+            bwait(&sm->full[s], (g_cons / NS) & 1);
+            tc_after();
+            const uint32_t st = su32(ring + s * CHUNK);
+            const uint32_t bo = 2 * k * LBOB;
+            const uint64_t prh = sdesc(upb + 0 * PART + bo, LBOB, 128), prl = sdesc(upb + 1 * PART + bo, LBOB, 128);
+            const uint64_t pih = sdesc(upb + 2 * PART + bo, LBOB, 128), pil = sdesc(upb + 3 * PART + bo, LBOB, 128);
+            const uint32_t acc = k != 0;
 #pragma unroll
-          for (int mt = 0; mt < 4; ++mt) {
-            const uint64_t ah = sdesc(st + 4096 * mt, 128, 256), al = sdesc(st + CHUNK / 2 + 4096 * mt, 128, 256);
-            const uint32_t d = tmem + T_Q + JN * mt;
-            mma(d, ah, bh, ID, k != 0);
-            mma(d, ah, bl, ID, 1);
-            mma(d, al, bh, ID, 1);
+            for (int m = 0; m < 2; ++m) {
+              const uint64_t arh = sdesc(st + tile_off(0, 0, m), 128, 256), arl = sdesc(st + tile_off(0, 1, m), 128, 256);
+              const uint64_t aih = sdesc(st + tile_off(1, 0, m), 128, 256), ail = sdesc(st + tile_off(1, 1, m), 128, 256);
+              const uint32_t dr = tmem + T_Q + JN * m, di = tmem + T_Q + JN * (2 + m);
+              mma(dr, arh, prh, ID, acc);  // Re Q += Ar Pr
+              mma(dr, arh, prl, ID, 1);
+              mma(dr, arl, prh, ID, 1);
+              mma(dr, aih, pih, ID_NEG, 1);  // Re Q -= Ai Pi
+              mma(dr, aih, pil, ID_NEG, 1);
+              mma(dr, ail, pih, ID_NEG, 1);
+              mma(di, arh, pih, ID, acc);  // Im Q += Ar Pi
+              mma(di, arh, pil, ID, 1);
+              mma(di, arl, pih, ID, 1);
+              mma(di, aih, prh, ID, 1);  // Im Q += Ai Pr
+              mma(di, aih, prl, ID, 1);
+              mma(di, ail, prh, ID, 1);
+            }
+            commit_mc(&sm->empty[s], 0xFF);
+            // refill the stage of the previous K-step (its MMAs are likely done)
+            if (k >= 1) issue_next();
           }
-          commit_mc(&sm->empty[s], 0xFF);
-          // refill the stage of the previous K-step (its MMAs are likely done)
-          if (k >= 1) issue_next();
-        }
-        commit(&sm->q_full);
-        issue_next();  // NS K-steps of the next product in flight during the SIMT phase
+          commit(&sm->q_full);
+          issue_next();  // NS K-steps of the next product in flight during the SIMT phase
         }
         __syncwarp();
       }
@@ -958,7 +978,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
         for (int i = 0; i < 8; ++i) A[c0 + i] = P[c0 + i] * ((A[c0 + i] * sy[i]) * qs);
       }
       col_partials(A, sm, warp);
-      named_sync(BAR_MATH, NMATH);
+      named_sync(BAR_MATH, NT);
       if (tid < JN) {  // alpha_j, NotHpd (linsolve.py:277-280)
         const float curv = col_total(sm, tid);
         const float rzj = sm->rzs[tid];
@@ -966,7 +986,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
         if (curv <= 0.0f && act) sm->not_hpd = 1;
         sm->coef[0][tid] = act ? rzj / (curv > 0.0f ? curv : 1.0f) : 0.0f;
       }
-      named_sync(BAR_MATH, NMATH);
+      named_sync(BAR_MATH, NT);
       // w += alpha m, r -= alpha Pm, rz partials (linsolve.py:281-284)
 #pragma unroll
       for (int c0 = 0; c0 < JN; c0 += 8) {
@@ -990,14 +1010,14 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       }
       col_partials(A, sm, warp);
       tmem_wait_st();
-      named_sync(BAR_MATH, NMATH);
+      named_sync(BAR_MATH, NT);
       if (tid < JN) {  // beta_j, rz update (linsolve.py:284-288)
         const float rn = col_total(sm, tid);
         const float rzj = sm->rzs[tid];
         sm->coef[1][tid] = rzj > 0.0f ? rn / rzj : 0.0f;
         sm->rzs[tid] = rn;
       }
-      named_sync(BAR_MATH, NMATH);
+      named_sync(BAR_MATH, NT);
       // m = z + beta m
 #pragma unroll
       for (int c0 = 0; c0 < JN; c0 += 8) {
@@ -1013,7 +1033,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       }
     }
 
-    // ---- GX = A X - xi X from Q = A'' X'' (X = sa X'')
+    // ---- GX = A X - xi X from Q = A X'' (X = sa X'')
     tmem_ld<JN>(tX, P);
     tmem_wait_ld();
     scale(P);
@@ -1033,26 +1053,26 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
         fro += (double)(P[c0 + i] * sa) * (double)g;  // Re tr(X^H GX)
       }
     }
-    // row-major complex outputs: lanes (2m, 2m+1) hold (Re, Im) of user kr;
-    // the even lane stores column pairs 4n, 4n+1 and the odd lane 4n+2, 4n+3
-    const bool odd = lane & 1;
-    float2* xo = p.X + b * (int64_t)KU * KU + (int64_t)kr * KU + JN * rank;
-    float2* go = p.GX + b * (int64_t)KU * KU + (int64_t)kr * KU + JN * rank;
+    // ---- outputs staged in the (idle: every chunk of this realization has
+    // landed and been consumed) ring as [user][column][re, im] with an odd row
+    // stride (conflict-free), then written as coalesced 256-B row segments
+    constexpr int SR = 2 * JN + 1;
+    float* stg = reinterpret_cast<float*>(ring);
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
 #pragma unroll
-    for (int jp = 0; jp < JN; jp += 2) {
-      const float x0 = P[jp] * sa, x1 = P[jp + 1] * sa, g0 = A[jp], g1 = A[jp + 1];
-      const float ox0 = __shfl_xor_sync(0xffffffffu, x0, 1), ox1 = __shfl_xor_sync(0xffffffffu, x1, 1);
-      const float og0 = __shfl_xor_sync(0xffffffffu, g0, 1), og1 = __shfl_xor_sync(0xffffffffu, g1, 1);
-      if (((jp >> 1) & 1) == (odd ? 1 : 0)) {
-        const float4 xv = odd ? make_float4(ox0, x0, ox1, x1) : make_float4(x0, ox0, x1, ox1);
-        const float4 gv = odd ? make_float4(og0, g0, og1, g1) : make_float4(g0, og0, g1, og1);
-        *reinterpret_cast<float4*>(xo + jp) = xv;
-        *reinterpret_cast<float4*>(go + jp) = gv;
+      for (int jj = 0; jj < JN; ++jj) stg[u * SR + 2 * jj + part] = pass == 0 ? P[jj] * sa : A[jj];
+      named_sync(BAR_MATH, NT);
+      float* out = reinterpret_cast<float*>((pass == 0 ? p.X : p.GX) + b * (int64_t)KU * KU + JN * rank);
+      for (int row = warp; row < KU; row += NT / 32) {
+        out[(int64_t)row * 2 * KU + lane] = stg[row * SR + lane];
+        out[(int64_t)row * 2 * KU + 32 + lane] = stg[row * SR + 32 + lane];
       }
+      named_sync(BAR_MATH, NT);
     }
     fro = warp_sum(fro);
     if (lane == 0) sm->dred[warp] = fro;
-    named_sync(BAR_MATH, NMATH);
+    named_sync(BAR_MATH, NT);
     if (tid == 0) {
       double s = 0.0;
 #pragma unroll
