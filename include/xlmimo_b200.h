@@ -149,6 +149,9 @@ int xl_rzf_general(int dtype, int method, int variant, const void* H, int64_t B,
 /* Test hook: when non-NULL, the fused kernel also writes the regularized Gram
  * A[B][K][K] (complex64) of every realization it processes. */
 void xl_debug_set_gram_out(void* A);
+/* Development hook: when non-NULL, the K = 256 cluster solver writes clock64
+ * stamps of cluster 0 / CTA 0 (phase boundaries) into buf[0..255]. */
+void xl_debug_lk_trace(void* buf);
 
 /* Per-user SINR/SE of an arbitrary precoder G on one full-array block:
  * sinr_eq9 (metrics.py:47-58) with coupling B = H^H G (metrics.py:35-44).

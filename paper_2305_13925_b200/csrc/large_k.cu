@@ -61,16 +61,25 @@ __device__ __forceinline__ uint64_t gtimer() {
 // mbarrier wait with a wall-clock bound (4 s): a protocol bug traps instead of
 // hanging the GPU.  try_wait carries a suspend-time hint, so waiting warps
 // sleep in hardware instead of taking issue slots from the working ones.
+template <bool SPIN = false>
 __device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity) {
   uint32_t done;
   uint64_t t0 = 0;
   for (uint32_t it = 0;; ++it) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, P1;\n\t}\n"
-        : "=r"(done)
-        : "r"(su32(bar)), "r"(parity), "r"(0x989680u)
-        : "memory");
+    if (SPIN)
+      asm volatile(
+          "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, P1;\n\t}\n"
+          : "=r"(done)
+          : "r"(su32(bar)), "r"(parity)
+          : "memory");
+    else
+      asm volatile(
+          "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+          "selp.u32 %0, 1, 0, P1;\n\t}\n"
+          : "=r"(done)
+          : "r"(su32(bar)), "r"(parity), "r"(0x989680u)
+          : "memory");
     if (done) return;
     if ((it & 15u) == 15u) {
       const uint64_t t = gtimer();
@@ -118,6 +127,14 @@ __device__ __forceinline__ void bulk_mc(void* dst, const void* src, uint32_t byt
 __device__ __forceinline__ void commit_mc(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          su32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void commit_mc_w(uint64_t* bar, uint16_t mask) {  // warp-collective, one elected lane
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
           su32(bar)),
       "h"(mask)
       : "memory");
@@ -249,7 +266,7 @@ __global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ 
                                                         const __grid_constant__ CUtensorMap smap, int M,
                                                         float* __restrict__ szv, float2* __restrict__ A, double xi,
                                                         const double* __restrict__ xi_b, int* __restrict__ rflag,
-                                                        int fixup) {
+                                                        unsigned* __restrict__ zmax, int fixup) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
   Small* sm = reinterpret_cast<Small*>(smem + NS * SB);
@@ -289,8 +306,8 @@ __global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ 
         for (int j = 0; j < pl.ns; ++j) tma2d(st + soff + j * SGL, &smap, BLK * pl.sb[j], y0 + c * CH, &sm->full[s]);
       }
     }
-  } else if (warp == W_MMA) {
-    if (lane == 0) {
+  } else if (warp == W_MMA) {  // the whole warp issues (mma_w elects one lane)
+    {
       constexpr int PG = 8 * 2 * BLK * 4, SG = 8 * BLK * 4;  // group strides (8 KiB pair, 4 KiB single)
       for (int c = 0; c < nch; ++c) {
         const int s = c % NS;
@@ -313,30 +330,31 @@ __global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ 
             }
             const uint64_t bh = sdesc(pbase, PG, 128), bl = sdesc(pbase + PG / 2, PG, 128);
             constexpr uint32_t ID256 = idesc(128, 256, 1, 1);
-            mma(tmem, ah, bh, ID256, acc);
-            mma(tmem, ah, bl, ID256, 1);
-            mma(tmem, al, bh, ID256, 1);
+            mma_w(tmem, ah, bh, ID256, acc);
+            mma_w(tmem, ah, bl, ID256, 1);
+            mma_w(tmem, al, bh, ID256, 1);
           } else {  // two N = 128 products on singles: (A = single 0, B = single 1), (single 1, single 1)
             constexpr uint32_t ID128 = idesc(128, 128, 1, 1);
             const uint32_t s0 = st + soff + 2 * ks * SG, s1 = s0 + SGL;
             const uint64_t h0 = sdesc(s0, SG, 128), l0 = sdesc(s0 + SG / 2, SG, 128);
             const uint64_t h1 = sdesc(s1, SG, 128), l1 = sdesc(s1 + SG / 2, SG, 128);
-            mma(tmem, h0, h1, ID128, acc);
-            mma(tmem, h0, l1, ID128, 1);
-            mma(tmem, l0, h1, ID128, 1);
-            mma(tmem + 128, h1, h1, ID128, acc);
-            mma(tmem + 128, h1, l1, ID128, 1);
-            mma(tmem + 128, l1, h1, ID128, 1);
+            mma_w(tmem, h0, h1, ID128, acc);
+            mma_w(tmem, h0, l1, ID128, 1);
+            mma_w(tmem, l0, h1, ID128, 1);
+            mma_w(tmem + 128, h1, h1, ID128, acc);
+            mma_w(tmem + 128, h1, l1, ID128, 1);
+            mma_w(tmem + 128, l1, h1, ID128, 1);
           }
         }
-        commit(&sm->freed[s]);
+        commit_w(&sm->freed[s]);
       }
-      commit(&sm->done);
+      commit_w(&sm->done);
     }
   } else {
     const int cw = warp - W_CONV0;
     float sz = fixup ? szv[b] : 1.0f;
     bool have = fixup != 0, over = false;
+    float zm = 0.0f;  // exact max |H| over this CTA's blocks (the W kernel's scale)
     for (int c = 0; c < nch; ++c) {
       const int s = c % NS;
       bwait(&sm->full[s], (c / NS) & 1);
@@ -351,6 +369,7 @@ __global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ 
       if (hp) gm = load8(pg, 2 * BLK * 4, lane, 8 * (cw & 1), vp);
       if (dos) gm = fmaxf(gm, load8(sg, BLK * 4, lane, 0, vs));
       gm = warp_max(gm);
+      zm = fmaxf(zm, gm);
       if (!have) {  // until the first non-zero chunk: max over the converter warps
         if (lane == 0) sm->rmax[cw] = gm;
         named_sync(BAR_CONV, 32 * NCONV);
@@ -358,8 +377,8 @@ __global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ 
 #pragma unroll
         for (int w = 1; w < NCONV; ++w) mx = fmaxf(mx, sm->rmax[w]);
         named_sync(BAR_CONV, 32 * NCONV);
-        if (mx > 0.0f) {
-          sz = pow2_scale(mx, 11);
+        if (mx > 0.0f) {  // max in [2^6, 2^7): 2^8-2^9 x headroom for later antennas
+          sz = pow2_scale(mx, 7);
           have = true;
         }
       }
@@ -373,6 +392,8 @@ __global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ 
       if (lane == 0) mbar_arrive(&sm->conv[s]);
     }
     if (!fixup && over && lane == 0) rflag[b] = 1;
+    // the CTAs of a realization together cover every block (CTA 0: 0-1, CTA 1: 0, 2-3)
+    if (lane == 0 && zm > 0.0f) atomicMax(zmax + b, __float_as_uint(zm));  // non-negative: bit order == value order
     // ---- epilogue: tile k = (I, J), lanes = rows 128 I + r, columns 128 J + c;
     // lane pairs (2i, 2i+1) form the complex entries (re = U[2i][2j] +
     // U[2i+1][2j+1], im = U[2i][2j+1] - U[2i+1][2j]); the upper triangle is
@@ -441,7 +462,6 @@ static_assert(NS * BOX >= 2 * 128 * KU * 2, "A staging fits the ring");
 // D1 = A Zr^T at 256 + 128 j and D2 = A Zi^T at 256 + 128 j + 64
 constexpr uint32_t T_AH = 0, T_AL = 128, T_ACC = 256;
 constexpr uint32_t ID = idesc(128, CHA, 0, 0);
-constexpr int BAR_CONV = 1;
 
 struct Small {
   uint64_t full[NS], conv[NS], freed[NS];
@@ -450,7 +470,6 @@ struct Small {
   uint32_t tmem_slot;
   float rmax[4][64];
   float sx[64];
-  float cmax[NCONV];
 };
 static_assert(sizeof(Small) <= SMALL, "W small");
 
@@ -480,16 +499,17 @@ __device__ __forceinline__ void build_rows(const float2* __restrict__ Xb, int t,
   }
 }
 
+// zmax[b]: the exact max |H_b| (bits of a non-negative float) from lk_gram, so
+// the split scale sz (max |sz H| in [2^10, 2^11)) never overflows fp16.
 __global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUtensorMap hmap, int M,
-                                                     float* __restrict__ szv, const float2* __restrict__ X,
+                                                     const unsigned* __restrict__ zmax, const float2* __restrict__ X,
                                                      const double* __restrict__ beta, float* __restrict__ W,
-                                                     float* __restrict__ F, int* __restrict__ rflag, int fixup) {
+                                                     float* __restrict__ F) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem + OFF_RING;
   Small* sm = reinterpret_cast<Small*>(smem + OFF_RING + NS * BOX);
   const int64_t b = blockIdx.x / TPR;
   const int t = blockIdx.x % TPR;
-  if (fixup && rflag[b] == 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ntile = M / CHA, nbox = ntile * (KU / BU);
   if (tid == 0) {
@@ -529,15 +549,15 @@ __global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUt
   build_rows(Xb, t, sm->sx, ring, ring + 128 * KU * 2);
   fence_async_smem();
   __syncthreads();
-  if (tid == 32 * W_MMA) {
+  if (warp == W_MMA) {
     tc_after();
     const uint32_t uh = su32(ring), ul = su32(ring + 128 * KU * 2);
 #pragma unroll
     for (int s = 0; s < KU / 16; ++s) {
-      tmem_cp(tmem + T_AH + 8 * s, sdesc(uh + 2 * s * 128, 128, SBOA));
-      tmem_cp(tmem + T_AL + 8 * s, sdesc(ul + 2 * s * 128, 128, SBOA));
+      tmem_cp_w(tmem + T_AH + 8 * s, sdesc(uh + 2 * s * 128, 128, SBOA));
+      tmem_cp_w(tmem + T_AL + 8 * s, sdesc(ul + 2 * s * 128, 128, SBOA));
     }
-    commit(&sm->cp_done);
+    commit_w(&sm->cp_done);
   }
   bwait(&sm->cp_done, 0);
   tc_after();
@@ -553,8 +573,8 @@ __global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUt
         tma2d(ring + s * BOX, &hmap, 2 * BU * kb, y0 + CHA * tt, &sm->full[s]);
       }
     }
-  } else if (warp == W_MMA) {
-    if (lane == 0) {
+  } else if (warp == W_MMA) {  // the whole warp issues (mma_ts_w elects one lane)
+    {
       for (int g = 0; g < nbox; ++g) {
         const int s = g % NS, tt = g / (KU / BU), kb = g % (KU / BU);
         if (kb == 0 && tt >= 2) bwait(&sm->acc_free[tt & 1], ((tt >> 1) - 1) & 1);
@@ -569,21 +589,20 @@ __global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUt
           const uint64_t brh = sdesc(st + 256 * ks, 128, 2048), brl = sdesc(st + 1024 + 256 * ks, 128, 2048);
           const uint64_t bih = sdesc(st + 512 + 256 * ks, 128, 2048), bil = sdesc(st + 1536 + 256 * ks, 128, 2048);
           const uint32_t acc = (kb | ks) != 0;
-          mma_ts(d1, ah, brh, ID, acc);
-          mma_ts(d1, ah, brl, ID, 1);
-          mma_ts(d1, al, brh, ID, 1);
-          mma_ts(d2, ah, bih, ID, acc);
-          mma_ts(d2, ah, bil, ID, 1);
-          mma_ts(d2, al, bih, ID, 1);
+          mma_ts_w(d1, ah, brh, ID, acc);
+          mma_ts_w(d1, ah, brl, ID, 1);
+          mma_ts_w(d1, al, brh, ID, 1);
+          mma_ts_w(d2, ah, bih, ID, acc);
+          mma_ts_w(d2, ah, bil, ID, 1);
+          mma_ts_w(d2, al, bih, ID, 1);
         }
-        commit(&sm->freed[s]);
-        if (kb == KU / BU - 1) commit(&sm->acc_full[tt & 1]);
+        commit_w(&sm->freed[s]);
+        if (kb == KU / BU - 1) commit_w(&sm->acc_full[tt & 1]);
       }
     }
   } else {
     const int cw = warp - W_CONV0;
-    float sz = fixup ? szv[b] : 1.0f;
-    bool have = fixup != 0, over = false;
+    const float sz = pow2_scale(__uint_as_float(zmax[b]), 11);
     const int crow = lane >> 2, pair = lane & 3;  // converter: antenna row of the group, user pair
     const int q = warp & 3, p = cw >> 2;
     const int r = 32 * q + lane;  // output row (TMEM lane)
@@ -634,24 +653,6 @@ __global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUt
         const int c = (it + crow) & 3;
         v[it] = *reinterpret_cast<const float4*>(gb + crow * 256 + 64 * c + 16 * pair);
       }
-      float gm = 0.0f;
-#pragma unroll
-      for (int it = 0; it < 4; ++it)
-        gm = fmaxf(gm, fmaxf(fmaxf(fabsf(v[it].x), fabsf(v[it].y)), fmaxf(fabsf(v[it].z), fabsf(v[it].w))));
-      gm = warp_max(gm);
-      if (!have) {
-        if (lane == 0) sm->cmax[cw] = gm;
-        named_sync(BAR_CONV, 32 * NCONV);
-        float mx = sm->cmax[0];
-#pragma unroll
-        for (int w = 1; w < NCONV; ++w) mx = fmaxf(mx, sm->cmax[w]);
-        named_sync(BAR_CONV, 32 * NCONV);
-        if (mx > 0.0f) {
-          sz = pow2_scale(mx, 11);
-          have = true;
-        }
-      }
-      over |= !(gm * sz < RANGE_MAX);
       __syncwarp();
 #pragma unroll
       for (int it = 0; it < 4; ++it) {
@@ -671,7 +672,6 @@ __global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUt
       if (kb == 0 && tt >= 1) drain(tt - 1);
     }
     drain(ntile - 1);
-    if (!fixup && over && lane == 0) rflag[b] = 1;
   }
   tc_before();
   __syncthreads();
@@ -688,22 +688,27 @@ constexpr int C = 8;                     // CTAs per cluster
 constexpr int JN = KU / C;               // RHS columns per CTA
 constexpr int NT = 512;                  // 16 warps: accumulator tile w >> 2, lane quadrant w & 3
 constexpr int TILE = 128 * 16 * 2;       // one 128-row x 16-K fp16 K-major operand tile (4 KiB)
-constexpr int CHUNK = 8 * TILE;          // one K-step of users: Ar, Ai (2 row tiles each) x hi, lo: 32 KiB
+constexpr int HALF = 4 * TILE;           // Re A or Im A of one K-step (2 row tiles x hi, lo): 16 KiB
+constexpr int CHUNK = 2 * HALF;          // one K-step of 16 users in the scratch slot
 constexpr int NCH = KU / 16;             // K-steps per product
-constexpr int NS = 4;
-constexpr int LBOB = JN * 16;            // MN-major B tile: 8-K-row group stride
-constexpr int PART = (KU / 8) * LBOB;    // one B tile (Pr or Pi, hi or lo): 16 KiB
+constexpr int NS = 3;                    // ring stages of one K-step chunk (32 KiB: one bulk copy each)
+constexpr int NB = 3 * JN;               // B tile columns: [-Pi | Pr | Pi]
+constexpr int LBOB = NB * 16;            // MN-major B tile: 8-K-row group stride
+constexpr int PART = (KU / 8) * LBOB;    // B tile hi or lo: 48 KiB
 constexpr int OFF_B = NS * CHUNK;
-constexpr int OFF_SMALL = OFF_B + 4 * PART;
-// TMEM: Q accumulator tiles (Re users 0-127, Re 128-255, Im 0-127, Im 128-255)
-// x 32 columns, then R and X in the same arrangement
-constexpr uint32_t T_Q = 0, T_R = 128, T_X = 256;
-constexpr uint32_t ID = idesc(128, JN, 0, 1);
-constexpr uint32_t ID_NEG = ID | (1u << 13);  // negate A: -Ai Pi
+constexpr int OFF_SMALL = OFF_B + 2 * PART;
+// TMEM: per row tile m the accumulator [Re Q | Im Q] (2 x 32 columns) at
+// 64 m; R and X in the same arrangement at 128 and 256; the A tiles of the
+// current half-chunk are copied (tcgen05.cp) into one of four 32-column
+// buffers at 384, so the products read A from TMEM (only B from smem)
+constexpr uint32_t T_Q = 0, T_R = 128, T_X = 256, T_A = 384;
+// [Re Q | Im Q] = Ar [Pr | Pi] + Ai [-Pi | Pr]: two N = 64 products per split
+// part, the B operands being 64-column windows of one [-Pi | Pr | Pi] tile
+constexpr uint32_t ID = idesc(128, 2 * JN, 0, 1);
 constexpr int BAR_MATH = 1;
 constexpr size_t SLOT_BYTES = (size_t)NCH * CHUNK;  // 512 KiB of split A per cluster
-// chunk layout: [Ar hi | Ar lo | Ai hi | Ai lo] x [row tile 0 | row tile 1]
-__host__ __device__ constexpr int tile_off(int ai, int lo, int m) { return ((2 * ai + lo) * 2 + m) * TILE; }
+// chunk layout: [Ar: hi m0, hi m1, lo m0, lo m1 | Ai: same]
+__host__ __device__ constexpr int tile_off(int ai, int lo, int m) { return ai * HALF + (2 * lo + m) * TILE; }
 
 struct Small {
   uint64_t full[NS], empty[NS], q_full;
@@ -733,6 +738,11 @@ struct Params {
   double* part;     // [B][C] Re tr(X^H GX) per CTA
   int32_t* status;  // [B]
   uint8_t* scratch; // [clusters][512 KiB] split (Re A, Im A), K-step chunks
+  long long* trace; // debug: clock64 stamps of cluster 0 / CTA 0 (xl_debug_lk_trace), or null
+  int unicast;      // 1: every CTA loads every chunk itself (no multicast; A/B)
+  int mma_reps;     // debug: issue each K-step's MMAs this many times (timing experiments)
+  int ss;           // 1: A operand straight from shared memory (no tcgen05.cp to TMEM)
+  int spin;         // 1: the MMA warp polls the ring barriers without a suspend hint
 };
 
 __device__ __forceinline__ void lds8(const float* a, float (&o)[8]) {
@@ -777,7 +787,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sm->full[s], 1);
-      mbar_init(&sm->empty[s], C);
+      mbar_init(&sm->empty[s], p.unicast ? 1 : C);
     }
     mbar_init(&sm->q_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -788,7 +798,8 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
   tc_after();
   const uint32_t tmem = sm->tmem_slot;
   const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
-  const uint32_t tQ = tl + T_Q + JN * tau, tR = tl + T_R + JN * tau, tX = tl + T_X + JN * tau;
+  const uint32_t tcol = 2 * JN * (tau & 1) + JN * (tau >> 1);
+  const uint32_t tQ = tl + T_Q + tcol, tR = tl + T_R + tcol, tX = tl + T_X + tcol;
   const uint32_t upb = su32(pb);
   uint32_t g_prod = 0, g_cons = 0, nq = 0;  // ring chunks produced / consumed, products
   // thread 0 streams the split A: chunk n of the realization's (T + 1) x 16
@@ -796,19 +807,34 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
   // CTA, copied by its owner CTA (n % 8) with one multicast once every CTA has
   // freed the stage
   int n_issued = 0, n_total = 0;
-  auto issue_next = [&]() {
+  // (called by all lanes of warp 0; lane 0 does the barrier / copy work)
+  // 32 KiB per copy: a lane's bulk copies are serviced about one at a time,
+  // so the fill rate grows with the copy size (tools/microbench/bulk_rules.cu)
+  auto issue_next = [&]() {  // chunk n: K-step n % NCH
     if (n_issued >= n_total) return;
     const int s = g_prod % NS, k = n_issued % NCH;
-    if (g_prod >= NS) bwait(&sm->empty[s], ((g_prod / NS) - 1) & 1);
-    mbar_expect_tx(&sm->full[s], CHUNK);
-    if ((k & (C - 1)) == (int)rank) bulk_mc(ring + s * CHUNK, slot + (size_t)k * CHUNK, CHUNK, &sm->full[s], 0xFF);
+    const uint8_t* src = slot + (size_t)k * CHUNK;
+    if (lane == 0) {
+      if (g_prod >= NS) bwait(&sm->empty[s], ((g_prod / NS) - 1) & 1);
+      mbar_expect_tx(&sm->full[s], CHUNK);
+      if (p.unicast) bulk_g2s(ring + s * CHUNK, src, CHUNK, &sm->full[s], policy_evict_normal());
+      else if ((k & (C - 1)) == (int)rank) bulk_mc(ring + s * CHUNK, src, CHUNK, &sm->full[s], 0xFF);
+    }
+    __syncwarp();
     ++g_prod;
     ++n_issued;
   };
 
+  const bool tr = p.trace && cid == 0 && rank == 0 && tid == 0;
+  int ntr = 0;
+  auto stamp = [&]() {
+    if (tr && ntr < 255) p.trace[ntr++] = clock64();
+  };
   for (int64_t b = cid; b < p.B; b += ncl) {
     const float2* a = p.A + b * (int64_t)KU * KU;
+    stamp();
     cluster_sync();  // the previous realization's chunks are consumed in every CTA
+    stamp();
     // ---- scale: diag(A) sa < 2^14; zero diagonal -> Splitting (linsolve.py:205-208)
     if (tid < KU) sm->cdg[tid] = a[(int64_t)tid * KU + tid].x;
     if (tid == 0) sm->not_hpd = 0;
@@ -853,8 +879,10 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       *reinterpret_cast<uint4*>(dst + tile_off(1, 1, m)) = li_;
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");
+    stamp();
     cluster_sync();  // the whole split A is in the slot
-    if (tid == 0) {
+    stamp();
+    if (warp == 1) {  // the producer warp of the product phases
       n_issued = 0;
       n_total = (p.T + 1) * NCH;
       for (int i = 0; i < NS; ++i) issue_next();
@@ -903,6 +931,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
     // Q = A v (v scaled per column): B tiles (Pr, Pi; hi, lo) written by all,
     // MMAs issued by thread 0
     auto product = [&](const float (&v)[JN]) {
+      // B tile columns [-Pi | Pr | Pi]: Re rows write Pr, Im rows write Pi and -Pi
 #pragma unroll
       for (int g = 0; g < JN / 8; ++g) {
         float sv[8], w8[8];
@@ -911,61 +940,83 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
         for (int i = 0; i < 8; ++i) w8[i] = v[8 * g + i] * sv[i];
         uint4 hi, lo;
         split8(w8, 1.0f, hi, lo);
-        const int o = (u >> 3) * LBOB + g * 128 + (u & 7) * 16;
-        *reinterpret_cast<uint4*>(pb + (2 * part) * PART + o) = hi;
-        *reinterpret_cast<uint4*>(pb + (2 * part + 1) * PART + o) = lo;
+        const int o = (u >> 3) * LBOB + (u & 7) * 16;
+        if (part == 0) {
+          *reinterpret_cast<uint4*>(pb + o + (4 + g) * 128) = hi;
+          *reinterpret_cast<uint4*>(pb + PART + o + (4 + g) * 128) = lo;
+        } else {
+          const uint4 nh = make_uint4(hi.x ^ 0x80008000u, hi.y ^ 0x80008000u, hi.z ^ 0x80008000u, hi.w ^ 0x80008000u);
+          const uint4 nl = make_uint4(lo.x ^ 0x80008000u, lo.y ^ 0x80008000u, lo.z ^ 0x80008000u, lo.w ^ 0x80008000u);
+          *reinterpret_cast<uint4*>(pb + o + (8 + g) * 128) = hi;
+          *reinterpret_cast<uint4*>(pb + PART + o + (8 + g) * 128) = lo;
+          *reinterpret_cast<uint4*>(pb + o + g * 128) = nh;
+          *reinterpret_cast<uint4*>(pb + PART + o + g * 128) = nl;
+        }
       }
       fence_async_smem();
       tc_before();
       named_sync(BAR_MATH, NT);
-      if (warp == 0) {  // lanes 1..31 wait at __syncwarp, not in a divergent spin beside the issuer
-        if (lane == 0) {
+      if (warp == 0) {  // the whole warp issues (tcgen05 ops elect one lane)
+        tc_after();
+        for (int k = 0; k < NCH; ++k) {  // K-step k: Re A half, then Im A half
+          const uint32_t gc = g_cons + k;
+          const int s = gc % NS;
+          if (p.spin) bwait<true>(&sm->full[s], (gc / NS) & 1);
+          else bwait(&sm->full[s], (gc / NS) & 1);
           tc_after();
-          for (int k = 0; k < NCH; ++k, ++g_cons) {
-            const int s = g_cons % NS;
-            bwait(&sm->full[s], (g_cons / NS) & 1);
-            tc_after();
-            const uint32_t st = su32(ring + s * CHUNK);
-            const uint32_t bo = 2 * k * LBOB;
-            const uint64_t prh = sdesc(upb + 0 * PART + bo, LBOB, 128), prl = sdesc(upb + 1 * PART + bo, LBOB, 128);
-            const uint64_t pih = sdesc(upb + 2 * PART + bo, LBOB, 128), pil = sdesc(upb + 3 * PART + bo, LBOB, 128);
-            const uint32_t acc = k != 0;
 #pragma unroll
-            for (int m = 0; m < 2; ++m) {
-              const uint64_t arh = sdesc(st + tile_off(0, 0, m), 128, 256), arl = sdesc(st + tile_off(0, 1, m), 128, 256);
-              const uint64_t aih = sdesc(st + tile_off(1, 0, m), 128, 256), ail = sdesc(st + tile_off(1, 1, m), 128, 256);
-              const uint32_t dr = tmem + T_Q + JN * m, di = tmem + T_Q + JN * (2 + m);
-              mma(dr, arh, prh, ID, acc);  // Re Q += Ar Pr
-              mma(dr, arh, prl, ID, 1);
-              mma(dr, arl, prh, ID, 1);
-              mma(dr, aih, pih, ID_NEG, 1);  // Re Q -= Ai Pi
-              mma(dr, aih, pil, ID_NEG, 1);
-              mma(dr, ail, pih, ID_NEG, 1);
-              mma(di, arh, pih, ID, acc);  // Im Q += Ar Pi
-              mma(di, arh, pil, ID, 1);
-              mma(di, arl, pih, ID, 1);
-              mma(di, aih, prh, ID, 1);  // Im Q += Ai Pr
-              mma(di, aih, prl, ID, 1);
-              mma(di, ail, prh, ID, 1);
+          for (int ai = 0; ai < 2; ++ai) {
+            const uint32_t st = su32(ring + s * CHUNK + ai * HALF);
+            const uint32_t ta = tmem + T_A + 32 * ((2 * gc + ai) & 3);
+            if (!p.ss) {
+#pragma unroll
+              for (int x = 0; x < 4; ++x) tmem_cp_w(ta + 8 * x, sdesc(st + x * TILE, 128, 256));
             }
-            commit_mc(&sm->empty[s], 0xFF);
-            // refill the stage of the previous K-step (its MMAs are likely done)
-            if (k >= 1) issue_next();
+            const uint32_t bo = upb + 2 * k * LBOB + (ai ? 0 : JN / 8 * 128);  // B2 = [-Pi | Pr], B1 = [Pr | Pi]
+            const uint64_t bh = sdesc(bo, LBOB, 128), bl = sdesc(bo + PART, LBOB, 128);
+            const uint32_t acc = (k | ai) != 0;
+            for (int rep = 0; rep < p.mma_reps; ++rep) {
+              const uint32_t d0 = tmem + T_Q, d1 = tmem + T_Q + 2 * JN;  // row tiles interleaved
+              if (p.ss) {
+                mma_w(d0, sdesc(st + 0 * TILE, 128, 256), bh, ID, acc);
+                mma_w(d1, sdesc(st + 1 * TILE, 128, 256), bh, ID, acc);
+                mma_w(d0, sdesc(st + 0 * TILE, 128, 256), bl, ID, 1);
+                mma_w(d1, sdesc(st + 1 * TILE, 128, 256), bl, ID, 1);
+                mma_w(d0, sdesc(st + 2 * TILE, 128, 256), bh, ID, 1);
+                mma_w(d1, sdesc(st + 3 * TILE, 128, 256), bh, ID, 1);
+              } else {
+                mma_ts_w(d0, ta + 0, bh, ID, acc);
+                mma_ts_w(d1, ta + 8, bh, ID, acc);
+                mma_ts_w(d0, ta + 0, bl, ID, 1);
+                mma_ts_w(d1, ta + 8, bl, ID, 1);
+                mma_ts_w(d0, ta + 16, bh, ID, 1);
+                mma_ts_w(d1, ta + 24, bh, ID, 1);
+              }
+            }
           }
-          commit(&sm->q_full);
-          issue_next();  // NS K-steps of the next product in flight during the SIMT phase
+          if (p.unicast) commit_w(&sm->empty[s]);
+          else commit_mc_w(&sm->empty[s], 0xFF);
         }
-        __syncwarp();
+        commit_w(&sm->q_full);
+        bwait(&sm->q_full, nq & 1);
+      } else if (warp == 1) {
+        // producer (decoupled from the MMA issuer: a lane's bulk-copy issue can
+        // stall it for hundreds of cycles): this product's remaining K-steps
+        // and the next product's first NS, each once its stage is free
+        for (int k = 0; k < NCH; ++k) issue_next();
       }
-      if (tid != 0) g_cons += NCH;
-      bwait(&sm->q_full, nq & 1);
+      g_cons += NCH;
+      named_sync(BAR_MATH, NT);  // the other warps block in hardware until the products are done
       ++nq;
       tc_after();
     };
 
     for (int t = 1; t <= p.T; ++t) {
+      stamp();
       scale(P);
+      stamp();
       product(P);
+      stamp();
       const float qs = (use_c && !textbook) ? icr : 1.0f;  // Algorithm 1: z = C^-1 P m
       tmem_ld<JN>(tQ, A);
       tmem_wait_ld();
@@ -1010,6 +1061,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       }
       col_partials(A, sm, warp);
       tmem_wait_st();
+      stamp();
       named_sync(BAR_MATH, NT);
       if (tid < JN) {  // beta_j, rz update (linsolve.py:284-288)
         const float rn = col_total(sm, tid);
@@ -1034,6 +1086,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
     }
 
     // ---- GX = A X - xi X from Q = A X'' (X = sa X'')
+    stamp();
     tmem_ld<JN>(tX, P);
     tmem_wait_ld();
     scale(P);
@@ -1070,6 +1123,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       }
       named_sync(BAR_MATH, NT);
     }
+    stamp();
     fro = warp_sum(fro);
     if (lane == 0) sm->dred[warp] = fro;
     named_sync(BAR_MATH, NT);
@@ -1174,17 +1228,22 @@ int lk_gram(const void* H, int64_t B, int M, double xi, const double* xi_b, void
   CUtensorMap pmap, smap;
   if (int e = make_hmap(&pmap, H, B, M, 2 * gram::BLK, gram::CH)) return e;
   if (int e = make_hmap(&smap, H, B, M, gram::BLK, gram::CH)) return e;
+  unsigned* zmax = (unsigned*)((char*)ws + 2 * al((size_t)B * 4));
   if (cudaMemsetAsync(rflag, 0, (size_t)B * sizeof(int), st) != cudaSuccess) return check_launch("lk flags");
+  if (cudaMemsetAsync(zmax, 0, (size_t)B * sizeof(unsigned), st) != cudaSuccess) return check_launch("lk zmax init");
   cudaFuncSetAttribute(gram::lk_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gram::SMEM);
   gram::lk_gram_kernel<<<(unsigned)(gram::TPR * B), gram::NT, gram::SMEM, st>>>(pmap, smap, M, sz, (float2*)A, xi,
-                                                                               xi_b, rflag, 0);
+                                                                               xi_b, rflag, zmax, 0);
   if (int e = check_launch("lk gram")) return e;
   lk_zmax_kernel<<<(unsigned)B, 512, 0, st>>>((const float4*)H, (int64_t)M * NC / 4, sz, rflag);
   if (int e = check_launch("lk zmax")) return e;
   gram::lk_gram_kernel<<<(unsigned)(gram::TPR * B), gram::NT, gram::SMEM, st>>>(pmap, smap, M, sz, (float2*)A, xi,
-                                                                               xi_b, rflag, 1);
+                                                                               xi_b, rflag, zmax, 1);
   return check_launch("lk gram fixup");
 }
+
+static long long* g_lk_trace = nullptr;
+void lk_debug_trace(void* p) { g_lk_trace = (long long*)p; }
 
 int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi, const double* xi_b, void* X,
              void* GX, double* part, int32_t* status, void* ws, cudaStream_t st) {
@@ -1194,7 +1253,12 @@ int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi
   int ncl = lk_clusters();
   if (ncl > 32) ncl = 32;
   if (ncl > B) ncl = (int)B;
-  pc::Params p{(const float2*)A, B, T, method, variant, xi, xi_b, (float2*)X, (float2*)GX, part, status, scratch};
+  const char* uc = getenv("XL_LK_UNICAST");
+  pc::Params p{(const float2*)A, B, T, method, variant, xi, xi_b, (float2*)X, (float2*)GX, part, status, scratch,
+               g_lk_trace, (uc && uc[0] == '1') ? 1 : 0, 1, 0, 0};
+  if (const char* sp = getenv("XL_LK_SPIN")) p.spin = sp[0] == '1';
+  if (const char* ss = getenv("XL_LK_SS")) p.ss = ss[0] == '1';
+  if (const char* mr = getenv("XL_LK_MMA_REPS")) p.mma_reps = atoi(mr) > 0 ? atoi(mr) : 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(pc::C * ncl), 1, 1);
   cfg.blockDim = dim3(pc::NT, 1, 1);
@@ -1216,20 +1280,13 @@ int lk_apply(const void* H, const void* X, const double* beta, int64_t B, int M,
              cudaStream_t st) {
   using namespace lk;
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  float* sz = (float*)((char*)ws + 2 * al((size_t)B * 4));
-  int* rflag = (int*)((char*)ws + 3 * al((size_t)B * 4));
+  const unsigned* zmax = (const unsigned*)((char*)ws + 2 * al((size_t)B * 4));  // from lk_gram
   CUtensorMap map;
   if (int e = make_hmap(&map, H, B, M, 2 * wk::BU, wk::CHA)) return e;
-  if (cudaMemsetAsync(rflag, 0, (size_t)B * sizeof(int), st) != cudaSuccess) return check_launch("lk w flags");
   cudaFuncSetAttribute(wk::lk_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wk::SMEM);
-  wk::lk_w_kernel<<<(unsigned)(wk::TPR * B), wk::NT, wk::SMEM, st>>>(map, M, sz, (const float2*)X, beta, (float*)W,
-                                                                     (float*)F, rflag, 0);
-  if (int e = check_launch("lk w")) return e;
-  lk_zmax_kernel<<<(unsigned)B, 512, 0, st>>>((const float4*)H, (int64_t)M * NC / 4, sz, rflag);
-  if (int e = check_launch("lk w zmax")) return e;
-  wk::lk_w_kernel<<<(unsigned)(wk::TPR * B), wk::NT, wk::SMEM, st>>>(map, M, sz, (const float2*)X, beta, (float*)W,
-                                                                     (float*)F, rflag, 1);
-  return check_launch("lk w fixup");
+  wk::lk_w_kernel<<<(unsigned)(wk::TPR * B), wk::NT, wk::SMEM, st>>>(map, M, zmax, (const float2*)X, beta, (float*)W,
+                                                                     (float*)F);
+  return check_launch("lk w");
 }
 
 }  // namespace xl

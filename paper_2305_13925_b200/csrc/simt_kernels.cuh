@@ -81,6 +81,7 @@ size_t lk_ws_bytes(int64_t B);
 int lk_gram(const void* H, int64_t B, int M, double xi, const double* xi_b, void* A, void* ws, cudaStream_t st);
 int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi, const double* xi_b, void* X,
              void* GX, double* part, int32_t* status, void* ws, cudaStream_t st);
+void lk_debug_trace(void* buf);
 int lk_apply(const void* H, const void* X, const double* beta, int64_t B, int M, void* W, void* F, void* ws,
              cudaStream_t st);
 

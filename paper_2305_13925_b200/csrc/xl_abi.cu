@@ -190,6 +190,7 @@ size_t xl_rzf_general_workspace_bytes(int dtype, int method, int64_t B, int32_t 
 
 static void* g_dbg_gram = nullptr;
 void xl_debug_set_gram_out(void* A) { g_dbg_gram = A; }
+void xl_debug_lk_trace(void* buf) { lk_debug_trace(buf); }
 
 // The general path over B realizations (workspace: simt_rzf_ws(B) + the
 // tensor-core sub-batch buffers).
