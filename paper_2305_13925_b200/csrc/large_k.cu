@@ -1255,9 +1255,9 @@ int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi
   if (ncl > B) ncl = (int)B;
   const char* uc = getenv("XL_LK_UNICAST");
   pc::Params p{(const float2*)A, B, T, method, variant, xi, xi_b, (float2*)X, (float2*)GX, part, status, scratch,
-               g_lk_trace, (uc && uc[0] == '1') ? 1 : 0, 1, 0, 0};
+               g_lk_trace, (uc && uc[0] == '1') ? 1 : 0, 1, 1, 0};
   if (const char* sp = getenv("XL_LK_SPIN")) p.spin = sp[0] == '1';
-  if (const char* ss = getenv("XL_LK_SS")) p.ss = ss[0] == '1';
+  if (const char* ss = getenv("XL_LK_SS")) p.ss = ss[0] == '1';  // default 1: A from shared memory (measured faster than tcgen05.cp + TMEM)
   if (const char* mr = getenv("XL_LK_MMA_REPS")) p.mma_reps = atoi(mr) > 0 ? atoi(mr) : 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(pc::C * ncl), 1, 1);
