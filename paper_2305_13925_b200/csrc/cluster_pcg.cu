@@ -175,16 +175,17 @@ __device__ __forceinline__ void write_b(const float (&v)[JH], const float* spx, 
 }
 
 // Q = A'' B (3xFP16: hi*hi + hi*lo + lo*hi), A'' in TMEM, B in smem; one thread.
+// warp-collective: all 32 lanes call it, tcgen05 ops elect one lane (tc_ptx.cuh)
 __device__ __forceinline__ void issue_q(uint32_t tmem, uint32_t ub, uint64_t* bar) {
   tc_after();
 #pragma unroll
   for (int s = 0; s < NC / 16; ++s) {
     const uint64_t dbh = sdesc(ub + 2 * s * LBOB, LBOB, 128), dbl = sdesc(ub + PART + 2 * s * LBOB, LBOB, 128);
-    mma_ts(tmem + T_Q, tmem + T_AH + 8 * s, dbh, ID_P, s != 0);
-    mma_ts(tmem + T_Q, tmem + T_AH + 8 * s, dbl, ID_P, 1);
-    mma_ts(tmem + T_Q, tmem + T_AL + 8 * s, dbh, ID_P, 1);
+    mma_ts_w(tmem + T_Q, tmem + T_AH + 8 * s, dbh, ID_P, s != 0);
+    mma_ts_w(tmem + T_Q, tmem + T_AH + 8 * s, dbl, ID_P, 1);
+    mma_ts_w(tmem + T_Q, tmem + T_AL + 8 * s, dbh, ID_P, 1);
   }
-  commit(bar);
+  commit_w(bar);
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) cluster_pcg_kernel(Params p) {
@@ -267,15 +268,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) cluster_pcg_k
   }
   fence_async_smem();
   __syncthreads();
-  if (tid == 0) {
+  if (warp == 0) {
     tc_after();
     const uint32_t ua = su32(pb);
 #pragma unroll
     for (int s = 0; s < NC / 16; ++s) {
-      tmem_cp(tmem + T_AH + 8 * s, sdesc(ua + 2 * s * 128, 128, SBOA));
-      tmem_cp(tmem + T_AL + 8 * s, sdesc(ua + PART + 2 * s * 128, 128, SBOA));
+      tmem_cp_w(tmem + T_AH + 8 * s, sdesc(ua + 2 * s * 128, 128, SBOA));
+      tmem_cp_w(tmem + T_AL + 8 * s, sdesc(ua + PART + 2 * s * 128, 128, SBOA));
     }
-    commit(&sm->cp_done);
+    commit_w(&sm->cp_done);
   }
 
   // ---- initial state (linsolve.py:224-229, 264-268): x = 0, r = I (Algorithm 1:
@@ -331,12 +332,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) cluster_pcg_k
     write_b(v, sm->spx, rg, h, pb);
     fence_async_smem();
     __syncthreads();
-    if (tid == 0) {
+    if (warp == 0) {
       constexpr uint32_t HALF = (ROWS / 8) * LBOB;
       const uint32_t off = rank * HALF;
-      mbar_expect_tx(&sm->pbar, 2 * HALF);
-      bulk_s2s(peer_pb + off, upb + off, HALF, peer_pbar);
-      bulk_s2s(peer_pb + PART + off, upb + PART + off, HALF, peer_pbar);
+      if (lane == 0) {
+        mbar_expect_tx(&sm->pbar, 2 * HALF);
+        bulk_s2s(peer_pb + off, upb + off, HALF, peer_pbar);
+        bulk_s2s(peer_pb + PART + off, upb + PART + off, HALF, peer_pbar);
+      }
+      __syncwarp();
       mbar_wait(&sm->pbar, nq & 1);
       issue_q(tmem, upb, &sm->q_full);
     }

@@ -225,7 +225,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
       fence_async_smem();
       named_sync(BAR_MATH, NMT);
       if (t == 1) stamp(k, 6);
-      if (mt == 0) issue_kxk<KU>(tmem + G::T_Q, uah, ual, ubh, ubl, &sm->q_full);
+      if (mt < 32) issue_kxk<KU>(tmem + G::T_Q, uah, ual, ubh, ubl, &sm->q_full);
       mbar_wait(&sm->q_full, nq & 1);
       ++nq;
       if (t == 1) stamp(k, 7);
@@ -354,7 +354,7 @@ __device__ __forceinline__ void math_role(const Params& p, Small* sm, uint8_t* a
     fence_async_smem();
     named_sync(BAR_MATH, NMT);
     stamp(k, 20);
-    if (mt == 0) issue_kxk<KU>(tmem + G::T_Q, uah, ual, ubh, ubl, &sm->q_full);
+    if (mt < 32) issue_kxk<KU>(tmem + G::T_Q, uah, ual, ubh, ubl, &sm->q_full);
     mbar_wait(&sm->q_full, nq & 1);
     ++nq;
     stamp(k, 21);

@@ -299,19 +299,20 @@ __device__ __forceinline__ void write_cols(const float* v, const float* scl, flo
 // Copy the K-major 128 x NC split A operand (hi, lo) from smem into TMEM
 // columns [t, t + NC/2) and [t + 64, t + 64 + NC/2).  Ordered before later
 // tcgen05.mma of the same thread.
+// Warp-collective (all 32 lanes, one elected lane issues: see tc_ptx.cuh).
 template <int KU>
 __device__ __forceinline__ void cp_A(uint32_t t, uint32_t ah, uint32_t al) {
   tc_after();
 #pragma unroll
   for (int s = 0; s < Geo<KU>::NC / 16; ++s) {
-    tmem_cp(t + 8 * s, pdesc<KU>(ah, s));
-    tmem_cp(t + 64 + 8 * s, pdesc<KU>(al, s));
+    tmem_cp_w(t + 8 * s, pdesc<KU>(ah, s));
+    tmem_cp_w(t + 64 + 8 * s, pdesc<KU>(al, s));
   }
 }
 
 // K x K tensor-core product Q = A'' * Bop (3xFP16), both operands in smem
 // (the TMEM A slot holds Xe of the previous realization while its W pass
-// streams), issued by one thread.
+// streams), issued by one warp (warp-collective: all 32 lanes call it).
 template <int KU>
 __device__ __forceinline__ void issue_kxk(uint32_t tq, uint32_t ah, uint32_t al, uint32_t bh, uint32_t bl,
                                           uint64_t* bar) {
@@ -321,11 +322,11 @@ __device__ __forceinline__ void issue_kxk(uint32_t tq, uint32_t ah, uint32_t al,
   for (int s = 0; s < G::NC / 16; ++s) {
     const uint64_t dah = pdesc<KU>(ah, s), dal = pdesc<KU>(al, s);
     const uint64_t dbh = bdesc<KU>(bh, s), dbl = bdesc<KU>(bl, s);
-    mma(tq, dah, dbh, G::ID_P, s != 0);
-    mma(tq, dah, dbl, G::ID_P, 1);
-    mma(tq, dal, dbh, G::ID_P, 1);
+    mma_w(tq, dah, dbh, G::ID_P, s != 0);
+    mma_w(tq, dah, dbl, G::ID_P, 1);
+    mma_w(tq, dal, dbh, G::ID_P, 1);
   }
-  commit(bar);
+  commit_w(bar);
 }
 
 #include "fused_math.cuh"
@@ -594,7 +595,8 @@ __global__ void __launch_bounds__(Lay<KU>::NT, 1) fused_rzf_kernel(Params p) {
     });
   } else if (warp == W_MMA) {
     // ------------------------------------------- streaming MMA issuer ------
-    if (lane == 0) {
+    // the whole warp runs the loop; tcgen05 instructions elect one lane
+    {
       uint32_t i = 0, wc = 0;
       uint32_t wuse[2] = {0, 0};
       for_items([&](uint32_t k, int pass, int64_t, bool has_next) {
@@ -615,21 +617,21 @@ __global__ void __launch_bounds__(Lay<KU>::NT, 1) fused_rzf_kernel(Params p) {
             if (dbg_bits(p) & 16) break;
             const uint64_t dh = sdesc(zh + 4 * ks * G::CMA, 2 * G::CMA, 128);
             const uint64_t dl = sdesc(zl + 4 * ks * G::CMA, 2 * G::CMA, 128);
-            mma(tmem + G::T_GRAM, dh, dh, G::ID_GRAM, (c | ks) != 0);
-            mma(tmem + G::T_GRAM, dh, dl, G::ID_GRAM, 1);            // XL_GRAM2: dl holds 2 Zl
-            if (!XL_GRAM2) mma(tmem + G::T_GRAM, dl, dh, G::ID_GRAM, 1);
+            mma_w(tmem + G::T_GRAM, dh, dh, G::ID_GRAM, (c | ks) != 0);
+            mma_w(tmem + G::T_GRAM, dh, dl, G::ID_GRAM, 1);            // XL_GRAM2: dl holds 2 Zl
+            if (!XL_GRAM2) mma_w(tmem + G::T_GRAM, dl, dh, G::ID_GRAM, 1);
           }
-          commit(&sm->stage_free[s]);
+          commit_w(&sm->stage_free[s]);
           item_stamp(i, 3);
         }
-        commit(&sm->gram_full);
+        commit_w(&sm->gram_full);
         stamp(k, 9);
         return;
        }
         mbar_wait(&sm->xe_ready, k & 1);
         stamp(k, 10);
         cp_A<KU>(tmem + G::T_XE, su32(aeh), su32(ael));  // Xe -> TMEM (A operand)
-        commit(&sm->xe_consumed);  // smem Xe may now be overwritten by A(k+1)
+        commit_w(&sm->xe_consumed);  // smem Xe may now be overwritten by A(k+1)
         for (int c = 0; c < nch; ++c, ++i, ++wc) {  // W^T = Xe^T Z^T
           const int s = i % NS;
           const int j = G::wsel(c, wc);
@@ -644,12 +646,12 @@ __global__ void __launch_bounds__(Lay<KU>::NT, 1) fused_rzf_kernel(Params p) {
 #pragma unroll
           for (int ks = 0; ks < NC / 16; ++ks) {
             const uint64_t dzh = sdesc(zh + 256 * ks, 128, 2 * G::CMA), dzl = sdesc(zl + 256 * ks, 128, 2 * G::CMA);
-            mma_ts(d, txe + 8 * ks, dzh, G::ID_W, ks != 0);
-            mma_ts(d, txe + 8 * ks, dzl, G::ID_W, 1);
-            mma_ts(d, txe + 64 + 8 * ks, dzh, G::ID_W, 1);
+            mma_ts_w(d, txe + 8 * ks, dzh, G::ID_W, ks != 0);
+            mma_ts_w(d, txe + 8 * ks, dzl, G::ID_W, 1);
+            mma_ts_w(d, txe + 64 + 8 * ks, dzh, G::ID_W, 1);
           }
-          commit(&sm->stage_free[s]);
-          commit(&sm->wfull[j]);
+          commit_w(&sm->stage_free[s]);
+          commit_w(&sm->wfull[j]);
           ++wuse[j];
           item_stamp(i, 3);
         }

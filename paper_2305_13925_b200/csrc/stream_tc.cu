@@ -192,8 +192,8 @@ __global__ void __launch_bounds__(NT, 1) gram_kernel(const float2* __restrict__ 
   float sz = fixup ? szv[b] : 1.0f;
   if (warp == W_PROD) {
     if (lane == 0) produce(H, b, M, ring, sm);
-  } else if (warp == W_MMA) {
-    if (lane == 0) {
+  } else if (warp == W_MMA) {  // the whole warp issues (tcgen05 ops elect one lane)
+    {
       for (int c = 0; c < nch; ++c) {
         const int s = c % NS;
         mbar_wait(&sm->conv_full[s], (c / NS) & 1);
@@ -204,14 +204,14 @@ __global__ void __launch_bounds__(NT, 1) gram_kernel(const float2* __restrict__ 
           const uint32_t o = 4 * ks * CMA;  // two groups per K-step
           const uint64_t bh = sdesc(zh + o, GS, 128), bl = sdesc(zl + o, GS, 128);
           const uint64_t a0 = bh, a1 = sdesc(zh + o + 16 * 128, GS, 128);
-          mma(tmem, a0, bh, ID_GRAM, (c | ks) != 0);
-          mma(tmem, a0, bl, ID_GRAM, 1);  // the lo tile holds 2 Zl
-          mma(tmem + 256, a1, bh, ID_GRAM, (c | ks) != 0);
-          mma(tmem + 256, a1, bl, ID_GRAM, 1);
+          mma_w(tmem, a0, bh, ID_GRAM, (c | ks) != 0);
+          mma_w(tmem, a0, bl, ID_GRAM, 1);  // the lo tile holds 2 Zl
+          mma_w(tmem + 256, a1, bh, ID_GRAM, (c | ks) != 0);
+          mma_w(tmem + 256, a1, bl, ID_GRAM, 1);
         }
-        commit(&sm->stage_free[s]);
+        commit_w(&sm->stage_free[s]);
       }
-      commit(&sm->done);
+      commit_w(&sm->done);
     }
   } else {
     const int cw = warp - W_CONV0;
@@ -385,23 +385,23 @@ __global__ void __launch_bounds__(NT, 1) w_kernel(const float2* __restrict__ H, 
     fence_async_smem();
   }
   __syncthreads();
-  if (tid == 32 * W_MMA) {
+  if (warp == W_MMA) {
     tc_after();
     const uint32_t ua = su32(ring);
 #pragma unroll
     for (int s = 0; s < NC / 16; ++s) {
-      tmem_cp(tmem + T_AH + 8 * s, sdesc(ua + 2 * s * 128, 128, SBOA));
-      tmem_cp(tmem + T_AL + 8 * s, sdesc(ua + 16 * SBOA + 2 * s * 128, 128, SBOA));
+      tmem_cp_w(tmem + T_AH + 8 * s, sdesc(ua + 2 * s * 128, 128, SBOA));
+      tmem_cp_w(tmem + T_AL + 8 * s, sdesc(ua + 16 * SBOA + 2 * s * 128, 128, SBOA));
     }
-    commit(&sm->cp_done);
+    commit_w(&sm->cp_done);
   }
   if (warp == W_PROD) {
     if (lane == 0) {
       mbar_wait(&sm->cp_done, 0);  // the staging tile (ring) has been copied
       produce(H, b, M, ring, sm);
     }
-  } else if (warp == W_MMA) {
-    if (lane == 0) {
+  } else if (warp == W_MMA) {  // the whole warp issues (tcgen05 ops elect one lane)
+    {
       for (int c = 0; c < nch; ++c) {
         const int s = c % NS, jb = c & 1;
         if (c >= 2) mbar_wait(&sm->acc_free[jb], ((c >> 1) - 1) & 1);
@@ -412,12 +412,12 @@ __global__ void __launch_bounds__(NT, 1) w_kernel(const float2* __restrict__ H, 
 #pragma unroll
         for (int ks = 0; ks < NC / 16; ++ks) {
           const uint64_t dzh = sdesc(zh + 256 * ks, 128, GS), dzl = sdesc(zl + 256 * ks, 128, GS);
-          mma_ts(d, tmem + T_AH + 8 * ks, dzh, ID_W, ks != 0);
-          mma_ts(d, tmem + T_AH + 8 * ks, dzl, ID_W, 1);
-          mma_ts(d, tmem + T_AL + 8 * ks, dzh, ID_W, 1);
+          mma_ts_w(d, tmem + T_AH + 8 * ks, dzh, ID_W, ks != 0);
+          mma_ts_w(d, tmem + T_AH + 8 * ks, dzl, ID_W, 1);
+          mma_ts_w(d, tmem + T_AL + 8 * ks, dzh, ID_W, 1);
         }
-        commit(&sm->stage_free[s]);
-        commit(&sm->acc_full[jb]);
+        commit_w(&sm->stage_free[s]);
+        commit_w(&sm->acc_full[jb]);
       }
     }
   } else {
