@@ -149,34 +149,7 @@ __global__ void scale_copy_kernel(const float2* __restrict__ W, float2* __restri
   }
 }
 
-// W <- beta W (and F <- the unscaled product when requested), complex128
-__global__ void scale_c128_kernel(double2* __restrict__ W, double2* __restrict__ F, const double* __restrict__ beta,
-                                  int64_t per, int64_t total) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const double s = beta[e / per];
-    const double2 w = W[e];
-    if (F) F[e] = w;
-    W[e] = make_double2(w.x * s, w.y * s);
-  }
-}
 
-__global__ void herm_add_kernel(double2* __restrict__ A, int K, const double* __restrict__ xi_b, double xi) {
-  // (P + P^H)/2 + xi I on the ZGEMM result (precoder.py:59-60)
-  const int64_t b = blockIdx.x;
-  double2* a = A + b * (int64_t)K * K;
-  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < K * K; e += gridDim.y * blockDim.x) {
-    const int i = e / K, j = e % K;
-    if (j > i) continue;
-    const double2 p = a[(int64_t)i * K + j], q = a[(int64_t)j * K + i];
-    if (i == j) {
-      a[e] = make_double2(p.x + (xi_b ? xi_b[b] : xi), 0.0);
-    } else {
-      const double re = 0.5 * (p.x + q.x), im = 0.5 * (p.y - q.y);
-      a[(int64_t)i * K + j] = make_double2(re, im);
-      a[(int64_t)j * K + i] = make_double2(re, -im);
-    }
-  }
-}
 
 
 // ---------------------------------------------------------------------------
@@ -660,17 +633,10 @@ int tc_gram(int dtype, const void* H, int64_t Bc, int M, int K, const double* xi
   cublasSetWorkspace(h, p, CUBLAS_WS);
   p += CUBLAS_WS;
   if (dtype == XL_C128) {
-    const cuDoubleComplex one = make_cuDoubleComplex(1, 0), zero = make_cuDoubleComplex(0, 0);
-    // column-major C = H_cm H_cm^H (K x K) has the memory of row-major H^H H
-    int e = cublas_check(cublasZgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_C, K, K, M, &one,
-                                                   (const cuDoubleComplex*)H, K, (long long)M * K,
-                                                   (const cuDoubleComplex*)H, K, (long long)M * K, &zero,
-                                                   (cuDoubleComplex*)A, K, (long long)K * K, (int)Bc),
-                         "tc gram zgemm");
-    if (e) return e;
-    const unsigned gk = grid_for((int64_t)K * K, 256);
-    herm_add_kernel<<<dim3((unsigned)Bc, gk > 64 ? 64 : gk), 256, 0, st>>>((double2*)A, K, xi_b, xi);
-    return check_launch("tc herm");
+    // A = H^H H + xi I on the FP64 tensor cores (dmma.cu): lower-triangle tiles,
+    // written with their conjugate mirror -- Hermitian by construction
+    return zgemm_dmma(1, H, (int64_t)M * K, K, 0, H, (int64_t)M * K, K, A, (int64_t)K * K, K, K, K, M, Bc, 2,
+                      nullptr, nullptr, xi_b, xi, st);
   }
   const int n2 = 2 * K;
   float* S = (float*)p;
@@ -717,18 +683,9 @@ int tc_apply(int dtype, const void* H, const void* X, const double* beta, int64_
   cublasSetWorkspace(h, p, CUBLAS_WS);
   p += CUBLAS_WS;
   if (dtype == XL_C128) {
-    // W_cm (K x M) = X_mem (col-major view = X^T) . H_cm: the memory of row-major H X;
-    // beta applied by the epilogue kernel below
-    const cuDoubleComplex one = make_cuDoubleComplex(1, 0), zero = make_cuDoubleComplex(0, 0);
-    int e = cublas_check(cublasZgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, K, M, K, &one,
-                                                   (const cuDoubleComplex*)X, K, (long long)K * K,
-                                                   (const cuDoubleComplex*)H, K, (long long)M * K, &zero,
-                                                   (cuDoubleComplex*)W, K, (long long)M * K, (int)Bc),
-                         "tc apply zgemm");
-    if (e) return e;
-    const int64_t per = (int64_t)M * K, total = Bc * per;
-    scale_c128_kernel<<<grid_for(total, 256), 256, 0, st>>>((double2*)W, (double2*)F, beta, per, total);
-    return check_launch("tc scale");
+    // W = beta H X (F = H X) on the FP64 tensor cores (dmma.cu)
+    return zgemm_dmma(0, H, (int64_t)M * K, K, 0, X, (int64_t)K * K, K, W, (int64_t)M * K, K, M, K, K, Bc, 1, beta,
+                      F, nullptr, 0.0, st);
   }
   const int n2 = 2 * K;
   float* S = (float*)p;
@@ -858,20 +815,14 @@ bool tc_pcg64_supported(int K) { return 2 * K <= 32 * 2 * PCG_V64; }
 // A is A), then the per-column update; X out row-major.
 int tc_pcg64(int method, int variant, const void* A, int64_t B, int K, int T, void* X, int32_t* status, void* cws,
              void* bufs, cudaStream_t st) {
-  cublasHandle_t h = handle_for_device();
-  if (!h) { set_error("cublasCreate failed"); return XL_ERR_CUDA; }
-  cublasSetStream(h, st);
-  cublasSetWorkspace(h, cws, CUBLAS_WS);
+  (void)cws;
   const PcgState64 s = pcg_state64((char*)bufs, B, K);
   pcg_init64_kernel<<<(unsigned)B, 256, 0, st>>>((const double2*)A, s, K, method, variant, status);
   if (int e = check_launch("tc pcg64 init")) return e;
-  const cuDoubleComplex one = make_cuDoubleComplex(1, 0), zero = make_cuDoubleComplex(0, 0);
   const long long sk = (long long)K * K;
   for (int t = 1; t <= T; ++t) {
-    int e = cublas_check(cublasZgemmStridedBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, K, K, K, &one,
-                                                   (const cuDoubleComplex*)A, K, sk, (const cuDoubleComplex*)s.P, K,
-                                                   sk, &zero, (cuDoubleComplex*)s.Q, K, sk, (int)B),
-                         "tc pcg64 zgemm");
+    // column-major Q = A P: in row-major views Q^T = P^T A^T (dmma.cu, opB = T)
+    int e = zgemm_dmma(0, s.P, sk, K, 1, A, sk, K, s.Q, sk, K, K, K, K, B, 0, nullptr, nullptr, nullptr, 0.0, st);
     if (e) return e;
     pcg_update64_kernel<<<(unsigned)B, 256, 0, st>>>(s, K, method, variant, status);
     if ((e = check_launch("tc pcg64 update"))) return e;
@@ -884,17 +835,10 @@ int tc_pcg64(int method, int variant, const void* A, int64_t B, int K, int T, vo
 // After tc_pcg64: GX = (A - xi I) X and the ||F||^2 partials per 32 x 32 tile.
 int tc_gx64(const void* A, const double* xi_b, double xi, int64_t B, int K, void* GX, double* part, void* cws,
             void* bufs, cudaStream_t st) {
-  cublasHandle_t h = handle_for_device();
-  if (!h) { set_error("cublasCreate failed"); return XL_ERR_CUDA; }
-  cublasSetStream(h, st);
-  cublasSetWorkspace(h, cws, CUBLAS_WS);
+  (void)cws;
   const PcgState64 s = pcg_state64((char*)bufs, B, K);
-  const cuDoubleComplex one = make_cuDoubleComplex(1, 0), zero = make_cuDoubleComplex(0, 0);
   const long long sk = (long long)K * K;
-  int e = cublas_check(cublasZgemmStridedBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, K, K, K, &one, (const cuDoubleComplex*)A,
-                                                 K, sk, (const cuDoubleComplex*)s.X, K, sk, &zero,
-                                                 (cuDoubleComplex*)s.Q, K, sk, (int)B),
-                       "tc gx64 zgemm");
+  int e = zgemm_dmma(0, s.X, sk, K, 1, A, sk, K, s.Q, sk, K, K, K, K, B, 0, nullptr, nullptr, nullptr, 0.0, st);
   if (e) return e;
   const unsigned nt = (unsigned)((K + XT - 1) / XT);
   cm_to_rm64_kernel<<<dim3((unsigned)B, nt, nt), 256, 0, st>>>(s.X, s.Q, K, xi_b, xi, (double2*)GX, part);

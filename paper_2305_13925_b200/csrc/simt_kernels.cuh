@@ -85,6 +85,13 @@ void lk_debug_trace(void* buf);
 int lk_apply(const void* H, const void* X, const double* beta, int64_t B, int M, void* W, void* F, void* ws,
              cudaStream_t st);
 
+// dmma.cu: batched complex128 GEMM on the FP64 tensor cores (row-major;
+// opA 0 = N, 1 = conjugate transpose; opB 0 = N, 1 = transpose; epi 0 store,
+// 1 = beta scale (+ unscaled copy F), 2 = Hermitian lower tiles + mirror + xi I)
+int zgemm_dmma(int opA, const void* A, int64_t sA, int lda, int opB, const void* B, int64_t sB, int ldb, void* C,
+               int64_t sC, int ldc, int M, int N, int K, int64_t batch, int epi, const double* beta, void* F,
+               const double* xi_b, double xi, cudaStream_t st);
+
 int launch_ber(int dtype, const void* Bc, const int8_t* bits, const void* noise, int64_t B, int K,
                int nsym, int64_t* errors, cudaStream_t st);
 
