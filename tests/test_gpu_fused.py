@@ -197,3 +197,47 @@ def test_concurrent_streams_use_separate_workspaces():
     torch.cuda.synchronize()
     assert torch.equal(o1.W, ref1.W) and torch.equal(o2.W, ref2.W)
     assert torch.equal(o1.sum_se, ref1.sum_se) and torch.equal(o2.sum_se, ref2.sum_se)
+
+
+def test_host_pipeline_reruns_range_rows():
+    """The host-buffer API keeps rzf_batched(check=True)'s contract: a
+    realization the fused kernel flags XL_STATUS_RANGE is re-run on the
+    general kernels and its W / sum-SE / status scattered back."""
+    m = X.ChannelModel(S=4, K=16, p=1.0, r=0.5)
+    H = X.generate_channels(m, seed=5, first=0, B=5, dtype=torch.complex64)
+    H[3, 192:] *= 1e4
+    Hh = H.cpu().pin_memory()
+    Wh = torch.empty_like(Hh).pin_memory()
+    Sh = torch.empty(5, dtype=torch.float64).pin_memory()
+    Sth = torch.empty(5, dtype=torch.int32).pin_memory()
+    pipe = BT.HostPipeline(m.M, m.K, chunk=2)
+    pipe.run(Hh, Wh, Sh, Sth, 1.6, 10.0, "jacpcg", 4)
+    assert Sth.tolist() == [0] * 5
+    ref = BT.rzf_batched(H, 1.6, 10.0, T=4)
+    assert torch.equal(Wh, ref.W.cpu()) and torch.equal(Sh, ref.sum_se.cpu())
+    # per-realization xi through the pipeline (sliced per chunk)
+    xi = torch.linspace(1.0, 2.0, 5, dtype=torch.float64)
+    pipe.run(Hh, Wh, Sh, Sth, xi, 10.0, "jacpcg", 4)
+    ref = BT.rzf_batched(H, xi.cuda(), 10.0, T=4)
+    assert torch.equal(Wh, ref.W.cpu()) and Sth.tolist() == [0] * 5
+
+
+def test_out_buffers_and_xi_are_checked():
+    """Caller-provided outputs are validated before their pointers reach the
+    kernels; per-realization xi must be positive (precoder.py:55-56)."""
+    from paper_2305_13925_b200.errors import ConfigurationError
+    m = X.ChannelModel(S=4, K=16, p=1.0, r=0.5)
+    H = X.generate_channels(m, seed=5, first=0, B=4, dtype=torch.complex64)
+    bad = BT.alloc_outputs(H[:3])
+    with pytest.raises(ConfigurationError):
+        BT.rzf_batched(H, 1.6, 10.0, out=bad)
+    wrong = BT.alloc_outputs(H)
+    wrong.beta = torch.empty(4, dtype=torch.float32, device=H.device)
+    with pytest.raises(ConfigurationError):
+        BT.rzf_batched(H, 1.6, 10.0, out=wrong)
+    with pytest.raises(ConfigurationError):
+        BT.rzf_batched(H, torch.tensor([1.0, 0.0, 1.0, 1.0], device=H.device), 10.0)
+    # the range re-run indexes the device copy of a CPU-tensor xi
+    H[1, 192:] *= 1e4
+    out = BT.rzf_batched(H, torch.tensor([1.6, 1.7, 1.8, 1.9], dtype=torch.float64), 10.0, T=4)
+    assert out.status.cpu().tolist() == [0, 0, 0, 0]
