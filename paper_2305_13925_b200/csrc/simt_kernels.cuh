@@ -92,6 +92,12 @@ int zgemm_dmma(int opA, const void* A, int64_t sA, int lda, int opB, const void*
                int64_t sC, int ldc, int M, int N, int K, int64_t batch, int epi, const double* beta, void* F,
                const double* xi_b, double xi, cudaStream_t st);
 
+// fused_c128.cu: one CTA per realization, whole chain on chip, DMMA products (K in {16, 32})
+bool fc128_supported(int dtype, int method, int M, int K);
+int fc128_rzf(int method, int variant, const void* H, int64_t B, int M, int K, double xi, const double* xi_b,
+              double power, int T, double sigma2, void* W, void* F, double* beta, double* gamma, double* sum_se,
+              void* X, int32_t* status, cudaStream_t st);
+
 int launch_ber(int dtype, const void* Bc, const int8_t* bits, const void* noise, int64_t B, int K,
                int nsym, int64_t* errors, cudaStream_t st);
 

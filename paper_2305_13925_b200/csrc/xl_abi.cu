@@ -337,6 +337,10 @@ static int rzf_impl(bool allow_fused, int dtype, int method, int variant, const 
     return launch_fused(dtype, method, variant, H, B, M, K, xi, xi_per_batch, power, T,
                         sigma2, W, F, beta, gamma, sum_se, X, status, workspace, ws_bytes,
                         g_dbg_gram, st);
+  // complex128, K in {16, 32}: one fused DMMA kernel per realization (cfg1)
+  if (allow_fused && fc128_supported(dtype, method, M, K))
+    return fc128_rzf(method, variant, H, B, M, K, xi, xi_per_batch, power, T, sigma2, W, F, beta, gamma, sum_se, X,
+                     status, st);
 
   // ---- general path: Gram -> solve -> GX, beta -> W = beta H X -> SINR
   return general_path(dtype, method, variant, H, B, M, K, xi, xi_per_batch, power, T, sigma2, W, F, beta,
