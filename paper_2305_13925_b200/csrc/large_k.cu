@@ -295,15 +295,21 @@ __global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ 
   const uint32_t tmem = sm->tmem_slot;
 
   if (warp == W_PROD) {
-    if (lane == 0) {
+    // one lane per box of a chunk: a lane's TMA copies are serviced about one
+    // at a time (tools/microbench/bulk_rules.cu), so boxes go out in parallel
+    const int nbx = (hp ? 1 : 0) + pl.ns;
+    if (lane < nbx) {
       const int y0 = (int)(b * M);
       for (int c = 0; c < nch; ++c) {
         const int s = c % NS;
-        if (c >= NS) bwait(&sm->freed[s], ((c / NS) - 1) & 1);
-        mbar_expect_tx(&sm->full[s], stage_bytes);
+        if (c >= NS) bwait<true>(&sm->freed[s], ((c / NS) - 1) & 1);
+        if (lane == 0) mbar_expect_tx(&sm->full[s], stage_bytes);
         uint8_t* st = ring + s * SB;
-        if (hp) tma2d(st, &pmap, BLK * pl.pb, y0 + c * CH, &sm->full[s]);
-        for (int j = 0; j < pl.ns; ++j) tma2d(st + soff + j * SGL, &smap, BLK * pl.sb[j], y0 + c * CH, &sm->full[s]);
+        if (hp && lane == 0) tma2d(st, &pmap, BLK * pl.pb, y0 + c * CH, &sm->full[s]);
+        else {
+          const int j = lane - (hp ? 1 : 0);
+          tma2d(st + soff + j * SGL, &smap, BLK * pl.sb[j], y0 + c * CH, &sm->full[s]);
+        }
       }
     }
   } else if (warp == W_MMA) {  // the whole warp issues (mma_w elects one lane)
@@ -564,11 +570,14 @@ __global__ void __launch_bounds__(NT, 1) lk_w_kernel(const __grid_constant__ CUt
   __syncthreads();
 
   if (warp == W_PROD) {
-    if (lane == 0) {
+    // lane l issues boxes g = l mod 8: a lane's TMA copies are serviced about
+    // one at a time (tools/microbench/bulk_rules.cu), 8 lanes keep 8 in flight
+    constexpr int NL = 8;
+    if (lane < NL) {
       const int y0 = (int)(b * M);
-      for (int g = 0; g < nbox; ++g) {
+      for (int g = lane; g < nbox; g += NL) {
         const int s = g % NS, tt = g / (KU / BU), kb = g % (KU / BU);
-        if (g >= NS) bwait(&sm->freed[s], ((g / NS) - 1) & 1);
+        if (g >= NS) bwait<true>(&sm->freed[s], ((g / NS) - 1) & 1);
         mbar_expect_tx(&sm->full[s], BOX);
         tma2d(ring + s * BOX, &hmap, 2 * BU * kb, y0 + CHA * tt, &sm->full[s]);
       }
@@ -815,7 +824,8 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
     const int s = g_prod % NS, k = n_issued % NCH;
     const uint8_t* src = slot + (size_t)k * CHUNK;
     if (lane == 0) {
-      if (g_prod >= NS) bwait(&sm->empty[s], ((g_prod / NS) - 1) & 1);
+      if (g_prod >= NS) bwait<true>(&sm->empty[s], ((g_prod / NS) - 1) & 1);
+      if (p.trace && cid == 0 && rank == 0 && g_prod < 64) p.trace[128 + g_prod] = clock64();
       mbar_expect_tx(&sm->full[s], CHUNK);
       if (p.unicast) bulk_g2s(ring + s * CHUNK, src, CHUNK, &sm->full[s], policy_evict_normal());
       else if ((k & (C - 1)) == (int)rank) bulk_mc(ring + s * CHUNK, src, CHUNK, &sm->full[s], 0xFF);
@@ -828,7 +838,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
   const bool tr = p.trace && cid == 0 && rank == 0 && tid == 0;
   int ntr = 0;
   auto stamp = [&]() {
-    if (tr && ntr < 255) p.trace[ntr++] = clock64();
+    if (tr && ntr < 128) p.trace[ntr++] = clock64();
   };
   for (int64_t b = cid; b < p.B; b += ncl) {
     const float2* a = p.A + b * (int64_t)KU * KU;
@@ -884,7 +894,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
     stamp();
     if (warp == 1) {  // the producer warp of the product phases
       n_issued = 0;
-      n_total = (p.T + 1) * NCH;
+      n_total = p.T * NCH;  // T products (GX comes from the residual)
       for (int i = 0; i < NS; ++i) issue_next();
     }
 
@@ -963,15 +973,23 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
           const int s = gc % NS;
           if (p.spin) bwait<true>(&sm->full[s], (gc / NS) & 1);
           else bwait(&sm->full[s], (gc / NS) & 1);
+          if (p.trace && cid == 0 && rank == 0 && lane == 0 && gc < 64) p.trace[192 + gc] = clock64();
           tc_after();
+          if (!p.ss) {  // TMEM A operand: copy the chunk, then free its stage at once
+#pragma unroll
+            for (int ai = 0; ai < 2; ++ai) {
+              const uint32_t st = su32(ring + s * CHUNK + ai * HALF);
+              const uint32_t ta = tmem + T_A + 32 * ((2 * gc + ai) & 3);
+#pragma unroll
+              for (int x = 0; x < 4; ++x) tmem_cp_w(ta + 8 * x, sdesc(st + x * TILE, 128, 256));
+            }
+            if (p.unicast) commit_w(&sm->empty[s]);
+            else commit_mc_w(&sm->empty[s], 0xFF);
+          }
 #pragma unroll
           for (int ai = 0; ai < 2; ++ai) {
             const uint32_t st = su32(ring + s * CHUNK + ai * HALF);
             const uint32_t ta = tmem + T_A + 32 * ((2 * gc + ai) & 3);
-            if (!p.ss) {
-#pragma unroll
-              for (int x = 0; x < 4; ++x) tmem_cp_w(ta + 8 * x, sdesc(st + x * TILE, 128, 256));
-            }
             const uint32_t bo = upb + 2 * k * LBOB + (ai ? 0 : JN / 8 * 128);  // B2 = [-Pi | Pr], B1 = [Pr | Pi]
             const uint64_t bh = sdesc(bo, LBOB, 128), bl = sdesc(bo + PART, LBOB, 128);
             const uint32_t acc = (k | ai) != 0;
@@ -994,8 +1012,10 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
               }
             }
           }
-          if (p.unicast) commit_w(&sm->empty[s]);
-          else commit_mc_w(&sm->empty[s], 0xFF);
+          if (p.ss) {
+            if (p.unicast) commit_w(&sm->empty[s]);
+            else commit_mc_w(&sm->empty[s], 0xFF);
+          }
         }
         commit_w(&sm->q_full);
         bwait(&sm->q_full, nq & 1);
@@ -1085,26 +1105,24 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       }
     }
 
-    // ---- GX = A X - xi X from Q = A X'' (X = sa X'')
+    // ---- GX = A X - xi X without another product: the recursively updated
+    // residual is r = I - A X (textbook / CG) or C^-1 (I - A X) (Algorithm 1),
+    // so A X = I - C r (C = I unless Algorithm 1); X = sa X''
     stamp();
     tmem_ld<JN>(tX, P);
-    tmem_wait_ld();
-    scale(P);
-    product(P);
-    tmem_ld<JN>(tQ, A);
+    tmem_ld<JN>(tR, A);
     tmem_wait_ld();
     double fro = 0.0;
     const double xsa = alpha * (double)sa;
+    const float crr = (use_c && !textbook) ? cr : 1.0f;
 #pragma unroll
-    for (int c0 = 0; c0 < JN; c0 += 8) {
-      float sy[8];
-      lds8(sm->spy + c0, sy);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float g = (float)((double)(A[c0 + i] * sy[i]) - xsa * (double)P[c0 + i]);
-        A[c0 + i] = g;
-        fro += (double)(P[c0 + i] * sa) * (double)g;  // Re tr(X^H GX)
-      }
+    for (int jj = 0; jj < JN; ++jj) {
+      const int jg = JN * (int)rank + jj;
+      const float e = (part == 0 && u == jg) ? 1.0f : 0.0f;
+      const float ax = e - crr * A[jj];
+      const float g = (float)((double)ax - xsa * (double)P[jj]);
+      A[jj] = g;
+      fro += (double)(P[jj] * sa) * (double)g;  // Re tr(X^H GX)
     }
     // ---- outputs staged in the (idle: every chunk of this realization has
     // landed and been consumed) ring as [user][column][re, im] with an odd row

@@ -30,3 +30,11 @@ per = len(labels)
 for i in range(1, min(n, 2 * per)):
     print(f"{labels[i % per]:>12s} +{t[i] - t[i - 1]:8d} cycles")
 print("realization:", t[per] - t[0] if n > per else None, "cycles")
+
+# per-chunk: producer issue time (after its empty wait) and consumer landing time
+iss = t[128:192]
+lnd = t[192:256]
+print("chunk  issue->land  land gap")
+for n in range(1, 48):
+    if iss[n] and lnd[n]:
+        print(f"{n:5d} {lnd[n] - iss[n]:10d} {lnd[n] - lnd[n - 1]:9d}")
