@@ -186,3 +186,24 @@ def test_fused_gain_spread(K, spread_db):
          max_user_column=col)
     assert we.max() <= 1e-4 and se.max() <= 1e-4, (we.max(), se.max())
     assert col <= 1e-3, col
+
+
+def test_se_vs_m_rows_vs_oracle(tmp_path):
+    """The se_vs_m experiment rows (experiments.py:73-80) from the batched
+    path: per M, every method on one paired batch, ergodic mean / SEM."""
+    from paper_2305_13925_b200 import experiments as E
+    K, trials, T, snr = 16, 48, 4, 10.0
+    model_for_m = lambda M: X.ChannelModel(S=M // 64, K=K, p=0.5, r=0.5)  # noqa: E731
+    rows = list(E.rows_se_vs_m(model_for_m, [128, 256], ["jacpcg", "cg", "direct"], trials, T, snr, seed=3))
+    assert [r[:2] for r in rows] == [[128, "jacpcg"], [128, "cg"], [128, "direct"],
+                                     [256, "jacpcg"], [256, "cg"], [256, "direct"]]
+    for M, method, mean, sem, n in rows:
+        m = model_for_m(M)
+        H = O.generate_channels(3 + 1_000_003 * M, 0, trials, m.S, m.K, m.p, m.r, Ms=m.Ms)
+        H = H.astype(np.complex64).astype(np.complex128)
+        s = np.array([O.precoder_and_se(h, K / 10 ** (snr / 10), 10 ** (snr / 10), 1.0, method, T,
+                                        "textbook")[3] for h in H])
+        rm, rs = O.sum_se(s)
+        assert n == trials and abs(mean - rm) <= 1e-4 * abs(rm) and abs(sem - rs) <= 1e-3 * rs, (M, method)
+    out = E.write_experiment("se_vs_m", iter(rows), str(tmp_path / "se.csv"), {"K": K}, 3)
+    assert open(out).read().splitlines()[0] == "M,method,mean_sum_se,sem,trials"
