@@ -422,25 +422,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) cluster_pcg_k
     }
   }
 
-  // ---- GX = A X - xi X from Q = A'' (X'' scaled per column); X = sa X''
+  // ---- GX = A X - xi X without another product: the recursively updated
+  // residual is r = I - A X (textbook / CG) or C^-1 (I - A X) (Algorithm 1),
+  // so A X = I - C r (C = I unless Algorithm 1); X = sa X''
 #pragma unroll
   for (int jj = 0; jj < JH; ++jj) P[jj] = xs[(h * JH + jj) * ROWS + r];
-  pair_scale(P);
-  product(P);
-  tmem_ld<JH>(tQ, A);
+  tmem_ld<JH>(tR, A);
   tmem_wait_ld();
   double fro = 0.0;
   const double xsa = alpha * (double)sa;
+  const float crr = (use_c && !textbook) ? cr : 1.0f;
 #pragma unroll
-  for (int c0 = 0; c0 < JH; c0 += 8) {
-    float sy[8];
-    lds8(sm->spy + h * JH + c0, sy);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float g = (float)((double)(A[c0 + i] * sy[i]) - xsa * (double)P[c0 + i]);
-      A[c0 + i] = g;
-      fro += (double)(P[c0 + i] * sa) * (double)g;  // Re tr(X^H GX), X = sa X''
-    }
+  for (int jj = 0; jj < JH; ++jj) {
+    const float e = (rg == 2 * (h * JH + jj)) ? 1.0f : 0.0f;
+    const float g = (float)((double)(e - crr * A[jj]) - xsa * (double)P[jj]);
+    A[jj] = g;
+    fro += (double)(P[jj] * sa) * (double)g;  // Re tr(X^H GX), X = sa X''
   }
   // row-major complex outputs: lanes (2m, 2m+1) hold (Re, Im) of user kr;
   // the even lane stores column pairs 4n, 4n+1 and the odd lane 4n+2, 4n+3
