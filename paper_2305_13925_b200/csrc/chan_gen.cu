@@ -265,11 +265,193 @@ chan_real_kernel(uint64_t seed, int64_t first, int S, int Ms, int K, double p,
   }
 }
 
+// complex64, Ms = 64: chan_real_kernel with y = R^{1/2} g on the tensor cores
+// (mma.sync m16n8k8 TF32, 3xTF32: R^{1/2} = Rh + Rl, g = gh + gl, y = Rh gh +
+// Rh gl + Rl gh with fp32 accumulation, ~1e-7 relative -- the SIMT FFMA loop
+// was 55% of the kernel's instructions).  Per subarray and chunk of <= 64
+// visible users the (64 x 64) x (64 x 2 users) real product is 4 x 16 output
+// tiles of 16 x 8 over the 8 warps (two column tiles each, all four row tiles).
+__device__ __forceinline__ uint32_t tf32_of(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+constexpr int TC_MS = 64, TC_RS = TC_MS + 4, TC_GS = 2 * KCH + 4;  // padded row strides (floats)
+
+__global__ void __launch_bounds__(256, 2)
+chan_tc_kernel(uint64_t seed, int64_t first, int S, int K, double p, const double* __restrict__ Rsqrt,
+               double beta_bar, double dmin, double dmax, float2* __restrict__ H, int32_t* __restrict__ status) {
+  constexpr int Ms = TC_MS;
+  const int64_t bl = blockIdx.x;
+  const uint64_t bg = (uint64_t)(first + bl);
+  const uint32_t b_lo = (uint32_t)bg, b_hi = (uint32_t)(bg >> 32);
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  const int M = S * Ms;
+  extern __shared__ double smem[];
+  uint32_t* rsh = (uint32_t*)smem;                 // [Ms][TC_RS] tf32 hi of R^{1/2}
+  uint32_t* rsl = rsh + Ms * TC_RS;                // lo
+  float* gf = (float*)(rsl + Ms * TC_RS);          // [Ms][TC_GS]: (Re, Im) of the chunk's users
+  float* amp = gf + Ms * TC_GS;                    // K
+  uint32_t* vis = (uint32_t*)(amp + ((K + 3) & ~3));
+  const int sw = (S + 31) / 32;
+  int* vlist = (int*)(vis + ((K * sw + 3) & ~3));  // K compacted user indices
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < Ms * Ms; e += blockDim.x) {
+    const float x = (float)Rsqrt[e];
+    const uint32_t h = tf32_of(x);
+    rsh[(e / Ms) * TC_RS + e % Ms] = h;
+    rsl[(e / Ms) * TC_RS + e % Ms] = tf32_of(x - __uint_as_float(h));
+  }
+  const int nq = (S + 3) / 4;
+  for (int k = tid; k < K; k += blockDim.x) {
+    uint4 x = philox4x32_10(make_uint4(0u, (uint32_t)k | (PURPOSE_DIST << 24), b_lo, b_hi), k0, k1);
+    double d = dmin + (dmax - dmin) * u01(x.x);
+    double bdb = -35.3 - 37.6 * log10(d);
+    double gain = pow(10.0, bdb / 10.0) / beta_bar;
+    bool found = false;
+    for (int att = 0; att < MAX_VIS_ATTEMPTS && !found; ++att) {
+      for (int w = 0; w < sw; ++w) vis[k * sw + w] = 0u;
+      for (int q = 0; q < nq; ++q) {
+        uint4 y = philox4x32_10(make_uint4((uint32_t)(att * nq + q), (uint32_t)k | (PURPOSE_VIS << 24), b_lo, b_hi), k0, k1);
+        uint32_t wv[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          int ss = 4 * q + e;
+          if (ss < S && u01(wv[e]) < p) {
+            vis[k * sw + (ss >> 5)] |= 1u << (ss & 31);
+            found = true;
+          }
+        }
+      }
+    }
+    if (!found) status[bl] = XL_STATUS_NO_VISIBLE;
+    amp[k] = found ? (float)sqrt(gain) : 0.0f;
+  }
+  __syncthreads();
+  const int half = Ms / 2;
+  __shared__ int nvis;
+  const int gq = lane >> 2, tq = lane & 3;  // mma fragment coordinates
+  for (int s = 0; s < S; ++s) {
+    if (tid < 32) {  // warp 0: ballot compaction in user order
+      int n = 0;
+      for (int kb = 0; kb < K; kb += 32) {
+        const int k = kb + tid;
+        const bool v = k < K && ((vis[k * sw + (s >> 5)] >> (s & 31)) & 1u);
+        const unsigned bal = __ballot_sync(0xffffffffu, v);
+        if (v) vlist[n + __popc(bal & ((1u << tid) - 1u))] = k;
+        n += __popc(bal);
+      }
+      if (tid == 0) nvis = n;
+    }
+    // zero rows of the users that do not see subarray s
+    if (blockDim.x % K == 0) {
+      const int k = tid % K;
+      if (!((vis[k * sw + (s >> 5)] >> (s & 31)) & 1u)) {
+        float2* hp = H + (bl * M + (int64_t)s * Ms) * K + k;
+        for (int i = tid / K; i < Ms; i += blockDim.x / K) hp[(int64_t)i * K] = make_float2(0.0f, 0.0f);
+      }
+    } else {
+      for (int e = tid; e < Ms * K; e += blockDim.x) {
+        const int i = e / K, k = e % K;
+        if (!((vis[k * sw + (s >> 5)] >> (s & 31)) & 1u)) H[(bl * M + (int64_t)s * Ms + i) * K + k] = make_float2(0.0f, 0.0f);
+      }
+    }
+    __syncthreads();
+    const int nv = nvis;
+    for (int vc = 0; vc < nv; vc += KCH) {
+      const int kn = min(KCH, nv - vc);
+      for (int e = tid; e < half * kn; e += blockDim.x) {
+        const int kk = e / half, t = e % half, k = vlist[vc + kk];
+        uint4 z = philox4x32_10(make_uint4((uint32_t)(s * half + t), (uint32_t)k | (PURPOSE_FADE << 24), b_lo, b_hi), k0, k1);
+        float r0, i0, r1, i1;
+        box_muller(z.x, z.y, r0, i0);
+        box_muller(z.z, z.w, r1, i1);
+        *reinterpret_cast<float2*>(gf + (2 * t) * TC_GS + 2 * kk) = make_float2(r0, i0);
+        *reinterpret_cast<float2*>(gf + (2 * t + 1) * TC_GS + 2 * kk) = make_float2(r1, i1);
+      }
+      __syncthreads();
+      // warp w: column tiles 2w, 2w + 1 (columns 16 w .. 16 w + 15 = users 8 w .. 8 w + 7)
+      const int ncol = 2 * kn;
+      if (16 * warp < ncol) {
+        float acc[4][2][4];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.0f;
+#pragma unroll 2
+        for (int kk0 = 0; kk0 < Ms; kk0 += 8) {
+          uint32_t bh[2][2], blo[2][2];
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const int col = 16 * warp + 8 * nt + gq;
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const float x = gf[(kk0 + tq + 4 * h2) * TC_GS + col];
+              const uint32_t hx = tf32_of(x);
+              bh[nt][h2] = hx;
+              blo[nt][h2] = tf32_of(x - __uint_as_float(hx));
+            }
+          }
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt) {
+            const int r0 = 16 * mt + gq;
+            const uint32_t ah[4] = {rsh[r0 * TC_RS + kk0 + tq], rsh[(r0 + 8) * TC_RS + kk0 + tq],
+                                    rsh[r0 * TC_RS + kk0 + tq + 4], rsh[(r0 + 8) * TC_RS + kk0 + tq + 4]};
+            const uint32_t al[4] = {rsl[r0 * TC_RS + kk0 + tq], rsl[(r0 + 8) * TC_RS + kk0 + tq],
+                                    rsl[r0 * TC_RS + kk0 + tq + 4], rsl[(r0 + 8) * TC_RS + kk0 + tq + 4]};
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              mma_tf32(acc[mt][nt], ah, bh[nt][0], bh[nt][1]);
+              mma_tf32(acc[mt][nt], ah, blo[nt][0], blo[nt][1]);
+              mma_tf32(acc[mt][nt], al, bh[nt][0], bh[nt][1]);
+            }
+          }
+        }
+        // c0, c1: row 16 mt + gq, columns 2 tq, 2 tq + 1 of the tile = (Re, Im) of one user
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const int kk = 8 * warp + 4 * nt + tq;
+          if (kk < kn) {
+            const int k = vlist[vc + kk];
+            const float a = amp[k];
+            float2* hp = H + (bl * M + (int64_t)s * Ms) * K + k;
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+              hp[(int64_t)(16 * mt + gq) * K] = make_float2(acc[mt][nt][0] * a, acc[mt][nt][1] * a);
+              hp[(int64_t)(16 * mt + gq + 8) * K] = make_float2(acc[mt][nt][2] * a, acc[mt][nt][3] * a);
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 int launch_channel(int dtype, uint64_t seed, int64_t first, int64_t B, int S, int Ms,
                    int K, double p, const double* Rsqrt, double beta_bar, double dmin,
                    double dmax, void* H, int32_t* status, cudaStream_t st) {
   if (S > 65535 || (Ms & 1)) { set_error("channel: unsupported S/Ms"); return XL_ERR_UNSUPPORTED; }
   size_t rsz = dtype == XL_C64 ? 4 : 8;
+  if (dtype == XL_C64 && Ms == TC_MS && (int64_t)S * K <= VIS_BITS && B <= 0x7fffffff) {
+    // complex64, Ms = 64: R^{1/2} g on the tensor cores (3xTF32)
+    const int sw = (S + 31) / 32;
+    const size_t smem = 4 * (2 * (size_t)TC_MS * TC_RS + (size_t)TC_MS * TC_GS + ((K + 3) & ~3) +
+                             (size_t)((K * sw + 3) & ~3) + (size_t)K);
+    cudaFuncSetAttribute(chan_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    chan_tc_kernel<<<(unsigned)B, 256, smem, st>>>(seed, first, S, K, p, Rsqrt, beta_bar, dmin, dmax, (float2*)H,
+                                                   status);
+    return check_launch("channel_generate");
+  }
   if ((int64_t)S * K <= VIS_BITS && Ms % 8 == 0 && B <= 0x7fffffff) {  // one CTA per realization
     const int sw = (S + 31) / 32;
     size_t smem = rsz * ((size_t)Ms * Ms + ((K + 1) & ~1)) + 4 * (size_t)((K * sw + 3) & ~3) +

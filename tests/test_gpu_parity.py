@@ -412,10 +412,13 @@ def test_degenerate_realization_flagged():
 
 @pytest.mark.parametrize("dt,tol", [(torch.complex128, 1e-12), (torch.complex64, 2e-6)])
 def test_channel_generator_vs_oracle(dt, tol):
-    for (S, K, p, r) in ((4, 16, 0.5, 0.5), (16, 64, 0.4, 0.7), (3, 5, 0.3, 0.9)):
+    # cfg4's shape (64 x 128, p = 0.3) and > 64 visible users per subarray (two user chunks
+    # on the tensor-core generator, the second one partial)
+    for (S, K, p, r, B) in ((4, 16, 0.5, 0.5, 6), (16, 64, 0.4, 0.7, 6), (3, 5, 0.3, 0.9, 6),
+                            (64, 128, 0.3, 0.5, 2), (4, 100, 0.95, 0.9, 3)):
         m = X.ChannelModel(S=S, K=K, p=p, r=r)
-        H = X.generate_channels(m, seed=123, first=77, B=6, dtype=dt).cpu().numpy()
-        ref = O.generate_channels(123, 77, 6, S, K, p, r)
+        H = X.generate_channels(m, seed=123, first=77, B=B, dtype=dt).cpu().numpy()
+        ref = O.generate_channels(123, 77, B, S, K, p, r)
         # exact zeros on invisible subarrays
         np.testing.assert_array_equal(H == 0, ref == 0)
         assert relf(H, ref) < tol
