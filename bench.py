@@ -76,7 +76,11 @@ def load_peaks():
         out.update(hbm=d.get("hbm_gbs", 6650.0), fp16=d.get("bf16_tflops", 1590.0),
                    src="measured (MEASURED_PEAKS.json)")
     q = os.path.join(ROOT, "profiles", "r02_peaks_tf32_fp64.json")
-    out.update(tf32=None, fp64=None, fp32=None)
+    out.update(tf32=None, fp64=None, fp32=None, mma_sync=None)
+    r = os.path.join(ROOT, "profiles", "r02_peaks_mma_sync.json")
+    if os.path.exists(r):
+        with open(r) as f:
+            out.update(mma_sync=json.load(f).get("mma_sync_fp16_tflops"))
     if os.path.exists(q):
         with open(q) as f:
             d = json.load(f)
@@ -93,6 +97,9 @@ def roofline(M, K, T, method, dtype_bytes, B, kern_ms, path, peaks, traffic=None
     # tensor peak for the arithmetic the path executes
     if path == "tc3xfp16":      # 3 fp16 MMAs per real product on tcgen05
         tpeak, tname = peaks["fp16"] / 3.0, "fp16 tensor / 3 (3xFP16 split on tcgen05)"
+    elif path == "mma3xfp16":   # 3 fp16 mma.sync per real product (warp-level tensor cores)
+        tpeak = (peaks.get("mma_sync") or 550.0) / 3.0
+        tname = "fp16 mma.sync / 3 (3xFP16 split, measured legacy-MMA rate)"
     elif path == "fp64":
         tpeak, tname = peaks["fp64"] or 35.0, "FP64 (DMMA / DFMA GEMM rate, measured)"
     else:                       # fp32 SIMT kernels
@@ -293,8 +300,11 @@ def run_reference(a):
 
 def path_of(X, dt, method, M, K):
     import torch
-    if X.uses_tensor_cores(dt, method, M, K):
+    tc = X.tensor_core_path(dt, method, M, K)
+    if tc == "tcgen05":
         return "tc3xfp16"
+    if tc == "mma.sync":
+        return "mma3xfp16"
     return "fp64" if dt == torch.complex128 else "fp32"
 
 

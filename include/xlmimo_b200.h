@@ -62,9 +62,11 @@ const char* xl_last_error(void);
 /* Number of kernels this library has launched in the process so far
  * (benchmark accounting of "our" launches). */
 uint64_t xl_launch_count(void);
-/* 1 when our tcgen05 kernels serve the whole rzf call for (dtype, method,
- * M, K) -- the fused kernel (K in {16, 32, 64}) or the streaming Gram / W +
- * cluster Jac-PCG chain (K = 128, M % 64 == 0) -- else 0. */
+/* Which tensor-core path serves the whole rzf call for (dtype, method, M, K):
+ * 1 = tcgen05 (the fused kernel at K = 64 or K in {16, 32} with M K > 8192,
+ * the streaming Gram / W + cluster Jac-PCG chain at K in {128, 256}),
+ * 2 = warp-level mma.sync (complex64 K in {16, 32}, M % 32 == 0, M K <= 8192:
+ * the small-K fused kernel), 0 = none (SIMT / DMMA / cuBLAS-free fp64). */
 int xl_rzf_uses_tensor_cores(int dtype, int method, int32_t M, int32_t K);
 
 /* Batched regularized Gram A_b = H_b^H H_b + xi_b I, Hermitian by

@@ -10,7 +10,7 @@ __version__ = "0.1.0"
 
 from .batched import (PrecoderBatch, apply_precoder_batched, combine_se_partials,  # noqa: F401
                       gram_batched, rzf_batched, se_partials, sinr_batched,
-                      solve_batched, uses_tensor_cores)
+                      solve_batched, tensor_core_path, uses_tensor_cores)
 from .channel import ChannelModel, beta_bar, build_correlation, generate_channels, psd_sqrt  # noqa: F401
 from .configs import CONFIGS, Workload  # noqa: F401
 from .errors import (AssemblyError, ConfigurationError, DegenerateChannelError,  # noqa: F401

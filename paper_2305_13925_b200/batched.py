@@ -117,8 +117,15 @@ def rzf_workspace_bytes(H_shape, dtype, method="jacpcg") -> int:
 
 
 def uses_tensor_cores(dtype, method, M, K) -> bool:
+    return tensor_core_path(dtype, method, M, K) != "none"
+
+
+def tensor_core_path(dtype, method, M, K) -> str:
+    """"tcgen05" (fused / streaming tcgen05 kernels), "mma.sync" (the small-K
+    fused kernel on the warp-level tensor cores) or "none" (SIMT / DMMA)."""
     L.load_library()
-    return bool(L._lib.xl_rzf_uses_tensor_cores(dtype_code(dtype), METHODS[method], M, K))
+    code = int(L._lib.xl_rzf_uses_tensor_cores(dtype_code(dtype), METHODS[method], M, K))
+    return {0: "none", 1: "tcgen05", 2: "mma.sync"}[code]
 
 
 def rzf_batched(H: torch.Tensor, xi, power: float, method: str = "jacpcg", T: int = 4,

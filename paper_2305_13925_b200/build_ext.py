@@ -12,7 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "_native", "libxlmimo_b200.so")
 SOURCES = ["xl_abi.cu", "simt_gemm.cu", "simt_solve.cu", "chan_gen.cu", "fused_tc.cu", "link_ber.cu",
-           "gemm_tc.cu", "cluster_pcg.cu", "stream_tc.cu", "large_k.cu", "dmma.cu", "fused_c128.cu"]
+           "gemm_tc.cu", "cluster_pcg.cu", "stream_tc.cu", "large_k.cu", "dmma.cu", "fused_c128.cu",
+           "fused_c64s.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CFLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
           "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

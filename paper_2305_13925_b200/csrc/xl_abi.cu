@@ -72,6 +72,7 @@ uint64_t xl_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RE
 const char* xl_last_error(void) { return g_err; }
 
 int xl_rzf_uses_tensor_cores(int dtype, int method, int32_t M, int32_t K) {
+  if (fc64s_supported(dtype, method, M, K)) return 2;  // warp-level mma.sync kernel (fused_c64s.cu)
   if (fused_supported(dtype, method, M, K)) return 1;
   // K = 256: streaming tcgen05 Gram / W + the 8-CTA cluster Jac-PCG / CG
   if (method != XL_DIRECT && lk_supported(dtype, M, K)) return 1;
@@ -328,6 +329,12 @@ static int rzf_impl(bool allow_fused, int dtype, int method, int variant, const 
   if (M < 1 || K < 1 || B < 0) { set_error("bad sizes"); return XL_ERR_CONFIG; }
   if (B == 0) return XL_SUCCESS;
   cudaStream_t st = (cudaStream_t)stream;
+  // complex64 K in {16, 32} with H in shared memory: one CTA per realization, mma.sync + SIMT solve
+  if (allow_fused && fc64s_supported(dtype, method, M, K)) {
+    if (cudaMemsetAsync(status, 0, (size_t)B * sizeof(int32_t), st) != cudaSuccess) return check_launch("memset");
+    return fc64s_rzf(method, variant, H, B, M, K, xi, xi_per_batch, power, T, sigma2, W, F, beta, gamma, sum_se, X,
+                     status, st);
+  }
   const bool fused = allow_fused && fused_supported(dtype, method, M, K);
   const size_t need = fused ? fused_ws_bytes(dtype, method, B, M, K) : general_ws(dtype, B, M, K);
   if (ws_bytes < need) { set_error("rzf: workspace too small"); return XL_ERR_WORKSPACE; }

@@ -51,12 +51,27 @@ def _check(H, out, alpha, power, method, T, variant):
             continue
         assert abs(beta[b] - be) <= max(1e-4, wt) * be
         if gam is not None:
-            np.testing.assert_allclose(gam[b], g, rtol=max(1e-3, 10 * wt), atol=1e-6 * np.abs(g).max())
+            # per-user SINR: a ratio whose interference sum amplifies W's relative
+            # error ~10x; for the chaotic recurrences (CG at T = 6) up to ~30x (measured)
+            gfac = 30 if method == "cg" else 10
+            np.testing.assert_allclose(gam[b], g, rtol=max(1e-3, gfac * wt), atol=1e-6 * np.abs(g).max())
 
 
-@pytest.mark.parametrize("S,K", [(16, 64), (4, 32), (4, 16), (2, 64), (1, 16), (64, 64), (48, 32)])
-def test_fused_shapes_vs_oracle(S, K):
-    assert BT.uses_tensor_cores(torch.complex64, "jacpcg", 64 * S, K)
+@pytest.fixture(params=["mma.sync", "tcgen05"])
+def small_k_path(request, monkeypatch):
+    """K <= 32 shapes run on both fused kernels: the mma.sync small-K kernel
+    (default when M K <= 8192) and the tcgen05 kernel (XL_SMALL_K_MMA=0)."""
+    if request.param == "tcgen05":
+        monkeypatch.setenv("XL_SMALL_K_MMA", "0")
+    else:
+        monkeypatch.delenv("XL_SMALL_K_MMA", raising=False)
+    return request.param
+
+
+@pytest.mark.parametrize("S,K", [(16, 64), (4, 32), (4, 16), (2, 64), (1, 16), (64, 64), (48, 32), (8, 16)])
+def test_fused_shapes_vs_oracle(S, K, small_k_path):
+    want = small_k_path if (K <= 32 and 64 * S * K <= 8192) else "tcgen05"
+    assert BT.tensor_core_path(torch.complex64, "jacpcg", 64 * S, K) == want
     m = X.ChannelModel(S=S, K=K, p=0.6, r=0.7)
     H = X.generate_channels(m, seed=21, first=5, B=5, dtype=torch.complex64)
     alpha, power = K / 10.0, 10.0
@@ -66,7 +81,7 @@ def test_fused_shapes_vs_oracle(S, K):
 
 @pytest.mark.parametrize("method,variant", [("cg", "textbook"), ("jacpcg", "algorithm")])
 @pytest.mark.parametrize("T", [1, 3, 6])
-def test_fused_methods(method, variant, T):
+def test_fused_methods(method, variant, T, small_k_path):
     m = X.ChannelModel(S=4, K=32, p=0.5, r=0.5)
     H = X.generate_channels(m, seed=3, first=0, B=4, dtype=torch.complex64)
     out = BT.rzf_batched(H, 3.2, 10.0, method=method, T=T, variant=variant)
@@ -139,13 +154,18 @@ def test_fused_scale_invariance(scale):
     _check(Hs, out, 3.2 * scale * scale, 10.0, "jacpcg", 4, "textbook")
 
 
-def test_fused_range_fallback():
-    """A chunk far above the first chunk's scale overflows the fp16 split:
-    the kernel flags XL_STATUS_RANGE and rzf_batched re-runs it on the
-    general kernels (check=True), matching the oracle."""
+def test_fused_range_fallback(monkeypatch):
+    """A chunk far above the first chunk's scale overflows the tcgen05
+    kernel's fp16 split: it flags XL_STATUS_RANGE and rzf_batched re-runs it
+    on the general kernels (check=True), matching the oracle.  The mma.sync
+    small-K kernel scales every user column separately and needs no re-run."""
     m = X.ChannelModel(S=4, K=16, p=1.0, r=0.5)
     H = X.generate_channels(m, seed=5, first=0, B=2, dtype=torch.complex64)
     H[0, 192:] *= 1e4
+    small = BT.rzf_batched(H, 1.6, 10.0, T=4, check=False)
+    assert small.status.cpu().tolist() == [0, 0]
+    _check(H, small, 1.6, 10.0, "jacpcg", 4, "textbook")
+    monkeypatch.setenv("XL_SMALL_K_MMA", "0")
     raw = BT.rzf_batched(H, 1.6, 10.0, T=4, check=False)
     assert raw.status.cpu().tolist()[0] == L.XL_STATUS_RANGE
     out = BT.rzf_batched(H, 1.6, 10.0, T=4)
@@ -199,10 +219,11 @@ def test_concurrent_streams_use_separate_workspaces():
     assert torch.equal(o1.sum_se, ref1.sum_se) and torch.equal(o2.sum_se, ref2.sum_se)
 
 
-def test_host_pipeline_reruns_range_rows():
+def test_host_pipeline_reruns_range_rows(monkeypatch):
     """The host-buffer API keeps rzf_batched(check=True)'s contract: a
     realization the fused kernel flags XL_STATUS_RANGE is re-run on the
     general kernels and its W / sum-SE / status scattered back."""
+    monkeypatch.setenv("XL_SMALL_K_MMA", "0")  # the tcgen05 kernel (the one that flags RANGE)
     m = X.ChannelModel(S=4, K=16, p=1.0, r=0.5)
     H = X.generate_channels(m, seed=5, first=0, B=5, dtype=torch.complex64)
     H[3, 192:] *= 1e4
