@@ -21,13 +21,16 @@
 //     Operands come from swizzled smem tiles through ldmatrix, with no TMEM
 //     round trip, so two CTAs per SM overlap one realization's tensor work
 //     with the other's SIMT solve.
-//   * The K x K solve in fp32 SIMT, the state of each thread's RG x 1 block
-//     of X, R, P, Q in registers (thread = column j, rows ig*RG ..), the
-//     column reductions through one shared-memory partial row per warp
-//     group (three barriers per iteration).  G is kept without xi (A p =
-//     G p + xi p), so GX = G X is an explicit product with no cancellation
-//     against xi X at low SNR; P0 is diagonal (x0 = 0, b = I), so the first
-//     product is a column scaling: T iterations cost T K x K products.
+//   * The K x K solve on the same tensor cores in 3xTF32 (mma.sync m16n8k8;
+//     TF32 keeps fp32's exponent range, so P and X need no scaling), the
+//     vector recurrences in fp32 SIMT.  Warp w < K / 8 owns columns
+//     [8w, 8w + 8) of X, R, P, Q (the RHS columns are independent) in the
+//     products' accumulator layout: the column reductions are warp shuffles
+//     and the B operand is the warp's own columns, so the PCG loop has no
+//     block barrier.  G is kept without xi (A p = G p + xi p), so GX = G X
+//     is an explicit product with no cancellation against xi X at low SNR;
+//     P0 is diagonal (x0 = 0, b = I), so the first product is a column
+//     scaling: T iterations cost T K x K products (GX included).
 //
 // Scaling: every user column k of Z (its re and im components) is scaled by
 // s_k = 2^e_k so that its largest |component| lies in [2^14, 2^15) -- the
@@ -37,6 +40,7 @@
 #include <cuda_fp16.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "xl_common.cuh"
@@ -56,20 +60,25 @@ struct Params {
   float2 *W, *F, *X;
   double *beta, *gamma, *sum_se;
   int32_t* status;
+  int pf;  // L2 prefetch distance in realizations (the resident CTAs of the grid)
+  long long* trace;  // dev (XL_SMALL_K_TRACE=<first CTA + 1>): clock64 phase stamps of 64 CTAs
+  unsigned trace0;
 };
+#define STAMP(n)                                                               \
+  do {                                                                         \
+    if (p.trace && threadIdx.x == 0 && blockIdx.x - p.trace0 < 64u)                              \
+      p.trace[(blockIdx.x - p.trace0) * 64 + (n)] = clock64();                                     \
+  } while (0)
 
 template <int K>
 struct G {
   static constexpr int NC = 2 * K;        // real components (re/im interleaved, as in H)
   static constexpr int RC = NC * 2 / 16;  // 16-B chunks per fp16 row (8 for K = 32, 4 for K = 16)
-  static constexpr int RG = K * K / NT;   // solver rows per thread (4 / 1)
-  static constexpr int NG = NT / K;       // solver row groups (8 / 16)
   static constexpr int US = NC + 2;       // fp32 U row stride (2-way conflicts on the fragment stores)
   static constexpr int XT_BYTES = (NC * US * 4 > 2 * NC * NC * 2) ? NC * US * 4 : 2 * NC * NC * 2;
   static constexpr int MT = NC / 16, NTL = NC / 8;           // m16 / n8 tiles of a 2K x 2K product
   static constexpr int GNP = K == 32 ? 4 : 2;                // Gram n-tiles per warp
   static constexpr int GWARPS = MT * NTL / GNP;              // Gram warps (8 / 4)
-  static_assert(RG * NG == K, "solver mapping");
   static_assert(GWARPS <= NW, "Gram mapping");
 };
 
@@ -143,30 +152,10 @@ __device__ __forceinline__ double seg_sum(double v) {  // sum over aligned SEG-l
   return v;
 }
 
-// q[rr] = sum_k G[i0 + rr][k] P[k][j]  (G, P row-major K x K complex in smem)
-template <int K, int RG>
-__device__ __forceinline__ void gemv_cols(const float2* Gs, const float2* Ps, int i0, int j, float2 (&qv)[RG]) {
-#pragma unroll
-  for (int rr = 0; rr < RG; ++rr) qv[rr] = make_float2(0.f, 0.f);
-#pragma unroll 4
-  for (int k = 0; k < K; k += 2) {
-    const float2 p0 = Ps[k * K + j], p1 = Ps[(k + 1) * K + j];
-#pragma unroll
-    for (int rr = 0; rr < RG; ++rr) {
-      const float4 a = *reinterpret_cast<const float4*>(Gs + (i0 + rr) * K + k);
-      float2& q = qv[rr];
-      q.x = fmaf(a.x, p0.x, q.x); q.x = fmaf(-a.y, p0.y, q.x);
-      q.y = fmaf(a.x, p0.y, q.y); q.y = fmaf(a.y, p0.x, q.y);
-      q.x = fmaf(a.z, p1.x, q.x); q.x = fmaf(-a.w, p1.y, q.x);
-      q.y = fmaf(a.z, p1.y, q.y); q.y = fmaf(a.w, p1.x, q.y);
-    }
-  }
-}
-
 template <int K>
 __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
   using g = G<K>;
-  constexpr int NC = g::NC, RC = g::RC, NG = g::NG, US = g::US;
+  constexpr int NC = g::NC, RC = g::RC, US = g::US;
   extern __shared__ __align__(128) uint8_t smem[];
   const int M = p.M;
   uint8_t* Zh = smem;                                        // [M][NC] fp16, swizzled
@@ -181,10 +170,10 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
   float* tcs = sc + K;                                       // [K] 1 / X' column scales t_j
   float* cdg = tcs + K;                                      // [K] A_ii
   float* isc = cdg + K;                                      // [K] 1 / s_k
-  float* part1 = isc + K;                                    // [NG][K]
-  float* part2 = part1 + NG * K;                             // [NG][K] (K = 32 SINR: [4][K] doubles)
-  double* dred = reinterpret_cast<double*>(part2 + NG * K);  // [NW]
-  float* sse = reinterpret_cast<float*>(dred + NW);          // [NW]
+  double* rowp = reinterpret_cast<double*>(isc + K);         // [K / 8][K] SINR row partials
+  double* dred = rowp + (K / 8) * K;                         // [NW]
+  float* colx = reinterpret_cast<float*>(dred + NW);         // [3][K / 16][K] column exchange slots
+  float* sse = colx + 3 * (K / 16) * K;                      // [NW]
   int* flags = reinterpret_cast<int*>(sse + NW);             // [0] status bits, [1..K] column max bits
   const int64_t b = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -192,6 +181,7 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
   const bool textbook = use_c && p.variant == XL_TEXTBOOK;
   const bool alg1 = use_c && !textbook;
   const float xi = (float)(p.xi_b ? p.xi_b[b] : p.xi);
+  STAMP(0);
 
   // ---- H -> registers (16-B loads) -> per-user column max -> scaled fp16 split tiles
   {
@@ -200,6 +190,10 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
     const float4* H4 = reinterpret_cast<const float4*>(p.H + b * (int64_t)M * K);
     const int nl = M * PR / NT;
     if (tid <= K) flags[tid] = 0;
+    if (tid == 0 && b + p.pf < p.B) {  // the CTA that runs after the next wave finds its H in L2
+      const float2* nx = p.H + (b + p.pf) * (int64_t)M * K;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx), "r"((uint32_t)(M * K * 8)) : "memory");
+    }
     float4 v[NLMAX];
 #pragma unroll
     for (int i = 0; i < NLMAX; ++i)
@@ -218,11 +212,13 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
       m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
     }
     __syncthreads();  // flags zeroed
+    STAMP(1);
     if (lane < PR) {
       atomicMax(&flags[1 + 2 * u], __float_as_int(m0));
       atomicMax(&flags[2 + 2 * u], __float_as_int(m1));
     }
     __syncthreads();
+    STAMP(2);
     const float s0 = col_scale(__int_as_float(flags[1 + 2 * u])), s1 = col_scale(__int_as_float(flags[2 + 2 * u]));
     if (tid < K) {
       const float sv = col_scale(__int_as_float(flags[1 + tid]));
@@ -242,6 +238,7 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
       }
   }
   __syncthreads();
+  STAMP(3);
 
   // ---- Gram on the tensor cores: U = Zh^T Zh + 2 Zh^T Zl over the M antennas
   if (warp < g::GWARPS) {
@@ -280,6 +277,7 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
     }
   }
   __syncthreads();
+  STAMP(4);
 
   // ---- G = H^H H (unscaled exactly; no xi: A p = G p + xi p)
   for (int e = tid; e < K * K; e += NT) {
@@ -297,246 +295,300 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
     if (i == j) cdg[i] = gr + xi;  // A_ii: the Jacobi preconditioner
   }
   __syncthreads();
+  STAMP(5);
 
-  // ---- element ownership: thread holds NE complex entries (ie[e], je[e]) of
-  // X, R, P, Q, GX.  K = 32: the m16n8 accumulator layout of the tensor-core
-  // products (warp = 16 rows x 8 columns); K = 16: row tid / 16, column tid % 16.
-  constexpr int NE = K == 32 ? 4 : 1;
-  const int gq = lane >> 2, tq = lane & 3, wmt = warp & 1, wnt = warp >> 1;
+  // ---- The solve.  Column block cb (8 RHS columns, independent of the
+  // others) is owned by NMT = K / 16 warps, warp = one m16 row tile of it, in
+  // the accumulator layout of its tensor-core products: entry e = 2 h + c is
+  // (i = 16 mt + g + 8 h, j = 8 cb + 2 t + c).  Column reductions are warp
+  // shuffles plus (K = 32) one exchange with the partner warp through shared
+  // memory and a 64-thread named barrier; the B operand of a product is the
+  // block's own columns.  No block-wide barrier inside the PCG loop.
+  constexpr int NMT = K / 16, NCB = K / 8, NSW = NMT * NCB, KS = K / 4, KSUB = K / 8, NE = 4;
+  static_assert(NSW <= NW, "solver warps");
+  const int gq = lane >> 2, tq = lane & 3;
+  const int cb = warp / NMT, mt = warp % NMT;
+  const bool solver = warp < NSW;
+  // A fragments of the products: A = [Gr | Gi] (K x 2K), 3xTF32 split, per
+  // [m-tile][k-step][lane] {a0..a3} hi then lo (in the U region, free now)
+  for (int f = tid; f < NMT * KS * 32; f += NT) {
+    const int fm = f / (KS * 32), ks = (f / 32) % KS, ln = f & 31, g8 = ln >> 2, t8 = ln & 3;
+    const int r0 = 16 * fm + g8, c0 = 8 * ks + t8;
+    auto av = [&](int rr, int cc) { return cc < K ? Gs[rr * K + cc].x : Gs[rr * K + cc - K].y; };
+    uint4 h, l;
+    split_tf32(av(r0, c0), h.x, l.x);
+    split_tf32(av(r0 + 8, c0), h.y, l.y);
+    split_tf32(av(r0, c0 + 4), h.z, l.z);
+    split_tf32(av(r0 + 8, c0 + 4), h.w, l.w);
+    GA[2 * f] = h;
+    GA[2 * f + 1] = l;
+  }
   int ie[NE], je[NE];
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
-    if constexpr (K == 32) {
-      ie[e] = 16 * wmt + gq + 8 * (e >> 1);
-      je[e] = 8 * wnt + 2 * tq + (e & 1);
-    } else {
-      ie[e] = tid / K;
-      je[e] = tid % K;
-    }
+    ie[e] = 16 * mt + gq + 8 * (e >> 1);
+    je[e] = 8 * cb + 2 * tq + (e & 1);
   }
-  // column sums of one value per owned entry, in a fixed order (part: scratch [NG][K])
-  constexpr int NCOLS = K == 32 ? 2 : 1;
-  auto col_sums = [&](const float (&v)[NE], float* part, float (&out)[NCOLS], bool is_max) {
-    if constexpr (K == 32) {
-      float a = is_max ? fmaxf(v[0], v[2]) : v[0] + v[2];
-      float c = is_max ? fmaxf(v[1], v[3]) : v[1] + v[3];
+  auto pair_sync = [&]() {  // the NMT warps of column block cb (immediate barrier ids 1..NCB)
+    if constexpr (NMT > 1) {
+      switch (cb) {
+        case 0: asm volatile("bar.sync 1, 64;" ::: "memory"); break;
+        case 1: asm volatile("bar.sync 2, 64;" ::: "memory"); break;
+        case 2: asm volatile("bar.sync 3, 64;" ::: "memory"); break;
+        default: asm volatile("bar.sync 4, 64;" ::: "memory"); break;
+      }
+    } else {
+      __syncwarp();
+    }
+  };
+  static_assert(NMT <= 2 && NCB <= 4, "pair barriers");
+  // column c in {0, 1} of this thread: its two rows, the 8 row lanes, then the
+  // partner warp's half through exchange slot `slot` (fixed order: mt 0 + mt 1)
+  auto col_sum = [&](const float (&v)[NE], float (&out)[2], bool is_max, int slot) {
+    float a[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      a[c] = is_max ? fmaxf(v[c], v[2 + c]) : v[c] + v[2 + c];
 #pragma unroll
       for (int o = 4; o < 32; o <<= 1) {
-        const float a2 = __shfl_xor_sync(0xffffffffu, a, o), c2 = __shfl_xor_sync(0xffffffffu, c, o);
-        a = is_max ? fmaxf(a, a2) : a + a2;
-        c = is_max ? fmaxf(c, c2) : c + c2;
+        const float a2 = __shfl_xor_sync(0xffffffffu, a[c], o);
+        a[c] = is_max ? fmaxf(a[c], a2) : a[c] + a2;
       }
+    }
+    if constexpr (NMT > 1) {
+      float* xs = colx + slot * (NMT * K);  // [slot][mt][j]
       if (gq == 0) {
-        part[wmt * K + je[0]] = a;
-        part[wmt * K + je[1]] = c;
+        xs[mt * K + je[0]] = a[0];
+        xs[mt * K + je[1]] = a[1];
       }
-      __syncthreads();
+      pair_sync();
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const float x0 = part[je[c]], x1 = part[K + je[c]];
+        const float x0 = xs[je[c]], x1 = xs[K + je[c]];
         out[c] = is_max ? fmaxf(x0, x1) : x0 + x1;
       }
     } else {
-      part[ie[0] * K + je[0]] = v[0];
-      __syncthreads();
-      float acc = part[je[0]];
-#pragma unroll 4
-      for (int gI = 1; gI < NG; ++gI) acc = is_max ? fmaxf(acc, part[gI * K + je[0]]) : acc + part[gI * K + je[0]];
-      out[0] = acc;
+      out[0] = a[0];
+      out[1] = a[1];
     }
   };
-
-  // P (or X) -> the operand of the next K x K product
+  // v (P or X: this warp's rows of its block's columns) -> B fragments
+  // [half re/im][ksub][column n][t] x {b0h, b1h, b0l, b1l}; then the pair barrier
   auto put_operand = [&](const float2 (&v)[NE]) {
-    if constexpr (K == 32) {
-      // B fragments of the 3xTF32 m16n8k8 products, [half re/im][ksub][column n][t] x {b0h, b1h, b0l, b1l}
-      uint32_t* bw = reinterpret_cast<uint32_t*>(BF);
+    uint32_t* bw = reinterpret_cast<uint32_t*>(BF);
 #pragma unroll
-      for (int e = 0; e < NE; ++e) {
-        const int k = ie[e], ksub = k >> 3, tt = k & 3, slot = (k >> 2) & 1;
-        uint32_t h, l;
-        split_tf32(v[e].x, h, l);
-        uint32_t* w0 = bw + (((0 * 4 + ksub) * K + je[e]) * 4 + tt) * 4 + slot;
-        w0[0] = h;
-        w0[2] = l;
-        split_tf32(v[e].y, h, l);
-        uint32_t* w1 = bw + (((1 * 4 + ksub) * K + je[e]) * 4 + tt) * 4 + slot;
-        w1[0] = h;
-        w1[2] = l;
-      }
-    } else {
-      Ps[ie[0] * K + je[0]] = v[0];
+    for (int e = 0; e < NE; ++e) {
+      const int k = ie[e], ksub = k >> 3, tt = k & 3, slot = (k >> 2) & 1;
+      uint32_t h, l;
+      split_tf32(v[e].x, h, l);
+      uint32_t* w0 = bw + (((0 * KSUB + ksub) * K + je[e]) * 4 + tt) * 4 + slot;
+      w0[0] = h;
+      w0[2] = l;
+      split_tf32(v[e].y, h, l);
+      uint32_t* w1 = bw + (((1 * KSUB + ksub) * K + je[e]) * 4 + tt) * 4 + slot;
+      w1[0] = h;
+      w1[2] = l;
     }
+    pair_sync();
   };
-  // q = G v for the owned entries (v as last put_operand'ed)
+  // q = G v on this warp's tile (v as last put_operand'ed): Qr = Gr Vr - Gi Vi,
+  // Qi = Gr Vi + Gi Vr; four accumulator chains (hi*hi apart from the two
+  // correction terms) of KS and 2 KS MMAs
   auto product = [&](float2 (&q)[NE]) {
-    if constexpr (K == 32) {
-      // eight independent accumulator chains (hi*hi apart from the two
-      // correction terms; the Gr and Gi blocks apart) of <= 8 MMAs each
-      float acc[8][4];
+    float acc[4][4];
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[a][e] = 0.f;
-      const uint4* bre = BF + (0 * 4 * K + 8 * wnt + gq) * 4 + tq;
-      const uint4* bim = BF + (1 * 4 * K + 8 * wnt + gq) * 4 + tq;
+      for (int d = 0; d < 4; ++d) acc[a][d] = 0.f;
+    const uint4* bre = BF + (0 * KSUB * K + 8 * cb + gq) * 4 + tq;
+    const uint4* bim = BF + (1 * KSUB * K + 8 * cb + gq) * 4 + tq;
+    const uint4* ga = GA + (mt * KS * 32 + lane) * 2;
 #pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        const uint4 ah = GA[((wmt * 8 + ks) * 32 + lane) * 2], al = GA[((wmt * 8 + ks) * 32 + lane) * 2 + 1];
-        const uint4 br = bre[(ks & 3) * K * 4], bi = bim[(ks & 3) * K * 4];
-        // Gr block (ks < 4): Qr += Gr Pr, Qi += Gr Pi; Gi block: Qr -= Gi Pi, Qi += Gi Pr
-        const uint4& b1 = ks < 4 ? br : bi;
-        const uint4& b2 = ks < 4 ? bi : br;
-        const int o = ks < 4 ? 0 : 4;
-        mma_tf32(acc[o + 0], ah, b1.x, b1.y);
-        mma_tf32(acc[o + 1], al, b1.x, b1.y);
-        mma_tf32(acc[o + 1], ah, b1.z, b1.w);
-        mma_tf32(acc[o + 2], ah, b2.x, b2.y);
-        mma_tf32(acc[o + 3], al, b2.x, b2.y);
-        mma_tf32(acc[o + 3], ah, b2.z, b2.w);
+    for (int ks = 0; ks < KS; ++ks) {
+      const uint4 br = bre[(ks % KSUB) * K * 4], bi = bim[(ks % KSUB) * K * 4];
+      const uint4 ah = ga[ks * 64], al = ga[ks * 64 + 1];
+      uint4 b1 = br, b2 = bi;  // Gr block: Qr += Gr Vr, Qi += Gr Vi
+      if (ks >= KSUB) {        // Gi block: Qr += Gi (-Vi), Qi += Gi Vr
+        b1 = make_uint4(bi.x ^ 0x80000000u, bi.y ^ 0x80000000u, bi.z ^ 0x80000000u, bi.w ^ 0x80000000u);
+        b2 = br;
       }
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        q[e] = make_float2((acc[0][e] + acc[1][e]) - (acc[4][e] + acc[5][e]),
-                           (acc[2][e] + acc[3][e]) + (acc[6][e] + acc[7][e]));
-    } else {
-      gemv_cols<K, 1>(Gs, Ps, ie[0], je[0], q);
+      mma_tf32(acc[0], ah, b1.x, b1.y);
+      mma_tf32(acc[1], al, b1.x, b1.y);
+      mma_tf32(acc[1], ah, b1.z, b1.w);
+      mma_tf32(acc[2], ah, b2.x, b2.y);
+      mma_tf32(acc[3], al, b2.x, b2.y);
+      mma_tf32(acc[3], ah, b2.z, b2.w);
     }
+#pragma unroll
+    for (int d = 0; d < 4; ++d) q[d] = make_float2(acc[0][d] + acc[1][d], acc[2][d] + acc[3][d]);
   };
 
-  if constexpr (K == 32) {
-    // A fragments of the products: A = [Gr | Gi] (K x 2K), 3xTF32 split, per
-    // [m-tile][k-step][lane] {a0..a3} hi then lo (in the U region, free now)
-    for (int f = tid; f < 2 * 8 * 32; f += NT) {
-      const int mt = f >> 8, ks = (f >> 5) & 7, ln = f & 31, g8 = ln >> 2, t8 = ln & 3;
-      const int r0 = 16 * mt + g8, c0 = 8 * ks + t8;
-      auto av = [&](int rr, int cc) { return cc < K ? Gs[rr * K + cc].x : Gs[rr * K + cc - K].y; };
-      uint4 h, l;
-      split_tf32(av(r0, c0), h.x, l.x);
-      split_tf32(av(r0 + 8, c0), h.y, l.y);
-      split_tf32(av(r0, c0 + 4), h.z, l.z);
-      split_tf32(av(r0 + 8, c0 + 4), h.w, l.w);
-      GA[2 * f] = h;
-      GA[2 * f + 1] = l;
+  // ---- Jac-PCG / CG (linsolve.py:217-294) on the K identity RHS, w0 = 0
+  float icr[NE], icc[2], rz[2];
+  float2 x[NE], r[NE], pv[NE], qv[NE];
+  if (solver) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      icc[c] = use_c ? 1.f / cdg[je[c]] : 1.f;
+      rz[c] = textbook ? icc[c] : (use_c ? icc[c] * icc[c] : 1.f);
+    }
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const float ci = cdg[ie[e]];
+      icr[e] = use_c ? 1.f / ci : 1.f;
+      if (use_c && ci == 0.f && ie[e] == je[e]) atomicOr(flags, 2);
+      const float d = (ie[e] == je[e]) ? 1.f : 0.f;
+      const float rv = alg1 ? d * icr[e] : d;
+      x[e] = make_float2(0.f, 0.f);
+      r[e] = make_float2(rv, 0.f);
+      pv[e] = make_float2(textbook ? d * icr[e] : rv, 0.f);
+      // first product: P0 = diag(p_jj), so (G + xi I) P0 is a column scaling
+      // (every other term of the sum is an exact zero)
+      const float pjj = use_c ? icc[e & 1] : 1.f;
+      float2 gij = Gs[ie[e] * K + je[e]];
+      if (ie[e] == je[e]) gij.x += xi;
+      qv[e] = make_float2(gij.x * pjj, gij.y * pjj);
     }
   }
-
-  // ---- Jac-PCG / CG (linsolve.py:217-294) on the K identity RHS, w0 = 0.
-  // Per-column scalars (rz, alpha, beta) live in NCOL slots: entry e is in
-  // column slot e % NCOL.
-  constexpr int NCOL = K == 32 ? 2 : 1;
-  float icr[NE], icc[NCOL], rz[NCOL];
-  float2 x[NE], r[NE], pv[NE], qv[NE];
+  __syncthreads();  // G read (fragments, first product): the operand region may overwrite it
+  STAMP(11);
+  if (solver) {
+    for (int t = 1; t <= p.T; ++t) {
+      if (t > 1) {
+        product(qv);
 #pragma unroll
-  for (int c = 0; c < NCOL; ++c) {
-    icc[c] = use_c ? 1.f / cdg[je[c]] : 1.f;
-    rz[c] = textbook ? icc[c] : (use_c ? icc[c] * icc[c] : 1.f);
-  }
-#pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    const float ci = cdg[ie[e]];
-    icr[e] = use_c ? 1.f / ci : 1.f;
-    if (use_c && ci == 0.f && ie[e] == je[e]) atomicOr(flags, 2);
-    const float d = (ie[e] == je[e]) ? 1.f : 0.f;
-    const float rv = alg1 ? d * icr[e] : d;
-    x[e] = make_float2(0.f, 0.f);
-    r[e] = make_float2(rv, 0.f);
-    pv[e] = make_float2(textbook ? d * icr[e] : rv, 0.f);
-    // first product: P0 = diag(p_jj), so (G + xi I) P0 is a column scaling
-    // (every other term of the sum is an exact zero)
-    const float pjj = use_c ? icc[e % NCOL] : 1.f;
-    float2 gij = Gs[ie[e] * K + je[e]];
-    if (ie[e] == je[e]) gij.x += xi;
-    qv[e] = make_float2(gij.x * pjj, gij.y * pjj);
-  }
-  for (int t = 1; t <= p.T; ++t) {
-    if (t > 1) {
-      product(qv);
+        for (int e = 0; e < NE; ++e) {
+          qv[e].x = fmaf(xi, pv[e].x, qv[e].x);  // A p = G p + xi p
+          qv[e].y = fmaf(xi, pv[e].y, qv[e].y);
+        }
+      }
+      STAMP(12 + 4 * t);
+      float cp[NE];
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
-        qv[e].x = fmaf(xi, pv[e].x, qv[e].x);  // A p = G p + xi p
-        qv[e].y = fmaf(xi, pv[e].y, qv[e].y);
+        const float qf = alg1 ? icr[e] : 1.f;  // Algorithm 1: z = C^-1 A p
+        cp[e] = pv[e].x * (qv[e].x * qf) + pv[e].y * (qv[e].y * qf);
       }
-    }
-    float cp[NE];
+      float curv[2], al[2];
+      col_sum(cp, curv, false, 0);
 #pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      const float qf = alg1 ? icr[e] : 1.f;  // Algorithm 1: z = C^-1 A p
-      cp[e] = pv[e].x * (qv[e].x * qf) + pv[e].y * (qv[e].y * qf);
-    }
-    float curv[NCOL];
-    col_sums(cp, part1, curv, false);
-    float al[NCOL];
+      for (int c = 0; c < 2; ++c) {
+        const bool act = rz[c] > 0.f;
+        if (curv[c] <= 0.f && act) atomicOr(flags, 1);
+        al[c] = act ? rz[c] / (curv[c] > 0.f ? curv[c] : 1.f) : 0.f;
+      }
+      float rp[NE];
 #pragma unroll
-    for (int c = 0; c < NCOL; ++c) {
-      const bool act = rz[c] > 0.f;
-      if (curv[c] <= 0.f && act) atomicOr(flags, 1);
-      al[c] = act ? rz[c] / (curv[c] > 0.f ? curv[c] : 1.f) : 0.f;
-    }
-    float rp[NE];
+      for (int e = 0; e < NE; ++e) {
+        const float a = al[e & 1], qf = alg1 ? icr[e] : 1.f;
+        x[e].x = fmaf(a, pv[e].x, x[e].x);
+        x[e].y = fmaf(a, pv[e].y, x[e].y);
+        r[e].x -= a * (qv[e].x * qf);
+        r[e].y -= a * (qv[e].y * qf);
+        const float ic = textbook ? icr[e] : 1.f;
+        rp[e] = r[e].x * (r[e].x * ic) + r[e].y * (r[e].y * ic);
+      }
+      if (t == p.T) break;  // the last direction update feeds nothing
+      STAMP(13 + 4 * t);
+      float rn[2], be[2];
+      col_sum(rp, rn, false, 1);
 #pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      const float a = al[e % NCOL], qf = alg1 ? icr[e] : 1.f;
-      x[e].x = fmaf(a, pv[e].x, x[e].x);
-      x[e].y = fmaf(a, pv[e].y, x[e].y);
-      r[e].x -= a * (qv[e].x * qf);
-      r[e].y -= a * (qv[e].y * qf);
-      const float ic = textbook ? icr[e] : 1.f;
-      rp[e] = r[e].x * (r[e].x * ic) + r[e].y * (r[e].y * ic);
-    }
-    if (t == p.T) break;  // the last direction update feeds nothing
-    float rn[NCOL], be[NCOL];
-    col_sums(rp, part2, rn, false);
+      for (int c = 0; c < 2; ++c) {
+        be[c] = rz[c] > 0.f ? rn[c] / rz[c] : 0.f;
+        rz[c] = rn[c];
+      }
 #pragma unroll
-    for (int c = 0; c < NCOL; ++c) {
-      be[c] = rz[c] > 0.f ? rn[c] / rz[c] : 0.f;
-      rz[c] = rn[c];
+      for (int e = 0; e < NE; ++e) {
+        const float ic = textbook ? icr[e] : 1.f, bb = be[e & 1];
+        pv[e] = make_float2(fmaf(r[e].x, ic, bb * pv[e].x), fmaf(r[e].y, ic, bb * pv[e].y));
+      }
+      STAMP(14 + 4 * t);
+      put_operand(pv);  // the partner is past this iteration's product (barrier of slot 0)
+      STAMP(15 + 4 * t);
     }
-#pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      const float ic = textbook ? icr[e] : 1.f, bb = be[e % NCOL];
-      pv[e] = make_float2(fmaf(r[e].x, ic, bb * pv[e].x), fmaf(r[e].y, ic, bb * pv[e].y));
-    }
-    // every thread is past this iteration's product (two barriers ago); at
-    // t = 1 past the G reads of the fragment build and of the column scaling
-    put_operand(pv);
-    __syncthreads();
   }
+  STAMP(6);
 
-  // ---- GX = G X; ||F||^2 = Re tr(X^H GX) (fp64); beta
-  // (the loop left after the curvature barrier of iteration T: nothing reads the operand any more)
-  put_operand(x);
-  __syncthreads();
+  // ---- GX = G X (own tile); ||F||^2 = Re tr(X^H GX) (fp64); SINR row partials
   float2 gx[NE];
-  product(gx);
-  double fp = 0.0;
+  double sig = 0.0;
+  int diag_i = -1;
+  if (solver) {
+    put_operand(x);  // the partner is past its last product (barrier of slot 0 in iteration T)
+    product(gx);
+    double fp = 0.0;
 #pragma unroll
-  for (int e = 0; e < NE; ++e) fp += (double)x[e].x * gx[e].x + (double)x[e].y * gx[e].y;
-  fp = warp_sum(fp);
-  if (lane == 0) dred[warp] = fp;
-  // column max of X' = S^-1 X (the W operand scale t_j); the barrier inside
-  // also publishes dred
-  float xm[NE], cm[NCOLS];
+    for (int e = 0; e < NE; ++e) fp += (double)x[e].x * gx[e].x + (double)x[e].y * gx[e].y;
+    fp = warp_sum(fp);
+    if (lane == 0) dred[warp] = fp;
+    // row partials of |GX|^2 over this block's 8 columns (the diagonal apart)
 #pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    const float is = isc[ie[e]];
-    xm[e] = fmaxf(fabsf(x[e].x * is), fabsf(x[e].y * is));
+    for (int hh = 0; hh < 2; ++hh) {
+      double v2 = 0.0;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int e = 2 * hh + c;
+        const double v = (double)gx[e].x * gx[e].x + (double)gx[e].y * gx[e].y;
+        if (ie[e] == je[e]) {
+          sig = v;
+          diag_i = ie[e];
+        } else {
+          v2 += v;
+        }
+      }
+      v2 += __shfl_xor_sync(0xffffffffu, v2, 1);
+      v2 += __shfl_xor_sync(0xffffffffu, v2, 2);
+      if (tq == 0) rowp[cb * K + ie[2 * hh]] = v2;
+    }
+    // column max of X' = S^-1 X (the W operand scale t_j): this warp's rows,
+    // combined with the partner's after the block barrier
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      float a = fmaxf(fmaxf(fabsf(x[c].x), fabsf(x[c].y)) * isc[ie[c]],
+                      fmaxf(fabsf(x[2 + c].x), fabsf(x[2 + c].y)) * isc[ie[2 + c]]);
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+      if (gq == 0) colx[2 * NMT * K + mt * K + je[c]] = a;
+    }
   }
-  col_sums(xm, part1, cm, true);
+  __syncthreads();
+  STAMP(8);
   double fro = 0.0;
 #pragma unroll
-  for (int w = 0; w < NW; ++w) fro += dred[w];
+  for (int w = 0; w < NSW; ++w) fro += dred[w];
   const bool degenerate = !(fro > 0.0);
   const double btd = degenerate ? 0.0 : sqrt(p.power / fro);
 
-  // Xe'^T (fp16 hi | lo): rows n = output components, columns c = input components
-  {
+  if (solver) {
+    // SINR / SE from B = beta GX (row k: user k; interference summed directly)
+    float se = 0.f;
+    if (diag_i >= 0) {
+      const int i = diag_i;
+      double intf = 0.0;
+#pragma unroll
+      for (int w = 0; w < NCB; ++w) intf += rowp[w * K + i];
+      const double b2 = btd * btd;
+      const double gam = (b2 * sig) / (b2 * intf + p.sigma2);
+      if (p.gamma) p.gamma[b * K + i] = gam;
+      se = log1pf((float)gam) * 1.4426950408889634f;  // log2(1 + gamma)
+    }
+    se = warp_sum(se);
+    if (lane == 0) sse[warp] = se;
+    // Xe'^T (fp16 hi | lo): rows n = output components, columns c = input components
     uint8_t* XTh = XT;
     uint8_t* XTl = XT + NC * NC * 2;
+    float tjc[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      float m = colx[2 * NMT * K + je[c]];
+#pragma unroll
+      for (int q2 = 1; q2 < NMT; ++q2) m = fmaxf(m, colx[2 * NMT * K + q2 * K + je[c]]);
+      tjc[c] = col_scale(m);
+    }
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       const int i = ie[e], j = je[e];
-      const float tj = col_scale(cm[e % NCOLS]);
+      const float tj = tjc[e & 1];
       if (i == 0) tcs[j] = 1.f / tj;  // exact: a power of two
       const float f = tj * isc[i];
       const float xr = x[e].x * f, xim = x[e].y * f;
@@ -550,65 +602,14 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
       *reinterpret_cast<uint32_t*>(XTh + o1) = h1;
       *reinterpret_cast<uint32_t*>(XTl + o1) = l1;
     }
-  }
-  if (p.X) {
-    float2* Xo = p.X + b * (int64_t)K * K;
+    if (p.X) {
+      float2* Xo = p.X + b * (int64_t)K * K;
 #pragma unroll
-    for (int e = 0; e < NE; ++e) Xo[ie[e] * K + je[e]] = x[e];
-  }
-
-  // ---- SINR / SE from B = beta GX (row k: user k; interference summed directly)
-  {
-    const double b2 = btd * btd;
-    double sig = 0.0, intf = 0.0;
-    int diag_e = -1;
-    if constexpr (K == 32) {
-      // row partials over this thread's two columns, then over the 4 lanes of a row
-      double rp2[2] = {0.0, 0.0};
-#pragma unroll
-      for (int e = 0; e < NE; ++e) {
-        const double v = b2 * ((double)gx[e].x * gx[e].x + (double)gx[e].y * gx[e].y);
-        if (ie[e] == je[e]) {
-          sig = v;
-          diag_e = e;
-        } else {
-          rp2[e >> 1] += v;
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        rp2[h] += __shfl_xor_sync(0xffffffffu, rp2[h], 1);
-        rp2[h] += __shfl_xor_sync(0xffffffffu, rp2[h], 2);
-      }
-      double* rowp = reinterpret_cast<double*>(part2);  // [4 column groups][K]
-      if (tq == 0) {
-        rowp[wnt * K + ie[0]] = rp2[0];
-        rowp[wnt * K + ie[2]] = rp2[1];
-      }
-      __syncthreads();
-      if (diag_e >= 0) {
-        const int i = ie[diag_e];
-        intf = ((rowp[i] + rowp[K + i]) + rowp[2 * K + i]) + rowp[3 * K + i];
-      }
-    } else {
-      const double v = b2 * ((double)gx[0].x * gx[0].x + (double)gx[0].y * gx[0].y);
-      const bool d = ie[0] == je[0];
-      intf = seg_sum<K>(d ? 0.0 : v);
-      if (d) {
-        sig = v;
-        diag_e = 0;
-      }
+      for (int e = 0; e < NE; ++e) Xo[ie[e] * K + je[e]] = x[e];
     }
-    float se = 0.f;
-    if (diag_e >= 0) {
-      const double gam = sig / (intf + p.sigma2);
-      if (p.gamma) p.gamma[b * K + ie[diag_e]] = gam;
-      se = log1pf((float)gam) * 1.4426950408889634f;  // log2(1 + gamma)
-    }
-    se = warp_sum(se);
-    if (lane == 0) sse[warp] = se;
   }
   __syncthreads();  // XT, tcs, sse
+  STAMP(10);
 
   // ---- W = beta Z' Xe' / t_j on the tensor cores (3xFP16), two m-tiles per warp step
   {
@@ -655,6 +656,7 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
           }
         }
       }
+      STAMP(7);
 #pragma unroll
       for (int n = 0; n < NTL; ++n) {
         const int ju = 4 * n + t4;  // user column of this thread's (re, im) pair
@@ -673,9 +675,10 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
       }
     }
   }
+  STAMP(9);
   if (tid == 0) {
     double s = 0.0;
-    for (int w = 0; w < NW; ++w) s += (double)sse[w];
+    for (int w = 0; w < (K / 16) * (K / 8); ++w) s += (double)sse[w];
     p.sum_se[b] = s;
     p.beta[b] = btd;
     int st = 0;
@@ -689,8 +692,8 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
 template <int K>
 size_t smem_bytes(int M) {
   using g = G<K>;
-  return (size_t)M * g::NC * 2 * 2 + 2 * (size_t)K * K * 8 + g::XT_BYTES + 4 * K * 4 + 2 * g::NG * K * 4 +
-         NW * 8 + NW * 4 + (K + 1) * 4;
+  return (size_t)M * g::NC * 2 * 2 + 2 * (size_t)K * K * 8 + g::XT_BYTES + 4 * K * 4 + (K / 8) * K * 8 +
+         NW * 8 + 3 * (K / 16) * K * 4 + NW * 4 + (K + 1) * 4;
 }
 
 }  // namespace fs
@@ -706,16 +709,44 @@ bool fc64s_supported(int dtype, int method, int M, int K) {
 int fc64s_rzf(int method, int variant, const void* H, int64_t B, int M, int K, double xi, const double* xi_b,
               double power, int T, double sigma2, void* W, void* F, double* beta, double* gamma, double* sum_se,
               void* X, int32_t* status, cudaStream_t st) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
   fs::Params p{(const float2*)H, B, M, method, variant, T, xi, xi_b, power, sigma2, (float2*)W, (float2*)F,
-               (float2*)X, beta, gamma, sum_se, status};
-  if (K == 16) {
-    const size_t sm = fs::smem_bytes<16>(M);
-    cudaFuncSetAttribute(fs::small_k_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    fs::small_k_kernel<16><<<(unsigned)B, fs::NT, sm, st>>>(p);
-  } else {
-    const size_t sm = fs::smem_bytes<32>(M);
-    cudaFuncSetAttribute(fs::small_k_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    fs::small_k_kernel<32><<<(unsigned)B, fs::NT, sm, st>>>(p);
+               (float2*)X, beta, gamma, sum_se, status, 0, nullptr, 0};
+  static long long* trace = nullptr;
+  const char* tr = getenv("XL_SMALL_K_TRACE");
+  if (tr && atoi(tr) > 0) {
+    p.trace0 = (unsigned)(atoi(tr) - 1);
+    if (!trace) cudaMalloc(&trace, 64 * 64 * sizeof(long long));
+    cudaMemsetAsync(trace, 0, 64 * 64 * sizeof(long long), st);
+    p.trace = trace;
+  }
+  auto launch = [&](auto kern, size_t sm) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fs::NT, sm);
+    p.pf = (per_sm > 0 ? per_sm : 1) * nsm;
+    kern<<<(unsigned)B, fs::NT, sm, st>>>(p);
+  };
+  if (K == 16) launch(fs::small_k_kernel<16>, fs::smem_bytes<16>(M));
+  else launch(fs::small_k_kernel<32>, fs::smem_bytes<32>(M));
+  if (p.trace) {  // dev: per-phase cycle deltas, averaged over the traced CTAs
+    static long long h[64 * 64];
+    cudaMemcpyAsync(h, p.trace, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    double acc[64] = {0};
+    int n = 0;
+    for (int c = 0; c < 64 && c + (int64_t)p.trace0 < B; ++c, ++n)
+      for (int k = 1; k < 64; ++k)
+        if (h[c * 64 + k]) acc[k] += (double)(h[c * 64 + k] - h[c * 64]);
+    fprintf(stderr, "small_k trace (cycles since start, mean of %d CTAs):", n);
+    for (int k = 1; k < 64; ++k)
+      if (acc[k] != 0) fprintf(stderr, " %d:%.0f", k, acc[k] / n);
+    fprintf(stderr, "\n");
   }
   return check_launch("fused c64 small K (mma.sync)");
 }
