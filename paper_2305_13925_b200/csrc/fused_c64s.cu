@@ -21,13 +21,14 @@
 //     Operands come from swizzled smem tiles through ldmatrix, with no TMEM
 //     round trip, so two CTAs per SM overlap one realization's tensor work
 //     with the other's SIMT solve.
-//   * The K x K solve on the same tensor cores in 3xTF32 (mma.sync m16n8k8;
-//     TF32 keeps fp32's exponent range, so P and X need no scaling), the
-//     vector recurrences in fp32 SIMT.  Warp w < K / 8 owns columns
-//     [8w, 8w + 8) of X, R, P, Q (the RHS columns are independent) in the
-//     products' accumulator layout: the column reductions are warp shuffles
-//     and the B operand is the warp's own columns, so the PCG loop has no
-//     block barrier.  G is kept without xi (A p = G p + xi p), so GX = G X
+//   * The K x K solve's products on the same tensor cores in 3xFP16 on
+//     G' = D G D and B' = D^-1 P F (D, F powers of two: D from G's diagonal,
+//     F from a per-column bound on P's largest component), A fragments held
+//     in registers for the whole solve; the vector recurrences in fp32 SIMT.
+//     Column block cb (8 RHS columns; the columns are independent) is owned
+//     by K / 16 warps in the products' accumulator layout: the column
+//     reductions are warp shuffles plus one pair exchange, and the B operand
+//     is the block's own columns, so the PCG loop has no block barrier.  G is kept without xi (A p = G p + xi p), so GX = G X
 //     is an explicit product with no cancellation against xi X at low SNR;
 //     P0 is diagonal (x0 = 0, b = I), so the first product is a column
 //     scaling: T iterations cost T K x K products (GX included).
@@ -77,8 +78,9 @@ struct G {
   static constexpr int US = NC + 2;       // fp32 U row stride (2-way conflicts on the fragment stores)
   static constexpr int XT_BYTES = (NC * US * 4 > 2 * NC * NC * 2) ? NC * US * 4 : 2 * NC * NC * 2;
   static constexpr int MT = NC / 16, NTL = NC / 8;           // m16 / n8 tiles of a 2K x 2K product
-  static constexpr int GNP = K == 32 ? 4 : 2;                // Gram n-tiles per warp
-  static constexpr int GWARPS = MT * NTL / GNP;              // Gram warps (8 / 4)
+  static constexpr int GNP = 2;                              // Gram n-tiles per warp
+  static constexpr int GMP = K == 32 ? 2 : 1;                // Gram m-tiles per warp
+  static constexpr int GWARPS = MT * NTL / (GNP * GMP);      // Gram warps (8 / 4)
   static_assert(GWARPS <= NW, "Gram mapping");
 };
 
@@ -112,23 +114,6 @@ __device__ __forceinline__ void hmma(float (&d)[4], const uint32_t (&a)[4], uint
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {  // x ~ hi + lo, 22 bits
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(x - __uint_as_float(hi)));
-}
-__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint4& a, uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
-}
-// 3xTF32: d += a_lo b_hi + a_hi b_lo + a_hi b_hi (b = {b0 hi, b1 hi, b0 lo, b1 lo})
-__device__ __forceinline__ void mma3_tf32(float (&d)[4], const uint4& ah, const uint4& al, const uint4& b) {
-  mma_tf32(d, al, b.x, b.y);
-  mma_tf32(d, ah, b.z, b.w);
-  mma_tf32(d, ah, b.x, b.y);
-}
 // fp16 split of a pair: hi = fp16(x), lo = fp16(x - hi) (paired conversions)
 __device__ __forceinline__ void split2(float x, float y, uint32_t& hi, uint32_t& lo) {
   const __half2 h = __floats2half2_rn(x, y);
@@ -137,14 +122,17 @@ __device__ __forceinline__ void split2(float x, float y, uint32_t& hi, uint32_t&
   hi = *reinterpret_cast<const uint32_t*>(&h);
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
-// The power of two that puts m's leading bit at 2^14 (m in [2^14, 2^15) after
-// scaling); 1 for m = 0 / inf / nan.  m = 1.f x 2^(E - 127) -> 2^(141 - E).
-__device__ __forceinline__ float col_scale(float m) {
+// The power of two s with m s in [2^(t-1), 2^t); 1 for m = 0 / inf / nan.
+// m = 1.f x 2^(E - 127) -> s = 2^(t - 1 - (E - 127)), biased exponent t + 253 - E.
+template <int TB>
+__device__ __forceinline__ float pow2s(float m) {
   if (!(m > 0.f) || !isfinite(m)) return 1.f;
   const int E = (__float_as_int(m) >> 23) & 0xff;  // 0 for subnormal m: clamped below
-  const int f = 268 - E;
-  return __int_as_float((f > 254 ? 254 : f) << 23);
+  const int f = TB + 253 - E;
+  return __int_as_float((f > 254 ? 254 : (f < 1 ? 1 : f)) << 23);
 }
+// the per-column scale of the fp16 W / Gram operands: max in [2^14, 2^15)
+__device__ __forceinline__ float col_scale(float m) { return pow2s<15>(m); }
 template <int SEG>
 __device__ __forceinline__ double seg_sum(double v) {  // sum over aligned SEG-lane segments
 #pragma unroll
@@ -164,16 +152,17 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
   float2* Ps = Gs + K * K;                                   // [K][K] P, then X
   uint8_t* XT = reinterpret_cast<uint8_t*>(Ps + K * K);      // Xe'^T hi | lo ([NC][NC] fp16) ...
   float* Us = reinterpret_cast<float*>(XT);                  // ... aliased by U ([NC][US] fp32)
-  uint4* GA = reinterpret_cast<uint4*>(XT);                  // ... and by the K = 32 product A fragments
-  uint4* BF = reinterpret_cast<uint4*>(Gs);                  // K = 32 product B fragments (over G, P)
+  uint4* BF = reinterpret_cast<uint4*>(Gs);                  // K x K product B' fragments (over G, P)
   float* sc = reinterpret_cast<float*>(XT + g::XT_BYTES);    // [K] column scales s_k
   float* tcs = sc + K;                                       // [K] 1 / X' column scales t_j
   float* cdg = tcs + K;                                      // [K] A_ii
   float* isc = cdg + K;                                      // [K] 1 / s_k
-  double* rowp = reinterpret_cast<double*>(isc + K);         // [K / 8][K] SINR row partials
+  float* dsc = isc + K;                                      // [K] G' = D G D row / column scales
+  float* idsc = dsc + K;                                     // [K] 1 / dsc
+  double* rowp = reinterpret_cast<double*>(idsc + K);        // [K / 8][K] SINR row partials
   double* dred = rowp + (K / 8) * K;                         // [NW]
-  float* colx = reinterpret_cast<float*>(dred + NW);         // [3][K / 16][K] column exchange slots
-  float* sse = colx + 3 * (K / 16) * K;                      // [NW]
+  float* colx = reinterpret_cast<float*>(dred + NW);         // [5][K / 16][K] column exchange slots
+  float* sse = colx + 5 * (K / 16) * K;                      // [NW]
   int* flags = reinterpret_cast<int*>(sse + NW);             // [0] status bits, [1..K] column max bits
   const int64_t b = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -241,40 +230,51 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
   STAMP(3);
 
   // ---- Gram on the tensor cores: U = Zh^T Zh + 2 Zh^T Zl over the M antennas
+  // (warp tile GMP m16 x GNP n8: the A and B fragment loads per k-step are
+  // balanced, 4 ldmatrix.x4 per warp at K = 32)
   if (warp < g::GWARPS) {
-    constexpr int GNP = g::GNP;
-    const int m0 = (warp % g::MT) * 16, n0 = (warp / g::MT) * GNP * 8;
-    float acc[GNP][4], acl[GNP][4];
+    constexpr int GNP = g::GNP, GMP = g::GMP;
+    const int m0 = (warp % (g::MT / GMP)) * 16 * GMP, n0 = (warp / (g::MT / GMP)) * GNP * 8;
+    float acc[GMP][GNP][4], acl[GMP][GNP][4];
 #pragma unroll
-    for (int n = 0; n < GNP; ++n)
+    for (int mm = 0; mm < GMP; ++mm)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[n][e] = acl[n][e] = 0.f;
+      for (int n = 0; n < GNP; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[mm][n][e] = acl[mm][n][e] = 0.f;
     const int q = lane >> 3, r = lane & 7;
     const uint32_t zh = smem_u32(Zh), zl = smem_u32(Zl);
     for (int k0 = 0; k0 < M; k0 += 16) {
-      uint32_t af[4];
-      ldsm4t(zh + swz<RC>(k0 + r + (q >> 1) * 8, (m0 >> 3) + (q & 1)), af);  // A = Zh^T (m = comp, k = antenna)
+      uint32_t af[GMP][4];
+#pragma unroll
+      for (int mm = 0; mm < GMP; ++mm)  // A = Zh^T (m = comp, k = antenna)
+        ldsm4t(zh + swz<RC>(k0 + r + (q >> 1) * 8, ((m0 + 16 * mm) >> 3) + (q & 1)), af[mm]);
 #pragma unroll
       for (int n = 0; n < GNP; n += 2) {
         const uint32_t bo = swz<RC>(k0 + r + (q & 1) * 8, ((n0 + 8 * n) >> 3) + (q >> 1));
         uint32_t bh[4], bl[4];
         ldsm4t(zh + bo, bh);
         ldsm4t(zl + bo, bl);
-        hmma(acc[n], af, bh[0], bh[1]);
-        hmma(acc[n + 1], af, bh[2], bh[3]);
-        hmma(acl[n], af, bl[0], bl[1]);
-        hmma(acl[n + 1], af, bl[2], bl[3]);
+#pragma unroll
+        for (int mm = 0; mm < GMP; ++mm) {
+          hmma(acc[mm][n], af[mm], bh[0], bh[1]);
+          hmma(acc[mm][n + 1], af[mm], bh[2], bh[3]);
+          hmma(acl[mm][n], af[mm], bl[0], bl[1]);
+          hmma(acl[mm][n + 1], af[mm], bl[2], bl[3]);
+        }
       }
     }
     const int gr = lane >> 2, t2 = 2 * (lane & 3);
 #pragma unroll
-    for (int n = 0; n < GNP; ++n) {
-      const int c = n0 + 8 * n + t2;
-      *reinterpret_cast<float2*>(Us + (m0 + gr) * US + c) =
-          make_float2(fmaf(2.f, acl[n][0], acc[n][0]), fmaf(2.f, acl[n][1], acc[n][1]));
-      *reinterpret_cast<float2*>(Us + (m0 + gr + 8) * US + c) =
-          make_float2(fmaf(2.f, acl[n][2], acc[n][2]), fmaf(2.f, acl[n][3], acc[n][3]));
-    }
+    for (int mm = 0; mm < GMP; ++mm)
+#pragma unroll
+      for (int n = 0; n < GNP; ++n) {
+        const int c = n0 + 8 * n + t2, rr = m0 + 16 * mm + gr;
+        *reinterpret_cast<float2*>(Us + rr * US + c) =
+            make_float2(fmaf(2.f, acl[mm][n][0], acc[mm][n][0]), fmaf(2.f, acl[mm][n][1], acc[mm][n][1]));
+        *reinterpret_cast<float2*>(Us + (rr + 8) * US + c) =
+            make_float2(fmaf(2.f, acl[mm][n][2], acc[mm][n][2]), fmaf(2.f, acl[mm][n][3], acc[mm][n][3]));
+      }
   }
   __syncthreads();
   STAMP(4);
@@ -292,7 +292,13 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
     const float inv = isc[i] * isc[j];  // exact: powers of two
     const float gr = (s00 + s11) * inv;
     Gs[i * K + j] = make_float2(gr, i == j ? 0.f : (s01 - s10) * inv);
-    if (i == j) cdg[i] = gr + xi;  // A_ii: the Jacobi preconditioner
+    if (i == j) {
+      cdg[i] = gr + xi;  // A_ii: the Jacobi preconditioner
+      // D: sqrt(G_ii) d_i in [2^6, 2^7), so |G'_ij| <= sqrt(G'_ii G'_jj) < 2^14 (fp16 range)
+      const float d = pow2s<7>(sqrtf(gr));
+      dsc[i] = d;
+      idsc[i] = 1.f / d;  // exact: a power of two
+    }
   }
   __syncthreads();
   STAMP(5);
@@ -304,24 +310,29 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
   // shuffles plus (K = 32) one exchange with the partner warp through shared
   // memory and a 64-thread named barrier; the B operand of a product is the
   // block's own columns.  No block-wide barrier inside the PCG loop.
-  constexpr int NMT = K / 16, NCB = K / 8, NSW = NMT * NCB, KS = K / 4, KSUB = K / 8, NE = 4;
+  constexpr int NMT = K / 16, NCB = K / 8, NSW = NMT * NCB, KS = K / 8, KSUB = K / 16, NE = 4;
   static_assert(NSW <= NW, "solver warps");
   const int gq = lane >> 2, tq = lane & 3;
   const int cb = warp / NMT, mt = warp % NMT;
   const bool solver = warp < NSW;
-  // A fragments of the products: A = [Gr | Gi] (K x 2K), 3xTF32 split, per
-  // [m-tile][k-step][lane] {a0..a3} hi then lo (in the U region, free now)
-  for (int f = tid; f < NMT * KS * 32; f += NT) {
-    const int fm = f / (KS * 32), ks = (f / 32) % KS, ln = f & 31, g8 = ln >> 2, t8 = ln & 3;
-    const int r0 = 16 * fm + g8, c0 = 8 * ks + t8;
-    auto av = [&](int rr, int cc) { return cc < K ? Gs[rr * K + cc].x : Gs[rr * K + cc - K].y; };
-    uint4 h, l;
-    split_tf32(av(r0, c0), h.x, l.x);
-    split_tf32(av(r0 + 8, c0), h.y, l.y);
-    split_tf32(av(r0, c0 + 4), h.z, l.z);
-    split_tf32(av(r0 + 8, c0 + 4), h.w, l.w);
-    GA[2 * f] = h;
-    GA[2 * f + 1] = l;
+  // The K x K products run on mma.sync m16n8k16 in 3xFP16 on G' = D G D
+  // (D = diag(d_i), powers of two) and B' = D^-1 V F (F = diag(f_j), powers
+  // of two from a bound on each column's largest component): q = G v =
+  // D^-1 (G' B') F^-1, every scaling exact.  A = [G'r | G'i] (K x 2K): this
+  // warp's m-tile fragments (hi, lo) stay in registers for the whole solve.
+  uint32_t afh[KS][4], afl[KS][4];
+  if (solver) {
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int rg = 0; rg < 4; ++rg) {
+        const int i = 16 * mt + gq + 8 * (rg & 1), c = 16 * ks + 2 * tq + 8 * (rg >> 1);
+        const int k = c < K ? c : c - K;  // the pair (c, c + 1) lies in one half
+        const float2 g0 = Gs[i * K + k], g1 = Gs[i * K + k + 1];
+        const float di = dsc[i];
+        const float v0 = (c < K ? g0.x : g0.y) * di * dsc[k], v1 = (c < K ? g1.x : g1.y) * di * dsc[k + 1];
+        split2(v0, v1, afh[ks][rg], afl[ks][rg]);
+      }
   }
   int ie[NE], je[NE];
 #pragma unroll
@@ -344,24 +355,22 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
   static_assert(NMT <= 2 && NCB <= 4, "pair barriers");
   // column c in {0, 1} of this thread: its two rows, the 8 row lanes, then the
   // partner warp's half through exchange slot `slot` (fixed order: mt 0 + mt 1)
-  auto col_sum = [&](const float (&v)[NE], float (&out)[2], bool is_max, int slot) {
-    float a[2];
+  auto col_red = [&](float a0, float a1, bool is_max, int slot, float (&out)[2], bool sync) {
+    float a[2] = {a0, a1};
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      a[c] = is_max ? fmaxf(v[c], v[2 + c]) : v[c] + v[2 + c];
+    for (int c = 0; c < 2; ++c)
 #pragma unroll
       for (int o = 4; o < 32; o <<= 1) {
         const float a2 = __shfl_xor_sync(0xffffffffu, a[c], o);
         a[c] = is_max ? fmaxf(a[c], a2) : a[c] + a2;
       }
-    }
     if constexpr (NMT > 1) {
       float* xs = colx + slot * (NMT * K);  // [slot][mt][j]
       if (gq == 0) {
         xs[mt * K + je[0]] = a[0];
         xs[mt * K + je[1]] = a[1];
       }
-      pair_sync();
+      if (sync) pair_sync();
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const float x0 = xs[je[c]], x1 = xs[K + je[c]];
@@ -372,65 +381,77 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
       out[1] = a[1];
     }
   };
-  // v (P or X: this warp's rows of its block's columns) -> B fragments
-  // [half re/im][ksub][column n][t] x {b0h, b1h, b0l, b1l}; then the pair barrier
-  auto put_operand = [&](const float2 (&v)[NE]) {
-    uint32_t* bw = reinterpret_cast<uint32_t*>(BF);
+  auto col_sum = [&](const float (&v)[NE], float (&out)[2], bool is_max, int slot) {
+    col_red(is_max ? fmaxf(v[0], v[2]) : v[0] + v[2], is_max ? fmaxf(v[1], v[3]) : v[1] + v[3], is_max, slot, out,
+            true);
+  };
+  // B' fragments [half re/im][ksub][column n][slot t ^ ((n >> 1) & 3)] x
+  // {b0h, b1h, b0l, b1l} (uint4), the im half 64 B further (conflict-free
+  // STS.128 / LDS.128 phases)
+  auto bf_index = [&](int half, int ksub, int n, int t) {
+    return half * (KSUB * K * 4 + 4) + (ksub * K + n) * 4 + (t ^ ((n >> 1) & 3));
+  };
+  // v (P or X: this warp's rows of its block's columns) -> B' = D^-1 v F;
+  // lane pairs (g, g ^ 1) exchange so that the even lane packs the re half
+  // and the odd lane the im half of rows (g & ~1, g | 1); then the pair barrier
+  auto put_operand = [&](const float2 (&v)[NE], const float (&fs)[2]) {
+    const bool odd = gq & 1;
 #pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      const int k = ie[e], ksub = k >> 3, tt = k & 3, slot = (k >> 2) & 1;
-      uint32_t h, l;
-      split_tf32(v[e].x, h, l);
-      uint32_t* w0 = bw + (((0 * KSUB + ksub) * K + je[e]) * 4 + tt) * 4 + slot;
-      w0[0] = h;
-      w0[2] = l;
-      split_tf32(v[e].y, h, l);
-      uint32_t* w1 = bw + (((1 * KSUB + ksub) * K + je[e]) * 4 + tt) * 4 + slot;
-      w1[0] = h;
-      w1[2] = l;
+    for (int c = 0; c < 2; ++c) {
+      uint32_t hw[2], lw[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = 2 * h + c;
+        const float sc2 = idsc[ie[e]] * fs[c];
+        const float re = v[e].x * sc2, im = v[e].y * sc2;
+        const float other = __shfl_xor_sync(0xffffffffu, odd ? re : im, 4);
+        if (odd) split2(other, im, hw[h], lw[h]);  // rows (g - 1, g) of the im half
+        else split2(re, other, hw[h], lw[h]);      // rows (g, g + 1) of the re half
+      }
+      BF[bf_index(odd ? 1 : 0, mt, je[c], gq >> 1)] = make_uint4(hw[0], hw[1], lw[0], lw[1]);
     }
     pair_sync();
   };
-  // q = G v on this warp's tile (v as last put_operand'ed): Qr = Gr Vr - Gi Vi,
-  // Qi = Gr Vi + Gi Vr; four accumulator chains (hi*hi apart from the two
-  // correction terms) of KS and 2 KS MMAs
-  auto product = [&](float2 (&q)[NE]) {
+  // q = G v on this warp's tile (v as last put_operand'ed with column scales
+  // fs): Qr = Gr Vr - Gi Vi, Qi = Gr Vi + Gi Vr
+  auto product = [&](float2 (&q)[NE], const float (&fs)[2]) {
     float acc[4][4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a2 = 0; a2 < 4; ++a2)
 #pragma unroll
-      for (int d = 0; d < 4; ++d) acc[a][d] = 0.f;
-    const uint4* bre = BF + (0 * KSUB * K + 8 * cb + gq) * 4 + tq;
-    const uint4* bim = BF + (1 * KSUB * K + 8 * cb + gq) * 4 + tq;
-    const uint4* ga = GA + (mt * KS * 32 + lane) * 2;
+      for (int d = 0; d < 4; ++d) acc[a2][d] = 0.f;
+    const int n = 8 * cb + gq;
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
-      const uint4 br = bre[(ks % KSUB) * K * 4], bi = bim[(ks % KSUB) * K * 4];
-      const uint4 ah = ga[ks * 64], al = ga[ks * 64 + 1];
+      const uint4 br = BF[bf_index(0, ks % KSUB, n, tq)], bi = BF[bf_index(1, ks % KSUB, n, tq)];
       uint4 b1 = br, b2 = bi;  // Gr block: Qr += Gr Vr, Qi += Gr Vi
       if (ks >= KSUB) {        // Gi block: Qr += Gi (-Vi), Qi += Gi Vr
-        b1 = make_uint4(bi.x ^ 0x80000000u, bi.y ^ 0x80000000u, bi.z ^ 0x80000000u, bi.w ^ 0x80000000u);
+        b1 = make_uint4(bi.x ^ 0x80008000u, bi.y ^ 0x80008000u, bi.z ^ 0x80008000u, bi.w ^ 0x80008000u);
         b2 = br;
       }
-      mma_tf32(acc[0], ah, b1.x, b1.y);
-      mma_tf32(acc[1], al, b1.x, b1.y);
-      mma_tf32(acc[1], ah, b1.z, b1.w);
-      mma_tf32(acc[2], ah, b2.x, b2.y);
-      mma_tf32(acc[3], al, b2.x, b2.y);
-      mma_tf32(acc[3], ah, b2.z, b2.w);
+      hmma(acc[0], afh[ks], b1.x, b1.y);
+      hmma(acc[1], afh[ks], b1.z, b1.w);
+      hmma(acc[1], afl[ks], b1.x, b1.y);
+      hmma(acc[2], afh[ks], b2.x, b2.y);
+      hmma(acc[3], afh[ks], b2.z, b2.w);
+      hmma(acc[3], afl[ks], b2.x, b2.y);
     }
 #pragma unroll
-    for (int d = 0; d < 4; ++d) q[d] = make_float2(acc[0][d] + acc[1][d], acc[2][d] + acc[3][d]);
+    for (int d = 0; d < 4; ++d) {
+      const float u2 = idsc[ie[d]] / fs[d & 1];  // exact: powers of two
+      q[d] = make_float2((acc[0][d] + acc[1][d]) * u2, (acc[2][d] + acc[3][d]) * u2);
+    }
   };
 
   // ---- Jac-PCG / CG (linsolve.py:217-294) on the K identity RHS, w0 = 0
-  float icr[NE], icc[2], rz[2];
+  float icr[NE], icc[2], rz[2], pbm[2], pfs[2];
   float2 x[NE], r[NE], pv[NE], qv[NE];
   if (solver) {
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       icc[c] = use_c ? 1.f / cdg[je[c]] : 1.f;
       rz[c] = textbook ? icc[c] : (use_c ? icc[c] * icc[c] : 1.f);
+      pbm[c] = (use_c ? icc[c] : 1.f) * idsc[je[c]];  // max_k |P0_kj| / d_k (P0 diagonal)
     }
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
@@ -455,7 +476,7 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
   if (solver) {
     for (int t = 1; t <= p.T; ++t) {
       if (t > 1) {
-        product(qv);
+        product(qv, pfs);
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
           qv[e].x = fmaf(xi, pv[e].x, qv[e].x);  // A p = G p + xi p
@@ -470,14 +491,25 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
         cp[e] = pv[e].x * (qv[e].x * qf) + pv[e].y * (qv[e].y * qf);
       }
       float curv[2], al[2];
-      col_sum(cp, curv, false, 0);
+      if (t == 1) {
+        // P0 = diag(p_jj): the only non-zero term of column j's curvature is
+        // p_jj (A_jj p_jj) qf_j (the sum of it and exact zeros, computed here
+        // by every owner of the column without a reduction)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const float pjj = use_c ? icc[c] : 1.f, qf = alg1 ? icc[c] : 1.f;
+          curv[c] = pjj * ((cdg[je[c]] * pjj) * qf);
+        }
+      } else {
+        col_sum(cp, curv, false, 0);
+      }
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const bool act = rz[c] > 0.f;
         if (curv[c] <= 0.f && act) atomicOr(flags, 1);
         al[c] = act ? rz[c] / (curv[c] > 0.f ? curv[c] : 1.f) : 0.f;
       }
-      float rp[NE];
+      float rp[NE], rm[NE];
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
         const float a = al[e & 1], qf = alg1 ? icr[e] : 1.f;
@@ -487,15 +519,23 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
         r[e].y -= a * (qv[e].y * qf);
         const float ic = textbook ? icr[e] : 1.f;
         rp[e] = r[e].x * (r[e].x * ic) + r[e].y * (r[e].y * ic);
+        rm[e] = fmaxf(fabsf(r[e].x * ic), fabsf(r[e].y * ic)) * idsc[ie[e]];
       }
       if (t == p.T) break;  // the last direction update feeds nothing
       STAMP(13 + 4 * t);
-      float rn[2], be[2];
+      // rz and the column max of |R C^-b| / d (one exchange: two slots, one barrier)
+      float rn[2], be[2], rmx[2];
+      col_red(rm[0] > rm[2] ? rm[0] : rm[2], rm[1] > rm[3] ? rm[1] : rm[3], true, 3, rmx, false);
       col_sum(rp, rn, false, 1);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
+        const float x0 = colx[3 * NMT * K + je[c]];
+        rmx[c] = NMT > 1 ? fmaxf(x0, colx[3 * NMT * K + K + je[c]]) : rmx[c];
         be[c] = rz[c] > 0.f ? rn[c] / rz[c] : 0.f;
         rz[c] = rn[c];
+        // |P_new| <= |R C^-b| + |beta| |P|, per component: the next operand's scale
+        pbm[c] = rmx[c] + fabsf(be[c]) * pbm[c];
+        pfs[c] = pow2s<14>(pbm[c]);
       }
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
@@ -503,7 +543,7 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
         pv[e] = make_float2(fmaf(r[e].x, ic, bb * pv[e].x), fmaf(r[e].y, ic, bb * pv[e].y));
       }
       STAMP(14 + 4 * t);
-      put_operand(pv);  // the partner is past this iteration's product (barrier of slot 0)
+      put_operand(pv, pfs);  // the partner is past this iteration's product (barrier of slot 0)
       STAMP(15 + 4 * t);
     }
   }
@@ -514,8 +554,15 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
   double sig = 0.0;
   int diag_i = -1;
   if (solver) {
-    put_operand(x);  // the partner is past its last product (barrier of slot 0 in iteration T)
-    product(gx);
+    // X's exact column max (one exchange) -> its operand scale
+    float xa[NE], xmx[2], xfs[2];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) xa[e] = fmaxf(fabsf(x[e].x), fabsf(x[e].y)) * idsc[ie[e]];
+    col_sum(xa, xmx, true, 4);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) xfs[c] = pow2s<14>(xmx[c]);
+    put_operand(x, xfs);  // the partner is past its last product (barrier of slot 0 in iteration T)
+    product(gx, xfs);
     double fp = 0.0;
 #pragma unroll
     for (int e = 0; e < NE; ++e) fp += (double)x[e].x * gx[e].x + (double)x[e].y * gx[e].y;
@@ -692,8 +739,8 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
 template <int K>
 size_t smem_bytes(int M) {
   using g = G<K>;
-  return (size_t)M * g::NC * 2 * 2 + 2 * (size_t)K * K * 8 + g::XT_BYTES + 4 * K * 4 + (K / 8) * K * 8 +
-         NW * 8 + 3 * (K / 16) * K * 4 + NW * 4 + (K + 1) * 4;
+  return (size_t)M * g::NC * 2 * 2 + 2 * (size_t)K * K * 8 + g::XT_BYTES + 6 * K * 4 + (K / 8) * K * 8 +
+         NW * 8 + 5 * (K / 16) * K * 4 + NW * 4 + (K + 1) * 4;
 }
 
 }  // namespace fs
