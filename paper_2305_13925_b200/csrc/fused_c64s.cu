@@ -116,9 +116,10 @@ __device__ __forceinline__ void hmma(float (&d)[4], const uint32_t (&a)[4], uint
 }
 // fp16 split of a pair: hi = fp16(x), lo = fp16(x - hi) (paired conversions)
 __device__ __forceinline__ void split2(float x, float y, uint32_t& hi, uint32_t& lo) {
-  const __half2 h = __floats2half2_rn(x, y);
+  const float2 v = make_float2(x, y);
+  const __half2 h = __float22half2_rn(v);
   const float2 hf = __half22float2(h);
-  const __half2 l = __floats2half2_rn(x - hf.x, y - hf.y);
+  const __half2 l = __float22half2_rn(__fadd2_rn(v, make_float2(-hf.x, -hf.y)));
   hi = *reinterpret_cast<const uint32_t*>(&h);
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
@@ -130,6 +131,10 @@ __device__ __forceinline__ float pow2s(float m) {
   const int E = (__float_as_int(m) >> 23) & 0xff;  // 0 for subnormal m: clamped below
   const int f = TB + 253 - E;
   return __int_as_float((f > 254 ? 254 : (f < 1 ? 1 : f)) << 23);
+}
+// 1 / s for a power of two s in the normal range (exact)
+__device__ __forceinline__ float pow2_inv(float s) {
+  return __int_as_float((254 - ((__float_as_int(s) >> 23) & 0xff)) << 23);
 }
 // the per-column scale of the fp16 W / Gram operands: max in [2^14, 2^15)
 __device__ __forceinline__ float col_scale(float m) { return pow2s<15>(m); }
@@ -212,7 +217,7 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
     if (tid < K) {
       const float sv = col_scale(__int_as_float(flags[1 + tid]));
       sc[tid] = sv;
-      isc[tid] = 1.f / sv;  // exact: a power of two
+      isc[tid] = pow2_inv(sv);
     }
 #pragma unroll
     for (int i = 0; i < NLMAX; ++i)
@@ -297,7 +302,7 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
       // D: sqrt(G_ii) d_i in [2^6, 2^7), so |G'_ij| <= sqrt(G'_ii G'_jj) < 2^14 (fp16 range)
       const float d = pow2s<7>(sqrtf(gr));
       dsc[i] = d;
-      idsc[i] = 1.f / d;  // exact: a power of two
+      idsc[i] = pow2_inv(d);
     }
   }
   __syncthreads();
@@ -414,7 +419,7 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
   };
   // q = G v on this warp's tile (v as last put_operand'ed with column scales
   // fs): Qr = Gr Vr - Gi Vi, Qi = Gr Vi + Gi Vr
-  auto product = [&](float2 (&q)[NE], const float (&fs)[2]) {
+  auto product = [&](float2 (&q)[NE], const float (&ifs)[2]) {
     float acc[4][4];
 #pragma unroll
     for (int a2 = 0; a2 < 4; ++a2)
@@ -438,13 +443,13 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
     }
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
-      const float u2 = idsc[ie[d]] / fs[d & 1];  // exact: powers of two
+      const float u2 = idsc[ie[d]] * ifs[d & 1];  // exact: powers of two
       q[d] = make_float2((acc[0][d] + acc[1][d]) * u2, (acc[2][d] + acc[3][d]) * u2);
     }
   };
 
   // ---- Jac-PCG / CG (linsolve.py:217-294) on the K identity RHS, w0 = 0
-  float icr[NE], icc[2], rz[2], pbm[2], pfs[2];
+  float icr[NE], icc[2], rz[2], pbm[2], pfs[2], pifs[2];
   float2 x[NE], r[NE], pv[NE], qv[NE];
   if (solver) {
 #pragma unroll
@@ -476,7 +481,7 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
   if (solver) {
     for (int t = 1; t <= p.T; ++t) {
       if (t > 1) {
-        product(qv, pfs);
+        product(qv, pifs);
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
           qv[e].x = fmaf(xi, pv[e].x, qv[e].x);  // A p = G p + xi p
@@ -507,7 +512,7 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
       for (int c = 0; c < 2; ++c) {
         const bool act = rz[c] > 0.f;
         if (curv[c] <= 0.f && act) atomicOr(flags, 1);
-        al[c] = act ? rz[c] / (curv[c] > 0.f ? curv[c] : 1.f) : 0.f;
+        al[c] = act ? rz[c] * __frcp_rn(curv[c] > 0.f ? curv[c] : 1.f) : 0.f;
       }
       float rp[NE], rm[NE];
 #pragma unroll
@@ -531,11 +536,12 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
       for (int c = 0; c < 2; ++c) {
         const float x0 = colx[3 * NMT * K + je[c]];
         rmx[c] = NMT > 1 ? fmaxf(x0, colx[3 * NMT * K + K + je[c]]) : rmx[c];
-        be[c] = rz[c] > 0.f ? rn[c] / rz[c] : 0.f;
+        be[c] = rz[c] > 0.f ? rn[c] * __frcp_rn(rz[c]) : 0.f;
         rz[c] = rn[c];
         // |P_new| <= |R C^-b| + |beta| |P|, per component: the next operand's scale
         pbm[c] = rmx[c] + fabsf(be[c]) * pbm[c];
         pfs[c] = pow2s<14>(pbm[c]);
+        pifs[c] = pow2_inv(pfs[c]);
       }
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
@@ -559,10 +565,14 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
 #pragma unroll
     for (int e = 0; e < NE; ++e) xa[e] = fmaxf(fabsf(x[e].x), fabsf(x[e].y)) * idsc[ie[e]];
     col_sum(xa, xmx, true, 4);
+    float xifs[2];
 #pragma unroll
-    for (int c = 0; c < 2; ++c) xfs[c] = pow2s<14>(xmx[c]);
+    for (int c = 0; c < 2; ++c) {
+      xfs[c] = pow2s<14>(xmx[c]);
+      xifs[c] = pow2_inv(xfs[c]);
+    }
     put_operand(x, xfs);  // the partner is past its last product (barrier of slot 0 in iteration T)
-    product(gx, xfs);
+    product(gx, xifs);
     double fp = 0.0;
 #pragma unroll
     for (int e = 0; e < NE; ++e) fp += (double)x[e].x * gx[e].x + (double)x[e].y * gx[e].y;
@@ -636,7 +646,7 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
     for (int e = 0; e < NE; ++e) {
       const int i = ie[e], j = je[e];
       const float tj = tjc[e & 1];
-      if (i == 0) tcs[j] = 1.f / tj;  // exact: a power of two
+      if (i == 0) tcs[j] = pow2_inv(tj);
       const float f = tj * isc[i];
       const float xr = x[e].x * f, xim = x[e].y * f;
       uint32_t h0, l0, h1, l1;
@@ -707,14 +717,22 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
 #pragma unroll
       for (int n = 0; n < NTL; ++n) {
         const int ju = 4 * n + t4;  // user column of this thread's (re, im) pair
-        const float it = its[n];
-        const float ws = bt * it;
+        const float ws = bt * its[n];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int a = 32 * mp + 16 * h + gr;
           __stcs(Wb + (int64_t)a * K + ju, make_float2(acc[h][n][0] * ws, acc[h][n][1] * ws));
           __stcs(Wb + (int64_t)(a + 8) * K + ju, make_float2(acc[h][n][2] * ws, acc[h][n][3] * ws));
-          if (Fb) {
+        }
+      }
+      if (Fb) {
+#pragma unroll
+        for (int n = 0; n < NTL; ++n) {
+          const int ju = 4 * n + t4;
+          const float it = its[n];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int a = 32 * mp + 16 * h + gr;
             __stcs(Fb + (int64_t)a * K + ju, make_float2(acc[h][n][0] * it, acc[h][n][1] * it));
             __stcs(Fb + (int64_t)(a + 8) * K + ju, make_float2(acc[h][n][2] * it, acc[h][n][3] * it));
           }
