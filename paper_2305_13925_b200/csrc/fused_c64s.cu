@@ -3,6 +3,7 @@
 //
 //   A = H^H H + xi I        gram_regularized (precoder.py:53-61)
 //   Jac-PCG / CG, T iters   linsolve.py:217-294 on the K identity RHS, w0 = 0
+//   or direct: X = A^-1     rzf_direct (precoder.py:73-78), Gauss-Jordan in place
 //   GX, ||F||^2, beta       precoder.py:64-70 (K x K form)
 //   W = beta H X, F = H X   precoder.py:90
 //   B = beta GX, SINR, SE   coupling + sinr_eq9 (metrics.py:35-58)
@@ -174,6 +175,7 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
   const bool use_c = p.method == XL_JACPCG;
   const bool textbook = use_c && p.variant == XL_TEXTBOOK;
   const bool alg1 = use_c && !textbook;
+  const bool direct = p.method == XL_DIRECT;
   const float xi = (float)(p.xi_b ? p.xi_b[b] : p.xi);
   STAMP(0);
 
@@ -474,11 +476,53 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
       float2 gij = Gs[ie[e] * K + je[e]];
       if (ie[e] == je[e]) gij.x += xi;
       qv[e] = make_float2(gij.x * pjj, gij.y * pjj);
+      if (direct) x[e] = gij;  // A = G + xi I, inverted in place below
     }
   }
   __syncthreads();  // G read (fragments, first product): the operand region may overwrite it
   STAMP(11);
-  if (solver) {
+  if (direct) {
+    // ---- rzf_direct (precoder.py:73-78): X = A^-1 by in-place Gauss-Jordan
+    // elimination without pivoting (A Hermitian positive definite: its pivots
+    // are the squared Cholesky diagonal, so a pivot <= 0 is exactly the
+    // Cholesky breakdown of linsolve.py:113-116 -> XL_STATUS_CHOLESKY).  Step
+    // k publishes row k and column k (double-buffered: one barrier per step).
+    float2* rowb = reinterpret_cast<float2*>(XT);  // [2][K]
+    float2* colb = rowb + 2 * K;                   // [2][K]
+    for (int k = 0; k < K; ++k) {
+      const int buf = (k & 1) * K;
+      if (solver) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          if (ie[e] == k) rowb[buf + je[e]] = x[e];
+          if (je[e] == k) colb[buf + ie[e]] = x[e];
+        }
+      }
+      __syncthreads();
+      const float pk = rowb[buf + k].x;
+      if (!(pk > 0.f)) {
+        if (tid == 0) flags[0] |= 4;
+      }
+      const float ip = 1.f / pk;
+      if (solver) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          const int i = ie[e], j = je[e];
+          if (i == k && j == k) {
+            x[e] = make_float2(ip, 0.f);
+          } else if (i == k) {
+            x[e] = make_float2(x[e].x * ip, x[e].y * ip);
+          } else if (j == k) {
+            x[e] = make_float2(-x[e].x * ip, -x[e].y * ip);
+          } else {
+            const float2 a = colb[buf + i], c = rowb[buf + j];  // a_ik, a_kj (old)
+            const float2 m = make_float2((a.x * c.x - a.y * c.y) * ip, (a.x * c.y + a.y * c.x) * ip);
+            x[e] = make_float2(x[e].x - m.x, x[e].y - m.y);
+          }
+        }
+      }
+    }
+  } else if (solver) {
     for (int t = 1; t <= p.T; ++t) {
       if (t > 1) {
         product(qv, pifs);
@@ -747,7 +791,8 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
     p.sum_se[b] = s;
     p.beta[b] = btd;
     int st = 0;
-    if (flags[0] & 2) st = XL_STATUS_SPLITTING;
+    if (flags[0] & 4) st = XL_STATUS_CHOLESKY;
+    else if (flags[0] & 2) st = XL_STATUS_SPLITTING;
     else if (flags[0] & 1) st = XL_STATUS_NOT_HPD;
     else if (degenerate) st = XL_STATUS_DEGENERATE;
     p.status[b] = st;
@@ -764,7 +809,7 @@ size_t smem_bytes(int M) {
 }  // namespace fs
 
 bool fc64s_supported(int dtype, int method, int M, int K) {
-  if (dtype != XL_C64 || (method != XL_JACPCG && method != XL_CG)) return false;
+  if (dtype != XL_C64 || (method != XL_JACPCG && method != XL_CG && method != XL_DIRECT)) return false;
   const char* e = getenv("XL_SMALL_K_MMA");  // "0": keep the tcgen05 kernel (A/B, tests)
   if (e && e[0] == '0') return false;
   if (K != 16 && K != 32) return false;
