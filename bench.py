@@ -301,7 +301,7 @@ def run_reference(a):
 def path_of(X, dt, method, M, K):
     import torch
     tc = X.tensor_core_path(dt, method, M, K)
-    if tc == "tcgen05":
+    if tc in ("tcgen05", "tcgen05+mma.sync"):  # the latter: Gram / W (most flops) on tcgen05
         return "tc3xfp16"
     if tc == "mma.sync":
         return "mma3xfp16"

@@ -66,7 +66,8 @@ uint64_t xl_launch_count(void);
  * 1 = tcgen05 (the fused kernel at K = 64 or K in {16, 32} with M K > 8192,
  * the streaming Gram / W + cluster Jac-PCG chain at K in {128, 256}),
  * 2 = warp-level mma.sync (complex64 K in {16, 32}, M % 32 == 0, M K <= 8192:
- * the small-K fused kernel), 0 = none (SIMT / DMMA / cuBLAS-free fp64). */
+ * the small-K fused kernel), 3 = the same kernel with its Gram / W on tcgen05
+ * (K = 32, M % 128 == 0; XL_SMALL_K_TC=0 selects 2), 0 = none (SIMT / DMMA). */
 int xl_rzf_uses_tensor_cores(int dtype, int method, int32_t M, int32_t K);
 
 /* Batched regularized Gram A_b = H_b^H H_b + xi_b I, Hermitian by

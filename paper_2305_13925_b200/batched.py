@@ -121,11 +121,13 @@ def uses_tensor_cores(dtype, method, M, K) -> bool:
 
 
 def tensor_core_path(dtype, method, M, K) -> str:
-    """"tcgen05" (fused / streaming tcgen05 kernels), "mma.sync" (the small-K
-    fused kernel on the warp-level tensor cores) or "none" (SIMT / DMMA)."""
+    """"tcgen05" (fused / streaming tcgen05 kernels), "tcgen05+mma.sync" (the
+    small-K kernel with tcgen05 Gram / W and the K x K solve on mma.sync),
+    "mma.sync" (the small-K kernel entirely on the warp-level tensor cores) or
+    "none" (SIMT / DMMA)."""
     L.load_library()
     code = int(L._lib.xl_rzf_uses_tensor_cores(dtype_code(dtype), METHODS[method], M, K))
-    return {0: "none", 1: "tcgen05", 2: "mma.sync"}[code]
+    return {0: "none", 1: "tcgen05", 2: "mma.sync", 3: "tcgen05+mma.sync"}[code]
 
 
 def rzf_batched(H: torch.Tensor, xi, power: float, method: str = "jacpcg", T: int = 4,

@@ -49,6 +49,9 @@
 
 namespace xl {
 namespace fs {
+namespace t {
+#include "tc_ptx.cuh"  // tcgen05 / TMEM / mbarrier wrappers (TC variant)
+}
 
 constexpr int NT = 256, NW = NT / 32;
 
@@ -139,6 +142,27 @@ __device__ __forceinline__ float pow2_inv(float s) {
 }
 // the per-column scale of the fp16 W / Gram operands: max in [2^14, 2^15)
 __device__ __forceinline__ float col_scale(float m) { return pow2s<15>(m); }
+// tcgen05.ld 16x256b x8: 16 TMEM lanes x 64 columns; thread t gets, per 8-column
+// group n, (lane t/4, cols 8n + 2(t%4), +1) then (lane t/4 + 8, same columns)
+__device__ __forceinline__ void tmem_ld_16x256b_x8(uint32_t ta, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(ta));
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+// tcgen05 shared-memory descriptor, SWIZZLE_128B (layout type 2 at bits 61-63,
+// version 1 at bit 46; addresses and offsets in 16-B units)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
+}
 template <int SEG>
 __device__ __forceinline__ double seg_sum(double v) {  // sum over aligned SEG-lane segments
 #pragma unroll
@@ -146,13 +170,18 @@ __device__ __forceinline__ double seg_sum(double v) {  // sum over aligned SEG-l
   return v;
 }
 
-template <int K>
+// TC (K = 32, M % 128 == 0): the Gram and W run on tcgen05 (TMEM accumulators,
+// one elected lane issues, async), Z and Xe' in the canonical no-swizzle
+// core-matrix layout, the W epilogue from TMEM (thread = antenna row).
+// Otherwise both run on mma.sync from XOR-swizzled tiles.
+template <int K, bool TC>
 __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
   using g = G<K>;
   constexpr int NC = g::NC, RC = g::RC, US = g::US;
-  extern __shared__ __align__(128) uint8_t smem[];
+  static_assert(!TC || K == 32, "tcgen05 variant: K = 32");
+  extern __shared__ __align__(1024) uint8_t smem[];
   const int M = p.M;
-  uint8_t* Zh = smem;                                        // [M][NC] fp16, swizzled
+  uint8_t* Zh = smem;                                        // [M][NC] fp16, swizzled (= SWIZZLE_128B canonical)
   uint8_t* Zl = Zh + (size_t)M * NC * 2;
   float2* Gs = reinterpret_cast<float2*>(Zl + (size_t)M * NC * 2);  // [K][K] G = H^H H (no xi)
   float2* Ps = Gs + K * K;                                   // [K][K] P, then X
@@ -170,6 +199,8 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
   float* colx = reinterpret_cast<float*>(dred + NW);         // [5][K / 16][K] column exchange slots
   float* sse = colx + 5 * (K / 16) * K;                      // [NW]
   int* flags = reinterpret_cast<int*>(sse + NW);             // [0] status bits, [1..K] column max bits
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(flags + ((K + 2) & ~1));  // TC: MMA completion
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 1);             // TC: TMEM base
   const int64_t b = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool use_c = p.method == XL_JACPCG;
@@ -190,6 +221,16 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
       const float2* nx = p.H + (b + p.pf) * (int64_t)M * K;
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx), "r"((uint32_t)(M * K * 8)) : "memory");
     }
+    if constexpr (TC) {
+      if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+      }
+      if (tid == 0) {
+        t::mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
+    }
     float4 v[NLMAX];
 #pragma unroll
     for (int i = 0; i < NLMAX; ++i)
@@ -207,7 +248,9 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
       m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
       m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
     }
-    __syncthreads();  // flags zeroed
+    if constexpr (TC) t::tc_before();
+    __syncthreads();  // flags zeroed (TC: TMEM allocated, barrier initialised)
+    if constexpr (TC) t::tc_after();
     STAMP(1);
     if (lane < PR) {
       atomicMax(&flags[1 + 2 * u], __float_as_int(m0));
@@ -233,13 +276,45 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
         *reinterpret_cast<uint2*>(Zl + off) = lo;
       }
   }
+  if constexpr (TC) t::fence_async_smem();  // generic-proxy tile writes -> the tensor cores' async proxy
   __syncthreads();
   STAMP(3);
+  const uint32_t tmem = TC ? *tslot : 0u;
 
   // ---- Gram on the tensor cores: U = Zh^T Zh + 2 Zh^T Zl over the M antennas
   // (warp tile GMP m16 x GNP n8: the A and B fragment loads per k-step are
   // balanced, 4 ldmatrix.x4 per warp at K = 32)
-  if (warp < g::GWARPS) {
+  if constexpr (TC) {
+    // U (TMEM cols 0-63) = Zh^T Zh, V (cols 64-127) = Zh^T Zl: M = 128 (the second
+    // 64-component atom of A is the Zl plane: rows 64-127 ignored), N = 64, K = 16
+    // antennas per MMA.  The swizzled tiles are SWIZZLE_128B canonical (MN-major
+    // here: a 128-B row holds one antenna's 64 components)
+    constexpr uint32_t IDG = t::idesc(128, NC, 1, 1);
+    constexpr uint32_t ZPL = 256 * NC * 2;  // one 256-antenna fp16 plane
+    if (warp == 0) {
+      t::tc_after();
+      const uint32_t zh = smem_u32(Zh), zl = smem_u32(Zl);
+      if ((zh & 1023u) != 0) asm volatile("trap;");  // SWIZZLE_128B atoms need 1024-B alignment
+      for (int ks = 0; ks < M / 16; ++ks) {
+        const uint64_t dh = sw128_desc(zh + ks * 2048, ZPL, 1024), dl = sw128_desc(zl + ks * 2048, ZPL, 1024);
+        t::mma_w(tmem, dh, dh, IDG, ks > 0);
+        t::mma_w(tmem + 64, dh, dl, IDG, ks > 0);
+      }
+      t::commit_w(mbar);
+    }
+    t::mbar_wait(mbar, 0);
+    t::tc_after();
+    if (warp < 2) {  // TMEM lanes 0-63 = U rows (component c1)
+      float d[64], e2[64];
+      t::tmem_ld<64>(tmem + ((32u * warp) << 16), d);
+      t::tmem_ld<64>(tmem + ((32u * warp) << 16) + 64, e2);
+      t::tmem_wait_ld();
+      float* ur = Us + (32 * warp + lane) * US;
+#pragma unroll
+      for (int c = 0; c < 64; c += 2)
+        *reinterpret_cast<float2*>(ur + c) = make_float2(fmaf(2.f, e2[c], d[c]), fmaf(2.f, e2[c + 1], d[c + 1]));
+    }
+  } else if (warp < g::GWARPS) {
     constexpr int GNP = g::GNP, GMP = g::GMP;
     const int m0 = (warp % (g::MT / GMP)) * 16 * GMP, n0 = (warp / (g::MT / GMP)) * GNP * 8;
     float acc[GMP][GNP][4], acl[GMP][GNP][4];
@@ -709,11 +784,74 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
       for (int e = 0; e < NE; ++e) Xo[ie[e] * K + je[e]] = x[e];
     }
   }
+  if constexpr (TC) t::fence_async_smem();
   __syncthreads();  // XT, tcs, sse
   STAMP(10);
 
-  // ---- W = beta Z' Xe' / t_j on the tensor cores (3xFP16), two m-tiles per warp step
-  {
+  // ---- W = beta Z' Xe' / t_j
+  if constexpr (TC) {
+    // tcgen05: D_mt (TMEM cols 128 + 64 mt) = Zh Xh + Zh Xl + Zl Xh for the 128-antenna
+    // tile mt; A = Z and B = Xe'^T both SWIZZLE_128B K-major (8-row groups 1024 B
+    // apart, a K step of 16 components = +32 B)
+    constexpr uint32_t IDW = t::idesc(128, NC, 0, 0);
+    if (warp == 0) {
+      t::tc_after();
+      const uint32_t zh = smem_u32(Zh), zl = smem_u32(Zl), xh = smem_u32(XT), xl = xh + NC * NC * 2;
+      if ((xh & 1023u) != 0) asm volatile("trap;");
+      for (int mt = 0; mt < M / 128; ++mt)
+#pragma unroll
+        for (int ks = 0; ks < NC / 16; ++ks) {
+          const uint64_t ah = sw128_desc(zh + mt * 16384 + ks * 32, 16, 1024);
+          const uint64_t al = sw128_desc(zl + mt * 16384 + ks * 32, 16, 1024);
+          const uint64_t bh = sw128_desc(xh + ks * 32, 16, 1024), bl = sw128_desc(xl + ks * 32, 16, 1024);
+          const uint32_t d = tmem + 128 + 64 * mt;
+          t::mma_w(d, ah, bh, IDW, ks > 0);
+          t::mma_w(d, ah, bl, IDW, 1);
+          t::mma_w(d, al, bh, IDW, 1);
+        }
+      t::commit_w(mbar);
+    }
+    t::mbar_wait(mbar, 1);
+    t::tc_after();
+    STAMP(7);
+    // TMEM -> registers in the mma.sync accumulator layout (tcgen05.ld 16x256b: thread
+    // t holds rows t/4, t/4 + 8 of a 16-lane slab, columns 2 (t%4) + {0, 1} of every
+    // 8-column group) -> beta / t_j -> 8-B streaming stores, 32 B contiguous per row
+    const float bt = (float)btd;
+    float2* Wb = p.W + b * (int64_t)M * K;
+    float2* Fb = p.F ? p.F + b * (int64_t)M * K : nullptr;
+    const int gr = lane >> 2, t4 = lane & 3;
+    float ws[8], its8[8];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      its8[n] = tcs[4 * n + t4];
+      ws[n] = bt * its8[n];
+    }
+    for (int mt = warp >> 2; mt < M / 128; mt += 2)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = 128 * mt + 32 * (warp & 3) + 16 * h + gr;
+        float d[32];
+        tmem_ld_16x256b_x8(tmem + 128 + 64 * mt + ((32u * (warp & 3) + 16u * h) << 16), d);
+        t::tmem_wait_ld();
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+          const int j = 4 * n + t4;
+          __stcs(Wb + (int64_t)a * K + j, make_float2(d[4 * n] * ws[n], d[4 * n + 1] * ws[n]));
+          __stcs(Wb + (int64_t)(a + 8) * K + j, make_float2(d[4 * n + 2] * ws[n], d[4 * n + 3] * ws[n]));
+          if (Fb) {
+            __stcs(Fb + (int64_t)a * K + j, make_float2(d[4 * n] * its8[n], d[4 * n + 1] * its8[n]));
+            __stcs(Fb + (int64_t)(a + 8) * K + j, make_float2(d[4 * n + 2] * its8[n], d[4 * n + 3] * its8[n]));
+          }
+        }
+      }
+    t::tc_before();
+    __syncthreads();  // every TMEM read done
+    if (warp == 0) {
+      t::tc_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    }
+  } else {
     constexpr int NTL = g::NTL;
     const uint32_t zh = smem_u32(Zh), zl = smem_u32(Zl), xh = smem_u32(XT), xl = xh + NC * NC * 2;
     const int q = lane >> 3, r8 = lane & 7, gr = lane >> 2, t4 = lane & 3;
@@ -803,10 +941,16 @@ template <int K>
 size_t smem_bytes(int M) {
   using g = G<K>;
   return (size_t)M * g::NC * 2 * 2 + 2 * (size_t)K * K * 8 + g::XT_BYTES + 6 * K * 4 + (K / 8) * K * 8 +
-         NW * 8 + 5 * (K / 16) * K * 4 + NW * 4 + (K + 1) * 4;
+         NW * 8 + 5 * (K / 16) * K * 4 + NW * 4 + (K + 2) * 4 + 16;
 }
 
 }  // namespace fs
+
+// the K = 32 variant with tcgen05 Gram / W (XL_SMALL_K_TC=0 keeps mma.sync)
+bool fc64s_uses_tcgen05(int M, int K) {
+  const char* tce = getenv("XL_SMALL_K_TC");
+  return K == 32 && M % 128 == 0 && !(tce && tce[0] == '0');
+}
 
 bool fc64s_supported(int dtype, int method, int M, int K) {
   if (dtype != XL_C64 || (method != XL_JACPCG && method != XL_CG && method != XL_DIRECT)) return false;
@@ -842,8 +986,10 @@ int fc64s_rzf(int method, int variant, const void* H, int64_t B, int M, int K, d
     p.pf = (per_sm > 0 ? per_sm : 1) * nsm;
     kern<<<(unsigned)B, fs::NT, sm, st>>>(p);
   };
-  if (K == 16) launch(fs::small_k_kernel<16>, fs::smem_bytes<16>(M));
-  else launch(fs::small_k_kernel<32>, fs::smem_bytes<32>(M));
+  const bool tc = fc64s_uses_tcgen05(M, K);
+  if (K == 16) launch(fs::small_k_kernel<16, false>, fs::smem_bytes<16>(M));
+  else if (tc) launch(fs::small_k_kernel<32, true>, fs::smem_bytes<32>(M));
+  else launch(fs::small_k_kernel<32, false>, fs::smem_bytes<32>(M));
   if (p.trace) {  // dev: per-phase cycle deltas, averaged over the traced CTAs
     static long long h[64 * 64];
     cudaMemcpyAsync(h, p.trace, sizeof(h), cudaMemcpyDeviceToHost, st);

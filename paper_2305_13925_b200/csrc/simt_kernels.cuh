@@ -100,6 +100,7 @@ int fc128_rzf(int method, int variant, const void* H, int64_t B, int M, int K, d
 
 // fused_c64s.cu: one CTA per realization (two per SM), Gram / W on mma.sync (3xFP16), fp32 SIMT solve
 bool fc64s_supported(int dtype, int method, int M, int K);
+bool fc64s_uses_tcgen05(int M, int K);
 int fc64s_rzf(int method, int variant, const void* H, int64_t B, int M, int K, double xi, const double* xi_b,
               double power, int T, double sigma2, void* W, void* F, double* beta, double* gamma, double* sum_se,
               void* X, int32_t* status, cudaStream_t st);

@@ -72,7 +72,8 @@ uint64_t xl_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RE
 const char* xl_last_error(void) { return g_err; }
 
 int xl_rzf_uses_tensor_cores(int dtype, int method, int32_t M, int32_t K) {
-  if (fc64s_supported(dtype, method, M, K)) return 2;  // warp-level mma.sync kernel (fused_c64s.cu)
+  // small-K kernel (fused_c64s.cu): 3 = tcgen05 Gram / W + mma.sync solve, 2 = all mma.sync
+  if (fc64s_supported(dtype, method, M, K)) return fc64s_uses_tcgen05(M, K) ? 3 : 2;
   if (fused_supported(dtype, method, M, K)) return 1;
   // K = 256: streaming tcgen05 Gram / W + the 8-CTA cluster Jac-PCG / CG
   if (method != XL_DIRECT && lk_supported(dtype, M, K)) return 1;

@@ -57,21 +57,33 @@ def _check(H, out, alpha, power, method, T, variant):
             np.testing.assert_allclose(gam[b], g, rtol=max(1e-3, gfac * wt), atol=1e-6 * np.abs(g).max())
 
 
-@pytest.fixture(params=["mma.sync", "tcgen05"])
+@pytest.fixture(params=["small-k", "small-k-mma", "tcgen05"])
 def small_k_path(request, monkeypatch):
-    """K <= 32 shapes run on both fused kernels: the mma.sync small-K kernel
-    (default when M K <= 8192) and the tcgen05 kernel (XL_SMALL_K_MMA=0)."""
+    """K <= 32 shapes run on every fused kernel: the small-K kernel (default
+    when M K <= 8192; at K = 32, M % 128 == 0 its Gram / W on tcgen05), the
+    same with mma.sync Gram / W (XL_SMALL_K_TC=0) and the tcgen05 fused
+    kernel (XL_SMALL_K_MMA=0)."""
+    monkeypatch.delenv("XL_SMALL_K_MMA", raising=False)
+    monkeypatch.delenv("XL_SMALL_K_TC", raising=False)
     if request.param == "tcgen05":
         monkeypatch.setenv("XL_SMALL_K_MMA", "0")
-    else:
-        monkeypatch.delenv("XL_SMALL_K_MMA", raising=False)
+    elif request.param == "small-k-mma":
+        monkeypatch.setenv("XL_SMALL_K_TC", "0")
     return request.param
 
 
-@pytest.mark.parametrize("S,K", [(16, 64), (4, 32), (4, 16), (2, 64), (1, 16), (64, 64), (48, 32), (8, 16)])
+def _expected_path(param, M, K):
+    if K > 32 or M * K > 8192 or param == "tcgen05":
+        return "tcgen05"
+    if param == "small-k" and K == 32 and M % 128 == 0:
+        return "tcgen05+mma.sync"
+    return "mma.sync"
+
+
+@pytest.mark.parametrize("S,K", [(16, 64), (4, 32), (4, 16), (2, 64), (1, 16), (64, 64), (48, 32), (8, 16),
+                                 (2, 32), (3, 32)])
 def test_fused_shapes_vs_oracle(S, K, small_k_path):
-    want = small_k_path if (K <= 32 and 64 * S * K <= 8192) else "tcgen05"
-    assert BT.tensor_core_path(torch.complex64, "jacpcg", 64 * S, K) == want
+    assert BT.tensor_core_path(torch.complex64, "jacpcg", 64 * S, K) == _expected_path(small_k_path, 64 * S, K)
     m = X.ChannelModel(S=S, K=K, p=0.6, r=0.7)
     H = X.generate_channels(m, seed=21, first=5, B=5, dtype=torch.complex64)
     alpha, power = K / 10.0, 10.0
