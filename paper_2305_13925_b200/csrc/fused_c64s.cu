@@ -304,14 +304,15 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
     }
     t::mbar_wait(mbar, 0);
     t::tc_after();
-    if (warp < 2) {  // TMEM lanes 0-63 = U rows (component c1)
-      float d[64], e2[64];
-      t::tmem_ld<64>(tmem + ((32u * warp) << 16), d);
-      t::tmem_ld<64>(tmem + ((32u * warp) << 16) + 64, e2);
+    if ((warp & 3) < 2) {  // TMEM lanes 0-63 = U rows (component c1); warps 0, 1 | 4, 5: column halves
+      const int c0 = 32 * (warp >> 2);
+      float d[32], e2[32];
+      t::tmem_ld<32>(tmem + ((32u * (warp & 3)) << 16) + c0, d);
+      t::tmem_ld<32>(tmem + ((32u * (warp & 3)) << 16) + 64 + c0, e2);
       t::tmem_wait_ld();
-      float* ur = Us + (32 * warp + lane) * US;
+      float* ur = Us + (32 * (warp & 3) + lane) * US + c0;
 #pragma unroll
-      for (int c = 0; c < 64; c += 2)
+      for (int c = 0; c < 32; c += 2)
         *reinterpret_cast<float2*>(ur + c) = make_float2(fmaf(2.f, e2[c], d[c]), fmaf(2.f, e2[c + 1], d[c + 1]));
     }
   } else if (warp < g::GWARPS) {
