@@ -129,6 +129,21 @@ int xl_rzf(int dtype, int method, int variant, const void* H, int64_t B,
            int32_t* status, void* workspace, size_t ws_bytes,
            xl_stream_t stream);
 
+/* xl_rzf with the solver telemetry of SolverOutcome (linsolve.py:60-68):
+ *   iterations [B] (T for Jac-PCG / CG in fixed-T mode, 0 for XL_DIRECT);
+ *   trace [B][T+1] or NULL: the squared relative least-squares error
+ *   ||A x_t - I||_F^2 / ||I||_F^2 after t = 0..T iterations (_ls_error,
+ *   linsolve.py:89-91; XL_DIRECT: one entry).
+ * The trace_opt / iterations outputs of SURVEY.md section 8(b)'s xl_rzf; runs
+ * on the general kernels (the SIMT solver records the trace) with the
+ * workspace of xl_rzf_general_workspace_bytes.  Same status codes as xl_rzf. */
+int xl_rzf_traced(int dtype, int method, int variant, const void* H, int64_t B,
+                  int32_t M, int32_t K, double xi, const double* xi_per_batch,
+                  double power, int32_t T, double sigma2, void* W, void* F,
+                  double* beta, double* gamma, double* sum_se, void* X,
+                  int32_t* iterations, double* trace, int32_t* status,
+                  void* workspace, size_t ws_bytes, xl_stream_t stream);
+
 /* Second half of the hot path for a given solution X ~= A^{-1} (e.g. from
  * xl_solve with an eps stop): F = H X, beta = sqrt(power/||F||_F^2),
  * W = beta F, SINR/SE.  precoder.py:88-91 + 64-70, metrics.py:47-58. */

@@ -69,6 +69,8 @@ _SIGNATURES = {
     "xl_rzf_general_workspace_bytes": (_sz, [_int, _int, _i64, _i32, _i32]),
     "xl_rzf_general": (_int, [_int, _int, _int, _p, _i64, _i32, _i32, _f64, _p, _f64, _i32,
                               _f64, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
+    "xl_rzf_traced": (_int, [_int, _int, _int, _p, _i64, _i32, _i32, _f64, _p, _f64, _i32,
+                             _f64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "xl_debug_set_gram_out": (None, [_p]),
     "xl_debug_lk_trace": (None, [_p]),
     "xl_apply_precoder_workspace_bytes": (_sz, [_int, _i64, _i32, _i32]),

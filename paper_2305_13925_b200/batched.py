@@ -96,6 +96,8 @@ class PrecoderBatch:
     gamma: torch.Tensor | None = None   # [B, K] float64
     F: torch.Tensor | None = None       # [B, M, K]
     X: torch.Tensor | None = None       # [B, K, K]
+    iterations: torch.Tensor | None = None  # [B] int32 (want_trace)
+    trace: torch.Tensor | None = None       # [B, T + 1] float64 (want_trace): _ls_error per iteration
 
 
 def alloc_outputs(H: torch.Tensor, want_gamma=True, want_F=False, want_X=False):
@@ -133,7 +135,8 @@ def tensor_core_path(dtype, method, M, K) -> str:
 def rzf_batched(H: torch.Tensor, xi, power: float, method: str = "jacpcg", T: int = 4,
                 variant: str = "textbook", sigma2: float = 1.0, *, want_gamma=True,
                 want_F=False, want_X=False, out: PrecoderBatch | None = None,
-                check: bool = True, stream=None, general: bool = False) -> PrecoderBatch:
+                check: bool = True, stream=None, general: bool = False,
+                want_trace: bool = False) -> PrecoderBatch:
     """Batched RZF precoder + SINR/SE (the hot path, one fused launch when the
     tcgen05 kernel covers the shape).
 
@@ -143,6 +146,9 @@ def rzf_batched(H: torch.Tensor, xi, power: float, method: str = "jacpcg", T: in
     realizations the fused kernel flagged XL_STATUS_RANGE on the general GPU
     kernels, and raises the reference exception of the first failing
     realization.  ``general=True`` forces the general (SIMT) kernels.
+    ``want_trace=True`` also returns the solver telemetry of the reference's
+    SolverOutcome (``iterations``, ``trace`` = residual_trace,
+    linsolve.py:60-68, 89-91) through ``xl_rzf_traced`` (general kernels).
     """
     lib = L.lib()
     if method not in METHODS:
@@ -157,6 +163,26 @@ def rzf_batched(H: torch.Tensor, xi, power: float, method: str = "jacpcg", T: in
         out = alloc_outputs(H, want_gamma, want_F, want_X)
     else:
         _check_out(out, H)
+    if want_trace:
+        nt = 1 if method == "direct" else int(T) + 1
+        if out.iterations is None:
+            out.iterations = torch.empty(B, dtype=torch.int32, device=H.device)
+        if out.trace is None:
+            out.trace = torch.empty(B, nt, dtype=torch.float64, device=H.device)
+        if tuple(out.trace.shape) != (B, nt) or out.trace.dtype != torch.float64 or \
+                tuple(out.iterations.shape) != (B,) or out.iterations.dtype != torch.int32:
+            raise ConfigurationError(f"out.trace must be float64 [{B}, {nt}], out.iterations int32 [{B}]")
+        nbytes = int(lib.xl_rzf_general_workspace_bytes(dc, METHODS[method], B, M, K))
+        ws = _WS.get(H.device, nbytes, stream)
+        rc = lib.xl_rzf_traced(dc, METHODS[method], VARIANTS[variant], L.ptr(H), B, M, K, xs,
+                               L.ptr(xt), float(power), int(T), float(sigma2), L.ptr(out.W),
+                               L.ptr(out.F), L.ptr(out.beta), L.ptr(out.gamma), L.ptr(out.sum_se),
+                               L.ptr(out.X), L.ptr(out.iterations), L.ptr(out.trace), L.ptr(out.status),
+                               L.ptr(ws), ws.numel(), L.stream_ptr(stream))
+        L.check(rc, "xl_rzf_traced")
+        if check:
+            L.raise_status(out.status.cpu().numpy(), "rzf_batched")
+        return out
     if general:
         nbytes = int(lib.xl_rzf_general_workspace_bytes(dc, METHODS[method], B, M, K))
         fn = lib.xl_rzf_general

@@ -199,7 +199,10 @@ void xl_debug_lk_trace(void* buf) { lk_debug_trace(buf); }
 static int general_path(int dtype, int method, int variant, const void* H, int64_t B, int32_t M, int32_t K,
                          double xi, const double* xi_per_batch, double power, int32_t T, double sigma2, void* W,
                          void* F, double* beta, double* gamma, double* sum_se, void* X, int32_t* status,
-                         void* workspace, cudaStream_t st) {
+                         void* workspace, cudaStream_t st, double* trace = nullptr,
+                         int32_t* iterations = nullptr) {
+  // solver telemetry (xl_rzf_traced) comes from the SIMT solver, which records it
+  const bool telemetry = trace != nullptr || iterations != nullptr;
   const bool lkp = lk_supported(dtype, M, K);
   const bool tc = !lkp && tc_general_supported(dtype, M, K);
   const size_t cs = csize(dtype), kk = (size_t)B * K * K * cs;
@@ -255,10 +258,10 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   };
   // K = 128 (complex64): the fused 2-CTA-cluster solver keeps the PCG state on
   // chip and also returns GX and the ||F||^2 partials (cluster_pcg.cu)
-  const bool lks = lkp && method != XL_DIRECT;
-  const bool cpc = tc && dtype == XL_C64 && method != XL_DIRECT && cpcg_supported(K);
-  const bool tcp = tc && dtype == XL_C64 && method != XL_DIRECT && !cpc && tc_pcg_supported(K);
-  const bool tcp64 = tc && dtype == XL_C128 && method != XL_DIRECT && tc_pcg64_supported(K);
+  const bool lks = !telemetry && lkp && method != XL_DIRECT;
+  const bool cpc = !telemetry && tc && dtype == XL_C64 && method != XL_DIRECT && cpcg_supported(K);
+  const bool tcp = !telemetry && tc && dtype == XL_C64 && method != XL_DIRECT && !cpc && tc_pcg_supported(K);
+  const bool tcp64 = !telemetry && tc && dtype == XL_C128 && method != XL_DIRECT && tc_pcg64_supported(K);
   const int64_t sH = (int64_t)M * K, sK = (int64_t)K * K;
   const int np = gemm_tiles(K, K);
   void* GX = sw;  // the solver workspace is free again (>= B K K)
@@ -271,7 +274,8 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   } else if (tcp64) {
     if ((e = tc_pcg64(method, variant, A, B, K, T, Xo, status, tcws, pcgws, st))) return e;
   } else if ((e = xl_solve(dtype, method, variant, A, B, K, nullptr, K, nullptr, nullptr, method == XL_CG,
-                           T, -1.0, Xo, iters, nullptr, nullptr, status, sw, sws, stream))) {
+                           T, -1.0, Xo, iterations ? iterations : iters, trace, nullptr, status, sw, sws,
+                           stream))) {
     return e;
   }
   // Coupling and ||F||^2 from the K x K side: GX = (A - xi I) X,
@@ -361,6 +365,26 @@ int xl_rzf(int dtype, int method, int variant, const void* H, int64_t B, int32_t
            void* X, int32_t* status, void* workspace, size_t ws_bytes, xl_stream_t stream) {
   return rzf_impl(true, dtype, method, variant, H, B, M, K, xi, xi_per_batch, power, T, sigma2,
                   W, F, beta, gamma, sum_se, X, status, workspace, ws_bytes, stream);
+}
+
+int xl_rzf_traced(int dtype, int method, int variant, const void* H, int64_t B, int32_t M, int32_t K,
+                  double xi, const double* xi_per_batch, double power, int32_t T, double sigma2, void* W,
+                  void* F, double* beta, double* gamma, double* sum_se, void* X, int32_t* iterations,
+                  double* trace, int32_t* status, void* workspace, size_t ws_bytes, xl_stream_t stream) {
+  if (int e = check_dtype(dtype)) return e;
+  if (method != XL_JACPCG && method != XL_CG && method != XL_DIRECT) { set_error("unknown method %d", method); return XL_ERR_CONFIG; }
+  if (variant != XL_TEXTBOOK && variant != XL_ALGORITHM) { set_error("unknown PCG variant %d", variant); return XL_ERR_CONFIG; }
+  if (method != XL_DIRECT && T < 1) { set_error("iteration count T must be >= 1, got %d", T); return XL_ERR_CONFIG; }
+  if (!xi_per_batch && !(xi > 0)) { set_error("regularization xi must be positive, got %g", xi); return XL_ERR_CONFIG; }
+  if (!(sigma2 > 0)) { set_error("noise power must be positive, got %g", sigma2); return XL_ERR_CONFIG; }
+  if (M < 1 || K < 1 || B < 0) { set_error("bad sizes"); return XL_ERR_CONFIG; }
+  if (!iterations) { set_error("rzf_traced: iterations is required"); return XL_ERR_CONFIG; }
+  if (B == 0) return XL_SUCCESS;
+  if (ws_bytes < general_ws(dtype, B, M, K)) { set_error("rzf_traced: workspace too small"); return XL_ERR_WORKSPACE; }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(status, 0, (size_t)B * sizeof(int32_t), st) != cudaSuccess) return check_launch("memset");
+  return general_path(dtype, method, variant, H, B, M, K, xi, xi_per_batch, power, T, sigma2, W, F, beta, gamma,
+                      sum_se, X, status, workspace, st, trace, iterations);
 }
 
 int xl_rzf_general(int dtype, int method, int variant, const void* H, int64_t B, int32_t M,

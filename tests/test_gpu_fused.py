@@ -274,3 +274,31 @@ def test_out_buffers_and_xi_are_checked():
     H[1, 192:] *= 1e4
     out = BT.rzf_batched(H, torch.tensor([1.6, 1.7, 1.8, 1.9], dtype=torch.float64), 10.0, T=4)
     assert out.status.cpu().tolist() == [0, 0, 0, 0]
+
+
+@pytest.mark.parametrize("method", ["jacpcg", "cg", "direct"])
+def test_rzf_traced_telemetry_vs_oracle(method):
+    """xl_rzf_traced: W / SE as xl_rzf plus SolverOutcome's iterations and
+    residual_trace (linsolve.py:60-68, _ls_error :89-91) against the oracle."""
+    m = X.ChannelModel(S=4, K=32, p=0.5, r=0.5)
+    H = X.generate_channels(m, seed=12, first=0, B=3, dtype=torch.complex64)
+    alpha, power, T = 3.2, 10.0, 4
+    out = BT.rzf_batched(H, alpha, power, method=method, T=T, want_trace=True)
+    ref = BT.rzf_batched(H, alpha, power, method=method, T=T)
+    if method != "cg":  # unpreconditioned CG: two fp32-level executions differ more (see _check)
+        assert relf(out.W.cpu().numpy(), ref.W.cpu().numpy()) < 1e-5
+    Hn = H.cpu().numpy().astype(np.complex128)
+    its, tr = out.iterations.cpu().numpy(), out.trace.cpu().numpy()
+    assert tr.shape == (3, 1 if method == "direct" else T + 1)
+    for b in range(3):
+        P = O.gram_regularized(Hn[b], alpha)
+        I = np.eye(P.shape[0], dtype=complex)
+        if method == "direct":
+            o = O.direct_solve(P, I)
+        elif method == "cg":
+            o = O.cg_solve(P, I, T)
+        else:
+            o = O.jacpcg_solve(P, I, T, variant="textbook")
+        assert its[b] == o.iterations
+        np.testing.assert_allclose(tr[b], o.residual_trace, rtol=2e-3, atol=1e-10)
+    _check(H, out, alpha, power, method, T, "textbook")
