@@ -100,6 +100,29 @@ def test_fused_methods(method, variant, T, small_k_path):
     _check(H, out, 3.2, 10.0, method, T, variant)
 
 
+@pytest.mark.parametrize("S,K", [(1, 16), (2, 32), (3, 32), (4, 16)])
+@pytest.mark.parametrize("xi_per_b", [False, True])
+def test_small_k_direct_vs_oracle(S, K, xi_per_b, monkeypatch):
+    """Direct RZF (precoder.py:73-78) in the small-K kernel: Gauss-Jordan on the
+    warp-pair layout, against the oracle's Cholesky solve; scalar and
+    per-realization xi; tcgen05 (M % 128 == 0) and mma.sync Gram / W."""
+    monkeypatch.delenv("XL_SMALL_K_MMA", raising=False)
+    m = X.ChannelModel(S=S, K=K, p=0.6, r=0.5)
+    H = X.generate_channels(m, seed=17, first=3, B=4, dtype=torch.complex64)
+    assert BT.tensor_core_path(torch.complex64, "direct", 64 * S, K) in ("mma.sync", "tcgen05+mma.sync")
+    if xi_per_b:
+        xi = torch.tensor([K / 10.0, K / 1.0, K / 100.0, K / 3.0], dtype=torch.float64, device="cuda")
+        out = BT.rzf_batched(H, xi, 10.0, method="direct")
+        Hn = H.cpu().numpy().astype(np.complex128)
+        for b in range(4):
+            G, _, _, s = O.precoder_and_se(Hn[b], float(xi[b]), 10.0, 1.0, "direct", 1, "textbook")
+            assert relf(out.W[b].cpu().numpy(), G) <= W_TOL
+            assert abs(out.sum_se[b].item() - s) <= SE_TOL * abs(s)
+    else:
+        out = BT.rzf_batched(H, K / 10.0, 10.0, method="direct")
+        _check(H, out, K / 10.0, 10.0, "direct", 1, "textbook")
+
+
 def test_fused_snr_sweep_per_realization_xi():
     """configs[1]-style SNR sweep in one batch via per-realization xi."""
     m = X.ChannelModel(S=4, K=32, p=0.5, r=0.5)
