@@ -235,6 +235,21 @@ def test_fused_determinism_and_batch_independence():
     assert torch.equal(sub.W, a.W[37:41]) and torch.equal(sub.sum_se, a.sum_se[37:41])
 
 
+@pytest.mark.parametrize("method", ["jacpcg", "cg", "direct"])
+def test_small_k_determinism_and_batch_independence(method, small_k_path):
+    """The small-K kernel (warp-pair named barriers, tcgen05 mbarrier, TMEM) and
+    its variants: bit-identical re-runs and sub-batches (a race in an exchange
+    slot or a TMEM / smem reuse would show up here; compute-sanitizer is closed
+    on this pool, profiles/r02_sanitizer.md)."""
+    wl = X.CONFIGS["cfg2"]
+    H = X.generate_channels(wl.model, seed=4, first=0, B=600, dtype=torch.complex64)
+    a = BT.rzf_batched(H, wl.alpha(), wl.power(), method=method, T=wl.T)
+    b = BT.rzf_batched(H, wl.alpha(), wl.power(), method=method, T=wl.T)
+    assert torch.equal(a.W, b.W) and torch.equal(a.sum_se, b.sum_se) and torch.equal(a.gamma, b.gamma)
+    sub = BT.rzf_batched(H[297:301].contiguous(), wl.alpha(), wl.power(), method=method, T=wl.T)
+    assert torch.equal(sub.W, a.W[297:301]) and torch.equal(sub.sum_se, a.sum_se[297:301])
+
+
 def test_concurrent_streams_use_separate_workspaces():
     """Two batches precoded concurrently on two streams (the per-stream
     workspace cache): results identical to the serial runs."""
