@@ -39,11 +39,13 @@
 // fp16 split then keeps ~22 bits for every column regardless of the gain
 // spread between users.  The Gram is unscaled exactly (A_ij = G'_ij / s_i s_j),
 // and W uses Xe' = S^-1 X T with a per-output-column power of two t_j.
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "xl_common.cuh"
 
@@ -175,7 +177,7 @@ __device__ __forceinline__ double seg_sum(double v) {  // sum over aligned SEG-l
 // core-matrix layout, the W epilogue from TMEM (thread = antenna row).
 // Otherwise both run on mma.sync from XOR-swizzled tiles.
 template <int K, bool TC>
-__global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
+__global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p, const __grid_constant__ CUtensorMap wmap) {
   using g = G<K>;
   constexpr int NC = g::NC, RC = g::RC, US = g::US;
   static_assert(!TC || K == 32, "tcgen05 variant: K = 32");
@@ -815,39 +817,47 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
     t::mbar_wait(mbar, 1);
     t::tc_after();
     STAMP(7);
-    // TMEM -> registers in the mma.sync accumulator layout (tcgen05.ld 16x256b: thread
-    // t holds rows t/4, t/4 + 8 of a 16-lane slab, columns 2 (t%4) + {0, 1} of every
-    // 8-column group) -> beta / t_j -> 8-B streaming stores, 32 B contiguous per row
+    // TMEM -> registers (tcgen05.ld 32x32b: thread = antenna row, 64 columns) ->
+    // beta / t_j -> SWIZZLE_128B staging in the (now free) Z region: box (tile mt,
+    // column half hf) = 128 rows x 128 B, 16-B chunk c of row r at c ^ (r & 7)
+    // (conflict-free with a static chunk order) -> 2-D TMA tensor stores, which
+    // un-swizzle into the row-major W.  (Fragment stores from registers held the
+    // CTA ~3.6 k cycles at the per-SM store rate; the TMA store drains on its own.)
     const float bt = (float)btd;
-    float2* Wb = p.W + b * (int64_t)M * K;
     float2* Fb = p.F ? p.F + b * (int64_t)M * K : nullptr;
-    const int gr = lane >> 2, t4 = lane & 3;
-    float ws[8], its8[8];
+    for (int mt = warp >> 2; mt < M / 128; mt += 2) {
+      const int r = 32 * (warp & 3) + lane, a = 128 * mt + r;
+      float d[64];
+      t::tmem_ld<64>(tmem + 128 + 64 * mt + ((32u * (warp & 3)) << 16), d);
+      t::tmem_wait_ld();
 #pragma unroll
-    for (int n = 0; n < 8; ++n) {
-      its8[n] = tcs[4 * n + t4];
-      ws[n] = bt * its8[n];
-    }
-    for (int mt = warp >> 2; mt < M / 128; mt += 2)
+      for (int hf = 0; hf < 2; ++hf) {
+        uint8_t* box = smem + (size_t)(2 * mt + hf) * 16384 + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int a = 128 * mt + 32 * (warp & 3) + 16 * h + gr;
-        float d[32];
-        tmem_ld_16x256b_x8(tmem + 128 + 64 * mt + ((32u * (warp & 3) + 16u * h) << 16), d);
-        t::tmem_wait_ld();
-#pragma unroll
-        for (int n = 0; n < 8; ++n) {
-          const int j = 4 * n + t4;
-          __stcs(Wb + (int64_t)a * K + j, make_float2(d[4 * n] * ws[n], d[4 * n + 1] * ws[n]));
-          __stcs(Wb + (int64_t)(a + 8) * K + j, make_float2(d[4 * n + 2] * ws[n], d[4 * n + 3] * ws[n]));
-          if (Fb) {
-            __stcs(Fb + (int64_t)a * K + j, make_float2(d[4 * n] * its8[n], d[4 * n + 1] * its8[n]));
-            __stcs(Fb + (int64_t)(a + 8) * K + j, make_float2(d[4 * n + 2] * its8[n], d[4 * n + 3] * its8[n]));
-          }
+        for (int c = 0; c < 8; ++c) {  // users 16 hf + 2 c, +1
+          const int j0 = 16 * hf + 2 * c;
+          const float f0 = tcs[j0], f1 = tcs[j0 + 1], w0 = bt * f0, w1 = bt * f1;
+          const float* v = d + 32 * hf + 4 * c;
+          *reinterpret_cast<float4*>(box + ((c ^ (r & 7)) << 4)) =
+              make_float4(v[0] * w0, v[1] * w0, v[2] * w1, v[3] * w1);
+          if (Fb)
+            __stcs(reinterpret_cast<float4*>(Fb + (int64_t)a * K + j0),
+                   make_float4(v[0] * f0, v[1] * f0, v[2] * f1, v[3] * f1));
         }
       }
+    }
     t::tc_before();
-    __syncthreads();  // every TMEM read done
+    t::fence_async_smem();
+    __syncthreads();  // every TMEM read done; the staged W visible to the TMA unit
+    if (tid == 0) {
+      const int y0 = (int)(b * M);
+      for (int bx = 0; bx < 2 * (M / 128); ++bx)
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                         reinterpret_cast<uint64_t>(&wmap)),
+                     "r"(32 * (bx & 1)), "r"(y0 + 128 * (bx >> 1)), "r"(smem_u32(smem + (size_t)bx * 16384))
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
     if (warp == 0) {
       t::tc_after();
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
@@ -935,6 +945,8 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p) {
     else if (flags[0] & 1) st = XL_STATUS_NOT_HPD;
     else if (degenerate) st = XL_STATUS_DEGENERATE;
     p.status[b] = st;
+    // the W tensor stores read shared memory: it must outlive them
+    if constexpr (TC) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
 }
 
@@ -946,6 +958,10 @@ size_t smem_bytes(int M) {
 }
 
 }  // namespace fs
+
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 // the K = 32 variant with tcgen05 Gram / W (XL_SMALL_K_TC=0 keeps mma.sync)
 bool fc64s_uses_tcgen05(int M, int K) {
@@ -980,14 +996,37 @@ int fc64s_rzf(int method, int variant, const void* H, int64_t B, int M, int K, d
     cudaMemsetAsync(trace, 0, 64 * 64 * sizeof(long long), st);
     p.trace = trace;
   }
+  CUtensorMap wmap;
+  memset(&wmap, 0, sizeof(wmap));
   auto launch = [&](auto kern, size_t sm) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fs::NT, sm);
     p.pf = (per_sm > 0 ? per_sm : 1) * nsm;
-    kern<<<(unsigned)B, fs::NT, sm, st>>>(p);
+    kern<<<(unsigned)B, fs::NT, sm, st>>>(p, wmap);
   };
   const bool tc = fc64s_uses_tcgen05(M, K);
+  if (tc) {  // W [B M rows][2K floats] for the epilogue's 2-D tensor stores: boxes of 128 rows x 32 floats
+    static EncodeTiled enc = nullptr;
+    if (!enc) {
+      void* fp = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        enc = (EncodeTiled)fp;
+    }
+    if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return XL_ERR_CUDA; }
+    const cuuint64_t dims[2] = {(cuuint64_t)(2 * K), (cuuint64_t)(B * M)};
+    const cuuint64_t strides[1] = {(cuuint64_t)(2 * K) * 4};
+    const cuuint32_t box[2] = {32, 128};
+    const cuuint32_t es[2] = {1, 1};
+    if (enc(&wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, W, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      set_error("W tensor map encode failed");
+      return XL_ERR_CUDA;
+    }
+  }
   if (K == 16) launch(fs::small_k_kernel<16, false>, fs::smem_bytes<16>(M));
   else if (tc) launch(fs::small_k_kernel<32, true>, fs::smem_bytes<32>(M));
   else launch(fs::small_k_kernel<32, false>, fs::smem_bytes<32>(M));
