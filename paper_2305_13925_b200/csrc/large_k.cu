@@ -894,7 +894,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
     stamp();
     if (warp == 1) {  // the producer warp of the product phases
       n_issued = 0;
-      n_total = p.T * NCH;  // T products (GX comes from the residual)
+      n_total = (p.T - 1) * NCH;  // T - 1 products (the first is a column scaling, GX comes from the residual)
       for (int i = 0; i < NS; ++i) issue_next();
     }
 
@@ -1031,11 +1031,44 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       tc_after();
     };
 
+    // Q = A P0 for the diagonal P0 (x0 = 0, b = I): column j of A times p_jj,
+    // read from A in global memory (every other term of the product is an
+    // exact zero) and stored in TMEM in the product's scaled units
+    // (the CTA's 256 x 32 slab of A is read coalesced into the idle B-tile
+    // region -- row stride 33 complex -- then each thread takes its row)
+    auto first_q = [&]() {
+      constexpr int SS = JN + 1;
+      float2* slab = reinterpret_cast<float2*>(pb);
+      const float4* a4 = reinterpret_cast<const float4*>(a + JN * (int)rank);
+      for (int f = tid; f < KU * (JN / 2); f += NT) {  // float4 f: row f / 16, columns 2 (f % 16), +1
+        const int row = f / (JN / 2), c2 = f % (JN / 2);
+        const float4 v = __ldg(a4 + (int64_t)row * (KU / 2) + c2);
+        slab[row * SS + 2 * c2] = make_float2(v.x, v.y);
+        slab[row * SS + 2 * c2 + 1] = make_float2(v.z, v.w);
+      }
+      named_sync(BAR_MATH, NT);
+#pragma unroll
+      for (int c0 = 0; c0 < JN; c0 += 8) {
+        float sx[8], q8[8];
+        lds8(sm->spx + c0, sx);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int jg = JN * (int)rank + c0 + i;
+          const float2 av = slab[u * SS + c0 + i];
+          const float p0 = use_c ? 1.0f / (sm->cdg[jg] * sa) : 1.0f;
+          q8[i] = ((sa * (part ? av.y : av.x)) * p0) * sx[i];
+        }
+        tmem_st8(tQ + c0, q8);
+      }
+      tmem_wait_st();
+      named_sync(BAR_MATH, NT);  // the slab region is the next product's B tile
+    };
     for (int t = 1; t <= p.T; ++t) {
       stamp();
       scale(P);
       stamp();
-      product(P);
+      if (t == 1) first_q();
+      else product(P);
       stamp();
       const float qs = (use_c && !textbook) ? icr : 1.0f;  // Algorithm 1: z = C^-1 P m
       tmem_ld<JN>(tQ, A);
