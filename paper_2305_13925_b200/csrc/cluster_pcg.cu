@@ -349,9 +349,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) cluster_pcg_k
     tc_after();
   };
 
+  // Q = A'' P0 for the diagonal P0 (x0 = 0, b = I): column j of A'' times p_jj
+  // (every other term of the product is an exact zero), from this thread's row
+  // of A in global memory, into the TMEM accumulator in the product's units
+  auto first_q = [&]() {
+    const float4* arow = reinterpret_cast<const float4*>(a + (int64_t)kr * KU + h * JH);
+#pragma unroll
+    for (int c0 = 0; c0 < JH; c0 += 8) {
+      float sx[8], q8[8];
+      lds8(sm->spx + h * JH + c0, sx);
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        const float4 v = __ldg(arow + (c0 + i) / 2);  // columns c0 + i, c0 + i + 1
+        const int jc = h * JH + c0 + i;
+        const float p0a = use_c ? 1.0f / (sm->cdg[jc] * sa) : 1.0f, p0b = use_c ? 1.0f / (sm->cdg[jc + 1] * sa) : 1.0f;
+        q8[i] = ((sa * (odd ? v.y : v.x)) * p0a) * sx[i];
+        q8[i + 1] = ((sa * (odd ? v.w : v.z)) * p0b) * sx[i + 1];
+      }
+      tmem_st8(tQ + c0, q8);
+    }
+    tmem_wait_st();
+  };
+
   for (int t = 1; t <= p.T; ++t) {
     pair_scale(P);
-    product(P);
+    if (t == 1) first_q();
+    else product(P);
     const float qs = (use_c && !textbook) ? icr : 1.0f;  // Algorithm 1: z = C^-1 P m
     tmem_ld<JH>(tQ, A);
     tmem_wait_ld();
