@@ -8,31 +8,32 @@
 //   W = beta H X, F = H X   precoder.py:90
 //   B = beta GX, SINR, SE   coupling + sinr_eq9 (metrics.py:35-58)
 //
-// Why not tcgen05 here.  At K <= 32 the persistent tcgen05 kernel
+// Why a separate kernel.  At K <= 32 the persistent tcgen05 kernel
 // (fused_tc.cu) is bound by its math role's latency chain (one realization
 // per SM at a time, a TMEM round trip and seven barrier rounds per PCG
-// iteration).  This kernel splits the work by the unit
-// that suits it:
+// iteration).  Here two realizations share an SM and the
+// work is split by the unit that suits it:
 //
-//   * Gram and W (the M x 2K x 2K products, ~90% of the flops) on the warp-
-//     level tensor cores (mma.sync m16n8k16, fp16 inputs, fp32 accumulate),
-//     3xFP16 split like fused_tc.cu: x = hi + lo, hi = fp16(x),
-//     lo = fp16(x - hi); W = Zh Xh + Zh Xl + Zl Xh, and the Gram as
-//     U = Zh^T Zh + 2 Zh^T Zl, G = (U + U^T) / 2 (symmetric by construction).
-//     Operands come from swizzled smem tiles through ldmatrix, with no TMEM
-//     round trip, so two CTAs per SM overlap one realization's tensor work
-//     with the other's SIMT solve.
-//   * The K x K solve's products on the same tensor cores in 3xFP16 on
-//     G' = D G D and B' = D^-1 P F (D, F powers of two: D from G's diagonal,
-//     F from a per-column bound on P's largest component), A fragments held
-//     in registers for the whole solve; the vector recurrences in fp32 SIMT.
+//   * Gram and W (the M x 2K x 2K products, ~90% of the flops), 3xFP16 like
+//     fused_tc.cu: x = hi + lo, hi = fp16(x), lo = fp16(x - hi);
+//     W = Zh Xh + Zh Xl + Zl Xh, and the Gram as U = Zh^T Zh + 2 Zh^T Zl,
+//     G = (U + U^T) / 2 (Hermitian by construction).  TC (K = 32, M % 128
+//     == 0): tcgen05 with TMEM accumulators -- the XOR-swizzled tiles are the
+//     SWIZZLE_128B canonical layout -- and W leaving through SWIZZLE_128B
+//     staging + 2-D TMA tensor stores; otherwise mma.sync m16n8k16 from the
+//     same tiles through ldmatrix.
+//   * The K x K solve's products on mma.sync in 3xFP16 on G' = D G D and
+//     B' = D^-1 P F (D, F powers of two: D from G's diagonal, F from a
+//     per-column bound on P's largest component), A fragments held in
+//     registers for the whole solve; the vector recurrences in fp32 SIMT.
 //     Column block cb (8 RHS columns; the columns are independent) is owned
 //     by K / 16 warps in the products' accumulator layout: the column
 //     reductions are warp shuffles plus one pair exchange, and the B operand
-//     is the block's own columns, so the PCG loop has no block barrier.  G is kept without xi (A p = G p + xi p), so GX = G X
-//     is an explicit product with no cancellation against xi X at low SNR;
-//     P0 is diagonal (x0 = 0, b = I), so the first product is a column
-//     scaling: T iterations cost T K x K products (GX included).
+//     is the block's own columns, so the PCG loop has no block barrier.  G is
+//     kept without xi (A p = G p + xi p), so GX = G X is an explicit product
+//     with no cancellation against xi X at low SNR; P0 is diagonal (x0 = 0,
+//     b = I), so the first product is a column scaling: T iterations cost T
+//     K x K products (GX included).
 //
 // Scaling: every user column k of Z (its re and im components) is scaled by
 // s_k = 2^e_k so that its largest |component| lies in [2^14, 2^15) -- the
