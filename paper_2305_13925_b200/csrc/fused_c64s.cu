@@ -1006,7 +1006,9 @@ int fc64s_rzf(int method, int variant, const void* H, int64_t B, int M, int K, d
     p.pf = (per_sm > 0 ? per_sm : 1) * nsm;
     kern<<<(unsigned)B, fs::NT, sm, st>>>(p, wmap);
   };
-  const bool tc = fc64s_uses_tcgen05(M, K);
+  // (the W tensor map addresses rows with 32-bit coordinates: beyond 2^31 rows the
+  // mma.sync variant runs)
+  const bool tc = fc64s_uses_tcgen05(M, K) && B * (int64_t)M <= 0x7fffffffLL;
   if (tc) {  // W [B M rows][2K floats] for the epilogue's 2-D tensor stores: boxes of 128 rows x 32 floats
     static EncodeTiled enc = nullptr;
     if (!enc) {
