@@ -700,12 +700,28 @@ constexpr int TILE = 128 * 16 * 2;       // one 128-row x 16-K fp16 K-major oper
 constexpr int HALF = 4 * TILE;           // Re A or Im A of one K-step (2 row tiles x hi, lo): 16 KiB
 constexpr int CHUNK = 2 * HALF;          // one K-step of 16 users in the scratch slot
 constexpr int NCH = KU / 16;             // K-steps per product
-constexpr int NS = 3;                    // ring stages of one K-step chunk (32 KiB: one bulk copy each)
 constexpr int NB = 3 * JN;               // B tile columns: [-Pi | Pr | Pi]
 constexpr int LBOB = NB * 16;            // MN-major B tile: 8-K-row group stride
 constexpr int PART = (KU / 8) * LBOB;    // B tile hi or lo: 48 KiB
-constexpr int OFF_B = NS * CHUNK;
-constexpr int OFF_SMALL = OFF_B + 2 * PART;
+// Two layouts (template PR):
+//  PR = false: every CTA multiplies all 256 rows of A'' by its own 32 columns
+//              (M = 128 x 2 row tiles, N = 64, cta_group::1); ring stages are
+//              whole K-step chunks (32 KiB), three of them.
+//  PR = true:  CTA pairs (2p, 2p + 1) multiply as one cta_group::2 MMA of
+//              M = 256 (CTA 2p + v supplies row tile v of A'') by N = 128 (each
+//              CTA supplies its own 64 B-tile columns): each CTA lands and reads
+//              only its row tile (16 KiB per K-step, five stages) and each
+//              operand read feeds twice the flops.  The accumulator of CTA v
+//              holds row tile v of both CTAs' columns, so the peer's half
+//              (32 KiB) is exchanged through DSMEM after each product.
+template <bool PR> struct Lay {
+  static constexpr int STAGE = PR ? HALF : CHUNK;
+  static constexpr int NS = PR ? 5 : 3;
+  static constexpr int OFF_B = NS * STAGE;
+  static constexpr int OFF_QX = OFF_B + 2 * PART;       // PR: the peer's Q columns, [8][256 slots][4] floats
+  static constexpr int OFF_SMALL = OFF_QX + (PR ? 32768 : 0);
+};
+constexpr int NSMAX = 5;
 // TMEM: per row tile m the accumulator [Re Q | Im Q] (2 x 32 columns) at
 // 64 m; R and X in the same arrangement at 128 and 256; the A tiles of the
 // current half-chunk are copied (tcgen05.cp) into one of four 32-column
@@ -714,13 +730,19 @@ constexpr uint32_t T_Q = 0, T_R = 128, T_X = 256, T_A = 384;
 // [Re Q | Im Q] = Ar [Pr | Pi] + Ai [-Pi | Pr]: two N = 64 products per split
 // part, the B operands being 64-column windows of one [-Pi | Pr | Pi] tile
 constexpr uint32_t ID = idesc(128, 2 * JN, 0, 1);
+constexpr uint32_t ID2 = idesc(256, 4 * JN, 0, 1);  // pair MMA: M = 256, N = 128
 constexpr int BAR_MATH = 1;
 constexpr size_t SLOT_BYTES = (size_t)NCH * CHUNK;  // 512 KiB of split A per cluster
-// chunk layout: [Ar: hi m0, hi m1, lo m0, lo m1 | Ai: same]
-__host__ __device__ constexpr int tile_off(int ai, int lo, int m) { return ai * HALF + (2 * lo + m) * TILE; }
+// chunk layout, PR = false: [Ar: hi m0, hi m1, lo m0, lo m1 | Ai: same];
+// PR = true: [row tile m0: Ar hi, Ar lo, Ai hi, Ai lo | m1: same] (a row tile is one copy)
+template <bool PR>
+__host__ __device__ constexpr int tile_off(int ai, int lo, int m) {
+  return PR ? m * HALF + (2 * ai + lo) * TILE : ai * HALF + (2 * lo + m) * TILE;
+}
 
 struct Small {
-  uint64_t full[NS], empty[NS], q_full;
+  uint64_t full[NSMAX], empty[NSMAX], q_full;
+  uint64_t pfull[NSMAX], bready, qx;  // PR: peer stage landed (leader), peer B tile ready (leader), peer Q in
   uint32_t tmem_slot;
   int not_hpd;
   float red[16][JN];
@@ -732,9 +754,77 @@ struct Small {
   float dmax[16];
   double dred[16];
 };
-constexpr int SMEM = OFF_SMALL + (int)sizeof(Small);
-static_assert(SMEM <= 227 * 1024, "lk pcg smem");
-static_assert(NS * CHUNK >= KU * (2 * JN + 1) * 4, "X / GX staging fits the ring");
+template <bool PR> constexpr int smem_bytes() { return Lay<PR>::OFF_SMALL + (int)sizeof(Small); }
+static_assert(smem_bytes<false>() <= 227 * 1024 && smem_bytes<true>() <= 227 * 1024, "lk pcg smem");
+static_assert(Lay<false>::NS * Lay<false>::STAGE >= KU * (2 * JN + 1) * 4 &&
+                  Lay<true>::NS * Lay<true>::STAGE >= KU * (2 * JN + 1) * 4,
+              "X / GX staging fits the ring");
+static_assert(Lay<true>::NS <= NSMAX && Lay<false>::NS <= NSMAX, "ring barriers");
+
+// ---- cta_group::2 forms (every tcgen05 op of the pair kernel uses them)
+__device__ __forceinline__ void mma2_w(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void commit2_mc_w(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
+          su32(bar)),
+      "h"(mask)
+      : "memory");
+}
+template <bool PR>
+__device__ __forceinline__ void tmem_alloc512_g(uint32_t* slot) {
+  if (PR) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  } else {
+    tmem_alloc512(slot);
+  }
+}
+template <bool PR>
+__device__ __forceinline__ void tmem_free512_g(uint32_t t) {
+  if (PR) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(t));
+  else tmem_free512(t);
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// arrive (release at cluster scope) on an mbarrier of another CTA of the cluster
+__device__ __forceinline__ void mbar_arrive_cl(uint32_t cl_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
+}
+// wait with acquire at cluster scope (the phase was completed from another CTA)
+__device__ __forceinline__ void bwait_cl(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  uint64_t t0 = 0;
+  for (uint32_t it = 0;; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(done)
+        : "r"(su32(bar)), "r"(parity), "r"(0x989680u)
+        : "memory");
+    if (done) return;
+    if ((it & 15u) == 15u) {
+      const uint64_t t = gtimer();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 4000000000ull) asm volatile("trap;");
+    }
+  }
+}
+__device__ __forceinline__ void st_async_v4(uint32_t cl_addr, const float* v, uint32_t cl_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   cl_addr),
+               "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+               "r"(__float_as_uint(v[3])), "r"(cl_bar)
+               : "memory");
+}
 
 struct Params {
   const float2* A;  // [B][K][K] regularized Gram (Hermitian, xi on the diagonal)
@@ -779,11 +869,15 @@ __device__ __forceinline__ float col_total(const Small* sm, int j) {
 // 0 = Re, 1 = Im) of its 32 columns: P in registers, Q / R / X in TMEM.
 // Q = A P as complex products of the streamed split Re A / Im A tiles:
 // Re Q = Ar Pr - Ai Pi, Im Q = Ar Pi + Ai Pr (3xFP16 each: 24 MMAs per K-step).
+template <bool PR>
 __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
+  using L = Lay<PR>;
+  constexpr int NS = L::NS;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
-  uint8_t* pb = smem + OFF_B;
-  Small* sm = reinterpret_cast<Small*>(smem + OFF_SMALL);
+  uint8_t* pb = smem + L::OFF_B;
+  float* qxb = reinterpret_cast<float*>(smem + L::OFF_QX);
+  Small* sm = reinterpret_cast<Small*>(smem + L::OFF_SMALL);
   const uint32_t rank = cluster_rank();
   const uint32_t cid = cluster_id_x(), ncl = nclusters_x();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -793,23 +887,40 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
   const bool use_c = p.method == XL_JACPCG;
   const bool textbook = use_c && p.variant == XL_TEXTBOOK;
   uint8_t* slot = p.scratch + (size_t)cid * SLOT_BYTES;
+  // PR: pair rank v (row tile of A'' this CTA supplies / its accumulator holds);
+  // a thread whose user u lies in the other row tile gets its Q from the peer
+  const uint32_t pr = rank & 1u, peer = rank ^ 1u;
+  const bool leader = pr == 0;
+  const bool remote = PR && (uint32_t)(tau & 1) != pr;
+  const int qslot = part * 128 + q * 32 + lane;  // PR: exchange slot (same in sender and receiver)
+  const uint16_t pair_mask = (uint16_t)(3u << (rank & ~1u));
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sm->full[s], 1);
-      mbar_init(&sm->empty[s], p.unicast ? 1 : C);
+      mbar_init(&sm->empty[s], PR ? C / 2 : (p.unicast ? 1 : C));
+      mbar_init(&sm->pfull[s], 1);
     }
     mbar_init(&sm->q_full, 1);
+    mbar_init(&sm->bready, 1);
+    mbar_init(&sm->qx, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) tmem_alloc512(&sm->tmem_slot);
+  if (warp == 0) tmem_alloc512_g<PR>(&sm->tmem_slot);
   tc_before();
   __syncthreads();
   tc_after();
+  if (PR) cluster_sync();  // every CTA's barriers are initialised before any remote arrive / multicast
   const uint32_t tmem = sm->tmem_slot;
   const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+  // PR: the accumulator columns of pair CTA w's B half are [64 w, 64 w + 64), so
+  // the same offset reads this thread's own Q (local) or the peer's (to send)
   const uint32_t tcol = 2 * JN * (tau & 1) + JN * (tau >> 1);
   const uint32_t tQ = tl + T_Q + tcol, tR = tl + T_R + tcol, tX = tl + T_X + tcol;
   const uint32_t upb = su32(pb);
+  const uint32_t peer_qx = PR ? mapa_u32(su32(qxb), peer) : 0u;
+  const uint32_t peer_qxbar = PR ? mapa_u32(su32(&sm->qx), peer) : 0u;
+  const uint32_t lead_pfull = PR ? mapa_u32(su32(&sm->pfull[0]), rank & ~1u) : 0u;
+  const uint32_t lead_bready = PR ? mapa_u32(su32(&sm->bready), rank & ~1u) : 0u;
   uint32_t g_prod = 0, g_cons = 0, nq = 0;  // ring chunks produced / consumed, products
   // thread 0 streams the split A: chunk n of the realization's (T + 1) x 16
   // K-steps into the ring (stage g % NS of all eight CTAs), armed in every
@@ -826,9 +937,15 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
     if (lane == 0) {
       if (g_prod >= NS) bwait<true>(&sm->empty[s], ((g_prod / NS) - 1) & 1);
       if (p.trace && cid == 0 && rank == 0 && g_prod < 64) p.trace[128 + g_prod] = clock64();
-      mbar_expect_tx(&sm->full[s], CHUNK);
-      if (p.unicast) bulk_g2s(ring + s * CHUNK, src, CHUNK, &sm->full[s], policy_evict_normal());
-      else if ((k & (C - 1)) == (int)rank) bulk_mc(ring + s * CHUNK, src, CHUNK, &sm->full[s], 0xFF);
+      mbar_expect_tx(&sm->full[s], L::STAGE);
+      if (PR) {  // row tile pr of K-step k, to the four CTAs of this pair rank, by CTA 2 (k % 4) + pr
+        if ((k & 3) == (int)(rank >> 1))
+          bulk_mc(ring + s * L::STAGE, src + pr * HALF, HALF, &sm->full[s], pr ? 0xAA : 0x55);
+      } else if (p.unicast) {
+        bulk_g2s(ring + s * CHUNK, src, CHUNK, &sm->full[s], policy_evict_normal());
+      } else if ((k & (C - 1)) == (int)rank) {
+        bulk_mc(ring + s * CHUNK, src, CHUNK, &sm->full[s], 0xFF);
+      }
     }
     __syncwarp();
     ++g_prod;
@@ -883,10 +1000,10 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       split8(vi, sa, hi_, li_);
       const int s = 2 * (int)rank + (ko >> 1), kg = ko & 1, m = i >> 7;
       uint8_t* dst = slot + (size_t)s * CHUNK + ((i & 127) >> 3) * 256 + kg * 128 + (i & 7) * 16;
-      *reinterpret_cast<uint4*>(dst + tile_off(0, 0, m)) = hr;
-      *reinterpret_cast<uint4*>(dst + tile_off(0, 1, m)) = lr;
-      *reinterpret_cast<uint4*>(dst + tile_off(1, 0, m)) = hi_;
-      *reinterpret_cast<uint4*>(dst + tile_off(1, 1, m)) = li_;
+      *reinterpret_cast<uint4*>(dst + tile_off<PR>(0, 0, m)) = hr;
+      *reinterpret_cast<uint4*>(dst + tile_off<PR>(0, 1, m)) = lr;
+      *reinterpret_cast<uint4*>(dst + tile_off<PR>(1, 0, m)) = hi_;
+      *reinterpret_cast<uint4*>(dst + tile_off<PR>(1, 1, m)) = li_;
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");
     stamp();
@@ -941,6 +1058,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
     // Q = A v (v scaled per column): B tiles (Pr, Pi; hi, lo) written by all,
     // MMAs issued by thread 0
     auto product = [&](const float (&v)[JN]) {
+      if (PR && tid == 0) mbar_expect_tx(&sm->qx, 32768);  // this product's peer Q (before our B-ready)
       // B tile columns [-Pi | Pr | Pi]: Re rows write Pr, Im rows write Pi and -Pi
 #pragma unroll
       for (int g = 0; g < JN / 8; ++g) {
@@ -966,6 +1084,63 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       fence_async_smem();
       tc_before();
       named_sync(BAR_MATH, NT);
+      if constexpr (PR) {
+        if (tid == 0 && !leader) mbar_arrive_cl(lead_bready);  // the leader's MMAs read our B half
+        if (warp == 0) {
+          tc_after();
+          if (leader) {
+            bwait_cl(&sm->bready, nq & 1);
+            tc_after();
+            for (int k = 0; k < NCH; ++k) {
+              const uint32_t gc = g_cons + k;
+              const int s = gc % NS;
+              bwait(&sm->full[s], (gc / NS) & 1);
+              bwait_cl(&sm->pfull[s], (gc / NS) & 1);
+              if (p.trace && cid == 0 && rank == 0 && lane == 0 && gc < 64) p.trace[192 + gc] = clock64();
+              tc_after();
+              const uint32_t st = su32(ring + s * L::STAGE);
+#pragma unroll
+              for (int ai = 0; ai < 2; ++ai) {
+                const uint64_t ah = sdesc(st + tile_off<true>(ai, 0, 0), 128, 256);
+                const uint64_t al = sdesc(st + tile_off<true>(ai, 1, 0), 128, 256);
+                const uint32_t bo = upb + 2 * k * LBOB + (ai ? 0 : JN / 8 * 128);  // B2 = [-Pi | Pr], B1 = [Pr | Pi]
+                const uint64_t bh = sdesc(bo, LBOB, 128), bl = sdesc(bo + PART, LBOB, 128);
+                const uint32_t acc = (k | ai) != 0;
+                for (int rep = 0; rep < p.mma_reps; ++rep) {
+                  mma2_w(tmem + T_Q, ah, bh, ID2, acc);
+                  mma2_w(tmem + T_Q, ah, bl, ID2, 1);
+                  mma2_w(tmem + T_Q, al, bh, ID2, 1);
+                }
+              }
+              commit2_mc_w(&sm->empty[s], 0xFF);
+            }
+            commit2_mc_w(&sm->q_full, pair_mask);
+          } else {  // relay each landing of our row tile to the leader
+            for (int k = 0; k < NCH; ++k) {
+              const uint32_t gc = g_cons + k;
+              const int s = gc % NS;
+              bwait(&sm->full[s], (gc / NS) & 1);
+              if (lane == 0) mbar_arrive_cl(lead_pfull + 8u * (uint32_t)s);
+              __syncwarp();
+            }
+          }
+          bwait_cl(&sm->q_full, nq & 1);
+        } else if (warp == 1) {
+          for (int k = 0; k < NCH; ++k) issue_next();
+        }
+        g_cons += NCH;
+        named_sync(BAR_MATH, NT);
+        ++nq;
+        tc_after();
+        if (remote) {  // our accumulator's rows of the peer's columns -> the peer
+          float w[JN];
+          tmem_ld<JN>(tQ, w);
+          tmem_wait_ld();
+#pragma unroll
+          for (int g = 0; g < JN / 4; ++g)
+            st_async_v4(peer_qx + 16u * (uint32_t)(g * 256 + qslot), w + 4 * g, peer_qxbar);
+        }
+      } else {
       if (warp == 0) {  // the whole warp issues (tcgen05 ops elect one lane)
         tc_after();
         for (int k = 0; k < NCH; ++k) {  // K-step k: Re A half, then Im A half
@@ -1029,6 +1204,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       named_sync(BAR_MATH, NT);  // the other warps block in hardware until the products are done
       ++nq;
       tc_after();
+      }
     };
 
     // Q = A P0 for the diagonal P0 (x0 = 0, b = I): column j of A times p_jj,
@@ -1058,7 +1234,13 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
           const float p0 = use_c ? 1.0f / (sm->cdg[jg] * sa) : 1.0f;
           q8[i] = ((sa * (part ? av.y : av.x)) * p0) * sx[i];
         }
-        tmem_st8(tQ + c0, q8);
+        if (remote) {  // PR: this thread's Q lives in the exchange buffer
+          float4* qb = reinterpret_cast<float4*>(qxb);
+          qb[(c0 / 4) * 256 + qslot] = make_float4(q8[0], q8[1], q8[2], q8[3]);
+          qb[(c0 / 4 + 1) * 256 + qslot] = make_float4(q8[4], q8[5], q8[6], q8[7]);
+        } else {
+          tmem_st8(tQ + c0, q8);
+        }
       }
       tmem_wait_st();
       named_sync(BAR_MATH, NT);  // the slab region is the next product's B tile
@@ -1071,8 +1253,18 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       else product(P);
       stamp();
       const float qs = (use_c && !textbook) ? icr : 1.0f;  // Algorithm 1: z = C^-1 P m
-      tmem_ld<JN>(tQ, A);
-      tmem_wait_ld();
+      const float4* qb = reinterpret_cast<const float4*>(qxb);
+      if (remote) {  // PR: Q of this thread's rows was computed by the peer
+        if (t > 1) bwait_cl(&sm->qx, (nq - 1) & 1);
+#pragma unroll
+        for (int g = 0; g < JN / 4; ++g) {
+          const float4 x = qb[g * 256 + qslot];
+          A[4 * g] = x.x; A[4 * g + 1] = x.y; A[4 * g + 2] = x.z; A[4 * g + 3] = x.w;
+        }
+      } else {
+        tmem_ld<JN>(tQ, A);
+        tmem_wait_ld();
+      }
       // curvature m^H z per column (linsolve.py:276)
 #pragma unroll
       for (int c0 = 0; c0 < JN; c0 += 8) {
@@ -1095,7 +1287,12 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
 #pragma unroll
       for (int c0 = 0; c0 < JN; c0 += 8) {
         float qv[8], rv[8], xv[8], al8[8], sy[8];
-        tmem_ld8(tQ + c0, qv);
+        if (remote) {
+          const float4 x = qb[(c0 / 4) * 256 + qslot], y = qb[(c0 / 4 + 1) * 256 + qslot];
+          qv[0] = x.x; qv[1] = x.y; qv[2] = x.z; qv[3] = x.w; qv[4] = y.x; qv[5] = y.y; qv[6] = y.z; qv[7] = y.w;
+        } else {
+          tmem_ld8(tQ + c0, qv);
+        }
         tmem_ld8(tR + c0, rv);
         tmem_ld8(tX + c0, xv);
         lds8(sm->coef[0] + c0, al8);
@@ -1194,7 +1391,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
   cluster_sync();  // no multicast may target an exited CTA
   if (warp == 0) {
     tc_after();
-    tmem_free512(tmem);
+    tmem_free512_g<PR>(tmem);
   }
 }
 }  // namespace pc
@@ -1239,14 +1436,22 @@ bool lk_supported(int dtype, int M, int K) {
   return !(e && e[0] == 'l');
 }
 
+// the pair-MMA solver (PR) unless XL_LK_PAIR=0 (A/B, tests)
+static bool lk_pair() {
+  const char* e = getenv("XL_LK_PAIR");
+  return !(e && e[0] == '0');
+}
+
+template <bool PR>
 static int lk_clusters() {
   static int n = 0;
   if (n == 0) {
-    cudaFuncSetAttribute(lk::pc::lk_pcg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lk::pc::SMEM);
+    auto kern = lk::pc::lk_pcg_kernel<PR>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lk::pc::smem_bytes<PR>());
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(lk::pc::C * 16, 1, 1);
     cfg.blockDim = dim3(lk::pc::NT, 1, 1);
-    cfg.dynamicSmemBytes = lk::pc::SMEM;
+    cfg.dynamicSmemBytes = lk::pc::smem_bytes<PR>();
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = lk::pc::C;
@@ -1255,7 +1460,7 @@ static int lk_clusters() {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int c = 0;
-    if (cudaOccupancyMaxActiveClusters(&c, lk::pc::lk_pcg_kernel, &cfg) != cudaSuccess || c < 1) {
+    if (cudaOccupancyMaxActiveClusters(&c, kern, &cfg) != cudaSuccess || c < 1) {
       cudaGetLastError();
       c = 16;
     }
@@ -1301,7 +1506,8 @@ int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi
   using namespace lk;
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   uint8_t* scratch = (uint8_t*)ws + 4 * al((size_t)B * 4);
-  int ncl = lk_clusters();
+  const bool pair = lk_pair();
+  int ncl = pair ? lk_clusters<true>() : lk_clusters<false>();
   if (ncl > 32) ncl = 32;
   if (ncl > B) ncl = (int)B;
   const char* uc = getenv("XL_LK_UNICAST");
@@ -1313,7 +1519,7 @@ int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(pc::C * ncl), 1, 1);
   cfg.blockDim = dim3(pc::NT, 1, 1);
-  cfg.dynamicSmemBytes = pc::SMEM;
+  cfg.dynamicSmemBytes = pair ? pc::smem_bytes<true>() : pc::smem_bytes<false>();
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1322,8 +1528,9 @@ int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaFuncSetAttribute(pc::lk_pcg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pc::SMEM);
-  if (cudaLaunchKernelEx(&cfg, pc::lk_pcg_kernel, p) != cudaSuccess) return check_launch("lk pcg launch");
+  auto kern = pair ? pc::lk_pcg_kernel<true> : pc::lk_pcg_kernel<false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
+  if (cudaLaunchKernelEx(&cfg, kern, p) != cudaSuccess) return check_launch("lk pcg launch");
   return check_launch("lk pcg");
 }
 
