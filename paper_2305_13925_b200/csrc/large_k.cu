@@ -1359,6 +1359,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
     // stride (conflict-free), then written as coalesced 256-B row segments
     constexpr int SR = 2 * JN + 1;
     float* stg = reinterpret_cast<float*>(ring);
+    stamp();
 #pragma unroll 1
     for (int pass = 0; pass < 2; ++pass) {
 #pragma unroll
@@ -1370,6 +1371,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
         out[(int64_t)row * 2 * KU + 32 + lane] = stg[row * SR + 32 + lane];
       }
       named_sync(BAR_MATH, NT);
+      if (pass == 0) stamp();
     }
     stamp();
     fro = warp_sum(fro);
