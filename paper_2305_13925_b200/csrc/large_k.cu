@@ -755,6 +755,8 @@ struct Small {
   double dred[16];
 };
 template <bool PR> constexpr int smem_bytes() { return Lay<PR>::OFF_SMALL + (int)sizeof(Small); }
+template <bool PR> constexpr int cl_size() { return PR ? 4 : C; }  // CTAs per cluster
+constexpr int MAX_SLOTS = 64;  // scratch slots (one per resident cluster)
 static_assert(smem_bytes<false>() <= 227 * 1024 && smem_bytes<true>() <= 227 * 1024, "lk pcg smem");
 static_assert(Lay<false>::NS * Lay<false>::STAGE >= KU * (2 * JN + 1) * 4 &&
                   Lay<true>::NS * Lay<true>::STAGE >= KU * (2 * JN + 1) * 4,
@@ -873,6 +875,12 @@ template <bool PR>
 __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
   using L = Lay<PR>;
   constexpr int NS = L::NS;
+  // PR: clusters of CL = 4 CTAs (two pairs) each take one half of a
+  // realization's 256 RHS columns (work item = (b, half)), so 4-CTA clusters
+  // tile more of the 148 SMs than 8-CTA ones; each builds the whole split A''.
+  constexpr int CL = PR ? 4 : C;
+  constexpr int UPC = KU / CL;  // users of the split A'' this CTA builds
+  constexpr uint16_t ALL = (uint16_t)((1u << CL) - 1u);
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
   uint8_t* pb = smem + L::OFF_B;
@@ -897,7 +905,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sm->full[s], 1);
-      mbar_init(&sm->empty[s], PR ? C / 2 : (p.unicast ? 1 : C));
+      mbar_init(&sm->empty[s], PR ? CL / 2 : (p.unicast ? 1 : C));
       mbar_init(&sm->pfull[s], 1);
     }
     mbar_init(&sm->q_full, 1);
@@ -938,9 +946,9 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       if (g_prod >= NS) bwait<true>(&sm->empty[s], ((g_prod / NS) - 1) & 1);
       if (p.trace && cid == 0 && rank == 0 && g_prod < 64) p.trace[128 + g_prod] = clock64();
       mbar_expect_tx(&sm->full[s], L::STAGE);
-      if (PR) {  // row tile pr of K-step k, to the four CTAs of this pair rank, by CTA 2 (k % 4) + pr
-        if ((k & 3) == (int)(rank >> 1))
-          bulk_mc(ring + s * L::STAGE, src + pr * HALF, HALF, &sm->full[s], pr ? 0xAA : 0x55);
+      if (PR) {  // row tile pr of K-step k, to the CTAs of this pair rank, by CTA 2 (k % (CL / 2)) + pr
+        if ((k % (CL / 2)) == (int)(rank >> 1))
+          bulk_mc(ring + s * L::STAGE, src + pr * HALF, HALF, &sm->full[s], (uint16_t)((pr ? 0xAAAA : 0x5555) & ALL));
       } else if (p.unicast) {
         bulk_g2s(ring + s * CHUNK, src, CHUNK, &sm->full[s], policy_evict_normal());
       } else if ((k & (C - 1)) == (int)rank) {
@@ -957,7 +965,10 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
   auto stamp = [&]() {
     if (tr && ntr < 128) p.trace[ntr++] = clock64();
   };
-  for (int64_t b = cid; b < p.B; b += ncl) {
+  const int64_t nitems = PR ? 2 * p.B : p.B;
+  for (int64_t item = cid; item < nitems; item += ncl) {
+    const int64_t b = PR ? item >> 1 : item;
+    const int cb = PR ? 4 * (int)(item & 1) + (int)rank : (int)rank;  // the CTA's 32-column block
     const float2* a = p.A + b * (int64_t)KU * KU;
     stamp();
     cluster_sync();  // the previous realization's chunks are consumed in every CTA
@@ -983,22 +994,22 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       zsum += sm->dmax[8 + w];
     }
     const float sa = pow2_scale(dmax, 14);
-    // ---- this CTA's two K-step chunks (users k in [32 rank, 32 rank + 32)) of
+    // ---- this CTA's K-step chunks (users k in [UPC rank, UPC rank + UPC)) of
     // the split (Re A, Im A) -> the cluster's scratch slot, K-major core
     // matrices; a_ik = conj(A[k][i]) (A Hermitian): Re = A[k][i].x, Im = -A[k][i].y
-    for (int task = tid; task < 2 * KU * 2; task += NT) {
-      const int i = task & (KU - 1), ko = task >> 8;  // row, K-octet (0..3) of the CTA's 32 users
+    for (int task = tid; task < KU * (UPC / 8); task += NT) {
+      const int i = task & (KU - 1), ko = task >> 8;  // row, K-octet of the CTA's UPC users
       float vr[8], vi[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const float2 x = __ldg(a + (int64_t)(32 * (int)rank + 8 * ko + e) * KU + i);
+        const float2 x = __ldg(a + (int64_t)(UPC * (int)rank + 8 * ko + e) * KU + i);
         vr[e] = x.x;
         vi[e] = -x.y;
       }
       uint4 hr, lr, hi_, li_;
       split8(vr, sa, hr, lr);
       split8(vi, sa, hi_, li_);
-      const int s = 2 * (int)rank + (ko >> 1), kg = ko & 1, m = i >> 7;
+      const int s = (UPC / 16) * (int)rank + (ko >> 1), kg = ko & 1, m = i >> 7;
       uint8_t* dst = slot + (size_t)s * CHUNK + ((i & 127) >> 3) * 256 + kg * 128 + (i & 7) * 16;
       *reinterpret_cast<uint4*>(dst + tile_off<PR>(0, 0, m)) = hr;
       *reinterpret_cast<uint4*>(dst + tile_off<PR>(0, 1, m)) = lr;
@@ -1026,7 +1037,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       float rv[8], zx[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const int jg = JN * (int)rank + c0 + i;
+        const int jg = JN * cb + c0 + i;
         const float e = (part == 0 && u == jg) ? 1.0f : 0.0f;
         rv[i] = (use_c && !textbook) ? e * icr : e;
         P[c0 + i] = textbook ? e * icr : rv[i];
@@ -1036,7 +1047,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       tmem_st8(tX + c0, zx);
     }
     if (tid < JN) {
-      const float c0 = use_c ? sm->cdg[JN * rank + tid] * sa : 1.0f;
+      const float c0 = use_c ? sm->cdg[JN * cb + tid] * sa : 1.0f;
       const float ic = 1.0f / c0;
       sm->rzs[tid] = textbook ? ic : (use_c ? ic * ic : 1.0f);
     }
@@ -1112,7 +1123,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
                   mma2_w(tmem + T_Q, al, bh, ID2, 1);
                 }
               }
-              commit2_mc_w(&sm->empty[s], 0xFF);
+              commit2_mc_w(&sm->empty[s], ALL);
             }
             commit2_mc_w(&sm->q_full, pair_mask);
           } else {  // relay each landing of our row tile to the leader
@@ -1215,7 +1226,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
     auto first_q = [&]() {
       constexpr int SS = JN + 1;
       float2* slab = reinterpret_cast<float2*>(pb);
-      const float4* a4 = reinterpret_cast<const float4*>(a + JN * (int)rank);
+      const float4* a4 = reinterpret_cast<const float4*>(a + JN * cb);
       for (int f = tid; f < KU * (JN / 2); f += NT) {  // float4 f: row f / 16, columns 2 (f % 16), +1
         const int row = f / (JN / 2), c2 = f % (JN / 2);
         const float4 v = __ldg(a4 + (int64_t)row * (KU / 2) + c2);
@@ -1229,7 +1240,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
         lds8(sm->spx + c0, sx);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const int jg = JN * (int)rank + c0 + i;
+          const int jg = JN * cb + c0 + i;
           const float2 av = slab[u * SS + c0 + i];
           const float p0 = use_c ? 1.0f / (sm->cdg[jg] * sa) : 1.0f;
           q8[i] = ((sa * (part ? av.y : av.x)) * p0) * sx[i];
@@ -1347,7 +1358,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
     const float crr = (use_c && !textbook) ? cr : 1.0f;
 #pragma unroll
     for (int jj = 0; jj < JN; ++jj) {
-      const int jg = JN * (int)rank + jj;
+      const int jg = JN * cb + jj;
       const float e = (part == 0 && u == jg) ? 1.0f : 0.0f;
       const float ax = e - crr * A[jj];
       const float g = (float)((double)ax - xsa * (double)P[jj]);
@@ -1365,7 +1376,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
 #pragma unroll
       for (int jj = 0; jj < JN; ++jj) stg[u * SR + 2 * jj + part] = pass == 0 ? P[jj] * sa : A[jj];
       named_sync(BAR_MATH, NT);
-      float* out = reinterpret_cast<float*>((pass == 0 ? p.X : p.GX) + b * (int64_t)KU * KU + JN * rank);
+      float* out = reinterpret_cast<float*>((pass == 0 ? p.X : p.GX) + b * (int64_t)KU * KU + JN * cb);
       for (int row = warp; row < KU; row += NT / 32) {
         out[(int64_t)row * 2 * KU + lane] = stg[row * SR + lane];
         out[(int64_t)row * 2 * KU + 32 + lane] = stg[row * SR + 32 + lane];
@@ -1381,9 +1392,9 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < 16; ++w) s += sm->dred[w];
-      p.part[C * b + rank] = s;
+      p.part[C * b + cb] = s;
       if (zsum > 0.0f) {
-        if (rank == 0) p.status[b] = XL_STATUS_SPLITTING;
+        if (cb == 0) p.status[b] = XL_STATUS_SPLITTING;
       } else if (sm->not_hpd) {
         atomicCAS(reinterpret_cast<int*>(p.status + b), 0, XL_STATUS_NOT_HPD);
       }
@@ -1451,12 +1462,12 @@ static int lk_clusters() {
     auto kern = lk::pc::lk_pcg_kernel<PR>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lk::pc::smem_bytes<PR>());
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(lk::pc::C * 16, 1, 1);
+    cfg.gridDim = dim3(lk::pc::cl_size<PR>() * 16, 1, 1);
     cfg.blockDim = dim3(lk::pc::NT, 1, 1);
     cfg.dynamicSmemBytes = lk::pc::smem_bytes<PR>();
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = lk::pc::C;
+    at[0].val.clusterDim.x = lk::pc::cl_size<PR>();
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
@@ -1475,7 +1486,7 @@ static int lk_clusters() {
 // cluster solver's A'' slots
 size_t lk_ws_bytes(int64_t B) {
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  return 4 * al((size_t)B * 4) + (size_t)32 * lk::pc::SLOT_BYTES;
+  return 4 * al((size_t)B * 4) + (size_t)lk::pc::MAX_SLOTS * lk::pc::SLOT_BYTES;
 }
 
 int lk_gram(const void* H, int64_t B, int M, double xi, const double* xi_b, void* A, void* ws, cudaStream_t st) {
@@ -1510,8 +1521,9 @@ int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi
   uint8_t* scratch = (uint8_t*)ws + 4 * al((size_t)B * 4);
   const bool pair = lk_pair();
   int ncl = pair ? lk_clusters<true>() : lk_clusters<false>();
-  if (ncl > 32) ncl = 32;
-  if (ncl > B) ncl = (int)B;
+  if (ncl > pc::MAX_SLOTS) ncl = pc::MAX_SLOTS;
+  if (ncl > (pair ? 2 * B : B)) ncl = (int)(pair ? 2 * B : B);
+  const int cl = pair ? pc::cl_size<true>() : pc::cl_size<false>();
   const char* uc = getenv("XL_LK_UNICAST");
   pc::Params p{(const float2*)A, B, T, method, variant, xi, xi_b, (float2*)X, (float2*)GX, part, status, scratch,
                g_lk_trace, (uc && uc[0] == '1') ? 1 : 0, 1, 1, 0};
@@ -1519,13 +1531,13 @@ int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi
   if (const char* ss = getenv("XL_LK_SS")) p.ss = ss[0] == '1';  // default 1: A from shared memory (measured faster than tcgen05.cp + TMEM)
   if (const char* mr = getenv("XL_LK_MMA_REPS")) p.mma_reps = atoi(mr) > 0 ? atoi(mr) : 1;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(pc::C * ncl), 1, 1);
+  cfg.gridDim = dim3((unsigned)(cl * ncl), 1, 1);
   cfg.blockDim = dim3(pc::NT, 1, 1);
   cfg.dynamicSmemBytes = pair ? pc::smem_bytes<true>() : pc::smem_bytes<false>();
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = pc::C;
+  at[0].val.clusterDim.x = cl;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
