@@ -374,9 +374,9 @@ __global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ 
       uint8_t* sg = st + soff + (hp ? 0 : (cw >> 2) * SGL) + (cw & 3) * (8 * BLK * 4);
       if (hp) gm = load8(pg, 2 * BLK * 4, lane, 8 * (cw & 1), vp);
       if (dos) gm = fmaxf(gm, load8(sg, BLK * 4, lane, 0, vs));
-      gm = warp_max(gm);
-      zm = fmaxf(zm, gm);
+      zm = fmaxf(zm, gm);  // per lane: the warp / CTA reductions happen once, after the loop
       if (!have) {  // until the first non-zero chunk: max over the converter warps
+        gm = warp_max(gm);
         if (lane == 0) sm->rmax[cw] = gm;
         named_sync(BAR_CONV, 32 * NCONV);
         float mx = sm->rmax[0];
@@ -397,6 +397,8 @@ __global__ void __launch_bounds__(NT, 1) lk_gram_kernel(const __grid_constant__ 
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm->conv[s]);
     }
+    over = __any_sync(0xffffffffu, over);
+    zm = warp_max(zm);
     if (!fixup && over && lane == 0) rflag[b] = 1;
     // the CTAs of a realization together cover every block (CTA 0: 0-1, CTA 1: 0, 2-3)
     if (lane == 0 && zm > 0.0f) atomicMax(zmax + b, __float_as_uint(zm));  // non-negative: bit order == value order
@@ -905,7 +907,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sm->full[s], 1);
-      mbar_init(&sm->empty[s], PR ? CL / 2 : (p.unicast ? 1 : C));
+      mbar_init(&sm->empty[s], PR ? (p.unicast ? 1 : CL / 2) : (p.unicast ? 1 : C));
       mbar_init(&sm->pfull[s], 1);
     }
     mbar_init(&sm->q_full, 1);
@@ -947,7 +949,9 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       if (p.trace && cid == 0 && rank == 0 && g_prod < 64) p.trace[128 + g_prod] = clock64();
       mbar_expect_tx(&sm->full[s], L::STAGE);
       if (PR) {  // row tile pr of K-step k, to the CTAs of this pair rank, by CTA 2 (k % (CL / 2)) + pr
-        if ((k % (CL / 2)) == (int)(rank >> 1))
+        if (p.unicast)  // every CTA loads its own row tile; stages freed by its pair's MMAs only
+          bulk_g2s(ring + s * L::STAGE, src + pr * HALF, HALF, &sm->full[s], policy_evict_normal());
+        else if ((k % (CL / 2)) == (int)(rank >> 1))
           bulk_mc(ring + s * L::STAGE, src + pr * HALF, HALF, &sm->full[s], (uint16_t)((pr ? 0xAAAA : 0x5555) & ALL));
       } else if (p.unicast) {
         bulk_g2s(ring + s * CHUNK, src, CHUNK, &sm->full[s], policy_evict_normal());
@@ -1123,7 +1127,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
                   mma2_w(tmem + T_Q, al, bh, ID2, 1);
                 }
               }
-              commit2_mc_w(&sm->empty[s], ALL);
+              commit2_mc_w(&sm->empty[s], p.unicast ? pair_mask : ALL);
             }
             commit2_mc_w(&sm->q_full, pair_mask);
           } else {  // relay each landing of our row tile to the leader

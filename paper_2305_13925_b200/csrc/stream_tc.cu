@@ -77,12 +77,13 @@ __device__ __forceinline__ void load_group(const uint8_t* gb, int lane, float4 (
     v[it] = *reinterpret_cast<const float4*>(gb + (row * NC + cc) * 4);
   }
 }
-__device__ __forceinline__ float group_max(const float4 (&v)[NIT]) {
+// this lane's max |value| of the group (callers reduce over the warp only when needed)
+__device__ __forceinline__ float lane_max(const float4 (&v)[NIT]) {
   float mx = 0.0f;
 #pragma unroll
   for (int it = 0; it < NIT; ++it)
     mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[it].x), fabsf(v[it].y)), fmaxf(fabsf(v[it].z), fabsf(v[it].w))));
-  return warp_max(mx);
+  return mx;
 }
 // Split the group (loaded by load_group) in place into hi / (lmul * lo) fp16 tiles.
 __device__ __forceinline__ void store_group(uint8_t* gb, int lane, const float4 (&v)[NIT], float sz, float lmul) {
@@ -222,8 +223,9 @@ __global__ void __launch_bounds__(NT, 1) gram_kernel(const float2* __restrict__ 
       uint8_t* gb = ring + s * SB + cw * GS;
       float4 v[NIT];
       load_group(gb, lane, v);
-      const float gm = group_max(v);
+      float gm = lane_max(v);  // per lane: the range flag is OR-ed over the warp after the loop
       if (!have) {  // until the first non-zero chunk: max over the converter warps
+        gm = warp_max(gm);
         if (lane == 0) sm->rmax[0][cw] = gm;
         named_sync(BAR_CONV, 32 * NCONV);
         float mx = sm->rmax[0][0];
@@ -241,6 +243,7 @@ __global__ void __launch_bounds__(NT, 1) gram_kernel(const float2* __restrict__ 
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm->conv_full[s]);
     }
+    over = __any_sync(0xffffffffu, over);
     if (!fixup) {
       if (over && lane == 0) rflag[b] = 1;
       if (tid == 32 * W_CONV0) szv[b] = sz;
