@@ -1,6 +1,7 @@
 """K = 256 complex64 (cfg5 shape) on the hand-written tcgen05 chain of
-large_k.cu: streaming upper-triangular Gram tiles, the 8-CTA cluster
-Jac-PCG / CG sharing the split A'' by TMA multicast, and the W kernel with the
+large_k.cu: streaming upper-triangular Gram tiles, the cluster Jac-PCG / CG
+sharing the split A'' by TMA multicast (default: cta_group::2 pairs on 4-CTA
+clusters; XL_LK_PAIR=0: 8-CTA clusters of single-CTA MMAs), and the W kernel with the
 X operand in TMEM / shared memory -- against the complex128 oracle
 (linsolve.py:217-294, precoder.py:53-91) and against the split-operand
 library-GEMM path it replaces (XL_LARGE_K_256=library).
@@ -164,3 +165,31 @@ def test_k256_silent_user(method):
         Gr, _, _, s = O.precoder_and_se(Hq[b], wl.alpha(), wl.power(), 1.0, method, 6, "textbook")
         assert relf(out.W[b].cpu().numpy(), Gr) <= 1e-4
         assert abs(out.sum_se[b].item() - s) <= 1e-4 * abs(s)
+
+
+@pytest.mark.parametrize("method,variant", [("jacpcg", "textbook"), ("cg", "textbook"), ("jacpcg", "algorithm")])
+def test_k256_pair_solver_layouts_agree(method, variant):
+    """The pair-MMA solver (M = 256 row-split A'', N = 128, Q halves exchanged
+    through DSMEM), its unicast-load variant and the single-CTA 8-cluster layout
+    compute the same recurrence: W within fp32 rounding of each other and of the
+    oracle, on a batch with an odd number of work items per cluster wave."""
+    wl = X.CONFIGS["cfg5"]
+    T = 3 if variant == "algorithm" else 6
+    H = X.generate_channels(wl.model, seed=2, first=11, B=37, dtype=torch.complex64)
+    run = lambda: BT.rzf_batched(H, wl.alpha(), wl.power(), method=method, T=T, variant=variant, want_X=True)
+    pair = _run_env({"XL_LK_PAIR": None, "XL_LK_UNICAST": None}, run)
+    uni = _run_env({"XL_LK_PAIR": None, "XL_LK_UNICAST": "1"}, run)
+    single = _run_env({"XL_LK_PAIR": "0", "XL_LK_UNICAST": None}, run)
+    assert torch.equal(pair.W, uni.W)  # same products, only the load path differs
+    Hq = H.cpu().numpy().astype(np.complex128)
+    if variant == "textbook":
+        for b in range(H.shape[0]):
+            assert relf(pair.W[b].cpu().numpy(), single.W[b].cpu().numpy()) <= 2e-5
+    for b in (0, 18, 36):
+        Gr, _, _, s = O.precoder_and_se(Hq[b], wl.alpha(), wl.power(), 1.0, method, T, variant)
+        e, e1 = relf(pair.W[b].cpu().numpy(), Gr), relf(single.W[b].cpu().numpy(), Gr)
+        if variant == "algorithm":  # divergent recurrence (SURVEY F2): the fp32 sensitivity bound
+            fw, _ = _fp32_sensitivity(Hq[b], wl.alpha(), wl.power(), method, T, variant)
+            assert e <= max(1e-4, 10 * fw) and e1 <= max(1e-4, 10 * fw), (b, e, e1, fw)
+        else:
+            assert e <= 1e-4 and e1 <= 1e-4, (b, e, e1)
