@@ -932,14 +932,15 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
   const uint32_t lead_pfull = PR ? mapa_u32(su32(&sm->pfull[0]), rank & ~1u) : 0u;
   const uint32_t lead_bready = PR ? mapa_u32(su32(&sm->bready), rank & ~1u) : 0u;
   uint32_t g_prod = 0, g_cons = 0, nq = 0;  // ring chunks produced / consumed, products
-  // thread 0 streams the split A: chunk n of the realization's (T + 1) x 16
-  // K-steps into the ring (stage g % NS of all eight CTAs), armed in every
-  // CTA, copied by its owner CTA (n % 8) with one multicast once every CTA has
-  // freed the stage
+  // the producer warp streams the split A: chunk n of the item's (T - 1) x 16
+  // K-steps into ring stage g % NS of every CTA of the cluster, armed in every
+  // CTA, copied by its owner with one multicast once every consumer has freed
+  // the stage (PR: each pair rank gets its own 16 KiB row tile, owner CTA
+  // 2 (k % (CL / 2)) + rank parity; else the whole 32 KiB chunk, owner k % 8)
   int n_issued = 0, n_total = 0;
-  // (called by all lanes of warp 0; lane 0 does the barrier / copy work)
-  // 32 KiB per copy: a lane's bulk copies are serviced about one at a time,
-  // so the fill rate grows with the copy size (tools/microbench/bulk_rules.cu)
+  // (called by all lanes of warp 1; lane 0 does the barrier / copy work)
+  // a lane's bulk copies are serviced about one at a time, so the fill rate
+  // grows with the copy size (tools/microbench/bulk_rules.cu)
   auto issue_next = [&]() {  // chunk n: K-step n % NCH
     if (n_issued >= n_total) return;
     const int s = g_prod % NS, k = n_issued % NCH;
