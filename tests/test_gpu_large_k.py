@@ -193,3 +193,40 @@ def test_k256_pair_solver_layouts_agree(method, variant):
             assert e <= max(1e-4, 10 * fw) and e1 <= max(1e-4, 10 * fw), (b, e, e1, fw)
         else:
             assert e <= 1e-4 and e1 <= 1e-4, (b, e, e1)
+
+
+def test_k256_per_realization_xi_vs_oracle():
+    """Per-realization regularisation (one SNR point per realization, the
+    reference's xi = K / SNR per trial) through the pair solver: each
+    realization against the oracle at its own xi (precoder.py:53-61, 81-91)."""
+    wl = X.CONFIGS["cfg5"]
+    B = 7
+    H = X.generate_channels(wl.model, seed=4, first=31, B=B, dtype=torch.complex64)
+    snr_db = torch.linspace(-10.0, 20.0, B, dtype=torch.float64)
+    xi = K / (10.0 ** (snr_db / 10.0))
+    out = BT.rzf_batched(H, xi.cuda(), wl.power(), method="jacpcg", T=6)
+    Hq = H.cpu().numpy().astype(np.complex128)
+    for b in range(B):
+        Gr, br, _, s = O.precoder_and_se(Hq[b], float(xi[b]), wl.power(), 1.0, "jacpcg", 6, "textbook")
+        assert relf(out.W[b].cpu().numpy(), Gr) <= 1e-4, b
+        assert abs(out.sum_se[b].item() - s) <= 1e-4 * abs(s)
+        assert abs(out.beta[b].item() - br) <= 1e-4 * br
+
+
+def test_k256_host_pipeline_matches_device_call():
+    """The host-buffer API (pinned H in, W / sum-SE / status out, chunked over
+    three streams) on the K = 256 chain returns exactly the device call's
+    results, with a chunk that does not divide the batch."""
+    wl = X.CONFIGS["cfg5"]
+    B = 5
+    H = X.generate_channels(wl.model, seed=6, first=2, B=B, dtype=torch.complex64)
+    Hh = H.cpu().pin_memory()
+    Wh = torch.empty_like(Hh).pin_memory()
+    Sh = torch.empty(B, dtype=torch.float64).pin_memory()
+    Sth = torch.empty(B, dtype=torch.int32).pin_memory()
+    pipe = BT.HostPipeline(wl.M, K, chunk=2)
+    pipe.run(Hh, Wh, Sh, Sth, wl.alpha(), wl.power(), "jacpcg", 6)
+    torch.cuda.synchronize()
+    ref = BT.rzf_batched(H, wl.alpha(), wl.power(), T=6)
+    assert Sth.tolist() == [0] * B
+    assert torch.equal(Wh, ref.W.cpu()) and torch.equal(Sh, ref.sum_se.cpu())
