@@ -799,9 +799,14 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
-// arrive (release at cluster scope) on an mbarrier of another CTA of the cluster
-__device__ __forceinline__ void mbar_arrive_cl(uint32_t cl_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
+// arrive on an mbarrier of another CTA of the cluster with the default
+// (CTA-scope) release, as CUTLASS's 2-SM UMMA pipelines signal the peer after
+// fence.proxy.async: what it publishes is this CTA's shared memory, read by the
+// pair's tensor cores.  A .release.cluster arrive costs a cluster-scope fence
+// per call (measured: a third of the pair W kernel's stall samples, and ~2 k
+// cycles per product in the pair solver's relays).
+__device__ __forceinline__ void mbar_arrive_peer(uint32_t cl_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
 }
 // wait with acquire at cluster scope (the phase was completed from another CTA)
 __device__ __forceinline__ void bwait_cl(uint64_t* bar, uint32_t parity) {
@@ -1101,7 +1106,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       tc_before();
       named_sync(BAR_MATH, NT);
       if constexpr (PR) {
-        if (tid == 0 && !leader) mbar_arrive_cl(lead_bready);  // the leader's MMAs read our B half
+        if (tid == 0 && !leader) mbar_arrive_peer(lead_bready);  // the leader's MMAs read our B half
         if (warp == 0) {
           tc_after();
           if (leader) {
@@ -1136,7 +1141,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
               const uint32_t gc = g_cons + k;
               const int s = gc % NS;
               bwait(&sm->full[s], (gc / NS) & 1);
-              if (lane == 0) mbar_arrive_cl(lead_pfull + 8u * (uint32_t)s);
+              if (lane == 0) mbar_arrive_peer(lead_pfull + 8u * (uint32_t)s);
               __syncwarp();
             }
           }
@@ -1414,6 +1419,266 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
 }
 }  // namespace pc
 
+// ============================================================ W, CTA pairs ===
+// lk_w_kernel as cta_group::2 pairs (XL_LK_W2=1): output blocks t = 2p, 2p + 1
+// of one realization form a cluster of two and multiply as one M = 256 MMA
+// (each CTA's A = its block's X rows, written into its own TMEM with
+// tcgen05.st), N = 64 antennas split 32 / 32: each CTA lands and converts only
+// its 32-antenna half of every H box and the pair's tensor cores read both
+// halves, so per CTA and box the shared-memory port moves 36 KiB instead of 72.
+// The follower's converter warps signal the leader's MMA issuer directly
+// (mbarrier.arrive.release.cluster); they never hold outstanding global
+// stores (a dedicated epilogue warpgroup drains TMEM and writes W), which made
+// that release cost a third of the kernel in the first pair version.
+namespace wk2 {
+using wk::CHA;
+using wk::BU;
+using wk::TPR;
+using wk::T_AH;
+using wk::T_AL;
+using wk::T_ACC;
+constexpr int W_PROD = 0, W_MMA = 1, W_CONV0 = 2, NCONV = 8, W_EPI0 = W_CONV0 + NCONV, NEPI = 4;
+constexpr int NT = 32 * (W_EPI0 + NEPI);
+constexpr int HB = (CHA / 2) * 2 * BU * 4;  // 8 KiB: this CTA's 32 antennas of a box
+constexpr int NS = 20;                      // ring depth (160 KiB in flight)
+constexpr int SMALL = 2048;
+constexpr int SMEM = NS * HB + SMALL;
+static_assert(SMEM <= 227 * 1024, "lk W2 smem");
+constexpr uint32_t ID2 = idesc(256, CHA, 0, 0);
+
+struct Small {
+  uint64_t full[NS], conv[NS], freed[NS];
+  uint64_t acc_full[2], acc_free[2], pacc_free[2];
+  uint32_t tmem_slot;
+  float rmax[4][64];
+  float sx[64];
+};
+static_assert(sizeof(Small) <= SMALL, "W2 small");
+
+__device__ __forceinline__ void mma2_ts_w(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void tmem_st16u(uint32_t ta, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
+__global__ void __launch_bounds__(NT, 1) lk_w2_kernel(const __grid_constant__ CUtensorMap hmap, int M,
+                                                      const unsigned* __restrict__ zmax, const float2* __restrict__ X,
+                                                      const double* __restrict__ beta, float* __restrict__ W,
+                                                      float* __restrict__ F) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* ring = smem;
+  Small* sm = reinterpret_cast<Small*>(smem + NS * HB);
+  const int64_t b = blockIdx.x / TPR;
+  const int t = blockIdx.x % TPR;
+  const uint32_t pr = cluster_rank();  // == t & 1
+  const bool leader = pr == 0;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ntile = M / CHA, nbox = ntile * (KU / BU);
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm->full[s], 1);
+      mbar_init(&sm->conv[s], 2 * 4);  // leader: the 4 converter warps of this box in each CTA
+      mbar_init(&sm->freed[s], 1);
+    }
+    for (int j = 0; j < 2; ++j) {
+      mbar_init(&sm->acc_full[j], 1);
+      mbar_init(&sm->acc_free[j], NEPI);  // the local epilogue warps
+      mbar_init(&sm->pacc_free[j], 1);    // leader: the follower's epilogue (relayed)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == W_MMA) pc::tmem_alloc512_g<true>(&sm->tmem_slot);
+  const float2* Xb = X + b * (int64_t)KU * KU;
+  // ---- per-user scale sx[j'] = 2^e, max |X_:j'| sx < 2^14
+  if (tid < 256) {
+    const int jl = tid & 63, part = tid >> 6;
+    float m = 0.0f;
+#pragma unroll 8
+    for (int i = 64 * part; i < 64 * part + 64; ++i) {
+      const float2 x = __ldg(Xb + (int64_t)i * KU + 64 * t + jl);
+      m = fmaxf(m, fmaxf(fabsf(x.x), fabsf(x.y)));
+    }
+    sm->rmax[part][jl] = m;
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (tid < 64)
+    sm->sx[tid] = pow2_scale(fmaxf(fmaxf(sm->rmax[0][tid], sm->rmax[1][tid]), fmaxf(sm->rmax[2][tid], sm->rmax[3][tid])), 14);
+  __syncthreads();
+  const uint32_t tmem = sm->tmem_slot;
+  // ---- A hi / lo straight into TMEM (lane = output row r, column = two input
+  // users): converter warp cw writes its lane quadrant, users [128 h, +128)
+  if (warp >= W_CONV0 && warp < W_EPI0) {
+    const int cw = warp - W_CONV0, q = warp & 3, h = cw >> 2;
+    const int r = 32 * q + lane, jl = r >> 1;
+    const bool odd = r & 1;
+    const float sc = sm->sx[jl];
+    const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16);
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {  // 32 input users per step
+      const int i0 = 128 * h + 32 * c;
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const float2 x0 = __ldg(Xb + (int64_t)(i0 + 2 * e) * KU + 64 * t + jl);
+        const float2 x1 = __ldg(Xb + (int64_t)(i0 + 2 * e + 1) * KU + 64 * t + jl);
+        split2((odd ? x0.y : x0.x) * sc, (odd ? x1.y : x1.x) * sc, hi[e], lo[e]);
+      }
+      tmem_st16u(ta + T_AH + i0 / 2, hi);
+      tmem_st16u(ta + T_AL + i0 / 2, lo);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  tc_before();
+  cluster_sync();  // both CTAs' A rows are in TMEM, every barrier initialised
+  tc_after();
+
+  if (warp == W_PROD) {
+    constexpr int NL = 8;
+    if (lane < NL) {
+      const int y0 = (int)(b * M) + (CHA / 2) * (int)pr;
+      for (int g = lane; g < nbox; g += NL) {
+        const int s = g % NS, tt = g / (KU / BU), kb = g % (KU / BU);
+        if (g >= NS) bwait<true>(&sm->freed[s], ((g / NS) - 1) & 1);
+        mbar_expect_tx(&sm->full[s], HB);
+        tma2d(ring + s * HB, &hmap, 2 * BU * kb, y0 + CHA * tt, &sm->full[s]);
+      }
+    }
+  } else if (warp == W_MMA) {
+    if (leader) {
+      for (int g = 0; g < nbox; ++g) {
+        const int s = g % NS, tt = g / (KU / BU), kb = g % (KU / BU);
+        if (kb == 0 && tt >= 2) {
+          bwait(&sm->acc_free[tt & 1], ((tt >> 1) - 1) & 1);
+          pc::bwait_cl(&sm->pacc_free[tt & 1], ((tt >> 1) - 1) & 1);
+        }
+        pc::bwait_cl(&sm->conv[s], (g / NS) & 1);
+        tc_after();
+        const uint32_t st = su32(ring + s * HB);
+        const uint32_t d1 = tmem + T_ACC + 128 * (tt & 1), d2 = d1 + CHA;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const int sk = 2 * kb + ks;
+          const uint32_t ah = tmem + T_AH + 8 * sk, al = tmem + T_AL + 8 * sk;
+          const uint64_t brh = sdesc(st + 256 * ks, 128, 2048), brl = sdesc(st + 1024 + 256 * ks, 128, 2048);
+          const uint64_t bih = sdesc(st + 512 + 256 * ks, 128, 2048), bil = sdesc(st + 1536 + 256 * ks, 128, 2048);
+          const uint32_t acc = (kb | ks) != 0;
+          mma2_ts_w(d1, ah, brh, ID2, acc);
+          mma2_ts_w(d1, ah, brl, ID2, 1);
+          mma2_ts_w(d1, al, brh, ID2, 1);
+          mma2_ts_w(d2, ah, bih, ID2, acc);
+          mma2_ts_w(d2, ah, bil, ID2, 1);
+          mma2_ts_w(d2, al, bih, ID2, 1);
+        }
+        pc::commit2_mc_w(&sm->freed[s], 3);
+        if (kb == KU / BU - 1) pc::commit2_mc_w(&sm->acc_full[tt & 1], 3);
+      }
+    } else if (lane == 0) {  // relay: the follower's drain of tile tt - 2 -> the leader
+      const uint32_t lead_pfree = pc::mapa_u32(su32(&sm->pacc_free[0]), 0);
+      for (int tt = 2; tt < ntile; ++tt) {
+        bwait(&sm->acc_free[tt & 1], ((tt >> 1) - 1) & 1);
+        pc::mbar_arrive_peer(lead_pfree + 8u * (uint32_t)(tt & 1));
+      }
+    }
+  } else if (warp < W_EPI0) {  // converters: 8-antenna group grp of boxes g % 2 == par
+    const int cw = warp - W_CONV0;
+    const int grp = cw & 3, par = cw >> 2;
+    const float sz = pow2_scale(__uint_as_float(zmax[b]), 11);
+    const int crow = lane >> 2, pair = lane & 3;
+    const uint32_t conv_addr = pc::mapa_u32(su32(&sm->conv[0]), 0);
+    for (int g = par; g < nbox; g += 2) {
+      const int s = g % NS;
+      bwait(&sm->full[s], (g / NS) & 1);
+      uint8_t* gb = ring + s * HB + grp * 2048;  // 8 antennas x 64 components
+      float4 v[4];
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int c = (it + crow) & 3;
+        v[it] = *reinterpret_cast<const float4*>(gb + crow * 256 + 64 * c + 16 * pair);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int c = (it + crow) & 3;
+        uint32_t hr, lr, hi_, li_;
+        split2(v[it].x * sz, v[it].z * sz, hr, lr);
+        split2(v[it].y * sz, v[it].w * sz, hi_, li_);
+        const int o = crow * 16 + 4 * pair;
+        *reinterpret_cast<uint32_t*>(gb + 128 * c + o) = hr;
+        *reinterpret_cast<uint32_t*>(gb + 1024 + 128 * c + o) = lr;
+        *reinterpret_cast<uint32_t*>(gb + 128 * (4 + c) + o) = hi_;
+        *reinterpret_cast<uint32_t*>(gb + 1024 + 128 * (4 + c) + o) = li_;
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(&sm->conv[s]);
+        else pc::mbar_arrive_peer(conv_addr + 8u * (uint32_t)s);
+      }
+    }
+  } else {  // epilogue warpgroup: lane quadrant q, all 64 antennas of a tile in two halves
+    const int q = warp & 3;
+    const int r = 32 * q + lane;  // output row (TMEM lane)
+    const bool odd = r & 1;
+    const int col = 128 * t + r;
+    const double bt = beta[b];
+    const float srow = sm->sx[r >> 1];
+    const float sz = pow2_scale(__uint_as_float(zmax[b]), 11);
+    const float wmul = (float)(bt / ((double)srow * (double)sz));
+    const float fmul = 1.0f / (srow * sz);
+    const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16) + T_ACC;
+    for (int tt = 0; tt < ntile; ++tt) {
+      const int jb = tt & 1;
+      pc::bwait_cl(&sm->acc_full[jb], (tt >> 1) & 1);
+      tc_after();
+#pragma unroll 1
+      for (int hh = 0; hh < 2; ++hh) {
+        float v[32], u[32];
+        tmem_ld16(tq + 128 * jb + 32 * hh, v);
+        tmem_ld16(tq + 128 * jb + 32 * hh + 16, v + 16);
+        tmem_ld16(tq + 128 * jb + CHA + 32 * hh, u);
+        tmem_ld16(tq + 128 * jb + CHA + 32 * hh + 16, u + 16);
+        tmem_wait_ld();
+        if (hh == 1) {
+          tc_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm->acc_free[jb]);
+        }
+#pragma unroll
+        for (int n = 0; n < 32; ++n) {
+          const float o2 = __shfl_xor_sync(0xffffffffu, u[n], 1);
+          v[n] = odd ? v[n] + o2 : v[n] - o2;
+        }
+        const int64_t n0 = (int64_t)tt * CHA + 32 * hh;
+        float* wp = W + (b * (int64_t)M + n0) * NC + col;
+#pragma unroll
+        for (int n = 0; n < 32; ++n) __stcs(wp + (int64_t)n * NC, v[n] * wmul);
+        if (F) {
+          float* fp = F + (b * (int64_t)M + n0) * NC + col;
+#pragma unroll
+          for (int n = 0; n < 32; ++n) __stcs(fp + (int64_t)n * NC, v[n] * fmul);
+        }
+      }
+    }
+  }
+  tc_before();
+  cluster_sync();  // no remote arrive / multicast commit targets an exited CTA
+  if (warp == W_MMA) {
+    tc_after();
+    pc::tmem_free512_g<true>(tmem);
+  }
+}
+}  // namespace wk2
+
 // ------------------------------------------------------------------ host ----
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1559,6 +1824,27 @@ int lk_apply(const void* H, const void* X, const double* beta, int64_t B, int M,
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const unsigned* zmax = (const unsigned*)((char*)ws + 2 * al((size_t)B * 4));  // from lk_gram
   CUtensorMap map;
+  const char* w2 = getenv("XL_LK_W2");  // "0": the single-CTA W kernel (A/B, tests)
+  if (!(w2 && w2[0] == '0')) {  // CTA pairs: each CTA lands / converts half of every box
+    if (int e = make_hmap(&map, H, B, M, 2 * wk::BU, wk::CHA / 2)) return e;
+    cudaFuncSetAttribute(wk2::lk_w2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wk2::SMEM);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(wk::TPR * B), 1, 1);
+    cfg.blockDim = dim3(wk2::NT, 1, 1);
+    cfg.dynamicSmemBytes = wk2::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, wk2::lk_w2_kernel, map, M, zmax, (const float2*)X, beta, (float*)W, (float*)F) !=
+        cudaSuccess)
+      return check_launch("lk w2 launch");
+    return check_launch("lk w2");
+  }
   if (int e = make_hmap(&map, H, B, M, 2 * wk::BU, wk::CHA)) return e;
   cudaFuncSetAttribute(wk::lk_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wk::SMEM);
   wk::lk_w_kernel<<<(unsigned)(wk::TPR * B), wk::NT, wk::SMEM, st>>>(map, M, zmax, (const float2*)X, beta, (float*)W,
