@@ -1679,6 +1679,216 @@ __global__ void __launch_bounds__(NT, 1) lk_w2_kernel(const __grid_constant__ CU
 }
 }  // namespace wk2
 
+// ========================================================= Gram, CTA pairs ===
+// lk_gram_kernel as cta_group::2 pairs: the 512 x 512 real Gram's upper
+// triangle as three 256 x 256 super-tiles (0,0), (0,1), (1,1), one CTA pair
+// each (six CTAs per realization).  Pair CTA v of super-tile (I, J) supplies
+// the M rows of 64-user block 2I + v and the N half of block 2J + v: on the
+// diagonal super-tiles that is one block (landed and converted once, used as
+// both operands), off the diagonal two.  Per CTA and 32-antenna chunk the
+// shared-memory port moves 96-144 KiB instead of 144-216 KiB (a converted block
+// feeds an M = 256 x N = 256 MMA), for 20% more MMA work (the lower quarters
+// of the diagonal super-tiles).  The follower's converters signal the leader's
+// MMA issuer with CTA-scope peer arrives; each CTA keeps its own split scale
+// (first non-zero chunk) and the epilogue unscales column half k by the scale
+// of the CTA that supplied it.
+namespace gram2 {
+using gram::CH;
+using gram::BLK;
+using gram::SGL;
+using gram::NCONV;
+using gram::W_PROD;
+using gram::W_MMA;
+using gram::W_CONV0;
+using gram::NT;
+using gram::BAR_CONV;
+constexpr int TPR = 6;
+constexpr int NS = 4;
+constexpr int SB = 2 * SGL;  // 32 KiB: at most two single blocks per chunk
+constexpr int SMALL = 1024;
+constexpr int SMEM = NS * SB + SMALL;
+static_assert(SMEM <= 227 * 1024, "lk gram2 smem");
+constexpr uint32_t ID2 = idesc(256, 2 * BLK, 1, 1);
+constexpr int SG = 8 * BLK * 4;  // one 8-antenna group of a single block (4 KiB raw == hi + lo)
+
+struct Small {
+  uint64_t full[NS], conv[NS], freed[NS];
+  uint64_t done;
+  uint32_t tmem_slot;
+  float sz;
+  float rmax[NCONV];
+};
+static_assert(sizeof(Small) <= SMALL, "gram2 small");
+
+__global__ void __launch_bounds__(NT, 1) lk_gram2_kernel(const __grid_constant__ CUtensorMap smap, int M,
+                                                         float* __restrict__ szv, float2* __restrict__ A, double xi,
+                                                         const double* __restrict__ xi_b, int* __restrict__ rflag,
+                                                         unsigned* __restrict__ zmax, int fixup) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* ring = smem;
+  Small* sm = reinterpret_cast<Small*>(smem + NS * SB);
+  const int64_t b = blockIdx.x / TPR;
+  const int st_idx = (blockIdx.x % TPR) >> 1;  // super-tile 0: (0,0), 1: (0,1), 2: (1,1)
+  if (fixup && rflag[b] == 0) return;           // both CTAs of the pair share b
+  const uint32_t v = cluster_rank();
+  const bool leader = v == 0;
+  const int SI = st_idx == 2 ? 1 : 0, SJ = st_idx == 0 ? 0 : 1;
+  const bool diag = SI == SJ;
+  const int rowblk = 2 * SI + (int)v, colblk = 2 * SJ + (int)v;
+  const int nbx = diag ? 1 : 2;  // singles per chunk: [rowblk] or [rowblk, colblk]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nch = M / CH;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm->full[s], 1);
+      mbar_init(&sm->conv[s], 2 * NCONV);  // leader: every converter warp of both CTAs
+      mbar_init(&sm->freed[s], 1);
+    }
+    mbar_init(&sm->done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == W_MMA) pc::tmem_alloc512_g<true>(&sm->tmem_slot);
+  tc_before();
+  __syncthreads();
+  tc_after();
+  cluster_sync();  // barriers initialised in both CTAs before any peer arrive / multicast commit
+  const uint32_t tmem = sm->tmem_slot;
+
+  float sz = fixup ? szv[b] : 1.0f;
+  if (warp == W_PROD) {
+    if (lane < nbx) {
+      const int y0 = (int)(b * M);
+      const int blk = lane == 0 ? rowblk : colblk;
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % NS;
+        if (c >= NS) bwait<true>(&sm->freed[s], ((c / NS) - 1) & 1);
+        if (lane == 0) mbar_expect_tx(&sm->full[s], nbx * SGL);
+        tma2d(ring + s * SB + lane * SGL, &smap, BLK * blk, y0 + c * CH, &sm->full[s]);
+      }
+    }
+  } else if (warp == W_MMA) {
+    if (leader) {
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % NS;
+        pc::bwait_cl(&sm->conv[s], (c / NS) & 1);
+        tc_after();
+        const uint32_t sa = su32(ring + s * SB), sbb = sa + (diag ? 0 : SGL);
+#pragma unroll
+        for (int ks = 0; ks < CH / 16; ++ks) {
+          const uint32_t acc = (c | ks) != 0;
+          const uint64_t ah = sdesc(sa + 2 * ks * SG, SG, 128), al = sdesc(sa + 2 * ks * SG + SG / 2, SG, 128);
+          const uint64_t bh = sdesc(sbb + 2 * ks * SG, SG, 128), bl = sdesc(sbb + 2 * ks * SG + SG / 2, SG, 128);
+          pc::mma2_w(tmem, ah, bh, ID2, acc);
+          pc::mma2_w(tmem, ah, bl, ID2, 1);
+          pc::mma2_w(tmem, al, bh, ID2, 1);
+        }
+        pc::commit2_mc_w(&sm->freed[s], 3);
+      }
+      pc::commit2_mc_w(&sm->done, 3);
+    }
+  } else {
+    const int cw = warp - W_CONV0;
+    const bool active = cw < 4 * nbx;  // group cw & 3 of single cw >> 2
+    bool have = fixup != 0, over = false;
+    float zm = 0.0f;
+    const uint32_t conv_addr = pc::mapa_u32(su32(&sm->conv[0]), 0);
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % NS;
+      bwait(&sm->full[s], (c / NS) & 1);
+      uint8_t* sg = ring + s * SB + (cw >> 2) * SGL + (cw & 3) * SG;
+      float4 vs[8];
+      float gm = active ? gram::load8(sg, BLK * 4, lane, 0, vs) : 0.0f;
+      zm = fmaxf(zm, gm);
+      if (!have) {  // until the first non-zero chunk: max over the converter warps
+        gm = warp_max(gm);
+        if (lane == 0) sm->rmax[cw] = gm;
+        named_sync(BAR_CONV, 32 * NCONV);
+        float mx = sm->rmax[0];
+#pragma unroll
+        for (int w = 1; w < NCONV; ++w) mx = fmaxf(mx, sm->rmax[w]);
+        named_sync(BAR_CONV, 32 * NCONV);
+        if (mx > 0.0f) {
+          sz = pow2_scale(mx, 7);
+          have = true;
+        }
+      }
+      over |= !(gm * sz < RANGE_MAX);
+      __syncwarp();
+      if (active) gram::store8(sg, SG / 2, lane, 0, vs, sz);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(&sm->conv[s]);
+        else pc::mbar_arrive_peer(conv_addr + 8u * (uint32_t)s);
+      }
+    }
+    over = __any_sync(0xffffffffu, over);
+    zm = warp_max(zm);
+    if (!fixup && over && lane == 0) rflag[b] = 1;
+    if (lane == 0 && zm > 0.0f) atomicMax(zmax + b, __float_as_uint(zm));
+    if (tid == 32 * W_CONV0) sm->sz = sz;
+  }
+  tc_before();
+  cluster_sync();  // both CTAs' scales are published
+  tc_after();
+  if (warp >= W_CONV0) {
+    // ---- epilogue: column half k of the accumulator is tile (rowblk, 2 SJ + k),
+    // supplied by CTA k; the upper-triangle tiles are written with their
+    // conjugate mirror (Hermitian by construction), the lower one skipped
+    float szk[2];
+    {
+      float peer_sz;
+      asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(peer_sz) : "r"(pc::mapa_u32(su32(&sm->sz), v ^ 1u)));
+      szk[v] = sm->sz;
+      szk[v ^ 1u] = peer_sz;
+    }
+    pc::bwait_cl(&sm->done, 0);
+    tc_after();
+    const int cw = warp - W_CONV0;
+    const int q = warp & 3, p = cw >> 2;
+    const int r = 32 * q + lane;
+    const double xi_v = xi_b ? xi_b[b] : xi;
+    const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+    const bool odd = lane & 1;
+    float2* Ab = A + b * (int64_t)KU * KU;
+    const float isz_row = 1.0f / sm->sz;
+#pragma unroll 1
+    for (int k = 0; k < 2; ++k) {
+      const int I = rowblk, J = 2 * SJ + k;
+      if (I > J) continue;
+      const float un = isz_row / szk[k];
+      const int i = 64 * I + (r >> 1);
+#pragma unroll 1
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        float vv[16];
+        tmem_ld16(tl + 128 * k + 64 * p + c0, vv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+          const float g0 = vv[e] * un, g1 = vv[e + 1] * un;
+          const float p0 = __shfl_xor_sync(0xffffffffu, g0, 1), p1 = __shfl_xor_sync(0xffffffffu, g1, 1);
+          float re = odd ? (p0 + g1) : (g0 + p1);
+          const float im = odd ? (p1 - g0) : (g1 - p0);
+          const int j = 64 * J + ((64 * p + c0 + e) >> 1);
+          if (i == j) {
+            if (!odd) Ab[(int64_t)i * KU + j] = make_float2((float)((double)re + xi_v), 0.0f);
+          } else if (i < j) {
+            if (!odd) Ab[(int64_t)i * KU + j] = make_float2(re, im);
+            else Ab[(int64_t)j * KU + i] = make_float2(re, -im);
+          }
+        }
+      }
+    }
+  }
+  tc_before();
+  cluster_sync();  // no peer arrive / multicast commit targets an exited CTA
+  if (warp == W_MMA) {
+    tc_after();
+    pc::tmem_free512_g<true>(tmem);
+  }
+}
+}  // namespace gram2
+
 // ------------------------------------------------------------------ host ----
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1770,15 +1980,37 @@ int lk_gram(const void* H, int64_t B, int M, double xi, const double* xi_b, void
   unsigned* zmax = (unsigned*)((char*)ws + 2 * al((size_t)B * 4));
   if (cudaMemsetAsync(rflag, 0, (size_t)B * sizeof(int), st) != cudaSuccess) return check_launch("lk flags");
   if (cudaMemsetAsync(zmax, 0, (size_t)B * sizeof(unsigned), st) != cudaSuccess) return check_launch("lk zmax init");
-  cudaFuncSetAttribute(gram::lk_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gram::SMEM);
-  gram::lk_gram_kernel<<<(unsigned)(gram::TPR * B), gram::NT, gram::SMEM, st>>>(pmap, smap, M, sz, (float2*)A, xi,
-                                                                               xi_b, rflag, zmax, 0);
-  if (int e = check_launch("lk gram")) return e;
+  const char* g2 = getenv("XL_LK_GRAM2");  // "0": the 5-CTA single-CTA-MMA Gram (A/B, tests)
+  const bool pair = !(g2 && g2[0] == '0');
+  auto launch = [&](int fixup) -> int {
+    if (pair) {
+      cudaFuncSetAttribute(gram2::lk_gram2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gram2::SMEM);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(gram2::TPR * B), 1, 1);
+      cfg.blockDim = dim3(gram2::NT, 1, 1);
+      cfg.dynamicSmemBytes = gram2::SMEM;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      if (cudaLaunchKernelEx(&cfg, gram2::lk_gram2_kernel, smap, M, sz, (float2*)A, xi, xi_b, rflag, zmax, fixup) !=
+          cudaSuccess)
+        return check_launch("lk gram2 launch");
+      return check_launch(fixup ? "lk gram2 fixup" : "lk gram2");
+    }
+    cudaFuncSetAttribute(gram::lk_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gram::SMEM);
+    gram::lk_gram_kernel<<<(unsigned)(gram::TPR * B), gram::NT, gram::SMEM, st>>>(pmap, smap, M, sz, (float2*)A, xi,
+                                                                                 xi_b, rflag, zmax, fixup);
+    return check_launch(fixup ? "lk gram fixup" : "lk gram");
+  };
+  if (int e = launch(0)) return e;
   lk_zmax_kernel<<<(unsigned)B, 512, 0, st>>>((const float4*)H, (int64_t)M * NC / 4, sz, rflag);
   if (int e = check_launch("lk zmax")) return e;
-  gram::lk_gram_kernel<<<(unsigned)(gram::TPR * B), gram::NT, gram::SMEM, st>>>(pmap, smap, M, sz, (float2*)A, xi,
-                                                                               xi_b, rflag, zmax, 1);
-  return check_launch("lk gram fixup");
+  return launch(1);
 }
 
 static long long* g_lk_trace = nullptr;
