@@ -844,6 +844,8 @@ struct Params {
   float2* X;        // [B][K][K]
   float2* GX;       // [B][K][K]
   double* part;     // [B][C] Re tr(X^H GX) per CTA
+  double* rsq;      // [B][C][2][K] per (column block, part) row sums of GX^2, or null: GX written instead
+  float2* gdiag;    // [B][K] diagonal of GX (with rsq)
   int32_t* status;  // [B]
   uint8_t* scratch; // [clusters][512 KiB] split (Re A, Im A), K-step chunks
   long long* trace; // debug: clock64 stamps of cluster 0 / CTA 0 (xl_debug_lk_trace), or null
@@ -1363,9 +1365,12 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
     tmem_ld<JN>(tX, P);
     tmem_ld<JN>(tR, A);
     tmem_wait_ld();
+    stamp();
     double fro = 0.0;
     const double xsa = alpha * (double)sa;
     const float crr = (use_c && !textbook) ? cr : 1.0f;
+    double rs = 0.0;  // this thread's part of sum_j |GX_uj|^2 over the CTA's columns
+    float gd = 0.0f;  // its part of GX_uu when column u is the CTA's
 #pragma unroll
     for (int jj = 0; jj < JN; ++jj) {
       const int jg = JN * cb + jj;
@@ -1374,6 +1379,14 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       const float g = (float)((double)ax - xsa * (double)P[jj]);
       A[jj] = g;
       fro += (double)(P[jj] * sa) * (double)g;  // Re tr(X^H GX)
+      rs += (double)(g * g);
+      if (u == jg) gd = g;
+    }
+    // SINR inputs instead of GX itself (metrics.py:35-58 needs |B_kk|^2 and the
+    // row sums of |B_kj|^2 only): 16 KiB per realization instead of 512 KiB
+    if (p.rsq) {
+      p.rsq[((b * C + cb) * 2 + part) * KU + u] = rs;
+      if ((unsigned)(u - JN * cb) < (unsigned)JN) reinterpret_cast<float*>(p.gdiag + b * KU + u)[part] = gd;
     }
     // ---- outputs staged in the (idle: every chunk of this realization has
     // landed and been consumed) ring as [user][column][re, im] with an odd row
@@ -1382,7 +1395,7 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
     float* stg = reinterpret_cast<float*>(ring);
     stamp();
 #pragma unroll 1
-    for (int pass = 0; pass < 2; ++pass) {
+    for (int pass = 0; pass < (p.rsq ? 1 : 2); ++pass) {
 #pragma unroll
       for (int jj = 0; jj < JN; ++jj) stg[u * SR + 2 * jj + part] = pass == 0 ? P[jj] * sa : A[jj];
       named_sync(BAR_MATH, NT);
@@ -1889,6 +1902,35 @@ __global__ void __launch_bounds__(NT, 1) lk_gram2_kernel(const __grid_constant__
 }
 }  // namespace gram2
 
+// ------------------------------------------------------------------ SINR ----
+// gamma_k = |B_kk|^2 / (sum_j |B_kj|^2 - |B_kk|^2 + sigma2), B = beta GX
+// (coupling_matrix + sinr_eq9, metrics.py:35-58) from the solver's per-block
+// row sums and diagonal; sum-SE in user order (as sinr_kernel).
+__global__ void __launch_bounds__(KU) lk_sinr_kernel(const double* __restrict__ rsq, const float2* __restrict__ gd,
+                                                     const double* __restrict__ beta, double sigma2,
+                                                     double* __restrict__ gamma, double* __restrict__ sum_se) {
+  const int64_t b = blockIdx.x;
+  const int k = threadIdx.x;
+  __shared__ double sse[KU];
+  const double s2 = beta[b] * beta[b];
+  double tot = 0.0;
+#pragma unroll
+  for (int q = 0; q < 2 * pc::C; ++q) tot += rsq[(b * 2 * pc::C + q) * KU + k];
+  tot *= s2;
+  const float2 d = gd[b * KU + k];
+  const double sig = (double)cabs2(d) * s2;
+  const double g = sig / ((tot - sig) + sigma2);
+  const double se = log2(1.0 + g);
+  if (gamma) gamma[b * KU + k] = g;
+  sse[k] = se;
+  __syncthreads();
+  if (k == 0) {
+    double t = 0.0;
+    for (int i = 0; i < KU; ++i) t += sse[i];
+    sum_se[b] = t;
+  }
+}
+
 // ------------------------------------------------------------------ host ----
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -2027,8 +2069,11 @@ int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi
   if (ncl > (pair ? 2 * B : B)) ncl = (int)(pair ? 2 * B : B);
   const int cl = pair ? pc::cl_size<true>() : pc::cl_size<false>();
   const char* uc = getenv("XL_LK_UNICAST");
-  pc::Params p{(const float2*)A, B, T, method, variant, xi, xi_b, (float2*)X, (float2*)GX, part, status, scratch,
-               g_lk_trace, (uc && uc[0] == '1') ? 1 : 0, 1, 1, 0};
+  // the GX buffer holds the SINR partials instead (lk_sinr): [B][8][2][K] doubles, then [B][K] float2
+  double* rsq = (double*)GX;
+  float2* gdiag = (float2*)(rsq + (size_t)B * pc::C * 2 * KU);
+  pc::Params p{(const float2*)A, B, T, method, variant, xi, xi_b, (float2*)X, (float2*)GX, part, rsq, gdiag,
+               status, scratch, g_lk_trace, (uc && uc[0] == '1') ? 1 : 0, 1, 1, 0};
   if (const char* sp = getenv("XL_LK_SPIN")) p.spin = sp[0] == '1';
   if (const char* ss = getenv("XL_LK_SS")) p.ss = ss[0] == '1';  // default 1: A from shared memory (measured faster than tcgen05.cp + TMEM)
   if (const char* mr = getenv("XL_LK_MMA_REPS")) p.mma_reps = atoi(mr) > 0 ? atoi(mr) : 1;
@@ -2048,6 +2093,15 @@ int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
   if (cudaLaunchKernelEx(&cfg, kern, p) != cudaSuccess) return check_launch("lk pcg launch");
   return check_launch("lk pcg");
+}
+
+int lk_sinr(const void* GX, const double* beta, int64_t B, double sigma2, double* gamma, double* sum_se,
+            cudaStream_t st) {
+  using namespace lk;
+  const double* rsq = (const double*)GX;
+  const float2* gdiag = (const float2*)(rsq + (size_t)B * pc::C * 2 * KU);
+  lk_sinr_kernel<<<(unsigned)B, KU, 0, st>>>(rsq, gdiag, beta, sigma2, gamma, sum_se);
+  return check_launch("lk sinr");
 }
 
 int lk_apply(const void* H, const void* X, const double* beta, int64_t B, int M, void* W, void* F, void* ws,

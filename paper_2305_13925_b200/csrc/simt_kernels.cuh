@@ -82,6 +82,9 @@ int lk_gram(const void* H, int64_t B, int M, double xi, const double* xi_b, void
 int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi, const double* xi_b, void* X,
              void* GX, double* part, int32_t* status, void* ws, cudaStream_t st);
 void lk_debug_trace(void* buf);
+// SINR / sum-SE from the K = 256 solver's partials (written into its GX buffer)
+int lk_sinr(const void* GX, const double* beta, int64_t B, double sigma2, double* gamma, double* sum_se,
+            cudaStream_t st);
 int lk_apply(const void* H, const void* X, const double* beta, int64_t B, int M, void* W, void* F, void* ws,
              cudaStream_t st);
 

@@ -301,6 +301,7 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
       if ((e = launch_cgemm<float>(false, EPI_BSCALE, H, sH, K, Xo, sK, K, W, sH, K, B, M, K, K, beta, 0, nullptr, st))) return e;
       if (F && (e = launch_cgemm<float>(false, EPI_STORE, H, sH, K, Xo, sK, K, F, sH, K, B, M, K, K, nullptr, 0, nullptr, st))) return e;
     }
+    if (lks) return lk_sinr(GX, beta, B, sigma2, gamma, sum_se, st);
     return launch_sinr<float>(GX, B, K, sigma2, gamma, nullptr, sum_se, st, beta);
   }
   if (tcp64) {

@@ -25,7 +25,7 @@ n = next((i for i, v in enumerate(t) if v == 0), len(t))
 labels = ["top", "synced", "built", "slot ready"]
 for it in range(T):
     labels += [f"it{it + 1} start", "scaled", "product", "update+rz"]
-labels += ["gx start", "gx computed", "X written", "GX written"]
+labels += ["gx start", "gx loaded", "gx computed", "X written", "GX written"]
 per = len(labels)
 for i in range(1, min(n, 2 * per)):
     print(f"{labels[i % per]:>12s} +{t[i] - t[i - 1]:8d} cycles")
