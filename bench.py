@@ -120,13 +120,6 @@ def roofline(M, K, T, method, dtype_bytes, B, kern_ms, path, peaks, traffic=None
          "roofline_precoders_per_s": 1.0 / max(t_flop / B, t_bytes / B),
          "kernel_ms": kern_ms, "bytes_per_precoder": bytes_per,
          "algorithmic_bytes_per_launch": B * bytes_per, "flops_per_precoder": flops_per}
-    if path == "tc3xfp16" and peaks.get("tf32"):
-        # SURVEY.md 8(d)'s convention, for comparison only: c64 priced as 3xTF32
-        # at the measured TF32 rate (the kernels do not run TF32)
-        p3 = peaks["tf32"] / 3.0
-        t_roof = max(flops_per / (p3 * 1e12), bytes_per / (peaks["hbm"] * 1e9))
-        r["survey_convention_3xtf32"] = {"tensor_peak_tflops": p3, "roofline_precoders_per_s": 1.0 / t_roof,
-                                         "frac": (B / kern_s) * t_roof}
     return r
 
 
