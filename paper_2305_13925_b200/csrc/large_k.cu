@@ -765,48 +765,19 @@ static_assert(Lay<false>::NS * Lay<false>::STAGE >= KU * (2 * JN + 1) * 4 &&
               "X / GX staging fits the ring");
 static_assert(Lay<true>::NS <= NSMAX && Lay<false>::NS <= NSMAX, "ring barriers");
 
-// ---- cta_group::2 forms (every tcgen05 op of the pair kernel uses them)
-__device__ __forceinline__ void mma2_w(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(id), "r"(acc));
-}
-__device__ __forceinline__ void commit2_mc_w(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
-          su32(bar)),
-      "h"(mask)
-      : "memory");
-}
+// ---- cta_group::2 forms: tc_ptx.cuh (mma2_w, commit2_mc_w, mapa_u32, mbar_arrive_peer, ...)
 template <bool PR>
 __device__ __forceinline__ void tmem_alloc512_g(uint32_t* slot) {
   if (PR) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    tmem_alloc_pair512(slot);
   } else {
     tmem_alloc512(slot);
   }
 }
 template <bool PR>
 __device__ __forceinline__ void tmem_free512_g(uint32_t t) {
-  if (PR) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(t));
+  if (PR) tmem_free_pair512(t);
   else tmem_free512(t);
-}
-__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-  return r;
-}
-// arrive on an mbarrier of another CTA of the cluster with the default
-// (CTA-scope) release, as CUTLASS's 2-SM UMMA pipelines signal the peer after
-// fence.proxy.async: what it publishes is this CTA's shared memory, read by the
-// pair's tensor cores.  A .release.cluster arrive costs a cluster-scope fence
-// per call (measured: a third of the pair W kernel's stall samples, and ~2 k
-// cycles per product in the pair solver's relays).
-__device__ __forceinline__ void mbar_arrive_peer(uint32_t cl_addr) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
 }
 // wait with acquire at cluster scope (the phase was completed from another CTA)
 __device__ __forceinline__ void bwait_cl(uint64_t* bar, uint32_t parity) {
@@ -1468,12 +1439,6 @@ struct Small {
 };
 static_assert(sizeof(Small) <= SMALL, "W2 small");
 
-__device__ __forceinline__ void mma2_ts_w(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
-      "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
-}
 __device__ __forceinline__ void tmem_st16u(uint32_t ta, const uint32_t* v) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
@@ -1592,14 +1557,14 @@ __global__ void __launch_bounds__(NT, 1) lk_w2_kernel(const __grid_constant__ CU
           mma2_ts_w(d2, ah, bil, ID2, 1);
           mma2_ts_w(d2, al, bih, ID2, 1);
         }
-        pc::commit2_mc_w(&sm->freed[s], 3);
-        if (kb == KU / BU - 1) pc::commit2_mc_w(&sm->acc_full[tt & 1], 3);
+        commit2_mc_w(&sm->freed[s], 3);
+        if (kb == KU / BU - 1) commit2_mc_w(&sm->acc_full[tt & 1], 3);
       }
     } else if (lane == 0) {  // relay: the follower's drain of tile tt - 2 -> the leader
-      const uint32_t lead_pfree = pc::mapa_u32(su32(&sm->pacc_free[0]), 0);
+      const uint32_t lead_pfree = mapa_u32(su32(&sm->pacc_free[0]), 0);
       for (int tt = 2; tt < ntile; ++tt) {
         bwait(&sm->acc_free[tt & 1], ((tt >> 1) - 1) & 1);
-        pc::mbar_arrive_peer(lead_pfree + 8u * (uint32_t)(tt & 1));
+        mbar_arrive_peer(lead_pfree + 8u * (uint32_t)(tt & 1));
       }
     }
   } else if (warp < W_EPI0) {  // converters: 8-antenna group grp of boxes g % 2 == par
@@ -1607,7 +1572,7 @@ __global__ void __launch_bounds__(NT, 1) lk_w2_kernel(const __grid_constant__ CU
     const int grp = cw & 3, par = cw >> 2;
     const float sz = pow2_scale(__uint_as_float(zmax[b]), 11);
     const int crow = lane >> 2, pair = lane & 3;
-    const uint32_t conv_addr = pc::mapa_u32(su32(&sm->conv[0]), 0);
+    const uint32_t conv_addr = mapa_u32(su32(&sm->conv[0]), 0);
     for (int g = par; g < nbox; g += 2) {
       const int s = g % NS;
       bwait(&sm->full[s], (g / NS) & 1);
@@ -1635,7 +1600,7 @@ __global__ void __launch_bounds__(NT, 1) lk_w2_kernel(const __grid_constant__ CU
       __syncwarp();
       if (lane == 0) {
         if (leader) mbar_arrive(&sm->conv[s]);
-        else pc::mbar_arrive_peer(conv_addr + 8u * (uint32_t)s);
+        else mbar_arrive_peer(conv_addr + 8u * (uint32_t)s);
       }
     }
   } else {  // epilogue warpgroup: lane quadrant q, all 64 antennas of a tile in two halves
@@ -1791,20 +1756,20 @@ __global__ void __launch_bounds__(NT, 1) lk_gram2_kernel(const __grid_constant__
           const uint32_t acc = (c | ks) != 0;
           const uint64_t ah = sdesc(sa + 2 * ks * SG, SG, 128), al = sdesc(sa + 2 * ks * SG + SG / 2, SG, 128);
           const uint64_t bh = sdesc(sbb + 2 * ks * SG, SG, 128), bl = sdesc(sbb + 2 * ks * SG + SG / 2, SG, 128);
-          pc::mma2_w(tmem, ah, bh, ID2, acc);
-          pc::mma2_w(tmem, ah, bl, ID2, 1);
-          pc::mma2_w(tmem, al, bh, ID2, 1);
+          mma2_w(tmem, ah, bh, ID2, acc);
+          mma2_w(tmem, ah, bl, ID2, 1);
+          mma2_w(tmem, al, bh, ID2, 1);
         }
-        pc::commit2_mc_w(&sm->freed[s], 3);
+        commit2_mc_w(&sm->freed[s], 3);
       }
-      pc::commit2_mc_w(&sm->done, 3);
+      commit2_mc_w(&sm->done, 3);
     }
   } else {
     const int cw = warp - W_CONV0;
     const bool active = cw < 4 * nbx;  // group cw & 3 of single cw >> 2
     bool have = fixup != 0, over = false;
     float zm = 0.0f;
-    const uint32_t conv_addr = pc::mapa_u32(su32(&sm->conv[0]), 0);
+    const uint32_t conv_addr = mapa_u32(su32(&sm->conv[0]), 0);
     for (int c = 0; c < nch; ++c) {
       const int s = c % NS;
       bwait(&sm->full[s], (c / NS) & 1);
@@ -1832,7 +1797,7 @@ __global__ void __launch_bounds__(NT, 1) lk_gram2_kernel(const __grid_constant__
       __syncwarp();
       if (lane == 0) {
         if (leader) mbar_arrive(&sm->conv[s]);
-        else pc::mbar_arrive_peer(conv_addr + 8u * (uint32_t)s);
+        else mbar_arrive_peer(conv_addr + 8u * (uint32_t)s);
       }
     }
     over = __any_sync(0xffffffffu, over);
@@ -1851,7 +1816,7 @@ __global__ void __launch_bounds__(NT, 1) lk_gram2_kernel(const __grid_constant__
     float szk[2];
     {
       float peer_sz;
-      asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(peer_sz) : "r"(pc::mapa_u32(su32(&sm->sz), v ^ 1u)));
+      asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(peer_sz) : "r"(mapa_u32(su32(&sm->sz), v ^ 1u)));
       szk[v] = sm->sz;
       szk[v ^ 1u] = peer_sz;
     }

@@ -48,6 +48,9 @@ constexpr int SMALL = 2048;
 constexpr int SMEM = NS * SB + SMALL;
 static_assert(SMEM <= 227 * 1024, "stream smem");
 constexpr int BAR_CONV = 1;
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 struct Small {
   uint64_t raw_full[NS], conv_full[NS], stage_free[NS];
@@ -472,6 +475,229 @@ __global__ void __launch_bounds__(NT, 1) w_kernel(const float2* __restrict__ H, 
   }
 }
 
+// ---------------------------------------------------------- W, CTA pairs ----
+// w_kernel as cta_group::2 pairs (the default; XL_STREAM_W2=0 keeps w_kernel):
+// the two output halves of a realization form a cluster of two and multiply
+// as one M = 256 MMA (each CTA's A = its half's Xe^T rows, written into its
+// own TMEM with tcgen05.st), N = 64 antennas split 32 / 32: each CTA lands and
+// converts only its 32 antennas of every chunk, the pair's tensor cores read
+// both halves.  Converter warps only convert (the follower's signal the
+// leader's MMA issuer with CTA-scope peer arrives); a dedicated epilogue
+// warpgroup drains TMEM and stores W.
+namespace w2 {
+constexpr int HSB = SB / 2;               // 32 KiB: this CTA's 32 antennas of a chunk
+constexpr int NS2 = 6;                    // ring depth (192 KiB)
+constexpr int W_EPI0 = W_CONV0 + NCONV, NEPI = 4;
+constexpr int NT2 = 32 * (W_EPI0 + NEPI);  // 448 threads
+constexpr int SMEM2 = NS2 * HSB + SMALL;
+static_assert(SMEM2 <= 227 * 1024, "stream W2 smem");
+static_assert(KU * 64 * (int)sizeof(float2) <= NS2 * HSB, "X columns staged in the ring");
+constexpr uint32_t ID_W2 = idesc(256, CH, 0, 0);
+
+struct Small2 {
+  uint64_t raw_full[NS2], conv_full[NS2], stage_free[NS2];
+  uint64_t acc_full[2], acc_free[2], pacc_free[2];
+  uint64_t xs_done;
+  uint32_t tmem_slot;
+  float rmax[2][128];
+};
+static_assert(sizeof(Small2) <= SMALL, "stream W2 small region");
+
+__device__ __forceinline__ void tmem_st4(uint32_t ta, const uint32_t (&v)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ta), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+               "r"(v[3])
+               : "memory");
+}
+
+__global__ void __launch_bounds__(NT2, 1) w2_kernel(const float2* __restrict__ H, int M, const float* __restrict__ szv,
+                                                    const float2* __restrict__ X, const double* __restrict__ beta,
+                                                    float* __restrict__ W, float* __restrict__ F) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* ring = smem;
+  Small2* sm = reinterpret_cast<Small2*>(smem + NS2 * HSB);
+  const int64_t b = (int64_t)blockIdx.x >> 1;
+  const int half = blockIdx.x & 1;  // == cluster rank
+  const bool leader = half == 0;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nch = M / CH;
+  if (tid == 0) {
+    for (int s = 0; s < NS2; ++s) {
+      mbar_init(&sm->raw_full[s], 1);
+      mbar_init(&sm->conv_full[s], 2 * 4);  // leader: the 4 converter warps of the chunk in each CTA
+      mbar_init(&sm->stage_free[s], 1);
+    }
+    for (int j = 0; j < 2; ++j) {
+      mbar_init(&sm->acc_full[j], 1);
+      mbar_init(&sm->acc_free[j], NEPI);  // the local epilogue warps
+      mbar_init(&sm->pacc_free[j], 1);    // leader: the follower's epilogue (relayed)
+    }
+    mbar_init(&sm->xs_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == W_MMA) tmem_alloc_pair512(&sm->tmem_slot);
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = sm->tmem_slot;
+  const float sz = szv[b];
+  // ---- this half's 64 columns of X into the ring (bulk copies), then each
+  // converter thread (row r, user half kh) writes its split, row-scaled Xe^T
+  // entries straight into TMEM: column i of the 128 (hi) / 128 (lo) A columns
+  // holds components (2i, 2i + 1) = input user i
+  float2* xs = reinterpret_cast<float2*>(ring);  // xs[i * 64 + jl]
+  if (tid == 32 * W_PROD) {
+    constexpr uint32_t RB = 64 * sizeof(float2);
+    mbar_expect_tx(&sm->xs_done, KU * RB);
+    const float2* xsrc = X + b * (int64_t)KU * KU + 64 * half;
+    const uint64_t pol = policy_evict_first();
+    for (int i = 0; i < KU; ++i) bulk_g2s(xs + i * 64, xsrc + (int64_t)i * KU, RB, &sm->xs_done, pol);
+  }
+  float srow = 1.0f;
+  const int q = warp & 3;
+  if (warp >= W_CONV0 && warp < W_EPI0) {
+    const int cw = warp - W_CONV0, kh = cw >> 2;
+    const int r = 32 * q + lane;
+    const int jl = r >> 1;
+    const bool odd = (128 * half + r) & 1;
+    mbar_wait(&sm->xs_done, 0);
+    float mx = 0.0f;
+#pragma unroll 8
+    for (int i = 64 * kh; i < 64 * kh + 64; ++i) {
+      const float2 v = xs[i * 64 + jl];
+      mx = fmaxf(mx, fmaxf(fabsf(v.x), fabsf(v.y)));
+    }
+    sm->rmax[kh][r] = mx;
+    named_sync(BAR_CONV, 32 * NCONV);
+    srow = pow2_scale(fmaxf(sm->rmax[0][r], sm->rmax[1][r]), 14);
+    const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16);
+#pragma unroll 2
+    for (int i0 = 64 * kh; i0 < 64 * kh + 64; i0 += 4) {
+      uint32_t hw[4], lw[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 v = xs[(i0 + u) * 64 + jl];
+        split2((odd ? v.y : v.x) * srow, (odd ? v.x : -v.y) * srow, hw[u], lw[u]);
+      }
+      tmem_st4(ta + T_AH + i0, hw);
+      tmem_st4(ta + T_AL + i0, lw);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  if (warp >= W_EPI0) {  // the epilogue warps need their rows' scales too
+    const int r = 32 * q + lane;
+    mbar_wait(&sm->xs_done, 0);
+    float mx = 0.0f;
+    for (int i = 0; i < KU; ++i) {
+      const float2 v = xs[i * 64 + (r >> 1)];
+      mx = fmaxf(mx, fmaxf(fabsf(v.x), fabsf(v.y)));
+    }
+    srow = pow2_scale(mx, 14);
+  }
+  tc_before();
+  cluster_sync_all();  // both CTAs' A rows are in TMEM (and every barrier initialised); xs is dead
+  tc_after();
+
+  if (warp == W_PROD) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      const char* src = reinterpret_cast<const char*>(H + (b * (int64_t)M + (CH / 2) * half) * KU);
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % NS2;
+        if (c >= NS2) mbar_wait(&sm->stage_free[s], ((c / NS2) - 1) & 1);
+        mbar_expect_tx(&sm->raw_full[s], HSB);
+        bulk_g2s(ring + s * HSB, src + (int64_t)c * SB, HSB, &sm->raw_full[s], pol);
+      }
+    }
+  } else if (warp == W_MMA) {
+    if (leader) {
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % NS2, jb = c & 1;
+        if (c >= 2) {
+          mbar_wait(&sm->acc_free[jb], ((c >> 1) - 1) & 1);
+          mbar_wait_cl(&sm->pacc_free[jb], ((c >> 1) - 1) & 1);
+        }
+        mbar_wait_cl(&sm->conv_full[s], (c / NS2) & 1);
+        tc_after();
+        const uint32_t zh = su32(ring + s * HSB), zl = zh + CMA;
+        const uint32_t d = tmem + T_ACC + CH * jb;
+#pragma unroll
+        for (int ks = 0; ks < NC / 16; ++ks) {
+          const uint64_t dzh = sdesc(zh + 256 * ks, 128, GS), dzl = sdesc(zl + 256 * ks, 128, GS);
+          mma2_ts_w(d, tmem + T_AH + 8 * ks, dzh, ID_W2, ks != 0);
+          mma2_ts_w(d, tmem + T_AH + 8 * ks, dzl, ID_W2, 1);
+          mma2_ts_w(d, tmem + T_AL + 8 * ks, dzh, ID_W2, 1);
+        }
+        commit2_mc_w(&sm->stage_free[s], 3);
+        commit2_mc_w(&sm->acc_full[jb], 3);
+      }
+    } else if (lane == 0) {  // relay: the follower's drain of chunk c - 2 -> the leader
+      const uint32_t lead_pfree = mapa_u32(su32(&sm->pacc_free[0]), 0);
+      for (int c = 2; c < nch; ++c) {
+        mbar_wait(&sm->acc_free[c & 1], ((c >> 1) - 1) & 1);
+        mbar_arrive_peer(lead_pfree + 8u * (uint32_t)(c & 1));
+      }
+    }
+  } else if (warp < W_EPI0) {  // converters: 8-antenna group cw & 3 of chunks c % 2 == cw >> 2
+    const int cw = warp - W_CONV0;
+    const int grp = cw & 3, par = cw >> 2;
+    const uint32_t conv_addr = mapa_u32(su32(&sm->conv_full[0]), 0);
+    for (int c = par; c < nch; c += 2) {
+      const int s = c % NS2;
+      mbar_wait(&sm->raw_full[s], (c / NS2) & 1);
+      uint8_t* gb = ring + s * HSB + grp * GS;
+      float4 v[NIT];
+      load_group(gb, lane, v);
+      store_group(gb, lane, v, sz, 1.0f);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(&sm->conv_full[s]);
+        else mbar_arrive_peer(conv_addr + 8u * (uint32_t)s);
+      }
+    }
+  } else {  // epilogue warpgroup: lane quadrant q, the chunk's 64 antennas in two halves
+    const int r = 32 * q + lane;
+    const int m = 128 * half + r;
+    const double bt = beta[b];
+    const float wmul = (float)(bt / ((double)srow * (double)sz));
+    const float fmul = 1.0f / (srow * sz);
+    const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16) + T_ACC;
+    for (int c = 0; c < nch; ++c) {
+      const int jb = c & 1;
+      mbar_wait_cl(&sm->acc_full[jb], (c >> 1) & 1);
+      tc_after();
+#pragma unroll 1
+      for (int hh = 0; hh < 2; ++hh) {
+        float v[32];
+        tmem_ld16(tq + CH * jb + 32 * hh, v);
+        tmem_ld16(tq + CH * jb + 32 * hh + 16, v + 16);
+        tmem_wait_ld();
+        if (hh == 1) {
+          tc_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm->acc_free[jb]);
+        }
+        const int64_t n0 = (int64_t)c * CH + 32 * hh;
+        float* wp = W + (b * (int64_t)M + n0) * NC + m;
+#pragma unroll
+        for (int n = 0; n < 32; ++n) __stcs(wp + (int64_t)n * NC, v[n] * wmul);
+        if (F) {
+          float* fp = F + (b * (int64_t)M + n0) * NC + m;
+#pragma unroll
+          for (int n = 0; n < 32; ++n) __stcs(fp + (int64_t)n * NC, v[n] * fmul);
+        }
+      }
+    }
+  }
+  tc_before();
+  cluster_sync_all();  // no peer arrive / multicast commit targets an exited CTA
+  if (warp == W_MMA) {
+    tc_after();
+    tmem_free_pair512(tmem);
+  }
+}
+}  // namespace w2
+
 }  // namespace stc
 
 bool stc_supported(int dtype, int M, int K) {
@@ -499,6 +725,26 @@ int stc_gram(const void* H, int64_t B, int M, int K, double xi, const double* xi
 int stc_apply(const void* H, const void* X, const double* beta, const float* sz, int64_t B, int M, int K, void* W,
               void* F, cudaStream_t st) {
   if (!stc_supported(XL_C64, M, K)) { set_error("stream W: unsupported shape"); return XL_ERR_UNSUPPORTED; }
+  const char* w2 = getenv("XL_STREAM_W2");  // "0": the single-CTA w_kernel (A/B, tests)
+  if (!(w2 && w2[0] == '0')) {
+    cudaFuncSetAttribute(stc::w2::w2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, stc::w2::SMEM2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * B), 1, 1);
+    cfg.blockDim = dim3(stc::w2::NT2, 1, 1);
+    cfg.dynamicSmemBytes = stc::w2::SMEM2;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, stc::w2::w2_kernel, (const float2*)H, M, sz, (const float2*)X, beta, (float*)W,
+                           (float*)F) != cudaSuccess)
+      return check_launch("stream W2 launch");
+    return check_launch("stream W2");
+  }
   cudaFuncSetAttribute(stc::w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, stc::SMEM);
   stc::w_kernel<<<(unsigned)(2 * B), stc::NT, stc::SMEM, st>>>((const float2*)H, M, sz, (const float2*)X, beta,
                                                                (float*)W, (float*)F);

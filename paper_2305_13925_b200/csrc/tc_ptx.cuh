@@ -230,3 +230,64 @@ __device__ __forceinline__ void tmem_cp_w(uint32_t taddr, uint64_t desc) {
           taddr),
       "l"(desc));
 }
+
+// ------------------------------------------------ cta_group::2 (CTA pairs) ----
+// A kernel that issues one cta_group::2 tcgen05 op issues all of them that way
+// (alloc, mma, commit, dealloc); the even CTA of the pair issues the MMAs.
+__device__ __forceinline__ void mma2_w(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void mma2_ts_w(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
+}
+// arrive on the mbarrier at this offset in every CTA of `mask` when the
+// issuing thread's prior cta_group::2 tcgen05 operations complete
+__device__ __forceinline__ void commit2_mc_w(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
+          su32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_pair512(uint32_t* slot) {  // one warp of each CTA of the pair
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(slot)));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_free_pair512(uint32_t t) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(t));
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// arrive on an mbarrier of another CTA of the cluster with the default
+// (CTA-scope) release, as CUTLASS's 2-SM UMMA pipelines signal the peer after
+// fence.proxy.async: what it publishes is this CTA's shared memory, read by the
+// pair's tensor cores.  A .release.cluster arrive costs a cluster-scope fence
+// per call (measured: a third of the pair W kernel's stall samples, and ~2 k
+// cycles per product in the pair solver's relays).
+__device__ __forceinline__ void mbar_arrive_peer(uint32_t cl_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
+}
+// mbar_wait with acquire at cluster scope (the phase completes from the peer)
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0, spins = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(done)
+        : "r"(su32(bar)), "r"(parity), "r"(0x989680u)
+        : "memory");
+    if (++spins > (1u << 24)) asm volatile("trap;");
+  } while (!done);
+}
