@@ -43,6 +43,7 @@
 #include <stdlib.h>
 
 #include "xl_common.cuh"
+#include "simt_kernels.cuh"
 
 namespace xl {
 namespace lk {
@@ -1976,15 +1977,23 @@ size_t lk_ws_bytes(int64_t B) {
   return 4 * al((size_t)B * 4) + (size_t)lk::pc::MAX_SLOTS * lk::pc::SLOT_BYTES;
 }
 
-int lk_gram(const void* H, int64_t B, int M, double xi, const double* xi_b, void* A, void* ws, cudaStream_t st) {
-  using namespace lk;
+LkScratch lk_scratch(void* ws, int64_t B) {
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  float* sz = (float*)ws;
-  int* rflag = (int*)((char*)ws + al((size_t)B * 4));
+  char* p = (char*)ws;
+  LkScratch r;
+  r.sz = (float*)p;
+  r.rflag = (int*)(p + al((size_t)B * 4));
+  r.zmax = (unsigned*)(p + 2 * al((size_t)B * 4));
+  r.slots = (uint8_t*)(p + 4 * al((size_t)B * 4));
+  return r;
+}
+
+int lk_gram(const void* H, int64_t B, int M, double xi, const double* xi_b, void* A, float* sz, int* rflag,
+            unsigned* zmax, cudaStream_t st) {
+  using namespace lk;
   CUtensorMap pmap, smap;
   if (int e = make_hmap(&pmap, H, B, M, 2 * gram::BLK, gram::CH)) return e;
   if (int e = make_hmap(&smap, H, B, M, gram::BLK, gram::CH)) return e;
-  unsigned* zmax = (unsigned*)((char*)ws + 2 * al((size_t)B * 4));
   if (cudaMemsetAsync(rflag, 0, (size_t)B * sizeof(int), st) != cudaSuccess) return check_launch("lk flags");
   if (cudaMemsetAsync(zmax, 0, (size_t)B * sizeof(unsigned), st) != cudaSuccess) return check_launch("lk zmax init");
   const char* g2 = getenv("XL_LK_GRAM2");  // "0": the 5-CTA single-CTA-MMA Gram (A/B, tests)
@@ -2024,10 +2033,8 @@ static long long* g_lk_trace = nullptr;
 void lk_debug_trace(void* p) { g_lk_trace = (long long*)p; }
 
 int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi, const double* xi_b, void* X,
-             void* GX, double* part, int32_t* status, void* ws, cudaStream_t st) {
+             void* GX, double* part, int32_t* status, uint8_t* scratch, cudaStream_t st) {
   using namespace lk;
-  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  uint8_t* scratch = (uint8_t*)ws + 4 * al((size_t)B * 4);
   const bool pair = lk_pair();
   int ncl = pair ? lk_clusters<true>() : lk_clusters<false>();
   if (ncl > pc::MAX_SLOTS) ncl = pc::MAX_SLOTS;
@@ -2069,11 +2076,9 @@ int lk_sinr(const void* GX, const double* beta, int64_t B, double sigma2, double
   return check_launch("lk sinr");
 }
 
-int lk_apply(const void* H, const void* X, const double* beta, int64_t B, int M, void* W, void* F, void* ws,
-             cudaStream_t st) {
+int lk_apply(const void* H, const void* X, const double* beta, int64_t B, int M, void* W, void* F,
+             const unsigned* zmax, cudaStream_t st) {  // zmax: from lk_gram
   using namespace lk;
-  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  const unsigned* zmax = (const unsigned*)((char*)ws + 2 * al((size_t)B * 4));  // from lk_gram
   CUtensorMap map;
   const char* w2 = getenv("XL_LK_W2");  // "0": the single-CTA W kernel (A/B, tests)
   if (!(w2 && w2[0] == '0')) {  // CTA pairs: each CTA lands / converts half of every box

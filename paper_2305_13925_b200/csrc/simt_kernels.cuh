@@ -78,15 +78,24 @@ int tc_pcg(int method, int variant, const void* A, int64_t B, int K, int T, void
 // large_k.cu: K = 256 complex64 -- streaming tcgen05 Gram / W and the 8-CTA cluster Jac-PCG
 bool lk_supported(int dtype, int M, int K);
 size_t lk_ws_bytes(int64_t B);
-int lk_gram(const void* H, int64_t B, int M, double xi, const double* xi_b, void* A, void* ws, cudaStream_t st);
+// per-realization scales / range flags / exact maxima, then the solver's cluster slots
+struct LkScratch {
+  float* sz;
+  int* rflag;
+  unsigned* zmax;
+  uint8_t* slots;
+};
+LkScratch lk_scratch(void* ws, int64_t B);
+int lk_gram(const void* H, int64_t B, int M, double xi, const double* xi_b, void* A, float* sz, int* rflag,
+            unsigned* zmax, cudaStream_t st);
 int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi, const double* xi_b, void* X,
-             void* GX, double* part, int32_t* status, void* ws, cudaStream_t st);
+             void* GX, double* part, int32_t* status, uint8_t* slots, cudaStream_t st);
 void lk_debug_trace(void* buf);
 // SINR / sum-SE from the K = 256 solver's partials (written into its GX buffer)
 int lk_sinr(const void* GX, const double* beta, int64_t B, double sigma2, double* gamma, double* sum_se,
             cudaStream_t st);
-int lk_apply(const void* H, const void* X, const double* beta, int64_t B, int M, void* W, void* F, void* ws,
-             cudaStream_t st);
+int lk_apply(const void* H, const void* X, const double* beta, int64_t B, int M, void* W, void* F,
+             const unsigned* zmax, cudaStream_t st);
 
 // dmma.cu: batched complex128 GEMM on the FP64 tensor cores (row-major;
 // opA 0 = N, 1 = conjugate transpose; opB 0 = N, 1 = transpose; epi 0 store,

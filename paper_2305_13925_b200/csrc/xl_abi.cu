@@ -190,6 +190,78 @@ size_t xl_rzf_general_workspace_bytes(int dtype, int method, int64_t B, int32_t 
   return general_ws(dtype, B, M, K);
 }
 
+// K = 256 complex64 Jac-PCG / CG (no telemetry): the batch in chunks whose
+// kernels overlap across two streams -- the cluster solver of chunk i (a
+// persistent grid of 4-CTA clusters on 132 of the 148 SMs, latency- and
+// shared-memory-bound) runs while the Gram of chunk i + 1 and the beta / W /
+// SINR of chunk i - 1 fill the remaining SMs and the solver's tail waves.
+// XL_LK_PIPE=0: one chunk (the three kernels back to back).
+static int lk_pipeline(int method, int variant, const void* H, int64_t B, int32_t M, double xi,
+                       const double* xi_b, double power, int32_t T, double sigma2, void* W, void* F, double* beta,
+                       double* gamma, double* sum_se, void* Xo, int32_t* status, void* A, void* GX, double* part,
+                       void* tcws, cudaStream_t st) {
+  constexpr int K = 256, NP = 8;  // part entries per realization (one per 32-column block)
+  const LkScratch sc = lk_scratch(tcws, B);
+  const size_t oH = (size_t)M * K * 8, oK = (size_t)K * K * 8;
+  int64_t Bc = B;
+  const char* pe = getenv("XL_LK_PIPE");
+  if (!(pe && pe[0] == '0') && B >= 1024) Bc = B / 8 >= 512 ? (B + 7) / 8 : 512;
+  const int64_t n = (B + Bc - 1) / Bc;
+  auto gram = [&](int64_t b0, int64_t nb, cudaStream_t s) {
+    return lk_gram((const char*)H + b0 * oH, nb, M, xi, xi_b ? xi_b + b0 : nullptr, (char*)A + b0 * oK, sc.sz + b0,
+                   sc.rflag + b0, sc.zmax + b0, s);
+  };
+  auto solve = [&](int64_t b0, int64_t nb, cudaStream_t s) {
+    return lk_solve(method, variant, (const char*)A + b0 * oK, nb, T, xi, xi_b ? xi_b + b0 : nullptr,
+                    (char*)Xo + b0 * oK, (char*)GX + b0 * oK, part + b0 * NP, status + b0, sc.slots, s);
+  };
+  auto finish = [&](int64_t b0, int64_t nb, cudaStream_t s) {
+    int e;
+    if ((e = launch_beta_from_partials(nb, part + b0 * NP, NP, power, beta + b0, status + b0, s))) return e;
+    if ((e = lk_apply((const char*)H + b0 * oH, (const char*)Xo + b0 * oK, beta + b0, nb, M, (char*)W + b0 * oH,
+                      F ? (char*)F + b0 * oH : nullptr, sc.zmax + b0, s)))
+      return e;
+    return lk_sinr((char*)GX + b0 * oK, beta + b0, nb, sigma2, gamma ? gamma + b0 * K : nullptr, sum_se + b0, s);
+  };
+  int e;
+  if (n == 1) {
+    if ((e = gram(0, B, st)) || (e = solve(0, B, st))) return e;
+    return finish(0, B, st);
+  }
+  // a second stream and events per host thread (fork / join also inside graph capture)
+  static thread_local cudaStream_t aux = nullptr;
+  static thread_local cudaEvent_t ev[2 * 8 + 2];
+  static thread_local int dev_aux = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (aux == nullptr || dev_aux != dev) {
+    if (cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking) != cudaSuccess) return check_launch("lk aux stream");
+    for (auto& x : ev)
+      if (cudaEventCreateWithFlags(&x, cudaEventDisableTiming) != cudaSuccess) return check_launch("lk events");
+    dev_aux = dev;
+  }
+  cudaEvent_t *ev_g = ev, *ev_p = ev + 8, ev_fork = ev[16], ev_join = ev[17];
+  if (cudaEventRecord(ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(aux, ev_fork, 0) != cudaSuccess)
+    return check_launch("lk fork");
+  if ((e = gram(0, Bc, st))) return e;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t b0 = i * Bc, nb = B - b0 < Bc ? B - b0 : Bc;
+    if (i > 0 && cudaStreamWaitEvent(st, ev_g[i], 0) != cudaSuccess) return check_launch("lk wait gram");
+    if ((e = solve(b0, nb, st))) return e;
+    if (cudaEventRecord(ev_p[i], st) != cudaSuccess) return check_launch("lk record solve");
+    if (i + 1 < n) {
+      const int64_t b1 = b0 + Bc, nb1 = B - b1 < Bc ? B - b1 : Bc;
+      if ((e = gram(b1, nb1, aux))) return e;
+      if (cudaEventRecord(ev_g[i + 1], aux) != cudaSuccess) return check_launch("lk record gram");
+    }
+    if (cudaStreamWaitEvent(aux, ev_p[i], 0) != cudaSuccess) return check_launch("lk wait solve");
+    if ((e = finish(b0, nb, aux))) return e;
+  }
+  if (cudaEventRecord(ev_join, aux) != cudaSuccess || cudaStreamWaitEvent(st, ev_join, 0) != cudaSuccess)
+    return check_launch("lk join");
+  return XL_SUCCESS;
+}
+
 static void* g_dbg_gram = nullptr;
 void xl_debug_set_gram_out(void* A) { g_dbg_gram = A; }
 void xl_debug_lk_trace(void* buf) { lk_debug_trace(buf); }
@@ -227,10 +299,14 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   void* Xo = X ? X : Xw;
   const xl_stream_t stream = (xl_stream_t)st;
   int e;
+  if (lkp && !telemetry && method != XL_DIRECT)
+    return lk_pipeline(method, variant, H, B, M, xi, xi_per_batch, power, T, sigma2, W, F, beta, gamma, sum_se, Xo,
+                       status, A, sw, part, tcws, st);
   const int64_t Bc = tc ? tc_chunk_size(dtype, B, M, K) : B;
   const int64_t oH = (int64_t)M * K * (int64_t)cs, oK = (int64_t)K * K * (int64_t)cs;
   if (lkp) {  // K = 256: upper-triangular tcgen05 tiles, A emitted from TMEM
-    if ((e = lk_gram(H, B, M, xi, xi_per_batch, A, tcws, st))) return e;
+    const LkScratch ls = lk_scratch(tcws, B);
+    if ((e = lk_gram(H, B, M, xi, xi_per_batch, A, ls.sz, ls.rflag, ls.zmax, st))) return e;
   } else if (sc) {  // streaming tcgen05 Gram, A emitted from TMEM
     if ((e = stc_gram(H, B, M, K, xi, xi_per_batch, szb, A, rflag, st))) return e;
   } else if (tc) {
@@ -246,7 +322,7 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   // W = beta H X on the tensor cores, per sub-batch (the split rows are rebuilt:
   // the Gram sub-batches have overwritten them)
   auto tc_w = [&]() -> int {
-    if (lkp) return lk_apply(H, Xo, beta, B, M, W, F, tcws, st);
+    if (lkp) return lk_apply(H, Xo, beta, B, M, W, F, lk_scratch(tcws, B).zmax, st);
     if (sc) return stc_apply(H, Xo, beta, szb, B, M, K, W, F, st);
     for (int64_t b0 = 0; b0 < B; b0 += Bc) {
       const int64_t nb = B - b0 < Bc ? B - b0 : Bc;
@@ -266,7 +342,9 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   const int np = gemm_tiles(K, K);
   void* GX = sw;  // the solver workspace is free again (>= B K K)
   if (lks) {
-    if ((e = lk_solve(method, variant, A, B, T, xi, xi_per_batch, Xo, GX, part, status, tcws, st))) return e;
+    if ((e = lk_solve(method, variant, A, B, T, xi, xi_per_batch, Xo, GX, part, status, lk_scratch(tcws, B).slots,
+                      st)))
+      return e;
   } else if (cpc) {
     if ((e = cpcg_solve(method, variant, A, B, K, T, xi, xi_per_batch, Xo, GX, part, status, st))) return e;
   } else if (tcp) {
