@@ -333,12 +333,15 @@ def main(argv=None):
     first, B = rank_batch(a.scaling, total, world, rank)
     # cfg4 (configs[3]): generated on device in chunks of 2048 per GPU inside the
     # step (65536 do not fit HBM at once: 256 GiB); other configs: the rank's
-    # batch is resident in HBM, precoded in sub-batches of at most 16 GiB of H
+    # batch is resident in HBM, precoded in one call or in sub-batches (below)
     gen_in_step = wl.chunk is not None
     if gen_in_step:
         sub = min(wl.chunk, B)
     else:
-        sub = B if B * M * K * csz <= 16 * 2**30 else 2048
+        # one call per step while H, W and the K x K state fit comfortably in
+        # HBM (cfg5 c64: 32 GiB each of H and W); otherwise 2048-realization calls
+        sub = B if B * M * K * csz <= 32 * 2**30 and dt == torch.complex64 else (
+            B if B * M * K * csz <= 16 * 2**30 else 2048)
     assert B % sub == 0, "batch must be a multiple of the sub-batch"
     alpha, power = wl.alpha(), wl.power()
     lib = L.lib()
