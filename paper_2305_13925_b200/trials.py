@@ -68,43 +68,69 @@ def default_xi(K: int, snr_db: float) -> float:
     return K / 10.0 ** (snr_db / 10.0)
 
 
+_SIDE = {}
+
+
+def _side_streams(device, n: int):
+    """n cached side streams of a device (created once, reused by every call)."""
+    key = torch.device(device).index
+    lst = _SIDE.setdefault(key, [])
+    while len(lst) < n:
+        lst.append(torch.cuda.Stream(device=device))
+    return lst[:n]
+
+
 def se_grid_batched(H: torch.Tensor, points, variant: str = "textbook", sigma2: float = 1.0,
                     xi_rule=default_xi, keep_W: bool = False, timed: bool = False,
-                    check: bool = True, stream=None) -> SeGrid:
+                    check: bool = True, stream=None, lanes: int = 2) -> SeGrid:
     """Run every grid point on the same batch H (paired draws).
 
     ``points``: GridPoints (see :func:`grid_points`).  ``timed`` records the
     device time of every point's precoder call with CUDA events on the
-    launching stream.  ``check`` raises the reference exception of the first
+    stream it runs on.  ``check`` raises the reference exception of the first
     failing realization of any point (after the range re-run of rzf_batched).
+    ``lanes``: the points alternate over this many streams (the calling one
+    plus cached side streams, forked from and joined back into it), so a
+    point's last partial wave of CTAs overlaps the next point's first.
     """
     B, M, K = H.shape
     grid = SeGrid(points=list(points))
     outs = {}
     evs = {}
-    shared_W = None
     st = stream if stream is not None else torch.cuda.current_stream(H.device)
-    for p in grid.points:
+    streams = [st] + _side_streams(H.device, max(1, int(lanes)) - 1)
+    shared_W = [None] * len(streams)   # one scratch W per stream (W of a point is discarded)
+    fork = torch.cuda.Event()
+    fork.record(st)
+    for s in streams[1:]:
+        s.wait_event(fork)
+    for ip, p in enumerate(grid.points):
+        lane = ip % len(streams)
+        sp = streams[lane]
         snr_lin = 10.0 ** (p.snr_db / 10.0)
         power = sigma2 * snr_lin
         xi = xi_rule(K, p.snr_db)
         if timed:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-        if keep_W or shared_W is None:
+            e0.record(sp)
+        if keep_W or shared_W[lane] is None:
             o = BT.alloc_outputs(H, want_gamma=False)
             if not keep_W:
-                shared_W = o.W
-        else:   # W of a point is discarded: one scratch W serves every point
+                shared_W[lane] = o.W
+        else:
             f64 = dict(dtype=torch.float64, device=H.device)
-            o = BT.PrecoderBatch(W=shared_W, beta=torch.empty(B, **f64), sum_se=torch.empty(B, **f64),
+            o = BT.PrecoderBatch(W=shared_W[lane], beta=torch.empty(B, **f64), sum_se=torch.empty(B, **f64),
                                  status=torch.empty(B, dtype=torch.int32, device=H.device))
         BT.rzf_batched(H, xi, power, method=p.method, T=max(p.T, 1), variant=variant,
-                       sigma2=sigma2, out=o, check=False, stream=stream)
+                       sigma2=sigma2, out=o, check=False, stream=sp)
         if timed:
-            e1.record(st)
+            e1.record(sp)
             evs[p] = (e0, e1)
         outs[p] = o
+    for s in streams[1:]:   # join: everything after this call is ordered after every point
+        j = torch.cuda.Event()
+        j.record(s)
+        st.wait_event(j)
     if check:
         import numpy as np
         from . import _lib as L
