@@ -169,3 +169,26 @@ def test_k128_edge_shapes(B, M, T):
         Gr, br, gr, s = O.precoder_and_se(Hq[b], xi, 10.0, 1.0, "jacpcg", T, "textbook")
         assert relf(out.W[b].cpu().numpy(), Gr) <= 1e-4, (B, M, T, b)
         assert abs(out.sum_se[b].item() - s) <= 1e-4 * abs(s)
+
+
+def test_k128_pair_w_kernel_matches_single_cta():
+    """The K = 128 W product as a cta_group::2 pair (default) against the
+    single-CTA w_kernel (XL_STREAM_W2=0): W / F within fp32 rounding, sum-SE too."""
+    import os
+    wl = X.CONFIGS["cfg4"]
+    H = X.generate_channels(wl.model, seed=3, first=9, B=6, dtype=torch.complex64)
+    run = lambda: BT.rzf_batched(H, wl.alpha(), wl.power(), T=5, want_F=True)  # noqa: E731
+    ref = run()
+    torch.cuda.synchronize()
+    os.environ["XL_STREAM_W2"] = "0"
+    try:
+        alt = run()
+        torch.cuda.synchronize()
+    finally:
+        os.environ.pop("XL_STREAM_W2", None)
+    for b in range(H.shape[0]):
+        w0, w1 = ref.W[b].cpu().numpy(), alt.W[b].cpu().numpy()
+        assert np.linalg.norm(w0 - w1) <= 2e-5 * np.linalg.norm(w1)
+        f0, f1 = ref.F[b].cpu().numpy(), alt.F[b].cpu().numpy()
+        assert np.linalg.norm(f0 - f1) <= 2e-5 * np.linalg.norm(f1)
+    assert torch.equal(ref.sum_se, alt.sum_se)  # SINR comes from the solver, not from W

@@ -230,3 +230,26 @@ def test_k256_host_pipeline_matches_device_call():
     ref = BT.rzf_batched(H, wl.alpha(), wl.power(), T=6)
     assert Sth.tolist() == [0] * B
     assert torch.equal(Wh, ref.W.cpu()) and torch.equal(Sh, ref.sum_se.cpu())
+
+
+@pytest.mark.parametrize("env", [{"XL_LK_PIPE": "0"}, {"XL_LK_GRAM2": "0"}, {"XL_LK_W2": "0"}])
+def test_k256_kernel_variants_agree(env):
+    """The default K = 256 chain (pair Gram super-tiles, pair W kernel, chunks
+    pipelined over two streams) against each single-CTA / one-chunk variant it
+    replaced: W and sum-SE within fp32 rounding, on a batch that the pipeline
+    splits into chunks with a ragged last one."""
+    wl = X.CONFIGS["cfg5"]
+    H = X.generate_channels(wl.model, seed=9, first=40, B=1100, dtype=torch.complex64)
+    run = lambda: BT.rzf_batched(H, wl.alpha(), wl.power(), T=6)  # noqa: E731
+    ref = _run_env({k: None for k in env}, run)
+    alt = _run_env(env, run)
+    assert ref.status.cpu().tolist() == alt.status.cpu().tolist() == [0] * H.shape[0]
+    if "XL_LK_PIPE" in env:  # same kernels, same chunk-independent arithmetic: bit-identical
+        assert torch.equal(ref.W, alt.W) and torch.equal(ref.sum_se, alt.sum_se)
+    else:
+        for b in (0, 517, 1099):
+            assert relf(ref.W[b].cpu().numpy(), alt.W[b].cpu().numpy()) <= 2e-5
+        assert torch.allclose(ref.sum_se, alt.sum_se, rtol=1e-5, atol=0)
+    Hq = H[1099].cpu().numpy().astype(np.complex128)
+    Gr, _, _, s = O.precoder_and_se(Hq, wl.alpha(), wl.power(), 1.0, "jacpcg", 6, "textbook")
+    assert relf(ref.W[1099].cpu().numpy(), Gr) <= 1e-4 and abs(ref.sum_se[1099].item() - s) <= 1e-4 * abs(s)
