@@ -441,11 +441,12 @@ def test_se_partials_vs_oracle():
     assert mean == pytest.approx(rm, rel=1e-13) and sem == pytest.approx(rs, rel=1e-9)
 
 
-@pytest.mark.parametrize("cfg,B", [("cfg1", 100), ("cfg2", 300), ("cfg3", 64), ("cfg4", 4)])
+@pytest.mark.parametrize("cfg,B", [("cfg1", 100), ("cfg2", 300), ("cfg3", 64), ("cfg4", 4), ("cfg5", 1100)])
 def test_graphed_rzf_matches_direct_calls(cfg, B):
     """CUDA-graph replay of the whole precoder chain (fused kernel, SIMT general
     path, the K = 128 tcgen05 chain with its 2-CTA clusters and DSMEM bulk
-    copies, the small-K kernel with its TMEM allocation and W tensor map)
+    copies, the small-K kernel with its TMEM allocation and W tensor map, the
+    K = 256 chain's chunks forked onto a second stream and joined back)
     gives the same bits as the direct call, on two different inputs."""
     wl = X.CONFIGS[cfg]
     g = BT.GraphedRzf(B, wl.M, wl.K, wl.dtype, wl.alpha(), wl.power(), T=wl.T)
