@@ -818,6 +818,7 @@ struct Params {
   double* part;     // [B][C] Re tr(X^H GX) per CTA
   double* rsq;      // [B][C][2][K] per (column block, part) row sums of GX^2, or null: GX written instead
   float2* gdiag;    // [B][K] diagonal of GX (with rsq)
+  float* xmax;      // [B][K] max_i max(|Re X_ij|, |Im X_ij|) per column j (the W kernel's scales), or null
   int32_t* status;  // [B]
   uint8_t* scratch; // [clusters][512 KiB] split (Re A, Im A), K-step chunks
   long long* trace; // debug: clock64 stamps of cluster 0 / CTA 0 (xl_debug_lk_trace), or null
@@ -1379,6 +1380,14 @@ __global__ void __launch_bounds__(NT, 1) lk_pcg_kernel(Params p) {
       named_sync(BAR_MATH, NT);
       if (pass == 0) stamp();
     }
+    if (p.xmax) {  // per-column max |X| for the W kernel's row scales (saves it a pass over X)
+#pragma unroll
+      for (int jj = 0; jj < JN; ++jj) A[jj] = fabsf(P[jj] * sa);
+      col_partials<true>(A, sm, warp);
+      named_sync(BAR_MATH, NT);
+      if (tid < JN) p.xmax[b * KU + JN * cb + tid] = col_total<true>(sm, tid);
+      named_sync(BAR_MATH, NT);
+    }
     stamp();
     fro = warp_sum(fro);
     if (lane == 0) sm->dred[warp] = fro;
@@ -1451,7 +1460,7 @@ __device__ __forceinline__ void tmem_st16u(uint32_t ta, const uint32_t* v) {
 __global__ void __launch_bounds__(NT, 1) lk_w2_kernel(const __grid_constant__ CUtensorMap hmap, int M,
                                                       const unsigned* __restrict__ zmax, const float2* __restrict__ X,
                                                       const double* __restrict__ beta, float* __restrict__ W,
-                                                      float* __restrict__ F) {
+                                                      float* __restrict__ F, const float* __restrict__ xmax) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
   Small* sm = reinterpret_cast<Small*>(smem + NS * HB);
@@ -1477,22 +1486,29 @@ __global__ void __launch_bounds__(NT, 1) lk_w2_kernel(const __grid_constant__ CU
   if (warp == W_MMA) pc::tmem_alloc512_g<true>(&sm->tmem_slot);
   const float2* Xb = X + b * (int64_t)KU * KU;
   // ---- per-user scale sx[j'] = 2^e, max |X_:j'| sx < 2^14
-  if (tid < 256) {
-    const int jl = tid & 63, part = tid >> 6;
-    float m = 0.0f;
+  if (xmax) {  // the solver's per-column max |X|
+    if (tid < 64) sm->sx[tid] = pow2_scale(xmax[b * KU + 64 * t + tid], 14);
+    tc_before();
+    __syncthreads();
+    tc_after();
+  } else {
+    if (tid < 256) {
+      const int jl = tid & 63, part = tid >> 6;
+      float m = 0.0f;
 #pragma unroll 8
-    for (int i = 64 * part; i < 64 * part + 64; ++i) {
-      const float2 x = __ldg(Xb + (int64_t)i * KU + 64 * t + jl);
-      m = fmaxf(m, fmaxf(fabsf(x.x), fabsf(x.y)));
+      for (int i = 64 * part; i < 64 * part + 64; ++i) {
+        const float2 x = __ldg(Xb + (int64_t)i * KU + 64 * t + jl);
+        m = fmaxf(m, fmaxf(fabsf(x.x), fabsf(x.y)));
+      }
+      sm->rmax[part][jl] = m;
     }
-    sm->rmax[part][jl] = m;
+    tc_before();
+    __syncthreads();
+    tc_after();
+    if (tid < 64)
+      sm->sx[tid] = pow2_scale(fmaxf(fmaxf(sm->rmax[0][tid], sm->rmax[1][tid]), fmaxf(sm->rmax[2][tid], sm->rmax[3][tid])), 14);
+    __syncthreads();
   }
-  tc_before();
-  __syncthreads();
-  tc_after();
-  if (tid < 64)
-    sm->sx[tid] = pow2_scale(fmaxf(fmaxf(sm->rmax[0][tid], sm->rmax[1][tid]), fmaxf(sm->rmax[2][tid], sm->rmax[3][tid])), 14);
-  __syncthreads();
   const uint32_t tmem = sm->tmem_slot;
   // ---- A hi / lo straight into TMEM (lane = output row r, column = two input
   // users): converter warp cw writes its lane quadrant, users [128 h, +128)
@@ -2044,8 +2060,9 @@ int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi
   // the GX buffer holds the SINR partials instead (lk_sinr): [B][8][2][K] doubles, then [B][K] float2
   double* rsq = (double*)GX;
   float2* gdiag = (float2*)(rsq + (size_t)B * pc::C * 2 * KU);
+  float* xmax = lk_xmax(GX, B);
   pc::Params p{(const float2*)A, B, T, method, variant, xi, xi_b, (float2*)X, (float2*)GX, part, rsq, gdiag,
-               status, scratch, g_lk_trace, (uc && uc[0] == '1') ? 1 : 0, 1, 1, 0};
+               xmax, status, scratch, g_lk_trace, (uc && uc[0] == '1') ? 1 : 0, 1, 1, 0};
   if (const char* sp = getenv("XL_LK_SPIN")) p.spin = sp[0] == '1';
   if (const char* ss = getenv("XL_LK_SS")) p.ss = ss[0] == '1';  // default 1: A from shared memory (measured faster than tcgen05.cp + TMEM)
   if (const char* mr = getenv("XL_LK_MMA_REPS")) p.mma_reps = atoi(mr) > 0 ? atoi(mr) : 1;
@@ -2067,6 +2084,10 @@ int lk_solve(int method, int variant, const void* A, int64_t B, int T, double xi
   return check_launch("lk pcg");
 }
 
+float* lk_xmax(void* GX, int64_t B) {
+  return (float*)((float2*)((double*)GX + (size_t)B * lk::pc::C * 2 * lk::KU) + (size_t)B * lk::KU);
+}
+
 int lk_sinr(const void* GX, const double* beta, int64_t B, double sigma2, double* gamma, double* sum_se,
             cudaStream_t st) {
   using namespace lk;
@@ -2077,7 +2098,7 @@ int lk_sinr(const void* GX, const double* beta, int64_t B, double sigma2, double
 }
 
 int lk_apply(const void* H, const void* X, const double* beta, int64_t B, int M, void* W, void* F,
-             const unsigned* zmax, cudaStream_t st) {  // zmax: from lk_gram
+             const unsigned* zmax, const float* xmax, cudaStream_t st) {  // zmax: from lk_gram; xmax: lk_solve or null
   using namespace lk;
   CUtensorMap map;
   const char* w2 = getenv("XL_LK_W2");  // "0": the single-CTA W kernel (A/B, tests)
@@ -2096,7 +2117,7 @@ int lk_apply(const void* H, const void* X, const double* beta, int64_t B, int M,
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, wk2::lk_w2_kernel, map, M, zmax, (const float2*)X, beta, (float*)W, (float*)F) !=
+    if (cudaLaunchKernelEx(&cfg, wk2::lk_w2_kernel, map, M, zmax, (const float2*)X, beta, (float*)W, (float*)F, xmax) !=
         cudaSuccess)
       return check_launch("lk w2 launch");
     return check_launch("lk w2");

@@ -95,7 +95,9 @@ void lk_debug_trace(void* buf);
 int lk_sinr(const void* GX, const double* beta, int64_t B, double sigma2, double* gamma, double* sum_se,
             cudaStream_t st);
 int lk_apply(const void* H, const void* X, const double* beta, int64_t B, int M, void* W, void* F,
-             const unsigned* zmax, cudaStream_t st);
+             const unsigned* zmax, const float* xmax, cudaStream_t st);
+// the solver's per-column max |X| (in its GX buffer, after the SINR partials)
+float* lk_xmax(void* GX, int64_t B);
 
 // dmma.cu: batched complex128 GEMM on the FP64 tensor cores (row-major;
 // opA 0 = N, 1 = conjugate transpose; opB 0 = N, 1 = transpose; epi 0 store,

@@ -219,7 +219,7 @@ static int lk_pipeline(int method, int variant, const void* H, int64_t B, int32_
     int e;
     if ((e = launch_beta_from_partials(nb, part + b0 * NP, NP, power, beta + b0, status + b0, s))) return e;
     if ((e = lk_apply((const char*)H + b0 * oH, (const char*)Xo + b0 * oK, beta + b0, nb, M, (char*)W + b0 * oH,
-                      F ? (char*)F + b0 * oH : nullptr, sc.zmax + b0, s)))
+                      F ? (char*)F + b0 * oH : nullptr, sc.zmax + b0, lk_xmax((char*)GX + b0 * oK, nb), s)))
       return e;
     return lk_sinr((char*)GX + b0 * oK, beta + b0, nb, sigma2, gamma ? gamma + b0 * K : nullptr, sum_se + b0, s);
   };
@@ -322,7 +322,7 @@ static int general_path(int dtype, int method, int variant, const void* H, int64
   // W = beta H X on the tensor cores, per sub-batch (the split rows are rebuilt:
   // the Gram sub-batches have overwritten them)
   auto tc_w = [&]() -> int {
-    if (lkp) return lk_apply(H, Xo, beta, B, M, W, F, lk_scratch(tcws, B).zmax, st);
+    if (lkp) return lk_apply(H, Xo, beta, B, M, W, F, lk_scratch(tcws, B).zmax, nullptr, st);
     if (sc) return stc_apply(H, Xo, beta, szb, B, M, K, W, F, st);
     for (int64_t b0 = 0; b0 < B; b0 += Bc) {
       const int64_t nb = B - b0 < Bc ? B - b0 : Bc;
