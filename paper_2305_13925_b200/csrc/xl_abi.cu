@@ -228,19 +228,24 @@ static int lk_pipeline(int method, int variant, const void* H, int64_t B, int32_
     if ((e = gram(0, B, st)) || (e = solve(0, B, st))) return e;
     return finish(0, B, st);
   }
-  // a second stream and events per host thread (fork / join also inside graph capture)
-  static thread_local cudaStream_t aux = nullptr;
-  static thread_local cudaEvent_t ev[2 * 8 + 2];
-  static thread_local int dev_aux = -1;
+  // a second stream and events per host thread and device (fork / join also inside graph capture)
+  struct Side {
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev[2 * 8 + 2];
+  };
+  constexpr int MAX_DEV = 64;
+  static thread_local Side side[MAX_DEV];
   int dev = 0;
   cudaGetDevice(&dev);
-  if (aux == nullptr || dev_aux != dev) {
-    if (cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking) != cudaSuccess) return check_launch("lk aux stream");
-    for (auto& x : ev)
+  if (dev < 0 || dev >= MAX_DEV) { set_error("lk pipeline: device %d out of range", dev); return XL_ERR_UNSUPPORTED; }
+  Side& sd = side[dev];
+  if (sd.aux == nullptr) {
+    if (cudaStreamCreateWithFlags(&sd.aux, cudaStreamNonBlocking) != cudaSuccess) return check_launch("lk aux stream");
+    for (auto& x : sd.ev)
       if (cudaEventCreateWithFlags(&x, cudaEventDisableTiming) != cudaSuccess) return check_launch("lk events");
-    dev_aux = dev;
   }
-  cudaEvent_t *ev_g = ev, *ev_p = ev + 8, ev_fork = ev[16], ev_join = ev[17];
+  cudaStream_t aux = sd.aux;
+  cudaEvent_t *ev_g = sd.ev, *ev_p = sd.ev + 8, ev_fork = sd.ev[16], ev_join = sd.ev[17];
   if (cudaEventRecord(ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(aux, ev_fork, 0) != cudaSuccess)
     return check_launch("lk fork");
   if ((e = gram(0, Bc, st))) return e;
