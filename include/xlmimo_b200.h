@@ -15,7 +15,11 @@
  *    columns = users, exactly the reference layout), A/X[B][K][K].
  *  - All pointers are DEVICE pointers unless stated otherwise; calls are
  *    stream-ordered and asynchronous; no hidden allocation (caller passes a
- *    workspace sized by the matching *_workspace_bytes()).
+ *    workspace sized by the matching *_workspace_bytes()).  One exception to
+ *    "one stream": an xl_rzf call on K = 256 complex64 with B >= 1024 runs its
+ *    chunks over the caller's stream and one internal stream (created once
+ *    per host thread and device), forked from and joined back into `stream`
+ *    with events -- still ordered on `stream` and CUDA-graph capturable.
  *  - Return value: XL_SUCCESS or an XL_ERR_* code (host-side argument errors
  *    map to the reference's ConfigurationError).  Numerical failures are
  *    reported per realization in status[B] (XL_STATUS_*), which the Python
