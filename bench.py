@@ -254,7 +254,8 @@ def _ref_config(a, wl, world):
     from paper_2305_13925_b200.distributed import rank_batch
     B = a.batch or wl.B
     _, nb = rank_batch(a.scaling, B, world, 0)
-    return {"workload": f"{a.config}: M={wl.M}, K={wl.K}, T={wl.T}, {a.method}",
+    return {"workload": f"{a.config}: M={wl.M}, K={wl.K}, T={wl.T}, {a.method}, "
+                        f"{nb} realizations per GPU",
             "M": wl.M, "K": wl.K, "T": wl.T, "method": a.method, "variant": "textbook",
             "dtype": "c64" if "128" not in str(wl.dtype) else "c128",
             "global_batch": B if a.scaling == "strong" else B * world,
@@ -279,7 +280,8 @@ def run_reference(a):
     v = statistics.median(vals)
     cb["value"] = v
     cfg = _ref_config(a, wl, world)
-    cfg["sample"] = f"reference algorithm (CPU port, complex128), per-step sample of {secs:.0f} s"
+    cb["sample"] = (f"reference algorithm (CPU port, complex128), per-step sample of {secs:.0f} s; "
+                    + str(cb.get("sample", "")))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
             "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": 1000.0 * secs, "higher_is_better": True, "scaling": a.scaling,
