@@ -140,6 +140,14 @@ __device__ __forceinline__ float pow2s(float m) {
   return __int_as_float((f > 254 ? 254 : (f < 1 ? 1 : f)) << 23);
 }
 // 1 / s for a power of two s in the normal range (exact)
+// 1 / v by rcp.approx and one Newton step: within an ulp or two of the rounded
+// quotient, and without the range-check branch of the IEEE reciprocal (those
+// branches sit on the latency-bound solver chains)
+__device__ __forceinline__ float rcp_nr(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r * fmaf(-v, r, 2.f);
+}
 __device__ __forceinline__ float pow2_inv(float s) {
   return __int_as_float((254 - ((__float_as_int(s) >> 23) & 0xff)) << 23);
 }
@@ -582,22 +590,20 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p, const __grid_c
       if (!(pk > 0.f)) {
         if (tid == 0) flags[0] |= 4;
       }
-      const float ip = 1.f / pk;
+      const float ip = rcp_nr(pk);  // (a pivot <= 0 is flagged above)
       if (solver) {
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
+          // every case computed, then selected (divergent if/else chains cost
+          // ~2x the step: tools/microbench/gj_step.cu)
           const int i = ie[e], j = je[e];
-          if (i == k && j == k) {
-            x[e] = make_float2(ip, 0.f);
-          } else if (i == k) {
-            x[e] = make_float2(x[e].x * ip, x[e].y * ip);
-          } else if (j == k) {
-            x[e] = make_float2(-x[e].x * ip, -x[e].y * ip);
-          } else {
-            const float2 a = colb[buf + i], c = rowb[buf + j];  // a_ik, a_kj (old)
-            const float2 m = make_float2((a.x * c.x - a.y * c.y) * ip, (a.x * c.y + a.y * c.x) * ip);
-            x[e] = make_float2(x[e].x - m.x, x[e].y - m.y);
-          }
+          const float2 a = colb[buf + i], c = rowb[buf + j];  // a_ik, a_kj (old)
+          const float2 gen = make_float2(x[e].x - (a.x * c.x - a.y * c.y) * ip,
+                                         x[e].y - (a.x * c.y + a.y * c.x) * ip);
+          const float sr = (j == k) ? -ip : ip;  // row k: x / p, column k: -x / p
+          float2 v = (i == k || j == k) ? make_float2(x[e].x * sr, x[e].y * sr) : gen;
+          if (i == k && j == k) v = make_float2(ip, 0.f);
+          x[e] = v;
         }
       }
     }
@@ -635,7 +641,7 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p, const __grid_c
       for (int c = 0; c < 2; ++c) {
         const bool act = rz[c] > 0.f;
         if (curv[c] <= 0.f && act) atomicOr(flags, 1);
-        al[c] = act ? rz[c] * __frcp_rn(curv[c] > 0.f ? curv[c] : 1.f) : 0.f;
+        al[c] = act ? rz[c] * rcp_nr(curv[c] > 0.f ? curv[c] : 1.f) : 0.f;
       }
       float rp[NE], rm[NE];
 #pragma unroll
@@ -659,7 +665,7 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p, const __grid_c
       for (int c = 0; c < 2; ++c) {
         const float x0 = colx[3 * NMT * K + je[c]];
         rmx[c] = NMT > 1 ? fmaxf(x0, colx[3 * NMT * K + K + je[c]]) : rmx[c];
-        be[c] = rz[c] > 0.f ? rn[c] * __frcp_rn(rz[c]) : 0.f;
+        be[c] = rz[c] > 0.f ? rn[c] * rcp_nr(rz[c]) : 0.f;
         rz[c] = rn[c];
         // |P_new| <= |R C^-b| + |beta| |P|, per component: the next operand's scale
         pbm[c] = rmx[c] + fabsf(be[c]) * pbm[c];
