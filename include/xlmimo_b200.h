@@ -201,6 +201,13 @@ int xl_channel_generate(int dtype, uint64_t seed, int64_t first, int64_t B,
 int xl_se_partials(const double* sum_se, int64_t B, int64_t chunk,
                    double* partials, xl_stream_t stream);
 
+/* mean_sem[0..1] = {mean, SEM (ddof = 1)} of the realizations behind
+ * n_chunks ordered partials (as produced by xl_se_partials, possibly
+ * gathered over ranks), summed in chunk order on the device: the tail of
+ * sum_se's mean/SEM (metrics.py:61-68) without a host round trip. */
+int xl_se_combine(const double* partials, int64_t n_chunks, double* mean_sem,
+                  xl_stream_t stream);
+
 /* BER detection chain of ber_montecarlo (metrics.py:124-140) for a batch of
  * channel draws: Y = Bc s + n with s = QPSK(bits) ((1-2b0) + j(1-2b1))/sqrt(2)
  * (metrics.py:73-77), genie scaling by diag(Bc) with zero gains replaced by 1,

@@ -81,6 +81,7 @@ _SIGNATURES = {
     "xl_channel_generate": (_int, [_int, _u64, _i64, _i64, _i32, _i32, _i32, _f64, _p,
                                    _f64, _f64, _f64, _p, _p, _p]),
     "xl_se_partials": (_int, [_p, _i64, _i64, _p, _p]),
+    "xl_se_combine": (_int, [_p, _i64, _p, _p]),
     "xl_ber_errors": (_int, [_int, _p, _p, _p, _i64, _i32, _i32, _p, _p]),
 }
 

@@ -89,7 +89,8 @@ __global__ void __launch_bounds__(NT) fused_c128_kernel(Params p) {
   double* cdg = reinterpret_cast<double*>(Qs + K * K);  // [K] Re diag(A) (preconditioner)
   double* rzs = cdg + K;                                  // [K] rz per column
   double* coef = rzs + K;                                 // [K] alpha / beta per column
-  double* red = coef + K;                                 // [NW] reductions
+  double* icd = coef + K;                                 // [K] 1 / cdg (computed once)
+  double* red = icd + K;                                  // [NW] reductions
   int* flags = reinterpret_cast<int*>(red + NW);          // [0] not_hpd
   constexpr int NTL = K / 8;
   const int64_t b = blockIdx.x;
@@ -98,10 +99,15 @@ __global__ void __launch_bounds__(NT) fused_c128_kernel(Params p) {
   const bool textbook = use_c && p.variant == XL_TEXTBOOK;
   const double xi = p.xi_b ? p.xi_b[b] : p.xi;
 
-  // ---- H -> smem (coalesced 16-B loads)
+  // ---- H -> smem (16-B cp.async: every load in flight at once, not one DRAM
+  // round trip per loop trip)
   const double2* Hb = p.H + b * (int64_t)M * K;
-  for (int e = tid; e < M * K; e += NT) Hs[e] = Hb[e];
+  for (int e = tid; e < M * K; e += NT)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(Hs + e)),
+                 "l"(Hb + e)
+                 : "memory");
   if (tid == 0) flags[0] = 0;
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
 
   // ---- Gram: warp w sums antennas [w M/8, (w+1) M/8) for every 8 x 8 tile
@@ -152,6 +158,7 @@ __global__ void __launch_bounds__(NT) fused_c128_kernel(Params p) {
   if (tid < K) {
     As[tid * K + tid] = make_double2(As[tid * K + tid].x + xi, 0.0);
     cdg[tid] = As[tid * K + tid].x;
+    icd[tid] = 1.0 / cdg[tid];
   }
   __syncthreads();
   // zero preconditioner diagonal -> Splitting (linsolve.py:205-208)
@@ -165,7 +172,7 @@ __global__ void __launch_bounds__(NT) fused_c128_kernel(Params p) {
   for (int e = tid; e < K * K; e += NT) {
     const int i = e / K, j = e % K;
     const double ei = (i == j) ? 1.0 : 0.0;
-    const double ic = use_c ? 1.0 / cdg[i] : 1.0;
+    const double ic = use_c ? icd[i] : 1.0;
     const double r = (use_c && !textbook) ? ei * ic : ei;
     Xs[e] = make_double2(0.0, 0.0);
     Rs[e] = make_double2(r, 0.0);
@@ -174,7 +181,7 @@ __global__ void __launch_bounds__(NT) fused_c128_kernel(Params p) {
   __syncthreads();
   // rz_j = Re(r_j^H z_j): identity columns, z = r / c (textbook), r (CG / Algorithm 1)
   if (tid < K) {
-    const double ic = use_c ? 1.0 / cdg[tid] : 1.0;
+    const double ic = use_c ? icd[tid] : 1.0;
     rzs[tid] = textbook ? ic : (use_c ? ic * ic : 1.0);
   }
   __syncthreads();
@@ -185,7 +192,7 @@ __global__ void __launch_bounds__(NT) fused_c128_kernel(Params p) {
     __syncthreads();
     if (use_c && !textbook)
       for (int e = tid; e < K * K; e += NT) {
-        const double ic = 1.0 / cdg[e / K];
+        const double ic = icd[e / K];
         Qs[e] = make_double2(Qs[e].x * ic, Qs[e].y * ic);
       }
     __syncthreads();
@@ -220,7 +227,7 @@ __global__ void __launch_bounds__(NT) fused_c128_kernel(Params p) {
       double rn = 0.0;
       for (int i = 0; i < K; ++i) {
         const double2 r = Rs[i * K + j];
-        const double ic = textbook ? 1.0 / cdg[i] : 1.0;
+        const double ic = textbook ? icd[i] : 1.0;
         rn += r.x * (r.x * ic) + r.y * (r.y * ic);
       }
       const double rzj = rzs[j];
@@ -230,7 +237,7 @@ __global__ void __launch_bounds__(NT) fused_c128_kernel(Params p) {
     __syncthreads();
     for (int e = tid; e < K * K; e += NT) {
       const double be = coef[e % K];
-      const double ic = textbook ? 1.0 / cdg[e / K] : 1.0;
+      const double ic = textbook ? icd[e / K] : 1.0;
       const double2 r = Rs[e], m = Ps[e];
       Ps[e] = make_double2(r.x * ic + be * m.x, r.y * ic + be * m.y);
     }
@@ -306,7 +313,7 @@ __global__ void __launch_bounds__(NT) fused_c128_kernel(Params p) {
 
 template <int K>
 size_t smem_bytes(int M) {
-  return ((size_t)M * K + 5 * K * K) * sizeof(double2) + (3 * K + NW) * sizeof(double) + 16;
+  return ((size_t)M * K + 5 * K * K) * sizeof(double2) + (4 * K + NW) * sizeof(double) + 16;
 }
 
 }  // namespace fc

@@ -297,6 +297,27 @@ __global__ void se_partials_kernel(const double* __restrict__ s, int64_t B, int6
   if (threadIdx.x == 0) { out[3 * c] = r1[0]; out[3 * c + 1] = r2[0]; out[3 * c + 2] = (double)(hi - lo); }
 }
 
+// {mean, SEM (ddof = 1)} from ordered chunk partials, summed in chunk order by
+// one thread (the few partials of a step; one launch instead of a dozen
+// elementwise ones inside a replayed step)
+__global__ void se_combine_kernel(const double* __restrict__ parts, int64_t nc, double* __restrict__ out) {
+  double s = 0.0, q = 0.0, n = 0.0;
+  for (int64_t c = 0; c < nc; ++c) {
+    s += parts[3 * c];
+    q += parts[3 * c + 1];
+    n += parts[3 * c + 2];
+  }
+  const double mean = s / n;
+  const double var = fmax(q - n * mean * mean, 0.0) / fmax(n - 1.0, 1.0);
+  out[0] = mean;
+  out[1] = n > 1.0 ? sqrt(var / n) : 0.0;
+}
+
+int launch_se_combine(const double* parts, int64_t nc, double* out, cudaStream_t st) {
+  se_combine_kernel<<<1, 1, 0, st>>>(parts, nc, out);
+  return check_launch("se_combine");
+}
+
 int launch_se_partials(const double* s, int64_t B, int64_t chunk, double* out, cudaStream_t st) {
   int64_t nc = (B + chunk - 1) / chunk;
   se_partials_kernel<<<(unsigned)nc, 256, 0, st>>>(s, B, chunk, out);

@@ -25,6 +25,7 @@ int launch_sinr(const void* Bc, int64_t B, int K, double sigma2, double* gamma,
 int launch_beta_from_partials(int64_t B, const double* partial, int nparts, double power, double* beta,
                               int32_t* status, cudaStream_t st);
 int launch_se_partials(const double* s, int64_t B, int64_t chunk, double* out, cudaStream_t st);
+int launch_se_combine(const double* parts, int64_t nc, double* out, cudaStream_t st);
 
 // PCG / CG / Jac-PCG (linsolve.py:183-294) and Cholesky (linsolve.py:109-119).
 struct SolveArgs {

@@ -544,6 +544,11 @@ int xl_se_partials(const double* sum_se, int64_t B, int64_t chunk, double* parti
   return launch_se_partials(sum_se, B, chunk, partials, (cudaStream_t)stream);
 }
 
+int xl_se_combine(const double* partials, int64_t n_chunks, double* mean_sem, xl_stream_t stream) {
+  if (n_chunks < 1) { set_error("xl_se_combine needs at least one chunk"); return XL_ERR_CONFIG; }
+  return launch_se_combine(partials, n_chunks, mean_sem, (cudaStream_t)stream);
+}
+
 int xl_ber_errors(int dtype, const void* Bc, const int8_t* bits, const void* noise, int64_t B,
                   int32_t K, int32_t nsym, int64_t* errors, xl_stream_t stream) {
   if (int e = check_dtype(dtype)) return e;

@@ -50,7 +50,15 @@ def rank_batch(scaling: str, per_rank_or_total: int, world: int, rank: int) -> t
 
 
 def combine_partials_device(parts: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
-    """(mean, sem) as 0-d tensors from ordered [n_chunks, 3] partials."""
+    """(mean, sem) as 0-d tensors from ordered [n_chunks, 3] partials (on a GPU:
+    one xl_se_combine launch)."""
+    if parts.is_cuda:
+        from . import _lib as L
+        parts = parts.contiguous()
+        out = torch.empty(2, dtype=torch.float64, device=parts.device)
+        L.check(L.lib().xl_se_combine(L.ptr(parts), parts.shape[0], L.ptr(out), L.stream_ptr(None)),
+                "xl_se_combine")
+        return out[0], out[1]
     s, q, n = parts[:, 0].sum(), parts[:, 1].sum(), parts[:, 2].sum()
     mean = s / n
     var = torch.clamp(q - n * mean * mean, min=0.0) / torch.clamp(n - 1.0, min=1.0)

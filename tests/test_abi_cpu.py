@@ -60,6 +60,7 @@ def test_host_side_validation_without_device(lib):
     assert lib.xl_rzf(*rz) == L.XL_ERR_CONFIG                                            # sigma2 = 0
     assert b"noise power" in lib.xl_last_error()
     assert lib.xl_se_partials(None, 4, 0, None, None) == L.XL_ERR_CONFIG
+    assert lib.xl_se_combine(None, 0, None, None) == L.XL_ERR_CONFIG
     # stationary solvers (linsolve.py:128-176): T < 1, omega <= 0, unknown method
     st = [0, L.XL_JOR, None, 1, 4, None, 4, None, 0.5, 0, -1.0] + [None] * 6 + [0, None]
     assert lib.xl_solve_stationary(*st) == L.XL_ERR_CONFIG                               # T = 0

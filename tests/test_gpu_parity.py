@@ -439,6 +439,13 @@ def test_se_partials_vs_oracle():
     mean, sem = BT.combine_se_partials(parts)
     rm, rs = O.sum_se(x.cpu().numpy())
     assert mean == pytest.approx(rm, rel=1e-13) and sem == pytest.approx(rs, rel=1e-9)
+    # the device combine (xl_se_combine, one launch) sums the partials in the
+    # same chunk order as the host combine
+    from paper_2305_13925_b200.distributed import combine_partials_device, ergodic_se
+    dm, ds = combine_partials_device(BT.se_partials(x, 2048))
+    assert float(dm) == mean and float(ds) == pytest.approx(sem, rel=1e-14)
+    em, es = ergodic_se(x[:1], chunk=2048, group=False)  # one realization: SEM 0
+    assert float(em) == float(x[0]) and float(es) == 0.0
 
 
 @pytest.mark.parametrize("cfg,B", [("cfg1", 100), ("cfg2", 300), ("cfg3", 64), ("cfg4", 4), ("cfg5", 1100)])
