@@ -436,12 +436,7 @@ __global__ void __launch_bounds__(NT, 2) small_k_kernel(Params p, const __grid_c
   }
   auto pair_sync = [&]() {  // the NMT warps of column block cb (immediate barrier ids 1..NCB)
     if constexpr (NMT > 1) {
-      switch (cb) {
-        case 0: asm volatile("bar.sync 1, 64;" ::: "memory"); break;
-        case 1: asm volatile("bar.sync 2, 64;" ::: "memory"); break;
-        case 2: asm volatile("bar.sync 3, 64;" ::: "memory"); break;
-        default: asm volatile("bar.sync 4, 64;" ::: "memory"); break;
-      }
+      asm volatile("bar.sync %0, 64;" ::"r"(cb + 1) : "memory");  // warp-uniform id, no branch
     } else {
       __syncwarp();
     }
