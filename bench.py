@@ -254,13 +254,18 @@ def _ref_config(a, wl, world):
     from paper_2305_13925_b200.distributed import rank_batch
     B = a.batch or wl.B
     _, nb = rank_batch(a.scaling, B, world, 0)
+    csz = 16 if "128" in str(wl.dtype) else 8
     return {"workload": f"{a.config}: M={wl.M}, K={wl.K}, T={wl.T}, {a.method}, "
                         f"{nb} realizations per GPU",
             "M": wl.M, "K": wl.K, "T": wl.T, "method": a.method, "variant": "textbook",
             "dtype": "c64" if "128" not in str(wl.dtype) else "c128",
             "global_batch": B if a.scaling == "strong" else B * world,
             "batch_per_gpu": nb, "scaling": a.scaling,
-            "parallelism": f"realization-sharded x{world}"}
+            "parallelism": f"realization-sharded x{world}",
+            # properties of the workload, stated as on our arm
+            "channel_generation_timed": wl.chunk is not None,
+            "l2": (f"inputs {nb * wl.M * wl.K * csz / 2**30:.2f} GiB per GPU >> 126 MB L2"
+                   if nb * wl.M * wl.K * csz > 2**28 else "inputs below 256 MiB")}
 
 
 def run_reference(a):
@@ -535,8 +540,7 @@ def main(argv=None):
                                           f"(generation of chunk n+1 overlaps precoding of chunk n)"
                                           if gen_in_step else
                                           (f", precoded in sub-batches of {sub}" if sub < B else "")),
-                           "sub_batch": sub, "channel_generation_timed": gen_in_step,
-                           "cuda_graph": graphed,
+                           "channel_generation_timed": gen_in_step,
                            "M": M, "K": K, "T": T, "method": a.method, "variant": "textbook",
                            "dtype": "c64" if dt == torch.complex64 else "c128",
                            "batch_per_gpu": B, "global_batch": total if a.scaling == "strong" else B * world,
@@ -544,6 +548,7 @@ def main(argv=None):
                            "parallelism": f"realization-sharded x{world}",
                            "l2": f"inputs {B * M * K * csz / 2**30:.2f} GiB per GPU >> 126 MB L2"
                                  if B * M * K * csz > 2**28 else "inputs below 256 MiB"},
+                "harness": {"sub_batch": sub, "cuda_graph": graphed},
                 "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
                 "gpu_launches": launches, "clocks": clk.summary(),
                 "ergodic_se": {"mean": float(se_mean[0]), "sem": float(se_mean[1]),
